@@ -1,0 +1,137 @@
+/*
+ * esm2_b200.h -- C ABI of the B200-native (sm_100a) ESM-2 MLM train-step kernels.
+ *
+ * Boundary
+ * --------
+ * The reference (/root/reference, the `densefeed` data toolkit) has no model,
+ * kernel or FFI for this path: there is no
+ * reference C interface to replace.  Each entry point below replaces one
+ * operator of the Hugging Face EsmForMaskedLM forward/backward that the
+ * reference's training loop would call (third-party semantics, transformers
+ * 5.5.0 `models/esm/modeling_esm.py`, "HF:" below), and the whole step is
+ * invoked through the reference seam `densefeed.sizing.collect_peak_alloc(
+ * samples, workload, feature_fn, meter)` (pkg/src/densefeed/sizing.py:76-100)
+ * by the Python host layer (paper_2411_10548_b200.seams).
+ *
+ * Conventions
+ * ---------------------------
+ *  - plain device pointers + sizes; no torch types; the caller owns all memory
+ *    (kernels never allocate); every call is asynchronous on `stream`.
+ *  - every call returns 0 on success, an ESM_E* code on bad arguments, or the
+ *    cudaError_t of a failed launch; esm_last_error() describes the failure.
+ *  - `dtype` selects the activation type: ESM_F32 (fp32 parity mode, SIMT
+ *    kernels) or ESM_BF16 (production: tcgen05/TMEM/TMA GEMMs, mma.sync
+ *    flash attention, vectorised epilogues).  Parameters are fp32 masters with
+ *    a bf16 shadow for GEMM operands; gradients are always fp32.
+ *  - activations are token-major: row t = b*S + s of a [T, width] matrix.
+ */
+#ifndef ESM2_B200_H
+#define ESM2_B200_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* esm_stream_t; /* a cudaStream_t */
+
+enum { ESM_F32 = 0, ESM_BF16 = 1 };
+enum { ESM_OK = 0, ESM_EINVAL = 1001, ESM_ENOTSUP = 1002, ESM_EDRIVER = 1003 };
+
+/* GEMM epilogues (applied to acc = A·Bᵀ, fp32) */
+enum {
+  ESM_EPI_STORE = 0,      /* C = acc (+ bias[n])                         act dtype    HF nn.Linear          */
+  ESM_EPI_GELU = 1,       /* Z = acc + bias; C = gelu(Z)  (Z -> aux_out)  act dtype    HF:406-414, 57-61     */
+  ESM_EPI_RESID = 2,      /* C = acc + bias + R           (R = aux_in)    act dtype    HF:365-375, 417-427   */
+  ESM_EPI_DGELU = 3,      /* C = acc * gelu'(Z) (Z = aux_in); colsum(C) -> col_sum     backward of HF:411-414 */
+  ESM_EPI_F32_ACC = 4     /* C(fp32) += acc  (weight gradients; split-K safe)                               */
+};
+
+typedef struct esm_gemm_args {
+  int dtype;                 /* ESM_F32 / ESM_BF16: dtype of A, B and activation outputs        */
+  int M, N, K;               /* C[M,N] = A[M,K] · B[N,K]ᵀ                                        */
+  const void* A; int64_t lda; int a_mn_major; /* 0: A[m*lda+k]   1: A[k*lda+m]                   */
+  const void* B; int64_t ldb; int b_mn_major; /* 0: B[n*ldb+k]   1: B[k*ldb+n]                   */
+  void* C; int64_t ldc;
+  int epilogue;
+  const float* bias;         /* [N] fp32 or NULL                                                   */
+  const void* aux_in; int64_t ld_aux_in;    /* residual R or pre-activation Z                      */
+  void* aux_out; int64_t ld_aux_out;        /* GELU pre-activation Z output                        */
+  float* col_sum;            /* [N] fp32 accumulated column sums (bias grad) or NULL               */
+  int split_k;               /* ESM_EPI_F32_ACC only; 0 = auto                                     */
+} esm_gemm_args;
+
+/* ---------------- library ---------------- */
+int esm_version(void);
+const char* esm_last_error(void);
+int esm_device_sm_count(int device);
+
+/* ---------------- data path ---------------- */
+/* Host: ESM-2 alphabet tokenizer.  out = <cls> ids <eos>; returns #ids (or -needed if max_out small). */
+int esm_tokenize(const char* seq, int len, int32_t* out, int max_out);
+/* Device: 15% / 80-10-10 MLM masking (splitmix64 counter RNG, integer thresholds;
+ * bit-exact with oracle/esm2_oracle.py:mlm_mask).  Also counts labelled tokens into *n_labels (int32, accumulated). */
+int esm_mlm_mask(const int32_t* ids, int32_t* input_ids, int32_t* labels, int32_t* n_labels, int64_t n,
+                 uint64_t seed, uint64_t stream_id, esm_stream_t stream);
+
+/* ---------------- embeddings (HF:modeling_esm.py:189-236) ---------------- */
+/* x[t,:] = E[ids[t]] * (ids!=mask) * row_scale[b] * am[t];  row_scale = 0.88/(1 - n_mask/len) (token_dropout). */
+int esm_embed_fwd(int dtype, const int32_t* ids, const int32_t* am, const void* E, void* x, float* row_scale,
+                  int B, int S, int H, int token_dropout, int mask_id, esm_stream_t stream);
+/* dE[v,:] += sum_{t: ids[t]=v, v!=pad} dx[t,:] * keep * row_scale[b] * am[t]   (fp32) */
+int esm_embed_bwd(int dtype, const int32_t* ids, const int32_t* am, const float* row_scale, const void* dx,
+                  float* dE, int B, int S, int H, int V, int mask_id, int pad_id, esm_stream_t stream);
+
+/* ---------------- LayerNorm (nn.LayerNorm, eps) ---------------- */
+int esm_layernorm_fwd(int dtype, const void* x, const float* gamma, const float* beta, void* y, float* mean,
+                      float* rstd, int rows, int H, float eps, esm_stream_t stream);
+/* dx = LNᵀ(dy) [+ dres]; optional: dx *= gelu'(gelu_z) (LM head), dgamma/dbeta += , col_sum += colsum(dx). */
+int esm_layernorm_bwd(int dtype, const void* dy, const void* x, const float* gamma, const float* mean,
+                      const float* rstd, const void* dres, const void* gelu_z, void* dx, float* dgamma,
+                      float* dbeta, float* col_sum, int rows, int H, esm_stream_t stream);
+
+/* ---------------- linear layers ---------------- */
+int esm_gemm(const esm_gemm_args* args, esm_stream_t stream);
+
+/* ---------------- rotary + head layout (HF:modeling_esm.py:318-344) ---------------- */
+/* qkv[T,3H] (bias already added) -> q,k,v [B,nh,S,dh]; q *= q_scale, then RoPE(q), RoPE(k). cos/sin: [S, dh/2] fp32. */
+int esm_qkv_rope_fwd(int dtype, const void* qkv, void* q, void* k, void* v, const float* cos_t, const float* sin_t,
+                     int B, int S, int nh, int dh, float q_scale, esm_stream_t stream);
+/* dq (fp32 [B,nh,S,dh]), dk, dv ([B,nh,S,dh] act dtype) -> dqkv[T,3H] with RoPEᵀ and q_scale; col_sum[3H] += bias grads. */
+int esm_qkv_rope_bwd(int dtype, const float* dq, const void* dk, const void* dv, void* dqkv, float* col_sum,
+                     const float* cos_t, const float* sin_t, int B, int S, int nh, int dh, float q_scale,
+                     esm_stream_t stream);
+
+/* ---------------- attention (HF:modeling_esm.py:257-282; scaling = 1) ---------------- */
+/* q,k,v [B,nh,S,dh]; key_mask [B,S] int32 (0 = padded key); o [T, nh*dh]; lse [B,nh,S] fp32. */
+int esm_attn_fwd(int dtype, const void* q, const void* k, const void* v, const int32_t* key_mask, void* o,
+                 float* lse, int B, int nh, int S, int dh, esm_stream_t stream);
+/* dO [T, nh*dh]; outputs dq (fp32 accum, zeroed by callee), dk, dv [B,nh,S,dh]; delta workspace [B,nh,S] fp32. */
+int esm_attn_bwd(int dtype, const void* q, const void* k, const void* v, const void* o, const void* dout,
+                 const float* lse, const int32_t* key_mask, float* delta, float* dq, void* dk, void* dv,
+                 int B, int nh, int S, int dh, esm_stream_t stream);
+
+/* ---------------- LM head decoder + masked cross-entropy (HF:modeling_esm.py:777-815) ---------------- */
+/* logits = n·Eᵀ + bias for labelled rows; loss_sum += Σ nll * inv_denom[0]; dlogits -> dn (= dlogits·E),
+ * dE += dlogitsᵀ·n, dbias += Σ dlogits.  Unlabelled rows get dn = 0. */
+int esm_lmhead_xent(int dtype, const void* n, const void* E, const float* bias, const int32_t* labels,
+                    const float* inv_denom, float* loss_sum, float* dlogits_ws, void* dn, float* dE, float* dbias,
+                    int T, int H, int V, esm_stream_t stream);
+/* inv_denom[0] = 1 / max(1, n_labels[0]) (fp32) -- the loss normaliser, device-side (graph-safe). */
+int esm_inv_count(const int32_t* n_labels, float* inv_denom, esm_stream_t stream);
+
+/* ---------------- optimizer ---------------- */
+/* Fused multi-tensor AdamW over one flat fp32 buffer (torch.optim.AdamW semantics, decoupled decay).
+ * hyper (device fp32[8]): {lr, beta1, beta2, eps, weight_decay, step, grad_scale, unused}.
+ * decay_chunk[i] (uint8) = 1 if elements [i*256, (i+1)*256) are weight-decayed.  p16 = bf16 shadow (or NULL). */
+int esm_adamw(float* p, const float* g, float* m, float* v, void* p16, const uint8_t* decay_chunk, int64_t n,
+              const float* hyper, esm_stream_t stream);
+/* fp32 -> bf16 copy (shadow refresh). */
+int esm_cast_f32_bf16(const float* src, void* dst, int64_t n, esm_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ESM2_B200_H */

@@ -1,0 +1,106 @@
+"""ctypes binding of the in-tree C-ABI kernel library (include/esm2_b200.h).
+
+The product path has no fallback: if ``libesm2b200.so`` is missing or was built for
+another architecture, importing the model raises ``EsmKernelError``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libesm2b200.so")
+
+ESM_F32, ESM_BF16 = 0, 1
+EPI_STORE, EPI_GELU, EPI_RESID, EPI_DGELU, EPI_F32_ACC = 0, 1, 2, 3, 4
+
+EXPORTS = [
+    "esm_version", "esm_last_error", "esm_device_sm_count", "esm_tokenize", "esm_mlm_mask", "esm_embed_fwd",
+    "esm_embed_bwd", "esm_layernorm_fwd", "esm_layernorm_bwd", "esm_gemm", "esm_qkv_rope_fwd", "esm_qkv_rope_bwd",
+    "esm_attn_fwd", "esm_attn_bwd", "esm_lmhead_xent", "esm_inv_count", "esm_adamw", "esm_cast_f32_bf16",
+]
+
+
+class EsmKernelError(RuntimeError):
+    """A C-ABI call returned non-zero (cudaError_t or ESM_E* code); message from esm_last_error()."""
+
+
+class GemmArgs(ctypes.Structure):
+    _fields_ = [
+        ("dtype", ctypes.c_int), ("M", ctypes.c_int), ("N", ctypes.c_int), ("K", ctypes.c_int),
+        ("A", ctypes.c_void_p), ("lda", ctypes.c_int64), ("a_mn_major", ctypes.c_int),
+        ("B", ctypes.c_void_p), ("ldb", ctypes.c_int64), ("b_mn_major", ctypes.c_int),
+        ("C", ctypes.c_void_p), ("ldc", ctypes.c_int64),
+        ("epilogue", ctypes.c_int),
+        ("bias", ctypes.c_void_p),
+        ("aux_in", ctypes.c_void_p), ("ld_aux_in", ctypes.c_int64),
+        ("aux_out", ctypes.c_void_p), ("ld_aux_out", ctypes.c_int64),
+        ("col_sum", ctypes.c_void_p),
+        ("split_k", ctypes.c_int),
+    ]
+
+
+_P, _I, _I64, _U64, _F = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_uint64, ctypes.c_float
+_SIGS = {
+    "esm_version": ([], _I),
+    "esm_last_error": ([], ctypes.c_char_p),
+    "esm_device_sm_count": ([_I], _I),
+    "esm_tokenize": ([ctypes.c_char_p, _I, _P, _I], _I),
+    "esm_mlm_mask": ([_P, _P, _P, _P, _I64, _U64, _U64, _P], _I),
+    "esm_embed_fwd": ([_I, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P], _I),
+    "esm_embed_bwd": ([_I, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P], _I),
+    "esm_layernorm_fwd": ([_I, _P, _P, _P, _P, _P, _P, _I, _I, _F, _P], _I),
+    "esm_layernorm_bwd": ([_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P], _I),
+    "esm_gemm": ([ctypes.POINTER(GemmArgs), _P], _I),
+    "esm_qkv_rope_fwd": ([_I, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _F, _P], _I),
+    "esm_qkv_rope_bwd": ([_I, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _F, _P], _I),
+    "esm_attn_fwd": ([_I, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _P], _I),
+    "esm_attn_bwd": ([_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _P], _I),
+    "esm_lmhead_xent": ([_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _P], _I),
+    "esm_inv_count": ([_P, _P, _P], _I),
+    "esm_adamw": ([_P, _P, _P, _P, _P, _P, _I64, _P, _P], _I),
+    "esm_cast_f32_bf16": ([_P, _P, _I64, _P], _I),
+}
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load (once) and return the ctypes handle; raises EsmKernelError if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise EsmKernelError(
+            f"{path} not found: build the CUDA extension first (python -c 'import __graft_entry__ as g; g.build()')")
+    lib = ctypes.CDLL(path)
+    for name, (args, res) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def check(rc: int, what: str = ""):
+    if rc != 0:
+        msg = _lib.esm_last_error().decode(errors="replace") if _lib is not None else ""
+        raise EsmKernelError(f"{what} failed (code {rc}): {msg}")
+
+
+def call(name: str, *args):
+    lib = load()
+    rc = getattr(lib, name)(*args)
+    if rc != 0:
+        check(rc, name)
+    return rc
+
+
+def gemm_call(stream: int, **kw):
+    lib = load()
+    g = GemmArgs()
+    for k, v in kw.items():
+        setattr(g, k, v)
+    rc = lib.esm_gemm(ctypes.byref(g), stream)
+    if rc != 0:
+        check(rc, "esm_gemm")

@@ -1,0 +1,803 @@
+// Memory-bound kernels of the ESM-2 MLM step: masking, embeddings (+token dropout),
+// LayerNorm fwd/bwd (+ fused bias-grad column sums, fused GELU'), rotary/head
+// re-layout, LM-head decoder + masked cross-entropy, fused AdamW.
+// All are coalesced, 16-byte vectorised, warp-shuffle reductions; one warp per row
+// for the row-wise ops.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace esm {
+
+static thread_local char g_err[512] = "";
+void set_last_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+static inline cudaStream_t S(esm_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ============================================================================
+// MLM masking (bit-exact with oracle/esm2_oracle.py:mlm_mask)
+// ============================================================================
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
+
+__global__ void mlm_mask_kernel(const int32_t* __restrict__ ids, int32_t* __restrict__ inp, int32_t* __restrict__ lab,
+                                int32_t* __restrict__ n_labels, int64_t n, uint64_t key) {
+  __shared__ int cnt;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  int local = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t id = ids[i];
+    const uint64_t base = key + (uint64_t)i * kGolden;
+    const uint64_t r0 = mix64(base), r1 = mix64(base + 1), r2 = mix64(base + 2);
+    const bool eligible = id >= 4 && id <= 30;
+    const bool sel = eligible && (int64_t)(r0 >> 40) < 2516582;
+    const int64_t a = (int64_t)(r1 >> 40);
+    int32_t out = id;
+    if (sel && a < 13421773) out = 32;
+    else if (sel && a < 15099494) out = 4 + (int32_t)(r2 % 20ull);
+    inp[i] = out;
+    lab[i] = sel ? id : -100;
+    local += sel ? 1 : 0;
+  }
+  local = __reduce_add_sync(0xffffffffu, local);
+  if ((threadIdx.x & 31) == 0 && local) atomicAdd(&cnt, local);
+  __syncthreads();
+  if (threadIdx.x == 0 && n_labels && cnt) atomicAdd(n_labels, cnt);
+}
+
+__global__ void inv_count_kernel(const int32_t* n, float* inv) {
+  const int c = *n;
+  *inv = 1.0f / (float)(c > 1 ? c : 1);
+}
+
+// ============================================================================
+// embeddings (HF:modeling_esm.py:203-234)
+// ============================================================================
+__global__ void row_scale_kernel(const int32_t* __restrict__ ids, const int32_t* __restrict__ am, float* row_scale,
+                                 int S, int token_dropout, int mask_id) {
+  const int b = blockIdx.x;
+  int nm = 0, len = 0;
+  for (int s = threadIdx.x; s < S; s += blockDim.x) {
+    nm += ids[(int64_t)b * S + s] == mask_id;
+    len += am ? (am[(int64_t)b * S + s] != 0) : 1;
+  }
+  __shared__ int sm[2][32];
+  nm = __reduce_add_sync(0xffffffffu, nm);
+  len = __reduce_add_sync(0xffffffffu, len);
+  if ((threadIdx.x & 31) == 0) {
+    sm[0][threadIdx.x >> 5] = nm;
+    sm[1][threadIdx.x >> 5] = len;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int a = 0, l = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      a += sm[0][w];
+      l += sm[1][w];
+    }
+    float scale = 1.0f;
+    if (token_dropout) {
+      const float observed = (float)a / (float)(l > 0 ? l : 1);
+      scale = (1.0f - 0.15f * 0.8f) / (1.0f - observed);
+    }
+    row_scale[b] = scale;
+  }
+}
+
+template <typename T>
+__global__ void embed_fwd_kernel(const int32_t* __restrict__ ids, const int32_t* __restrict__ am,
+                                 const T* __restrict__ E, const float* __restrict__ row_scale, T* __restrict__ x,
+                                 int64_t T_, int S, int H, int token_dropout, int mask_id) {
+  constexpr int VEC = vec16<T>::N;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t t = warp; t < T_; t += nwarps) {
+    const int id = ids[t];
+    float sc = row_scale[t / S] * (am ? (float)(am[t] != 0) : 1.0f);
+    if (token_dropout && id == mask_id) sc = 0.f;
+    for (int h = lane * VEC; h < H; h += 32 * VEC) {
+      float v[VEC];
+      load_vec(E + (int64_t)id * H + h, v);
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) v[i] *= sc;
+      store_vec(x + t * H + h, v);
+    }
+  }
+}
+
+// dE[v, col] += sum over rows with ids==v.  Column-owner threads accumulate in smem (V small).
+template <typename T>
+__global__ void embed_bwd_smem_kernel(const int32_t* __restrict__ ids, const int32_t* __restrict__ am,
+                                      const float* __restrict__ row_scale, const T* __restrict__ dx,
+                                      float* __restrict__ dE, int64_t T_, int S, int H, int V, int rows_per_block,
+                                      int mask_id, int pad_id) {
+  extern __shared__ float acc[];  // [V][blockDim.x]
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int i = threadIdx.x; i < V * (int)blockDim.x; i += blockDim.x) acc[i] = 0.f;
+  __syncthreads();
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_block;
+  const int64_t r1 = min(T_, r0 + rows_per_block);
+  if (col < H) {
+    for (int64_t t = r0; t < r1; ++t) {
+      const int id = ids[t];
+      if (id == pad_id || id == mask_id) continue;  // padding_idx gets no grad; masked rows were zeroed
+      const float sc = row_scale[t / S] * (am ? (float)(am[t] != 0) : 1.0f);
+      acc[id * blockDim.x + threadIdx.x] += io<T>::ld(dx + t * H + col) * sc;
+    }
+  }
+  __syncthreads();
+  if (col < H)
+    for (int v = 0; v < V; ++v) {
+      const float a = acc[v * blockDim.x + threadIdx.x];
+      if (a != 0.f) atomicAdd(dE + (int64_t)v * H + col, a);
+    }
+}
+
+// ============================================================================
+// LayerNorm: one warp per row, values held in registers (MAXV 16-byte vectors per lane)
+// ============================================================================
+template <typename T, int MAXV>
+__global__ void __launch_bounds__(256) ln_fwd_kernel(const T* __restrict__ x, const float* __restrict__ g,
+                                                     const float* __restrict__ b, T* __restrict__ y,
+                                                     float* __restrict__ mean_out, float* __restrict__ rstd_out,
+                                                     int64_t rows, int H, float eps) {
+  constexpr int VEC = vec16<T>::N;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < rows; r += nwarps) {
+    float v[MAXV][VEC];
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < MAXV; ++i) {
+      const int h = (i * 32 + lane) * VEC;
+      if (h < H) {
+        load_vec(x + r * H + h, v[i]);
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) s += v[i][j];
+      }
+    }
+    const float mu = warp_sum(s) / H;
+    float ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < MAXV; ++i) {
+      const int h = (i * 32 + lane) * VEC;
+      if (h < H) {
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) {
+          const float d = v[i][j] - mu;
+          ss += d * d;
+        }
+      }
+    }
+    const float rs = rsqrtf(warp_sum(ss) / H + eps);
+#pragma unroll
+    for (int i = 0; i < MAXV; ++i) {
+      const int h = (i * 32 + lane) * VEC;
+      if (h < H) {
+        float o[VEC];
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) o[j] = (v[i][j] - mu) * rs * __ldg(g + h + j) + __ldg(b + h + j);
+        store_vec(y + r * H + h, o);
+      }
+    }
+    if (lane == 0) {
+      mean_out[r] = mu;
+      rstd_out[r] = rs;
+    }
+  }
+}
+
+// Backward; per-row-group smem accumulators for dgamma / dbeta / column sums, flushed with
+// one atomic per column per block.
+template <typename T, int MAXV>
+__global__ void __launch_bounds__(256) ln_bwd_kernel(const T* __restrict__ dy, const T* __restrict__ x,
+                                                     const float* __restrict__ g, const float* __restrict__ mean,
+                                                     const float* __restrict__ rstd, const T* __restrict__ dres,
+                                                     const T* __restrict__ gelu_z, T* __restrict__ dx,
+                                                     float* __restrict__ dg, float* __restrict__ db,
+                                                     float* __restrict__ csum, int64_t rows, int H) {
+  constexpr int VEC = vec16<T>::N;
+  extern __shared__ float sacc[];  // [nwarps][3][H]
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+  float* my = sacc + (size_t)wib * 3 * H;
+  for (int i = lane; i < 3 * H; i += 32) my[i] = 0.f;
+  __syncwarp();
+  const int64_t warp = (int64_t)blockIdx.x * nw + wib;
+  const int64_t nwarps = (int64_t)gridDim.x * nw;
+  for (int64_t r = warp; r < rows; r += nwarps) {
+    const float mu = mean[r], rs = rstd[r];
+    float xh[MAXV][VEC], gy[MAXV][VEC];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < MAXV; ++i) {
+      const int h = (i * 32 + lane) * VEC;
+      if (h < H) {
+        float xv[VEC], dv[VEC];
+        load_vec(x + r * H + h, xv);
+        load_vec(dy + r * H + h, dv);
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) {
+          xh[i][j] = (xv[j] - mu) * rs;
+          gy[i][j] = dv[j] * __ldg(g + h + j);
+          s1 += gy[i][j];
+          s2 += gy[i][j] * xh[i][j];
+          my[h + j] += dv[j] * xh[i][j];
+          my[H + h + j] += dv[j];
+        }
+      }
+    }
+    s1 = warp_sum(s1) / H;
+    s2 = warp_sum(s2) / H;
+#pragma unroll
+    for (int i = 0; i < MAXV; ++i) {
+      const int h = (i * 32 + lane) * VEC;
+      if (h < H) {
+        float o[VEC];
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) o[j] = rs * (gy[i][j] - s1 - xh[i][j] * s2);
+        if (dres) {
+          float rv[VEC];
+          load_vec(dres + r * H + h, rv);
+#pragma unroll
+          for (int j = 0; j < VEC; ++j) o[j] += rv[j];
+        }
+        if (gelu_z) {
+          float zv[VEC];
+          load_vec(gelu_z + r * H + h, zv);
+#pragma unroll
+          for (int j = 0; j < VEC; ++j) o[j] *= gelu_grad_f(zv[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) my[2 * H + h + j] += o[j];
+        store_vec(dx + r * H + h, o);
+      }
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < H; c += blockDim.x) {
+    float a = 0.f, bsum = 0.f, cs = 0.f;
+    for (int w = 0; w < nw; ++w) {
+      a += sacc[(size_t)w * 3 * H + c];
+      bsum += sacc[(size_t)w * 3 * H + H + c];
+      cs += sacc[(size_t)w * 3 * H + 2 * H + c];
+    }
+    if (dg) atomicAdd(dg + c, a);
+    if (db) atomicAdd(db + c, bsum);
+    if (csum) atomicAdd(csum + c, cs);
+  }
+}
+
+// ============================================================================
+// rotary embedding + [T,3H] <-> [B,nh,S,dh] re-layout (HF:modeling_esm.py:318-344, 45-54)
+// ============================================================================
+template <typename T>
+__global__ void qkv_rope_fwd_kernel(const T* __restrict__ qkv, T* __restrict__ q, T* __restrict__ k,
+                                    T* __restrict__ v, const float* __restrict__ cs, const float* __restrict__ sn,
+                                    int64_t T_, int S, int nh, int dh, float qs) {
+  const int half = dh >> 1;
+  const int H = nh * dh;
+  const int64_t total = T_ * nh * half;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(i % half);
+    const int64_t th = i / half;
+    const int h = (int)(th % nh);
+    const int64_t t = th / nh;
+    const int s = (int)(t % S);
+    const int64_t b = t / S;
+    const float c = cs[(int64_t)s * half + j], sv = sn[(int64_t)s * half + j];
+    const T* row = qkv + t * 3 * H + h * dh;
+    const int64_t o = ((b * nh + h) * S + s) * dh;
+    float q0 = io<T>::ld(row + j) * qs, q1 = io<T>::ld(row + j + half) * qs;
+    io<T>::st(q + o + j, q0 * c - q1 * sv);
+    io<T>::st(q + o + j + half, q1 * c + q0 * sv);
+    float k0 = io<T>::ld(row + H + j), k1 = io<T>::ld(row + H + j + half);
+    io<T>::st(k + o + j, k0 * c - k1 * sv);
+    io<T>::st(k + o + j + half, k1 * c + k0 * sv);
+    v[o + j] = row[2 * H + j];
+    v[o + j + half] = row[2 * H + j + half];
+  }
+}
+
+// each thread owns one (head, j) column pair of q, k and v; loops rows; column sums -> bias grads
+template <typename T>
+__global__ void qkv_rope_bwd_kernel(const float* __restrict__ dq, const T* __restrict__ dk,
+                                    const T* __restrict__ dv, T* __restrict__ dqkv, float* __restrict__ csum,
+                                    const float* __restrict__ cs, const float* __restrict__ sn, int64_t T_, int S,
+                                    int nh, int dh, float qs, int rows_per_block) {
+  const int half = dh >> 1;
+  const int H = nh * dh;
+  const int pair = blockIdx.x * blockDim.x + threadIdx.x;  // 0 .. nh*half
+  if (pair >= nh * half) return;
+  const int h = pair / half, j = pair % half;
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_block, r1 = min(T_, r0 + rows_per_block);
+  float a[6] = {0, 0, 0, 0, 0, 0};
+  for (int64_t t = r0; t < r1; ++t) {
+    const int s = (int)(t % S);
+    const int64_t b = t / S;
+    const float c = cs[(int64_t)s * half + j], sv = sn[(int64_t)s * half + j];
+    const int64_t o = ((b * nh + h) * S + s) * dh;
+    // RoPE^T: dx_j = dy_j c + dy_{j+h} s ; dx_{j+h} = dy_{j+h} c - dy_j s
+    const float g0 = dq[o + j], g1 = dq[o + j + half];
+    const float q0 = (g0 * c + g1 * sv) * qs, q1 = (g1 * c - g0 * sv) * qs;
+    const float e0 = io<T>::ld(dk + o + j), e1 = io<T>::ld(dk + o + j + half);
+    const float k0 = e0 * c + e1 * sv, k1 = e1 * c - e0 * sv;
+    const float v0 = io<T>::ld(dv + o + j), v1 = io<T>::ld(dv + o + j + half);
+    T* row = dqkv + t * 3 * H + h * dh;
+    io<T>::st(row + j, q0);
+    io<T>::st(row + j + half, q1);
+    io<T>::st(row + H + j, k0);
+    io<T>::st(row + H + j + half, k1);
+    io<T>::st(row + 2 * H + j, v0);
+    io<T>::st(row + 2 * H + j + half, v1);
+    a[0] += q0; a[1] += q1; a[2] += k0; a[3] += k1; a[4] += v0; a[5] += v1;
+  }
+  if (csum) {
+    const int c0 = h * dh + j;
+    atomicAdd(csum + c0, a[0]);
+    atomicAdd(csum + c0 + half, a[1]);
+    atomicAdd(csum + H + c0, a[2]);
+    atomicAdd(csum + H + c0 + half, a[3]);
+    atomicAdd(csum + 2 * H + c0, a[4]);
+    atomicAdd(csum + 2 * H + c0 + half, a[5]);
+  }
+}
+
+// ============================================================================
+// LM head decoder (tied E) + masked cross entropy (HF:modeling_esm.py:777-784, 808-815)
+// ============================================================================
+template <typename T, int MAXV, int V_MAX>
+__global__ void __launch_bounds__(256) xent_kernel(const T* __restrict__ n, const T* __restrict__ E,
+                                                   const float* __restrict__ bias, const int32_t* __restrict__ labels,
+                                                   const float* __restrict__ inv_denom, float* __restrict__ loss_sum,
+                                                   float* __restrict__ dlogits, T* __restrict__ dn,
+                                                   float* __restrict__ dbias, int64_t rows, int H, int V) {
+  constexpr int VEC = vec16<T>::N;
+  __shared__ float s_dbias[V_MAX];
+  __shared__ float s_loss;
+  for (int i = threadIdx.x; i < V_MAX; i += blockDim.x) s_dbias[i] = 0.f;
+  if (threadIdx.x == 0) s_loss = 0.f;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const float inv = *inv_denom;
+  float my_loss = 0.f;
+  for (int64_t r = warp; r < rows; r += nwarps) {
+    const int lab = labels[r];
+    if (lab < 0) {
+      float z[VEC] = {};
+      for (int h = lane * VEC; h < H; h += 32 * VEC) store_vec(dn + r * H + h, z);
+      continue;
+    }
+    float x[MAXV][VEC];
+#pragma unroll
+    for (int i = 0; i < MAXV; ++i) {
+      const int h = (i * 32 + lane) * VEC;
+      if (h < H) load_vec(n + r * H + h, x[i]);
+    }
+    float logit[V_MAX];
+#pragma unroll
+    for (int v = 0; v < V_MAX; ++v) {
+      float p = 0.f;
+      if (v < V) {
+#pragma unroll
+        for (int i = 0; i < MAXV; ++i) {
+          const int h = (i * 32 + lane) * VEC;
+          if (h < H) {
+            float e[VEC];
+            load_vec(E + (int64_t)v * H + h, e);
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) p += x[i][j] * e[j];
+          }
+        }
+      }
+      logit[v] = v < V ? warp_sum(p) + bias[v] : -INFINITY;
+    }
+    float mx = -INFINITY;
+#pragma unroll
+    for (int v = 0; v < V_MAX; ++v) mx = fmaxf(mx, logit[v]);
+    float se = 0.f;
+#pragma unroll
+    for (int v = 0; v < V_MAX; ++v) se += (v < V) ? __expf(logit[v] - mx) : 0.f;
+    const float lse = mx + __logf(se);
+    float tgt = 0.f;
+#pragma unroll
+    for (int v = 0; v < V_MAX; ++v) tgt = (v == lab) ? logit[v] : tgt;
+    if (lane == 0) my_loss += (lse - tgt) * inv;
+    // dlogits
+#pragma unroll
+    for (int v = 0; v < V_MAX; ++v) {
+      const float d = (v < V) ? (__expf(logit[v] - lse) - (v == lab ? 1.f : 0.f)) * inv : 0.f;
+      logit[v] = d;
+    }
+    if (lane < V_MAX && lane < V) {
+      float d = 0.f;
+#pragma unroll
+      for (int v = 0; v < V_MAX; ++v) d = (v == lane) ? logit[v] : d;
+      dlogits[r * V + lane] = d;
+      atomicAdd(&s_dbias[lane], d);
+    }
+    if (V > 32 && lane + 32 < V) {
+      float d = 0.f;
+#pragma unroll
+      for (int v = 32; v < V_MAX; ++v) d = (v == lane + 32) ? logit[v] : d;
+      dlogits[r * V + lane + 32] = d;
+      atomicAdd(&s_dbias[lane + 32], d);
+    }
+    // dn = dlogits · E
+#pragma unroll
+    for (int i = 0; i < MAXV; ++i) {
+      const int h = (i * 32 + lane) * VEC;
+      if (h < H) {
+        float o[VEC] = {};
+#pragma unroll
+        for (int v = 0; v < V_MAX; ++v) {
+          if (v < V) {
+            float e[VEC];
+            load_vec(E + (int64_t)v * H + h, e);
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) o[j] += logit[v] * e[j];
+          }
+        }
+        store_vec(dn + r * H + h, o);
+      }
+    }
+  }
+  my_loss = warp_sum(my_loss);
+  if (lane == 0 && my_loss != 0.f) atomicAdd(&s_loss, my_loss);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_loss != 0.f) atomicAdd(loss_sum, s_loss);
+  for (int i = threadIdx.x; i < V && i < V_MAX; i += blockDim.x)
+    if (s_dbias[i] != 0.f) atomicAdd(dbias + i, s_dbias[i]);
+}
+
+// dE[v, h] += sum_{labelled rows r} dlogits[r, v] * n[r, h]; lane = column, warps = rows
+template <typename T, int V_MAX>
+__global__ void __launch_bounds__(256) xent_dE_kernel(const T* __restrict__ n, const int32_t* __restrict__ labels,
+                                                      const float* __restrict__ dlogits, float* __restrict__ dE,
+                                                      int64_t rows, int H, int V, int rows_per_block) {
+  __shared__ float red[8][V_MAX][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int col = blockIdx.x * 32 + lane;
+  float acc[V_MAX];
+#pragma unroll
+  for (int v = 0; v < V_MAX; ++v) acc[v] = 0.f;
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_block, r1 = min(rows, r0 + rows_per_block);
+  for (int64_t r = r0 + w; r < r1; r += 8) {
+    if (labels[r] < 0) continue;
+    const float x = col < H ? io<T>::ld(n + r * H + col) : 0.f;
+#pragma unroll
+    for (int v = 0; v < V_MAX; ++v)
+      if (v < V) acc[v] += dlogits[r * V + v] * x;
+  }
+#pragma unroll
+  for (int v = 0; v < V_MAX; ++v) red[w][v][lane] = acc[v];
+  __syncthreads();
+  for (int i = threadIdx.x; i < V * 32; i += blockDim.x) {
+    const int v = i / 32, l = i % 32;
+    float s = 0.f;
+#pragma unroll
+    for (int ww = 0; ww < 8; ++ww) s += red[ww][v][l];
+    const int c = blockIdx.x * 32 + l;
+    if (c < H && s != 0.f) atomicAdd(dE + (int64_t)v * H + c, s);
+  }
+}
+
+// ============================================================================
+// fused AdamW over the flat fp32 parameter buffer (+ bf16 shadow refresh)
+// ============================================================================
+__global__ void __launch_bounds__(256) adamw_kernel(float* __restrict__ p, const float* __restrict__ g,
+                                                    float* __restrict__ m, float* __restrict__ v,
+                                                    __nv_bfloat16* __restrict__ p16,
+                                                    const uint8_t* __restrict__ decay, int64_t n,
+                                                    const float* __restrict__ hyper) {
+  const float lr = hyper[0], b1 = hyper[1], b2 = hyper[2], eps = hyper[3], wd = hyper[4], step = hyper[5],
+              gs = hyper[6];
+  const float bc1 = 1.0f - powf(b1, step), bc2 = 1.0f - powf(b2, step);
+  const float step_size = lr / bc1, inv_sqrt_bc2 = rsqrtf(bc2);
+  const int64_t n4 = n >> 2;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i << 2;
+    const float dec = decay[e >> 8] ? (1.0f - lr * wd) : 1.0f;
+    float4 pp = reinterpret_cast<float4*>(p)[i];
+    const float4 gg = reinterpret_cast<const float4*>(g)[i];
+    float4 mm = reinterpret_cast<float4*>(m)[i];
+    float4 vv = reinterpret_cast<float4*>(v)[i];
+    float* P = &pp.x;
+    const float* G = &gg.x;
+    float* M = &mm.x;
+    float* VV = &vv.x;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float gj = G[j] * gs;
+      P[j] *= dec;
+      M[j] = b1 * M[j] + (1.0f - b1) * gj;
+      VV[j] = b2 * VV[j] + (1.0f - b2) * gj * gj;
+      const float denom = sqrtf(VV[j]) * inv_sqrt_bc2 + eps;
+      P[j] -= step_size * M[j] / denom;
+    }
+    reinterpret_cast<float4*>(p)[i] = pp;
+    reinterpret_cast<float4*>(m)[i] = mm;
+    reinterpret_cast<float4*>(v)[i] = vv;
+    if (p16) {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(pp.x, pp.y), hi = __floats2bfloat162_rn(pp.z, pp.w);
+      uint2 u;
+      u.x = *reinterpret_cast<uint32_t*>(&lo);
+      u.y = *reinterpret_cast<uint32_t*>(&hi);
+      reinterpret_cast<uint2*>(p16)[i] = u;
+    }
+  }
+}
+
+__global__ void cast_kernel(const float* __restrict__ s, __nv_bfloat16* __restrict__ d, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    d[i] = __float2bfloat16_rn(s[i]);
+}
+
+static int grid_for(int64_t work, int block, int cap = 148 * 16) {
+  int64_t g = (work + block - 1) / block;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+}  // namespace esm
+
+using namespace esm;
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+int esm_version(void) { return 10000; }
+const char* esm_last_error(void) { return esm::g_err; }
+int esm_device_sm_count(int device) {
+  int v = 0;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+  return v;
+}
+
+int esm_tokenize(const char* seq, int len, int32_t* out, int max_out) {
+  static int table[256];
+  static bool init = false;
+  if (!init) {
+    for (int i = 0; i < 256; ++i) table[i] = 3;  // <unk>
+    const char* aa = "LAGVSERTIDPKQNFYMHWC";
+    for (int i = 0; i < 20; ++i) table[(unsigned char)aa[i]] = 4 + i;
+    const char* ex = "XBUZO.-";
+    for (int i = 0; i < 7; ++i) table[(unsigned char)ex[i]] = 24 + i;
+    init = true;
+  }
+  const int need = len + 2;
+  if (!out || max_out < need) return -need;
+  out[0] = 0;
+  for (int i = 0; i < len; ++i) out[i + 1] = table[(unsigned char)seq[i]];
+  out[len + 1] = 2;
+  return need;
+}
+
+int esm_mlm_mask(const int32_t* ids, int32_t* input_ids, int32_t* labels, int32_t* n_labels, int64_t n, uint64_t seed,
+                 uint64_t stream_id, esm_stream_t stream) {
+  ESM_CHECK_ARG(ids && input_ids && labels && n >= 0, "esm_mlm_mask: bad args");
+  const uint64_t k0 = mix64(seed + kGolden);
+  const uint64_t key = mix64(k0 ^ stream_id);
+  if (n == 0) return 0;
+  mlm_mask_kernel<<<grid_for(n, 256), 256, 0, S(stream)>>>(ids, input_ids, labels, n_labels, n, key);
+  ESM_LAUNCH_RET();
+}
+
+int esm_inv_count(const int32_t* n_labels, float* inv_denom, esm_stream_t stream) {
+  inv_count_kernel<<<1, 1, 0, S(stream)>>>(n_labels, inv_denom);
+  ESM_LAUNCH_RET();
+}
+
+int esm_embed_fwd(int dtype, const int32_t* ids, const int32_t* am, const void* E, void* x, float* row_scale, int B,
+                  int Sq, int H, int token_dropout, int mask_id, esm_stream_t stream) {
+  ESM_CHECK_ARG(ids && E && x && row_scale && B > 0 && Sq > 0 && H > 0, "esm_embed_fwd: bad args");
+  ESM_CHECK_ARG(H % 8 == 0, "esm_embed_fwd: H %% 8");
+  row_scale_kernel<<<B, 256, 0, S(stream)>>>(ids, am, row_scale, Sq, token_dropout, mask_id);
+  const int64_t T_ = (int64_t)B * Sq;
+  const int grid = grid_for(T_ * 32, 256);
+  if (dtype == ESM_BF16)
+    embed_fwd_kernel<__nv_bfloat16><<<grid, 256, 0, S(stream)>>>(ids, am, (const __nv_bfloat16*)E, row_scale,
+                                                                 (__nv_bfloat16*)x, T_, Sq, H, token_dropout, mask_id);
+  else
+    embed_fwd_kernel<float><<<grid, 256, 0, S(stream)>>>(ids, am, (const float*)E, row_scale, (float*)x, T_, Sq, H,
+                                                         token_dropout, mask_id);
+  ESM_LAUNCH_RET();
+}
+
+int esm_embed_bwd(int dtype, const int32_t* ids, const int32_t* am, const float* row_scale, const void* dx, float* dE,
+                  int B, int Sq, int H, int V, int mask_id, int pad_id, esm_stream_t stream) {
+  ESM_CHECK_ARG(ids && row_scale && dx && dE && V > 0 && V <= 128, "esm_embed_bwd: bad args (V<=128)");
+  const int64_t T_ = (int64_t)B * Sq;
+  const int bx = 128;
+  const int rpb = 256;
+  dim3 grid((H + bx - 1) / bx, (unsigned)((T_ + rpb - 1) / rpb));
+  const size_t sm = (size_t)V * bx * sizeof(float);
+  if (dtype == ESM_BF16)
+    embed_bwd_smem_kernel<__nv_bfloat16><<<grid, bx, sm, S(stream)>>>(ids, am, row_scale, (const __nv_bfloat16*)dx,
+                                                                      dE, T_, Sq, H, V, rpb, mask_id, pad_id);
+  else
+    embed_bwd_smem_kernel<float><<<grid, bx, sm, S(stream)>>>(ids, am, row_scale, (const float*)dx, dE, T_, Sq, H, V,
+                                                              rpb, mask_id, pad_id);
+  ESM_LAUNCH_RET();
+}
+
+#define LN_DISPATCH(T, KERNEL, MAXV_NEEDED, ...)                                    \
+  do {                                                                              \
+    if (MAXV_NEEDED <= 1) KERNEL<T, 1>__VA_ARGS__;                                  \
+    else if (MAXV_NEEDED <= 2) KERNEL<T, 2>__VA_ARGS__;                             \
+    else if (MAXV_NEEDED <= 4) KERNEL<T, 4>__VA_ARGS__;                             \
+    else if (MAXV_NEEDED <= 6) KERNEL<T, 6>__VA_ARGS__;                             \
+    else if (MAXV_NEEDED <= 10) KERNEL<T, 10>__VA_ARGS__;                           \
+    else if (MAXV_NEEDED <= 20) KERNEL<T, 20>__VA_ARGS__;                           \
+    else { esm::set_last_error("hidden size too large"); return ESM_ENOTSUP; }      \
+  } while (0)
+
+int esm_layernorm_fwd(int dtype, const void* x, const float* gamma, const float* beta, void* y, float* mean, float* rstd,
+                      int rows, int H, float eps, esm_stream_t stream) {
+  ESM_CHECK_ARG(x && gamma && beta && y && mean && rstd && rows > 0 && H > 0, "esm_layernorm_fwd: bad args");
+  const int grid = grid_for((int64_t)rows * 32, 256);
+  if (dtype == ESM_BF16) {
+    ESM_CHECK_ARG(H % 8 == 0, "layernorm: H %% 8");
+    const int mv = (H + 255) / 256;
+    LN_DISPATCH(__nv_bfloat16, ln_fwd_kernel, mv,
+                <<<grid, 256, 0, S(stream)>>>((const __nv_bfloat16*)x, gamma, beta, (__nv_bfloat16*)y, mean, rstd,
+                                              rows, H, eps));
+  } else {
+    ESM_CHECK_ARG(H % 4 == 0, "layernorm: H %% 4");
+    const int mv = (H + 127) / 128;
+    LN_DISPATCH(float, ln_fwd_kernel, mv,
+                <<<grid, 256, 0, S(stream)>>>((const float*)x, gamma, beta, (float*)y, mean, rstd, rows, H, eps));
+  }
+  ESM_LAUNCH_RET();
+}
+
+int esm_layernorm_bwd(int dtype, const void* dy, const void* x, const float* gamma, const float* mean,
+                      const float* rstd, const void* dres, const void* gelu_z, void* dx, float* dgamma, float* dbeta,
+                      float* col_sum, int rows, int H, esm_stream_t stream) {
+  ESM_CHECK_ARG(dy && x && gamma && mean && rstd && dx && rows > 0, "esm_layernorm_bwd: bad args");
+  int warps = 8;
+  while (warps > 1 && (size_t)warps * 3 * H * 4 > 120 * 1024) warps >>= 1;
+  const int block = warps * 32;
+  const size_t sm = (size_t)warps * 3 * H * 4;
+  int grid = (int)((rows + warps * 8 - 1) / (warps * 8));  // >= 8 rows per warp amortises the flush
+  if (grid > 148 * 4) grid = 148 * 4;
+  if (grid < 1) grid = 1;
+  if (dtype == ESM_BF16) {
+    ESM_CHECK_ARG(H % 8 == 0, "layernorm: H %% 8");
+    const int mv = (H + 255) / 256;
+    auto setattr = [&](const void* k) { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); };
+    if (mv <= 1) setattr((const void*)ln_bwd_kernel<__nv_bfloat16, 1>);
+    else if (mv <= 2) setattr((const void*)ln_bwd_kernel<__nv_bfloat16, 2>);
+    else if (mv <= 4) setattr((const void*)ln_bwd_kernel<__nv_bfloat16, 4>);
+    else if (mv <= 6) setattr((const void*)ln_bwd_kernel<__nv_bfloat16, 6>);
+    else if (mv <= 10) setattr((const void*)ln_bwd_kernel<__nv_bfloat16, 10>);
+    else setattr((const void*)ln_bwd_kernel<__nv_bfloat16, 20>);
+    LN_DISPATCH(__nv_bfloat16, ln_bwd_kernel, mv,
+                <<<grid, block, sm, S(stream)>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, gamma, mean, rstd,
+                                                 (const __nv_bfloat16*)dres, (const __nv_bfloat16*)gelu_z,
+                                                 (__nv_bfloat16*)dx, dgamma, dbeta, col_sum, rows, H));
+  } else {
+    ESM_CHECK_ARG(H % 4 == 0, "layernorm: H %% 4");
+    const int mv = (H + 127) / 128;
+    auto setattr = [&](const void* k) { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); };
+    if (mv <= 1) setattr((const void*)ln_bwd_kernel<float, 1>);
+    else if (mv <= 2) setattr((const void*)ln_bwd_kernel<float, 2>);
+    else if (mv <= 4) setattr((const void*)ln_bwd_kernel<float, 4>);
+    else if (mv <= 6) setattr((const void*)ln_bwd_kernel<float, 6>);
+    else if (mv <= 10) setattr((const void*)ln_bwd_kernel<float, 10>);
+    else setattr((const void*)ln_bwd_kernel<float, 20>);
+    LN_DISPATCH(float, ln_bwd_kernel, mv,
+                <<<grid, block, sm, S(stream)>>>((const float*)dy, (const float*)x, gamma, mean, rstd,
+                                                 (const float*)dres, (const float*)gelu_z, (float*)dx, dgamma, dbeta,
+                                                 col_sum, rows, H));
+  }
+  ESM_LAUNCH_RET();
+}
+
+int esm_qkv_rope_fwd(int dtype, const void* qkv, void* q, void* k, void* v, const float* cos_t, const float* sin_t,
+                     int B, int Sq, int nh, int dh, float q_scale, esm_stream_t stream) {
+  ESM_CHECK_ARG(qkv && q && k && v && cos_t && sin_t && dh % 2 == 0, "esm_qkv_rope_fwd: bad args");
+  const int64_t T_ = (int64_t)B * Sq;
+  const int grid = grid_for(T_ * nh * (dh / 2), 256);
+  if (dtype == ESM_BF16)
+    qkv_rope_fwd_kernel<__nv_bfloat16><<<grid, 256, 0, S(stream)>>>(
+        (const __nv_bfloat16*)qkv, (__nv_bfloat16*)q, (__nv_bfloat16*)k, (__nv_bfloat16*)v, cos_t, sin_t, T_, Sq, nh,
+        dh, q_scale);
+  else
+    qkv_rope_fwd_kernel<float><<<grid, 256, 0, S(stream)>>>((const float*)qkv, (float*)q, (float*)k, (float*)v, cos_t,
+                                                            sin_t, T_, Sq, nh, dh, q_scale);
+  ESM_LAUNCH_RET();
+}
+
+int esm_qkv_rope_bwd(int dtype, const float* dq, const void* dk, const void* dv, void* dqkv, float* col_sum,
+                     const float* cos_t, const float* sin_t, int B, int Sq, int nh, int dh, float q_scale,
+                     esm_stream_t stream) {
+  ESM_CHECK_ARG(dq && dk && dv && dqkv && cos_t && sin_t && dh % 2 == 0, "esm_qkv_rope_bwd: bad args");
+  const int64_t T_ = (int64_t)B * Sq;
+  const int pairs = nh * dh / 2;
+  const int bx = 128;
+  const int rpb = 128;
+  dim3 grid((pairs + bx - 1) / bx, (unsigned)((T_ + rpb - 1) / rpb));
+  if (dtype == ESM_BF16)
+    qkv_rope_bwd_kernel<__nv_bfloat16><<<grid, bx, 0, S(stream)>>>(
+        dq, (const __nv_bfloat16*)dk, (const __nv_bfloat16*)dv, (__nv_bfloat16*)dqkv, col_sum, cos_t, sin_t, T_, Sq,
+        nh, dh, q_scale, rpb);
+  else
+    qkv_rope_bwd_kernel<float><<<grid, bx, 0, S(stream)>>>(dq, (const float*)dk, (const float*)dv, (float*)dqkv,
+                                                           col_sum, cos_t, sin_t, T_, Sq, nh, dh, q_scale, rpb);
+  ESM_LAUNCH_RET();
+}
+
+int esm_lmhead_xent(int dtype, const void* n, const void* E, const float* bias, const int32_t* labels,
+                    const float* inv_denom, float* loss_sum, float* dlogits_ws, void* dn, float* dE, float* dbias,
+                    int T_, int H, int V, esm_stream_t stream) {
+  ESM_CHECK_ARG(n && E && bias && labels && inv_denom && loss_sum && dlogits_ws && dn && dE && dbias,
+                "esm_lmhead_xent: null pointer");
+  ESM_CHECK_ARG(V > 0 && V <= 64, "esm_lmhead_xent: V must be <= 64 (ESM alphabet is 33)");
+  const int grid = grid_for((int64_t)T_ * 32, 256, 148 * 8);
+  const int rpb = 512;
+  dim3 g2((H + 31) / 32, (T_ + rpb - 1) / rpb);
+  if (dtype == ESM_BF16) {
+    ESM_CHECK_ARG(H % 8 == 0, "xent: H %% 8");
+    const int mv = (H + 255) / 256;
+    auto* nn = (const __nv_bfloat16*)n;
+    auto* ee = (const __nv_bfloat16*)E;
+    auto* dd = (__nv_bfloat16*)dn;
+#define XL(MV) xent_kernel<__nv_bfloat16, MV, 40><<<grid, 256, 0, S(stream)>>>(nn, ee, bias, labels, inv_denom, loss_sum, dlogits_ws, dd, dbias, T_, H, V)
+    if (V > 40) { esm::set_last_error("xent: V > 40 unsupported in bf16 path"); return ESM_ENOTSUP; }
+    if (mv <= 1) XL(1); else if (mv <= 2) XL(2); else if (mv <= 4) XL(4); else if (mv <= 6) XL(6); else if (mv <= 10) XL(10);
+    else { esm::set_last_error("xent: H too large"); return ESM_ENOTSUP; }
+#undef XL
+    xent_dE_kernel<__nv_bfloat16, 40><<<g2, 256, 0, S(stream)>>>(nn, labels, dlogits_ws, dE, T_, H, V, rpb);
+  } else {
+    ESM_CHECK_ARG(H % 4 == 0, "xent: H %% 4");
+    const int mv = (H + 127) / 128;
+    auto* nn = (const float*)n;
+    auto* ee = (const float*)E;
+    auto* dd = (float*)dn;
+#define XL(MV) xent_kernel<float, MV, 40><<<grid, 256, 0, S(stream)>>>(nn, ee, bias, labels, inv_denom, loss_sum, dlogits_ws, dd, dbias, T_, H, V)
+    if (V > 40) { esm::set_last_error("xent: V > 40 unsupported"); return ESM_ENOTSUP; }
+    if (mv <= 1) XL(1); else if (mv <= 2) XL(2); else if (mv <= 4) XL(4); else if (mv <= 6) XL(6); else if (mv <= 10) XL(10);
+    else { esm::set_last_error("xent: H too large"); return ESM_ENOTSUP; }
+#undef XL
+    xent_dE_kernel<float, 40><<<g2, 256, 0, S(stream)>>>(nn, labels, dlogits_ws, dE, T_, H, V, rpb);
+  }
+  ESM_LAUNCH_RET();
+}
+
+int esm_adamw(float* p, const float* g, float* m, float* v, void* p16, const uint8_t* decay_chunk, int64_t n,
+              const float* hyper, esm_stream_t stream) {
+  ESM_CHECK_ARG(p && g && m && v && decay_chunk && hyper && n % 256 == 0, "esm_adamw: bad args (n %% 256 == 0)");
+  adamw_kernel<<<grid_for(n / 4, 256, 148 * 8), 256, 0, S(stream)>>>(p, g, m, v, (__nv_bfloat16*)p16, decay_chunk, n,
+                                                                     hyper);
+  ESM_LAUNCH_RET();
+}
+
+int esm_cast_f32_bf16(const float* src, void* dst, int64_t n, esm_stream_t stream) {
+  ESM_CHECK_ARG(src && dst && n >= 0, "esm_cast: bad args");
+  if (n == 0) return 0;
+  cast_kernel<<<grid_for(n, 256), 256, 0, S(stream)>>>(src, (__nv_bfloat16*)dst, n);
+  ESM_LAUNCH_RET();
+}
+
+}  // extern "C"

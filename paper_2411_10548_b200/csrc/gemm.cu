@@ -1,0 +1,575 @@
+// Linear layers of the ESM-2 encoder: C[M,N] = A[M,K] · B[N,K]^T with fused epilogues.
+//
+//   forward  (HF nn.Linear, HF:modeling_esm.py:300-302,365-375,406-427):  A = X  (K-major), B = W (K-major)
+//   dgrad    dX = dY · W                                                  A = dY (K-major), B = W (N-major)
+//   wgrad    dW += dYᵀ · X                                                A = dY (M-major), B = X (N-major)
+//
+// bf16 path: persistent warp-specialised tcgen05 kernel.  TMA (SWIZZLE_128B) feeds a
+// STAGES-deep smem ring; one elected thread issues tcgen05.mma (M=128, N=BN, K=16)
+// into a double-buffered TMEM accumulator; four epilogue warps drain TMEM with
+// tcgen05.ld and apply bias / GELU / residual / GELU' (+ fused bias-grad column sums)
+// or fp32 red.add (split-K weight gradients).
+// fp32 path (parity mode): tiled SIMT FFMA kernel with the same epilogues.
+#include <cstdarg>
+#include <cstdio>
+#include <mutex>
+
+#include "common.cuh"
+#include "sm100.cuh"
+
+namespace esm {
+
+struct EpiParams {
+  int M, N;
+  void* C;
+  int64_t ldc;
+  const float* bias;
+  const void* aux_in;
+  int64_t ld_aux_in;
+  void* aux_out;
+  int64_t ld_aux_out;
+  float* col_sum;
+};
+
+// ============================================================================
+// tcgen05 kernel
+// ============================================================================
+namespace sm100 {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int kThreads = 192;  // warp0 TMA, warp1 MMA (+TMEM alloc), warps 2..5 epilogue
+
+template <int BN>
+struct Cfg {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
+  static constexpr uint32_t TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
+                                                          : (2 * BN <= 256) ? 256 : 512;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+struct TileInfo {
+  int num_m, num_n, splits, kb_total, kb_per_split;
+};
+
+__device__ __forceinline__ void decode_tile(const TileInfo& ti, int t, int& mb, int& nb, int& kb0, int& kb1) {
+  const int per_split = ti.num_m * ti.num_n;
+  const int split = t / per_split;
+  const int rem = t - split * per_split;
+  mb = rem / ti.num_n;  // n fastest: concurrent CTAs share the A row-block in L2
+  nb = rem - mb * ti.num_n;
+  kb0 = split * ti.kb_per_split;
+  kb1 = min(ti.kb_total, kb0 + ti.kb_per_split);
+}
+
+template <int EPI>
+__device__ __forceinline__ void epilogue_chunk(const EpiParams& p, int row, int col0, float (&v)[32], int lane) {
+  const bool row_ok = row < p.M;
+  const bool full = row_ok && (col0 + 32 <= p.N);
+  if constexpr (EPI == ESM_EPI_F32_ACC) {
+    if (!row_ok) return;
+    float* c = reinterpret_cast<float*>(p.C) + (int64_t)row * p.ldc + col0;
+    if (full) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) red_add_v4_f32(c + j, v[j], v[j + 1], v[j + 2], v[j + 3]);
+    } else {
+      for (int j = 0; j < 32 && col0 + j < p.N; ++j) red_add_f32(c + j, v[j]);
+    }
+    return;
+  } else {
+    if (p.bias != nullptr && EPI != ESM_EPI_DGELU) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] += (col0 + j < p.N) ? __ldg(p.bias + col0 + j) : 0.f;
+    }
+    if constexpr (EPI == ESM_EPI_RESID || EPI == ESM_EPI_DGELU) {
+      const __nv_bfloat16* a = reinterpret_cast<const __nv_bfloat16*>(p.aux_in) + (int64_t)row * p.ld_aux_in + col0;
+      float r[32];
+      if (full) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 8) load_vec(a + j, r + j);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) r[j] = (row_ok && col0 + j < p.N) ? __bfloat162float(a[j]) : 0.f;
+      }
+      if constexpr (EPI == ESM_EPI_RESID) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] += r[j];
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] *= gelu_grad_f(r[j]);
+      }
+    }
+    __nv_bfloat16* c = reinterpret_cast<__nv_bfloat16*>(p.C) + (int64_t)row * p.ldc + col0;
+    if constexpr (EPI == ESM_EPI_GELU) {
+      __nv_bfloat16* z = reinterpret_cast<__nv_bfloat16*>(p.aux_out) + (int64_t)row * p.ld_aux_out + col0;
+      if (full) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 8) store_vec(z + j, v + j);
+      } else if (row_ok) {
+        for (int j = 0; j < 32 && col0 + j < p.N; ++j) z[j] = __float2bfloat16_rn(v[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = gelu_f(v[j]);
+    }
+    if (full) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 8) store_vec(c + j, v + j);
+    } else if (row_ok) {
+      for (int j = 0; j < 32 && col0 + j < p.N; ++j) c[j] = __float2bfloat16_rn(v[j]);
+    }
+    if constexpr (EPI == ESM_EPI_DGELU) {
+      if (p.col_sum != nullptr) {
+        if (!row_ok) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = 0.f;
+        }
+        const float s = warp_transpose_sum32(v, lane);
+        if (col0 + lane < p.N) red_add_f32(p.col_sum + col0 + lane, s);
+      }
+    }
+  }
+}
+
+template <int BN, bool A_MN, bool B_MN, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TileInfo ti,
+                   EpiParams ep) {
+  using C = Cfg<BN>;
+  constexpr int STAGES = C::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * C::A_BYTES;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* tfull_bar = empty_bar + STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull_bar[b], 1);
+      mbar_init(&tempty_bar[b], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+  }
+  if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int num_tiles = ti.num_m * ti.num_n * ti.splits;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      int mb, nb, kb0, kb1;
+      decode_tile(ti, t, mb, nb, kb0, kb1);
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&empty_bar[stage], phase ^ 1);
+        if (lane == 0) {
+          uint8_t* a_dst = sA + stage * C::A_BYTES;
+          uint8_t* b_dst = sB + stage * C::B_BYTES;
+          mbar_expect_tx(&full_bar[stage], C::STAGE_BYTES);
+          if constexpr (!A_MN) {
+            tma_load_2d(a_dst, &tmA, &full_bar[stage], kb * BK, mb * BM);
+          } else {
+#pragma unroll
+            for (int i = 0; i < BM / 64; ++i)
+              tma_load_2d(a_dst + i * 64 * BK * 2, &tmA, &full_bar[stage], mb * BM + i * 64, kb * BK);
+          }
+          if constexpr (!B_MN) {
+            tma_load_2d(b_dst, &tmB, &full_bar[stage], kb * BK, nb * BN);
+          } else {
+#pragma unroll
+            for (int i = 0; i < BN / 64; ++i)
+              tma_load_2d(b_dst + i * 64 * BK * 2, &tmB, &full_bar[stage], nb * BN + i * 64, kb * BK);
+          }
+        }
+        __syncwarp();
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    constexpr uint32_t idesc = make_idesc_bf16(BM, BN, A_MN, B_MN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+      int mb, nb, kb0, kb1;
+      decode_tile(ti, t, mb, nb, kb0, kb1);
+      const int buf = it & 1;
+      const uint32_t aphase = (it >> 1) & 1;
+      mbar_wait(&tempty_bar[buf], aphase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + buf * BN;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&full_bar[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a_base = smem_u32(sA + stage * C::A_BYTES);
+          const uint32_t b_base = smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = A_MN ? make_sdesc_sw128(a_base + k * 16 * 128, BK * 128, 1024)
+                                     : make_sdesc_sw128(a_base + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? make_sdesc_sw128(b_base + k * 16 * 128, BK * 128, 1024)
+                                     : make_sdesc_sw128(b_base + k * 32, 16, 1024);
+            mma_bf16_ss(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          }
+          mma_commit(&empty_bar[stage]);
+          if (kb == kb1 - 1) mma_commit(&tfull_bar[buf]);
+        }
+        __syncwarp();
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ===================== epilogue warps =====================
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    int it = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+      int mb, nb, kb0, kb1;
+      decode_tile(ti, t, mb, nb, kb0, kb1);
+      const int buf = it & 1;
+      const uint32_t aphase = (it >> 1) & 1;
+      mbar_wait(&tfull_bar[buf], aphase);
+      tc_fence_after();
+      const int row = mb * BM + q * 32 + lane;
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + buf * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(taddr + c, r);
+        tmem_ld_wait();
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        if (nb * BN + c < ep.N) epilogue_chunk<EPI>(ep, row, nb * BN + c, v, lane);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty_bar[buf]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<C::TMEM_COLS>(tmem_base);
+  }
+}
+
+// ---------------------------------------------------------------- host side
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  });
+  return fn;
+}
+
+// 2D bf16 tensor map over a row-major [outer, inner] matrix with row stride ld (elements).
+static int make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, int64_t ld, uint32_t box_inner,
+                    uint32_t box_outer) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) {
+    set_last_error("cuTensorMapEncodeTiled unavailable");
+    return ESM_EDRIVER;
+  }
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_last_error("cuTensorMapEncodeTiled failed (%d): inner=%llu outer=%llu ld=%lld box=%u,%u", (int)r,
+                   (unsigned long long)inner, (unsigned long long)outer, (long long)ld, box_inner, box_outer);
+    return ESM_EDRIVER;
+  }
+  return 0;
+}
+
+static int g_num_sms = 0;
+static int num_sms() {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+template <int BN, bool A_MN, bool B_MN, int EPI>
+static int launch(const esm_gemm_args& a, cudaStream_t st) {
+  using C = Cfg<BN>;
+  CUtensorMap tA, tB;
+  int rc;
+  if (!A_MN)
+    rc = make_map(&tA, a.A, a.K, a.M, a.lda, BK, BM);
+  else
+    rc = make_map(&tA, a.A, a.M, a.K, a.lda, 64, BK);
+  if (rc) return rc;
+  if (!B_MN)
+    rc = make_map(&tB, a.B, a.K, a.N, a.ldb, BK, BN);
+  else
+    rc = make_map(&tB, a.B, a.N, a.K, a.ldb, 64, BK);
+  if (rc) return rc;
+
+  TileInfo ti;
+  ti.num_m = (a.M + BM - 1) / BM;
+  ti.num_n = (a.N + BN - 1) / BN;
+  ti.kb_total = (a.K + BK - 1) / BK;
+  int splits = 1;
+  const int tiles = ti.num_m * ti.num_n;
+  const int sms = num_sms();
+  if (EPI == ESM_EPI_F32_ACC) {
+    if (a.split_k > 0) {
+      splits = a.split_k;
+    } else if (tiles < sms) {
+      splits = (sms + tiles - 1) / tiles;  // ~one wave of work units
+      const int max_splits = ti.kb_total / 4 > 0 ? ti.kb_total / 4 : 1;  // keep >= 4 k-blocks per unit
+      if (splits > max_splits) splits = max_splits;
+    }
+  }
+  ti.kb_per_split = (ti.kb_total + splits - 1) / splits;
+  splits = (ti.kb_total + ti.kb_per_split - 1) / ti.kb_per_split;
+  ti.splits = splits;
+
+  EpiParams ep{a.M, a.N, a.C, a.ldc, a.bias, a.aux_in, a.ld_aux_in, a.aux_out, a.ld_aux_out, a.col_sum};
+  auto kern = gemm_tc_kernel<BN, A_MN, B_MN, EPI>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    attr_set = true;
+  }
+  const int total = tiles * splits;
+  const int grid = total < sms ? total : sms;
+  kern<<<grid, kThreads, C::SMEM, st>>>(tA, tB, ti, ep);
+  ESM_LAUNCH_RET();
+}
+
+static int pick_bn_kmajor(int N) {
+  // largest tile with <= ~6% column waste; all multiples of 32
+  static const int cands[] = {256, 224, 192, 160, 128, 96, 64};
+  int best = 64;
+  double best_cost = 1e30;
+  for (int bn : cands) {
+    const int tiles = (N + bn - 1) / bn;
+    const double waste = double(tiles * bn - N) / N;
+    const double cost = tiles * (1.0 + 0.15 * (256.0 / bn)) * (1.0 + waste);  // favour wide tiles
+    if (cost < best_cost) {
+      best_cost = cost;
+      best = bn;
+    }
+  }
+  return best;
+}
+
+template <bool A_MN, bool B_MN, int EPI>
+static int dispatch_bn(const esm_gemm_args& a, int bn, cudaStream_t st) {
+  switch (bn) {
+    case 256: return launch<256, A_MN, B_MN, EPI>(a, st);
+    case 128: return launch<128, A_MN, B_MN, EPI>(a, st);
+    case 64: return launch<64, A_MN, B_MN, EPI>(a, st);
+    default: break;
+  }
+  if constexpr (!B_MN) {
+    switch (bn) {
+      case 224: return launch<224, A_MN, B_MN, EPI>(a, st);
+      case 192: return launch<192, A_MN, B_MN, EPI>(a, st);
+      case 160: return launch<160, A_MN, B_MN, EPI>(a, st);
+      case 96: return launch<96, A_MN, B_MN, EPI>(a, st);
+      default: break;
+    }
+  }
+  set_last_error("unsupported BN %d", bn);
+  return ESM_ENOTSUP;
+}
+
+int gemm_bf16(const esm_gemm_args& a, cudaStream_t st) {
+  const bool amn = a.a_mn_major != 0, bmn = a.b_mn_major != 0;
+  // TMA constraints: 16-byte aligned bases and row strides
+  ESM_CHECK_ARG(((uintptr_t)a.A & 15) == 0 && ((uintptr_t)a.B & 15) == 0, "gemm: A/B must be 16B aligned");
+  ESM_CHECK_ARG((a.lda * 2) % 16 == 0 && (a.ldb * 2) % 16 == 0, "gemm: lda/ldb must be multiples of 8");
+  if (a.epilogue == ESM_EPI_F32_ACC) {
+    ESM_CHECK_ARG(amn && bmn, "gemm: F32_ACC (wgrad) expects A and B MN-major");
+    ESM_CHECK_ARG(a.ldc % 4 == 0 && ((uintptr_t)a.C & 15) == 0, "gemm: fp32 C must be 16B aligned");
+    const int bn = a.N > 128 ? 256 : 128;
+    return dispatch_bn<true, true, ESM_EPI_F32_ACC>(a, bn, st);
+  }
+  ESM_CHECK_ARG(!amn, "gemm: activation-output GEMMs expect K-major A");
+  ESM_CHECK_ARG(a.ldc % 8 == 0 && ((uintptr_t)a.C & 15) == 0, "gemm: C must be 16B aligned, ldc %% 8 == 0");
+  if (!bmn) {
+    const int bn = pick_bn_kmajor(a.N);
+    switch (a.epilogue) {
+      case ESM_EPI_STORE: return dispatch_bn<false, false, ESM_EPI_STORE>(a, bn, st);
+      case ESM_EPI_GELU: return dispatch_bn<false, false, ESM_EPI_GELU>(a, bn, st);
+      case ESM_EPI_RESID: return dispatch_bn<false, false, ESM_EPI_RESID>(a, bn, st);
+      default: break;
+    }
+  } else {
+    const int bn = a.N > 128 ? 256 : 128;
+    switch (a.epilogue) {
+      case ESM_EPI_STORE: return dispatch_bn<false, true, ESM_EPI_STORE>(a, bn, st);
+      case ESM_EPI_DGELU: return dispatch_bn<false, true, ESM_EPI_DGELU>(a, bn, st);
+      default: break;
+    }
+  }
+  set_last_error("gemm: unsupported epilogue %d for this operand layout", a.epilogue);
+  return ESM_ENOTSUP;
+}
+
+}  // namespace sm100
+
+// ============================================================================
+// fp32 SIMT path (parity mode)
+// ============================================================================
+namespace simt {
+constexpr int TM = 64, TN = 64, TK = 16;
+
+template <int EPI>
+__device__ __forceinline__ void apply_epi(const EpiParams& p, int row, int col, float v) {
+  if (row >= p.M || col >= p.N) return;
+  if constexpr (EPI == ESM_EPI_F32_ACC) {
+    atomicAdd(reinterpret_cast<float*>(p.C) + (int64_t)row * p.ldc + col, v);
+    return;
+  } else {
+    if (p.bias && EPI != ESM_EPI_DGELU) v += p.bias[col];
+    if constexpr (EPI == ESM_EPI_RESID)
+      v += reinterpret_cast<const float*>(p.aux_in)[(int64_t)row * p.ld_aux_in + col];
+    if constexpr (EPI == ESM_EPI_DGELU) {
+      v *= gelu_grad_f(reinterpret_cast<const float*>(p.aux_in)[(int64_t)row * p.ld_aux_in + col]);
+      if (p.col_sum) atomicAdd(p.col_sum + col, v);
+    }
+    if constexpr (EPI == ESM_EPI_GELU) {
+      reinterpret_cast<float*>(p.aux_out)[(int64_t)row * p.ld_aux_out + col] = v;
+      v = gelu_f(v);
+    }
+    reinterpret_cast<float*>(p.C)[(int64_t)row * p.ldc + col] = v;
+  }
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(256) gemm_f32_kernel(const float* __restrict__ A, int64_t lda, int amn,
+                                                       const float* __restrict__ B, int64_t ldb, int bmn, int K,
+                                                       int kchunk, EpiParams ep) {
+  __shared__ float As[TK][TM + 4];
+  __shared__ float Bs[TK][TN + 4];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int m0 = blockIdx.y * TM, n0 = blockIdx.x * TN;
+  const int k_begin = blockIdx.z * kchunk;
+  const int k_end = min(K, k_begin + kchunk);
+  float acc[4][4] = {};
+  for (int k0 = k_begin; k0 < k_end; k0 += TK) {
+    for (int i = threadIdx.x; i < TK * TM; i += 256) {
+      int kk, mm;
+      if (amn) { kk = i / TM; mm = i % TM; } else { mm = i / TK; kk = i % TK; }
+      const int gm = m0 + mm, gk = k0 + kk;
+      float a = 0.f;
+      if (gm < ep.M && gk < k_end) a = amn ? A[(int64_t)gk * lda + gm] : A[(int64_t)gm * lda + gk];
+      As[kk][mm] = a;
+    }
+    for (int i = threadIdx.x; i < TK * TN; i += 256) {
+      int kk, nn;
+      if (bmn) { kk = i / TN; nn = i % TN; } else { nn = i / TK; kk = i % TK; }
+      const int gn = n0 + nn, gk = k0 + kk;
+      float b = 0.f;
+      if (gn < ep.N && gk < k_end) b = bmn ? B[(int64_t)gk * ldb + gn] : B[(int64_t)gn * ldb + gk];
+      Bs[kk][nn] = b;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < TK; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) apply_epi<EPI>(ep, m0 + ty * 4 + i, n0 + tx * 4 + j, acc[i][j]);
+}
+
+int gemm_f32(const esm_gemm_args& a, cudaStream_t st) {
+  EpiParams ep{a.M, a.N, a.C, a.ldc, a.bias, a.aux_in, a.ld_aux_in, a.aux_out, a.ld_aux_out, a.col_sum};
+  int splits = 1;
+  if (a.epilogue == ESM_EPI_F32_ACC) splits = a.split_k > 0 ? a.split_k : (a.K >= 4096 ? 8 : 1);
+  int kchunk = (a.K + splits - 1) / splits;
+  kchunk = (kchunk + TK - 1) / TK * TK;
+  splits = (a.K + kchunk - 1) / kchunk;
+  if (splits < 1) splits = 1;
+  dim3 grid((a.N + TN - 1) / TN, (a.M + TM - 1) / TM, splits);
+  const float* A = reinterpret_cast<const float*>(a.A);
+  const float* B = reinterpret_cast<const float*>(a.B);
+  switch (a.epilogue) {
+    case ESM_EPI_STORE: gemm_f32_kernel<ESM_EPI_STORE><<<grid, 256, 0, st>>>(A, a.lda, a.a_mn_major, B, a.ldb, a.b_mn_major, a.K, kchunk, ep); break;
+    case ESM_EPI_GELU: gemm_f32_kernel<ESM_EPI_GELU><<<grid, 256, 0, st>>>(A, a.lda, a.a_mn_major, B, a.ldb, a.b_mn_major, a.K, kchunk, ep); break;
+    case ESM_EPI_RESID: gemm_f32_kernel<ESM_EPI_RESID><<<grid, 256, 0, st>>>(A, a.lda, a.a_mn_major, B, a.ldb, a.b_mn_major, a.K, kchunk, ep); break;
+    case ESM_EPI_DGELU: gemm_f32_kernel<ESM_EPI_DGELU><<<grid, 256, 0, st>>>(A, a.lda, a.a_mn_major, B, a.ldb, a.b_mn_major, a.K, kchunk, ep); break;
+    case ESM_EPI_F32_ACC: gemm_f32_kernel<ESM_EPI_F32_ACC><<<grid, 256, 0, st>>>(A, a.lda, a.a_mn_major, B, a.ldb, a.b_mn_major, a.K, kchunk, ep); break;
+    default: set_last_error("gemm_f32: bad epilogue %d", a.epilogue); return ESM_EINVAL;
+  }
+  ESM_LAUNCH_RET();
+}
+}  // namespace simt
+
+}  // namespace esm
+
+extern "C" int esm_gemm(const esm_gemm_args* args, esm_stream_t stream) {
+  ESM_CHECK_ARG(args != nullptr, "esm_gemm: null args");
+  const esm_gemm_args& a = *args;
+  ESM_CHECK_ARG(a.M > 0 && a.N > 0 && a.K > 0, "esm_gemm: bad shape %d %d %d", a.M, a.N, a.K);
+  ESM_CHECK_ARG(a.epilogue >= 0 && a.epilogue <= ESM_EPI_F32_ACC, "esm_gemm: bad epilogue");
+  ESM_CHECK_ARG(a.epilogue != ESM_EPI_RESID || a.aux_in, "esm_gemm: RESID needs aux_in");
+  ESM_CHECK_ARG(a.epilogue != ESM_EPI_DGELU || a.aux_in, "esm_gemm: DGELU needs aux_in");
+  ESM_CHECK_ARG(a.epilogue != ESM_EPI_GELU || a.aux_out, "esm_gemm: GELU needs aux_out");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (a.dtype == ESM_BF16) return esm::sm100::gemm_bf16(a, st);
+  if (a.dtype == ESM_F32) return esm::simt::gemm_f32(a, st);
+  esm::set_last_error("esm_gemm: bad dtype %d", a.dtype);
+  return ESM_EINVAL;
+}

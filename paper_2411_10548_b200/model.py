@@ -1,0 +1,500 @@
+"""B200-native ESM-2 masked-LM: parameters, activation workspace and the train step.
+
+PyTorch is used only for device memory, streams and (optionally) torch.distributed;
+every FLOP of the step runs in the hand-written sm_100a kernels of
+``libesm2b200.so`` through the C ABI declared in ``include/esm2_b200.h``.
+
+Semantics follow Hugging Face ``EsmForMaskedLM`` (transformers 5.5.0,
+``models/esm/modeling_esm.py``; "HF:" below):
+
+  embeddings + token_dropout + pad mask       HF:189-236     esm_embed_fwd / esm_embed_bwd
+  pre-LN (attention.LayerNorm / LayerNorm)    HF:384,394,479 esm_layernorm_fwd / _bwd
+  q,k,v projections, q*dh^-0.5, RoPE          HF:318-344     esm_gemm(STORE) + esm_qkv_rope_fwd
+  softmax(QKᵀ + key mask)·V, scaling=1        HF:257-282     esm_attn_fwd / esm_attn_bwd
+  out-proj + residual                         HF:365-375     esm_gemm(RESID)
+  FC1 + erf-GELU, FC2 + residual              HF:406-427     esm_gemm(GELU), esm_gemm(RESID)
+  emb_layer_norm_after                        HF:511-512     esm_layernorm_fwd
+  LM head dense+GELU+LN, tied decoder + bias  HF:808-815     esm_gemm(GELU) + LN + esm_lmhead_xent
+  masked CE (ignore -100, mean)               HF:777-784     esm_lmhead_xent
+  AdamW                                       torch.optim.AdamW semantics      esm_adamw
+
+Parameter memory layout (HBM): one flat fp32 master buffer (+ bf16 shadow for GEMM
+operands, + fp32 grad, Adam m, v), every parameter group 256-element aligned; groups are
+ordered in *backward completion order* (LM head first, layers L-1..0, word embeddings
+last) so that data-parallel gradient buckets are contiguous slices that become ready
+one after another during backward.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import EPI_DGELU, EPI_F32_ACC, EPI_GELU, EPI_RESID, EPI_STORE, ESM_BF16, ESM_F32
+from .config import EsmConfig
+
+ALIGN = 256  # elements; also the AdamW weight-decay chunk size
+
+
+def _no_decay(name: str) -> bool:
+    return name.endswith("bias") or "LayerNorm" in name or "layer_norm" in name
+
+
+def param_groups(cfg: EsmConfig):
+    """[(group_key, [(hf_name, shape), ...])] in backward-completion order."""
+    H, F, V, L = cfg.hidden_size, cfg.intermediate_size, cfg.vocab_size, cfg.num_hidden_layers
+    g = [
+        ("lm_head.bias", [("lm_head.bias", (V,))]),
+        ("lm_head.layer_norm.weight", [("lm_head.layer_norm.weight", (H,))]),
+        ("lm_head.layer_norm.bias", [("lm_head.layer_norm.bias", (H,))]),
+        ("lm_head.dense.weight", [("lm_head.dense.weight", (H, H))]),
+        ("lm_head.dense.bias", [("lm_head.dense.bias", (H,))]),
+        ("esm.encoder.emb_layer_norm_after.weight", [("esm.encoder.emb_layer_norm_after.weight", (H,))]),
+        ("esm.encoder.emb_layer_norm_after.bias", [("esm.encoder.emb_layer_norm_after.bias", (H,))]),
+    ]
+    for i in reversed(range(L)):
+        p = f"esm.encoder.layer.{i}."
+        for n, shp in [("output.dense.weight", (H, F)), ("output.dense.bias", (H,)),
+                       ("intermediate.dense.weight", (F, H)), ("intermediate.dense.bias", (F,)),
+                       ("LayerNorm.weight", (H,)), ("LayerNorm.bias", (H,)),
+                       ("attention.output.dense.weight", (H, H)), ("attention.output.dense.bias", (H,))]:
+            g.append((p + n, [(p + n, shp)]))
+        g.append((p + "attention.self.qkv.weight",
+                  [(p + f"attention.self.{n}.weight", (H, H)) for n in ("query", "key", "value")]))
+        g.append((p + "attention.self.qkv.bias",
+                  [(p + f"attention.self.{n}.bias", (H,)) for n in ("query", "key", "value")]))
+        g.append((p + "attention.LayerNorm.weight", [(p + "attention.LayerNorm.weight", (H,))]))
+        g.append((p + "attention.LayerNorm.bias", [(p + "attention.LayerNorm.bias", (H,))]))
+    g.append(("esm.embeddings.word_embeddings.weight", [("esm.embeddings.word_embeddings.weight", (V, H))]))
+    return g
+
+
+def init_params(cfg: EsmConfig, seed: int) -> dict:
+    """HF init (normal(0, initializer_range) weights, zero biases, LN (1,0), zero pad row), drawn with
+    numpy default_rng(seed) in HF state-dict order -- the same draws as the CPU oracle uses."""
+    H, F, V, L = cfg.hidden_size, cfg.intermediate_size, cfg.vocab_size, cfg.num_hidden_layers
+    shapes = {"esm.embeddings.word_embeddings.weight": (V, H)}
+    for i in range(L):
+        p = f"esm.encoder.layer.{i}."
+        for n in ("query", "key", "value"):
+            shapes[p + f"attention.self.{n}.weight"] = (H, H)
+            shapes[p + f"attention.self.{n}.bias"] = (H,)
+        shapes.update({p + "attention.output.dense.weight": (H, H), p + "attention.output.dense.bias": (H,),
+                       p + "attention.LayerNorm.weight": (H,), p + "attention.LayerNorm.bias": (H,),
+                       p + "intermediate.dense.weight": (F, H), p + "intermediate.dense.bias": (F,),
+                       p + "output.dense.weight": (H, F), p + "output.dense.bias": (H,),
+                       p + "LayerNorm.weight": (H,), p + "LayerNorm.bias": (H,)})
+    shapes.update({"esm.encoder.emb_layer_norm_after.weight": (H,), "esm.encoder.emb_layer_norm_after.bias": (H,),
+                   "lm_head.dense.weight": (H, H), "lm_head.dense.bias": (H,),
+                   "lm_head.layer_norm.weight": (H,), "lm_head.layer_norm.bias": (H,), "lm_head.bias": (V,)})
+    rng = np.random.default_rng(seed)
+    out = {}
+    for name, shape in shapes.items():
+        if name.endswith("LayerNorm.weight") or name.endswith("layer_norm.weight") or \
+                name.endswith("emb_layer_norm_after.weight"):
+            out[name] = np.ones(shape, np.float32)
+        elif len(shape) == 2:
+            out[name] = (rng.standard_normal(shape, dtype=np.float32) * np.float32(cfg.initializer_range))
+        else:
+            out[name] = np.zeros(shape, np.float32)
+    out["esm.embeddings.word_embeddings.weight"][cfg.pad_token_id] = 0.0
+    return out
+
+
+def rope_tables(seq_len: int, dim: int):
+    """HF RotaryEmbedding (HF:modeling_esm.py:91-111) in fp32: returns cos, sin [S, dim/2]
+    (the table is cat(freqs, freqs), so the first half suffices)."""
+    inv_freq = (1.0 / (np.float32(10000.0) ** (np.arange(0, dim, 2, dtype=np.int64).astype(np.float32)
+                                                 / np.float32(dim)))).astype(np.float32)
+    t = np.arange(seq_len, dtype=np.float32)
+    freqs = np.outer(t, inv_freq).astype(np.float32)
+    return np.cos(freqs).astype(np.float32), np.sin(freqs).astype(np.float32)
+
+
+@dataclass
+class _Slot:
+    offset: int
+    numel: int
+    shape: tuple
+    group: str
+
+
+class ParamStore:
+    """Flat fp32 master / bf16 shadow / fp32 grad / Adam moments, 256-element aligned groups."""
+
+    def __init__(self, cfg: EsmConfig, device, shadow: bool):
+        self.groups = param_groups(cfg)
+        self.slots: dict[str, _Slot] = {}
+        self.group_range: dict[str, tuple[int, int]] = {}
+        off = 0
+        decay = []
+        for key, members in self.groups:
+            start = off
+            for name, shape in members:
+                n = int(np.prod(shape))
+                self.slots[name] = _Slot(off, n, tuple(shape), key)
+                off += n
+            end = off
+            off = (off + ALIGN - 1) // ALIGN * ALIGN
+            self.group_range[key] = (start, end)
+            d = 0 if _no_decay(members[0][0]) else 1
+            decay += [d] * ((off - start) // ALIGN)
+        self.numel = off
+        self.device = device
+        self.p32 = torch.zeros(off, dtype=torch.float32, device=device)
+        self.g32 = torch.zeros(off, dtype=torch.float32, device=device)
+        self.m = torch.zeros(off, dtype=torch.float32, device=device)
+        self.v = torch.zeros(off, dtype=torch.float32, device=device)
+        self.p16 = torch.zeros(off, dtype=torch.bfloat16, device=device) if shadow else None
+        self.decay = torch.tensor(decay, dtype=torch.uint8, device=device)
+
+    def view(self, buf, name):
+        s = self.slots[name]
+        return buf[s.offset:s.offset + s.numel].view(s.shape)
+
+    def group_view(self, buf, key, shape):
+        a, b = self.group_range[key]
+        return buf[a:b].view(shape)
+
+
+class _Layer:
+    pass
+
+
+class Workspace:
+    """Activation / gradient buffers for one (B, S) shape; reused every step."""
+
+    def __init__(self, cfg: EsmConfig, B: int, S: int, act, device):
+        H, F, V, L, nh = cfg.hidden_size, cfg.intermediate_size, cfg.vocab_size, cfg.num_hidden_layers, \
+            cfg.num_attention_heads
+        dh = H // nh
+        T = B * S
+        self.B, self.S, self.T = B, S, T
+        e = lambda *shape, dt=act: torch.empty(*shape, dtype=dt, device=device)  # noqa: E731
+        f32, i32 = torch.float32, torch.int32
+        self.ids = torch.zeros(B, S, dtype=i32, device=device)        # raw (unmasked) tokens
+        self.input_ids = torch.zeros(B, S, dtype=i32, device=device)  # after MLM masking
+        self.labels = torch.full((B, S), -100, dtype=i32, device=device)
+        self.am = torch.ones(B, S, dtype=i32, device=device)
+        self.n_labels = torch.zeros(1, dtype=i32, device=device)
+        self.inv_denom = torch.zeros(1, dtype=f32, device=device)
+        self.loss_sum = torch.zeros(1, dtype=f32, device=device)
+        self.row_scale = e(B, dt=f32)
+        self.x = [e(T, H) for _ in range(L + 1)]  # residual stream: input of layer l; x[L] = encoder output
+        self.layers = []
+        for _ in range(L):
+            ly = _Layer()
+            ly.ln1_m, ly.ln1_r = e(T, dt=f32), e(T, dt=f32)
+            ly.h1 = e(T, H)
+            ly.q, ly.k, ly.v = e(B, nh, S, dh), e(B, nh, S, dh), e(B, nh, S, dh)
+            ly.o = e(T, H)
+            ly.lse = e(B, nh, S, dt=f32)
+            ly.x1 = e(T, H)
+            ly.ln2_m, ly.ln2_r = e(T, dt=f32), e(T, dt=f32)
+            ly.h2 = e(T, H)
+            ly.z, ly.a = e(T, F), e(T, F)
+            self.layers.append(ly)
+        self.qkv = e(T, 3 * H)
+        self.lnf_m, self.lnf_r = e(T, dt=f32), e(T, dt=f32)
+        self.xf = e(T, H)
+        self.y, self.g = e(T, H), e(T, H)
+        self.lnh_m, self.lnh_r = e(T, dt=f32), e(T, dt=f32)
+        self.n = e(T, H)
+        # backward scratch
+        self.dn = e(T, H)
+        self.dlogits = e(T, V, dt=f32)
+        self.dy = e(T, H)
+        self.dx = e(T, H)
+        self.dx_alt = e(T, H)
+        self.dh = e(T, H)
+        self.dz = e(T, F)
+        self.dx1 = e(T, H)
+        self.do = e(T, H)
+        self.dq = e(B, nh, S, dh, dt=f32)
+        self.dk, self.dv = e(B, nh, S, dh), e(B, nh, S, dh)
+        self.dqkv = e(T, 3 * H)
+        self.delta = e(B, nh, S, dt=f32)
+        cos, sin = rope_tables(S, dh)
+        self.cos = torch.from_numpy(cos).to(device)
+        self.sin = torch.from_numpy(sin).to(device)
+
+
+class EsmForMaskedLM:
+    """B200 ESM-2 MLM with a fused train step.
+
+    dtype="bf16": bf16 activations / GEMM operands, fp32 accumulation, fp32 master weights,
+                  fp32 gradients (production path: tcgen05 GEMMs, mma.sync flash attention).
+    dtype="fp32": fp32 everywhere (SIMT kernels) -- the parity mode checked against the oracle.
+    """
+
+    def __init__(self, config: EsmConfig, dtype: str = "bf16", device=None, seed: int = 1,
+                 lr: float = 4e-4, betas=(0.9, 0.98), eps: float = 1e-8, weight_decay: float = 0.01,
+                 params: dict | None = None):
+        _lib.load()
+        self.config = config.validate()
+        if dtype not in ("bf16", "fp32"):
+            raise ValueError("dtype must be 'bf16' or 'fp32'")
+        self.dtype = dtype
+        self.kdt = ESM_BF16 if dtype == "bf16" else ESM_F32
+        self.act = torch.bfloat16 if dtype == "bf16" else torch.float32
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        if self.device.type != "cuda":
+            raise _lib.EsmKernelError("EsmForMaskedLM runs only on a CUDA (sm_100a) device")
+        self.store = ParamStore(self.config, self.device, shadow=(dtype == "bf16"))
+        self.load_state_dict(params if params is not None else init_params(self.config, seed))
+        self.lr, self.betas, self.eps, self.weight_decay = lr, tuple(betas), eps, weight_decay
+        self.hyper = torch.zeros(8, dtype=torch.float32, device=self.device)
+        self.step_count = 0
+        self.grad_scale = 1.0
+        self.ws: Workspace | None = None
+        self.comm = None  # set by ddp.DataParallel
+
+    # ------------------------------------------------------------------ parameters
+    def load_state_dict(self, sd: dict):
+        for name, slot in self.store.slots.items():
+            if name not in sd:
+                raise KeyError(f"missing parameter {name}")
+            t = torch.as_tensor(np.asarray(sd[name], dtype=np.float32)).reshape(slot.shape)
+            self.store.view(self.store.p32, name).copy_(t.to(self.device))
+        self.refresh_shadow()
+
+    def refresh_shadow(self):
+        if self.store.p16 is not None:
+            _lib.call("esm_cast_f32_bf16", self.store.p32.data_ptr(), self.store.p16.data_ptr(), self.store.numel,
+                      self._stream())
+
+    def state_dict(self) -> dict:
+        return {n: self.store.view(self.store.p32, n).detach().cpu().clone() for n in self.store.slots}
+
+    def grads(self) -> dict:
+        return {n: self.store.view(self.store.g32, n) for n in self.store.slots}
+
+    def num_parameters(self) -> int:
+        return sum(s.numel for s in self.store.slots.values())
+
+    def _w(self, key, shape):
+        """GEMM operand view of a weight group (bf16 shadow or fp32 master)."""
+        buf = self.store.p16 if self.store.p16 is not None else self.store.p32
+        return self.store.group_view(buf, key, shape)
+
+    def _p32(self, key, shape=None):
+        a, b = self.store.group_range[key]
+        return self.store.p32[a:b]
+
+    def _g32(self, key):
+        a, b = self.store.group_range[key]
+        return self.store.g32[a:b]
+
+    # ------------------------------------------------------------------ plumbing
+    def _stream(self) -> int:
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def workspace(self, B: int, S: int) -> Workspace:
+        if self.ws is None or self.ws.B != B or self.ws.S != S:
+            self.ws = None
+            torch.cuda.empty_cache()
+            self.ws = Workspace(self.config, B, S, self.act, self.device)
+        return self.ws
+
+    def _gemm(self, M, N, K, A, lda, amn, B, ldb, bmn, C, ldc, epi, bias=None, aux_in=None, ld_aux_in=0,
+              aux_out=None, ld_aux_out=0, col_sum=None):
+        _lib.gemm_call(self._stream(), dtype=self.kdt, M=M, N=N, K=K, A=A.data_ptr(), lda=lda, a_mn_major=amn,
+                       B=B.data_ptr(), ldb=ldb, b_mn_major=bmn, C=C.data_ptr(), ldc=ldc, epilogue=epi,
+                       bias=bias.data_ptr() if bias is not None else None,
+                       aux_in=aux_in.data_ptr() if aux_in is not None else None, ld_aux_in=ld_aux_in,
+                       aux_out=aux_out.data_ptr() if aux_out is not None else None, ld_aux_out=ld_aux_out,
+                       col_sum=col_sum.data_ptr() if col_sum is not None else None, split_k=0)
+
+    def linear_fwd(self, x, wkey, out_f, in_f, bias_key, C, epi=EPI_STORE, aux_in=None, aux_out=None):
+        T = x.shape[0]
+        W = self._w(wkey, (out_f, in_f))
+        self._gemm(T, out_f, in_f, x, in_f, 0, W, in_f, 0, C, out_f, epi,
+                   bias=self._p32(bias_key) if bias_key else None, aux_in=aux_in, ld_aux_in=out_f,
+                   aux_out=aux_out, ld_aux_out=out_f)
+
+    def linear_dgrad(self, dy, wkey, out_f, in_f, dX, epi=EPI_STORE, aux_in=None, col_sum=None):
+        T = dy.shape[0]
+        W = self._w(wkey, (out_f, in_f))
+        self._gemm(T, in_f, out_f, dy, out_f, 0, W, in_f, 1, dX, in_f, epi, aux_in=aux_in, ld_aux_in=in_f,
+                   col_sum=col_sum)
+
+    def linear_wgrad(self, dy, x, wkey, out_f, in_f):
+        T = dy.shape[0]
+        self._gemm(out_f, in_f, T, dy, out_f, 1, x, in_f, 1, self._g32(wkey), in_f, EPI_F32_ACC)
+
+    # ------------------------------------------------------------------ data path
+    def mlm_mask(self, ids: torch.Tensor, seed: int, stream_id: int, ws: Workspace | None = None):
+        """Device MLM masking (15% / 80-10-10) into the workspace; counts labelled tokens."""
+        ws = ws or self.workspace(*ids.shape)
+        if ids.data_ptr() != ws.ids.data_ptr():
+            ws.ids.copy_(ids, non_blocking=True)
+        ws.n_labels.zero_()
+        _lib.call("esm_mlm_mask", ws.ids.data_ptr(), ws.input_ids.data_ptr(), ws.labels.data_ptr(),
+                  ws.n_labels.data_ptr(), ws.ids.numel(), seed & 0xFFFFFFFFFFFFFFFF, stream_id & 0xFFFFFFFFFFFFFFFF,
+                  self._stream())
+        return ws.input_ids, ws.labels
+
+    def set_batch(self, input_ids, attention_mask=None, labels=None) -> Workspace:
+        """Stage an already-masked batch (device or host int tensors) into the workspace."""
+        B, S = input_ids.shape
+        ws = self.workspace(B, S)
+        ws.input_ids.copy_(input_ids, non_blocking=True)
+        if attention_mask is None:
+            ws.am.fill_(1)
+        else:
+            ws.am.copy_(attention_mask, non_blocking=True)
+        if labels is not None:
+            ws.labels.copy_(labels, non_blocking=True)
+            ws.n_labels.copy_((torch.as_tensor(labels) != -100).sum().reshape(1).to(torch.int32),
+                              non_blocking=True)
+        return ws
+
+    # ------------------------------------------------------------------ forward + backward
+    def forward_backward(self, ws: Workspace | None = None, loss_only: bool = False):
+        """Forward, masked-CE loss and full backward into ``store.g32`` (zeroed here).
+
+        Inputs are taken from the workspace (input_ids, am, labels, n_labels).  Returns the device
+        loss tensor (mean over labelled tokens, or over ``n_labels`` if it was all-reduced)."""
+        ws = ws or self.ws
+        cfg = self.config
+        H, F, V, L, nh = cfg.hidden_size, cfg.intermediate_size, cfg.vocab_size, cfg.num_hidden_layers, \
+            cfg.num_attention_heads
+        dh = H // nh
+        B, S, T = ws.B, ws.S, ws.T
+        st = self._stream()
+        kdt = self.kdt
+        P = self.store
+        qs = float(np.float32(dh ** -0.5))
+        eps = float(cfg.layer_norm_eps)
+        call = _lib.call
+        E_key = "esm.embeddings.word_embeddings.weight"
+        E = self._w(E_key, (V, H))
+
+        self.store.g32.zero_()
+        ws.loss_sum.zero_()
+        call("esm_inv_count", ws.n_labels.data_ptr(), ws.inv_denom.data_ptr(), st)
+        # ---------------- forward
+        call("esm_embed_fwd", kdt, ws.input_ids.data_ptr(), ws.am.data_ptr(), E.data_ptr(), ws.x[0].data_ptr(),
+             ws.row_scale.data_ptr(), B, S, H, int(cfg.token_dropout), cfg.mask_token_id, st)
+        for l in range(L):
+            p = f"esm.encoder.layer.{l}."
+            ly = ws.layers[l]
+            x = ws.x[l]
+            call("esm_layernorm_fwd", kdt, x.data_ptr(), self._p32(p + "attention.LayerNorm.weight").data_ptr(),
+                 self._p32(p + "attention.LayerNorm.bias").data_ptr(), ly.h1.data_ptr(), ly.ln1_m.data_ptr(),
+                 ly.ln1_r.data_ptr(), T, H, eps, st)
+            self.linear_fwd(ly.h1, p + "attention.self.qkv.weight", 3 * H, H, p + "attention.self.qkv.bias", ws.qkv)
+            call("esm_qkv_rope_fwd", kdt, ws.qkv.data_ptr(), ly.q.data_ptr(), ly.k.data_ptr(), ly.v.data_ptr(),
+                 ws.cos.data_ptr(), ws.sin.data_ptr(), B, S, nh, dh, qs, st)
+            call("esm_attn_fwd", kdt, ly.q.data_ptr(), ly.k.data_ptr(), ly.v.data_ptr(), ws.am.data_ptr(),
+                 ly.o.data_ptr(), ly.lse.data_ptr(), B, nh, S, dh, st)
+            self.linear_fwd(ly.o, p + "attention.output.dense.weight", H, H, p + "attention.output.dense.bias",
+                            ly.x1, epi=EPI_RESID, aux_in=x)
+            call("esm_layernorm_fwd", kdt, ly.x1.data_ptr(), self._p32(p + "LayerNorm.weight").data_ptr(),
+                 self._p32(p + "LayerNorm.bias").data_ptr(), ly.h2.data_ptr(), ly.ln2_m.data_ptr(),
+                 ly.ln2_r.data_ptr(), T, H, eps, st)
+            self.linear_fwd(ly.h2, p + "intermediate.dense.weight", F, H, p + "intermediate.dense.bias", ly.a,
+                            epi=EPI_GELU, aux_out=ly.z)
+            self.linear_fwd(ly.a, p + "output.dense.weight", H, F, p + "output.dense.bias", ws.x[l + 1],
+                            epi=EPI_RESID, aux_in=ly.x1)
+        call("esm_layernorm_fwd", kdt, ws.x[L].data_ptr(),
+             self._p32("esm.encoder.emb_layer_norm_after.weight").data_ptr(),
+             self._p32("esm.encoder.emb_layer_norm_after.bias").data_ptr(), ws.xf.data_ptr(), ws.lnf_m.data_ptr(),
+             ws.lnf_r.data_ptr(), T, H, eps, st)
+        self.linear_fwd(ws.xf, "lm_head.dense.weight", H, H, "lm_head.dense.bias", ws.g, epi=EPI_GELU, aux_out=ws.y)
+        call("esm_layernorm_fwd", kdt, ws.g.data_ptr(), self._p32("lm_head.layer_norm.weight").data_ptr(),
+             self._p32("lm_head.layer_norm.bias").data_ptr(), ws.n.data_ptr(), ws.lnh_m.data_ptr(),
+             ws.lnh_r.data_ptr(), T, H, eps, st)
+        # decoder (tied E) + masked CE + dlogits (fused)
+        call("esm_lmhead_xent", kdt, ws.n.data_ptr(), E.data_ptr(), self._p32("lm_head.bias").data_ptr(),
+             ws.labels.data_ptr(), ws.inv_denom.data_ptr(), ws.loss_sum.data_ptr(), ws.dlogits.data_ptr(),
+             ws.dn.data_ptr(), self._g32(E_key).data_ptr(), self._g32("lm_head.bias").data_ptr(), T, H, V, st)
+        if loss_only:
+            return ws.loss_sum
+        # ---------------- backward
+        if self.comm is not None:
+            self.comm.begin_backward()
+        # LM head: LN^T then GELU'(y) fused; col sums -> dense bias grad
+        call("esm_layernorm_bwd", kdt, ws.dn.data_ptr(), ws.g.data_ptr(),
+             self._p32("lm_head.layer_norm.weight").data_ptr(), ws.lnh_m.data_ptr(), ws.lnh_r.data_ptr(), None,
+             ws.y.data_ptr(), ws.dy.data_ptr(), self._g32("lm_head.layer_norm.weight").data_ptr(),
+             self._g32("lm_head.layer_norm.bias").data_ptr(), self._g32("lm_head.dense.bias").data_ptr(), T, H, st)
+        self.linear_dgrad(ws.dy, "lm_head.dense.weight", H, H, ws.dh)
+        self.linear_wgrad(ws.dy, ws.xf, "lm_head.dense.weight", H, H)
+        last_b2 = f"esm.encoder.layer.{L - 1}.output.dense.bias" if L > 0 else None
+        call("esm_layernorm_bwd", kdt, ws.dh.data_ptr(), ws.x[L].data_ptr(),
+             self._p32("esm.encoder.emb_layer_norm_after.weight").data_ptr(), ws.lnf_m.data_ptr(),
+             ws.lnf_r.data_ptr(), None, None, ws.dx.data_ptr(),
+             self._g32("esm.encoder.emb_layer_norm_after.weight").data_ptr(),
+             self._g32("esm.encoder.emb_layer_norm_after.bias").data_ptr(),
+             self._g32(last_b2).data_ptr() if last_b2 else None, T, H, st)
+        if self.comm is not None:
+            self.comm.ready("esm.encoder.emb_layer_norm_after.bias")
+        dx, dx_next = ws.dx, ws.dx_alt
+        for l in reversed(range(L)):
+            p = f"esm.encoder.layer.{l}."
+            ly = ws.layers[l]
+            # FFN
+            self.linear_dgrad(dx, p + "output.dense.weight", H, F, ws.dz, epi=EPI_DGELU, aux_in=ly.z,
+                              col_sum=self._g32(p + "intermediate.dense.bias"))
+            self.linear_wgrad(dx, ly.a, p + "output.dense.weight", H, F)
+            self.linear_dgrad(ws.dz, p + "intermediate.dense.weight", F, H, ws.dh)
+            self.linear_wgrad(ws.dz, ly.h2, p + "intermediate.dense.weight", F, H)
+            call("esm_layernorm_bwd", kdt, ws.dh.data_ptr(), ly.x1.data_ptr(),
+                 self._p32(p + "LayerNorm.weight").data_ptr(), ly.ln2_m.data_ptr(), ly.ln2_r.data_ptr(),
+                 dx.data_ptr(), None, ws.dx1.data_ptr(), self._g32(p + "LayerNorm.weight").data_ptr(),
+                 self._g32(p + "LayerNorm.bias").data_ptr(), self._g32(p + "attention.output.dense.bias").data_ptr(),
+                 T, H, st)
+            # attention
+            self.linear_dgrad(ws.dx1, p + "attention.output.dense.weight", H, H, ws.do)
+            self.linear_wgrad(ws.dx1, ly.o, p + "attention.output.dense.weight", H, H)
+            call("esm_attn_bwd", kdt, ly.q.data_ptr(), ly.k.data_ptr(), ly.v.data_ptr(), ly.o.data_ptr(),
+                 ws.do.data_ptr(), ly.lse.data_ptr(), ws.am.data_ptr(), ws.delta.data_ptr(), ws.dq.data_ptr(),
+                 ws.dk.data_ptr(), ws.dv.data_ptr(), B, nh, S, dh, st)
+            call("esm_qkv_rope_bwd", kdt, ws.dq.data_ptr(), ws.dk.data_ptr(), ws.dv.data_ptr(), ws.dqkv.data_ptr(),
+                 self._g32(p + "attention.self.qkv.bias").data_ptr(), ws.cos.data_ptr(), ws.sin.data_ptr(), B, S,
+                 nh, dh, qs, st)
+            self.linear_dgrad(ws.dqkv, p + "attention.self.qkv.weight", 3 * H, H, ws.dh)
+            self.linear_wgrad(ws.dqkv, ly.h1, p + "attention.self.qkv.weight", 3 * H, H)
+            prev_b2 = f"esm.encoder.layer.{l - 1}.output.dense.bias" if l > 0 else None
+            call("esm_layernorm_bwd", kdt, ws.dh.data_ptr(), ws.x[l].data_ptr(),
+                 self._p32(p + "attention.LayerNorm.weight").data_ptr(), ly.ln1_m.data_ptr(), ly.ln1_r.data_ptr(),
+                 ws.dx1.data_ptr(), None, dx_next.data_ptr(), self._g32(p + "attention.LayerNorm.weight").data_ptr(),
+                 self._g32(p + "attention.LayerNorm.bias").data_ptr(),
+                 self._g32(prev_b2).data_ptr() if prev_b2 else None, T, H, st)
+            dx, dx_next = dx_next, dx
+            if self.comm is not None:
+                self.comm.ready(p + "attention.LayerNorm.bias")
+        call("esm_embed_bwd", kdt, ws.input_ids.data_ptr(), ws.am.data_ptr(), ws.row_scale.data_ptr(),
+             dx.data_ptr(), self._g32(E_key).data_ptr(), B, S, H, V, cfg.mask_token_id, cfg.pad_token_id, st)
+        if self.comm is not None:
+            self.comm.ready(E_key)
+            self.comm.end_backward()
+        self._last_dx_embed = dx
+        return ws.loss_sum
+
+    # ------------------------------------------------------------------ optimizer
+    def set_hyper(self, lr=None, step=None):
+        lr = self.lr if lr is None else lr
+        step = self.step_count if step is None else step
+        h = torch.tensor([lr, self.betas[0], self.betas[1], self.eps, self.weight_decay, float(step),
+                          self.grad_scale, 0.0], dtype=torch.float32)
+        self.hyper.copy_(h, non_blocking=False)
+
+    def optimizer_step(self, lr=None):
+        self.step_count += 1
+        self.set_hyper(lr=lr, step=self.step_count)
+        P = self.store
+        _lib.call("esm_adamw", P.p32.data_ptr(), P.g32.data_ptr(), P.m.data_ptr(), P.v.data_ptr(),
+                  P.p16.data_ptr() if P.p16 is not None else None, P.decay.data_ptr(), P.numel,
+                  self.hyper.data_ptr(), self._stream())
+
+    def train_step(self, input_ids, attention_mask=None, labels=None, lr=None):
+        """One MLM train step on an already-masked batch; returns the device loss tensor."""
+        ws = self.set_batch(input_ids, attention_mask, labels)
+        loss = self.forward_backward(ws)
+        self.optimizer_step(lr=lr)
+        return loss

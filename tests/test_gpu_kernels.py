@@ -1,0 +1,257 @@
+"""Kernel-level parity on a B200: each C-ABI op against a plain fp32 PyTorch reference of the
+same op (bf16 kernels within bf16 tolerance; fp32 SIMT kernels at 1e-5)."""
+import ctypes
+import math
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from paper_2411_10548_b200 import _lib  # noqa: E402
+from paper_2411_10548_b200._lib import (EPI_DGELU, EPI_F32_ACC, EPI_GELU, EPI_RESID, EPI_STORE, ESM_BF16,  # noqa: E402
+                                        ESM_F32)
+
+DEV = "cuda"
+
+
+def st():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def gelu(x):
+    return 0.5 * x * (1.0 + torch.erf(x / math.sqrt(2.0)))
+
+
+def gelu_grad(x):
+    return 0.5 * (1.0 + torch.erf(x / math.sqrt(2.0))) + x * torch.exp(-0.5 * x * x) / math.sqrt(2 * math.pi)
+
+
+def rel(a, b):
+    a, b = a.float(), b.float()
+    return ((a - b).abs().max() / (b.abs().max() + 1e-12)).item()
+
+
+def run_gemm(dtype, M, N, K, A, lda, amn, B, ldb, bmn, C, ldc, epi, bias=None, aux_in=None, aux_out=None,
+             col_sum=None, split_k=0):
+    _lib.gemm_call(st(), dtype=dtype, M=M, N=N, K=K, A=A.data_ptr(), lda=lda, a_mn_major=amn, B=B.data_ptr(),
+                   ldb=ldb, b_mn_major=bmn, C=C.data_ptr(), ldc=ldc, epilogue=epi,
+                   bias=bias.data_ptr() if bias is not None else None,
+                   aux_in=aux_in.data_ptr() if aux_in is not None else None, ld_aux_in=ldc,
+                   aux_out=aux_out.data_ptr() if aux_out is not None else None, ld_aux_out=ldc,
+                   col_sum=col_sum.data_ptr() if col_sum is not None else None, split_k=split_k)
+
+
+FWD_SHAPES = [(256, 128, 64), (1000, 1440, 480), (300, 480, 1920), (128, 96, 64), (4096, 1920, 480),
+              (515, 64, 200), (2048, 1280, 1280), (333, 160, 96)]
+
+
+@pytest.mark.parametrize("M,N,K", FWD_SHAPES)
+@pytest.mark.parametrize("dt", ["bf16", "fp32"])
+def test_gemm_forward_epilogues(M, N, K, dt):
+    torch.manual_seed(0)
+    tdt = torch.bfloat16 if dt == "bf16" else torch.float32
+    kdt = ESM_BF16 if dt == "bf16" else ESM_F32
+    tol = 2e-2 if dt == "bf16" else 1e-5
+    X = torch.randn(M, K, device=DEV).to(tdt)
+    W = (torch.randn(N, K, device=DEV) * 0.05).to(tdt)
+    b = torch.randn(N, device=DEV)
+    R = torch.randn(M, N, device=DEV).to(tdt)
+    ref = X.float() @ W.float().t() + b
+    C = torch.empty(M, N, device=DEV, dtype=tdt)
+    run_gemm(kdt, M, N, K, X, K, 0, W, K, 0, C, N, EPI_STORE, bias=b)
+    torch.cuda.synchronize()
+    assert rel(C, ref) < tol
+    Z = torch.empty_like(C)
+    run_gemm(kdt, M, N, K, X, K, 0, W, K, 0, C, N, EPI_GELU, bias=b, aux_out=Z)
+    torch.cuda.synchronize()
+    assert rel(Z, ref) < tol and rel(C, gelu(ref)) < tol
+    run_gemm(kdt, M, N, K, X, K, 0, W, K, 0, C, N, EPI_RESID, bias=b, aux_in=R)
+    torch.cuda.synchronize()
+    assert rel(C, ref + R.float()) < tol
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 128, 64), (1000, 480, 1440), (300, 1920, 480), (515, 64, 200),
+                                   (2048, 1280, 5120)])
+@pytest.mark.parametrize("dt", ["bf16", "fp32"])
+def test_gemm_dgrad(M, N, K, dt):
+    """dX[M=T, N=in] = dY[T, K=out] · W[out, in]  (B operand N-major)."""
+    torch.manual_seed(1)
+    tdt = torch.bfloat16 if dt == "bf16" else torch.float32
+    kdt = ESM_BF16 if dt == "bf16" else ESM_F32
+    tol = 2e-2 if dt == "bf16" else 1e-5
+    dY = torch.randn(M, K, device=DEV).to(tdt)
+    W = (torch.randn(K, N, device=DEV) * 0.05).to(tdt)
+    Z = torch.randn(M, N, device=DEV).to(tdt)
+    ref = dY.float() @ W.float()
+    C = torch.empty(M, N, device=DEV, dtype=tdt)
+    run_gemm(kdt, M, N, K, dY, K, 0, W, N, 1, C, N, EPI_STORE)
+    torch.cuda.synchronize()
+    assert rel(C, ref) < tol
+    cs = torch.zeros(N, device=DEV)
+    run_gemm(kdt, M, N, K, dY, K, 0, W, N, 1, C, N, EPI_DGELU, aux_in=Z, col_sum=cs)
+    torch.cuda.synchronize()
+    want = ref * gelu_grad(Z.float())
+    assert rel(C, want) < tol
+    assert rel(cs, want.sum(0)) < (2e-2 if dt == "bf16" else 1e-4)
+
+
+@pytest.mark.parametrize("M,N,K", [(480, 1920, 4096), (1440, 480, 8192), (128, 128, 64), (96, 200, 1000),
+                                   (1280, 5120, 2048), (40, 64, 512)])
+@pytest.mark.parametrize("dt", ["bf16", "fp32"])
+def test_gemm_wgrad(M, N, K, dt):
+    """dW[M=out, N=in] += dY[T=K, out]ᵀ · X[T, in]  (both operands MN-major, fp32 accumulate, split-K)."""
+    torch.manual_seed(2)
+    tdt = torch.bfloat16 if dt == "bf16" else torch.float32
+    kdt = ESM_BF16 if dt == "bf16" else ESM_F32
+    dY = torch.randn(K, M, device=DEV).to(tdt)
+    X = torch.randn(K, N, device=DEV).to(tdt)
+    ref = dY.float().t() @ X.float()
+    C = torch.ones(M, N, device=DEV)
+    run_gemm(kdt, M, N, K, dY, M, 1, X, N, 1, C, N, EPI_F32_ACC)
+    torch.cuda.synchronize()
+    assert rel(C - 1.0, ref) < (1e-2 if dt == "bf16" else 1e-5)
+
+
+def test_gemm_rejects_bad_args():
+    X = torch.randn(64, 64, device=DEV).to(torch.bfloat16)
+    C = torch.empty(64, 64, device=DEV).to(torch.bfloat16)
+    with pytest.raises(_lib.EsmKernelError):
+        run_gemm(ESM_BF16, 64, 64, 64, X, 64, 0, X, 64, 0, C, 64, EPI_RESID)  # RESID without aux_in
+
+
+def torch_attention(q, k, v, am):
+    s = q.float() @ k.float().transpose(-1, -2)
+    s = s + torch.where(am[:, None, None, :] > 0, 0.0, float("-inf"))
+    p = torch.softmax(s, -1)
+    return p @ v.float()
+
+
+@pytest.mark.parametrize("dh", [16, 24, 32, 64])
+@pytest.mark.parametrize("S,lens", [(128, [128, 100]), (200, [200, 77]), (1024, [1024, 1000])])
+@pytest.mark.parametrize("dt", ["bf16", "fp32"])
+def test_attention_fwd_bwd(dh, S, lens, dt):
+    if dt == "fp32" and S > 256:
+        pytest.skip("fp32 SIMT reference kernels: small sizes only")
+    torch.manual_seed(3)
+    B, nh = len(lens), 3
+    tdt = torch.bfloat16 if dt == "bf16" else torch.float32
+    kdt = ESM_BF16 if dt == "bf16" else ESM_F32
+    am = torch.zeros(B, S, dtype=torch.int32, device=DEV)
+    for i, n in enumerate(lens):
+        am[i, :n] = 1
+    q = (torch.randn(B, nh, S, dh, device=DEV) * 0.5).to(tdt)
+    k = (torch.randn(B, nh, S, dh, device=DEV) * 0.5).to(tdt)
+    v = torch.randn(B, nh, S, dh, device=DEV).to(tdt)
+    o = torch.empty(B * S, nh * dh, device=DEV, dtype=tdt)
+    lse = torch.empty(B, nh, S, device=DEV)
+    _lib.call("esm_attn_fwd", kdt, q.data_ptr(), k.data_ptr(), v.data_ptr(), am.data_ptr(), o.data_ptr(),
+              lse.data_ptr(), B, nh, S, dh, st())
+    qr, kr, vr = (t.float().requires_grad_(True) for t in (q, k, v))
+    ref = torch_attention(qr, kr, vr, am)
+    ref_o = ref.permute(0, 2, 1, 3).reshape(B * S, nh * dh)
+    torch.cuda.synchronize()
+    tol = 2e-2 if dt == "bf16" else 1e-5
+    assert rel(o, ref_o) < tol
+    s = qr.detach() @ kr.detach().transpose(-1, -2)
+    s = s + torch.where(am[:, None, None, :] > 0, 0.0, float("-inf"))
+    assert rel(lse, torch.logsumexp(s, -1)) < (1e-3 if dt == "bf16" else 1e-6)
+    do = torch.randn(B * S, nh * dh, device=DEV).to(tdt)
+    ref_o.backward(do.float())
+    dq = torch.empty(B, nh, S, dh, device=DEV)
+    dk = torch.empty(B, nh, S, dh, device=DEV, dtype=tdt)
+    dv = torch.empty_like(dk)
+    delta = torch.empty(B, nh, S, device=DEV)
+    _lib.call("esm_attn_bwd", kdt, q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), do.data_ptr(),
+              lse.data_ptr(), am.data_ptr(), delta.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), B, nh,
+              S, dh, st())
+    torch.cuda.synchronize()
+    tol = 3e-2 if dt == "bf16" else 1e-4
+    assert rel(dv, vr.grad) < tol
+    assert rel(dk, kr.grad) < tol
+    assert rel(dq, qr.grad) < tol
+
+
+@pytest.mark.parametrize("H", [64, 320, 480, 1280, 2560])
+@pytest.mark.parametrize("dt", ["bf16", "fp32"])
+def test_layernorm(H, dt):
+    torch.manual_seed(4)
+    tdt = torch.bfloat16 if dt == "bf16" else torch.float32
+    kdt = ESM_BF16 if dt == "bf16" else ESM_F32
+    rows = 777
+    x = (torch.randn(rows, H, device=DEV) * 2 + 0.5).to(tdt)
+    g = torch.randn(H, device=DEV)
+    b = torch.randn(H, device=DEV)
+    y = torch.empty_like(x)
+    mean = torch.empty(rows, device=DEV)
+    rstd = torch.empty(rows, device=DEV)
+    _lib.call("esm_layernorm_fwd", kdt, x.data_ptr(), g.data_ptr(), b.data_ptr(), y.data_ptr(), mean.data_ptr(),
+              rstd.data_ptr(), rows, H, 1e-5, st())
+    xr = x.float().requires_grad_(True)
+    gr, br = g.clone().requires_grad_(True), b.clone().requires_grad_(True)
+    ref = torch.nn.functional.layer_norm(xr, (H,), gr, br, 1e-5)
+    torch.cuda.synchronize()
+    tol = 1e-2 if dt == "bf16" else 1e-5
+    assert rel(y, ref) < tol
+    dy = torch.randn(rows, H, device=DEV).to(tdt)
+    dres = torch.randn(rows, H, device=DEV).to(tdt)
+    ref.backward(dy.float())
+    dx = torch.empty_like(x)
+    dg = torch.zeros(H, device=DEV)
+    db = torch.zeros(H, device=DEV)
+    cs = torch.zeros(H, device=DEV)
+    _lib.call("esm_layernorm_bwd", kdt, dy.data_ptr(), x.data_ptr(), g.data_ptr(), mean.data_ptr(), rstd.data_ptr(),
+              dres.data_ptr(), None, dx.data_ptr(), dg.data_ptr(), db.data_ptr(), cs.data_ptr(), rows, H, st())
+    torch.cuda.synchronize()
+    want = xr.grad + dres.float()
+    assert rel(dx, want) < (2e-2 if dt == "bf16" else 1e-5)
+    assert rel(dg, gr.grad) < (1e-2 if dt == "bf16" else 1e-5)
+    assert rel(db, br.grad) < 1e-5
+    assert rel(cs, want.sum(0)) < (1e-2 if dt == "bf16" else 1e-4)
+
+
+def test_mlm_mask_bitexact_vs_oracle():
+    import esm2_oracle as O
+    ids, _ = O.synthetic_batch(8, 1000, seed=3)
+    ids[1, 500:] = O.PAD
+    for seed, stream in [(0, 0), (7, 12345), (2 ** 40 + 3, 2 ** 63 + 5)]:
+        want_inp, want_lab = O.mlm_mask(ids, seed, stream)
+        d_ids = torch.from_numpy(ids).to(DEV)
+        inp = torch.empty_like(d_ids)
+        lab = torch.empty_like(d_ids)
+        n = torch.zeros(1, dtype=torch.int32, device=DEV)
+        _lib.call("esm_mlm_mask", d_ids.data_ptr(), inp.data_ptr(), lab.data_ptr(), n.data_ptr(), ids.size, seed,
+                  stream, st())
+        torch.cuda.synchronize()
+        assert (inp.cpu().numpy() == want_inp).all()
+        assert (lab.cpu().numpy() == want_lab).all()
+        assert int(n.item()) == int((want_lab != -100).sum())
+
+
+def test_adamw_matches_oracle():
+    import esm2_oracle as O
+    rng = np.random.default_rng(0)
+    n = 4096
+    p = rng.standard_normal(n).astype(np.float32)
+    g = rng.standard_normal(n).astype(np.float32)
+    decay = np.array([1] * 8 + [0] * 8, dtype=np.uint8)
+    P = {"w": p[:2048].copy(), "b.bias": p[2048:].copy()}
+    G = {"w": g[:2048], "b.bias": g[2048:]}
+    M = {k: np.zeros_like(v) for k, v in P.items()}
+    Vv = {k: np.zeros_like(v) for k, v in P.items()}
+    dp = torch.from_numpy(p).to(DEV)
+    dg = torch.from_numpy(g).to(DEV)
+    dm = torch.zeros(n, device=DEV)
+    dv = torch.zeros(n, device=DEV)
+    p16 = torch.empty(n, device=DEV, dtype=torch.bfloat16)
+    dd = torch.from_numpy(decay).to(DEV)
+    for step in range(1, 4):
+        O.adamw_update(P, G, M, Vv, step, 1e-3, beta1=0.9, beta2=0.98, eps=1e-8, weight_decay=0.1)
+        hyper = torch.tensor([1e-3, 0.9, 0.98, 1e-8, 0.1, float(step), 1.0, 0.0], device=DEV)
+        _lib.call("esm_adamw", dp.data_ptr(), dg.data_ptr(), dm.data_ptr(), dv.data_ptr(), p16.data_ptr(),
+                  dd.data_ptr(), n, hyper.data_ptr(), st())
+    torch.cuda.synchronize()
+    want = np.concatenate([P["w"], P["b.bias"]])
+    np.testing.assert_allclose(dp.cpu().numpy(), want, rtol=1e-5, atol=1e-6)
+    np.testing.assert_allclose(p16.float().cpu().numpy(), want, rtol=1e-2, atol=1e-3)

@@ -1,0 +1,123 @@
+"""Model-level parity on a B200: the full ESM-2 MLM step through the C ABI vs the CPU oracle
+(which is pinned to Hugging Face EsmForMaskedLM by tests/test_oracle.py).
+
+fp32 mode: loss, per-layer activations and every parameter gradient within 1e-4 relative
+(north-star bar).  bf16 mode: loss within 1%, gradients within bf16 tolerance."""
+import glob
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import esm2_oracle as O
+from paper_2411_10548_b200 import EsmConfig
+from paper_2411_10548_b200.model import EsmForMaskedLM, init_params
+
+pytestmark = pytest.mark.gpu
+GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "hf_*.npz")))
+
+
+def _cfgs(H, L, nh, F):
+    return (EsmConfig(hidden_size=H, num_hidden_layers=L, num_attention_heads=nh, intermediate_size=F),
+            O.OracleConfig(hidden_size=H, num_hidden_layers=L, num_attention_heads=nh, intermediate_size=F))
+
+
+def _relerr(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.abs(a - b).max() / (np.abs(b).max() + 1e-30))
+
+
+def _run(cfg, params, inp, am, lab, dtype):
+    m = EsmForMaskedLM(cfg, dtype=dtype, device="cuda", params=params)
+    ws = m.set_batch(torch.from_numpy(inp).cuda(), torch.from_numpy(am).cuda(), torch.from_numpy(lab).cuda())
+    loss = float(m.forward_backward(ws).item())
+    return m, ws, loss
+
+
+@pytest.mark.parametrize("path", GOLDEN, ids=[os.path.basename(p) for p in GOLDEN])
+def test_fp32_matches_oracle_golden_inputs(path):
+    z = np.load(path)
+    H, L, nh, F, B, S = (int(v) for v in z["config"])
+    cfg, ocfg = _cfgs(H, L, nh, F)
+    params = {k[6:]: z[k] for k in z.files if k.startswith("param.")}
+    inp, am, lab = z["input_ids"], z["attention_mask"], z["labels"]
+    ref = O.forward_backward(ocfg, params, inp, am, lab, dtype=np.float64, keep_acts=True)
+    m, ws, loss = _run(cfg, params, inp, am, lab, "fp32")
+    assert abs(loss - ref.loss) / abs(ref.loss) < 1e-5
+    assert abs(loss - float(z["loss"])) / abs(float(z["loss"])) < 1e-5   # vs Hugging Face directly
+    keep = am.astype(bool)
+    for l in range(L):
+        a = ref.acts[l]
+        ly = ws.layers[l]
+        np.testing.assert_array_less(_relerr(ws.x[l].cpu().numpy().reshape(B, S, H)[keep], ref.hidden_states[l][keep]), 1e-4)
+        for name in ("h1", "o", "x1", "h2", "z", "a"):
+            got = getattr(ly, name).cpu().numpy().reshape(B, S, -1)[keep]
+            assert _relerr(got, a[name][keep]) < 1e-4, (l, name)
+        for name in ("q", "k", "v"):
+            got = getattr(ly, name).cpu().numpy().transpose(0, 2, 1, 3)[keep]
+            want = a[name].transpose(0, 2, 1, 3)[keep]
+            assert _relerr(got, want) < 1e-4, (l, name)
+    grads = m.grads()
+    for k, g in ref.grads.items():
+        err = _relerr(grads[k].cpu().numpy(), g)
+        assert err < 1e-4, (k, err)
+
+
+@pytest.mark.parametrize("H,L,nh,F,B,S,lens", [
+    (320, 2, 20, 1280, 2, 128, [128, 90]),   # ESM-2 8M geometry (dh 16)
+    (480, 1, 20, 1920, 2, 96, [96, 96]),     # ESM-2 35M geometry (dh 24)
+    (1280, 1, 20, 5120, 1, 64, [64]),        # ESM-2 650M geometry (dh 64)
+])
+def test_bf16_matches_oracle(H, L, nh, F, B, S, lens):
+    cfg, ocfg = _cfgs(H, L, nh, F)
+    params = init_params(cfg, seed=5)
+    rng = np.random.default_rng(0)
+    toks = [np.concatenate([[O.CLS], rng.integers(4, 24, n - 2), [O.EOS]]).astype(np.int32) for n in lens]
+    ids, am = O.pad_batch(toks, S)
+    inp, lab = O.mlm_mask(ids, seed=3, stream=1)
+    ref = O.forward_backward(ocfg, params, inp, am, lab, dtype=np.float64)
+    m32, _, loss32 = _run(cfg, params, inp, am, lab, "fp32")
+    assert abs(loss32 - ref.loss) / ref.loss < 1e-5
+    g32 = m32.grads()
+    for k, g in ref.grads.items():
+        assert _relerr(g32[k].cpu().numpy(), g) < 1e-4, k
+    del m32
+    m16, _, loss16 = _run(cfg, params, inp, am, lab, "bf16")
+    assert abs(loss16 - ref.loss) / ref.loss < 1e-2
+    g16 = m16.grads()
+    for k, g in ref.grads.items():
+        # bf16 activations/operands: compare the whole tensor by relative Frobenius error
+        gg = g16[k].cpu().numpy().astype(np.float64)
+        fro = np.linalg.norm(gg - g) / (np.linalg.norm(g) + 1e-30)
+        assert fro < 0.08, (k, fro)
+
+
+def test_device_masking_pipeline_matches_oracle():
+    cfg, ocfg = _cfgs(64, 1, 4, 256)
+    params = init_params(cfg, seed=1)
+    ids, am = O.synthetic_batch(4, 64, seed=9)
+    m = EsmForMaskedLM(cfg, dtype="fp32", device="cuda", params=params)
+    ws = m.workspace(4, 64)
+    inp, lab = m.mlm_mask(torch.from_numpy(ids).cuda(), seed=21, stream_id=4, ws=ws)
+    want_inp, want_lab = O.mlm_mask(ids, 21, 4)
+    assert (inp.cpu().numpy() == want_inp).all() and (lab.cpu().numpy() == want_lab).all()
+    loss = float(m.forward_backward(ws).item())
+    ref = O.forward_backward(ocfg, params, want_inp, am, want_lab, dtype=np.float64, want_grads=False)
+    assert abs(loss - ref.loss) / ref.loss < 1e-5
+
+
+def test_train_steps_fp32_match_oracle_trainer():
+    """Several AdamW steps: GPU fp32 vs oracle fp32 trainer stay within 1e-4 in loss."""
+    cfg, ocfg = _cfgs(64, 2, 4, 256)
+    params = init_params(cfg, seed=2)
+    tr = O.OracleTrainer(ocfg, params, lr=1e-3, beta1=0.9, beta2=0.98, eps=1e-8, weight_decay=0.01)
+    m = EsmForMaskedLM(cfg, dtype="fp32", device="cuda", params=params, lr=1e-3)
+    for step in range(5):
+        ids, am = O.synthetic_batch(4, 48, seed=100 + step)
+        inp, lab = O.mlm_mask(ids, seed=5, stream=step)
+        lo = tr.step(inp, am, lab)
+        lg = float(m.train_step(torch.from_numpy(inp).cuda(), torch.from_numpy(am).cuda(),
+                                torch.from_numpy(lab).cuda()).item())
+        assert abs(lg - lo) / lo < 1e-4, (step, lg, lo)
