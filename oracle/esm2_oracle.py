@@ -284,6 +284,11 @@ class StepResult:
     acts: dict = field(default_factory=dict)
 
 
+def _wgrad(dy, x):
+    """sum over (b, s) of dy[b,s,:]^T x[b,s,:]  (BLAS matmul)."""
+    return dy.reshape(-1, dy.shape[-1]).T @ x.reshape(-1, x.shape[-1])
+
+
 def _linear(x, w, b=None):
     y = x @ w.T
     return y if b is None else y + b
@@ -388,11 +393,11 @@ def forward_backward(cfg: OracleConfig, params: dict, input_ids: np.ndarray, att
     dlg *= (sel / denom)[:, None]
     dlg = dlg.reshape(B, S, -1)
     G["lm_head.bias"] += dlg.sum((0, 1))
-    G["esm.embeddings.word_embeddings.weight"] += np.einsum("bsv,bsh->vh", dlg, n)
+    G["esm.embeddings.word_embeddings.weight"] += _wgrad(dlg, n)
     dn = dlg @ E
     dg, G["lm_head.layer_norm.weight"], G["lm_head.layer_norm.bias"] = layer_norm_bwd(dn, P["lm_head.layer_norm.weight"], lnh)
     dy = dg * gelu_grad(y)
-    G["lm_head.dense.weight"] = np.einsum("bso,bsi->oi", dy, xf)
+    G["lm_head.dense.weight"] = _wgrad(dy, xf)
     G["lm_head.dense.bias"] = dy.sum((0, 1))
     dxf = dy @ P["lm_head.dense.weight"]
     dx, G["esm.encoder.emb_layer_norm_after.weight"], G["esm.encoder.emb_layer_norm_after.bias"] = \
@@ -402,17 +407,17 @@ def forward_backward(cfg: OracleConfig, params: dict, input_ids: np.ndarray, att
         p = f"esm.encoder.layer.{i}."
         c = caches[i]
         # FFN
-        G[p + "output.dense.weight"] = np.einsum("bso,bsi->oi", dx, c["a"])
+        G[p + "output.dense.weight"] = _wgrad(dx, c["a"])
         G[p + "output.dense.bias"] = dx.sum((0, 1))
         da = dx @ P[p + "output.dense.weight"]
         dz = da * gelu_grad(c["z"])
-        G[p + "intermediate.dense.weight"] = np.einsum("bso,bsi->oi", dz, c["h2"])
+        G[p + "intermediate.dense.weight"] = _wgrad(dz, c["h2"])
         G[p + "intermediate.dense.bias"] = dz.sum((0, 1))
         dh2 = dz @ P[p + "intermediate.dense.weight"]
         dx1, G[p + "LayerNorm.weight"], G[p + "LayerNorm.bias"] = layer_norm_bwd(dh2, P[p + "LayerNorm.weight"], c["ln2"])
         dx1 = dx1 + dx
         # attention output projection
-        G[p + "attention.output.dense.weight"] = np.einsum("bso,bsi->oi", dx1, c["o"])
+        G[p + "attention.output.dense.weight"] = _wgrad(dx1, c["o"])
         G[p + "attention.output.dense.bias"] = dx1.sum((0, 1))
         do = (dx1 @ P[p + "attention.output.dense.weight"]).reshape(B, S, nh, dh).transpose(0, 2, 1, 3)
         # attention core (recompute P, flash-style)
@@ -436,7 +441,7 @@ def forward_backward(cfg: OracleConfig, params: dict, input_ids: np.ndarray, att
         h1 = c["h1"]
         dh1 = np.zeros_like(h1)
         for nm, dt in (("query", dq0), ("key", dk0), ("value", dv)):
-            G[p + f"attention.self.{nm}.weight"] = np.einsum("bso,bsi->oi", dt, h1)
+            G[p + f"attention.self.{nm}.weight"] = _wgrad(dt, h1)
             G[p + f"attention.self.{nm}.bias"] = dt.sum((0, 1))
             dh1 += dt @ P[p + f"attention.self.{nm}.weight"]
         dx0, G[p + "attention.LayerNorm.weight"], G[p + "attention.LayerNorm.bias"] = \

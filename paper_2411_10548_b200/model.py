@@ -250,7 +250,13 @@ class EsmForMaskedLM:
         self.step_count = 0
         self.grad_scale = 1.0
         self.ws: Workspace | None = None
-        self.comm = None  # set by ddp.DataParallel
+        self.comm = None  # set by ddp.GradAllReducer
+        self.timer = None  # optional KernelTimer (bench.py per-kernel roofline)
+        self.launches = 0  # kernels launched by this model (C-ABI calls x kernels per call)
+        self.graph = None
+        self._hyper_ring = [torch.zeros(8, dtype=torch.float32).pin_memory() for _ in range(4)]
+        self._hyper_ev = [None] * 4
+        self._hyper_i = 0
 
     # ------------------------------------------------------------------ parameters
     def load_state_dict(self, sd: dict):
@@ -299,8 +305,31 @@ class EsmForMaskedLM:
             self.ws = Workspace(self.config, B, S, self.act, self.device)
         return self.ws
 
+    # kernels launched per C-ABI entry point (for the bench's gpu_launches count)
+    _KERNELS = {"esm_embed_fwd": 2, "esm_attn_bwd": 2, "esm_lmhead_xent": 2}
+
+    def _call(self, name, *args, flops=0.0, nbytes=0.0):
+        t = self.timer
+        if t is not None:
+            t.begin(name)
+        _lib.call(name, *args)
+        if t is not None:
+            t.end(flops, nbytes)
+        self.launches += self._KERNELS.get(name, 1)
+
     def _gemm(self, M, N, K, A, lda, amn, B, ldb, bmn, C, ldc, epi, bias=None, aux_in=None, ld_aux_in=0,
               aux_out=None, ld_aux_out=0, col_sum=None):
+        t = self.timer
+        if t is not None:
+            t.begin("gemm_" + ("wgrad" if epi == EPI_F32_ACC else "dgrad" if bmn else "fwd"))
+        self.launches += 1
+        self._gemm_raw(M, N, K, A, lda, amn, B, ldb, bmn, C, ldc, epi, bias, aux_in, ld_aux_in, aux_out, ld_aux_out,
+                       col_sum)
+        if t is not None:
+            t.end(2.0 * M * N * K, 0.0)
+
+    def _gemm_raw(self, M, N, K, A, lda, amn, B, ldb, bmn, C, ldc, epi, bias, aux_in, ld_aux_in, aux_out,
+                  ld_aux_out, col_sum):
         _lib.gemm_call(self._stream(), dtype=self.kdt, M=M, N=N, K=K, A=A.data_ptr(), lda=lda, a_mn_major=amn,
                        B=B.data_ptr(), ldb=ldb, b_mn_major=bmn, C=C.data_ptr(), ldc=ldc, epilogue=epi,
                        bias=bias.data_ptr() if bias is not None else None,
@@ -369,12 +398,14 @@ class EsmForMaskedLM:
         P = self.store
         qs = float(np.float32(dh ** -0.5))
         eps = float(cfg.layer_norm_eps)
-        call = _lib.call
+        call = self._call
         E_key = "esm.embeddings.word_embeddings.weight"
         E = self._w(E_key, (V, H))
 
         self.store.g32.zero_()
         ws.loss_sum.zero_()
+        if self.comm is not None:
+            self.comm.reduce_count(ws.n_labels)  # global masked-token count -> loss normaliser
         call("esm_inv_count", ws.n_labels.data_ptr(), ws.inv_denom.data_ptr(), st)
         # ---------------- forward
         call("esm_embed_fwd", kdt, ws.input_ids.data_ptr(), ws.am.data_ptr(), E.data_ptr(), ws.x[0].data_ptr(),
@@ -390,7 +421,7 @@ class EsmForMaskedLM:
             call("esm_qkv_rope_fwd", kdt, ws.qkv.data_ptr(), ly.q.data_ptr(), ly.k.data_ptr(), ly.v.data_ptr(),
                  ws.cos.data_ptr(), ws.sin.data_ptr(), B, S, nh, dh, qs, st)
             call("esm_attn_fwd", kdt, ly.q.data_ptr(), ly.k.data_ptr(), ly.v.data_ptr(), ws.am.data_ptr(),
-                 ly.o.data_ptr(), ly.lse.data_ptr(), B, nh, S, dh, st)
+                 ly.o.data_ptr(), ly.lse.data_ptr(), B, nh, S, dh, st, flops=4.0 * B * nh * S * S * dh)
             self.linear_fwd(ly.o, p + "attention.output.dense.weight", H, H, p + "attention.output.dense.bias",
                             ly.x1, epi=EPI_RESID, aux_in=x)
             call("esm_layernorm_fwd", kdt, ly.x1.data_ptr(), self._p32(p + "LayerNorm.weight").data_ptr(),
@@ -453,7 +484,7 @@ class EsmForMaskedLM:
             self.linear_wgrad(ws.dx1, ly.o, p + "attention.output.dense.weight", H, H)
             call("esm_attn_bwd", kdt, ly.q.data_ptr(), ly.k.data_ptr(), ly.v.data_ptr(), ly.o.data_ptr(),
                  ws.do.data_ptr(), ly.lse.data_ptr(), ws.am.data_ptr(), ws.delta.data_ptr(), ws.dq.data_ptr(),
-                 ws.dk.data_ptr(), ws.dv.data_ptr(), B, nh, S, dh, st)
+                 ws.dk.data_ptr(), ws.dv.data_ptr(), B, nh, S, dh, st, flops=10.0 * B * nh * S * S * dh)
             call("esm_qkv_rope_bwd", kdt, ws.dq.data_ptr(), ws.dk.data_ptr(), ws.dv.data_ptr(), ws.dqkv.data_ptr(),
                  self._g32(p + "attention.self.qkv.bias").data_ptr(), ws.cos.data_ptr(), ws.sin.data_ptr(), B, S,
                  nh, dh, qs, st)
@@ -473,24 +504,66 @@ class EsmForMaskedLM:
         if self.comm is not None:
             self.comm.ready(E_key)
             self.comm.end_backward()
+            self.comm.reduce_loss(ws.loss_sum)
         self._last_dx_embed = dx
         return ws.loss_sum
 
     # ------------------------------------------------------------------ optimizer
     def set_hyper(self, lr=None, step=None):
+        """Stage AdamW hyper-parameters in device memory (read by the kernel: CUDA-graph safe)."""
         lr = self.lr if lr is None else lr
         step = self.step_count if step is None else step
-        h = torch.tensor([lr, self.betas[0], self.betas[1], self.eps, self.weight_decay, float(step),
-                          self.grad_scale, 0.0], dtype=torch.float32)
-        self.hyper.copy_(h, non_blocking=False)
+        i = self._hyper_i = (self._hyper_i + 1) % len(self._hyper_ring)
+        h, ev = self._hyper_ring[i], self._hyper_ev[i]
+        if ev is not None:
+            ev.synchronize()  # the H2D copy that last read this pinned slot has completed
+        h.copy_(torch.tensor([lr, self.betas[0], self.betas[1], self.eps, self.weight_decay, float(step),
+                              self.grad_scale, 0.0], dtype=torch.float32))
+        self.hyper.copy_(h, non_blocking=True)
+        ev = self._hyper_ev[i] = self._hyper_ev[i] or torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.device))
+
+    def _adamw(self):
+        P = self.store
+        self._call("esm_adamw", P.p32.data_ptr(), P.g32.data_ptr(), P.m.data_ptr(), P.v.data_ptr(),
+                   P.p16.data_ptr() if P.p16 is not None else None, P.decay.data_ptr(), P.numel,
+                   self.hyper.data_ptr(), self._stream(), nbytes=30.0 * P.numel)
 
     def optimizer_step(self, lr=None):
         self.step_count += 1
         self.set_hyper(lr=lr, step=self.step_count)
-        P = self.store
-        _lib.call("esm_adamw", P.p32.data_ptr(), P.g32.data_ptr(), P.m.data_ptr(), P.v.data_ptr(),
-                  P.p16.data_ptr() if P.p16 is not None else None, P.decay.data_ptr(), P.numel,
-                  self.hyper.data_ptr(), self._stream())
+        self._adamw()
+
+    # ------------------------------------------------------------------ CUDA graph
+    def capture(self, ws: Workspace | None = None):
+        """Capture forward + backward + AdamW for the workspace shape into one CUDA graph.
+        Inputs (input_ids / labels / am / n_labels) and hyper-parameters are read from their
+        static device buffers at replay; masking and H2D copies stay outside the graph."""
+        ws = ws or self.ws
+        if self.comm is not None:
+            raise RuntimeError("CUDA-graph capture is single-process only (NCCL buckets run eagerly)")
+        s = torch.cuda.Stream(self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(s):
+            self.forward_backward(ws)  # warm-up: lazy attributes, tensor-map encode paths
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        n0 = self.launches
+        with torch.cuda.graph(g):
+            self.forward_backward(ws)
+            self._adamw()
+        self.graph_launches = self.launches - n0
+        self.graph = g
+        return g
+
+    def graph_step(self, lr=None):
+        """Replay the captured step (after staging this step's batch in the workspace)."""
+        self.step_count += 1
+        self.set_hyper(lr=lr, step=self.step_count)
+        self.graph.replay()
+        self.launches += self.graph_launches
+        return self.ws.loss_sum
 
     def train_step(self, input_ids, attention_mask=None, labels=None, lr=None):
         """One MLM train step on an already-masked batch; returns the device loss tensor."""
