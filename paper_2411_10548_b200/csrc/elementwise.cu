@@ -147,34 +147,80 @@ __global__ void embed_bwd_smem_kernel(const int32_t* __restrict__ ids, const int
 }
 
 // ============================================================================
-// LayerNorm: one warp per row, values held in registers (MAXV 16-byte vectors per lane)
+// LayerNorm: a row is owned by a group of WPR warps (WPR*32 lanes); each lane owns MAXV fixed
+// 16-byte column vectors, so gamma/beta and the backward's dgamma/dbeta/column-sum
+// accumulators live in registers across all rows the group processes.
 // ============================================================================
-template <typename T, int MAXV>
+template <int WPR>
+__device__ __forceinline__ float2 group_sum2(float2 v, float2* red, int wig, int lane, int bar_id, int& parity) {
+  v.x = warp_sum(v.x);
+  v.y = warp_sum(v.y);
+  if constexpr (WPR == 1) {
+    return v;
+  } else {
+    float2* buf = red + parity * WPR;
+    if (lane == 0) buf[wig] = v;
+    asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(WPR * 32) : "memory");
+    float2 r = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int w = 0; w < WPR; ++w) {
+      r.x += buf[w].x;
+      r.y += buf[w].y;
+    }
+    parity ^= 1;
+    return r;
+  }
+}
+
+__device__ __forceinline__ void load_f32x(const float* p, float* o, int n) {
+  // n = 8 (bf16 VEC) or 4 (fp32 VEC); p 16B aligned
+  const float4 a = *reinterpret_cast<const float4*>(p);
+  o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w;
+  if (n == 8) {
+    const float4 b = *reinterpret_cast<const float4*>(p + 4);
+    o[4] = b.x; o[5] = b.y; o[6] = b.z; o[7] = b.w;
+  }
+}
+
+template <typename T, int MAXV, int WPR>
 __global__ void __launch_bounds__(256) ln_fwd_kernel(const T* __restrict__ x, const float* __restrict__ g,
                                                      const float* __restrict__ b, T* __restrict__ y,
                                                      float* __restrict__ mean_out, float* __restrict__ rstd_out,
                                                      int64_t rows, int H, float eps) {
   constexpr int VEC = vec16<T>::N;
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t r = warp; r < rows; r += nwarps) {
+  constexpr int GPB = 8 / WPR;  // groups per block
+  __shared__ float2 red[GPB][2 * WPR];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int grp = warp / WPR, wig = warp % WPR;
+  const int glane = wig * 32 + lane;
+  int parity = 0;
+  float gv[MAXV][VEC], bv[MAXV][VEC];
+#pragma unroll
+  for (int i = 0; i < MAXV; ++i) {
+    const int h = (i * WPR * 32 + glane) * VEC;
+    if (h < H) {
+      load_f32x(g + h, gv[i], VEC);
+      load_f32x(b + h, bv[i], VEC);
+    }
+  }
+  const float invH = 1.0f / H;
+  for (int64_t r = (int64_t)blockIdx.x * GPB + grp; r < rows; r += (int64_t)gridDim.x * GPB) {
     float v[MAXV][VEC];
     float s = 0.f;
 #pragma unroll
     for (int i = 0; i < MAXV; ++i) {
-      const int h = (i * 32 + lane) * VEC;
+      const int h = (i * WPR * 32 + glane) * VEC;
       if (h < H) {
         load_vec(x + r * H + h, v[i]);
 #pragma unroll
         for (int j = 0; j < VEC; ++j) s += v[i][j];
       }
     }
-    const float mu = warp_sum(s) / H;
+    const float mu = group_sum2<WPR>(make_float2(s, 0.f), red[grp], wig, lane, grp + 1, parity).x * invH;
     float ss = 0.f;
 #pragma unroll
     for (int i = 0; i < MAXV; ++i) {
-      const int h = (i * 32 + lane) * VEC;
+      const int h = (i * WPR * 32 + glane) * VEC;
       if (h < H) {
 #pragma unroll
         for (int j = 0; j < VEC; ++j) {
@@ -183,27 +229,25 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const T* __restrict__ x, co
         }
       }
     }
-    const float rs = rsqrtf(warp_sum(ss) / H + eps);
+    const float rs = rsqrtf(group_sum2<WPR>(make_float2(ss, 0.f), red[grp], wig, lane, grp + 1, parity).x * invH + eps);
 #pragma unroll
     for (int i = 0; i < MAXV; ++i) {
-      const int h = (i * 32 + lane) * VEC;
+      const int h = (i * WPR * 32 + glane) * VEC;
       if (h < H) {
         float o[VEC];
 #pragma unroll
-        for (int j = 0; j < VEC; ++j) o[j] = (v[i][j] - mu) * rs * __ldg(g + h + j) + __ldg(b + h + j);
+        for (int j = 0; j < VEC; ++j) o[j] = (v[i][j] - mu) * rs * gv[i][j] + bv[i][j];
         store_vec(y + r * H + h, o);
       }
     }
-    if (lane == 0) {
+    if (glane == 0) {
       mean_out[r] = mu;
       rstd_out[r] = rs;
     }
   }
 }
 
-// Backward; per-row-group smem accumulators for dgamma / dbeta / column sums, flushed with
-// one atomic per column per block.
-template <typename T, int MAXV>
+template <typename T, int MAXV, int WPR>
 __global__ void __launch_bounds__(256) ln_bwd_kernel(const T* __restrict__ dy, const T* __restrict__ x,
                                                      const float* __restrict__ g, const float* __restrict__ mean,
                                                      const float* __restrict__ rstd, const T* __restrict__ dres,
@@ -211,22 +255,30 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const T* __restrict__ dy, c
                                                      float* __restrict__ dg, float* __restrict__ db,
                                                      float* __restrict__ csum, int64_t rows, int H) {
   constexpr int VEC = vec16<T>::N;
-  extern __shared__ float sacc[];  // [nwarps][3][H]
-  const int lane = threadIdx.x & 31;
-  const int wib = threadIdx.x >> 5;
-  const int nw = blockDim.x >> 5;
-  float* my = sacc + (size_t)wib * 3 * H;
-  for (int i = lane; i < 3 * H; i += 32) my[i] = 0.f;
-  __syncwarp();
-  const int64_t warp = (int64_t)blockIdx.x * nw + wib;
-  const int64_t nwarps = (int64_t)gridDim.x * nw;
-  for (int64_t r = warp; r < rows; r += nwarps) {
+  constexpr int GPB = 8 / WPR;
+  __shared__ float2 red[GPB][2 * WPR];
+  extern __shared__ float sacc[];  // [3][H] block-level partial sums
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int grp = warp / WPR, wig = warp % WPR;
+  const int glane = wig * 32 + lane;
+  int parity = 0;
+  for (int i = threadIdx.x; i < 3 * H; i += blockDim.x) sacc[i] = 0.f;
+  float gv[MAXV][VEC], ag[MAXV][VEC], ab[MAXV][VEC], ac[MAXV][VEC];
+#pragma unroll
+  for (int i = 0; i < MAXV; ++i) {
+    const int h = (i * WPR * 32 + glane) * VEC;
+    if (h < H) load_f32x(g + h, gv[i], VEC);
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) ag[i][j] = ab[i][j] = ac[i][j] = 0.f;
+  }
+  const float invH = 1.0f / H;
+  for (int64_t r = (int64_t)blockIdx.x * GPB + grp; r < rows; r += (int64_t)gridDim.x * GPB) {
     const float mu = mean[r], rs = rstd[r];
     float xh[MAXV][VEC], gy[MAXV][VEC];
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
     for (int i = 0; i < MAXV; ++i) {
-      const int h = (i * 32 + lane) * VEC;
+      const int h = (i * WPR * 32 + glane) * VEC;
       if (h < H) {
         float xv[VEC], dv[VEC];
         load_vec(x + r * H + h, xv);
@@ -234,19 +286,20 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const T* __restrict__ dy, c
 #pragma unroll
         for (int j = 0; j < VEC; ++j) {
           xh[i][j] = (xv[j] - mu) * rs;
-          gy[i][j] = dv[j] * __ldg(g + h + j);
+          gy[i][j] = dv[j] * gv[i][j];
           s1 += gy[i][j];
           s2 += gy[i][j] * xh[i][j];
-          my[h + j] += dv[j] * xh[i][j];
-          my[H + h + j] += dv[j];
+          ag[i][j] += dv[j] * xh[i][j];
+          ab[i][j] += dv[j];
         }
       }
     }
-    s1 = warp_sum(s1) / H;
-    s2 = warp_sum(s2) / H;
+    const float2 red2 = group_sum2<WPR>(make_float2(s1, s2), red[grp], wig, lane, grp + 1, parity);
+    s1 = red2.x * invH;
+    s2 = red2.y * invH;
 #pragma unroll
     for (int i = 0; i < MAXV; ++i) {
-      const int h = (i * 32 + lane) * VEC;
+      const int h = (i * WPR * 32 + glane) * VEC;
       if (h < H) {
         float o[VEC];
 #pragma unroll
@@ -264,22 +317,29 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const T* __restrict__ dy, c
           for (int j = 0; j < VEC; ++j) o[j] *= gelu_grad_f(zv[j]);
         }
 #pragma unroll
-        for (int j = 0; j < VEC; ++j) my[2 * H + h + j] += o[j];
+        for (int j = 0; j < VEC; ++j) ac[i][j] += o[j];
         store_vec(dx + r * H + h, o);
       }
     }
   }
   __syncthreads();
-  for (int c = threadIdx.x; c < H; c += blockDim.x) {
-    float a = 0.f, bsum = 0.f, cs = 0.f;
-    for (int w = 0; w < nw; ++w) {
-      a += sacc[(size_t)w * 3 * H + c];
-      bsum += sacc[(size_t)w * 3 * H + H + c];
-      cs += sacc[(size_t)w * 3 * H + 2 * H + c];
+#pragma unroll
+  for (int i = 0; i < MAXV; ++i) {
+    const int h = (i * WPR * 32 + glane) * VEC;
+    if (h < H) {
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) {
+        atomicAdd(&sacc[h + j], ag[i][j]);
+        atomicAdd(&sacc[H + h + j], ab[i][j]);
+        atomicAdd(&sacc[2 * H + h + j], ac[i][j]);
+      }
     }
-    if (dg) atomicAdd(dg + c, a);
-    if (db) atomicAdd(db + c, bsum);
-    if (csum) atomicAdd(csum + c, cs);
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < H; c += blockDim.x) {
+    if (dg) atomicAdd(dg + c, sacc[c]);
+    if (db) atomicAdd(db + c, sacc[H + c]);
+    if (csum) atomicAdd(csum + c, sacc[2 * H + c]);
   }
 }
 
@@ -641,33 +701,47 @@ int esm_embed_bwd(int dtype, const int32_t* ids, const int32_t* am, const float*
   ESM_LAUNCH_RET();
 }
 
-#define LN_DISPATCH(T, KERNEL, MAXV_NEEDED, ...)                                    \
-  do {                                                                              \
-    if (MAXV_NEEDED <= 1) KERNEL<T, 1>__VA_ARGS__;                                  \
-    else if (MAXV_NEEDED <= 2) KERNEL<T, 2>__VA_ARGS__;                             \
-    else if (MAXV_NEEDED <= 4) KERNEL<T, 4>__VA_ARGS__;                             \
-    else if (MAXV_NEEDED <= 6) KERNEL<T, 6>__VA_ARGS__;                             \
-    else if (MAXV_NEEDED <= 10) KERNEL<T, 10>__VA_ARGS__;                           \
-    else if (MAXV_NEEDED <= 20) KERNEL<T, 20>__VA_ARGS__;                           \
-    else { esm::set_last_error("hidden size too large"); return ESM_ENOTSUP; }      \
+// choose (MAXV, WPR): WPR = smallest power of two with <= 3 vectors per lane
+static inline void ln_shape(int H, int vec, int& maxv, int& wpr) {
+  const int vectors = H / vec;
+  wpr = 1;
+  while (wpr < 8 && vectors > wpr * 32 * 3) wpr <<= 1;
+  maxv = (vectors + wpr * 32 - 1) / (wpr * 32);
+}
+
+#define LN_SWITCH(T, KERNEL, LAUNCH)                                                     \
+  do {                                                                                   \
+    if (mv == 1 && wpr == 1) LAUNCH(KERNEL<T, 1, 1>);                                    \
+    else if (mv == 2 && wpr == 1) LAUNCH(KERNEL<T, 2, 1>);                               \
+    else if (mv == 3 && wpr == 1) LAUNCH(KERNEL<T, 3, 1>);                               \
+    else if (mv == 2 && wpr == 2) LAUNCH(KERNEL<T, 2, 2>);                               \
+    else if (mv == 3 && wpr == 2) LAUNCH(KERNEL<T, 3, 2>);                               \
+    else if (mv == 2 && wpr == 4) LAUNCH(KERNEL<T, 2, 4>);                               \
+    else if (mv == 3 && wpr == 4) LAUNCH(KERNEL<T, 3, 4>);                               \
+    else if (mv == 2 && wpr == 8) LAUNCH(KERNEL<T, 2, 8>);                               \
+    else if (mv == 3 && wpr == 8) LAUNCH(KERNEL<T, 3, 8>);                               \
+    else { esm::set_last_error("layernorm: H=%d unsupported", H); return ESM_ENOTSUP; }  \
   } while (0)
 
 int esm_layernorm_fwd(int dtype, const void* x, const float* gamma, const float* beta, void* y, float* mean, float* rstd,
                       int rows, int H, float eps, esm_stream_t stream) {
   ESM_CHECK_ARG(x && gamma && beta && y && mean && rstd && rows > 0 && H > 0, "esm_layernorm_fwd: bad args");
-  const int grid = grid_for((int64_t)rows * 32, 256);
+  const int vec = dtype == ESM_BF16 ? 8 : 4;
+  ESM_CHECK_ARG(H % vec == 0, "layernorm: H %% %d", vec);
+  int mv, wpr;
+  ln_shape(H, vec, mv, wpr);
+  const int gpb = 8 / wpr;
+  int grid = (int)((rows + gpb - 1) / gpb);
+  if (grid > 148 * 8) grid = 148 * 8;
+#define L_F(...) __VA_ARGS__<<<grid, 256, 0, S(stream)>>>((const TT*)x, gamma, beta, (TT*)y, mean, rstd, rows, H, eps)
   if (dtype == ESM_BF16) {
-    ESM_CHECK_ARG(H % 8 == 0, "layernorm: H %% 8");
-    const int mv = (H + 255) / 256;
-    LN_DISPATCH(__nv_bfloat16, ln_fwd_kernel, mv,
-                <<<grid, 256, 0, S(stream)>>>((const __nv_bfloat16*)x, gamma, beta, (__nv_bfloat16*)y, mean, rstd,
-                                              rows, H, eps));
+    using TT = __nv_bfloat16;
+    LN_SWITCH(TT, ln_fwd_kernel, L_F);
   } else {
-    ESM_CHECK_ARG(H % 4 == 0, "layernorm: H %% 4");
-    const int mv = (H + 127) / 128;
-    LN_DISPATCH(float, ln_fwd_kernel, mv,
-                <<<grid, 256, 0, S(stream)>>>((const float*)x, gamma, beta, (float*)y, mean, rstd, rows, H, eps));
+    using TT = float;
+    LN_SWITCH(TT, ln_fwd_kernel, L_F);
   }
+#undef L_F
   ESM_LAUNCH_RET();
 }
 
@@ -675,42 +749,30 @@ int esm_layernorm_bwd(int dtype, const void* dy, const void* x, const float* gam
                       const float* rstd, const void* dres, const void* gelu_z, void* dx, float* dgamma, float* dbeta,
                       float* col_sum, int rows, int H, esm_stream_t stream) {
   ESM_CHECK_ARG(dy && x && gamma && mean && rstd && dx && rows > 0, "esm_layernorm_bwd: bad args");
-  int warps = 8;
-  while (warps > 1 && (size_t)warps * 3 * H * 4 > 120 * 1024) warps >>= 1;
-  const int block = warps * 32;
-  const size_t sm = (size_t)warps * 3 * H * 4;
-  int grid = (int)((rows + warps * 8 - 1) / (warps * 8));  // >= 8 rows per warp amortises the flush
-  if (grid > 148 * 4) grid = 148 * 4;
-  if (grid < 1) grid = 1;
+  const int vec = dtype == ESM_BF16 ? 8 : 4;
+  ESM_CHECK_ARG(H % vec == 0, "layernorm: H %% %d", vec);
+  int mv, wpr;
+  ln_shape(H, vec, mv, wpr);
+  const size_t sm = (size_t)3 * H * sizeof(float);
+  ESM_CHECK_ARG(sm <= 200 * 1024, "layernorm_bwd: H too large");
+  int grid = 148 * 2;
+  const int gpb = 8 / wpr;
+  if ((int64_t)grid * gpb > rows) grid = (int)((rows + gpb - 1) / gpb);
+#define L_B(...)                                                                                     \
+  do {                                                                                               \
+    cudaFuncSetAttribute(__VA_ARGS__, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);         \
+    __VA_ARGS__<<<grid, 256, sm, S(stream)>>>((const TT*)dy, (const TT*)x, gamma, mean, rstd,        \
+                                              (const TT*)dres, (const TT*)gelu_z, (TT*)dx, dgamma,   \
+                                              dbeta, col_sum, rows, H);                              \
+  } while (0)
   if (dtype == ESM_BF16) {
-    ESM_CHECK_ARG(H % 8 == 0, "layernorm: H %% 8");
-    const int mv = (H + 255) / 256;
-    auto setattr = [&](const void* k) { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); };
-    if (mv <= 1) setattr((const void*)ln_bwd_kernel<__nv_bfloat16, 1>);
-    else if (mv <= 2) setattr((const void*)ln_bwd_kernel<__nv_bfloat16, 2>);
-    else if (mv <= 4) setattr((const void*)ln_bwd_kernel<__nv_bfloat16, 4>);
-    else if (mv <= 6) setattr((const void*)ln_bwd_kernel<__nv_bfloat16, 6>);
-    else if (mv <= 10) setattr((const void*)ln_bwd_kernel<__nv_bfloat16, 10>);
-    else setattr((const void*)ln_bwd_kernel<__nv_bfloat16, 20>);
-    LN_DISPATCH(__nv_bfloat16, ln_bwd_kernel, mv,
-                <<<grid, block, sm, S(stream)>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, gamma, mean, rstd,
-                                                 (const __nv_bfloat16*)dres, (const __nv_bfloat16*)gelu_z,
-                                                 (__nv_bfloat16*)dx, dgamma, dbeta, col_sum, rows, H));
+    using TT = __nv_bfloat16;
+    LN_SWITCH(TT, ln_bwd_kernel, L_B);
   } else {
-    ESM_CHECK_ARG(H % 4 == 0, "layernorm: H %% 4");
-    const int mv = (H + 127) / 128;
-    auto setattr = [&](const void* k) { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); };
-    if (mv <= 1) setattr((const void*)ln_bwd_kernel<float, 1>);
-    else if (mv <= 2) setattr((const void*)ln_bwd_kernel<float, 2>);
-    else if (mv <= 4) setattr((const void*)ln_bwd_kernel<float, 4>);
-    else if (mv <= 6) setattr((const void*)ln_bwd_kernel<float, 6>);
-    else if (mv <= 10) setattr((const void*)ln_bwd_kernel<float, 10>);
-    else setattr((const void*)ln_bwd_kernel<float, 20>);
-    LN_DISPATCH(float, ln_bwd_kernel, mv,
-                <<<grid, block, sm, S(stream)>>>((const float*)dy, (const float*)x, gamma, mean, rstd,
-                                                 (const float*)dres, (const float*)gelu_z, (float*)dx, dgamma, dbeta,
-                                                 col_sum, rows, H));
+    using TT = float;
+    LN_SWITCH(TT, ln_bwd_kernel, L_B);
   }
+#undef L_B
   ESM_LAUNCH_RET();
 }
 

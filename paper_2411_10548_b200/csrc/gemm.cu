@@ -81,8 +81,20 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& p, int row, int 
     return;
   } else {
     if (p.bias != nullptr && EPI != ESM_EPI_DGELU) {
+      if (col0 + 32 <= p.N) {
+        const float4* b4 = reinterpret_cast<const float4*>(p.bias + col0);  // bias is 1 KB aligned
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] += (col0 + j < p.N) ? __ldg(p.bias + col0 + j) : 0.f;
+        for (int j = 0; j < 8; ++j) {
+          const float4 t = __ldg(b4 + j);
+          v[4 * j] += t.x;
+          v[4 * j + 1] += t.y;
+          v[4 * j + 2] += t.z;
+          v[4 * j + 3] += t.w;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] += (col0 + j < p.N) ? __ldg(p.bias + col0 + j) : 0.f;
+      }
     }
     if constexpr (EPI == ESM_EPI_RESID || EPI == ESM_EPI_DGELU) {
       const __nv_bfloat16* a = reinterpret_cast<const __nv_bfloat16*>(p.aux_in) + (int64_t)row * p.ld_aux_in + col0;
