@@ -6,6 +6,8 @@
 //       (dh=24 is zero-padded to K=32 for QKᵀ only).  Backward parallelises over key blocks and
 //       accumulates dQ with fp32 vector reductions (red.global.add.v2.f32).
 // fp32: SIMT reference-precision kernels (parity mode).
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace esm {
@@ -681,6 +683,19 @@ __global__ void __launch_bounds__(64) bwd_dkv_f32_kernel(const float* __restrict
 }  // namespace attn
 }  // namespace esm
 
+namespace esm {
+int attn_fwd_tc(const void* q, const void* k, const void* v, const int32_t* km, void* o, float* lse, int B, int nh,
+                int S, int dh, cudaStream_t st);
+static int legacy_attention() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ESM_ATTN_LEGACY");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v;
+}
+}  // namespace esm
+
 using namespace esm;
 
 extern "C" int esm_attn_fwd(int dtype, const void* q, const void* k, const void* v, const int32_t* key_mask, void* o,
@@ -688,6 +703,9 @@ extern "C" int esm_attn_fwd(int dtype, const void* q, const void* k, const void*
   ESM_CHECK_ARG(q && k && v && o && lse && B > 0 && nh > 0 && S > 0, "esm_attn_fwd: bad args");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   dim3 grid((S + 63) / 64, B * nh);
+  if (dtype == ESM_BF16 && !legacy_attention()) {
+    return attn_fwd_tc(q, k, v, key_mask, o, lse, B, nh, S, dh, st);
+  }
   if (dtype == ESM_BF16) {
     auto* Q = (const __nv_bfloat16*)q;
     auto* K = (const __nv_bfloat16*)k;

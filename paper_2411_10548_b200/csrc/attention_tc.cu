@@ -1,0 +1,440 @@
+// Flash attention forward on Blackwell tensor cores (tcgen05 + TMEM + TMA), ESM-2 semantics:
+// non-causal, q pre-scaled (scaling = 1), key-padding mask (HF:modeling_esm.py:257-282).
+//
+// One CTA = 128 queries of one (batch, head).  Warp roles:
+//   warp 0      TMA producer: Q once, then K/V tiles of 128 keys into a 2-stage smem ring
+//   warp 1      MMA issuer (one elected lane): S_j = Q K_jᵀ into TMEM (double buffered),
+//               O += P_{j-1} V_{j-1} with P read straight from TMEM (A-from-TMEM "TS" MMA)
+//   warps 2..5  softmax: thread = one query row (its TMEM lane); exp2 online softmax with
+//               lazy O rescaling (only when the running max grows by > 2^8), P written back
+//               to TMEM as packed bf16 over its own S buffer; final O / l and LSE to HBM.
+// Head dims 16/24/32/64 are zero-padded by TMA (OOB fill) to DP = 16/32/32/64 and use the
+// matching 32/64/64/128-byte swizzle.  Right-padded (prefix) key masks skip whole key tiles;
+// arbitrary masks fall back to per-key mask loads.
+#include <mutex>
+
+#include "common.cuh"
+#include "sm100.cuh"
+
+namespace esm {
+namespace fa {
+using namespace sm100;
+
+constexpr int BM = 128;
+constexpr int kThreads = 192;
+constexpr float L2E = 1.4426950408889634f;
+constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
+
+template <int DH, int BN_>
+struct Shape {
+  static constexpr int BN = BN_;                                    // keys per tile
+  static constexpr int DP = DH <= 16 ? 16 : (DH <= 32 ? 32 : 64);  // padded head dim (MMA K / N)
+  static constexpr int ROWB = DP * 2;                               // smem row bytes = swizzle span
+  static constexpr uint32_t LAYOUT = ROWB == 128 ? 2u : (ROWB == 64 ? 4u : 6u);  // SW128 / SW64 / SW32
+  static constexpr int Q_BYTES = BM * ROWB;
+  static constexpr int KV_BYTES = BN * ROWB;
+  static constexpr int STAGES = 3;
+  // TMEM: S0 [0,BN) S1 [BN,2BN) O [2BN, 2BN+DP)
+  static constexpr uint32_t TMEM_COLS = (2 * BN + DP) <= 256 ? 256 : 512;
+};
+
+__device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)layout << 61;
+  return d;
+}
+
+// D[tmem] (+)= A[tmem] * B[smem]^T
+__device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// Scan the key mask of batch b: number of valid keys and whether the mask is a prefix.
+__device__ __forceinline__ void scan_mask(const int32_t* __restrict__ km, int b, int S, int* s_len, int* s_nonprefix) {
+  if (threadIdx.x == 0) {
+    *s_len = 0;
+    *s_nonprefix = 0;
+  }
+  __syncthreads();
+  int cnt = 0;
+  for (int s = threadIdx.x; s < S; s += blockDim.x) cnt += km ? (km[(int64_t)b * S + s] != 0) : 1;
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  if ((threadIdx.x & 31) == 0) atomicAdd(s_len, cnt);
+  __syncthreads();
+  const int len = *s_len;
+  int bad = 0;
+  if (km)
+    for (int s = threadIdx.x; s < S; s += blockDim.x) bad |= ((km[(int64_t)b * S + s] != 0) != (s < len));
+  bad = __reduce_or_sync(0xffffffffu, bad);
+  if ((threadIdx.x & 31) == 0 && bad) atomicOr(s_nonprefix, 1);
+  __syncthreads();
+}
+
+template <int DH, int BN>
+__global__ void __launch_bounds__(kThreads, 2)
+    fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+               const __grid_constant__ CUtensorMap tmV, const int32_t* __restrict__ key_mask,
+               __nv_bfloat16* __restrict__ O, float* __restrict__ LSE, int S, int nh) {
+  using SH = Shape<DH, BN>;
+  constexpr int DP = SH::DP, ROWB = SH::ROWB, ST = SH::STAGES;
+  constexpr int QB = SH::Q_BYTES, TB = SH::KV_BYTES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = sQ + QB;
+  uint8_t* sV = sK + ST * TB;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + ST * TB);
+  uint64_t* q_full = bars;                 // 1
+  uint64_t* kv_full = bars + 1;            // ST
+  uint64_t* kv_empty = kv_full + ST;       // ST
+  uint64_t* s_full = kv_empty + ST;        // 2
+  uint64_t* p_full = s_full + 2;           // 2
+  uint64_t* o_done = p_full + 2;           // 1
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 1);
+  int* s_len = reinterpret_cast<int*>(tmem_slot + 1);
+  int* s_np = s_len + 1;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int bh = blockIdx.y, b = bh / nh, h = bh % nh;
+  const int q0 = blockIdx.x * BM;
+  const int H = nh * DH;
+
+  scan_mask(key_mask, b, S, s_len, s_np);
+  const int kv_len = *s_len;
+  const bool nonprefix = *s_np != 0;
+  const int ntiles = nonprefix ? (S + BN - 1) / BN : (kv_len + BN - 1) / BN;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int i = 0; i < ST; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 4);
+    }
+    mbar_init(o_done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<SH::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+  const uint32_t t_o = tbase + 2 * BN;
+
+  const int row0 = bh * S;  // first row of this head in the [B*nh*S, DH] views
+  if (warp == 0) {
+    // ======================= TMA producer =======================
+    if (lane == 0) {
+      tma_prefetch(&tmQ);
+      tma_prefetch(&tmK);
+      tma_prefetch(&tmV);
+      mbar_expect_tx(q_full, QB);
+      tma_load_2d(sQ, &tmQ, q_full, 0, row0 + q0);
+    }
+    for (int j = 0; j < ntiles; ++j) {
+      const int st = j % ST;
+      mbar_wait(&kv_empty[st], ((j / ST) & 1) ^ 1);
+      if (lane == 0) {
+        mbar_expect_tx(&kv_full[st], 2 * TB);
+        tma_load_2d(sK + st * TB, &tmK, &kv_full[st], 0, row0 + j * BN);
+        tma_load_2d(sV + st * TB, &tmV, &kv_full[st], 0, row0 + j * BN);
+      }
+      __syncwarp();
+    }
+  } else if (warp == 1) {
+    // ======================= MMA issuer =======================
+    constexpr uint32_t idesc_s = make_idesc_bf16(BM, BN, false, false);  // S = Q Kᵀ, both K-major
+    constexpr uint32_t idesc_o = make_idesc_bf16(BM, DP, false, true);   // O += P V, V N-major
+    const uint32_t q_addr = smem_u32(sQ);
+    mbar_wait(q_full, 0);
+    for (int j = 0; j <= ntiles; ++j) {
+      if (j < ntiles) {
+        const int st = j % ST;
+        mbar_wait(&kv_full[st], (j / ST) & 1);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t k_addr = smem_u32(sK + st * TB);
+          const uint32_t d = tbase + (j & 1) * BN;
+#pragma unroll
+          for (int k = 0; k < DP / 16; ++k) {
+            const uint64_t ad = make_sdesc(q_addr + k * 32, 16, 8 * ROWB, SH::LAYOUT);
+            const uint64_t bd = make_sdesc(k_addr + k * 32, 16, 8 * ROWB, SH::LAYOUT);
+            mma_bf16_ss(d, ad, bd, idesc_s, k > 0 ? 1u : 0u);
+          }
+          mma_commit(&s_full[j & 1]);
+        }
+        __syncwarp();
+      }
+      if (j >= 1) {
+        const int i = j - 1;  // O += P_i V_i
+        const int st = i % ST;
+        mbar_wait(&p_full[i & 1], (i >> 1) & 1);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t v_addr = smem_u32(sV + st * TB);
+          const uint32_t p_tmem = tbase + (i & 1) * BN;
+#pragma unroll
+          for (int k = 0; k < BN / 16; ++k) {
+            // V tile: 128 key rows (K) x DP (N, contiguous); 16 keys per MMA = 16 rows
+            const uint64_t bd = make_sdesc(v_addr + k * 16 * ROWB, BN * ROWB, 8 * ROWB, SH::LAYOUT);
+            mma_bf16_ts(t_o, p_tmem + k * 8, bd, idesc_o, (i > 0 || k > 0) ? 1u : 0u);
+          }
+          mma_commit(&kv_empty[st]);
+          mma_commit(o_done);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ======================= softmax warps =======================
+    const int qq = warp & 3;
+    const int r = qq * 32 + lane;  // query row within tile == TMEM lane
+    const uint32_t lane_off = (uint32_t)(qq * 32) << 16;
+    float m_used = -INFINITY, l = 0.f;
+    for (int j = 0; j < ntiles; ++j) {
+      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      tc_fence_after();
+      const uint32_t sbase = tbase + lane_off + (j & 1) * BN;
+      float s[BN];
+#pragma unroll
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t u[32];
+        tmem_ld32(sbase + c, u);
+#pragma unroll
+        for (int e = 0; e < 32; ++e) s[c + e] = __uint_as_float(u[e]);
+      }
+      tmem_ld_wait();
+      const int kbase = j * BN;
+      float mx = -INFINITY;
+      if (!nonprefix) {
+        const int valid = kv_len - kbase;  // keys [0, valid) of this tile are real
+        if (valid >= BN) {
+#pragma unroll
+          for (int c = 0; c < BN; ++c) mx = fmaxf(mx, s[c]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < BN; ++c) {
+            s[c] = c < valid ? s[c] : -INFINITY;
+            mx = fmaxf(mx, s[c]);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < BN; ++c) {
+          const int kk = kbase + c;
+          const bool ok = kk < S && key_mask[(int64_t)b * S + kk] != 0;
+          s[c] = ok ? s[c] : -INFINITY;
+          mx = fmaxf(mx, s[c]);
+        }
+      }
+      const float mnew = mx * L2E;
+      const bool grow = mnew > m_used + RESCALE_THRESHOLD;
+      if (__any_sync(0xffffffffu, grow)) {  // warp-uniform: tcgen05.ld/st are warp-collective
+        // raise the reference max; rescale running sum and (if any PV issued) O in TMEM
+        const float f = grow ? ex2(m_used - mnew) : 1.0f;  // 0 on the first tile
+        l *= f;
+        if (j > 0) {
+          mbar_wait(o_done, (j - 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < DP; c += 16) {
+            uint32_t u[16];
+            tmem_ld16(t_o + lane_off + c, u);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) u[e] = __float_as_uint(__uint_as_float(u[e]) * f);
+            tmem_st16(t_o + lane_off + c, u);
+          }
+        }
+        if (grow) m_used = mnew;
+      }
+      const float moff = m_used == -INFINITY ? 0.f : m_used;
+      float ls = 0.f;
+#pragma unroll
+      for (int c = 0; c < BN; c += 64) {
+        uint32_t pk[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const float p0 = ex2(fmaf(s[c + 2 * e], L2E, -moff));
+          const float p1 = ex2(fmaf(s[c + 2 * e + 1], L2E, -moff));
+          ls += p0 + p1;
+          pk[e] = pack2(p0, p1);
+        }
+        tmem_st32(sbase + c / 2, pk);  // P (bf16x2) over the first 64 columns of this S buffer
+      }
+      l += ls;
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[j & 1]);
+    }
+    // ---- epilogue: wait for the last PV, O / l, LSE
+    const int qrow = q0 + r;
+    float inv = l > 0.f ? 1.f / l : 0.f;
+    if (ntiles > 0) {
+      mbar_wait(o_done, (ntiles - 1) & 1);
+      tc_fence_after();
+    }
+    float o[DP];
+#pragma unroll
+    for (int c = 0; c < DP; c += 16) {
+      uint32_t u[16];
+      tmem_ld16(t_o + lane_off + c, u);
+      tmem_ld_wait();
+#pragma unroll
+      for (int e = 0; e < 16; ++e) o[c + e] = ntiles > 0 ? __uint_as_float(u[e]) * inv : 0.f;
+    }
+    if (qrow < S) {
+      __nv_bfloat16* dst = O + ((int64_t)b * S + qrow) * H + h * DH;
+#pragma unroll
+      for (int c = 0; c < DH; c += 8) {
+        uint4 w;
+        w.x = pack2(o[c], o[c + 1]);
+        w.y = pack2(o[c + 2], o[c + 3]);
+        w.z = pack2(o[c + 4], o[c + 5]);
+        w.w = pack2(o[c + 6], o[c + 7]);
+        *reinterpret_cast<uint4*>(dst + c) = w;
+      }
+      LSE[(int64_t)bh * S + qrow] = l > 0.f ? (m_used + log2f(l)) / L2E : -INFINITY;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<SH::TMEM_COLS>(tbase);
+  }
+}
+
+// ---------------------------------------------------------------------------- host
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static PFN_encodeTiled encoder() {
+  static PFN_encodeTiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  });
+  return fn;
+}
+
+template <int DH, int ROWS>
+static int head_map(CUtensorMap* m, const void* base, int64_t rows) {
+  using SH = Shape<DH, 64>;
+  PFN_encodeTiled enc = encoder();
+  if (!enc) {
+    set_last_error("cuTensorMapEncodeTiled unavailable");
+    return ESM_EDRIVER;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)DH, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)DH * 2};
+  cuuint32_t box[2] = {(cuuint32_t)SH::DP, (cuuint32_t)ROWS};
+  cuuint32_t estr[2] = {1, 1};
+  const CUtensorMapSwizzle sw = SH::ROWB == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : SH::ROWB == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                 : CU_TENSOR_MAP_SWIZZLE_32B;
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_last_error("attention tensor map encode failed (%d)", (int)r);
+    return ESM_EDRIVER;
+  }
+  return 0;
+}
+
+template <int DH, int BN>
+int launch_fwd(const void* q, const void* k, const void* v, const int32_t* km, void* o, float* lse, int B, int nh,
+               int S, cudaStream_t st) {
+  using SH = Shape<DH, BN>;
+  CUtensorMap tq, tk, tv;
+  const int64_t rows = (int64_t)B * nh * S;
+  int rc;
+  if ((rc = head_map<DH, BM>(&tq, q, rows)) || (rc = head_map<DH, BN>(&tk, k, rows)) ||
+      (rc = head_map<DH, BN>(&tv, v, rows)))
+    return rc;
+  const int smem = SH::Q_BYTES + 2 * SH::STAGES * SH::KV_BYTES + 1024 + 256;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(fwd_kernel<DH, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  dim3 grid((S + BM - 1) / BM, B * nh);
+  fwd_kernel<DH, BN><<<grid, kThreads, smem, st>>>(tq, tk, tv, km, (__nv_bfloat16*)o, lse, S, nh);
+  ESM_LAUNCH_RET();
+}
+
+}  // namespace fa
+
+int attn_fwd_tc(const void* q, const void* k, const void* v, const int32_t* km, void* o, float* lse, int B, int nh,
+                int S, int dh, cudaStream_t st) {
+  ESM_CHECK_ARG(((uintptr_t)q & 15) == 0 && ((uintptr_t)k & 15) == 0 && ((uintptr_t)v & 15) == 0,
+                "attention: q/k/v must be 16B aligned");
+  switch (dh) {
+    case 16: return fa::launch_fwd<16, 64>(q, k, v, km, o, lse, B, nh, S, st);
+    case 24: return fa::launch_fwd<24, 64>(q, k, v, km, o, lse, B, nh, S, st);
+    case 32: return fa::launch_fwd<32, 64>(q, k, v, km, o, lse, B, nh, S, st);
+    case 64: return fa::launch_fwd<64, 64>(q, k, v, km, o, lse, B, nh, S, st);
+    default: set_last_error("attention: head dim %d unsupported", dh); return ESM_ENOTSUP;
+  }
+}
+
+}  // namespace esm

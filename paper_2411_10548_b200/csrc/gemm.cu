@@ -12,6 +12,7 @@
 // fp32 path (parity mode): tiled SIMT FFMA kernel with the same epilogues.
 #include <cstdarg>
 #include <cstdio>
+#include <cstring>
 #include <mutex>
 
 #include "common.cuh"
@@ -38,17 +39,31 @@ namespace sm100 {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int kThreads = 192;  // warp0 TMA, warp1 MMA (+TMEM alloc), warps 2..5 epilogue
+constexpr int kEpiWarps = 8;    // two epilogue warps per TMEM lane quarter (interleaved 32-column chunks)
+constexpr int kThreads = 64 + 32 * kEpiWarps;  // warp0 TMA, warp1 MMA (+TMEM alloc), warps 2.. epilogue
 
-template <int BN>
+// Epilogue staging per warp: a 32x32 output chunk in swizzled smem, written to HBM by TMA.
+template <int EPI>
+struct EpiCfg {
+  static constexpr bool F32 = EPI == ESM_EPI_F32_ACC;
+  static constexpr int CHUNK = F32 ? 32 * 32 * 4 : 32 * 32 * 2;  // bytes per 32x32 chunk
+  static constexpr int NOUT = EPI == ESM_EPI_GELU ? 2 : 1;        // outputs per chunk (GELU: C and Z)
+  static constexpr bool AUX = EPI == ESM_EPI_RESID || EPI == ESM_EPI_DGELU;
+  static constexpr int WARP_BYTES = 2 * NOUT * CHUNK + (AUX ? 2 * CHUNK : 0);
+  static constexpr int BYTES = kEpiWarps * WARP_BYTES;
+};
+
+template <int BN, int EPI>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
+  static constexpr int BUDGET = 224 * 1024 - EpiCfg<EPI>::BYTES - 1024 - 512;
+  static constexpr int STAGES = BUDGET / STAGE_BYTES > 8 ? 8 : BUDGET / STAGE_BYTES;
   static constexpr uint32_t TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                                           : (2 * BN <= 256) ? 256 : 512;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + EpiCfg<EPI>::BYTES + 1024 /*align*/ + 512 /*barriers*/;
+  static_assert(STAGES >= 2, "not enough shared memory for the pipeline");
 };
 
 struct TileInfo {
@@ -65,101 +80,55 @@ __device__ __forceinline__ void decode_tile(const TileInfo& ti, int t, int& mb, 
   kb1 = min(ti.kb_total, kb0 + ti.kb_per_split);
 }
 
-template <int EPI>
-__device__ __forceinline__ void epilogue_chunk(const EpiParams& p, int row, int col0, float (&v)[32], int lane) {
-  const bool row_ok = row < p.M;
-  const bool full = row_ok && (col0 + 32 <= p.N);
-  if constexpr (EPI == ESM_EPI_F32_ACC) {
-    if (!row_ok) return;
-    float* c = reinterpret_cast<float*>(p.C) + (int64_t)row * p.ldc + col0;
-    if (full) {
-#pragma unroll
-      for (int j = 0; j < 32; j += 4) red_add_v4_f32(c + j, v[j], v[j + 1], v[j + 2], v[j + 3]);
-    } else {
-      for (int j = 0; j < 32 && col0 + j < p.N; ++j) red_add_f32(c + j, v[j]);
-    }
-    return;
-  } else {
-    if (p.bias != nullptr && EPI != ESM_EPI_DGELU) {
-      if (col0 + 32 <= p.N) {
-        const float4* b4 = reinterpret_cast<const float4*>(p.bias + col0);  // bias is 1 KB aligned
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float4 t = __ldg(b4 + j);
-          v[4 * j] += t.x;
-          v[4 * j + 1] += t.y;
-          v[4 * j + 2] += t.z;
-          v[4 * j + 3] += t.w;
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] += (col0 + j < p.N) ? __ldg(p.bias + col0 + j) : 0.f;
-      }
-    }
-    if constexpr (EPI == ESM_EPI_RESID || EPI == ESM_EPI_DGELU) {
-      const __nv_bfloat16* a = reinterpret_cast<const __nv_bfloat16*>(p.aux_in) + (int64_t)row * p.ld_aux_in + col0;
-      float r[32];
-      if (full) {
-#pragma unroll
-        for (int j = 0; j < 32; j += 8) load_vec(a + j, r + j);
-      } else {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) r[j] = (row_ok && col0 + j < p.N) ? __bfloat162float(a[j]) : 0.f;
-      }
-      if constexpr (EPI == ESM_EPI_RESID) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] += r[j];
-      } else {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] *= gelu_grad_f(r[j]);
-      }
-    }
-    __nv_bfloat16* c = reinterpret_cast<__nv_bfloat16*>(p.C) + (int64_t)row * p.ldc + col0;
-    if constexpr (EPI == ESM_EPI_GELU) {
-      __nv_bfloat16* z = reinterpret_cast<__nv_bfloat16*>(p.aux_out) + (int64_t)row * p.ld_aux_out + col0;
-      if (full) {
-#pragma unroll
-        for (int j = 0; j < 32; j += 8) store_vec(z + j, v + j);
-      } else if (row_ok) {
-        for (int j = 0; j < 32 && col0 + j < p.N; ++j) z[j] = __float2bfloat16_rn(v[j]);
-      }
-#pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = gelu_f(v[j]);
-    }
-    if (full) {
-#pragma unroll
-      for (int j = 0; j < 32; j += 8) store_vec(c + j, v + j);
-    } else if (row_ok) {
-      for (int j = 0; j < 32 && col0 + j < p.N; ++j) c[j] = __float2bfloat16_rn(v[j]);
-    }
-    if constexpr (EPI == ESM_EPI_DGELU) {
-      if (p.col_sum != nullptr) {
-        if (!row_ok) {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = 0.f;
-        }
-        const float s = warp_transpose_sum32(v, lane);
-        if (col0 + lane < p.N) red_add_f32(p.col_sum + col0 + lane, s);
-      }
-    }
-  }
+// ---- TMA store / reduce of a staged chunk, and bulk-group bookkeeping
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
 }
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// Swizzled 16-byte chunk offset inside a staged chunk: bf16 32x32 (64 B rows, SWIZZLE_64B) or
+// fp32 32x32 (128 B rows, SWIZZLE_128B) -- the layouts TMA uses for the matching tensor maps.
+template <bool F32>
+__device__ __forceinline__ uint32_t stage_off(int row, int chunk16) {
+  if constexpr (F32) return row * 128 + ((chunk16 ^ (row & 7)) << 4);
+  else return row * 64 + ((chunk16 ^ ((row >> 1) & 3)) << 4);
+}
+
+struct EpiMaps {
+  CUtensorMap c, z, r;
+};
 
 template <int BN, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TileInfo ti,
-                   EpiParams ep) {
-  using C = Cfg<BN>;
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ EpiMaps maps, TileInfo ti, EpiParams ep) {
+  using C = Cfg<BN, EPI>;
+  using E = EpiCfg<EPI>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * C::A_BYTES;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
+  uint8_t* sEpi = smem + STAGES * C::STAGE_BYTES;  // 1 KB aligned (stage sizes are multiples of 1 KB)
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(sEpi + E::BYTES);
   uint64_t* empty_bar = full_bar + STAGES;
   uint64_t* tfull_bar = empty_bar + STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* aux_bar = tempty_bar + 2;  // [kEpiWarps][2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + 2 * kEpiWarps);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -171,8 +140,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull_bar[b], 1);
-      mbar_init(&tempty_bar[b], 4);
+      mbar_init(&tempty_bar[b], kEpiWarps);
     }
+    for (int i = 0; i < 2 * kEpiWarps; ++i) mbar_init(&aux_bar[i], 1);
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -262,31 +232,129 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ===================== epilogue warps =====================
+    const int ew = warp - 2;
     const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int half = ew >> 2;
+    uint8_t* my = sEpi + ew * E::WARP_BYTES;
+    uint8_t* obuf = my;                              // [2][NOUT][CHUNK]
+    uint8_t* abuf = my + 2 * E::NOUT * E::CHUNK;     // [2][CHUNK]  (AUX only)
+    uint64_t* abar = aux_bar + 2 * ew;
+    uint32_t aux_phase = 0;  // bit b = expected parity of aux buffer b
+    int ob = 0, ab = 0;
     int it = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
       int mb, nb, kb0, kb1;
       decode_tile(ti, t, mb, nb, kb0, kb1);
       const int buf = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
+      const int row0 = mb * BM + q * 32;
+      const int ncols = min(BN, ep.N - nb * BN);
+      if constexpr (E::AUX) {  // prefetch the residual / pre-activation chunk of the first column block
+        if (lane == 0 && half * 32 < ncols) {
+          mbar_expect_tx(&abar[ab], E::CHUNK);
+          tma_load_2d(abuf + ab * E::CHUNK, &maps.r, &abar[ab], nb * BN + half * 32, row0);
+        }
+      }
       mbar_wait(&tfull_bar[buf], aphase);
       tc_fence_after();
-      const int row = mb * BM + q * 32 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + buf * BN;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = half * 32; c < ncols; c += 64) {
+        const int col0 = nb * BN + c;
         uint32_t r[32];
         tmem_ld32(taddr + c, r);
+        if constexpr (E::AUX) {
+          if (lane == 0 && c + 64 < ncols) {  // prefetch the next chunk into the other buffer
+            fence_async_smem();
+            mbar_expect_tx(&abar[ab ^ 1], E::CHUNK);
+            tma_load_2d(abuf + (ab ^ 1) * E::CHUNK, &maps.r, &abar[ab ^ 1], col0 + 64, row0);
+          }
+        }
         tmem_ld_wait();
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        if (nb * BN + c < ep.N) epilogue_chunk<EPI>(ep, row, nb * BN + c, v, lane);
+        if constexpr (EPI != ESM_EPI_F32_ACC && EPI != ESM_EPI_DGELU) {
+          if (ep.bias != nullptr) {
+            if (col0 + 32 <= ep.N) {
+              const float4* b4 = reinterpret_cast<const float4*>(ep.bias + col0);  // 1 KB aligned groups
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const float4 bb = __ldg(b4 + j);
+                v[4 * j] += bb.x;
+                v[4 * j + 1] += bb.y;
+                v[4 * j + 2] += bb.z;
+                v[4 * j + 3] += bb.w;
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] += (col0 + j < ep.N) ? __ldg(ep.bias + col0 + j) : 0.f;
+            }
+          }
+        }
+        if constexpr (E::AUX) {
+          mbar_wait(&abar[ab], (aux_phase >> ab) & 1u);
+          aux_phase ^= 1u << ab;
+          const uint8_t* a = abuf + ab * E::CHUNK;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            float rv[8];
+            load_vec(reinterpret_cast<const __nv_bfloat16*>(a + stage_off<false>(lane, k)), rv);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              if constexpr (EPI == ESM_EPI_RESID) v[8 * k + e] += rv[e];
+              else v[8 * k + e] *= gelu_grad_f(rv[e]);
+            }
+          }
+          __syncwarp();
+          ab ^= 1;
+        }
+        // stage the outputs (wait until the TMA store that last read this buffer is done)
+        if (lane == 0) bulk_wait_read<1>();
+        __syncwarp();
+        uint8_t* o = obuf + ob * E::NOUT * E::CHUNK;
+        if constexpr (EPI == ESM_EPI_F32_ACC) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            *reinterpret_cast<float4*>(o + stage_off<true>(lane, k)) =
+                make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+        } else {
+          if constexpr (EPI == ESM_EPI_GELU) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              store_vec(reinterpret_cast<__nv_bfloat16*>(o + E::CHUNK + stage_off<false>(lane, k)), v + 8 * k);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = gelu_f(v[j]);
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            store_vec(reinterpret_cast<__nv_bfloat16*>(o + stage_off<false>(lane, k)), v + 8 * k);
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (EPI == ESM_EPI_F32_ACC) {
+            tma_reduce_add_2d(&maps.c, o, col0, row0);
+          } else {
+            tma_store_2d(&maps.c, o, col0, row0);
+            if constexpr (EPI == ESM_EPI_GELU) tma_store_2d(&maps.z, o + E::CHUNK, col0, row0);
+          }
+          bulk_commit();
+        }
+        ob ^= 1;
+        if constexpr (EPI == ESM_EPI_DGELU) {
+          if (ep.col_sum != nullptr) {  // rows >= M are exactly 0 (TMA zero-filled A)
+            const float s = warp_transpose_sum32(v, lane);
+            if (col0 + lane < ep.N) red_add_f32(ep.col_sum + col0 + lane, s);
+          }
+        }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty_bar[buf]);
     }
+    if (lane == 0) bulk_wait_all();
+    __syncwarp();
   }
   __syncthreads();
   if (warp == 1) {
@@ -313,21 +381,22 @@ static PFN_encodeTiled get_encode() {
   return fn;
 }
 
-// 2D bf16 tensor map over a row-major [outer, inner] matrix with row stride ld (elements).
+// 2D tensor map over a row-major [outer, inner] matrix with row stride ld (elements).
 static int make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, int64_t ld, uint32_t box_inner,
-                    uint32_t box_outer) {
+                    uint32_t box_outer, bool f32 = false, CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B) {
   PFN_encodeTiled enc = get_encode();
   if (!enc) {
     set_last_error("cuTensorMapEncodeTiled unavailable");
     return ESM_EDRIVER;
   }
+  const int es = f32 ? 4 : 2;
   cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * es};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = enc(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_last_error("cuTensorMapEncodeTiled failed (%d): inner=%llu outer=%llu ld=%lld box=%u,%u", (int)r,
                    (unsigned long long)inner, (unsigned long long)outer, (long long)ld, box_inner, box_outer);
@@ -349,8 +418,10 @@ static int num_sms() {
 
 template <int BN, bool A_MN, bool B_MN, int EPI>
 static int launch(const esm_gemm_args& a, cudaStream_t st) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, EPI>;
   CUtensorMap tA, tB;
+  EpiMaps maps;
+  memset(&maps, 0, sizeof(maps));
   int rc;
   if (!A_MN)
     rc = make_map(&tA, a.A, a.K, a.M, a.lda, BK, BM);
@@ -361,6 +432,17 @@ static int launch(const esm_gemm_args& a, cudaStream_t st) {
     rc = make_map(&tB, a.B, a.K, a.N, a.ldb, BK, BN);
   else
     rc = make_map(&tB, a.B, a.N, a.K, a.ldb, 64, BK);
+  if (rc) return rc;
+  // epilogue maps: 32x32 chunks; bf16 -> SWIZZLE_64B (64 B rows), fp32 -> SWIZZLE_128B (128 B rows)
+  if (EPI == ESM_EPI_F32_ACC) {
+    rc = make_map(&maps.c, a.C, a.N, a.M, a.ldc, 32, 32, true, CU_TENSOR_MAP_SWIZZLE_128B);
+  } else {
+    rc = make_map(&maps.c, a.C, a.N, a.M, a.ldc, 32, 32, false, CU_TENSOR_MAP_SWIZZLE_64B);
+    if (!rc && EPI == ESM_EPI_GELU)
+      rc = make_map(&maps.z, a.aux_out, a.N, a.M, a.ld_aux_out, 32, 32, false, CU_TENSOR_MAP_SWIZZLE_64B);
+    if (!rc && (EPI == ESM_EPI_RESID || EPI == ESM_EPI_DGELU))
+      rc = make_map(&maps.r, a.aux_in, a.N, a.M, a.ld_aux_in, 32, 32, false, CU_TENSOR_MAP_SWIZZLE_64B);
+  }
   if (rc) return rc;
 
   TileInfo ti;
@@ -392,7 +474,7 @@ static int launch(const esm_gemm_args& a, cudaStream_t st) {
   }
   const int total = tiles * splits;
   const int grid = total < sms ? total : sms;
-  kern<<<grid, kThreads, C::SMEM, st>>>(tA, tB, ti, ep);
+  kern<<<grid, kThreads, C::SMEM, st>>>(tA, tB, maps, ti, ep);
   ESM_LAUNCH_RET();
 }
 
@@ -446,6 +528,8 @@ int gemm_bf16(const esm_gemm_args& a, cudaStream_t st) {
     return dispatch_bn<true, true, ESM_EPI_F32_ACC>(a, bn, st);
   }
   ESM_CHECK_ARG(!amn, "gemm: activation-output GEMMs expect K-major A");
+  ESM_CHECK_ARG(!a.aux_in || (((uintptr_t)a.aux_in & 15) == 0 && a.ld_aux_in % 8 == 0), "gemm: aux_in alignment");
+  ESM_CHECK_ARG(!a.aux_out || (((uintptr_t)a.aux_out & 15) == 0 && a.ld_aux_out % 8 == 0), "gemm: aux_out alignment");
   ESM_CHECK_ARG(a.ldc % 8 == 0 && ((uintptr_t)a.C & 15) == 0, "gemm: C must be 16B aligned, ldc %% 8 == 0");
   if (!bmn) {
     const int bn = pick_bn_kmajor(a.N);

@@ -1,0 +1,103 @@
+"""Per-kernel microbenchmarks (CUDA events) on the ESM-2 shapes: attention fwd/bwd and GEMMs.
+
+    python scripts/microbench.py attn [--legacy]
+    python scripts/microbench.py gemm
+"""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2411_10548_b200 import _lib  # noqa: E402
+from paper_2411_10548_b200._lib import EPI_F32_ACC, EPI_GELU, EPI_RESID, EPI_STORE, ESM_BF16  # noqa: E402
+
+
+def timeit(fn, iters=10, warm=3, graph=True):
+    """GPU time per call; launches are captured in a CUDA graph so host launch cost is excluded."""
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    if graph:
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                for _ in range(iters):
+                    fn()
+        torch.cuda.current_stream().wait_stream(s)
+        g.replay()
+        torch.cuda.synchronize()
+        run = g.replay
+    else:
+        def run():
+            for _ in range(iters):
+                fn()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    run()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / iters
+
+
+def cur():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def attn():
+    for (B, nh, S, dh) in [(32, 20, 1024, 24), (16, 20, 1024, 64), (8, 20, 512, 16), (4, 40, 1024, 64)]:
+        q = (torch.randn(B, nh, S, dh, device="cuda") * 0.5).bfloat16()
+        k = (torch.randn(B, nh, S, dh, device="cuda") * 0.5).bfloat16()
+        v = torch.randn(B, nh, S, dh, device="cuda").bfloat16()
+        am = torch.ones(B, S, dtype=torch.int32, device="cuda")
+        o = torch.empty(B * S, nh * dh, device="cuda", dtype=torch.bfloat16)
+        lse = torch.empty(B, nh, S, device="cuda")
+        do = torch.randn_like(o)
+        dq = torch.empty(B, nh, S, dh, device="cuda")
+        dk, dv = torch.empty_like(q), torch.empty_like(q)
+        delta = torch.empty(B, nh, S, device="cuda")
+        f = lambda: _lib.call("esm_attn_fwd", ESM_BF16, q.data_ptr(), k.data_ptr(), v.data_ptr(), am.data_ptr(),  # noqa
+                              o.data_ptr(), lse.data_ptr(), B, nh, S, dh, cur())
+        g = lambda: _lib.call("esm_attn_bwd", ESM_BF16, q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),  # noqa
+                              do.data_ptr(), lse.data_ptr(), am.data_ptr(), delta.data_ptr(), dq.data_ptr(),
+                              dk.data_ptr(), dv.data_ptr(), B, nh, S, dh, cur())
+        tf, tb = timeit(f), timeit(g)
+        fl = 4.0 * B * nh * S * S * dh
+        print(f"attn B={B} nh={nh} S={S} dh={dh}: fwd {tf:.3f} ms ({fl / tf / 1e9:.0f} TF/s)  "
+              f"bwd {tb:.3f} ms ({2.5 * fl / tb / 1e9:.0f} TF/s)", flush=True)
+
+
+def gemm():
+    T = 32768
+    for (name, M, N, K, amn, bmn, epi) in [
+        ("35M qkv fwd", T, 1440, 480, 0, 0, EPI_STORE), ("35M fc1 fwd", T, 1920, 480, 0, 0, EPI_GELU),
+        ("35M fc2 fwd", T, 480, 1920, 0, 0, EPI_RESID), ("35M fc2 dgrad", T, 1920, 480, 0, 1, EPI_STORE),
+        ("35M fc1 dgrad", T, 480, 1920, 0, 1, EPI_STORE), ("35M fc1 wgrad", 1920, 480, T, 1, 1, EPI_F32_ACC),
+        ("35M fc2 wgrad", 480, 1920, T, 1, 1, EPI_F32_ACC),
+        ("650M fc1 fwd", 16384, 5120, 1280, 0, 0, EPI_GELU), ("650M fc2 fwd", 16384, 1280, 5120, 0, 0, EPI_RESID),
+        ("650M fc2 dgrad", 16384, 5120, 1280, 0, 1, EPI_STORE), ("650M fc1 wgrad", 5120, 1280, 16384, 1, 1, EPI_F32_ACC),
+        ("8192^3 store", 8192, 8192, 8192, 0, 0, EPI_STORE)]:
+        if len(sys.argv) > 2 and sys.argv[2] not in name:
+            continue
+        A = torch.randn((K, M) if amn else (M, K), device="cuda").bfloat16()
+        Bm = torch.randn((K, N) if bmn else (N, K), device="cuda").bfloat16()
+        if epi == EPI_F32_ACC:
+            C = torch.zeros(M, N, device="cuda")
+        else:
+            C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        aux = torch.empty(M, N, device="cuda", dtype=torch.bfloat16) if epi in (EPI_GELU, EPI_RESID) else None
+        bias = torch.zeros(N, device="cuda")
+        kw = dict(dtype=ESM_BF16, M=M, N=N, K=K, A=A.data_ptr(), lda=M if amn else K, a_mn_major=amn,
+                  B=Bm.data_ptr(), ldb=N if bmn else K, b_mn_major=bmn, C=C.data_ptr(), ldc=N, epilogue=epi,
+                  bias=bias.data_ptr() if epi != EPI_F32_ACC else None,
+                  aux_in=aux.data_ptr() if epi == EPI_RESID else None, ld_aux_in=N,
+                  aux_out=aux.data_ptr() if epi == EPI_GELU else None, ld_aux_out=N)
+        t = timeit(lambda: _lib.gemm_call(cur(), **kw), graph=os.environ.get("MB_NOGRAPH") is None)
+        print(f"gemm {name:16s} M={M} N={N} K={K}: {t:.3f} ms  {2.0 * M * N * K / t / 1e9:.0f} TF/s", flush=True)
+
+
+if __name__ == "__main__":
+    what = sys.argv[1] if len(sys.argv) > 1 else "attn"
+    {"attn": attn, "gemm": gemm}[what]()
