@@ -686,6 +686,8 @@ __global__ void __launch_bounds__(64) bwd_dkv_f32_kernel(const float* __restrict
 namespace esm {
 int attn_fwd_tc(const void* q, const void* k, const void* v, const int32_t* km, void* o, float* lse, int B, int nh,
                 int S, int dh, cudaStream_t st);
+int attn_bwd_tc(const void* q, const void* k, const void* v, const void* dout, const float* lse, const float* delta,
+                const int32_t* km, float* dq, void* dk, void* dv, int B, int nh, int S, int dh, cudaStream_t st);
 static int legacy_attention() {
   static int v = -1;
   if (v < 0) {
@@ -739,6 +741,12 @@ extern "C" int esm_attn_bwd(int dtype, const void* q, const void* k, const void*
     attn::delta_kernel<__nv_bfloat16><<<dgrid, 256, 0, st>>>((const __nv_bfloat16*)o, (const __nv_bfloat16*)dout,
                                                              delta, T_, S, nh, dh);
     cudaMemsetAsync(dq, 0, sizeof(float) * T_ * nh * dh, st);
+    // tcgen05 backward wins for dh = 64 (650M / 3B); the mma.sync kernel is faster for small heads
+    if (!legacy_attention() && S % 4 == 0 && dh == 64) {
+      const int rc = attn_bwd_tc(q, k, v, dout, lse, delta, key_mask, dq, dk, dv, B, nh, S, dh, st);
+      if (rc) return rc;
+      ESM_LAUNCH_RET();
+    }
     auto* Q = (const __nv_bfloat16*)q;
     auto* K = (const __nv_bfloat16*)k;
     auto* V = (const __nv_bfloat16*)v;

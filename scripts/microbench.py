@@ -47,7 +47,10 @@ def cur():
 
 
 def attn():
-    for (B, nh, S, dh) in [(32, 20, 1024, 24), (16, 20, 1024, 64), (8, 20, 512, 16), (4, 40, 1024, 64)]:
+    shapes = [(32, 20, 1024, 24), (16, 20, 1024, 64), (8, 20, 512, 16), (4, 40, 1024, 64)]
+    if len(sys.argv) > 2:
+        shapes = [tuple(int(x) for x in sys.argv[2].split(","))]
+    for (B, nh, S, dh) in shapes:
         q = (torch.randn(B, nh, S, dh, device="cuda") * 0.5).bfloat16()
         k = (torch.randn(B, nh, S, dh, device="cuda") * 0.5).bfloat16()
         v = torch.randn(B, nh, S, dh, device="cuda").bfloat16()
@@ -63,7 +66,8 @@ def attn():
         g = lambda: _lib.call("esm_attn_bwd", ESM_BF16, q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),  # noqa
                               do.data_ptr(), lse.data_ptr(), am.data_ptr(), delta.data_ptr(), dq.data_ptr(),
                               dk.data_ptr(), dv.data_ptr(), B, nh, S, dh, cur())
-        tf, tb = timeit(f), timeit(g)
+        ng = os.environ.get("MB_NOGRAPH") is None
+        tf, tb = timeit(f, graph=ng), timeit(g, graph=ng)
         fl = 4.0 * B * nh * S * S * dh
         print(f"attn B={B} nh={nh} S={S} dh={dh}: fwd {tf:.3f} ms ({fl / tf / 1e9:.0f} TF/s)  "
               f"bwd {tb:.3f} ms ({2.5 * fl / tb / 1e9:.0f} TF/s)", flush=True)
