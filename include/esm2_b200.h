@@ -46,7 +46,8 @@ enum {
   ESM_EPI_GELU = 1,       /* Z = acc + bias; C = gelu(Z)  (Z -> aux_out)  act dtype    HF:406-414, 57-61     */
   ESM_EPI_RESID = 2,      /* C = acc + bias + R           (R = aux_in)    act dtype    HF:365-375, 417-427   */
   ESM_EPI_DGELU = 3,      /* C = acc * gelu'(Z) (Z = aux_in); colsum(C) -> col_sum     backward of HF:411-414 */
-  ESM_EPI_F32_ACC = 4     /* C(fp32) += acc  (weight gradients; split-K safe)                               */
+  ESM_EPI_F32_ACC = 4,    /* C(fp32) += acc  (weight gradients; split-K safe)                               */
+  ESM_EPI_QKV_ROPE = 5    /* acc + bias -> q*scale, RoPE(q), RoPE(k), v scattered to [B,nh,S,dh]  HF:318-344 (bf16) */
 };
 
 typedef struct esm_gemm_args {
@@ -61,6 +62,12 @@ typedef struct esm_gemm_args {
   void* aux_out; int64_t ld_aux_out;        /* GELU pre-activation Z output                        */
   float* col_sum;            /* [N] fp32 accumulated column sums (bias grad) or NULL               */
   int split_k;               /* ESM_EPI_F32_ACC only; 0 = auto                                     */
+  /* ESM_EPI_QKV_ROPE only: N = 3*n_heads*head_dim, rows t = b*seq_len + s */
+  const float* rope_cos;     /* [seq_len, head_dim/2] fp32 */
+  const float* rope_sin;
+  void* q_out; void* k_out; void* v_out;   /* [B, n_heads, seq_len, head_dim] */
+  int seq_len, n_heads, head_dim;
+  float q_scale;
 } esm_gemm_args;
 
 /* ---------------- library ---------------- */

@@ -12,7 +12,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libesm2b200.so")
 
 ESM_F32, ESM_BF16 = 0, 1
-EPI_STORE, EPI_GELU, EPI_RESID, EPI_DGELU, EPI_F32_ACC = 0, 1, 2, 3, 4
+EPI_STORE, EPI_GELU, EPI_RESID, EPI_DGELU, EPI_F32_ACC, EPI_QKV_ROPE = 0, 1, 2, 3, 4, 5
 
 EXPORTS = [
     "esm_version", "esm_last_error", "esm_device_sm_count", "esm_tokenize", "esm_mlm_mask", "esm_embed_fwd",
@@ -37,6 +37,10 @@ class GemmArgs(ctypes.Structure):
         ("aux_out", ctypes.c_void_p), ("ld_aux_out", ctypes.c_int64),
         ("col_sum", ctypes.c_void_p),
         ("split_k", ctypes.c_int),
+        ("rope_cos", ctypes.c_void_p), ("rope_sin", ctypes.c_void_p),
+        ("q_out", ctypes.c_void_p), ("k_out", ctypes.c_void_p), ("v_out", ctypes.c_void_p),
+        ("seq_len", ctypes.c_int), ("n_heads", ctypes.c_int), ("head_dim", ctypes.c_int),
+        ("q_scale", ctypes.c_float),
     ]
 
 

@@ -30,6 +30,12 @@ struct EpiParams {
   void* aux_out;
   int64_t ld_aux_out;
   float* col_sum;
+  // QKV + RoPE epilogue
+  const float* rope_cos;
+  const float* rope_sin;
+  __nv_bfloat16* qkv_out[3];
+  int seq_len, n_heads, head_dim;
+  float q_scale;
 };
 
 // ============================================================================
@@ -45,11 +51,12 @@ constexpr int kThreads = 64 + 32 * kEpiWarps;  // warp0 TMA, warp1 MMA (+TMEM al
 // Epilogue staging per warp: a 32x32 output chunk in swizzled smem, written to HBM by TMA.
 template <int EPI>
 struct EpiCfg {
+  static constexpr bool QKV = EPI >= 16;  // ESM_EPI_QKV_ROPE specialised per head dim: EPI = 16 + dh
   static constexpr bool F32 = EPI == ESM_EPI_F32_ACC;
   static constexpr int CHUNK = F32 ? 32 * 32 * 4 : 32 * 32 * 2;  // bytes per 32x32 chunk
   static constexpr int NOUT = EPI == ESM_EPI_GELU ? 2 : 1;        // outputs per chunk (GELU: C and Z)
   static constexpr bool AUX = EPI == ESM_EPI_RESID || EPI == ESM_EPI_DGELU;
-  static constexpr int WARP_BYTES = 2 * NOUT * CHUNK + (AUX ? 2 * CHUNK : 0);
+  static constexpr int WARP_BYTES = QKV ? 0 : 2 * NOUT * CHUNK + (AUX ? 2 * CHUNK : 0);
   static constexpr int BYTES = kEpiWarps * WARP_BYTES;
 };
 
@@ -258,6 +265,61 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull_bar[buf], aphase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + buf * BN;
+      if constexpr (E::QKV) {
+        // thread = token row; one head (DH columns) at a time: bias, q-scale, RoPE, scatter
+        constexpr int DH = EPI - 16, HALF = DH / 2;
+        const int t = row0 + lane;
+        const int Hd = ep.n_heads * DH;
+        const int sq = t % ep.seq_len, bb = t / ep.seq_len;
+        for (int hh = half; hh * DH < ncols; hh += 2) {
+          uint32_t u[DH];
+#pragma unroll
+          for (int j = 0; j < DH; j += 8)
+            tmem_ld8(taddr + hh * DH + j, u[j], u[j + 1], u[j + 2], u[j + 3], u[j + 4], u[j + 5], u[j + 6], u[j + 7]);
+          tmem_ld_wait();
+          float x[DH];
+#pragma unroll
+          for (int j = 0; j < DH; ++j) x[j] = __uint_as_float(u[j]);
+          const int gcol = nb * BN + hh * DH;
+          const int part = gcol / Hd, head = (gcol - part * Hd) / DH;
+          const float4* b4 = reinterpret_cast<const float4*>(ep.bias + gcol);
+#pragma unroll
+          for (int j = 0; j < DH / 4; ++j) {
+            const float4 bb4 = __ldg(b4 + j);
+            x[4 * j] += bb4.x;
+            x[4 * j + 1] += bb4.y;
+            x[4 * j + 2] += bb4.z;
+            x[4 * j + 3] += bb4.w;
+          }
+          if (part < 2) {
+            const float sc = part == 0 ? ep.q_scale : 1.0f;
+            const float4* c4 = reinterpret_cast<const float4*>(ep.rope_cos + (int64_t)sq * HALF);
+            const float4* s4 = reinterpret_cast<const float4*>(ep.rope_sin + (int64_t)sq * HALF);
+#pragma unroll
+            for (int j = 0; j < HALF / 4; ++j) {
+              const float4 cc = __ldg(c4 + j), ss = __ldg(s4 + j);
+              const float cv[4] = {cc.x, cc.y, cc.z, cc.w}, sv[4] = {ss.x, ss.y, ss.z, ss.w};
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int jj = 4 * j + u;
+                const float a = x[jj] * sc, b2 = x[jj + HALF] * sc;
+                x[jj] = a * cv[u] - b2 * sv[u];
+                x[jj + HALF] = b2 * cv[u] + a * sv[u];
+              }
+            }
+          }
+          if (t < ep.M) {
+            __nv_bfloat16* base = part == 0 ? ep.qkv_out[0] : (part == 1 ? ep.qkv_out[1] : ep.qkv_out[2]);
+            __nv_bfloat16* dst = base + (((int64_t)bb * ep.n_heads + head) * ep.seq_len + sq) * DH;
+#pragma unroll
+            for (int j = 0; j < DH; j += 8) store_vec(dst + j, x + j);
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty_bar[buf]);
+        continue;
+      }
 #pragma unroll 1
       for (int c = half * 32; c < ncols; c += 64) {
         const int col0 = nb * BN + c;
@@ -434,7 +496,9 @@ static int launch(const esm_gemm_args& a, cudaStream_t st) {
     rc = make_map(&tB, a.B, a.N, a.K, a.ldb, 64, BK);
   if (rc) return rc;
   // epilogue maps: 32x32 chunks; bf16 -> SWIZZLE_64B (64 B rows), fp32 -> SWIZZLE_128B (128 B rows)
-  if (EPI == ESM_EPI_F32_ACC) {
+  if (EPI >= 16) {
+    // QKV epilogue stores directly (no TMA maps)
+  } else if (EPI == ESM_EPI_F32_ACC) {
     rc = make_map(&maps.c, a.C, a.N, a.M, a.ldc, 32, 32, true, CU_TENSOR_MAP_SWIZZLE_128B);
   } else {
     rc = make_map(&maps.c, a.C, a.N, a.M, a.ldc, 32, 32, false, CU_TENSOR_MAP_SWIZZLE_64B);
@@ -455,17 +519,29 @@ static int launch(const esm_gemm_args& a, cudaStream_t st) {
   if (EPI == ESM_EPI_F32_ACC) {
     if (a.split_k > 0) {
       splits = a.split_k;
-    } else if (tiles < sms) {
-      splits = (sms + tiles - 1) / tiles;  // ~one wave of work units
-      const int max_splits = ti.kb_total / 4 > 0 ? ti.kb_total / 4 : 1;  // keep >= 4 k-blocks per unit
-      if (splits > max_splits) splits = max_splits;
+    } else {
+      // minimise (waves of work units) / splits, i.e. the per-SM k-block count, with >= 8 k-blocks per unit
+      const int max_splits = ti.kb_total / 8 > 0 ? ti.kb_total / 8 : 1;
+      double best = 1e30;
+      for (int sp = 1; sp <= max_splits && sp <= 64; ++sp) {
+        const int units = tiles * sp;
+        const double waves = (double)((units + sms - 1) / sms);
+        const double cost = waves / sp * (1.0 + 0.01 * sp);  // small penalty for extra reduce traffic
+        if (cost < best - 1e-12) {
+          best = cost;
+          splits = sp;
+        }
+      }
     }
   }
   ti.kb_per_split = (ti.kb_total + splits - 1) / splits;
   splits = (ti.kb_total + ti.kb_per_split - 1) / ti.kb_per_split;
   ti.splits = splits;
 
-  EpiParams ep{a.M, a.N, a.C, a.ldc, a.bias, a.aux_in, a.ld_aux_in, a.aux_out, a.ld_aux_out, a.col_sum};
+  EpiParams ep{a.M, a.N, a.C, a.ldc, a.bias, a.aux_in, a.ld_aux_in, a.aux_out, a.ld_aux_out, a.col_sum,
+               a.rope_cos, a.rope_sin,
+               {(__nv_bfloat16*)a.q_out, (__nv_bfloat16*)a.k_out, (__nv_bfloat16*)a.v_out},
+               a.seq_len, a.n_heads, a.head_dim, a.q_scale};
   auto kern = gemm_tc_kernel<BN, A_MN, B_MN, EPI>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -530,7 +606,20 @@ int gemm_bf16(const esm_gemm_args& a, cudaStream_t st) {
   ESM_CHECK_ARG(!amn, "gemm: activation-output GEMMs expect K-major A");
   ESM_CHECK_ARG(!a.aux_in || (((uintptr_t)a.aux_in & 15) == 0 && a.ld_aux_in % 8 == 0), "gemm: aux_in alignment");
   ESM_CHECK_ARG(!a.aux_out || (((uintptr_t)a.aux_out & 15) == 0 && a.ld_aux_out % 8 == 0), "gemm: aux_out alignment");
-  ESM_CHECK_ARG(a.ldc % 8 == 0 && ((uintptr_t)a.C & 15) == 0, "gemm: C must be 16B aligned, ldc %% 8 == 0");
+  ESM_CHECK_ARG(a.epilogue == ESM_EPI_QKV_ROPE || (a.ldc % 8 == 0 && ((uintptr_t)a.C & 15) == 0),
+                "gemm: C must be 16B aligned, ldc %% 8 == 0");
+  if (a.epilogue == ESM_EPI_QKV_ROPE) {
+    ESM_CHECK_ARG(!bmn && a.bias && a.rope_cos && a.rope_sin && a.q_out && a.k_out && a.v_out,
+                  "gemm: QKV_ROPE needs bias, rope tables and q/k/v outputs");
+    ESM_CHECK_ARG(a.N == 3 * a.n_heads * a.head_dim && a.M % a.seq_len == 0, "gemm: QKV_ROPE shape");
+    switch (a.head_dim) {
+      case 16: return launch<256, false, false, 16 + 16>(a, st);
+      case 24: return launch<240, false, false, 16 + 24>(a, st);
+      case 32: return launch<256, false, false, 16 + 32>(a, st);
+      case 64: return launch<256, false, false, 16 + 64>(a, st);
+      default: set_last_error("gemm: QKV_ROPE head_dim %d unsupported", a.head_dim); return ESM_ENOTSUP;
+    }
+  }
   if (!bmn) {
     const int bn = pick_bn_kmajor(a.N);
     switch (a.epilogue) {
@@ -659,7 +748,8 @@ extern "C" int esm_gemm(const esm_gemm_args* args, esm_stream_t stream) {
   ESM_CHECK_ARG(args != nullptr, "esm_gemm: null args");
   const esm_gemm_args& a = *args;
   ESM_CHECK_ARG(a.M > 0 && a.N > 0 && a.K > 0, "esm_gemm: bad shape %d %d %d", a.M, a.N, a.K);
-  ESM_CHECK_ARG(a.epilogue >= 0 && a.epilogue <= ESM_EPI_F32_ACC, "esm_gemm: bad epilogue");
+  ESM_CHECK_ARG(a.epilogue >= 0 && a.epilogue <= ESM_EPI_QKV_ROPE, "esm_gemm: bad epilogue");
+  ESM_CHECK_ARG(a.epilogue != ESM_EPI_QKV_ROPE || a.dtype == ESM_BF16, "esm_gemm: QKV_ROPE is bf16-only");
   ESM_CHECK_ARG(a.epilogue != ESM_EPI_RESID || a.aux_in, "esm_gemm: RESID needs aux_in");
   ESM_CHECK_ARG(a.epilogue != ESM_EPI_DGELU || a.aux_in, "esm_gemm: DGELU needs aux_in");
   ESM_CHECK_ARG(a.epilogue != ESM_EPI_GELU || a.aux_out, "esm_gemm: GELU needs aux_out");

@@ -33,7 +33,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import EPI_DGELU, EPI_F32_ACC, EPI_GELU, EPI_RESID, EPI_STORE, ESM_BF16, ESM_F32
+from ._lib import EPI_DGELU, EPI_F32_ACC, EPI_GELU, EPI_QKV_ROPE, EPI_RESID, EPI_STORE, ESM_BF16, ESM_F32
 from .config import EsmConfig
 
 ALIGN = 256  # elements; also the AdamW weight-decay chunk size
@@ -344,6 +344,20 @@ class EsmForMaskedLM:
                    bias=self._p32(bias_key) if bias_key else None, aux_in=aux_in, ld_aux_in=out_f,
                    aux_out=aux_out, ld_aux_out=out_f)
 
+    def _qkv_rope_gemm(self, ly, p, ws, T, H, nh, dh, S, qs):
+        W = self._w(p + "attention.self.qkv.weight", (3 * H, H))
+        t = self.timer
+        if t is not None:
+            t.begin("gemm_fwd")
+        _lib.gemm_call(self._stream(), dtype=self.kdt, M=T, N=3 * H, K=H, A=ly.h1.data_ptr(), lda=H, a_mn_major=0,
+                       B=W.data_ptr(), ldb=H, b_mn_major=0, C=None, ldc=0, epilogue=EPI_QKV_ROPE,
+                       bias=self._p32(p + "attention.self.qkv.bias").data_ptr(), rope_cos=ws.cos.data_ptr(),
+                       rope_sin=ws.sin.data_ptr(), q_out=ly.q.data_ptr(), k_out=ly.k.data_ptr(),
+                       v_out=ly.v.data_ptr(), seq_len=S, n_heads=nh, head_dim=dh, q_scale=qs)
+        if t is not None:
+            t.end(2.0 * T * 3 * H * H, 0.0)
+        self.launches += 1
+
     def linear_dgrad(self, dy, wkey, out_f, in_f, dX, epi=EPI_STORE, aux_in=None, col_sum=None):
         T = dy.shape[0]
         W = self._w(wkey, (out_f, in_f))
@@ -417,9 +431,13 @@ class EsmForMaskedLM:
             call("esm_layernorm_fwd", kdt, x.data_ptr(), self._p32(p + "attention.LayerNorm.weight").data_ptr(),
                  self._p32(p + "attention.LayerNorm.bias").data_ptr(), ly.h1.data_ptr(), ly.ln1_m.data_ptr(),
                  ly.ln1_r.data_ptr(), T, H, eps, st)
-            self.linear_fwd(ly.h1, p + "attention.self.qkv.weight", 3 * H, H, p + "attention.self.qkv.bias", ws.qkv)
-            call("esm_qkv_rope_fwd", kdt, ws.qkv.data_ptr(), ly.q.data_ptr(), ly.k.data_ptr(), ly.v.data_ptr(),
-                 ws.cos.data_ptr(), ws.sin.data_ptr(), B, S, nh, dh, qs, st)
+            if kdt == ESM_BF16:  # QKV GEMM with bias, q-scale, RoPE and head re-layout fused in the epilogue
+                self._qkv_rope_gemm(ly, p, ws, T, H, nh, dh, S, qs)
+            else:
+                self.linear_fwd(ly.h1, p + "attention.self.qkv.weight", 3 * H, H, p + "attention.self.qkv.bias",
+                                ws.qkv)
+                call("esm_qkv_rope_fwd", kdt, ws.qkv.data_ptr(), ly.q.data_ptr(), ly.k.data_ptr(), ly.v.data_ptr(),
+                     ws.cos.data_ptr(), ws.sin.data_ptr(), B, S, nh, dh, qs, st)
             call("esm_attn_fwd", kdt, ly.q.data_ptr(), ly.k.data_ptr(), ly.v.data_ptr(), ws.am.data_ptr(),
                  ly.o.data_ptr(), ly.lse.data_ptr(), B, nh, S, dh, st, flops=4.0 * B * nh * S * S * dh)
             self.linear_fwd(ly.o, p + "attention.output.dense.weight", H, H, p + "attention.output.dense.bias",

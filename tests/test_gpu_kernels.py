@@ -10,8 +10,8 @@ import torch
 pytestmark = pytest.mark.gpu
 
 from paper_2411_10548_b200 import _lib  # noqa: E402
-from paper_2411_10548_b200._lib import (EPI_DGELU, EPI_F32_ACC, EPI_GELU, EPI_RESID, EPI_STORE, ESM_BF16,  # noqa: E402
-                                        ESM_F32)
+from paper_2411_10548_b200._lib import (EPI_DGELU, EPI_F32_ACC, EPI_GELU, EPI_QKV_ROPE, EPI_RESID, EPI_STORE,  # noqa: E402
+                                        ESM_BF16, ESM_F32)
 
 DEV = "cuda"
 
@@ -255,3 +255,33 @@ def test_adamw_matches_oracle():
     want = np.concatenate([P["w"], P["b.bias"]])
     np.testing.assert_allclose(dp.cpu().numpy(), want, rtol=1e-5, atol=1e-6)
     np.testing.assert_allclose(p16.float().cpu().numpy(), want, rtol=1e-2, atol=1e-3)
+
+
+@pytest.mark.parametrize("B,S,nh,dh", [(2, 128, 20, 24), (3, 100, 20, 16), (2, 64, 20, 64), (1, 96, 4, 32)])
+def test_gemm_qkv_rope_epilogue(B, S, nh, dh):
+    """Fused QKV GEMM epilogue (bias, q-scale, RoPE, head scatter) == GEMM + esm_qkv_rope_fwd."""
+    from paper_2411_10548_b200.model import rope_tables
+    torch.manual_seed(5)
+    H = nh * dh
+    T = B * S
+    X = torch.randn(T, H, device=DEV).bfloat16()
+    W = (torch.randn(3 * H, H, device=DEV) * 0.05).bfloat16()
+    b = torch.randn(3 * H, device=DEV)
+    cos, sin = (torch.from_numpy(t).to(DEV) for t in rope_tables(S, dh))
+    qs = dh ** -0.5
+    q, k, v = (torch.empty(B, nh, S, dh, device=DEV, dtype=torch.bfloat16) for _ in range(3))
+    _lib.gemm_call(st(), dtype=ESM_BF16, M=T, N=3 * H, K=H, A=X.data_ptr(), lda=H, a_mn_major=0, B=W.data_ptr(),
+                   ldb=H, b_mn_major=0, C=None, ldc=0, epilogue=EPI_QKV_ROPE, bias=b.data_ptr(),
+                   rope_cos=cos.data_ptr(), rope_sin=sin.data_ptr(), q_out=q.data_ptr(), k_out=k.data_ptr(),
+                   v_out=v.data_ptr(), seq_len=S, n_heads=nh, head_dim=dh, q_scale=qs)
+    qkv = (X.float() @ W.float().t() + b).view(B, S, 3, nh, dh).permute(2, 0, 3, 1, 4)
+    half = dh // 2
+    c = torch.cat([cos, cos], -1)[None, None]
+    s_ = torch.cat([sin, sin], -1)[None, None]
+
+    def rope(x):
+        return x * c + torch.cat([-x[..., half:], x[..., :half]], -1) * s_
+    torch.cuda.synchronize()
+    assert rel(q, rope(qkv[0] * qs)) < 2e-2
+    assert rel(k, rope(qkv[1])) < 2e-2
+    assert rel(v, qkv[2]) < 2e-2
