@@ -741,8 +741,7 @@ extern "C" int esm_attn_bwd(int dtype, const void* q, const void* k, const void*
     attn::delta_kernel<__nv_bfloat16><<<dgrid, 256, 0, st>>>((const __nv_bfloat16*)o, (const __nv_bfloat16*)dout,
                                                              delta, T_, S, nh, dh);
     cudaMemsetAsync(dq, 0, sizeof(float) * T_ * nh * dh, st);
-    // tcgen05 backward wins for dh = 64 (650M / 3B); the mma.sync kernel is faster for small heads
-    if (!legacy_attention() && S % 4 == 0 && dh == 64) {
+    if (!legacy_attention() && S % 4 == 0) {
       const int rc = attn_bwd_tc(q, k, v, dout, lse, delta, key_mask, dq, dk, dv, B, nh, S, dh, st);
       if (rc) return rc;
       ESM_LAUNCH_RET();

@@ -128,8 +128,8 @@ __global__ void __launch_bounds__(kThreads, 2)
   using SH = Shape<DH, BN>;
   constexpr int DP = SH::DP, ROWB = SH::ROWB, ST = SH::STAGES;
   constexpr int QB = SH::Q_BYTES, TB = SH::KV_BYTES;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps shared provenance
   uint8_t* sQ = smem;
   uint8_t* sK = sQ + QB;
   uint8_t* sV = sK + ST * TB;
@@ -360,17 +360,17 @@ __global__ void __launch_bounds__(kThreads, 2)
 }
 
 // ============================================================================ backward
-// CTA = 128 keys of one (batch, head); loop over 128-query blocks.
+// CTA = 128 keys of one (batch, head); loop over 64-query blocks (processed in pairs).
 //   warp 0     TMA: K, V once; Q_i, dO_i tiles + LSE_i / Delta_i (bulk copies) per block (2 stages)
-//   warp 1     MMA: S^T = K Q_i^T, dP^T = V dO_i^T (TMEM); after softmax-bwd:
-//              dV += P^T dO_i, dK += dS^T Q_i (A = P^T / dS^T read from TMEM),
-//              dQ_i = dS K (A = dS^T staged in smem as an M-major operand)
-//   warps 2-9  softmax-bwd, thread = key row, two warps per TMEM lane quarter (64 query columns
-//              each): P^T = exp2(S^T - LSE), dS^T = P^T (dP^T - Delta); P^T / dS^T written back to
-//              TMEM (bf16, over S^T / dP^T), dS^T also to smem
-//   warps 10-13 dQ epilogue, thread = query row: TMEM -> fp32 red.add into dQ (HBM)
+//   warp 1     MMA: S^T = K Q_i^T, dP^T = V dO_i^T into TMEM; after softmax-bwd:
+//              dV += P^T dO_i, dK += dS^T Q_i (A = P^T / dS^T read from TMEM); once per block pair
+//              dQ_pair = dS K (M = 128 queries; A = dS^T of both blocks staged in smem, M-major)
+//   warps 2-5  softmax-bwd, thread = key row: P^T = exp2(S^T - LSE), dS^T = P^T (dP^T - Delta);
+//              P^T / dS^T written back to TMEM (bf16, over S^T / dP^T), dS^T also to smem; they also
+//              drain each pair's dQ (thread = query row) into HBM with fp32 vector reductions.
+// TMEM: S^T 64 + dP^T 64 + dV/dK/dQ 3*DP columns -> 256 for dh <= 32, so two CTAs share an SM.
 // Prefix (right-padded) masks: key blocks past the valid length write zero dK/dV and exit.
-constexpr int kBwdThreads = 448;
+constexpr int kBwdThreads = 320;  // TMA, MMA, 8 softmax-bwd warps
 
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -380,42 +380,53 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 }
 
 template <int DH>
+struct BwdShape {
+  static constexpr int DP = Shape<DH, 64>::DP, ROWB = Shape<DH, 64>::ROWB;
+  static constexpr uint32_t LAYOUT = Shape<DH, 64>::LAYOUT;
+  static constexpr int QB = 64 * ROWB, KB = 128 * ROWB;
+  static constexpr int NBUF = DP <= 32 ? 3 : 2;  // {S^T, dP^T} TMEM buffers (128 columns each)
+  static constexpr int QST = DP <= 32 ? 6 : 4;   // Q / dO / LSE / Delta stages (>= NBUF + 1)
+  static constexpr int DS_BUF = 2 * 128 * 128;  // one pair: [2 query chunks of 64][128 key rows][128 B]
+  static constexpr int SMEM = 2 * DS_BUF + 2 * KB + 2 * QST * QB + 2 * QST * 64 * 4 + 1024 + 256;
+};
+
+// TMEM: {S^T, dP^T} x NBUF buffers (64 columns each) at [0, 128*NBUF); dV, dK, 2 x dQ (DP columns each).
+template <int DH>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
                const int32_t* __restrict__ key_mask, const float* __restrict__ LSE, const float* __restrict__ Delta,
                float* __restrict__ dQ, __nv_bfloat16* __restrict__ dK, __nv_bfloat16* __restrict__ dV, int S,
                int nh) {
-  using SH = Shape<DH, 128>;
-  constexpr int DP = SH::DP, ROWB = SH::ROWB;
-  constexpr int TB = 128 * ROWB;
-  constexpr int DS_BYTES = 2 * 128 * 128;  // dS^T: [2 query chunks of 64][128 key rows][128 B]
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sdS = smem;
-  uint8_t* sK = sdS + DS_BYTES;
-  uint8_t* sV = sK + TB;
-  uint8_t* sQ = sV + TB;       // [2][TB]
-  uint8_t* sdO = sQ + 2 * TB;  // [2][TB]
-  float* sL = reinterpret_cast<float*>(sdO + 2 * TB);  // [2][128]
-  float* sD = sL + 256;                                // [2][128]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sD + 256);
+  using BS = BwdShape<DH>;
+  constexpr int DP = BS::DP, ROWB = BS::ROWB, QB = BS::QB, KB = BS::KB, QST = BS::QST, NBUF = BS::NBUF;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps shared provenance
+  uint8_t* sdS = smem;               // [2][DS_BUF]
+  uint8_t* sK = sdS + 2 * BS::DS_BUF;
+  uint8_t* sV = sK + KB;
+  uint8_t* sQ = sV + KB;             // [QST][QB]
+  uint8_t* sdO = sQ + QST * QB;      // [QST][QB]
+  float* sL = reinterpret_cast<float*>(sdO + QST * QB);  // [QST][64]
+  float* sD = sL + QST * 64;                             // [QST][64]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sD + QST * 64);
   uint64_t* kv_full = bars;
-  uint64_t* qdo_full = bars + 1;   // [2]
-  uint64_t* qdo_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;
-  uint64_t* ds_full = bars + 6;
-  uint64_t* dq_full = bars + 7;
-  uint64_t* dq_empty = bars + 8;
-  uint64_t* dsm_empty = bars + 9;
-  uint64_t* dkv_done = bars + 10;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
+  uint64_t* qdo_full = bars + 1;           // [QST]
+  uint64_t* qdo_empty = qdo_full + QST;    // [QST]
+  uint64_t* s_full = qdo_empty + QST;      // [NBUF]
+  uint64_t* ds_full = s_full + NBUF;       // [NBUF]
+  uint64_t* dq_full = ds_full + NBUF;      // [2]
+  uint64_t* dq_empty = dq_full + 2;        // [2]
+  uint64_t* dsm_empty = dq_empty + 2;      // [2]
+  uint64_t* dkv_done = dsm_empty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dkv_done + 1);
   int* s_len = reinterpret_cast<int*>(tmem_slot + 1);
   int* s_np = s_len + 1;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int bh = blockIdx.y, b = bh / nh, h = bh % nh;
   const int k0 = blockIdx.x * 128;
+
   scan_mask(key_mask, b, S, s_len, s_np);
   const int kv_len = *s_len;
   const bool nonprefix = *s_np != 0;
@@ -429,19 +440,25 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
     return;
   }
-  const int nq = (S + 127) / 128;
+  const int nq = (S + 63) / 64;
+  const int nqe = nq + (nq & 1);  // whole pairs (a trailing virtual block holds no queries)
+  const int npairs = nqe / 2;
 
   if (threadIdx.x == 0) {
     mbar_init(kv_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < QST; ++i) {
       mbar_init(&qdo_full[i], 1);
       mbar_init(&qdo_empty[i], 1);
     }
-    mbar_init(s_full, 1);
-    mbar_init(ds_full, 8);
-    mbar_init(dq_full, 1);
-    mbar_init(dq_empty, 4);
-    mbar_init(dsm_empty, 1);
+    for (int i = 0; i < NBUF; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&ds_full[i], 8);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&dsm_empty[i], 1);
+      mbar_init(&dq_full[i], 1);
+      mbar_init(&dq_empty[i], 8);
+    }
     mbar_init(dkv_done, 1);
     fence_mbar_init();
   }
@@ -450,7 +467,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
-  const uint32_t tS = tbase, tDP = tbase + 128, tdV = tbase + 256, tdK = tbase + 320, tdQ = tbase + 384;
+  const uint32_t tdV = tbase + 128 * NBUF, tdK = tdV + DP, tdQ0 = tdK + DP;  // dQ double buffered: tdQ0 + (p&1)*DP
   const int row0 = bh * S;
 
   if (warp == 0) {
@@ -460,179 +477,186 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tma_prefetch(&tmK);
       tma_prefetch(&tmV);
       tma_prefetch(&tmdO);
-      mbar_expect_tx(kv_full, 2 * TB);
+      mbar_expect_tx(kv_full, 2 * KB);
       tma_load_2d(sK, &tmK, kv_full, 0, row0 + k0);
       tma_load_2d(sV, &tmV, kv_full, 0, row0 + k0);
     }
-    for (int i = 0; i < nq; ++i) {
-      const int st = i & 1;
-      mbar_wait(&qdo_empty[st], ((i >> 1) & 1) ^ 1);
+    for (int i = 0; i < nqe; ++i) {
+      const int st = i % QST, use = i / QST;
+      mbar_wait(&qdo_empty[st], (use & 1) ^ 1);
       if (lane == 0) {
-        const int q0 = i * 128;
-        const int nvalid = min(128, S - q0);
+        const int q0 = i * 64;
+        const int nvalid = max(0, min(64, S - q0));
         const uint32_t vb = (uint32_t)nvalid * 4;
-        mbar_expect_tx(&qdo_full[st], 2 * TB + 2 * vb);
-        tma_load_2d(sQ + st * TB, &tmQ, &qdo_full[st], 0, row0 + q0);
-        tma_load_2d(sdO + st * TB, &tmdO, &qdo_full[st], h * DH, b * S + q0);
-        bulk_load(sL + st * 128, LSE + (int64_t)bh * S + q0, vb, &qdo_full[st]);
-        bulk_load(sD + st * 128, Delta + (int64_t)bh * S + q0, vb, &qdo_full[st]);
+        mbar_expect_tx(&qdo_full[st], 2 * QB + 2 * vb);
+        tma_load_2d(sQ + st * QB, &tmQ, &qdo_full[st], 0, row0 + q0);
+        tma_load_2d(sdO + st * QB, &tmdO, &qdo_full[st], h * DH, b * S + q0);
+        if (vb) {
+          bulk_load(sL + st * 64, LSE + (int64_t)bh * S + q0, vb, &qdo_full[st]);
+          bulk_load(sD + st * 64, Delta + (int64_t)bh * S + q0, vb, &qdo_full[st]);
+        }
       }
       __syncwarp();
     }
   } else if (warp == 1) {
     // ======================= MMA issuer =======================
-    constexpr uint32_t idesc_s = make_idesc_bf16(128, 128, false, false);  // S^T, dP^T
-    constexpr uint32_t idesc_kv = make_idesc_bf16(128, DP, false, true);   // dV, dK (A from TMEM)
-    constexpr uint32_t idesc_q = make_idesc_bf16(128, DP, true, true);     // dQ (A = dS^T smem, M-major)
-    const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV), ds_addr = smem_u32(sdS);
-    mbar_wait(kv_full, 0);
-    for (int i = 0; i < nq; ++i) {
-      const int st = i & 1;
-      mbar_wait(&qdo_full[st], (i >> 1) & 1);
+    constexpr uint32_t idesc_s = make_idesc_bf16(128, 64, false, false);  // S^T, dP^T: 128 keys x 64 queries
+    constexpr uint32_t idesc_kv = make_idesc_bf16(128, DP, false, true);  // dV, dK (A from TMEM)
+    constexpr uint32_t idesc_q = make_idesc_bf16(128, DP, true, true);    // dQ (A = dS^T smem, M-major)
+    const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV);
+    auto issue_s = [&](int j) {  // S^T(j), dP^T(j) into buffer j % NBUF
+      const int st = j % QST;
+      mbar_wait(&qdo_full[st], (j / QST) & 1);
       tc_fence_after();
-      const uint32_t q_addr = smem_u32(sQ + st * TB), o_addr = smem_u32(sdO + st * TB);
       if (lane == 0) {
+        const uint32_t q_addr = smem_u32(sQ + st * QB), o_addr = smem_u32(sdO + st * QB);
+        const uint32_t tS = tbase + (j % NBUF) * 128, tDP = tS + 64;
 #pragma unroll
         for (int k = 0; k < DP / 16; ++k) {
-          mma_bf16_ss(tS, make_sdesc(k_addr + k * 32, 16, 8 * ROWB, SH::LAYOUT),
-                      make_sdesc(q_addr + k * 32, 16, 8 * ROWB, SH::LAYOUT), idesc_s, k > 0 ? 1u : 0u);
-          mma_bf16_ss(tDP, make_sdesc(v_addr + k * 32, 16, 8 * ROWB, SH::LAYOUT),
-                      make_sdesc(o_addr + k * 32, 16, 8 * ROWB, SH::LAYOUT), idesc_s, k > 0 ? 1u : 0u);
+          mma_bf16_ss(tS, make_sdesc(k_addr + k * 32, 16, 8 * ROWB, BS::LAYOUT),
+                      make_sdesc(q_addr + k * 32, 16, 8 * ROWB, BS::LAYOUT), idesc_s, k > 0 ? 1u : 0u);
+          mma_bf16_ss(tDP, make_sdesc(v_addr + k * 32, 16, 8 * ROWB, BS::LAYOUT),
+                      make_sdesc(o_addr + k * 32, 16, 8 * ROWB, BS::LAYOUT), idesc_s, k > 0 ? 1u : 0u);
         }
-        mma_commit(s_full);
+        mma_commit(&s_full[j % NBUF]);
       }
       __syncwarp();
-      mbar_wait(ds_full, i & 1);
-      if (i > 0) mbar_wait(dq_empty, (i - 1) & 1);
+    };
+    mbar_wait(kv_full, 0);
+    for (int j = 0; j < NBUF && j < nqe; ++j) issue_s(j);
+    for (int i = 0; i < nqe; ++i) {
+      const int st = i % QST, p = i >> 1;
+      mbar_wait(&ds_full[i % NBUF], (i / NBUF) & 1);
+      if ((i & 1) && p >= 2) mbar_wait(&dq_empty[p & 1], ((p >> 1) - 1) & 1);
       tc_fence_after();
       if (lane == 0) {
+        const uint32_t q_addr = smem_u32(sQ + st * QB), o_addr = smem_u32(sdO + st * QB);
+        const uint32_t tS = tbase + (i % NBUF) * 128, tDP = tS + 64;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {  // 16 queries per step
+        for (int k = 0; k < 4; ++k) {  // 16 queries per step
           const uint32_t acc = (i > 0 || k > 0) ? 1u : 0u;
-          mma_bf16_ts(tdV, tS + k * 8, make_sdesc(o_addr + k * 16 * ROWB, 128 * ROWB, 8 * ROWB, SH::LAYOUT),
-                      idesc_kv, acc);
-          mma_bf16_ts(tdK, tDP + k * 8, make_sdesc(q_addr + k * 16 * ROWB, 128 * ROWB, 8 * ROWB, SH::LAYOUT),
-                      idesc_kv, acc);
+          mma_bf16_ts(tdV, tS + k * 8, make_sdesc(o_addr + k * 16 * ROWB, QB, 8 * ROWB, BS::LAYOUT), idesc_kv, acc);
+          mma_bf16_ts(tdK, tDP + k * 8, make_sdesc(q_addr + k * 16 * ROWB, QB, 8 * ROWB, BS::LAYOUT), idesc_kv,
+                      acc);
         }
+        if (i & 1) {
+          const uint32_t ds_addr = smem_u32(sdS + (p & 1) * BS::DS_BUF);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {  // 16 keys per step
-          mma_bf16_ss(tdQ, make_sdesc(ds_addr + k * 16 * 128, 128 * 128, 1024, 2u),
-                      make_sdesc(k_addr + k * 16 * ROWB, 128 * ROWB, 8 * ROWB, SH::LAYOUT), idesc_q,
-                      k > 0 ? 1u : 0u);
+          for (int k = 0; k < 8; ++k)  // 16 keys per step
+            mma_bf16_ss(tdQ0 + (p & 1) * DP, make_sdesc(ds_addr + k * 16 * 128, 128 * 128, 1024, 2u),
+                        make_sdesc(k_addr + k * 16 * ROWB, KB, 8 * ROWB, BS::LAYOUT), idesc_q, k > 0 ? 1u : 0u);
+          mma_commit(&dq_full[p & 1]);
+          mma_commit(&dsm_empty[p & 1]);
         }
         mma_commit(&qdo_empty[st]);
-        mma_commit(dq_full);
-        mma_commit(dsm_empty);
-        if (i == nq - 1) mma_commit(dkv_done);
+        if (i == nqe - 1) mma_commit(dkv_done);
       }
       __syncwarp();
+      if (i + NBUF < nqe) issue_s(i + NBUF);  // buffer i % NBUF is free once dV/dK(i) are issued (in-order)
     }
-  } else if (warp < 10) {
-    // ======================= softmax-bwd: thread = key row =======================
+  } else {
+    // ============ softmax-bwd (thread = key row; 2 warps per lane quarter, 32 queries each) + dQ drain ============
     const int qq = warp & 3;
-    const int hf = (warp - 2) >> 2;  // which 64 query columns
+    const int hf = (warp - 2) >> 2;
     const int kr = qq * 32 + lane;
     const int key = k0 + kr;
     const bool kvalid = key < S && (nonprefix ? key_mask[(int64_t)b * S + key] != 0 : key < kv_len);
     const uint32_t lane_off = (uint32_t)(qq * 32) << 16;
-    for (int i = 0; i < nq; ++i) {
-      const int st = i & 1;
-      const int q0 = i * 128;
-      const float* lse = sL + st * 128;
-      const float* dl = sD + st * 128;
-      mbar_wait(s_full, i & 1);
+    constexpr int DQH = DP / 2;  // dQ columns drained by this warp
+
+    auto drain_dq = [&](int pp) {  // thread = query row of pair pp, columns [hf*DQH, hf*DQH + DQH)
+      mbar_wait(&dq_full[pp & 1], (pp >> 1) & 1);
       tc_fence_after();
-      if (i > 0) mbar_wait(dsm_empty, (i - 1) & 1);  // dQ MMA of the previous block has read sdS
-      uint32_t pp[32], dd[32];  // this warp's 64 query columns of P^T / dS^T, packed bf16x2
-      const int qmax0 = S - q0 - hf * 64;
+      uint32_t u[DQH];
+      const uint32_t tq = tdQ0 + (pp & 1) * DP;
 #pragma unroll
-      for (int h2 = 0; h2 < 2; ++h2) {
-        const int c = hf * 64 + h2 * 32;
-        uint32_t us[32], ud[32];
-        tmem_ld32(tS + lane_off + c, us);
-        tmem_ld32(tDP + lane_off + c, ud);
-        tmem_ld_wait();
+      for (int c = 0; c < DQH; c += 8)
+        tmem_ld8(tq + lane_off + hf * DQH + c, u[c], u[c + 1], u[c + 2], u[c + 3], u[c + 4], u[c + 5], u[c + 6],
+                 u[c + 7]);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&dq_empty[pp & 1]);
+      const int q = pp * 128 + kr;
+      if (q < S) {
+        float* dst = dQ + ((int64_t)bh * S + q) * DH + hf * DQH;
 #pragma unroll
-        for (int e = 0; e < 32; e += 4) {
-          const float4 l4 = *reinterpret_cast<const float4*>(lse + c + e);
-          const float4 d4 = *reinterpret_cast<const float4*>(dl + c + e);
-          const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv4[4] = {d4.x, d4.y, d4.z, d4.w};
-          float p[4], ds[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const float pe = ex2((__uint_as_float(us[e + u]) - lv[u]) * L2E);
-            p[u] = (kvalid && h2 * 32 + e + u < qmax0) ? pe : 0.f;
-            ds[u] = p[u] * (__uint_as_float(ud[e + u]) - dv4[u]);
-          }
-          pp[h2 * 16 + (e >> 1)] = pack2(p[0], p[1]);
-          pp[h2 * 16 + (e >> 1) + 1] = pack2(p[2], p[3]);
-          dd[h2 * 16 + (e >> 1)] = pack2(ds[0], ds[1]);
-          dd[h2 * 16 + (e >> 1) + 1] = pack2(ds[2], ds[3]);
-        }
+        for (int c = 0; c < DQH; c += 4)
+          if (hf * DQH + c < DH)
+            red_add_v4_f32(dst + c, __uint_as_float(u[c]), __uint_as_float(u[c + 1]), __uint_as_float(u[c + 2]),
+                           __uint_as_float(u[c + 3]));
       }
-      // both warps of this lane quarter must finish reading S^T / dP^T before P^T / dS^T
-      // (packed into the first 64 columns) overwrite them
-      asm volatile("bar.sync %0, 64;" ::"r"(1 + qq) : "memory");
-      tmem_st32(tS + lane_off + hf * 32, pp);
-      tmem_st32(tDP + lane_off + hf * 32, dd);
-      {  // dS^T row -> smem (M-major A operand of dQ = dS K): query chunk hf, SWIZZLE_128B rows
-        uint8_t* rowp = sdS + hf * (128 * 128) + kr * 128;
+    };
+
+    for (int i = 0; i < nqe; ++i) {
+      const int st = i % QST, p = i >> 1, ch = i & 1;
+      const int c = hf * 32;
+      const float* lse = sL + st * 64 + c;
+      const float* dl = sD + st * 64 + c;
+      const uint32_t tS = tbase + (i % NBUF) * 128, tDP = tS + 64;
+      mbar_wait(&s_full[i % NBUF], (i / NBUF) & 1);
+      tc_fence_after();
+      uint32_t us[32], ud[32];
+      tmem_ld32(tS + lane_off + c, us);
+      tmem_ld32(tDP + lane_off + c, ud);
+      if (ch == 0 && p >= 2) mbar_wait(&dsm_empty[p & 1], ((p >> 1) - 1) & 1);
+      tmem_ld_wait();
+      uint32_t pp[16], dd[16];
+      const int qmax = S - i * 64 - c;
 #pragma unroll
-        for (int g = 0; g < 8; ++g)
-          *reinterpret_cast<uint4*>(rowp + ((g ^ (kr & 7)) << 4)) =
-              make_uint4(dd[4 * g], dd[4 * g + 1], dd[4 * g + 2], dd[4 * g + 3]);
+      for (int e = 0; e < 32; e += 4) {
+        const float4 l4 = *reinterpret_cast<const float4*>(lse + e);
+        const float4 d4 = *reinterpret_cast<const float4*>(dl + e);
+        const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv4[4] = {d4.x, d4.y, d4.z, d4.w};
+        float pr[4], ds[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float pe = ex2((__uint_as_float(us[e + u]) - lv[u]) * L2E);
+          pr[u] = (kvalid && e + u < qmax) ? pe : 0.f;
+          ds[u] = pr[u] * (__uint_as_float(ud[e + u]) - dv4[u]);
+        }
+        pp[e >> 1] = pack2(pr[0], pr[1]);
+        pp[(e >> 1) + 1] = pack2(pr[2], pr[3]);
+        dd[e >> 1] = pack2(ds[0], ds[1]);
+        dd[(e >> 1) + 1] = pack2(ds[2], ds[3]);
+      }
+      // both warps of this lane quarter must have read S^T / dP^T before the packed P^T / dS^T overwrite them
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + qq) : "memory");
+      tmem_st16(tS + lane_off + hf * 16, pp);
+      tmem_st16(tDP + lane_off + hf * 16, dd);
+      uint8_t* rowp = sdS + (p & 1) * BS::DS_BUF + ch * (128 * 128) + kr * 128;
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        const int c16 = hf * 4 + g;
+        *reinterpret_cast<uint4*>(rowp + ((c16 ^ (kr & 7)) << 4)) =
+            make_uint4(dd[4 * g], dd[4 * g + 1], dd[4 * g + 2], dd[4 * g + 3]);
       }
       tmem_st_wait();
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(ds_full);
+      if (lane == 0) mbar_arrive(&ds_full[i % NBUF]);
+      if (ch == 1 && p >= 1) drain_dq(p - 1);  // dQ of the previous pair finished long ago (double buffered)
     }
-    // ---- final dK (hf == 0) / dV (hf == 1) rows
+    drain_dq(npairs - 1);
+    // ---- final rows: dK (hf == 0) or dV (hf == 1)
     mbar_wait(dkv_done, 0);
     tc_fence_after();
-    float kv[DP];
-    const uint32_t tsrc = hf == 0 ? tdK : tdV;
+    uint32_t u[DP];
+    const uint32_t src = (hf == 0 ? tdK : tdV) + lane_off;
 #pragma unroll
-    for (int c = 0; c < DP; c += 16) {
-      uint32_t u[16];
-      tmem_ld16(tsrc + lane_off + c, u);
-      tmem_ld_wait();
-#pragma unroll
-      for (int e = 0; e < 16; ++e) kv[c + e] = __uint_as_float(u[e]);
-    }
+    for (int cc = 0; cc < DP; cc += 8)
+      tmem_ld8(src + cc, u[cc], u[cc + 1], u[cc + 2], u[cc + 3], u[cc + 4], u[cc + 5], u[cc + 6], u[cc + 7]);
+    tmem_ld_wait();
     if (key < S) {
       __nv_bfloat16* dst = (hf == 0 ? dK : dV) + ((int64_t)bh * S + key) * DH;
 #pragma unroll
-      for (int c = 0; c < DH; c += 8)
-        *reinterpret_cast<uint4*>(dst + c) = make_uint4(pack2(kv[c], kv[c + 1]), pack2(kv[c + 2], kv[c + 3]),
-                                                        pack2(kv[c + 4], kv[c + 5]), pack2(kv[c + 6], kv[c + 7]));
-    }
-  } else {
-    // ======================= dQ epilogue: thread = query row =======================
-    const int qq = warp & 3;
-    const uint32_t lane_off = (uint32_t)(qq * 32) << 16;
-    for (int i = 0; i < nq; ++i) {
-      mbar_wait(dq_full, i & 1);
-      tc_fence_after();
-      float dq[DP];
-#pragma unroll
-      for (int c = 0; c < DP; c += 16) {
-        uint32_t u[16];
-        tmem_ld16(tdQ + lane_off + c, u);
-        tmem_ld_wait();
-#pragma unroll
-        for (int e = 0; e < 16; ++e) dq[c + e] = __uint_as_float(u[e]);
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(dq_empty);
-      const int q = i * 128 + qq * 32 + lane;
-      if (q < S) {
-        float* dst = dQ + ((int64_t)bh * S + q) * DH;
-#pragma unroll
-        for (int c = 0; c < DH; c += 4) red_add_v4_f32(dst + c, dq[c], dq[c + 1], dq[c + 2], dq[c + 3]);
-      }
+      for (int cc = 0; cc < DH; cc += 8)
+        *reinterpret_cast<uint4*>(dst + cc) = make_uint4(
+            pack2(__uint_as_float(u[cc]), __uint_as_float(u[cc + 1])),
+            pack2(__uint_as_float(u[cc + 2]), __uint_as_float(u[cc + 3])),
+            pack2(__uint_as_float(u[cc + 4]), __uint_as_float(u[cc + 5])),
+            pack2(__uint_as_float(u[cc + 6]), __uint_as_float(u[cc + 7])));
     }
   }
   tc_fence_before();
@@ -710,18 +734,19 @@ int launch_fwd(const void* q, const void* k, const void* v, const int32_t* km, v
 template <int DH>
 int launch_bwd(const void* q, const void* k, const void* v, const void* dout, const float* lse, const float* delta,
                const int32_t* km, float* dq, void* dk, void* dv, int B, int nh, int S, cudaStream_t st) {
-  using SH = Shape<DH, 128>;
+  using SH = Shape<DH, 64>;
+  using BS = BwdShape<DH>;
   CUtensorMap tq, tk, tv, tdo;
   const int64_t rows = (int64_t)B * nh * S;
   int rc;
-  if ((rc = head_map<DH, 128>(&tq, q, rows)) || (rc = head_map<DH, 128>(&tk, k, rows)) ||
+  if ((rc = head_map<DH, 64>(&tq, q, rows)) || (rc = head_map<DH, 128>(&tk, k, rows)) ||
       (rc = head_map<DH, 128>(&tv, v, rows)))
     return rc;
-  {  // dO is token-major [B*S, nh*DH]; box = DP columns of one head x 128 tokens
+  {  // dO is token-major [B*S, nh*DH]; box = DP columns of one head x 64 tokens
     PFN_encodeTiled enc = encoder();
     cuuint64_t dims[2] = {(cuuint64_t)nh * DH, (cuuint64_t)B * S};
     cuuint64_t strides[1] = {(cuuint64_t)nh * DH * 2};
-    cuuint32_t box[2] = {(cuuint32_t)SH::DP, 128};
+    cuuint32_t box[2] = {(cuuint32_t)SH::DP, 64};
     cuuint32_t estr[2] = {1, 1};
     const CUtensorMapSwizzle sw = SH::ROWB == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
                                   : SH::ROWB == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
@@ -733,15 +758,14 @@ int launch_bwd(const void* q, const void* k, const void* v, const void* dout, co
       return ESM_EDRIVER;
     }
   }
-  const int smem = 2 * 128 * 128 + 6 * 128 * SH::ROWB + 4 * 128 * 4 + 1024 + 256;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(bwd_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(bwd_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, BS::SMEM);
     attr = true;
   }
   dim3 grid((S + 127) / 128, B * nh);
-  bwd_kernel<DH><<<grid, kBwdThreads, smem, st>>>(tq, tk, tv, tdo, km, lse, delta, dq, (__nv_bfloat16*)dk,
-                                                  (__nv_bfloat16*)dv, S, nh);
+  bwd_kernel<DH><<<grid, kBwdThreads, BS::SMEM, st>>>(tq, tk, tv, tdo, km, lse, delta, dq, (__nv_bfloat16*)dk,
+                                                      (__nv_bfloat16*)dv, S, nh);
   ESM_LAUNCH_RET();
 }
 

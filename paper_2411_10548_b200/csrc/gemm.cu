@@ -125,8 +125,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   using C = Cfg<BN, EPI>;
   using E = EpiCfg<EPI>;
   constexpr int STAGES = C::STAGES;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps shared provenance
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * C::A_BYTES;
   uint8_t* sEpi = smem + STAGES * C::STAGE_BYTES;  // 1 KB aligned (stage sizes are multiples of 1 KB)
