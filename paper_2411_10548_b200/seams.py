@@ -1,0 +1,75 @@
+"""Adapters that plug the B200 train step into the reference's own seams.
+
+The reference (``densefeed``) owns the layer around the hot path:
+
+* ``densefeed.sizing.collect_peak_alloc(samples, workload, feature_fn, meter)``
+  (pkg/src/densefeed/sizing.py:76-100) -- the only place a training workload is invoked and
+  metered.  ``make_workload`` returns the ``workload`` callable (one MLM train step on the GPU)
+  and ``CudaPeakMeter`` implements the ``ResourceMeter`` protocol ``reset()/peak()``
+  (sizing.py:24-29) with CUDA peak-allocation statistics.  Exceptions raised by the step
+  (e.g. CUDA OOM) propagate, so ``collect_peak_alloc`` records the sample as failed
+  (sizing.py:96-98) -- the OOM analogue the reference expects.
+* ``densefeed_bindings.batches(...) -> Iterator[list[int]]`` and ``BoundDataset[i] -> (tokens,
+  metadata)`` (pkg/bindings/src/densefeed_bindings/__init__.py:45-95) -- ``collate_indices``
+  turns one index batch into the padded int32 ``[B, S]`` ids + attention mask the step consumes.
+* ``length_features`` gives the ``[L, L^2]`` cost features (the corpus.py:57-60 pattern) so
+  ``fit_cost_model`` can model attention's quadratic memory.
+"""
+from __future__ import annotations
+
+from typing import Callable, Sequence
+
+import numpy as np
+import torch
+
+from .data import collate
+
+
+class CudaPeakMeter:
+    """ResourceMeter over CUDA allocator statistics: peak bytes allocated since ``reset()``."""
+
+    def __init__(self, device=None):
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+
+    def reset(self) -> None:
+        torch.cuda.synchronize(self.device)
+        torch.cuda.reset_peak_memory_stats(self.device)
+
+    def peak(self) -> float:
+        torch.cuda.synchronize(self.device)
+        return float(torch.cuda.max_memory_allocated(self.device))
+
+
+def length_features(sample) -> np.ndarray:
+    """Cost features of a sample (one token sequence, or a batch of them): [sum L, sum L^2]."""
+    if len(sample) and not isinstance(sample[0], (int, np.integer)):
+        lens = np.array([len(s) for s in sample], dtype=np.float64)
+    else:
+        lens = np.array([len(sample)], dtype=np.float64)
+    return np.array([lens.sum(), (lens * lens).sum()])
+
+
+def collate_indices(dataset, indices: Sequence[int], seq_len: int | None = None, pad_to: int = 8):
+    """One ``batches()`` index list -> (ids int32 [B, S], attention_mask int32 [B, S])."""
+    toks = [dataset[i][0] if isinstance(dataset[i], tuple) else dataset[i] for i in indices]
+    return collate(toks, seq_len=seq_len, pad_to=pad_to)
+
+
+def make_workload(model, seed: int = 0, pad_to: int = 8, lr: float | None = None) -> Callable:
+    """``workload(sample)`` for ``collect_peak_alloc``: one full MLM train step (device masking,
+    forward, backward, AdamW) on a sample = one token sequence or a list of them."""
+    state = {"step": 0}
+
+    def workload(sample):
+        batch = sample if (len(sample) and not isinstance(sample[0], (int, np.integer))) else [sample]
+        ids, am = collate(batch, pad_to=pad_to)
+        ids_d = torch.from_numpy(ids).to(model.device)
+        ws = model.workspace(*ids.shape)
+        ws.am.copy_(torch.from_numpy(am).to(model.device))
+        model.mlm_mask(ids_d, seed, state["step"], ws)
+        model.forward_backward(ws)
+        model.optimizer_step(lr=lr)
+        state["step"] += 1
+        return float(ws.loss_sum.item())
+
+    return workload

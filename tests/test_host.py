@@ -1,0 +1,160 @@
+"""CPU-only tests of the host side: C-ABI exports vs the header, native tokenizer vs the oracle,
+parameter layout / init parity with the oracle, collation, and the data-parallel gradient
+bucket all-reduce on gloo with world_size 2 (no GPU needed)."""
+import ctypes
+import os
+import re
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import esm2_oracle as O
+from paper_2411_10548_b200 import EsmConfig, _lib, preset
+from paper_2411_10548_b200.data import collate, synthetic_batch, tokenize
+from paper_2411_10548_b200.model import ALIGN, ParamStore, init_params, param_groups, rope_tables
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_declared_symbol():
+    hdr = open(os.path.join(ROOT, "include", "esm2_b200.h")).read()
+    declared = set(re.findall(r"^(?:int|const char\*)\s+(esm_\w+)\s*\(", hdr, flags=re.M))
+    assert len(declared) >= 18
+    lib = _lib.load()
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert declared == set(_lib.EXPORTS)
+    assert lib.esm_version() >= 10000
+
+
+def test_native_tokenizer_matches_oracle():
+    rng = np.random.default_rng(0)
+    alphabet = list("LAGVSERTIDPKQNFYMHWCXBUZO.-J*")
+    for _ in range(50):
+        seq = "".join(rng.choice(alphabet, size=rng.integers(0, 300)))
+        np.testing.assert_array_equal(tokenize(seq), O.tokenize(seq))
+
+
+def test_tokenizer_buffer_too_small_reports_needed():
+    lib = _lib.load()
+    out = np.zeros(4, np.int32)
+    assert lib.esm_tokenize(b"MKTAYIAK", 8, out.ctypes.data_as(ctypes.c_void_p), 4) == -10
+
+
+def test_init_params_and_rope_match_oracle():
+    cfg = EsmConfig(hidden_size=64, num_hidden_layers=2, num_attention_heads=4, intermediate_size=256)
+    ocfg = O.OracleConfig(hidden_size=64, num_hidden_layers=2, num_attention_heads=4, intermediate_size=256)
+    a, b = init_params(cfg, 7), O.init_params(ocfg, 7)
+    assert a.keys() == b.keys()
+    for k in a:
+        np.testing.assert_array_equal(a[k], b[k])
+    c, s = rope_tables(100, 24)
+    oc, os_ = O.rope_tables(100, 24)
+    np.testing.assert_array_equal(c, oc[:, :12])
+    np.testing.assert_array_equal(s, os_[:, :12])
+
+
+def test_param_store_layout():
+    cfg = preset("8m")
+    st = ParamStore(cfg, "cpu", shadow=False)
+    assert st.numel % ALIGN == 0
+    n = sum(s.numel for s in st.slots.values())
+    assert n == 7_511_233 or abs(n - 7.51e6) < 2e4  # ESM-2 8M parameter count (tied decoder)
+    # groups are 256-aligned, contiguous, in backward-completion order with embeddings last
+    keys = [k for k, _ in param_groups(cfg)]
+    assert keys[0] == "lm_head.bias" and keys[-1] == "esm.embeddings.word_embeddings.weight"
+    prev = -1
+    for k in keys:
+        a, b = st.group_range[k]
+        assert a % ALIGN == 0 and a > prev
+        prev = a
+    # q/k/v weights of one layer form one contiguous [3H, H] group
+    q = st.slots["esm.encoder.layer.0.attention.self.query.weight"]
+    v = st.slots["esm.encoder.layer.0.attention.self.value.weight"]
+    assert v.offset - q.offset == 2 * cfg.hidden_size ** 2
+    # decay flags: weights decay, biases / LayerNorm do not
+    d = st.decay.numpy()
+    a, _ = st.group_range["esm.encoder.layer.0.output.dense.weight"]
+    assert d[a // ALIGN] == 1
+    a, _ = st.group_range["esm.encoder.layer.0.LayerNorm.weight"]
+    assert d[a // ALIGN] == 0
+
+
+def test_presets_param_counts():
+    expect = {"8m": 7.51e6, "35m": 33.50e6, "650m": 651.04e6, "3b": 2839.01e6}
+    for name, n in expect.items():
+        cfg = preset(name)
+        H, F, V, L = cfg.hidden_size, cfg.intermediate_size, cfg.vocab_size, cfg.num_hidden_layers
+        total = V * H + L * (4 * H * H + 4 * H + 2 * H * F + F + H + 4 * H) + 2 * H + H * H + H + 2 * H + V
+        assert abs(total - n) / n < 1e-3, (name, total)
+
+
+def test_collate_and_synthetic():
+    ids, am = collate([[0, 5, 6, 2], [0, 7, 2]], pad_to=8)
+    assert ids.shape == (2, 8) and am.sum() == 7
+    assert (ids[1, 3:] == 1).all()
+    a, _ = synthetic_batch(3, 16, 5)
+    b, _ = O.synthetic_batch(3, 16, 5)
+    np.testing.assert_array_equal(a, b)
+
+
+def test_flops_per_token_matches_oracle():
+    cfg = preset("650m")
+    ocfg = O.OracleConfig(hidden_size=1280, num_hidden_layers=33, num_attention_heads=20, intermediate_size=5120)
+    assert cfg.train_flops_per_token(1024) == O.train_flops_per_token(ocfg, 1024)
+
+
+# ---------------------------------------------------------------- DDP bucketing on gloo
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _ddp_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2411_10548_b200.ddp import GradAllReducer
+        cfg = EsmConfig(hidden_size=64, num_hidden_layers=3, num_attention_heads=4, intermediate_size=256)
+        st = ParamStore(cfg, "cpu", shadow=False)
+        red = GradAllReducer(st, bucket_bytes=64 << 10)
+        g = torch.arange(st.numel, dtype=torch.float32) * (rank + 1)
+        st.g32.copy_(g)
+        red.begin_backward()
+        # readiness in backward order, as the model signals it
+        red.ready("esm.encoder.emb_layer_norm_after.bias")
+        for l in reversed(range(cfg.num_hidden_layers)):
+            red.ready(f"esm.encoder.layer.{l}.attention.LayerNorm.bias")
+        red.ready("esm.embeddings.word_embeddings.weight")
+        red.end_backward()
+        want = torch.arange(st.numel, dtype=torch.float32) * sum(r + 1 for r in range(world))
+        ok_grad = torch.equal(st.g32, want)
+        n = torch.tensor([10 * (rank + 1)], dtype=torch.int32)
+        red.reduce_count(n)
+        q.put((rank, ok_grad, int(n.item()), len(red.bucket_ends)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_grad_bucket_allreduce_gloo_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ddp_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok, n, nb in res:
+        assert ok, rank
+        assert n == 30
+        assert nb > 1  # several buckets -> overlap with backward is possible
