@@ -120,6 +120,14 @@ int esm_attn_bwd(int dtype, const void* q, const void* k, const void* v, const v
                  const float* lse, const int32_t* key_mask, float* delta, float* dq, void* dk, void* dv,
                  int B, int nh, int S, int dh, esm_stream_t stream);
 
+/* Fused backward for the ESM layer (bf16, S % 4 == 0): writes dqkv[T, 3H] = [dq, dk, dv] with RoPEᵀ (and
+ * q_scale on dq) applied -- the layout the QKV dgrad / wgrad GEMMs consume -- and col_sum[3H] += the q/k/v
+ * bias gradients.  dq_ws: fp32 [T, H] workspace (zeroed by callee); delta: [B, nh, S] fp32 workspace. */
+int esm_attn_bwd_qkv(const void* q, const void* k, const void* v, const void* o, const void* dout,
+                     const float* lse, const int32_t* key_mask, float* delta, float* dq_ws, void* dqkv,
+                     float* col_sum, const float* cos_t, const float* sin_t, float q_scale, int B, int nh, int S,
+                     int dh, esm_stream_t stream);
+
 /* ---------------- LM head decoder + masked cross-entropy (HF:modeling_esm.py:777-815) ---------------- */
 /* logits = n·Eᵀ + bias for labelled rows; loss_sum += Σ nll * inv_denom[0]; dlogits -> dn (= dlogits·E),
  * dE += dlogitsᵀ·n, dbias += Σ dlogits.  Unlabelled rows get dn = 0. */

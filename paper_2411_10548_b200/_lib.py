@@ -17,7 +17,7 @@ EPI_STORE, EPI_GELU, EPI_RESID, EPI_DGELU, EPI_F32_ACC, EPI_QKV_ROPE = 0, 1, 2, 
 EXPORTS = [
     "esm_version", "esm_last_error", "esm_device_sm_count", "esm_tokenize", "esm_mlm_mask", "esm_embed_fwd",
     "esm_embed_bwd", "esm_layernorm_fwd", "esm_layernorm_bwd", "esm_gemm", "esm_qkv_rope_fwd", "esm_qkv_rope_bwd",
-    "esm_attn_fwd", "esm_attn_bwd", "esm_lmhead_xent", "esm_inv_count", "esm_adamw", "esm_cast_f32_bf16",
+    "esm_attn_fwd", "esm_attn_bwd", "esm_attn_bwd_qkv", "esm_lmhead_xent", "esm_inv_count", "esm_adamw", "esm_cast_f32_bf16",
 ]
 
 
@@ -60,6 +60,7 @@ _SIGS = {
     "esm_qkv_rope_bwd": ([_I, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _F, _P], _I),
     "esm_attn_fwd": ([_I, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _P], _I),
     "esm_attn_bwd": ([_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _P], _I),
+    "esm_attn_bwd_qkv": ([_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _F, _I, _I, _I, _I, _P], _I),
     "esm_lmhead_xent": ([_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _P], _I),
     "esm_inv_count": ([_P, _P, _P], _I),
     "esm_adamw": ([_P, _P, _P, _P, _P, _P, _I64, _P, _P], _I),

@@ -257,25 +257,29 @@ __global__ void __launch_bounds__(128) fwd_bf16_kernel(const __nv_bfloat16* __re
 }
 
 // ---------------------------------------------------------------------------- backward
-// delta[q] = sum_d dO[q,d] * O[q,d]
+// delta[q] = sum_d dO[q,d] * O[q,d]; one thread per (token, head): consecutive threads read consecutive
+// heads of a token, i.e. contiguous 16-byte vectors of the token-major [T, H] rows.
 template <typename T>
 __global__ void delta_kernel(const T* __restrict__ O, const T* __restrict__ dO, float* __restrict__ delta,
                              int64_t T_, int S, int nh, int dh) {
+  constexpr int VEC = vec16<T>::N;
   const int H = nh * dh;
   const int64_t total = T_ * nh;
-  const int lane = threadIdx.x & 31;
-  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = w0; i < total; i += nw) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = i / nh;
-    const int h = (int)(i % nh);
+    const int h = (int)(i - t * nh);
+    const T* o = O + t * H + h * dh;
+    const T* g = dO + t * H + h * dh;
     float acc = 0.f;
-    for (int d = lane; d < dh; d += 32) acc += io<T>::ld(O + t * H + h * dh + d) * io<T>::ld(dO + t * H + h * dh + d);
-    acc = warp_sum(acc);
-    if (lane == 0) {
-      const int64_t b = t / S, s = t % S;
-      delta[(b * nh + h) * S + s] = acc;
+    for (int d = 0; d < dh; d += VEC) {
+      float a[VEC], c[VEC];
+      load_vec(o + d, a);
+      load_vec(g + d, c);
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) acc += a[e] * c[e];
     }
+    const int64_t b = t / S, s = t % S;
+    delta[(b * nh + h) * S + s] = acc;
   }
 }
 
@@ -680,6 +684,34 @@ __global__ void __launch_bounds__(64) bwd_dkv_f32_kernel(const float* __restrict
       }
 }
 
+// dq (fp32, token-major [T, H]) -> dqkv[:, 0:H] with RoPE^T and q_scale; col_sum[0:H] += column sums.
+__global__ void dq_finalize_kernel(const float* __restrict__ dq, __nv_bfloat16* __restrict__ dqkv,
+                                   float* __restrict__ csum, const float* __restrict__ cs, const float* __restrict__ sn,
+                                   int64_t T_, int S, int nh, int dh, float qs, int rows_per_block) {
+  const int half = dh >> 1;
+  const int H = nh * dh;
+  const int pair = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pair >= nh * half) return;
+  const int h = pair / half, j = pair - (pair / half) * half;
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_block, r1 = min(T_, r0 + rows_per_block);
+  float a0 = 0.f, a1 = 0.f;
+  for (int64_t t = r0; t < r1; ++t) {
+    const int s = (int)(t % S);
+    const float c = __ldg(cs + (int64_t)s * half + j), sv = __ldg(sn + (int64_t)s * half + j);
+    const float g0 = dq[t * H + h * dh + j], g1 = dq[t * H + h * dh + j + half];
+    const float q0 = (g0 * c + g1 * sv) * qs, q1 = (g1 * c - g0 * sv) * qs;
+    __nv_bfloat16* row = dqkv + t * 3 * H + h * dh;
+    row[j] = __float2bfloat16_rn(q0);
+    row[j + half] = __float2bfloat16_rn(q1);
+    a0 += q0;
+    a1 += q1;
+  }
+  if (csum) {
+    atomicAdd(csum + h * dh + j, a0);
+    atomicAdd(csum + h * dh + j + half, a1);
+  }
+}
+
 }  // namespace attn
 }  // namespace esm
 
@@ -687,7 +719,8 @@ namespace esm {
 int attn_fwd_tc(const void* q, const void* k, const void* v, const int32_t* km, void* o, float* lse, int B, int nh,
                 int S, int dh, cudaStream_t st);
 int attn_bwd_tc(const void* q, const void* k, const void* v, const void* dout, const float* lse, const float* delta,
-                const int32_t* km, float* dq, void* dk, void* dv, int B, int nh, int S, int dh, cudaStream_t st);
+                const int32_t* km, float* dq, void* dk, void* dv, int B, int nh, int S, int dh, cudaStream_t st,
+                void* dqkv, float* col_sum, const float* cos_t, const float* sin_t);
 static int legacy_attention() {
   static int v = -1;
   if (v < 0) {
@@ -735,14 +768,15 @@ extern "C" int esm_attn_bwd(int dtype, const void* q, const void* k, const void*
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int64_t T_ = (int64_t)B * S;
   dim3 grid((S + 63) / 64, B * nh);
-  int dgrid = (int)((T_ * nh * 32 + 255) / 256);
-  if (dgrid > 148 * 16) dgrid = 148 * 16;
+  int dgrid = (int)((T_ * nh + 255) / 256);
+  if (dgrid > 148 * 32) dgrid = 148 * 32;
   if (dtype == ESM_BF16) {
     attn::delta_kernel<__nv_bfloat16><<<dgrid, 256, 0, st>>>((const __nv_bfloat16*)o, (const __nv_bfloat16*)dout,
                                                              delta, T_, S, nh, dh);
     cudaMemsetAsync(dq, 0, sizeof(float) * T_ * nh * dh, st);
     if (!legacy_attention() && S % 4 == 0) {
-      const int rc = attn_bwd_tc(q, k, v, dout, lse, delta, key_mask, dq, dk, dv, B, nh, S, dh, st);
+      const int rc = attn_bwd_tc(q, k, v, dout, lse, delta, key_mask, dq, dk, dv, B, nh, S, dh, st, nullptr, nullptr,
+                                 nullptr, nullptr);
       if (rc) return rc;
       ESM_LAUNCH_RET();
     }
@@ -775,5 +809,30 @@ extern "C" int esm_attn_bwd(int dtype, const void* q, const void* k, const void*
                                                   (const float*)dout, lse, delta, key_mask, (float*)dk, (float*)dv, S,
                                                   nh, dh);
   }
+  ESM_LAUNCH_RET();
+}
+
+extern "C" int esm_attn_bwd_qkv(const void* q, const void* k, const void* v, const void* o, const void* dout,
+                                const float* lse, const int32_t* key_mask, float* delta, float* dq_ws, void* dqkv,
+                                float* col_sum, const float* cos_t, const float* sin_t, float q_scale, int B, int nh,
+                                int S, int dh, esm_stream_t stream) {
+  ESM_CHECK_ARG(q && k && v && o && dout && lse && delta && dq_ws && dqkv && col_sum && cos_t && sin_t,
+                "esm_attn_bwd_qkv: null pointer");
+  ESM_CHECK_ARG(S % 4 == 0 && dh % 8 == 0, "esm_attn_bwd_qkv: needs S %% 4 == 0 and dh %% 8 == 0");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t T_ = (int64_t)B * S;
+  int dgrid = (int)((T_ * nh + 255) / 256);
+  if (dgrid > 148 * 32) dgrid = 148 * 32;
+  attn::delta_kernel<__nv_bfloat16><<<dgrid, 256, 0, st>>>((const __nv_bfloat16*)o, (const __nv_bfloat16*)dout,
+                                                           delta, T_, S, nh, dh);
+  cudaMemsetAsync(dq_ws, 0, sizeof(float) * T_ * nh * dh, st);
+  const int rc = attn_bwd_tc(q, k, v, dout, lse, delta, key_mask, dq_ws, nullptr, nullptr, B, nh, S, dh, st, dqkv,
+                             col_sum, cos_t, sin_t);
+  if (rc) return rc;
+  const int pairs = nh * dh / 2;
+  const int rpb = 64;
+  dim3 grid((pairs + 127) / 128, (unsigned)((T_ + rpb - 1) / rpb));
+  attn::dq_finalize_kernel<<<grid, 128, 0, st>>>(dq_ws, (__nv_bfloat16*)dqkv, col_sum, cos_t, sin_t, T_, S, nh, dh,
+                                                 q_scale, rpb);
   ESM_LAUNCH_RET();
 }

@@ -379,6 +379,17 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
                : "memory");
 }
 
+// Optional fused output of the backward (esm_attn_bwd_qkv): dK (RoPE^T applied) and dV written straight
+// into the token-major dqkv [T, 3H] buffer the QKV dgrad/wgrad GEMMs consume, with their bias-gradient
+// column sums; dQ accumulated token-major [T, H] (finalised by dq_finalize_kernel).
+struct FusedOut {
+  __nv_bfloat16* dqkv;  // nullptr -> classic [B, nh, S, dh] outputs
+  float* col_sum;       // [3H]
+  const float* cos_t;   // [S, dh/2]
+  const float* sin_t;
+  int H;
+};
+
 template <int DH>
 struct BwdShape {
   static constexpr int DP = Shape<DH, 64>::DP, ROWB = Shape<DH, 64>::ROWB;
@@ -397,7 +408,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
                const int32_t* __restrict__ key_mask, const float* __restrict__ LSE, const float* __restrict__ Delta,
                float* __restrict__ dQ, __nv_bfloat16* __restrict__ dK, __nv_bfloat16* __restrict__ dV, int S,
-               int nh) {
+               int nh, const FusedOut fo) {
   using BS = BwdShape<DH>;
   constexpr int DP = BS::DP, ROWB = BS::ROWB, QB = BS::QB, KB = BS::KB, QST = BS::QST, NBUF = BS::NBUF;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -434,8 +445,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     for (int i = threadIdx.x; i < 128 * DH; i += blockDim.x) {
       const int kk = k0 + i / DH;
       if (kk < S) {
-        dK[((int64_t)bh * S + kk) * DH + i % DH] = __float2bfloat16_rn(0.f);
-        dV[((int64_t)bh * S + kk) * DH + i % DH] = __float2bfloat16_rn(0.f);
+        if (fo.dqkv) {
+          __nv_bfloat16* row = fo.dqkv + ((int64_t)b * S + kk) * 3 * fo.H + h * DH + i % DH;
+          row[fo.H] = __float2bfloat16_rn(0.f);
+          row[2 * fo.H] = __float2bfloat16_rn(0.f);
+        } else {
+          dK[((int64_t)bh * S + kk) * DH + i % DH] = __float2bfloat16_rn(0.f);
+          dV[((int64_t)bh * S + kk) * DH + i % DH] = __float2bfloat16_rn(0.f);
+        }
       }
     }
     return;
@@ -579,7 +596,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       if (lane == 0) mbar_arrive(&dq_empty[pp & 1]);
       const int q = pp * 128 + kr;
       if (q < S) {
-        float* dst = dQ + ((int64_t)bh * S + q) * DH + hf * DQH;
+        float* dst = (fo.dqkv ? dQ + ((int64_t)b * S + q) * fo.H + h * DH : dQ + ((int64_t)bh * S + q) * DH) +
+                     hf * DQH;
 #pragma unroll
         for (int c = 0; c < DQH; c += 4)
           if (hf * DQH + c < DH)
@@ -648,7 +666,40 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     for (int cc = 0; cc < DP; cc += 8)
       tmem_ld8(src + cc, u[cc], u[cc + 1], u[cc + 2], u[cc + 3], u[cc + 4], u[cc + 5], u[cc + 6], u[cc + 7]);
     tmem_ld_wait();
-    if (key < S) {
+    if (fo.dqkv) {
+      // fused: RoPE^T on dK, token-major store into dqkv, bias-gradient column sums
+      float val[DP];
+#pragma unroll
+      for (int cc = 0; cc < DP; ++cc) val[cc] = key < S ? __uint_as_float(u[cc]) : 0.f;
+      if (hf == 0 && key < S) {
+        constexpr int HALF = DH / 2;
+        const float* cs = fo.cos_t + (int64_t)key * HALF;
+        const float* sn = fo.sin_t + (int64_t)key * HALF;
+#pragma unroll
+        for (int j = 0; j < HALF; ++j) {
+          const float c = __ldg(cs + j), sv = __ldg(sn + j);
+          const float g0 = val[j], g1 = val[j + HALF];
+          val[j] = g0 * c + g1 * sv;
+          val[j + HALF] = g1 * c - g0 * sv;
+        }
+      }
+      if (key < S) {
+        __nv_bfloat16* dst = fo.dqkv + ((int64_t)b * S + key) * 3 * fo.H + (1 + hf) * fo.H + h * DH;
+#pragma unroll
+        for (int cc = 0; cc < DH; cc += 8)
+          *reinterpret_cast<uint4*>(dst + cc) =
+              make_uint4(pack2(val[cc], val[cc + 1]), pack2(val[cc + 2], val[cc + 3]), pack2(val[cc + 4], val[cc + 5]),
+                         pack2(val[cc + 6], val[cc + 7]));
+      }
+#pragma unroll
+      for (int c0 = 0; c0 < DH; c0 += 32) {
+        float t32[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) t32[j] = (c0 + j < DH) ? val[c0 + j] : 0.f;
+        const float cs = warp_transpose_sum32(t32, lane);
+        if (c0 + lane < DH) red_add_f32(fo.col_sum + (1 + hf) * fo.H + h * DH + c0 + lane, cs);
+      }
+    } else if (key < S) {
       __nv_bfloat16* dst = (hf == 0 ? dK : dV) + ((int64_t)bh * S + key) * DH;
 #pragma unroll
       for (int cc = 0; cc < DH; cc += 8)
@@ -733,7 +784,8 @@ int launch_fwd(const void* q, const void* k, const void* v, const int32_t* km, v
 
 template <int DH>
 int launch_bwd(const void* q, const void* k, const void* v, const void* dout, const float* lse, const float* delta,
-               const int32_t* km, float* dq, void* dk, void* dv, int B, int nh, int S, cudaStream_t st) {
+               const int32_t* km, float* dq, void* dk, void* dv, int B, int nh, int S, cudaStream_t st,
+               FusedOut fo) {
   using SH = Shape<DH, 64>;
   using BS = BwdShape<DH>;
   CUtensorMap tq, tk, tv, tdo;
@@ -765,20 +817,22 @@ int launch_bwd(const void* q, const void* k, const void* v, const void* dout, co
   }
   dim3 grid((S + 127) / 128, B * nh);
   bwd_kernel<DH><<<grid, kBwdThreads, BS::SMEM, st>>>(tq, tk, tv, tdo, km, lse, delta, dq, (__nv_bfloat16*)dk,
-                                                      (__nv_bfloat16*)dv, S, nh);
+                                                      (__nv_bfloat16*)dv, S, nh, fo);
   ESM_LAUNCH_RET();
 }
 
 }  // namespace fa
 
 int attn_bwd_tc(const void* q, const void* k, const void* v, const void* dout, const float* lse, const float* delta,
-                const int32_t* km, float* dq, void* dk, void* dv, int B, int nh, int S, int dh, cudaStream_t st) {
+                const int32_t* km, float* dq, void* dk, void* dv, int B, int nh, int S, int dh, cudaStream_t st,
+                void* dqkv, float* col_sum, const float* cos_t, const float* sin_t) {
   ESM_CHECK_ARG(S % 4 == 0, "attention bwd (tcgen05): S %% 4 == 0 required");
+  fa::FusedOut fo{(__nv_bfloat16*)dqkv, col_sum, cos_t, sin_t, nh * dh};
   switch (dh) {
-    case 16: return fa::launch_bwd<16>(q, k, v, dout, lse, delta, km, dq, dk, dv, B, nh, S, st);
-    case 24: return fa::launch_bwd<24>(q, k, v, dout, lse, delta, km, dq, dk, dv, B, nh, S, st);
-    case 32: return fa::launch_bwd<32>(q, k, v, dout, lse, delta, km, dq, dk, dv, B, nh, S, st);
-    case 64: return fa::launch_bwd<64>(q, k, v, dout, lse, delta, km, dq, dk, dv, B, nh, S, st);
+    case 16: return fa::launch_bwd<16>(q, k, v, dout, lse, delta, km, dq, dk, dv, B, nh, S, st, fo);
+    case 24: return fa::launch_bwd<24>(q, k, v, dout, lse, delta, km, dq, dk, dv, B, nh, S, st, fo);
+    case 32: return fa::launch_bwd<32>(q, k, v, dout, lse, delta, km, dq, dk, dv, B, nh, S, st, fo);
+    case 64: return fa::launch_bwd<64>(q, k, v, dout, lse, delta, km, dq, dk, dv, B, nh, S, st, fo);
     default: set_last_error("attention: head dim %d unsupported", dh); return ESM_ENOTSUP;
   }
 }

@@ -306,7 +306,7 @@ class EsmForMaskedLM:
         return self.ws
 
     # kernels launched per C-ABI entry point (for the bench's gpu_launches count)
-    _KERNELS = {"esm_embed_fwd": 2, "esm_attn_bwd": 2, "esm_lmhead_xent": 2}
+    _KERNELS = {"esm_embed_fwd": 2, "esm_attn_bwd": 2, "esm_attn_bwd_qkv": 3, "esm_lmhead_xent": 2}
 
     def _call(self, name, *args, flops=0.0, nbytes=0.0):
         t = self.timer
@@ -500,12 +500,19 @@ class EsmForMaskedLM:
             # attention
             self.linear_dgrad(ws.dx1, p + "attention.output.dense.weight", H, H, ws.do)
             self.linear_wgrad(ws.dx1, ly.o, p + "attention.output.dense.weight", H, H)
-            call("esm_attn_bwd", kdt, ly.q.data_ptr(), ly.k.data_ptr(), ly.v.data_ptr(), ly.o.data_ptr(),
-                 ws.do.data_ptr(), ly.lse.data_ptr(), ws.am.data_ptr(), ws.delta.data_ptr(), ws.dq.data_ptr(),
-                 ws.dk.data_ptr(), ws.dv.data_ptr(), B, nh, S, dh, st, flops=10.0 * B * nh * S * S * dh)
-            call("esm_qkv_rope_bwd", kdt, ws.dq.data_ptr(), ws.dk.data_ptr(), ws.dv.data_ptr(), ws.dqkv.data_ptr(),
-                 self._g32(p + "attention.self.qkv.bias").data_ptr(), ws.cos.data_ptr(), ws.sin.data_ptr(), B, S,
-                 nh, dh, qs, st)
+            if kdt == ESM_BF16 and S % 4 == 0:
+                # fused: attention backward writes dqkv [T,3H] (RoPE^T, q-scale) + q/k/v bias grads
+                call("esm_attn_bwd_qkv", ly.q.data_ptr(), ly.k.data_ptr(), ly.v.data_ptr(), ly.o.data_ptr(),
+                     ws.do.data_ptr(), ly.lse.data_ptr(), ws.am.data_ptr(), ws.delta.data_ptr(), ws.dq.data_ptr(),
+                     ws.dqkv.data_ptr(), self._g32(p + "attention.self.qkv.bias").data_ptr(), ws.cos.data_ptr(),
+                     ws.sin.data_ptr(), qs, B, nh, S, dh, st, flops=10.0 * B * nh * S * S * dh)
+            else:
+                call("esm_attn_bwd", kdt, ly.q.data_ptr(), ly.k.data_ptr(), ly.v.data_ptr(), ly.o.data_ptr(),
+                     ws.do.data_ptr(), ly.lse.data_ptr(), ws.am.data_ptr(), ws.delta.data_ptr(), ws.dq.data_ptr(),
+                     ws.dk.data_ptr(), ws.dv.data_ptr(), B, nh, S, dh, st, flops=10.0 * B * nh * S * S * dh)
+                call("esm_qkv_rope_bwd", kdt, ws.dq.data_ptr(), ws.dk.data_ptr(), ws.dv.data_ptr(),
+                     ws.dqkv.data_ptr(), self._g32(p + "attention.self.qkv.bias").data_ptr(), ws.cos.data_ptr(),
+                     ws.sin.data_ptr(), B, S, nh, dh, qs, st)
             self.linear_dgrad(ws.dqkv, p + "attention.self.qkv.weight", 3 * H, H, ws.dh)
             self.linear_wgrad(ws.dqkv, ly.h1, p + "attention.self.qkv.weight", 3 * H, H)
             prev_b2 = f"esm.encoder.layer.{l - 1}.output.dense.bias" if l > 0 else None

@@ -285,3 +285,42 @@ def test_gemm_qkv_rope_epilogue(B, S, nh, dh):
     assert rel(q, rope(qkv[0] * qs)) < 2e-2
     assert rel(k, rope(qkv[1])) < 2e-2
     assert rel(v, qkv[2]) < 2e-2
+
+
+@pytest.mark.parametrize("B,S,nh,dh,lens", [(2, 256, 3, 24, [256, 130]), (2, 192, 2, 64, [192, 64]),
+                                            (1, 128, 4, 16, [128]), (2, 100, 2, 32, [100, 37])])
+def test_attention_bwd_qkv_fused(B, S, nh, dh, lens):
+    """esm_attn_bwd_qkv (dqkv with RoPE^T + bias grads) == esm_attn_bwd + esm_qkv_rope_bwd."""
+    from paper_2411_10548_b200.model import rope_tables
+    torch.manual_seed(6)
+    H = nh * dh
+    am = torch.zeros(B, S, dtype=torch.int32, device=DEV)
+    for i, n in enumerate(lens):
+        am[i, :n] = 1
+    q, k, v = ((torch.randn(B, nh, S, dh, device=DEV) * 0.5).bfloat16() for _ in range(3))
+    o = torch.empty(B * S, H, device=DEV, dtype=torch.bfloat16)
+    lse = torch.empty(B, nh, S, device=DEV)
+    _lib.call("esm_attn_fwd", ESM_BF16, q.data_ptr(), k.data_ptr(), v.data_ptr(), am.data_ptr(), o.data_ptr(),
+              lse.data_ptr(), B, nh, S, dh, st())
+    do = torch.randn(B * S, H, device=DEV).bfloat16()
+    cos, sin = (torch.from_numpy(t).to(DEV) for t in rope_tables(S, dh))
+    qs = dh ** -0.5
+    delta = torch.empty(B, nh, S, device=DEV)
+    dq = torch.empty(B, nh, S, dh, device=DEV)
+    dk, dv = torch.empty_like(q), torch.empty_like(q)
+    _lib.call("esm_attn_bwd", ESM_BF16, q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), do.data_ptr(),
+              lse.data_ptr(), am.data_ptr(), delta.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), B, nh, S,
+              dh, st())
+    ref = torch.empty(B * S, 3 * H, device=DEV, dtype=torch.bfloat16)
+    ref_cs = torch.zeros(3 * H, device=DEV)
+    _lib.call("esm_qkv_rope_bwd", ESM_BF16, dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), ref.data_ptr(),
+              ref_cs.data_ptr(), cos.data_ptr(), sin.data_ptr(), B, S, nh, dh, qs, st())
+    got = torch.empty_like(ref)
+    cs = torch.zeros(3 * H, device=DEV)
+    ws = torch.empty(B * S, H, device=DEV)
+    _lib.call("esm_attn_bwd_qkv", q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), do.data_ptr(),
+              lse.data_ptr(), am.data_ptr(), delta.data_ptr(), ws.data_ptr(), got.data_ptr(), cs.data_ptr(),
+              cos.data_ptr(), sin.data_ptr(), qs, B, nh, S, dh, st())
+    torch.cuda.synchronize()
+    assert rel(got, ref) < 2e-2
+    assert rel(cs, ref_cs) < 2e-2
