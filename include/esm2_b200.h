@@ -115,14 +115,14 @@ int esm_qkv_rope_bwd(int dtype, const float* dq, const void* dk, const void* dv,
 /* q,k,v [B,nh,S,dh]; key_mask [B,S] int32 (0 = padded key); o [T, nh*dh]; lse [B,nh,S] fp32. */
 int esm_attn_fwd(int dtype, const void* q, const void* k, const void* v, const int32_t* key_mask, void* o,
                  float* lse, int B, int nh, int S, int dh, esm_stream_t stream);
-/* dO [T, nh*dh]; outputs dq (fp32 accum, zeroed by callee), dk, dv [B,nh,S,dh]; delta workspace [B,nh,S] fp32. */
+/* dO [T, nh*dh]; outputs dq (fp32 accum, zeroed by callee), dk, dv [B,nh,S,dh]; delta workspace [2,B,nh,S] fp32. */
 int esm_attn_bwd(int dtype, const void* q, const void* k, const void* v, const void* o, const void* dout,
                  const float* lse, const int32_t* key_mask, float* delta, float* dq, void* dk, void* dv,
                  int B, int nh, int S, int dh, esm_stream_t stream);
 
 /* Fused backward for the ESM layer (bf16, S % 4 == 0): writes dqkv[T, 3H] = [dq, dk, dv] with RoPEᵀ (and
  * q_scale on dq) applied -- the layout the QKV dgrad / wgrad GEMMs consume -- and col_sum[3H] += the q/k/v
- * bias gradients.  dq_ws: fp32 [T, H] workspace (zeroed by callee); delta: [B, nh, S] fp32 workspace. */
+ * bias gradients.  dq_ws: fp32 [T, H] workspace (zeroed by callee); delta: [2, B, nh, S] fp32 workspace. */
 int esm_attn_bwd_qkv(const void* q, const void* k, const void* v, const void* o, const void* dout,
                      const float* lse, const int32_t* key_mask, float* delta, float* dq_ws, void* dqkv,
                      float* col_sum, const float* cos_t, const float* sin_t, float q_scale, int B, int nh, int S,

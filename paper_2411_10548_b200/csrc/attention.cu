@@ -261,7 +261,8 @@ __global__ void __launch_bounds__(128) fwd_bf16_kernel(const __nv_bfloat16* __re
 // heads of a token, i.e. contiguous 16-byte vectors of the token-major [T, H] rows.
 template <typename T>
 __global__ void delta_kernel(const T* __restrict__ O, const T* __restrict__ dO, float* __restrict__ delta,
-                             int64_t T_, int S, int nh, int dh) {
+                             const float* __restrict__ lse, float* __restrict__ lse2, int64_t T_, int S, int nh,
+                             int dh) {
   constexpr int VEC = vec16<T>::N;
   const int H = nh * dh;
   const int64_t total = T_ * nh;
@@ -279,7 +280,9 @@ __global__ void delta_kernel(const T* __restrict__ O, const T* __restrict__ dO, 
       for (int e = 0; e < VEC; ++e) acc += a[e] * c[e];
     }
     const int64_t b = t / S, s = t % S;
-    delta[(b * nh + h) * S + s] = acc;
+    const int64_t idx = (b * nh + h) * S + s;
+    delta[idx] = acc;
+    if (lse2) lse2[idx] = lse[idx] * L2E;  // log2-domain LSE for the tcgen05 backward
   }
 }
 
@@ -718,7 +721,7 @@ __global__ void dq_finalize_kernel(const float* __restrict__ dq, __nv_bfloat16* 
 namespace esm {
 int attn_fwd_tc(const void* q, const void* k, const void* v, const int32_t* km, void* o, float* lse, int B, int nh,
                 int S, int dh, cudaStream_t st);
-int attn_bwd_tc(const void* q, const void* k, const void* v, const void* dout, const float* lse, const float* delta,
+int attn_bwd_tc(const void* q, const void* k, const void* v, const void* dout, const float* lse2, const float* delta,
                 const int32_t* km, float* dq, void* dk, void* dv, int B, int nh, int S, int dh, cudaStream_t st,
                 void* dqkv, float* col_sum, const float* cos_t, const float* sin_t);
 static int legacy_attention() {
@@ -771,11 +774,13 @@ extern "C" int esm_attn_bwd(int dtype, const void* q, const void* k, const void*
   int dgrid = (int)((T_ * nh + 255) / 256);
   if (dgrid > 148 * 32) dgrid = 148 * 32;
   if (dtype == ESM_BF16) {
+    const bool tc = !legacy_attention() && S % 4 == 0;
+    float* lse2 = delta + T_ * nh;  // workspace [2, B, nh, S]: Delta then log2-domain LSE
     attn::delta_kernel<__nv_bfloat16><<<dgrid, 256, 0, st>>>((const __nv_bfloat16*)o, (const __nv_bfloat16*)dout,
-                                                             delta, T_, S, nh, dh);
+                                                             delta, lse, tc ? lse2 : nullptr, T_, S, nh, dh);
     cudaMemsetAsync(dq, 0, sizeof(float) * T_ * nh * dh, st);
-    if (!legacy_attention() && S % 4 == 0) {
-      const int rc = attn_bwd_tc(q, k, v, dout, lse, delta, key_mask, dq, dk, dv, B, nh, S, dh, st, nullptr, nullptr,
+    if (tc) {
+      const int rc = attn_bwd_tc(q, k, v, dout, lse2, delta, key_mask, dq, dk, dv, B, nh, S, dh, st, nullptr, nullptr,
                                  nullptr, nullptr);
       if (rc) return rc;
       ESM_LAUNCH_RET();
@@ -802,7 +807,8 @@ extern "C" int esm_attn_bwd(int dtype, const void* q, const void* k, const void*
 #undef BWD
   } else {
     ESM_CHECK_ARG(dh <= attn::MAXD, "esm_attn_bwd: dh <= 64");
-    attn::delta_kernel<float><<<dgrid, 256, 0, st>>>((const float*)o, (const float*)dout, delta, T_, S, nh, dh);
+    attn::delta_kernel<float><<<dgrid, 256, 0, st>>>((const float*)o, (const float*)dout, delta, lse, nullptr, T_, S, nh,
+                                                     dh);
     attn::bwd_dq_f32_kernel<<<grid, 64, 0, st>>>((const float*)q, (const float*)k, (const float*)v,
                                                  (const float*)dout, lse, delta, key_mask, dq, S, nh, dh);
     attn::bwd_dkv_f32_kernel<<<grid, 64, 0, st>>>((const float*)q, (const float*)k, (const float*)v,
@@ -823,10 +829,11 @@ extern "C" int esm_attn_bwd_qkv(const void* q, const void* k, const void* v, con
   const int64_t T_ = (int64_t)B * S;
   int dgrid = (int)((T_ * nh + 255) / 256);
   if (dgrid > 148 * 32) dgrid = 148 * 32;
+  float* lse2 = delta + T_ * nh;
   attn::delta_kernel<__nv_bfloat16><<<dgrid, 256, 0, st>>>((const __nv_bfloat16*)o, (const __nv_bfloat16*)dout,
-                                                           delta, T_, S, nh, dh);
+                                                           delta, lse, lse2, T_, S, nh, dh);
   cudaMemsetAsync(dq_ws, 0, sizeof(float) * T_ * nh * dh, st);
-  const int rc = attn_bwd_tc(q, k, v, dout, lse, delta, key_mask, dq_ws, nullptr, nullptr, B, nh, S, dh, st, dqkv,
+  const int rc = attn_bwd_tc(q, k, v, dout, lse2, delta, key_mask, dq_ws, nullptr, nullptr, B, nh, S, dh, st, dqkv,
                              col_sum, cos_t, sin_t);
   if (rc) return rc;
   const int pairs = nh * dh / 2;

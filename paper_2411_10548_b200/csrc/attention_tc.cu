@@ -11,6 +11,7 @@
 // Head dims 16/24/32/64 are zero-padded by TMA (OOB fill) to DP = 16/32/32/64 and use the
 // matching 32/64/64/128-byte swizzle.  Right-padded (prefix) key masks skip whole key tiles;
 // arbitrary masks fall back to per-key mask loads.
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -388,7 +389,26 @@ struct FusedOut {
   const float* cos_t;   // [S, dh/2]
   const float* sin_t;
   int H;
+  unsigned long long* trace;  // debug timeline (nullptr in production): [role][block][event]
 };
+
+// trace slots: role r (0 = MMA, 1 = softmax warp 2, 2 = softmax warp 6), block i (< 64), event e (< 8)
+__device__ __forceinline__ void trace_ev(unsigned long long* tr, int role, int i, int e) {
+  if (tr != nullptr && blockIdx.x == 3 && blockIdx.y == 5 && i < 64) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+    tr[(role * 64 + i) * 8 + e] = t;
+  }
+}
+
+__device__ __forceinline__ void tma_reduce_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit_group() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 template <int DH>
 struct BwdShape {
@@ -398,7 +418,8 @@ struct BwdShape {
   static constexpr int NBUF = DP <= 32 ? 3 : 2;  // {S^T, dP^T} TMEM buffers (128 columns each)
   static constexpr int QST = DP <= 32 ? 6 : 4;   // Q / dO / LSE / Delta stages (>= NBUF + 1)
   static constexpr int DS_BUF = 2 * 128 * 128;  // one pair: [2 query chunks of 64][128 key rows][128 B]
-  static constexpr int SMEM = 2 * DS_BUF + 2 * KB + 2 * QST * QB + 2 * QST * 64 * 4 + 1024 + 256;
+  static constexpr int DQ_STAGE = 4 * 32 * DH * 4;  // fused dQ drain: 4 warps x 32 rows x DH fp32
+  static constexpr int SMEM = 2 * DS_BUF + 2 * KB + 2 * QST * QB + 2 * QST * 64 * 4 + DQ_STAGE + 1024 + 256;
 };
 
 // TMEM: {S^T, dP^T} x NBUF buffers (64 columns each) at [0, 128*NBUF); dV, dK, 2 x dQ (DP columns each).
@@ -406,9 +427,9 @@ template <int DH>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
-               const int32_t* __restrict__ key_mask, const float* __restrict__ LSE, const float* __restrict__ Delta,
-               float* __restrict__ dQ, __nv_bfloat16* __restrict__ dK, __nv_bfloat16* __restrict__ dV, int S,
-               int nh, const FusedOut fo) {
+               const __grid_constant__ CUtensorMap tmdQ, const int32_t* __restrict__ key_mask,
+               const float* __restrict__ LSE2, const float* __restrict__ Delta, float* __restrict__ dQ,
+               __nv_bfloat16* __restrict__ dK, __nv_bfloat16* __restrict__ dV, int S, int nh, const FusedOut fo) {
   using BS = BwdShape<DH>;
   constexpr int DP = BS::DP, ROWB = BS::ROWB, QB = BS::QB, KB = BS::KB, QST = BS::QST, NBUF = BS::NBUF;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -420,7 +441,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint8_t* sdO = sQ + QST * QB;      // [QST][QB]
   float* sL = reinterpret_cast<float*>(sdO + QST * QB);  // [QST][64]
   float* sD = sL + QST * 64;                             // [QST][64]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sD + QST * 64);
+  float* sDQ = sD + QST * 64;                            // [4][32][DH] fused dQ staging
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sDQ + 4 * 32 * DH);
   uint64_t* kv_full = bars;
   uint64_t* qdo_full = bars + 1;           // [QST]
   uint64_t* qdo_empty = qdo_full + QST;    // [QST]
@@ -509,7 +531,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tma_load_2d(sQ + st * QB, &tmQ, &qdo_full[st], 0, row0 + q0);
         tma_load_2d(sdO + st * QB, &tmdO, &qdo_full[st], h * DH, b * S + q0);
         if (vb) {
-          bulk_load(sL + st * 64, LSE + (int64_t)bh * S + q0, vb, &qdo_full[st]);
+          bulk_load(sL + st * 64, LSE2 + (int64_t)bh * S + q0, vb, &qdo_full[st]);
           bulk_load(sD + st * 64, Delta + (int64_t)bh * S + q0, vb, &qdo_full[st]);
         }
       }
@@ -543,7 +565,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     for (int j = 0; j < NBUF && j < nqe; ++j) issue_s(j);
     for (int i = 0; i < nqe; ++i) {
       const int st = i % QST, p = i >> 1;
+      if (lane == 0) trace_ev(fo.trace, 0, i, 0);
       mbar_wait(&ds_full[i % NBUF], (i / NBUF) & 1);
+      if (lane == 0) trace_ev(fo.trace, 0, i, 1);
       if ((i & 1) && p >= 2) mbar_wait(&dq_empty[p & 1], ((p >> 1) - 1) & 1);
       tc_fence_after();
       if (lane == 0) {
@@ -567,9 +591,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
         mma_commit(&qdo_empty[st]);
         if (i == nqe - 1) mma_commit(dkv_done);
+        trace_ev(fo.trace, 0, i, 2);
       }
       __syncwarp();
       if (i + NBUF < nqe) issue_s(i + NBUF);  // buffer i % NBUF is free once dV/dK(i) are issued (in-order)
+      if (lane == 0) trace_ev(fo.trace, 0, i, 3);
     }
   } else {
     // ============ softmax-bwd (thread = key row; 2 warps per lane quarter, 32 queries each) + dQ drain ============
@@ -581,11 +607,44 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const uint32_t lane_off = (uint32_t)(qq * 32) << 16;
     constexpr int DQH = DP / 2;  // dQ columns drained by this warp
 
-    auto drain_dq = [&](int pp) {  // thread = query row of pair pp, columns [hf*DQH, hf*DQH + DQH)
+    auto drain_dq = [&](int pp) {  // thread = query row of pair pp
       mbar_wait(&dq_full[pp & 1], (pp >> 1) & 1);
       tc_fence_after();
-      uint32_t u[DQH];
       const uint32_t tq = tdQ0 + (pp & 1) * DP;
+      if (fo.dqkv) {
+        // fused: the hf == 0 warp of each lane quarter drains all DP columns through smem and a
+        // TMA bulk reduce-add of its 32 x DH tile into the token-major fp32 dQ workspace
+        if (hf == 0) {
+          uint32_t u[DP];
+#pragma unroll
+          for (int c = 0; c < DP; c += 8)
+            tmem_ld8(tq + lane_off + c, u[c], u[c + 1], u[c + 2], u[c + 3], u[c + 4], u[c + 5], u[c + 6], u[c + 7]);
+          tmem_ld_wait();
+          tc_fence_before();
+          float* stage = sDQ + qq * 32 * DH;
+          if (lane == 0) bulk_wait_read0();  // previous reduce from this staging tile has read it
+          __syncwarp();
+          float4* row = reinterpret_cast<float4*>(stage + lane * DH);
+#pragma unroll
+          for (int c = 0; c < DH; c += 4)
+            row[c / 4] = make_float4(__uint_as_float(u[c]), __uint_as_float(u[c + 1]), __uint_as_float(u[c + 2]),
+                                     __uint_as_float(u[c + 3]));
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(&dq_empty[pp & 1]);
+            // rows past this sequence carry exact zeros (dS = 0 there), so spilling into the next rows is harmless
+            tma_reduce_2d(&tmdQ, stage, h * DH, b * S + pp * 128 + qq * 32);
+            bulk_commit_group();
+          }
+        } else {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&dq_empty[pp & 1]);
+        }
+        return;
+      }
+      uint32_t u[DQH];
 #pragma unroll
       for (int c = 0; c < DQH; c += 8)
         tmem_ld8(tq + lane_off + hf * DQH + c, u[c], u[c + 1], u[c + 2], u[c + 3], u[c + 4], u[c + 5], u[c + 6],
@@ -596,8 +655,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       if (lane == 0) mbar_arrive(&dq_empty[pp & 1]);
       const int q = pp * 128 + kr;
       if (q < S) {
-        float* dst = (fo.dqkv ? dQ + ((int64_t)b * S + q) * fo.H + h * DH : dQ + ((int64_t)bh * S + q) * DH) +
-                     hf * DQH;
+        float* dst = dQ + ((int64_t)bh * S + q) * DH + hf * DQH;
 #pragma unroll
         for (int c = 0; c < DQH; c += 4)
           if (hf * DQH + c < DH)
@@ -612,34 +670,56 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const float* lse = sL + st * 64 + c;
       const float* dl = sD + st * 64 + c;
       const uint32_t tS = tbase + (i % NBUF) * 128, tDP = tS + 64;
+      const int trole = (warp == 2) ? 1 : (warp == 6 ? 2 : -1);
+      if (lane == 0 && trole > 0) trace_ev(fo.trace, trole, i, 0);
       mbar_wait(&s_full[i % NBUF], (i / NBUF) & 1);
+      if (lane == 0 && trole > 0) trace_ev(fo.trace, trole, i, 1);
       tc_fence_after();
       uint32_t us[32], ud[32];
       tmem_ld32(tS + lane_off + c, us);
       tmem_ld32(tDP + lane_off + c, ud);
       if (ch == 0 && p >= 2) mbar_wait(&dsm_empty[p & 1], ((p >> 1) - 1) & 1);
       tmem_ld_wait();
+      if (lane == 0 && trole > 0) trace_ev(fo.trace, trole, i, 2);
       uint32_t pp[16], dd[16];
       const int qmax = S - i * 64 - c;
+      if (__all_sync(0xffffffffu, kvalid) && qmax >= 32) {  // full tile: no masking
 #pragma unroll
-      for (int e = 0; e < 32; e += 4) {
-        const float4 l4 = *reinterpret_cast<const float4*>(lse + e);
-        const float4 d4 = *reinterpret_cast<const float4*>(dl + e);
-        const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv4[4] = {d4.x, d4.y, d4.z, d4.w};
-        float pr[4], ds[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float pe = ex2((__uint_as_float(us[e + u]) - lv[u]) * L2E);
-          pr[u] = (kvalid && e + u < qmax) ? pe : 0.f;
-          ds[u] = pr[u] * (__uint_as_float(ud[e + u]) - dv4[u]);
+        for (int e = 0; e < 32; e += 4) {
+          const float4 l4 = *reinterpret_cast<const float4*>(lse + e);
+          const float4 d4 = *reinterpret_cast<const float4*>(dl + e);
+          const float p0 = ex2(fmaf(__uint_as_float(us[e]), L2E, -l4.x));
+          const float p1 = ex2(fmaf(__uint_as_float(us[e + 1]), L2E, -l4.y));
+          const float p2 = ex2(fmaf(__uint_as_float(us[e + 2]), L2E, -l4.z));
+          const float p3 = ex2(fmaf(__uint_as_float(us[e + 3]), L2E, -l4.w));
+          pp[e >> 1] = pack2(p0, p1);
+          pp[(e >> 1) + 1] = pack2(p2, p3);
+          dd[e >> 1] = pack2(p0 * (__uint_as_float(ud[e]) - d4.x), p1 * (__uint_as_float(ud[e + 1]) - d4.y));
+          dd[(e >> 1) + 1] = pack2(p2 * (__uint_as_float(ud[e + 2]) - d4.z), p3 * (__uint_as_float(ud[e + 3]) - d4.w));
         }
-        pp[e >> 1] = pack2(pr[0], pr[1]);
-        pp[(e >> 1) + 1] = pack2(pr[2], pr[3]);
-        dd[e >> 1] = pack2(ds[0], ds[1]);
-        dd[(e >> 1) + 1] = pack2(ds[2], ds[3]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 32; e += 4) {
+          const float4 l4 = *reinterpret_cast<const float4*>(lse + e);
+          const float4 d4 = *reinterpret_cast<const float4*>(dl + e);
+          const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv4[4] = {d4.x, d4.y, d4.z, d4.w};
+          float pr[4], ds[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float pe = ex2(fmaf(__uint_as_float(us[e + u]), L2E, -lv[u]));
+            pr[u] = (kvalid && e + u < qmax) ? pe : 0.f;
+            ds[u] = pr[u] * (__uint_as_float(ud[e + u]) - dv4[u]);
+          }
+          pp[e >> 1] = pack2(pr[0], pr[1]);
+          pp[(e >> 1) + 1] = pack2(pr[2], pr[3]);
+          dd[e >> 1] = pack2(ds[0], ds[1]);
+          dd[(e >> 1) + 1] = pack2(ds[2], ds[3]);
+        }
       }
       // both warps of this lane quarter must have read S^T / dP^T before the packed P^T / dS^T overwrite them
+      if (lane == 0 && trole > 0) trace_ev(fo.trace, trole, i, 3);
       asm volatile("bar.sync %0, 64;" ::"r"(1 + qq) : "memory");
+      if (lane == 0 && trole > 0) trace_ev(fo.trace, trole, i, 4);
       tmem_st16(tS + lane_off + hf * 16, pp);
       tmem_st16(tDP + lane_off + hf * 16, dd);
       uint8_t* rowp = sdS + (p & 1) * BS::DS_BUF + ch * (128 * 128) + kr * 128;
@@ -654,9 +734,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&ds_full[i % NBUF]);
+      if (lane == 0 && trole > 0) trace_ev(fo.trace, trole, i, 5);
       if (ch == 1 && p >= 1) drain_dq(p - 1);  // dQ of the previous pair finished long ago (double buffered)
+      if (lane == 0 && trole > 0) trace_ev(fo.trace, trole, i, 6);
     }
     drain_dq(npairs - 1);
+    if (fo.dqkv && hf == 0 && lane == 0) bulk_wait_all0();
     // ---- final rows: dK (hf == 0) or dV (hf == 1)
     mbar_wait(dkv_done, 0);
     tc_fence_after();
@@ -783,19 +866,19 @@ int launch_fwd(const void* q, const void* k, const void* v, const int32_t* km, v
 
 
 template <int DH>
-int launch_bwd(const void* q, const void* k, const void* v, const void* dout, const float* lse, const float* delta,
+int launch_bwd(const void* q, const void* k, const void* v, const void* dout, const float* lse2, const float* delta,
                const int32_t* km, float* dq, void* dk, void* dv, int B, int nh, int S, cudaStream_t st,
                FusedOut fo) {
   using SH = Shape<DH, 64>;
   using BS = BwdShape<DH>;
-  CUtensorMap tq, tk, tv, tdo;
+  CUtensorMap tq, tk, tv, tdo, tdq;
   const int64_t rows = (int64_t)B * nh * S;
   int rc;
   if ((rc = head_map<DH, 64>(&tq, q, rows)) || (rc = head_map<DH, 128>(&tk, k, rows)) ||
       (rc = head_map<DH, 128>(&tv, v, rows)))
     return rc;
+  PFN_encodeTiled enc = encoder();
   {  // dO is token-major [B*S, nh*DH]; box = DP columns of one head x 64 tokens
-    PFN_encodeTiled enc = encoder();
     cuuint64_t dims[2] = {(cuuint64_t)nh * DH, (cuuint64_t)B * S};
     cuuint64_t strides[1] = {(cuuint64_t)nh * DH * 2};
     cuuint32_t box[2] = {(cuuint32_t)SH::DP, 64};
@@ -810,29 +893,49 @@ int launch_bwd(const void* q, const void* k, const void* v, const void* dout, co
       return ESM_EDRIVER;
     }
   }
+  if (fo.dqkv) {  // fused: token-major fp32 dQ workspace [B*S, nh*DH]; box = DH columns x 32 tokens
+    cuuint64_t dims[2] = {(cuuint64_t)nh * DH, (cuuint64_t)B * S};
+    cuuint64_t strides[1] = {(cuuint64_t)nh * DH * 4};
+    cuuint32_t box[2] = {(cuuint32_t)DH, 32};
+    cuuint32_t estr[2] = {1, 1};
+    if (enc(&tdq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, dq, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+      set_last_error("attention bwd: dQ tensor map encode failed");
+      return ESM_EDRIVER;
+    }
+  } else {
+    tdq = tdo;  // unused
+  }
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(bwd_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, BS::SMEM);
     attr = true;
   }
   dim3 grid((S + 127) / 128, B * nh);
-  bwd_kernel<DH><<<grid, kBwdThreads, BS::SMEM, st>>>(tq, tk, tv, tdo, km, lse, delta, dq, (__nv_bfloat16*)dk,
-                                                      (__nv_bfloat16*)dv, S, nh, fo);
+  bwd_kernel<DH><<<grid, kBwdThreads, BS::SMEM, st>>>(tq, tk, tv, tdo, tdq, km, lse2, delta, dq,
+                                                      (__nv_bfloat16*)dk, (__nv_bfloat16*)dv, S, nh, fo);
   ESM_LAUNCH_RET();
 }
 
 }  // namespace fa
 
-int attn_bwd_tc(const void* q, const void* k, const void* v, const void* dout, const float* lse, const float* delta,
+static unsigned long long* g_attn_trace = nullptr;
+
+int attn_bwd_tc(const void* q, const void* k, const void* v, const void* dout, const float* lse2, const float* delta,
                 const int32_t* km, float* dq, void* dk, void* dv, int B, int nh, int S, int dh, cudaStream_t st,
                 void* dqkv, float* col_sum, const float* cos_t, const float* sin_t) {
   ESM_CHECK_ARG(S % 4 == 0, "attention bwd (tcgen05): S %% 4 == 0 required");
-  fa::FusedOut fo{(__nv_bfloat16*)dqkv, col_sum, cos_t, sin_t, nh * dh};
+  if (getenv("ESM_ATTN_TRACE") && g_attn_trace == nullptr) {
+    cudaMalloc(&g_attn_trace, 3 * 64 * 8 * 8);
+    cudaMemset(g_attn_trace, 0, 3 * 64 * 8 * 8);
+  }
+  fa::FusedOut fo{(__nv_bfloat16*)dqkv, col_sum, cos_t, sin_t, nh * dh, g_attn_trace};
   switch (dh) {
-    case 16: return fa::launch_bwd<16>(q, k, v, dout, lse, delta, km, dq, dk, dv, B, nh, S, st, fo);
-    case 24: return fa::launch_bwd<24>(q, k, v, dout, lse, delta, km, dq, dk, dv, B, nh, S, st, fo);
-    case 32: return fa::launch_bwd<32>(q, k, v, dout, lse, delta, km, dq, dk, dv, B, nh, S, st, fo);
-    case 64: return fa::launch_bwd<64>(q, k, v, dout, lse, delta, km, dq, dk, dv, B, nh, S, st, fo);
+    case 16: return fa::launch_bwd<16>(q, k, v, dout, lse2, delta, km, dq, dk, dv, B, nh, S, st, fo);
+    case 24: return fa::launch_bwd<24>(q, k, v, dout, lse2, delta, km, dq, dk, dv, B, nh, S, st, fo);
+    case 32: return fa::launch_bwd<32>(q, k, v, dout, lse2, delta, km, dq, dk, dv, B, nh, S, st, fo);
+    case 64: return fa::launch_bwd<64>(q, k, v, dout, lse2, delta, km, dq, dk, dv, B, nh, S, st, fo);
     default: set_last_error("attention: head dim %d unsupported", dh); return ESM_ENOTSUP;
   }
 }
@@ -851,3 +954,9 @@ int attn_fwd_tc(const void* q, const void* k, const void* v, const int32_t* km, 
 }
 
 }  // namespace esm
+
+extern "C" int esm_debug_attn_trace(unsigned long long* host_out) {
+  // debug only: the last attention-backward timeline recorded with ESM_ATTN_TRACE=1 (3 x 64 x 8 clock64)
+  if (esm::g_attn_trace == nullptr) return ESM_ENOTSUP;
+  return (int)cudaMemcpy(host_out, esm::g_attn_trace, 3 * 64 * 8 * 8, cudaMemcpyDeviceToHost);
+}

@@ -216,7 +216,7 @@ class Workspace:
         self.dq = e(B, nh, S, dh, dt=f32)
         self.dk, self.dv = e(B, nh, S, dh), e(B, nh, S, dh)
         self.dqkv = e(T, 3 * H)
-        self.delta = e(B, nh, S, dt=f32)
+        self.delta = e(2, B, nh, S, dt=f32)  # Delta and log2-domain LSE (attention backward workspace)
         cos, sin = rope_tables(S, dh)
         self.cos = torch.from_numpy(cos).to(device)
         self.sin = torch.from_numpy(sin).to(device)

@@ -21,7 +21,7 @@ def run(B, nh, S, dh, lens):
     do = torch.randn(B * S, nh * dh, device="cuda").bfloat16()
     ref.backward(do.float())
     dq = torch.empty(B, nh, S, dh, device="cuda"); dk = torch.empty_like(q); dv = torch.empty_like(q)
-    delta = torch.empty(B, nh, S, device="cuda")
+    delta = torch.empty(2, B, nh, S, device="cuda")
     _lib.call("esm_attn_bwd", ESM_BF16, q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), do.data_ptr(), lse.data_ptr(), am.data_ptr(), delta.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), B, nh, S, dh, st)
     torch.cuda.synchronize()
     print(f"B={B} nh={nh} S={S} dh={dh} lens={lens}")

@@ -60,7 +60,7 @@ def attn():
         do = torch.randn_like(o)
         dq = torch.empty(B, nh, S, dh, device="cuda")
         dk, dv = torch.empty_like(q), torch.empty_like(q)
-        delta = torch.empty(B, nh, S, device="cuda")
+        delta = torch.empty(2, B, nh, S, device="cuda")
         f = lambda: _lib.call("esm_attn_fwd", ESM_BF16, q.data_ptr(), k.data_ptr(), v.data_ptr(), am.data_ptr(),  # noqa
                               o.data_ptr(), lse.data_ptr(), B, nh, S, dh, cur())
         g = lambda: _lib.call("esm_attn_bwd", ESM_BF16, q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),  # noqa

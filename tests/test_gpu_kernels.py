@@ -162,7 +162,7 @@ def test_attention_fwd_bwd(dh, S, lens, dt):
     dq = torch.empty(B, nh, S, dh, device=DEV)
     dk = torch.empty(B, nh, S, dh, device=DEV, dtype=tdt)
     dv = torch.empty_like(dk)
-    delta = torch.empty(B, nh, S, device=DEV)
+    delta = torch.empty(2, B, nh, S, device=DEV)
     _lib.call("esm_attn_bwd", kdt, q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), do.data_ptr(),
               lse.data_ptr(), am.data_ptr(), delta.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), B, nh,
               S, dh, st())
@@ -305,7 +305,7 @@ def test_attention_bwd_qkv_fused(B, S, nh, dh, lens):
     do = torch.randn(B * S, H, device=DEV).bfloat16()
     cos, sin = (torch.from_numpy(t).to(DEV) for t in rope_tables(S, dh))
     qs = dh ** -0.5
-    delta = torch.empty(B, nh, S, device=DEV)
+    delta = torch.empty(2, B, nh, S, device=DEV)
     dq = torch.empty(B, nh, S, dh, device=DEV)
     dk, dv = torch.empty_like(q), torch.empty_like(q)
     _lib.call("esm_attn_bwd", ESM_BF16, q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), do.data_ptr(),
