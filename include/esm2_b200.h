@@ -47,7 +47,9 @@ enum {
   ESM_EPI_RESID = 2,      /* C = acc + bias + R           (R = aux_in)    act dtype    HF:365-375, 417-427   */
   ESM_EPI_DGELU = 3,      /* C = acc * gelu'(Z) (Z = aux_in); colsum(C) -> col_sum     backward of HF:411-414 */
   ESM_EPI_F32_ACC = 4,    /* C(fp32) += acc  (weight gradients; split-K safe)                               */
-  ESM_EPI_QKV_ROPE = 5    /* acc + bias -> q*scale, RoPE(q), RoPE(k), v scattered to [B,nh,S,dh]  HF:318-344 (bf16) */
+  ESM_EPI_QKV_ROPE = 5,   /* acc + bias -> q*scale, RoPE(q), RoPE(k), v scattered to [B,nh,S,dh]  HF:318-344 (bf16) */
+  ESM_EPI_STORE_LN = 6    /* C = acc = dy of a LayerNorm; col_sum += colsum(dy) (dbeta), col_sum2 += colsum(dy * xhat)
+                             (dgamma) with xhat = (X - row_mean) * row_rstd, X = aux_in (the LN input)  (bf16)   */
 };
 
 typedef struct esm_gemm_args {
@@ -68,6 +70,10 @@ typedef struct esm_gemm_args {
   void* q_out; void* k_out; void* v_out;   /* [B, n_heads, seq_len, head_dim] */
   int seq_len, n_heads, head_dim;
   float q_scale;
+  /* ESM_EPI_STORE_LN only */
+  const float* row_mean;     /* [M] */
+  const float* row_rstd;     /* [M] */
+  float* col_sum2;           /* [N] */
 } esm_gemm_args;
 
 /* ---------------- library ---------------- */

@@ -12,7 +12,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libesm2b200.so")
 
 ESM_F32, ESM_BF16 = 0, 1
-EPI_STORE, EPI_GELU, EPI_RESID, EPI_DGELU, EPI_F32_ACC, EPI_QKV_ROPE = 0, 1, 2, 3, 4, 5
+EPI_STORE, EPI_GELU, EPI_RESID, EPI_DGELU, EPI_F32_ACC, EPI_QKV_ROPE, EPI_STORE_LN = 0, 1, 2, 3, 4, 5, 6
 
 EXPORTS = [
     "esm_version", "esm_last_error", "esm_device_sm_count", "esm_tokenize", "esm_mlm_mask", "esm_embed_fwd",
@@ -41,6 +41,7 @@ class GemmArgs(ctypes.Structure):
         ("q_out", ctypes.c_void_p), ("k_out", ctypes.c_void_p), ("v_out", ctypes.c_void_p),
         ("seq_len", ctypes.c_int), ("n_heads", ctypes.c_int), ("head_dim", ctypes.c_int),
         ("q_scale", ctypes.c_float),
+        ("row_mean", ctypes.c_void_p), ("row_rstd", ctypes.c_void_p), ("col_sum2", ctypes.c_void_p),
     ]
 
 

@@ -247,13 +247,15 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const T* __restrict__ x, co
   }
 }
 
-template <typename T, int MAXV, int WPR>
-__global__ void __launch_bounds__(256, (MAXV <= 2 && sizeof(T) == 2) ? 2 : 1) ln_bwd_kernel(const T* __restrict__ dy, const T* __restrict__ x,
-                                                     const float* __restrict__ g, const float* __restrict__ mean,
-                                                     const float* __restrict__ rstd, const T* __restrict__ dres,
-                                                     const T* __restrict__ gelu_z, T* __restrict__ dx,
-                                                     float* __restrict__ dg, float* __restrict__ db,
-                                                     float* __restrict__ csum, int64_t rows, int H) {
+// Backward.  STATS: also accumulate dgamma / dbeta here (otherwise the dgrad GEMM that produced dy
+// computes them in its epilogue, ESM_EPI_STORE_LN).  Rows are held as raw 16-byte vectors (bf16 packed)
+// and all of a row's loads are issued before the reduction.
+template <typename T, int MAXV, int WPR, bool STATS>
+__global__ void __launch_bounds__(256, (sizeof(T) == 2 && (MAXV <= 2 || !STATS)) ? 2 : 1)
+    ln_bwd_kernel(const T* __restrict__ dy, const T* __restrict__ x, const float* __restrict__ g,
+                  const float* __restrict__ mean, const float* __restrict__ rstd, const T* __restrict__ dres,
+                  const T* __restrict__ gelu_z, T* __restrict__ dx, float* __restrict__ dg, float* __restrict__ db,
+                  float* __restrict__ csum, int64_t rows, int H) {
   constexpr int VEC = vec16<T>::N;
   constexpr int GPB = 8 / WPR;
   __shared__ float2 red[GPB][2 * WPR];
@@ -263,34 +265,51 @@ __global__ void __launch_bounds__(256, (MAXV <= 2 && sizeof(T) == 2) ? 2 : 1) ln
   const int glane = wig * 32 + lane;
   int parity = 0;
   for (int i = threadIdx.x; i < 3 * H; i += blockDim.x) sacc[i] = 0.f;
-  float gv[MAXV][VEC], ag[MAXV][VEC], ab[MAXV][VEC], ac[MAXV][VEC];
+  float gv[MAXV][VEC], ac[MAXV][VEC];
+  float ag[STATS ? MAXV : 1][VEC], ab[STATS ? MAXV : 1][VEC];
 #pragma unroll
   for (int i = 0; i < MAXV; ++i) {
     const int h = (i * WPR * 32 + glane) * VEC;
     if (h < H) load_f32x(g + h, gv[i], VEC);
 #pragma unroll
-    for (int j = 0; j < VEC; ++j) ag[i][j] = ab[i][j] = ac[i][j] = 0.f;
+    for (int j = 0; j < VEC; ++j) ac[i][j] = 0.f;
+    if constexpr (STATS) {
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) ag[i][j] = ab[i][j] = 0.f;
+    }
   }
   const float invH = 1.0f / H;
   for (int64_t r = (int64_t)blockIdx.x * GPB + grp; r < rows; r += (int64_t)gridDim.x * GPB) {
     const float mu = mean[r], rs = rstd[r];
-    float xh[MAXV][VEC], gy[MAXV][VEC];
+    uint4 xr[MAXV], dr[MAXV], rr[MAXV], zr[MAXV];
+#pragma unroll
+    for (int i = 0; i < MAXV; ++i) {
+      const int h = (i * WPR * 32 + glane) * VEC;
+      if (h < H) {
+        xr[i] = *reinterpret_cast<const uint4*>(x + r * H + h);
+        dr[i] = *reinterpret_cast<const uint4*>(dy + r * H + h);
+        if (dres) rr[i] = *reinterpret_cast<const uint4*>(dres + r * H + h);
+        if (gelu_z) zr[i] = *reinterpret_cast<const uint4*>(gelu_z + r * H + h);
+      }
+    }
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
     for (int i = 0; i < MAXV; ++i) {
       const int h = (i * WPR * 32 + glane) * VEC;
       if (h < H) {
         float xv[VEC], dv[VEC];
-        load_vec(x + r * H + h, xv);
-        load_vec(dy + r * H + h, dv);
+        load_vec(reinterpret_cast<const T*>(&xr[i]), xv);
+        load_vec(reinterpret_cast<const T*>(&dr[i]), dv);
 #pragma unroll
         for (int j = 0; j < VEC; ++j) {
-          xh[i][j] = (xv[j] - mu) * rs;
-          gy[i][j] = dv[j] * gv[i][j];
-          s1 += gy[i][j];
-          s2 += gy[i][j] * xh[i][j];
-          ag[i][j] += dv[j] * xh[i][j];
-          ab[i][j] += dv[j];
+          const float xh = (xv[j] - mu) * rs;
+          const float gy = dv[j] * gv[i][j];
+          s1 += gy;
+          s2 += gy * xh;
+          if constexpr (STATS) {
+            ag[i][j] += dv[j] * xh;
+            ab[i][j] += dv[j];
+          }
         }
       }
     }
@@ -301,18 +320,20 @@ __global__ void __launch_bounds__(256, (MAXV <= 2 && sizeof(T) == 2) ? 2 : 1) ln
     for (int i = 0; i < MAXV; ++i) {
       const int h = (i * WPR * 32 + glane) * VEC;
       if (h < H) {
-        float o[VEC];
+        float xv[VEC], dv[VEC], o[VEC];
+        load_vec(reinterpret_cast<const T*>(&xr[i]), xv);
+        load_vec(reinterpret_cast<const T*>(&dr[i]), dv);
 #pragma unroll
-        for (int j = 0; j < VEC; ++j) o[j] = rs * (gy[i][j] - s1 - xh[i][j] * s2);
+        for (int j = 0; j < VEC; ++j) o[j] = rs * (dv[j] * gv[i][j] - s1 - (xv[j] - mu) * rs * s2);
         if (dres) {
           float rv[VEC];
-          load_vec(dres + r * H + h, rv);
+          load_vec(reinterpret_cast<const T*>(&rr[i]), rv);
 #pragma unroll
           for (int j = 0; j < VEC; ++j) o[j] += rv[j];
         }
         if (gelu_z) {
           float zv[VEC];
-          load_vec(gelu_z + r * H + h, zv);
+          load_vec(reinterpret_cast<const T*>(&zr[i]), zv);
 #pragma unroll
           for (int j = 0; j < VEC; ++j) o[j] *= gelu_grad_f(zv[j]);
         }
@@ -329,16 +350,18 @@ __global__ void __launch_bounds__(256, (MAXV <= 2 && sizeof(T) == 2) ? 2 : 1) ln
     if (h < H) {
 #pragma unroll
       for (int j = 0; j < VEC; ++j) {
-        atomicAdd(&sacc[h + j], ag[i][j]);
-        atomicAdd(&sacc[H + h + j], ab[i][j]);
         atomicAdd(&sacc[2 * H + h + j], ac[i][j]);
+        if constexpr (STATS) {
+          atomicAdd(&sacc[h + j], ag[i][j]);
+          atomicAdd(&sacc[H + h + j], ab[i][j]);
+        }
       }
     }
   }
   __syncthreads();
   for (int c = threadIdx.x; c < H; c += blockDim.x) {
-    if (dg) atomicAdd(dg + c, sacc[c]);
-    if (db) atomicAdd(db + c, sacc[H + c]);
+    if (STATS && dg) atomicAdd(dg + c, sacc[c]);
+    if (STATS && db) atomicAdd(db + c, sacc[H + c]);
     if (csum) atomicAdd(csum + c, sacc[2 * H + c]);
   }
 }
@@ -723,6 +746,20 @@ static inline void ln_shape(int H, int vec, int& maxv, int& wpr) {
     else { esm::set_last_error("layernorm: H=%d unsupported", H); return ESM_ENOTSUP; }  \
   } while (0)
 
+#define LN_SWITCH2(KS)                                                                   \
+  do {                                                                                   \
+    if (mv == 1 && wpr == 1) L_B(KS(1, 1));                                              \
+    else if (mv == 2 && wpr == 1) L_B(KS(2, 1));                                         \
+    else if (mv == 3 && wpr == 1) L_B(KS(3, 1));                                         \
+    else if (mv == 2 && wpr == 2) L_B(KS(2, 2));                                         \
+    else if (mv == 3 && wpr == 2) L_B(KS(3, 2));                                         \
+    else if (mv == 2 && wpr == 4) L_B(KS(2, 4));                                         \
+    else if (mv == 3 && wpr == 4) L_B(KS(3, 4));                                         \
+    else if (mv == 2 && wpr == 8) L_B(KS(2, 8));                                         \
+    else if (mv == 3 && wpr == 8) L_B(KS(3, 8));                                         \
+    else { esm::set_last_error("layernorm: H=%d unsupported", H); return ESM_ENOTSUP; }  \
+  } while (0)
+
 int esm_layernorm_fwd(int dtype, const void* x, const float* gamma, const float* beta, void* y, float* mean, float* rstd,
                       int rows, int H, float eps, esm_stream_t stream) {
   ESM_CHECK_ARG(x && gamma && beta && y && mean && rstd && rows > 0 && H > 0, "esm_layernorm_fwd: bad args");
@@ -755,6 +792,7 @@ int esm_layernorm_bwd(int dtype, const void* dy, const void* x, const float* gam
   ln_shape(H, vec, mv, wpr);
   const size_t sm = (size_t)3 * H * sizeof(float);
   ESM_CHECK_ARG(sm <= 200 * 1024, "layernorm_bwd: H too large");
+  const bool stats = dgamma != nullptr || dbeta != nullptr;
   int grid = 148 * 2;
   const int gpb = 8 / wpr;
   if ((int64_t)grid * gpb > rows) grid = (int)((rows + gpb - 1) / gpb);
@@ -767,10 +805,26 @@ int esm_layernorm_bwd(int dtype, const void* dy, const void* x, const float* gam
   } while (0)
   if (dtype == ESM_BF16) {
     using TT = __nv_bfloat16;
-    LN_SWITCH(TT, ln_bwd_kernel, L_B);
+    if (stats) {
+#define KS(A, B) ln_bwd_kernel<TT, A, B, true>
+      LN_SWITCH2(KS);
+#undef KS
+    } else {
+#define KS(A, B) ln_bwd_kernel<TT, A, B, false>
+      LN_SWITCH2(KS);
+#undef KS
+    }
   } else {
     using TT = float;
-    LN_SWITCH(TT, ln_bwd_kernel, L_B);
+    if (stats) {
+#define KS(A, B) ln_bwd_kernel<TT, A, B, true>
+      LN_SWITCH2(KS);
+#undef KS
+    } else {
+#define KS(A, B) ln_bwd_kernel<TT, A, B, false>
+      LN_SWITCH2(KS);
+#undef KS
+    }
   }
 #undef L_B
   ESM_LAUNCH_RET();

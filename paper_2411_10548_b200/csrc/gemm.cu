@@ -36,6 +36,10 @@ struct EpiParams {
   __nv_bfloat16* qkv_out[3];
   int seq_len, n_heads, head_dim;
   float q_scale;
+  // LayerNorm-gradient statistics epilogue
+  const float* row_mean;
+  const float* row_rstd;
+  float* col_sum2;
 };
 
 // ============================================================================
@@ -55,7 +59,7 @@ struct EpiCfg {
   static constexpr bool F32 = EPI == ESM_EPI_F32_ACC;
   static constexpr int CHUNK = F32 ? 32 * 32 * 4 : 32 * 32 * 2;  // bytes per 32x32 chunk
   static constexpr int NOUT = EPI == ESM_EPI_GELU ? 2 : 1;        // outputs per chunk (GELU: C and Z)
-  static constexpr bool AUX = EPI == ESM_EPI_RESID || EPI == ESM_EPI_DGELU;
+  static constexpr bool AUX = EPI == ESM_EPI_RESID || EPI == ESM_EPI_DGELU || EPI == ESM_EPI_STORE_LN;
   static constexpr int WARP_BYTES = QKV ? 0 : 2 * NOUT * CHUNK + (AUX ? 2 * CHUNK : 0);
   static constexpr int BYTES = kEpiWarps * WARP_BYTES;
 };
@@ -336,7 +340,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        if constexpr (EPI != ESM_EPI_F32_ACC && EPI != ESM_EPI_DGELU) {
+        if constexpr (EPI != ESM_EPI_F32_ACC && EPI != ESM_EPI_DGELU && EPI != ESM_EPI_STORE_LN) {
           if (ep.bias != nullptr) {
             if (col0 + 32 <= ep.N) {
               const float4* b4 = reinterpret_cast<const float4*>(ep.bias + col0);  // 1 KB aligned groups
@@ -358,17 +362,39 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&abar[ab], (aux_phase >> ab) & 1u);
           aux_phase ^= 1u << ab;
           const uint8_t* a = abuf + ab * E::CHUNK;
+          if constexpr (EPI == ESM_EPI_STORE_LN) {
+            // dbeta += colsum(dy), dgamma += colsum(dy * xhat); rows >= M carry dy == 0
+            const int row = row0 + lane;
+            const float mu = row < ep.M ? __ldg(ep.row_mean + row) : 0.f;
+            const float rs = row < ep.M ? __ldg(ep.row_rstd + row) : 0.f;
+            float w[32];
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            float rv[8];
-            load_vec(reinterpret_cast<const __nv_bfloat16*>(a + stage_off<false>(lane, k)), rv);
+            for (int k = 0; k < 4; ++k) {
+              float xv[8];
+              load_vec(reinterpret_cast<const __nv_bfloat16*>(a + stage_off<false>(lane, k)), xv);
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              if constexpr (EPI == ESM_EPI_RESID) v[8 * k + e] += rv[e];
-              else v[8 * k + e] *= gelu_grad_f(rv[e]);
+              for (int e = 0; e < 8; ++e) w[8 * k + e] = v[8 * k + e] * (xv[e] - mu) * rs;
             }
+            __syncwarp();
+            const float s2 = warp_transpose_sum32(w, lane);
+            if (col0 + lane < ep.N) red_add_f32(ep.col_sum2 + col0 + lane, s2);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) w[j] = v[j];
+            const float s1 = warp_transpose_sum32(w, lane);
+            if (col0 + lane < ep.N) red_add_f32(ep.col_sum + col0 + lane, s1);
+          } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              float rv[8];
+              load_vec(reinterpret_cast<const __nv_bfloat16*>(a + stage_off<false>(lane, k)), rv);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                if constexpr (EPI == ESM_EPI_RESID) v[8 * k + e] += rv[e];
+                else v[8 * k + e] *= gelu_grad_f(rv[e]);
+              }
+            }
+            __syncwarp();
           }
-          __syncwarp();
           ab ^= 1;
         }
         // stage the outputs (wait until the TMA store that last read this buffer is done)
@@ -504,7 +530,7 @@ static int launch(const esm_gemm_args& a, cudaStream_t st) {
     rc = make_map(&maps.c, a.C, a.N, a.M, a.ldc, 32, 32, false, CU_TENSOR_MAP_SWIZZLE_64B);
     if (!rc && EPI == ESM_EPI_GELU)
       rc = make_map(&maps.z, a.aux_out, a.N, a.M, a.ld_aux_out, 32, 32, false, CU_TENSOR_MAP_SWIZZLE_64B);
-    if (!rc && (EPI == ESM_EPI_RESID || EPI == ESM_EPI_DGELU))
+    if (!rc && (EPI == ESM_EPI_RESID || EPI == ESM_EPI_DGELU || EPI == ESM_EPI_STORE_LN))
       rc = make_map(&maps.r, a.aux_in, a.N, a.M, a.ld_aux_in, 32, 32, false, CU_TENSOR_MAP_SWIZZLE_64B);
   }
   if (rc) return rc;
@@ -541,7 +567,7 @@ static int launch(const esm_gemm_args& a, cudaStream_t st) {
   EpiParams ep{a.M, a.N, a.C, a.ldc, a.bias, a.aux_in, a.ld_aux_in, a.aux_out, a.ld_aux_out, a.col_sum,
                a.rope_cos, a.rope_sin,
                {(__nv_bfloat16*)a.q_out, (__nv_bfloat16*)a.k_out, (__nv_bfloat16*)a.v_out},
-               a.seq_len, a.n_heads, a.head_dim, a.q_scale};
+               a.seq_len, a.n_heads, a.head_dim, a.q_scale, a.row_mean, a.row_rstd, a.col_sum2};
   auto kern = gemm_tc_kernel<BN, A_MN, B_MN, EPI>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -633,6 +659,9 @@ int gemm_bf16(const esm_gemm_args& a, cudaStream_t st) {
     switch (a.epilogue) {
       case ESM_EPI_STORE: return dispatch_bn<false, true, ESM_EPI_STORE>(a, bn, st);
       case ESM_EPI_DGELU: return dispatch_bn<false, true, ESM_EPI_DGELU>(a, bn, st);
+      case ESM_EPI_STORE_LN:
+        ESM_CHECK_ARG(a.aux_in && a.row_mean && a.row_rstd && a.col_sum && a.col_sum2, "gemm: STORE_LN args");
+        return dispatch_bn<false, true, ESM_EPI_STORE_LN>(a, bn, st);
       default: break;
     }
   }
@@ -748,7 +777,8 @@ extern "C" int esm_gemm(const esm_gemm_args* args, esm_stream_t stream) {
   ESM_CHECK_ARG(args != nullptr, "esm_gemm: null args");
   const esm_gemm_args& a = *args;
   ESM_CHECK_ARG(a.M > 0 && a.N > 0 && a.K > 0, "esm_gemm: bad shape %d %d %d", a.M, a.N, a.K);
-  ESM_CHECK_ARG(a.epilogue >= 0 && a.epilogue <= ESM_EPI_QKV_ROPE, "esm_gemm: bad epilogue");
+  ESM_CHECK_ARG(a.epilogue >= 0 && a.epilogue <= ESM_EPI_STORE_LN, "esm_gemm: bad epilogue");
+  ESM_CHECK_ARG(a.epilogue != ESM_EPI_STORE_LN || a.dtype == ESM_BF16, "esm_gemm: STORE_LN is bf16-only");
   ESM_CHECK_ARG(a.epilogue != ESM_EPI_QKV_ROPE || a.dtype == ESM_BF16, "esm_gemm: QKV_ROPE is bf16-only");
   ESM_CHECK_ARG(a.epilogue != ESM_EPI_RESID || a.aux_in, "esm_gemm: RESID needs aux_in");
   ESM_CHECK_ARG(a.epilogue != ESM_EPI_DGELU || a.aux_in, "esm_gemm: DGELU needs aux_in");

@@ -33,7 +33,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import EPI_DGELU, EPI_F32_ACC, EPI_GELU, EPI_QKV_ROPE, EPI_RESID, EPI_STORE, ESM_BF16, ESM_F32
+from ._lib import (EPI_DGELU, EPI_F32_ACC, EPI_GELU, EPI_QKV_ROPE, EPI_RESID, EPI_STORE, EPI_STORE_LN, ESM_BF16,
+                   ESM_F32)
 from .config import EsmConfig
 
 ALIGN = 256  # elements; also the AdamW weight-decay chunk size
@@ -318,18 +319,24 @@ class EsmForMaskedLM:
         self.launches += self._KERNELS.get(name, 1)
 
     def _gemm(self, M, N, K, A, lda, amn, B, ldb, bmn, C, ldc, epi, bias=None, aux_in=None, ld_aux_in=0,
-              aux_out=None, ld_aux_out=0, col_sum=None):
+              aux_out=None, ld_aux_out=0, col_sum=None, ln=None):
         t = self.timer
         if t is not None:
             t.begin("gemm_" + ("wgrad" if epi == EPI_F32_ACC else "dgrad" if bmn else "fwd"))
         self.launches += 1
         self._gemm_raw(M, N, K, A, lda, amn, B, ldb, bmn, C, ldc, epi, bias, aux_in, ld_aux_in, aux_out, ld_aux_out,
-                       col_sum)
+                       col_sum, ln)
         if t is not None:
             t.end(2.0 * M * N * K, 0.0)
 
     def _gemm_raw(self, M, N, K, A, lda, amn, B, ldb, bmn, C, ldc, epi, bias, aux_in, ld_aux_in, aux_out,
-                  ld_aux_out, col_sum):
+                  ld_aux_out, col_sum, ln=None):
+        if ln is not None:  # (row_mean, row_rstd, dgamma accumulator)
+            _lib.gemm_call(self._stream(), dtype=self.kdt, M=M, N=N, K=K, A=A.data_ptr(), lda=lda, a_mn_major=amn,
+                           B=B.data_ptr(), ldb=ldb, b_mn_major=bmn, C=C.data_ptr(), ldc=ldc, epilogue=epi,
+                           aux_in=aux_in.data_ptr(), ld_aux_in=ld_aux_in, col_sum=col_sum.data_ptr(),
+                           row_mean=ln[0].data_ptr(), row_rstd=ln[1].data_ptr(), col_sum2=ln[2].data_ptr())
+            return
         _lib.gemm_call(self._stream(), dtype=self.kdt, M=M, N=N, K=K, A=A.data_ptr(), lda=lda, a_mn_major=amn,
                        B=B.data_ptr(), ldb=ldb, b_mn_major=bmn, C=C.data_ptr(), ldc=ldc, epilogue=epi,
                        bias=bias.data_ptr() if bias is not None else None,
@@ -358,11 +365,19 @@ class EsmForMaskedLM:
             t.end(2.0 * T * 3 * H * H, 0.0)
         self.launches += 1
 
-    def linear_dgrad(self, dy, wkey, out_f, in_f, dX, epi=EPI_STORE, aux_in=None, col_sum=None):
+    def linear_dgrad(self, dy, wkey, out_f, in_f, dX, epi=EPI_STORE, aux_in=None, col_sum=None, ln=None):
+        """dX = dy · W.  ln = (ln_input, mean, rstd, ln_key): dX is that LayerNorm's output gradient and the
+        epilogue also accumulates its dbeta / dgamma (bf16 path)."""
         T = dy.shape[0]
         W = self._w(wkey, (out_f, in_f))
+        if ln is not None and self.kdt == ESM_BF16:
+            x_in, mu, rs, key = ln
+            self._gemm(T, in_f, out_f, dy, out_f, 0, W, in_f, 1, dX, in_f, EPI_STORE_LN, aux_in=x_in,
+                       ld_aux_in=in_f, col_sum=self._g32(key + ".bias"), ln=(mu, rs, self._g32(key + ".weight")))
+            return True
         self._gemm(T, in_f, out_f, dy, out_f, 0, W, in_f, 1, dX, in_f, epi, aux_in=aux_in, ld_aux_in=in_f,
                    col_sum=col_sum)
+        return False
 
     def linear_wgrad(self, dy, x, wkey, out_f, in_f):
         T = dy.shape[0]
@@ -471,14 +486,15 @@ class EsmForMaskedLM:
              self._p32("lm_head.layer_norm.weight").data_ptr(), ws.lnh_m.data_ptr(), ws.lnh_r.data_ptr(), None,
              ws.y.data_ptr(), ws.dy.data_ptr(), self._g32("lm_head.layer_norm.weight").data_ptr(),
              self._g32("lm_head.layer_norm.bias").data_ptr(), self._g32("lm_head.dense.bias").data_ptr(), T, H, st)
-        self.linear_dgrad(ws.dy, "lm_head.dense.weight", H, H, ws.dh)
+        fused = self.linear_dgrad(ws.dy, "lm_head.dense.weight", H, H, ws.dh,
+                                  ln=(ws.x[L], ws.lnf_m, ws.lnf_r, "esm.encoder.emb_layer_norm_after"))
         self.linear_wgrad(ws.dy, ws.xf, "lm_head.dense.weight", H, H)
         last_b2 = f"esm.encoder.layer.{L - 1}.output.dense.bias" if L > 0 else None
         call("esm_layernorm_bwd", kdt, ws.dh.data_ptr(), ws.x[L].data_ptr(),
              self._p32("esm.encoder.emb_layer_norm_after.weight").data_ptr(), ws.lnf_m.data_ptr(),
              ws.lnf_r.data_ptr(), None, None, ws.dx.data_ptr(),
-             self._g32("esm.encoder.emb_layer_norm_after.weight").data_ptr(),
-             self._g32("esm.encoder.emb_layer_norm_after.bias").data_ptr(),
+             None if fused else self._g32("esm.encoder.emb_layer_norm_after.weight").data_ptr(),
+             None if fused else self._g32("esm.encoder.emb_layer_norm_after.bias").data_ptr(),
              self._g32(last_b2).data_ptr() if last_b2 else None, T, H, st)
         if self.comm is not None:
             self.comm.ready("esm.encoder.emb_layer_norm_after.bias")
@@ -490,13 +506,15 @@ class EsmForMaskedLM:
             self.linear_dgrad(dx, p + "output.dense.weight", H, F, ws.dz, epi=EPI_DGELU, aux_in=ly.z,
                               col_sum=self._g32(p + "intermediate.dense.bias"))
             self.linear_wgrad(dx, ly.a, p + "output.dense.weight", H, F)
-            self.linear_dgrad(ws.dz, p + "intermediate.dense.weight", F, H, ws.dh)
+            fused = self.linear_dgrad(ws.dz, p + "intermediate.dense.weight", F, H, ws.dh,
+                                      ln=(ly.x1, ly.ln2_m, ly.ln2_r, p + "LayerNorm"))
             self.linear_wgrad(ws.dz, ly.h2, p + "intermediate.dense.weight", F, H)
             call("esm_layernorm_bwd", kdt, ws.dh.data_ptr(), ly.x1.data_ptr(),
                  self._p32(p + "LayerNorm.weight").data_ptr(), ly.ln2_m.data_ptr(), ly.ln2_r.data_ptr(),
-                 dx.data_ptr(), None, ws.dx1.data_ptr(), self._g32(p + "LayerNorm.weight").data_ptr(),
-                 self._g32(p + "LayerNorm.bias").data_ptr(), self._g32(p + "attention.output.dense.bias").data_ptr(),
-                 T, H, st)
+                 dx.data_ptr(), None, ws.dx1.data_ptr(),
+                 None if fused else self._g32(p + "LayerNorm.weight").data_ptr(),
+                 None if fused else self._g32(p + "LayerNorm.bias").data_ptr(),
+                 self._g32(p + "attention.output.dense.bias").data_ptr(), T, H, st)
             # attention
             self.linear_dgrad(ws.dx1, p + "attention.output.dense.weight", H, H, ws.do)
             self.linear_wgrad(ws.dx1, ly.o, p + "attention.output.dense.weight", H, H)
@@ -513,13 +531,15 @@ class EsmForMaskedLM:
                 call("esm_qkv_rope_bwd", kdt, ws.dq.data_ptr(), ws.dk.data_ptr(), ws.dv.data_ptr(),
                      ws.dqkv.data_ptr(), self._g32(p + "attention.self.qkv.bias").data_ptr(), ws.cos.data_ptr(),
                      ws.sin.data_ptr(), B, S, nh, dh, qs, st)
-            self.linear_dgrad(ws.dqkv, p + "attention.self.qkv.weight", 3 * H, H, ws.dh)
+            fused = self.linear_dgrad(ws.dqkv, p + "attention.self.qkv.weight", 3 * H, H, ws.dh,
+                                      ln=(ws.x[l], ly.ln1_m, ly.ln1_r, p + "attention.LayerNorm"))
             self.linear_wgrad(ws.dqkv, ly.h1, p + "attention.self.qkv.weight", 3 * H, H)
             prev_b2 = f"esm.encoder.layer.{l - 1}.output.dense.bias" if l > 0 else None
             call("esm_layernorm_bwd", kdt, ws.dh.data_ptr(), ws.x[l].data_ptr(),
                  self._p32(p + "attention.LayerNorm.weight").data_ptr(), ly.ln1_m.data_ptr(), ly.ln1_r.data_ptr(),
-                 ws.dx1.data_ptr(), None, dx_next.data_ptr(), self._g32(p + "attention.LayerNorm.weight").data_ptr(),
-                 self._g32(p + "attention.LayerNorm.bias").data_ptr(),
+                 ws.dx1.data_ptr(), None, dx_next.data_ptr(),
+                 None if fused else self._g32(p + "attention.LayerNorm.weight").data_ptr(),
+                 None if fused else self._g32(p + "attention.LayerNorm.bias").data_ptr(),
                  self._g32(prev_b2).data_ptr() if prev_b2 else None, T, H, st)
             dx, dx_next = dx_next, dx
             if self.comm is not None:
