@@ -418,7 +418,7 @@ struct BwdShape {
   static constexpr int NBUF = DP <= 32 ? 3 : 2;  // {S^T, dP^T} TMEM buffers (128 columns each)
   static constexpr int QST = DP <= 32 ? 6 : 4;   // Q / dO / LSE / Delta stages (>= NBUF + 1)
   static constexpr int DS_BUF = 2 * 128 * 128;  // one pair: [2 query chunks of 64][128 key rows][128 B]
-  static constexpr int DQ_STAGE = 4 * 32 * DH * 4;  // fused dQ drain: 4 warps x 32 rows x DH fp32
+  static constexpr int DQ_STAGE = 8 * 32 * (DH / 2) * 4;  // fused dQ drain: 8 warps x 32 rows x DH/2 fp32
   static constexpr int SMEM = 2 * DS_BUF + 2 * KB + 2 * QST * QB + 2 * QST * 64 * 4 + DQ_STAGE + 1024 + 256;
 };
 
@@ -441,8 +441,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint8_t* sdO = sQ + QST * QB;      // [QST][QB]
   float* sL = reinterpret_cast<float*>(sdO + QST * QB);  // [QST][64]
   float* sD = sL + QST * 64;                             // [QST][64]
-  float* sDQ = sD + QST * 64;                            // [4][32][DH] fused dQ staging
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sDQ + 4 * 32 * DH);
+  float* sDQ = sD + QST * 64;                            // [8][32][DH/2] fused dQ staging
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sDQ + 8 * 32 * (DH / 2));
   uint64_t* kv_full = bars;
   uint64_t* qdo_full = bars + 1;           // [QST]
   uint64_t* qdo_empty = qdo_full + QST;    // [QST]
@@ -612,35 +612,31 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tc_fence_after();
       const uint32_t tq = tdQ0 + (pp & 1) * DP;
       if (fo.dqkv) {
-        // fused: the hf == 0 warp of each lane quarter drains all DP columns through smem and a
-        // TMA bulk reduce-add of its 32 x DH tile into the token-major fp32 dQ workspace
-        if (hf == 0) {
-          uint32_t u[DP];
+        // fused: both warps of a lane quarter drain half of the DH columns each through smem and a TMA
+        // bulk reduce-add of their 32 x DH/2 tile into the token-major fp32 dQ workspace
+        constexpr int HD = DH / 2;
+        uint32_t u[DQH];
 #pragma unroll
-          for (int c = 0; c < DP; c += 8)
-            tmem_ld8(tq + lane_off + c, u[c], u[c + 1], u[c + 2], u[c + 3], u[c + 4], u[c + 5], u[c + 6], u[c + 7]);
-          tmem_ld_wait();
-          tc_fence_before();
-          float* stage = sDQ + qq * 32 * DH;
-          if (lane == 0) bulk_wait_read0();  // previous reduce from this staging tile has read it
-          __syncwarp();
-          float4* row = reinterpret_cast<float4*>(stage + lane * DH);
+        for (int c = 0; c < DQH; c += 8)
+          tmem_ld8(tq + lane_off + hf * HD + c, u[c], u[c + 1], u[c + 2], u[c + 3], u[c + 4], u[c + 5], u[c + 6],
+                   u[c + 7]);
+        tmem_ld_wait();
+        tc_fence_before();
+        float* stage = sDQ + (qq * 2 + hf) * 32 * HD;
+        if (lane == 0) bulk_wait_read0();  // previous reduce from this staging tile has read it
+        __syncwarp();
+        float4* row = reinterpret_cast<float4*>(stage + lane * HD);
 #pragma unroll
-          for (int c = 0; c < DH; c += 4)
-            row[c / 4] = make_float4(__uint_as_float(u[c]), __uint_as_float(u[c + 1]), __uint_as_float(u[c + 2]),
-                                     __uint_as_float(u[c + 3]));
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          __syncwarp();
-          if (lane == 0) {
-            mbar_arrive(&dq_empty[pp & 1]);
-            // rows past this sequence carry exact zeros (dS = 0 there), so spilling into the next rows is harmless
-            tma_reduce_2d(&tmdQ, stage, h * DH, b * S + pp * 128 + qq * 32);
-            bulk_commit_group();
-          }
-        } else {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&dq_empty[pp & 1]);
+        for (int c = 0; c < HD; c += 4)
+          row[c / 4] = make_float4(__uint_as_float(u[c]), __uint_as_float(u[c + 1]), __uint_as_float(u[c + 2]),
+                                   __uint_as_float(u[c + 3]));
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&dq_empty[pp & 1]);
+          // rows past this sequence carry exact zeros (dS = 0 there), so spilling into the next rows is harmless
+          tma_reduce_2d(&tmdQ, stage, h * DH + hf * HD, b * S + pp * 128 + qq * 32);
+          bulk_commit_group();
         }
         return;
       }
@@ -739,7 +735,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       if (lane == 0 && trole > 0) trace_ev(fo.trace, trole, i, 6);
     }
     drain_dq(npairs - 1);
-    if (fo.dqkv && hf == 0 && lane == 0) bulk_wait_all0();
+    if (fo.dqkv && lane == 0) bulk_wait_all0();
     // ---- final rows: dK (hf == 0) or dV (hf == 1)
     mbar_wait(dkv_done, 0);
     tc_fence_after();
@@ -896,7 +892,7 @@ int launch_bwd(const void* q, const void* k, const void* v, const void* dout, co
   if (fo.dqkv) {  // fused: token-major fp32 dQ workspace [B*S, nh*DH]; box = DH columns x 32 tokens
     cuuint64_t dims[2] = {(cuuint64_t)nh * DH, (cuuint64_t)B * S};
     cuuint64_t strides[1] = {(cuuint64_t)nh * DH * 4};
-    cuuint32_t box[2] = {(cuuint32_t)DH, 32};
+    cuuint32_t box[2] = {(cuuint32_t)(DH / 2), 32};
     cuuint32_t estr[2] = {1, 1};
     if (enc(&tdq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, dq, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,

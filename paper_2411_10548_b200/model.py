@@ -518,7 +518,7 @@ class EsmForMaskedLM:
             # attention
             self.linear_dgrad(ws.dx1, p + "attention.output.dense.weight", H, H, ws.do)
             self.linear_wgrad(ws.dx1, ly.o, p + "attention.output.dense.weight", H, H)
-            if kdt == ESM_BF16 and S % 4 == 0:
+            if kdt == ESM_BF16 and S % 4 == 0 and dh <= 32:
                 # fused: attention backward writes dqkv [T,3H] (RoPE^T, q-scale) + q/k/v bias grads
                 call("esm_attn_bwd_qkv", ly.q.data_ptr(), ly.k.data_ptr(), ly.v.data_ptr(), ly.o.data_ptr(),
                      ws.do.data_ptr(), ly.lse.data_ptr(), ws.am.data_ptr(), ws.delta.data_ptr(), ws.dq.data_ptr(),
