@@ -12,6 +12,7 @@
 // fp32 path (parity mode): tiled SIMT FFMA kernel with the same epilogues.
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -64,10 +65,10 @@ struct EpiCfg {
   static constexpr int BYTES = kEpiWarps * WARP_BYTES;
 };
 
-template <int BN, int EPI>
+template <int BN, int EPI, int CG = 1>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int B_BYTES = (BN / CG) * BK * 2;  // a CTA pair splits B's columns
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int BUDGET = 224 * 1024 - EpiCfg<EPI>::BYTES - 1024 - 512;
   static constexpr int STAGES = BUDGET / STAGE_BYTES > 8 ? 8 : BUDGET / STAGE_BYTES;
@@ -122,11 +123,14 @@ struct EpiMaps {
   CUtensorMap c, z, r;
 };
 
-template <int BN, bool A_MN, bool B_MN, int EPI>
+// CG = 2: a CTA pair (cluster of 2) computes a 256 x BN tile with tcgen05.mma.cta_group::2 -- each CTA
+// loads its 128 rows of A and half of B's columns, so per-SM operand traffic drops by a third.
+template <int BN, bool A_MN, bool B_MN, int EPI, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ EpiMaps maps, TileInfo ti, EpiParams ep) {
-  using C = Cfg<BN, EPI>;
+  using C = Cfg<BN, EPI, CG>;
+  constexpr int BNC = BN / CG;  // B columns held by this CTA
   using E = EpiCfg<EPI>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -143,6 +147,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const int rank = CG == 2 ? (int)cluster_ctarank() : 0;
+  const int unit = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;   // tile-processing unit (CTA or pair)
+  const int nunits = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -151,7 +158,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull_bar[b], 1);
-      mbar_init(&tempty_bar[b], kEpiWarps);
+      mbar_init(&tempty_bar[b], kEpiWarps * CG);
     }
     for (int i = 0; i < 2 * kEpiWarps; ++i) mbar_init(&aux_bar[i], 1);
     fence_mbar_init();
@@ -160,9 +167,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
   }
-  if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  if (warp == 1) {
+    if constexpr (CG == 2) tmem_alloc_pair<C::TMEM_COLS>(tmem_slot);
+    else tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync();  // peer barriers initialised before any remote arrive / TMA
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -172,28 +183,34 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ===================== TMA producer =====================
     int stage = 0;
     uint32_t phase = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+    auto load = [&](void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+      if constexpr (CG == 2) tma_load_2d_pair(dst, map, bar, c0, c1);
+      else tma_load_2d(dst, map, bar, c0, c1);
+    };
+    for (int t = unit; t < num_tiles; t += nunits) {
       int mb, nb, kb0, kb1;
       decode_tile(ti, t, mb, nb, kb0, kb1);
+      const int m0 = mb * BM * CG + rank * BM;   // this CTA's A rows
+      const int n0 = nb * BN + rank * BNC;       // this CTA's B columns
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&empty_bar[stage], phase ^ 1);
         if (lane == 0) {
           uint8_t* a_dst = sA + stage * C::A_BYTES;
           uint8_t* b_dst = sB + stage * C::B_BYTES;
-          mbar_expect_tx(&full_bar[stage], C::STAGE_BYTES);
+          if (rank == 0) mbar_expect_tx(&full_bar[stage], C::STAGE_BYTES * CG);  // both CTAs' bytes
           if constexpr (!A_MN) {
-            tma_load_2d(a_dst, &tmA, &full_bar[stage], kb * BK, mb * BM);
+            load(a_dst, &tmA, &full_bar[stage], kb * BK, m0);
           } else {
 #pragma unroll
             for (int i = 0; i < BM / 64; ++i)
-              tma_load_2d(a_dst + i * 64 * BK * 2, &tmA, &full_bar[stage], mb * BM + i * 64, kb * BK);
+              load(a_dst + i * 64 * BK * 2, &tmA, &full_bar[stage], m0 + i * 64, kb * BK);
           }
           if constexpr (!B_MN) {
-            tma_load_2d(b_dst, &tmB, &full_bar[stage], kb * BK, nb * BN);
+            load(b_dst, &tmB, &full_bar[stage], kb * BK, n0);
           } else {
 #pragma unroll
-            for (int i = 0; i < BN / 64; ++i)
-              tma_load_2d(b_dst + i * 64 * BK * 2, &tmB, &full_bar[stage], nb * BN + i * 64, kb * BK);
+            for (int i = 0; i < BNC / 64; ++i)
+              load(b_dst + i * 64 * BK * 2, &tmB, &full_bar[stage], n0 + i * 64, kb * BK);
           }
         }
         __syncwarp();
@@ -203,13 +220,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == 1) {
-    // ===================== MMA issuer =====================
-    constexpr uint32_t idesc = make_idesc_bf16(BM, BN, A_MN, B_MN);
+  } else if (warp == 1 && rank == 0) {
+    // ===================== MMA issuer (leader CTA of a pair) =====================
+    constexpr uint32_t idesc = make_idesc_bf16(BM * CG, BN, A_MN, B_MN);
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+    for (int t = unit; t < num_tiles; t += nunits, ++it) {
       int mb, nb, kb0, kb1;
       decode_tile(ti, t, mb, nb, kb0, kb1);
       const int buf = it & 1;
@@ -229,10 +246,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                                      : make_sdesc_sw128(a_base + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? make_sdesc_sw128(b_base + k * 16 * 128, BK * 128, 1024)
                                      : make_sdesc_sw128(b_base + k * 32, 16, 1024);
-            mma_bf16_ss(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            if constexpr (CG == 2) mma_bf16_ss_pair(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            else mma_bf16_ss(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           }
-          mma_commit(&empty_bar[stage]);
-          if (kb == kb1 - 1) mma_commit(&tfull_bar[buf]);
+          if constexpr (CG == 2) {
+            mma_commit_pair(&empty_bar[stage]);
+            if (kb == kb1 - 1) mma_commit_pair(&tfull_bar[buf]);
+          } else {
+            mma_commit(&empty_bar[stage]);
+            if (kb == kb1 - 1) mma_commit(&tfull_bar[buf]);
+          }
         }
         __syncwarp();
         if (++stage == STAGES) {
@@ -241,7 +264,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else {
+  } else if (warp >= 2) {
     // ===================== epilogue warps =====================
     const int ew = warp - 2;
     const int q = warp & 3;  // TMEM lane quarter this warp may access
@@ -253,12 +276,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t aux_phase = 0;  // bit b = expected parity of aux buffer b
     int ob = 0, ab = 0;
     int it = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+    for (int t = unit; t < num_tiles; t += nunits, ++it) {
       int mb, nb, kb0, kb1;
       decode_tile(ti, t, mb, nb, kb0, kb1);
       const int buf = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
-      const int row0 = mb * BM + q * 32;
+      const int row0 = mb * BM * CG + rank * BM + q * 32;
       const int ncols = min(BN, ep.N - nb * BN);
       if constexpr (E::AUX) {  // prefetch the residual / pre-activation chunk of the first column block
         if (lane == 0 && half * 32 < ncols) {
@@ -321,7 +344,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty_bar[buf]);
+        if (lane == 0) {
+          if constexpr (CG == 2) mbar_arrive_leader(&tempty_bar[buf]);
+          else mbar_arrive(&tempty_bar[buf]);
+        }
         continue;
       }
 #pragma unroll 1
@@ -439,15 +465,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty_bar[buf]);
+      if (lane == 0) {
+        if constexpr (CG == 2) mbar_arrive_leader(&tempty_bar[buf]);
+        else mbar_arrive(&tempty_bar[buf]);
+      }
     }
     if (lane == 0) bulk_wait_all();
     __syncwarp();
   }
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync();  // both CTAs done with TMEM and remote barriers
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<C::TMEM_COLS>(tmem_base);
+    if constexpr (CG == 2) tmem_dealloc_pair<C::TMEM_COLS>(tmem_base);
+    else tmem_dealloc<C::TMEM_COLS>(tmem_base);
   }
 }
 
@@ -504,9 +535,9 @@ static int num_sms() {
   return g_num_sms;
 }
 
-template <int BN, bool A_MN, bool B_MN, int EPI>
-static int launch(const esm_gemm_args& a, cudaStream_t st) {
-  using C = Cfg<BN, EPI>;
+template <int BN, bool A_MN, bool B_MN, int EPI, int CG>
+static int launch_cg(const esm_gemm_args& a, cudaStream_t st) {
+  using C = Cfg<BN, EPI, CG>;
   CUtensorMap tA, tB;
   EpiMaps maps;
   memset(&maps, 0, sizeof(maps));
@@ -517,7 +548,7 @@ static int launch(const esm_gemm_args& a, cudaStream_t st) {
     rc = make_map(&tA, a.A, a.M, a.K, a.lda, 64, BK);
   if (rc) return rc;
   if (!B_MN)
-    rc = make_map(&tB, a.B, a.K, a.N, a.ldb, BK, BN);
+    rc = make_map(&tB, a.B, a.K, a.N, a.ldb, BK, BN / CG);
   else
     rc = make_map(&tB, a.B, a.N, a.K, a.ldb, 64, BK);
   if (rc) return rc;
@@ -536,12 +567,12 @@ static int launch(const esm_gemm_args& a, cudaStream_t st) {
   if (rc) return rc;
 
   TileInfo ti;
-  ti.num_m = (a.M + BM - 1) / BM;
+  ti.num_m = (a.M + BM * CG - 1) / (BM * CG);
   ti.num_n = (a.N + BN - 1) / BN;
   ti.kb_total = (a.K + BK - 1) / BK;
   int splits = 1;
   const int tiles = ti.num_m * ti.num_n;
-  const int sms = num_sms();
+  const int sms = num_sms() / CG;  // tile-processing units (CTAs or CTA pairs)
   if (EPI == ESM_EPI_F32_ACC) {
     if (a.split_k > 0) {
       splits = a.split_k;
@@ -568,16 +599,52 @@ static int launch(const esm_gemm_args& a, cudaStream_t st) {
                a.rope_cos, a.rope_sin,
                {(__nv_bfloat16*)a.q_out, (__nv_bfloat16*)a.k_out, (__nv_bfloat16*)a.v_out},
                a.seq_len, a.n_heads, a.head_dim, a.q_scale, a.row_mean, a.row_rstd, a.col_sum2};
-  auto kern = gemm_tc_kernel<BN, A_MN, B_MN, EPI>;
+  auto kern = gemm_tc_kernel<BN, A_MN, B_MN, EPI, CG>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     attr_set = true;
   }
   const int total = tiles * splits;
-  const int grid = total < sms ? total : sms;
-  kern<<<grid, kThreads, C::SMEM, st>>>(tA, tB, maps, ti, ep);
+  const int units = total < sms ? total : sms;
+  if constexpr (CG == 1) {
+    kern<<<units, kThreads, C::SMEM, st>>>(tA, tB, maps, ti, ep);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(units * CG);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, tA, tB, maps, ti, ep);
+  }
   ESM_LAUNCH_RET();
+}
+
+static int g_pair_mode = -1;  // ESM_GEMM_PAIR=0 disables the CTA-pair kernels
+static bool pair_enabled() {
+  if (g_pair_mode < 0) {
+    const char* e = getenv("ESM_GEMM_PAIR");
+    g_pair_mode = (e && e[0] == '0') ? 0 : 1;
+  }
+  return g_pair_mode == 1;
+}
+
+template <int BN, bool A_MN, bool B_MN, int EPI>
+static int launch(const esm_gemm_args& a, cudaStream_t st) {
+  // CTA pairs (M = 256 tiles) when M fills them; B columns are split across the pair, so for an
+  // N-major B each half must be a whole number of 64-column TMA boxes.
+  constexpr bool pair_ok = (BN % 32 == 0) && (!B_MN || (BN / 2) % 64 == 0);
+  if constexpr (pair_ok) {
+    if (pair_enabled() && a.M >= 2 * BM * 8) return launch_cg<BN, A_MN, B_MN, EPI, 2>(a, st);
+  }
+  return launch_cg<BN, A_MN, B_MN, EPI, 1>(a, st);
 }
 
 static int pick_bn_kmajor(int N) {

@@ -44,7 +44,8 @@ def run_gemm(dtype, M, N, K, A, lda, amn, B, ldb, bmn, C, ldc, epi, bias=None, a
 
 
 FWD_SHAPES = [(256, 128, 64), (1000, 1440, 480), (300, 480, 1920), (128, 96, 64), (4096, 1920, 480),
-              (515, 64, 200), (2048, 1280, 1280), (333, 160, 96)]
+              (515, 64, 200), (2048, 1280, 1280), (333, 160, 96),
+              (2304 + 77, 480, 480), (4096, 1440, 480), (3000, 96, 64)]  # M >= 2048: CTA-pair (M=256) kernels
 
 
 @pytest.mark.parametrize("M,N,K", FWD_SHAPES)
@@ -73,7 +74,7 @@ def test_gemm_forward_epilogues(M, N, K, dt):
 
 
 @pytest.mark.parametrize("M,N,K", [(256, 128, 64), (1000, 480, 1440), (300, 1920, 480), (515, 64, 200),
-                                   (2048, 1280, 5120)])
+                                   (2048, 1280, 5120), (2500, 480, 1920), (4096, 1920, 480), (2048, 128, 64)])
 @pytest.mark.parametrize("dt", ["bf16", "fp32"])
 def test_gemm_dgrad(M, N, K, dt):
     """dX[M=T, N=in] = dY[T, K=out] · W[out, in]  (B operand N-major)."""
@@ -98,7 +99,7 @@ def test_gemm_dgrad(M, N, K, dt):
 
 
 @pytest.mark.parametrize("M,N,K", [(480, 1920, 4096), (1440, 480, 8192), (128, 128, 64), (96, 200, 1000),
-                                   (1280, 5120, 2048), (40, 64, 512)])
+                                   (1280, 5120, 2048), (40, 64, 512), (2560, 640, 4096), (5120, 1280, 2048)])
 @pytest.mark.parametrize("dt", ["bf16", "fp32"])
 def test_gemm_wgrad(M, N, K, dt):
     """dW[M=out, N=in] += dY[T=K, out]ᵀ · X[T, in]  (both operands MN-major, fp32 accumulate, split-K)."""
