@@ -251,10 +251,13 @@ class EsmForMaskedLM:
         self.step_count = 0
         self.grad_scale = 1.0
         self.ws: Workspace | None = None
+        self._ws_cache: dict = {}
+        self.max_workspaces = 3
         self.comm = None  # set by ddp.GradAllReducer
         self.timer = None  # optional KernelTimer (bench.py per-kernel roofline)
         self.launches = 0  # kernels launched by this model (C-ABI calls x kernels per call)
         self.graph = None
+        self.graph_launches = 0
         self._hyper_ring = [torch.zeros(8, dtype=torch.float32).pin_memory() for _ in range(4)]
         self._hyper_ev = [None] * 4
         self._hyper_i = 0
@@ -300,10 +303,22 @@ class EsmForMaskedLM:
         return torch.cuda.current_stream(self.device).cuda_stream
 
     def workspace(self, B: int, S: int) -> Workspace:
-        if self.ws is None or self.ws.B != B or self.ws.S != S:
-            self.ws = None
-            torch.cuda.empty_cache()
-            self.ws = Workspace(self.config, B, S, self.act, self.device)
+        """Activation workspace for a (B, S) shape.  Variable-shape training (bucketed batches) keeps an
+        LRU cache of up to ``max_workspaces`` shapes, each with its own CUDA graph once captured."""
+        key = (B, S)
+        cache = self._ws_cache
+        if key in cache:
+            cache[key] = cache.pop(key)  # most recently used
+        else:
+            while len(cache) >= self.max_workspaces:
+                old_key = next(iter(cache))
+                old = cache.pop(old_key)
+                if self.ws is old:
+                    self.ws = None
+                del old
+                torch.cuda.empty_cache()
+            cache[key] = Workspace(self.config, B, S, self.act, self.device)
+        self.ws = cache[key]
         return self.ws
 
     # kernels launched per C-ABI entry point (for the bench's gpu_launches count)
@@ -598,17 +613,41 @@ class EsmForMaskedLM:
         with torch.cuda.graph(g):
             self.forward_backward(ws)
             self._adamw()
-        self.graph_launches = self.launches - n0
+        ws.graph = g
+        ws.graph_launches = self.launches - n0
         self.graph = g
+        self.graph_launches = ws.graph_launches
         return g
 
-    def graph_step(self, lr=None):
-        """Replay the captured step (after staging this step's batch in the workspace)."""
+    def graph_step(self, lr=None, ws: Workspace | None = None):
+        """Replay the step captured for ``ws`` (default: the current workspace) after staging its batch."""
+        ws = ws or self.ws
+        if getattr(ws, "graph", None) is None:
+            raise RuntimeError("no CUDA graph captured for this workspace: call capture(ws) first")
         self.step_count += 1
         self.set_hyper(lr=lr, step=self.step_count)
-        self.graph.replay()
-        self.launches += self.graph_launches
-        return self.ws.loss_sum
+        ws.graph.replay()
+        self.launches += ws.graph_launches
+        return ws.loss_sum
+
+    def train_step_tokens(self, token_lists, seed: int, stream_id: int, lr=None, pad_to: int = 64,
+                          use_graph: bool = False):
+        """One MLM step on a list of token sequences (e.g. one ``bucket_batches`` batch): right-pad to a
+        multiple of ``pad_to``, mask on the device (bit-exact 15% / 80-10-10), forward, backward, AdamW.
+        Fully padded key tiles are skipped by the attention kernels.  Returns the device loss tensor."""
+        from .data import collate
+        ids, am = collate(token_lists, pad_to=pad_to)
+        ws = self.workspace(*ids.shape)
+        ws.ids.copy_(torch.from_numpy(ids), non_blocking=True)
+        ws.am.copy_(torch.from_numpy(am), non_blocking=True)
+        self.mlm_mask(ws.ids, seed, stream_id, ws)
+        if use_graph and self.comm is None:
+            if getattr(ws, "graph", None) is None:
+                self.capture(ws)
+            return self.graph_step(lr=lr, ws=ws)
+        loss = self.forward_backward(ws)
+        self.optimizer_step(lr=lr)
+        return loss
 
     def train_step(self, input_ids, attention_mask=None, labels=None, lr=None):
         """One MLM train step on an already-masked batch; returns the device loss tensor."""

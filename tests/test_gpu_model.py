@@ -121,3 +121,23 @@ def test_train_steps_fp32_match_oracle_trainer():
         lg = float(m.train_step(torch.from_numpy(inp).cuda(), torch.from_numpy(am).cuda(),
                                 torch.from_numpy(lab).cuda()).item())
         assert abs(lg - lo) / lo < 1e-4, (step, lg, lo)
+
+
+def test_varlen_bucketed_batches_match_oracle():
+    """Variable (B, S) batches through train_step_tokens (workspace cache, padded attention tiles
+    skipped) give the oracle's loss on the same padded batch, step after step."""
+    cfg, ocfg = _cfgs(64, 2, 4, 256)
+    params = init_params(cfg, seed=4)
+    m = EsmForMaskedLM(cfg, dtype="fp32", device="cuda", params=params, lr=1e-3)
+    tr = O.OracleTrainer(ocfg, params, lr=1e-3, beta1=0.9, beta2=0.98, eps=1e-8, weight_decay=0.01)
+    rng = np.random.default_rng(7)
+    from paper_2411_10548_b200.data import collate
+    for step, (nb, lo, hi) in enumerate([(4, 20, 60), (2, 100, 190), (6, 5, 30), (4, 20, 60)]):
+        toks = [np.concatenate([[O.CLS], rng.integers(4, 24, n - 2), [O.EOS]]).astype(np.int32)
+                for n in rng.integers(lo, hi, nb)]
+        ids, am = collate(toks, pad_to=64)
+        inp, lab = O.mlm_mask(ids, seed=9, stream=step)
+        want = tr.step(inp, am, lab)
+        got = float(m.train_step_tokens(toks, seed=9, stream_id=step).item())
+        assert abs(got - want) / want < 1e-4, (step, got, want)
+    assert len(m._ws_cache) <= m.max_workspaces
