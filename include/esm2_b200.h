@@ -88,12 +88,31 @@ int esm_tokenize(const char* seq, int len, int32_t* out, int max_out);
  * bit-exact with oracle/esm2_oracle.py:mlm_mask).  Also counts labelled tokens into *n_labels (int32, accumulated). */
 int esm_mlm_mask(const int32_t* ids, int32_t* input_ids, int32_t* labels, int32_t* n_labels, int64_t n,
                  uint64_t seed, uint64_t stream_id, esm_stream_t stream);
+/* Same draws, vocabulary given explicitly (Geneformer: eligible [2, V-1], <mask>=1, random from [2, V-1];
+ * reference pkg/src/densefeed/tokenizer.py:16-18 PAD_ID/MASK_ID/TOKEN_OFFSET).  Selected ids in
+ * [elig_lo, elig_hi]; 80% -> mask_id, 10% -> rand_lo + (r % rand_n), 10% kept. */
+int esm_mlm_mask_ex(const int32_t* ids, int32_t* input_ids, int32_t* labels, int32_t* n_labels, int64_t n,
+                    uint64_t seed, uint64_t stream_id, int elig_lo, int elig_hi, int mask_id, int rand_lo,
+                    int rand_n, esm_stream_t stream);
+
+/* Device: Geneformer rank-value tokenisation of CSR expression rows (replaces the reference's
+ * rank_encode, pkg/src/densefeed/tokenizer.py:68-83, applied per row as in corpus.py / bindings __getitem__).
+ * For output row b (source row rows[b], or b when rows == NULL): score = (double)vals / (double)medians[col],
+ * order = descending score, ties by ascending col, truncate to min(max_len, S), id = col + 2 (TOKEN_OFFSET),
+ * PAD = 0 past the length; am[b, i] = i < length.  lengths[b] (optional) = tokens written.
+ * *status (caller zeroes): 1 = a col >= n_genes (the reference's ValidationError), 2 = a row has more
+ * than max_nnz entries (<= 16384, staged in shared memory). */
+int esm_rank_encode(const int64_t* indptr, const int64_t* cols, const float* vals, const float* medians,
+                    int64_t n_genes, const int64_t* rows, int n_rows, int max_len, int S, int32_t* ids, int32_t* am,
+                    int32_t* lengths, int32_t* status, int max_nnz, esm_stream_t stream);
 
 /* ---------------- embeddings (HF:modeling_esm.py:189-236) ---------------- */
 /* x[t,:] = E[ids[t]] * (ids!=mask) * row_scale[b] * am[t];  row_scale = 0.88/(1 - n_mask/len) (token_dropout). */
 int esm_embed_fwd(int dtype, const int32_t* ids, const int32_t* am, const void* E, void* x, float* row_scale,
                   int B, int S, int H, int token_dropout, int mask_id, esm_stream_t stream);
-/* dE[v,:] += sum_{t: ids[t]=v, v!=pad} dx[t,:] * keep * row_scale[b] * am[t]   (fp32) */
+/* dE[v,:] += sum_{t: ids[t]=v, v!=pad, v!=mask_id} dx[t,:] * row_scale[b] * am[t]   (fp32).  mask_id = the
+ * token-dropout mask id (its rows were zeroed in the forward), or -1 without token dropout.  V <= 128:
+ * shared-memory column accumulators; larger V (Geneformer): per-row vector fp32 atomics. */
 int esm_embed_bwd(int dtype, const int32_t* ids, const int32_t* am, const float* row_scale, const void* dx,
                   float* dE, int B, int S, int H, int V, int mask_id, int pad_id, esm_stream_t stream);
 
@@ -140,6 +159,22 @@ int esm_attn_bwd_qkv(const void* q, const void* k, const void* v, const void* o,
 int esm_lmhead_xent(int dtype, const void* n, const void* E, const float* bias, const int32_t* labels,
                     const float* inv_denom, float* loss_sum, float* dlogits_ws, void* dn, float* dE, float* dbias,
                     int T, int H, int V, esm_stream_t stream);
+/* Large-vocabulary head (V > 40, Geneformer V = 25426): the decoder runs only on labelled rows.
+ * esm_label_compact: idx[0..cap) = ascending indices of rows with labels >= 0 (then -1), lab = their labels
+ * (then -100), *count = total labelled rows (may exceed cap: the caller sizes cap, rows past cap are dropped). */
+int esm_label_compact(const int32_t* labels, int64_t T, int32_t* idx, int32_t* lab, int32_t* count, int cap,
+                      esm_stream_t stream);
+/* dst[i,:] = src[idx[i],:] (0 where idx[i] < 0); H % 8 == 0. */
+int esm_gather_rows(int dtype, const void* src, const int32_t* idx, void* dst, int cap, int H, esm_stream_t stream);
+/* dst[T,H] = 0; dst[idx[i],:] = src[i,:] for idx[i] >= 0. */
+int esm_scatter_rows(int dtype, const void* src, const int32_t* idx, void* dst, int cap, int H, int64_t T,
+                     esm_stream_t stream);
+/* Per row r < rows with lab[r] >= 0: loss_sum += (logsumexp(x[r,:V]) - x[r,lab]) * inv_denom[0];
+ * x[r,:] <- (softmax - onehot) * inv_denom[0] in place (columns V..ld zeroed; rows with lab < 0 zeroed). */
+int esm_xent_rows(int dtype, void* logits, const int32_t* lab, int rows, int V, int64_t ld, const float* inv_denom,
+                  float* loss_sum, esm_stream_t stream);
+/* out[c] += sum_r x[r,c], c < V (fp32 accumulate) -- the decoder-bias gradient. */
+int esm_colsum_rows(int dtype, const void* x, int rows, int V, int64_t ld, float* out, esm_stream_t stream);
 /* inv_denom[0] = 1 / max(1, n_labels[0]) (fp32) -- the loss normaliser, device-side (graph-safe). */
 int esm_inv_count(const int32_t* n_labels, float* inv_denom, esm_stream_t stream);
 

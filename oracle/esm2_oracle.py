@@ -130,18 +130,21 @@ def mask_draws(key, n: int):
         return _mix64(base), _mix64(base + _U64(1)), _mix64(base + _U64(2))
 
 
-def mlm_mask(ids: np.ndarray, seed: int, stream: int):
-    """15% of eligible positions (ids 4..30) are selected; of those 80% -> <mask>,
-    10% -> uniform random standard AA, 10% unchanged.  labels = original id where
-    selected, else -100.  Returns (input_ids int32, labels int32)."""
+def mlm_mask(ids: np.ndarray, seed: int, stream: int, eligible=(4, 30), mask_id: int = MASK,
+             random_range=(AA_FIRST, AA_COUNT)):
+    """15% of eligible positions (ids in ``eligible``, inclusive; ESM-2: 4..30) are selected; of
+    those 80% -> ``mask_id``, 10% -> ``random_range[0] + r % random_range[1]`` (ESM-2: the 20
+    standard AAs), 10% unchanged.  labels = original id where selected, else -100.
+    Geneformer rank tokens (reference pkg/src/densefeed/tokenizer.py:16-18, PAD=0 MASK=1 offset 2):
+    eligible=(2, V-1), mask_id=1, random_range=(2, V-2).  Returns (input_ids int32, labels int32)."""
     flat = np.asarray(ids, dtype=np.int32).reshape(-1)
     r0, r1, r2 = mask_draws(mask_key(seed, stream), flat.size)
-    eligible = (flat >= 4) & (flat <= 30)
-    sel = eligible & ((r0 >> _U64(40)).astype(np.int64) < P_SELECT)
+    elig = (flat >= eligible[0]) & (flat <= eligible[1])
+    sel = elig & ((r0 >> _U64(40)).astype(np.int64) < P_SELECT)
     a = (r1 >> _U64(40)).astype(np.int64)
-    rnd = (AA_FIRST + (r2 % _U64(AA_COUNT))).astype(np.int32)
+    rnd = (random_range[0] + (r2 % _U64(random_range[1])).astype(np.int64)).astype(np.int32)
     out = flat.copy()
-    out = np.where(sel & (a < P_MASK), MASK, out)
+    out = np.where(sel & (a < P_MASK), mask_id, out)
     out = np.where(sel & (a >= P_MASK) & (a < P_RANDOM), rnd, out)
     labels = np.where(sel, flat, -100).astype(np.int32)
     return out.reshape(ids.shape).astype(np.int32), labels.reshape(ids.shape)

@@ -17,7 +17,9 @@ EPI_STORE, EPI_GELU, EPI_RESID, EPI_DGELU, EPI_F32_ACC, EPI_QKV_ROPE, EPI_STORE_
 EXPORTS = [
     "esm_version", "esm_last_error", "esm_device_sm_count", "esm_tokenize", "esm_mlm_mask", "esm_embed_fwd",
     "esm_embed_bwd", "esm_layernorm_fwd", "esm_layernorm_bwd", "esm_gemm", "esm_qkv_rope_fwd", "esm_qkv_rope_bwd",
-    "esm_attn_fwd", "esm_attn_bwd", "esm_attn_bwd_qkv", "esm_lmhead_xent", "esm_inv_count", "esm_adamw", "esm_cast_f32_bf16",
+    "esm_attn_fwd", "esm_attn_bwd", "esm_attn_bwd_qkv", "esm_lmhead_xent", "esm_inv_count",
+    "esm_mlm_mask_ex", "esm_label_compact", "esm_gather_rows", "esm_scatter_rows", "esm_xent_rows", "esm_colsum_rows",
+    "esm_rank_encode", "esm_adamw", "esm_cast_f32_bf16",
 ]
 
 
@@ -64,6 +66,13 @@ _SIGS = {
     "esm_attn_bwd_qkv": ([_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _F, _I, _I, _I, _I, _P], _I),
     "esm_lmhead_xent": ([_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _P], _I),
     "esm_inv_count": ([_P, _P, _P], _I),
+    "esm_mlm_mask_ex": ([_P, _P, _P, _P, _I64, _U64, _U64, _I, _I, _I, _I, _I, _P], _I),
+    "esm_label_compact": ([_P, _I64, _P, _P, _P, _I, _P], _I),
+    "esm_gather_rows": ([_I, _P, _P, _P, _I, _I, _P], _I),
+    "esm_scatter_rows": ([_I, _P, _P, _P, _I, _I, _I64, _P], _I),
+    "esm_xent_rows": ([_I, _P, _P, _I, _I, _I64, _P, _P, _P], _I),
+    "esm_colsum_rows": ([_I, _P, _I, _I, _I64, _P, _P], _I),
+    "esm_rank_encode": ([_P, _P, _P, _P, _I64, _P, _I, _I, _I, _P, _P, _P, _P, _I, _P], _I),
     "esm_adamw": ([_P, _P, _P, _P, _P, _P, _I64, _P, _P], _I),
     "esm_cast_f32_bf16": ([_P, _P, _I64, _P], _I),
 }

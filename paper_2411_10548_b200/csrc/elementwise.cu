@@ -32,7 +32,8 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
 constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
 
 __global__ void mlm_mask_kernel(const int32_t* __restrict__ ids, int32_t* __restrict__ inp, int32_t* __restrict__ lab,
-                                int32_t* __restrict__ n_labels, int64_t n, uint64_t key) {
+                                int32_t* __restrict__ n_labels, int64_t n, uint64_t key, int elig_lo, int elig_hi,
+                                int mask_id, int rand_lo, uint32_t rand_n) {
   __shared__ int cnt;
   if (threadIdx.x == 0) cnt = 0;
   __syncthreads();
@@ -41,12 +42,12 @@ __global__ void mlm_mask_kernel(const int32_t* __restrict__ ids, int32_t* __rest
     const int32_t id = ids[i];
     const uint64_t base = key + (uint64_t)i * kGolden;
     const uint64_t r0 = mix64(base), r1 = mix64(base + 1), r2 = mix64(base + 2);
-    const bool eligible = id >= 4 && id <= 30;
+    const bool eligible = id >= elig_lo && id <= elig_hi;
     const bool sel = eligible && (int64_t)(r0 >> 40) < 2516582;
     const int64_t a = (int64_t)(r1 >> 40);
     int32_t out = id;
-    if (sel && a < 13421773) out = 32;
-    else if (sel && a < 15099494) out = 4 + (int32_t)(r2 % 20ull);
+    if (sel && a < 13421773) out = mask_id;
+    else if (sel && a < 15099494) out = rand_lo + (int32_t)(r2 % (uint64_t)rand_n);
     inp[i] = out;
     lab[i] = sel ? id : -100;
     local += sel ? 1 : 0;
@@ -144,6 +145,30 @@ __global__ void embed_bwd_smem_kernel(const int32_t* __restrict__ ids, const int
       const float a = acc[v * blockDim.x + threadIdx.x];
       if (a != 0.f) atomicAdd(dE + (int64_t)v * H + col, a);
     }
+}
+
+// large vocabularies (Geneformer V ~ 25k): one warp per token row, vector fp32 reductions into dE[id]
+template <typename T>
+__global__ void embed_bwd_atomic_kernel(const int32_t* __restrict__ ids, const int32_t* __restrict__ am,
+                                        const float* __restrict__ row_scale, const T* __restrict__ dx,
+                                        float* __restrict__ dE, int64_t T_, int S, int H, int mask_id, int pad_id) {
+  constexpr int VEC = vec16<T>::N;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t t = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); t < T_; t += warps) {
+    const int id = ids[t];
+    if (id == pad_id || id == mask_id) continue;
+    const float sc = row_scale[t / S] * (am ? (float)(am[t] != 0) : 1.0f);
+    if (sc == 0.f) continue;
+    for (int c = lane * VEC; c < H; c += 32 * VEC) {
+      float v[VEC];
+      load_vec(dx + t * H + c, v);
+#pragma unroll
+      for (int e = 0; e < VEC; e += 4)
+        atomicAdd(reinterpret_cast<float4*>(dE + (int64_t)id * H + c + e),
+                  make_float4(v[e] * sc, v[e + 1] * sc, v[e + 2] * sc, v[e + 3] * sc));
+    }
+  }
 }
 
 // ============================================================================
@@ -676,14 +701,22 @@ int esm_tokenize(const char* seq, int len, int32_t* out, int max_out) {
   return need;
 }
 
-int esm_mlm_mask(const int32_t* ids, int32_t* input_ids, int32_t* labels, int32_t* n_labels, int64_t n, uint64_t seed,
-                 uint64_t stream_id, esm_stream_t stream) {
-  ESM_CHECK_ARG(ids && input_ids && labels && n >= 0, "esm_mlm_mask: bad args");
+int esm_mlm_mask_ex(const int32_t* ids, int32_t* input_ids, int32_t* labels, int32_t* n_labels, int64_t n,
+                    uint64_t seed, uint64_t stream_id, int elig_lo, int elig_hi, int mask_id, int rand_lo, int rand_n,
+                    esm_stream_t stream) {
+  ESM_CHECK_ARG(ids && input_ids && labels && n >= 0 && rand_n > 0 && elig_lo <= elig_hi, "esm_mlm_mask: bad args");
   const uint64_t k0 = mix64(seed + kGolden);
   const uint64_t key = mix64(k0 ^ stream_id);
   if (n == 0) return 0;
-  mlm_mask_kernel<<<grid_for(n, 256), 256, 0, S(stream)>>>(ids, input_ids, labels, n_labels, n, key);
+  mlm_mask_kernel<<<grid_for(n, 256), 256, 0, S(stream)>>>(ids, input_ids, labels, n_labels, n, key, elig_lo, elig_hi,
+                                                           mask_id, rand_lo, (uint32_t)rand_n);
   ESM_LAUNCH_RET();
+}
+
+int esm_mlm_mask(const int32_t* ids, int32_t* input_ids, int32_t* labels, int32_t* n_labels, int64_t n, uint64_t seed,
+                 uint64_t stream_id, esm_stream_t stream) {
+  // ESM-2 alphabet: amino acids 4..30 eligible, <mask>=32, random replacement from the 20 standard residues
+  return esm_mlm_mask_ex(ids, input_ids, labels, n_labels, n, seed, stream_id, 4, 30, 32, 4, 20, stream);
 }
 
 int esm_inv_count(const int32_t* n_labels, float* inv_denom, esm_stream_t stream) {
@@ -709,8 +742,19 @@ int esm_embed_fwd(int dtype, const int32_t* ids, const int32_t* am, const void* 
 
 int esm_embed_bwd(int dtype, const int32_t* ids, const int32_t* am, const float* row_scale, const void* dx, float* dE,
                   int B, int Sq, int H, int V, int mask_id, int pad_id, esm_stream_t stream) {
-  ESM_CHECK_ARG(ids && row_scale && dx && dE && V > 0 && V <= 128, "esm_embed_bwd: bad args (V<=128)");
+  ESM_CHECK_ARG(ids && row_scale && dx && dE && V > 0 && H % 8 == 0, "esm_embed_bwd: bad args");
   const int64_t T_ = (int64_t)B * Sq;
+  if (V > 128) {
+    const int grid = grid_for(T_ * 32, 256);
+    if (dtype == ESM_BF16)
+      embed_bwd_atomic_kernel<__nv_bfloat16><<<grid, 256, 0, S(stream)>>>(ids, am, row_scale,
+                                                                          (const __nv_bfloat16*)dx, dE, T_, Sq, H,
+                                                                          mask_id, pad_id);
+    else
+      embed_bwd_atomic_kernel<float><<<grid, 256, 0, S(stream)>>>(ids, am, row_scale, (const float*)dx, dE, T_, Sq,
+                                                                  H, mask_id, pad_id);
+    ESM_LAUNCH_RET();
+  }
   const int bx = 128;
   const int rpb = 256;
   dim3 grid((H + bx - 1) / bx, (unsigned)((T_ + rpb - 1) / rpb));

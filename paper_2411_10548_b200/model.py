@@ -38,6 +38,14 @@ from ._lib import (EPI_DGELU, EPI_F32_ACC, EPI_GELU, EPI_QKV_ROPE, EPI_RESID, EP
 from .config import EsmConfig
 
 ALIGN = 256  # elements; also the AdamW weight-decay chunk size
+LARGE_VOCAB = 40  # esm_lmhead_xent's per-row fused head handles V <= 40; larger V uses the GEMM head
+
+
+def head_capacity(T: int) -> int:
+    """Rows reserved for the labelled-row decoder: E[#labels] = 0.15*T (selection probability
+    2516582/2^24), std <= 0.36*sqrt(T); 8*sqrt(T) + 64 of headroom is > 20 sigma.  Batches staged with
+    explicit labels are checked against it on the host (set_batch)."""
+    return min(T, (int(0.15 * T + 8.0 * math.sqrt(T) + 64) + 127) // 128 * 128)
 
 
 def _no_decay(name: str) -> bool:
@@ -206,7 +214,19 @@ class Workspace:
         self.n = e(T, H)
         # backward scratch
         self.dn = e(T, H)
-        self.dlogits = e(T, V, dt=f32)
+        self.large_vocab = V > LARGE_VOCAB
+        if self.large_vocab:  # decoder on labelled rows only (esm_label_compact / gather / GEMM / xent_rows)
+            self.cap = head_capacity(T)
+            self.Vp = (V + 7) // 8 * 8
+            self.head_idx = torch.full((self.cap,), -1, dtype=i32, device=device)
+            self.head_lab = torch.full((self.cap,), -100, dtype=i32, device=device)
+            self.head_count = torch.zeros(1, dtype=i32, device=device)
+            self.n_lab = e(self.cap, H)
+            self.logits = e(self.cap, self.Vp)  # overwritten in place by dlogits
+            self.dn_lab = e(self.cap, H)
+            self.dlogits = None
+        else:
+            self.dlogits = e(T, V, dt=f32)
         self.dy = e(T, H)
         self.dx = e(T, H)
         self.dx_alt = e(T, H)
@@ -405,8 +425,10 @@ class EsmForMaskedLM:
         if ids.data_ptr() != ws.ids.data_ptr():
             ws.ids.copy_(ids, non_blocking=True)
         ws.n_labels.zero_()
-        _lib.call("esm_mlm_mask", ws.ids.data_ptr(), ws.input_ids.data_ptr(), ws.labels.data_ptr(),
+        cfg = self.config
+        _lib.call("esm_mlm_mask_ex", ws.ids.data_ptr(), ws.input_ids.data_ptr(), ws.labels.data_ptr(),
                   ws.n_labels.data_ptr(), ws.ids.numel(), seed & 0xFFFFFFFFFFFFFFFF, stream_id & 0xFFFFFFFFFFFFFFFF,
+                  cfg.mlm_eligible[0], cfg.mlm_eligible[1], cfg.mask_token_id, cfg.mlm_random[0], cfg.mlm_random[1],
                   self._stream())
         return ws.input_ids, ws.labels
 
@@ -421,9 +443,30 @@ class EsmForMaskedLM:
             ws.am.copy_(attention_mask, non_blocking=True)
         if labels is not None:
             ws.labels.copy_(labels, non_blocking=True)
-            ws.n_labels.copy_((torch.as_tensor(labels) != -100).sum().reshape(1).to(torch.int32),
-                              non_blocking=True)
+            n_lab = (torch.as_tensor(labels) != -100).sum().reshape(1).to(torch.int32)
+            if ws.large_vocab and int(n_lab.item()) > ws.cap:
+                raise ValueError(f"{int(n_lab.item())} labelled tokens exceed the LM-head capacity {ws.cap}")
+            ws.n_labels.copy_(n_lab, non_blocking=True)
         return ws
+
+    def _large_vocab_head(self, ws, E, E_key, T, H, V):
+        """Tied decoder + masked CE for large V (Geneformer): logits only for the labelled rows
+        (HF:modeling_esm.py:777-784 -- the loss only reads those rows), as tcgen05 GEMMs.
+        Produces loss_sum, ws.dn (= dlogits·E scattered back, 0 on unlabelled rows), dE and dbias."""
+        st, kdt, cap, Vp = self._stream(), self.kdt, ws.cap, ws.Vp
+        call = self._call
+        call("esm_label_compact", ws.labels.data_ptr(), T, ws.head_idx.data_ptr(), ws.head_lab.data_ptr(),
+             ws.head_count.data_ptr(), cap, st)
+        call("esm_gather_rows", kdt, ws.n.data_ptr(), ws.head_idx.data_ptr(), ws.n_lab.data_ptr(), cap, H, st)
+        # logits[cap, V] = n_lab · Eᵀ + bias
+        self._gemm(cap, V, H, ws.n_lab, H, 0, E, H, 0, ws.logits, Vp, EPI_STORE, bias=self._p32("lm_head.bias"))
+        call("esm_xent_rows", kdt, ws.logits.data_ptr(), ws.head_lab.data_ptr(), cap, V, Vp,
+             ws.inv_denom.data_ptr(), ws.loss_sum.data_ptr(), st)
+        call("esm_colsum_rows", kdt, ws.logits.data_ptr(), cap, V, Vp, self._g32("lm_head.bias").data_ptr(), st)
+        # dn_lab = dlogits · E ;  dE += dlogitsᵀ · n_lab
+        self._gemm(cap, H, V, ws.logits, Vp, 0, E, H, 1, ws.dn_lab, H, EPI_STORE)
+        self._gemm(V, H, cap, ws.logits, Vp, 1, ws.n_lab, H, 1, self._g32(E_key), H, EPI_F32_ACC)
+        call("esm_scatter_rows", kdt, ws.dn_lab.data_ptr(), ws.head_idx.data_ptr(), ws.dn.data_ptr(), cap, H, T, st)
 
     # ------------------------------------------------------------------ forward + backward
     def forward_backward(self, ws: Workspace | None = None, loss_only: bool = False):
@@ -487,10 +530,12 @@ class EsmForMaskedLM:
         call("esm_layernorm_fwd", kdt, ws.g.data_ptr(), self._p32("lm_head.layer_norm.weight").data_ptr(),
              self._p32("lm_head.layer_norm.bias").data_ptr(), ws.n.data_ptr(), ws.lnh_m.data_ptr(),
              ws.lnh_r.data_ptr(), T, H, eps, st)
-        # decoder (tied E) + masked CE + dlogits (fused)
-        call("esm_lmhead_xent", kdt, ws.n.data_ptr(), E.data_ptr(), self._p32("lm_head.bias").data_ptr(),
-             ws.labels.data_ptr(), ws.inv_denom.data_ptr(), ws.loss_sum.data_ptr(), ws.dlogits.data_ptr(),
-             ws.dn.data_ptr(), self._g32(E_key).data_ptr(), self._g32("lm_head.bias").data_ptr(), T, H, V, st)
+        if ws.large_vocab:
+            self._large_vocab_head(ws, E, E_key, T, H, V)
+        else:  # decoder (tied E) + masked CE + dlogits (fused, V <= 40)
+            call("esm_lmhead_xent", kdt, ws.n.data_ptr(), E.data_ptr(), self._p32("lm_head.bias").data_ptr(),
+                 ws.labels.data_ptr(), ws.inv_denom.data_ptr(), ws.loss_sum.data_ptr(), ws.dlogits.data_ptr(),
+                 ws.dn.data_ptr(), self._g32(E_key).data_ptr(), self._g32("lm_head.bias").data_ptr(), T, H, V, st)
         if loss_only:
             return ws.loss_sum
         # ---------------- backward
@@ -560,7 +605,8 @@ class EsmForMaskedLM:
             if self.comm is not None:
                 self.comm.ready(p + "attention.LayerNorm.bias")
         call("esm_embed_bwd", kdt, ws.input_ids.data_ptr(), ws.am.data_ptr(), ws.row_scale.data_ptr(),
-             dx.data_ptr(), self._g32(E_key).data_ptr(), B, S, H, V, cfg.mask_token_id, cfg.pad_token_id, st)
+             dx.data_ptr(), self._g32(E_key).data_ptr(), B, S, H, V,
+             cfg.mask_token_id if cfg.token_dropout else -1, cfg.pad_token_id, st)
         if self.comm is not None:
             self.comm.ready(E_key)
             self.comm.end_backward()
@@ -636,7 +682,7 @@ class EsmForMaskedLM:
         multiple of ``pad_to``, mask on the device (bit-exact 15% / 80-10-10), forward, backward, AdamW.
         Fully padded key tiles are skipped by the attention kernels.  Returns the device loss tensor."""
         from .data import collate
-        ids, am = collate(token_lists, pad_to=pad_to)
+        ids, am = collate(token_lists, pad_to=pad_to, pad_id=self.config.pad_token_id)
         ws = self.workspace(*ids.shape)
         ws.ids.copy_(torch.from_numpy(ids), non_blocking=True)
         ws.am.copy_(torch.from_numpy(am), non_blocking=True)

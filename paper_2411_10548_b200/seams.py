@@ -49,10 +49,12 @@ def length_features(sample) -> np.ndarray:
     return np.array([lens.sum(), (lens * lens).sum()])
 
 
-def collate_indices(dataset, indices: Sequence[int], seq_len: int | None = None, pad_to: int = 8):
-    """One ``batches()`` index list -> (ids int32 [B, S], attention_mask int32 [B, S])."""
+def collate_indices(dataset, indices: Sequence[int], seq_len: int | None = None, pad_to: int = 8,
+                    pad_id: int = 1):
+    """One ``batches()`` index list -> (ids int32 [B, S], attention_mask int32 [B, S]).
+    pad_id: 1 for ESM-2 token lists, 0 for the bindings' Geneformer rank tokens (tokenizer.py:16)."""
     toks = [dataset[i][0] if isinstance(dataset[i], tuple) else dataset[i] for i in indices]
-    return collate(toks, seq_len=seq_len, pad_to=pad_to)
+    return collate(toks, seq_len=seq_len, pad_to=pad_to, pad_id=pad_id)
 
 
 def make_workload(model, seed: int = 0, pad_to: int = 8, lr: float | None = None) -> Callable:
@@ -62,7 +64,7 @@ def make_workload(model, seed: int = 0, pad_to: int = 8, lr: float | None = None
 
     def workload(sample):
         batch = sample if (len(sample) and not isinstance(sample[0], (int, np.integer))) else [sample]
-        ids, am = collate(batch, pad_to=pad_to)
+        ids, am = collate(batch, pad_to=pad_to, pad_id=model.config.pad_token_id)
         ids_d = torch.from_numpy(ids).to(model.device)
         ws = model.workspace(*ids.shape)
         ws.am.copy_(torch.from_numpy(am).to(model.device))

@@ -1,0 +1,209 @@
+"""Geneformer config (BASELINE configs[4]) on a B200: the device rank-value tokeniser against the
+reference's own rank_encode outputs, generalised MLM masking, and the large-vocabulary LM head
+(labelled-row compaction + tcgen05 decoder GEMMs) against the CPU oracle."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import esm2_oracle as O
+import rank_oracle as R
+from paper_2411_10548_b200 import _lib
+from paper_2411_10548_b200.config import geneformer_config
+from paper_2411_10548_b200.data import RankEncoder, synthetic_expression_csr
+from paper_2411_10548_b200.model import EsmForMaskedLM, head_capacity, init_params
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "rank_encode.npz")
+
+
+def _relerr(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.abs(a - b).max() / (np.abs(b).max() + 1e-30))
+
+
+# ------------------------------------------------------------------ tokeniser
+@pytest.mark.parametrize("ml_index", range(6))
+def test_rank_encode_kernel_matches_reference_golden(ml_index):
+    z = np.load(GOLD)
+    ml = int(z["max_lens"][ml_index])
+    ip, c, v, med = z["indptr"], z["cols"], z["vals"], z["medians"]
+    enc = RankEncoder(med)
+    rows = np.arange(len(ip) - 1)
+    S = 6016
+    ids, am, lengths = enc(ip, c, v, rows, seq_len=S, max_len=ml)
+    ids, am, lengths = ids.cpu().numpy(), am.cpu().numpy(), lengths.cpu().numpy()
+    want_len = np.minimum(z[f"lengths_{ml}"], S)
+    assert np.array_equal(lengths, want_len)
+    toks = z[f"tokens_{ml}"]
+    off = np.r_[0, np.cumsum(z[f"lengths_{ml}"])]
+    for r in rows:
+        n = want_len[r]
+        assert np.array_equal(ids[r, :n], toks[off[r]:off[r] + n]), r
+        assert (ids[r, n:] == 0).all() and am[r, :n].all() and not am[r, n:].any()
+
+
+def test_rank_encode_kernel_edge_cases():
+    med = np.array([1.0, 2.0, 0.5, 1.0, 4.0], np.float32)
+    rows = [([3, 0, 1], [1.0, 1.0, 2.0]),            # all scores equal -> ascending gene
+            ([], []),                                 # empty row
+            ([4, 2, 0], [-0.0, 0.0, -1.0]),           # +-0 tie, negative last
+            ([1, 4, 3, 2], [np.nan, 1.0, np.nan, 3.0]),  # NaN last, ascending gene among NaN
+            ([0, 1, 2, 3, 4], [5.0, 4.0, 3.0, 2.0, 1.0])]
+    ip = np.r_[0, np.cumsum([len(r[0]) for r in rows])].astype(np.int64)
+    c = np.concatenate([np.asarray(r[0], np.int64) for r in rows])
+    v = np.concatenate([np.asarray(r[1], np.float32) for r in rows])
+    enc = RankEncoder(med)
+    for S, ml in ((8, 8), (8, 3), (2, 8)):
+        ids, am, lengths = enc(ip, c, v, np.arange(len(rows)), seq_len=S, max_len=ml)
+        want, want_am = R.rank_encode_batch(ip, c, v, med, range(len(rows)), ml, S)
+        assert np.array_equal(ids.cpu().numpy(), want) and np.array_equal(am.cpu().numpy(), want_am)
+    # gene index out of range -> ValidationError analogue
+    with pytest.raises(ValueError):
+        enc(np.array([0, 1], np.int64), np.array([5], np.int64), np.array([1.0], np.float32), [0], seq_len=4)
+
+
+def test_rank_encode_kernel_random_rows_vs_oracle():
+    n_genes = 25424
+    ip, c, v = synthetic_expression_csr(24, n_genes, seed=3, nnz=(1, 9000))
+    v[::7] = np.round(v[::7])        # ties
+    med = np.random.default_rng(4).uniform(0.5, 3.0, n_genes).astype(np.float32)
+    med[::5] = 1.0
+    rows = np.random.default_rng(5).permutation(24)[:16]
+    ids, am, _ = RankEncoder(med)(ip, c, v, rows, seq_len=2048)
+    want, want_am = R.rank_encode_batch(ip, c, v, med, rows, 2048, 2048)
+    assert np.array_equal(ids.cpu().numpy(), want) and np.array_equal(am.cpu().numpy(), want_am)
+
+
+# ------------------------------------------------------------------ masking
+def test_mlm_mask_geneformer_vocab_bit_exact():
+    cfg = geneformer_config()
+    V = cfg.vocab_size
+    rng = np.random.default_rng(1)
+    ids = rng.integers(2, V, size=(4, 2048)).astype(np.int32)
+    ids[1, 1500:] = 0
+    m = EsmForMaskedLM(geneformer_config(n_genes=V - 2, num_hidden_layers=1), dtype="bf16", device="cuda")
+    ws = m.workspace(4, 2048)
+    inp, lab = m.mlm_mask(torch.from_numpy(ids).cuda(), seed=11, stream_id=7, ws=ws)
+    want_inp, want_lab = O.mlm_mask(ids, 11, 7, eligible=(2, V - 1), mask_id=1, random_range=(2, V - 2))
+    assert np.array_equal(inp.cpu().numpy(), want_inp) and np.array_equal(lab.cpu().numpy(), want_lab)
+    assert int(ws.n_labels.item()) == int((want_lab != -100).sum())
+
+
+# ------------------------------------------------------------------ large-vocabulary head kernels
+def test_label_compact_and_xent_rows_vs_torch():
+    T, V, cap = 3000, 1000, 640
+    g = torch.Generator().manual_seed(0)
+    labels = torch.full((T,), -100, dtype=torch.int32)
+    pos = torch.randperm(T, generator=g)[:500]
+    labels[pos] = torch.randint(0, V, (500,), generator=g, dtype=torch.int32)
+    lab_d = labels.cuda()
+    idx = torch.empty(cap, dtype=torch.int32, device="cuda")
+    lab = torch.empty(cap, dtype=torch.int32, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    _lib.call("esm_label_compact", lab_d.data_ptr(), T, idx.data_ptr(), lab.data_ptr(), cnt.data_ptr(), cap, st)
+    want_idx = torch.nonzero(labels >= 0).flatten()
+    assert int(cnt.item()) == 500
+    assert torch.equal(idx[:500].cpu().long(), want_idx) and (idx[500:] == -1).all()
+    assert torch.equal(lab[:500].cpu(), labels[want_idx]) and (lab[500:] == -100).all()
+    # xent_rows: fp32 logits, in-place dlogits; padded ld
+    ld = 1008
+    x = torch.randn(cap, ld, generator=g) * 3
+    xd = x.cuda()
+    inv = torch.tensor([1.0 / 500], device="cuda")
+    loss = torch.zeros(1, device="cuda")
+    _lib.call("esm_xent_rows", _lib.ESM_F32, xd.data_ptr(), lab.data_ptr(), cap, V, ld, inv.data_ptr(),
+              loss.data_ptr(), st)
+    xl = x[:500, :V].double().requires_grad_(True)
+    ref = torch.nn.functional.cross_entropy(xl, labels[want_idx].long(), reduction="mean")
+    ref.backward()
+    ref_v = float(ref.detach())
+    assert abs(float(loss.item()) - ref_v) / ref_v < 1e-5
+    got = xd.cpu().double()
+    assert _relerr(got[:500, :V], xl.grad) < 1e-5
+    assert (got[500:] == 0).all() and (got[:, V:] == 0).all()
+    # colsum of the gradient = decoder-bias grad
+    out = torch.zeros(V, device="cuda")
+    _lib.call("esm_colsum_rows", _lib.ESM_F32, xd.data_ptr(), cap, V, ld, out.data_ptr(), st)
+    assert _relerr(out.cpu(), xl.grad.sum(0)) < 1e-5
+
+
+# ------------------------------------------------------------------ model parity
+def _gf_cfgs(n_genes, H, L, nh, F):
+    cfg = geneformer_config(n_genes=n_genes, hidden_size=H, num_hidden_layers=L, num_attention_heads=nh,
+                            intermediate_size=F)
+    ocfg = O.OracleConfig(vocab_size=cfg.vocab_size, hidden_size=H, num_hidden_layers=L, num_attention_heads=nh,
+                          intermediate_size=F, token_dropout=False, mask_token_id=1, pad_token_id=0)
+    return cfg, ocfg
+
+
+def _gf_batch(V, B, S, lens, seed):
+    rng = np.random.default_rng(seed)
+    ids = np.zeros((B, S), np.int32)
+    am = np.zeros((B, S), np.int32)
+    for b, n in enumerate(lens):
+        ids[b, :n] = rng.permutation(np.arange(2, V))[:n]
+        am[b, :n] = 1
+    inp, lab = O.mlm_mask(ids, seed=seed, stream=1, eligible=(2, V - 1), mask_id=1, random_range=(2, V - 2))
+    return inp, am, lab
+
+
+def test_large_vocab_fp32_matches_oracle():
+    """V = 300 > 40 forces the compacted-row GEMM head; fp32 mode within 1e-4 of the oracle
+    (loss and every gradient, incl. the tied embedding/decoder and the decoder bias)."""
+    cfg, ocfg = _gf_cfgs(298, 64, 2, 4, 128)
+    params = init_params(cfg, seed=6)
+    inp, am, lab = _gf_batch(cfg.vocab_size, 3, 64, [64, 50, 21], seed=2)
+    ref = O.forward_backward(ocfg, params, inp, am, lab, dtype=np.float64)
+    m = EsmForMaskedLM(cfg, dtype="fp32", device="cuda", params=params)
+    ws = m.set_batch(torch.from_numpy(inp).cuda(), torch.from_numpy(am).cuda(), torch.from_numpy(lab).cuda())
+    assert ws.large_vocab and ws.cap >= int((lab != -100).sum())
+    loss = float(m.forward_backward(ws).item())
+    assert abs(loss - ref.loss) / ref.loss < 1e-5
+    grads = m.grads()
+    for k, g in ref.grads.items():
+        assert _relerr(grads[k].cpu().numpy(), g) < 1e-4, k
+
+
+def test_geneformer_geometry_bf16_matches_oracle():
+    """Full Geneformer head (V = 25,426, H = 768, dh = 64) in bf16 vs the fp64 oracle."""
+    cfg, ocfg = _gf_cfgs(25424, 768, 1, 12, 3072)
+    params = init_params(cfg, seed=7)
+    inp, am, lab = _gf_batch(cfg.vocab_size, 2, 256, [256, 190], seed=3)
+    ref = O.forward_backward(ocfg, params, inp, am, lab, dtype=np.float64)
+    m = EsmForMaskedLM(cfg, dtype="bf16", device="cuda", params=params)
+    ws = m.set_batch(torch.from_numpy(inp).cuda(), torch.from_numpy(am).cuda(), torch.from_numpy(lab).cuda())
+    loss = float(m.forward_backward(ws).item())
+    assert abs(loss - ref.loss) / ref.loss < 1e-2
+    grads = m.grads()
+    for k, g in ref.grads.items():
+        gg = grads[k].cpu().numpy().astype(np.float64)
+        fro = np.linalg.norm(gg - g) / (np.linalg.norm(g) + 1e-30)
+        assert fro < 0.08, (k, fro)
+
+
+def test_geneformer_train_steps_fp32_match_oracle_trainer():
+    cfg, ocfg = _gf_cfgs(298, 64, 2, 4, 128)
+    params = init_params(cfg, seed=8)
+    tr = O.OracleTrainer(ocfg, params, lr=1e-3, beta1=0.9, beta2=0.98, eps=1e-8, weight_decay=0.01)
+    m = EsmForMaskedLM(cfg, dtype="fp32", device="cuda", params=params, lr=1e-3)
+    for step in range(4):
+        inp, am, lab = _gf_batch(cfg.vocab_size, 4, 64, [64, 64, 40, 12], seed=20 + step)
+        lo = tr.step(inp, am, lab)
+        lg = float(m.train_step(torch.from_numpy(inp).cuda(), torch.from_numpy(am).cuda(),
+                                torch.from_numpy(lab).cuda()).item())
+        assert abs(lg - lo) / lo < 1e-4, (step, lg, lo)
+
+
+def test_head_capacity_guard():
+    cfg, _ = _gf_cfgs(298, 64, 1, 4, 128)
+    m = EsmForMaskedLM(cfg, dtype="fp32", device="cuda")
+    T = 4 * 512
+    assert head_capacity(T) >= 0.15 * T + 8 * T ** 0.5
+    ids = torch.full((4, 512), 5, dtype=torch.int32)
+    lab = ids.clone()  # every token labelled -> exceeds the capacity
+    with pytest.raises(ValueError):
+        m.set_batch(ids, None, lab)

@@ -158,3 +158,23 @@ def test_grad_bucket_allreduce_gloo_world2():
         assert ok, rank
         assert n == 30
         assert nb > 1  # several buckets -> overlap with backward is possible
+
+
+def test_geneformer_preset_and_feed_host_logic():
+    """Geneformer config (BASELINE configs[4]): ~106M params, reference token layout, host-side
+    medians identical to the reference's compute_gene_stats (golden from the reference)."""
+    from paper_2411_10548_b200.data import gene_medians, synthetic_expression_csr
+    cfg = preset("geneformer")
+    H, F, V, L = cfg.hidden_size, cfg.intermediate_size, cfg.vocab_size, cfg.num_hidden_layers
+    total = V * H + L * (4 * H * H + 4 * H + 2 * H * F + F + H + 4 * H) + 2 * H + H * H + H + 2 * H + V
+    assert abs(total - 106e6) / 106e6 < 0.01
+    assert (cfg.pad_token_id, cfg.mask_token_id, cfg.mlm_eligible, cfg.token_dropout) == (0, 1, (2, V - 1), False)
+    assert abs(cfg.train_flops_per_token(2048) - 0.857e9) / 0.857e9 < 1e-3   # SURVEY.md §8d
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "rank_encode.npz"))
+    assert np.array_equal(gene_medians(z["indptr"], z["cols"], z["vals"], int(z["n_genes"])), z["medians"])
+    ip, c, v = synthetic_expression_csr(5, 1000, seed=1, nnz=(10, 50))
+    assert ip.shape == (6,) and c.size == ip[-1] == v.size and c.max() < 1000
+    for r in range(5):
+        assert (np.diff(c[ip[r]:ip[r + 1]]) > 0).all()
+    ids, am = collate([[5, 6, 7], [9]], pad_to=4, pad_id=0)
+    assert ids.tolist() == [[5, 6, 7, 0], [9, 0, 0, 0]] and am.sum() == 4
