@@ -30,7 +30,10 @@ WORKLOADS = {  # BASELINE.json configs -> (preset, batch per GPU, seq)
     "650m": ("esm2_t33_650M", 16, 1024),  # configs[2]: 650M DDP, seq 1024
     "3b": ("esm2_t36_3B", 4, 1024),       # configs[3]
     "8m": ("esm2_t6_8M", 8, 512),         # configs[0] geometry (CPU oracle config) on the GPU
+    "geneformer": ("geneformer", 16, 2048),  # configs[4]: Geneformer 106M, rank-value tokens, seq 2048
 }
+GF_GENES = 25424      # V = n_genes + 2 = 25,426
+GF_NNZ = (500, 4000)  # non-zero genes per synthetic cell
 
 
 def parse():
@@ -145,19 +148,28 @@ def cpu_reference_step_time(preset_name, seq, steps=1, warm=0):
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import numpy as np
     import esm2_oracle as O
-    from paper_2411_10548_b200.config import PRESETS
-    p = PRESETS[preset_name]
-    cfg = O.OracleConfig(hidden_size=p["hidden_size"], num_hidden_layers=p["num_hidden_layers"],
-                         num_attention_heads=p["num_attention_heads"], intermediate_size=p["intermediate_size"])
+    from paper_2411_10548_b200 import preset
+    c = preset(preset_name)
+    cfg = O.OracleConfig(vocab_size=c.vocab_size, hidden_size=c.hidden_size, num_hidden_layers=c.num_hidden_layers,
+                         num_attention_heads=c.num_attention_heads, intermediate_size=c.intermediate_size,
+                         token_dropout=c.token_dropout, mask_token_id=c.mask_token_id, pad_token_id=c.pad_token_id)
+    mk = dict(eligible=c.mlm_eligible, mask_id=c.mask_token_id, random_range=c.mlm_random)
     params = O.init_params(cfg, seed=1)
     tr = O.OracleTrainer(cfg, params, dtype=np.float32)
-    ids, am = O.synthetic_batch(1, seq, seed=0)
+    if c.vocab_size > 40:  # Geneformer: one full-length cell of rank tokens (oracle tokenizer)
+        import rank_oracle as R
+        from paper_2411_10548_b200.data import synthetic_expression_csr
+        ip, cols, vals = synthetic_expression_csr(1, c.vocab_size - 2, seed=0, nnz=(seq, seq))
+        med = np.ones(c.vocab_size - 2, np.float32)
+        ids, am = R.rank_encode_batch(ip, cols, vals, med, [0], seq, seq)
+    else:
+        ids, am = O.synthetic_batch(1, seq, seed=0)
     for i in range(warm):
-        inp, lab = O.mlm_mask(ids, 0, i)
+        inp, lab = O.mlm_mask(ids, 0, i, **mk)
         tr.step(inp, am, lab)
     t0 = time.perf_counter()
     for i in range(steps):
-        inp, lab = O.mlm_mask(ids, 0, 100 + i)
+        inp, lab = O.mlm_mask(ids, 0, 100 + i, **mk)
         tr.step(inp, am, lab)
     dt = (time.perf_counter() - t0) / steps
     return seq / dt, dt
@@ -172,7 +184,8 @@ def run_reference(args, rank, world):
     warm = min(args.warmup, 1)
     tps, dt = cpu_reference_step_time(preset_name, S, steps=max(1, args.steps), warm=warm)
     line = {
-        "impl": "reference", "metric": "ESM-2 MLM train tokens/sec", "value": tps, "unit": "tokens/s",
+        "impl": "reference", "metric": ("Geneformer" if args.config == "geneformer" else "ESM-2") +
+        " MLM train tokens/sec", "value": tps, "unit": "tokens/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{preset_name} MLM train step, reference CPU oracle, sample 1 x {S} tokens/step",
@@ -216,10 +229,28 @@ def main():
         model.comm = GradAllReducer(model.store)
     use_graph = (world == 1) and not args.no_graph
 
-    pool = [torch.from_numpy(synthetic_batch(B, S, seed=1000 * rank + i)[0]).to(dev) for i in range(2)]
+    gene = cfg.vocab_size > 40
+    if gene:  # Geneformer: synthetic cells -> rank-value tokens on the GPU (esm_rank_encode)
+        from paper_2411_10548_b200.data import RankEncoder, gene_medians, synthetic_expression_csr
+        csr = synthetic_expression_csr(4 * B, GF_GENES, seed=100 + rank, nnz=GF_NNZ)
+        enc = RankEncoder(gene_medians(*csr, GF_GENES), device=dev)
+        pool, pool_am = [], []
+        for i in range(2):
+            ids_i, am_i, _ = enc(*csr, np.arange(i * B, (i + 1) * B), seq_len=S)
+            pool.append(ids_i)
+            pool_am.append(am_i)
+        lens = [a.sum(1).double() for a in pool_am]
+        tokens_local = float(sum(float(x.sum()) for x in lens) / 2)     # non-pad tokens per step
+        attn_sq = float(sum(float((x * x).sum()) for x in lens) / 2)    # sum of len^2 (attention FLOPs)
+    else:
+        pool = [torch.from_numpy(synthetic_batch(B, S, seed=1000 * rank + i)[0]).to(dev) for i in range(2)]
+        pool_am = None
+        tokens_local, attn_sq = float(B * S), float(B * S * S)
     seed = 1234
 
     def step(i):
+        if pool_am is not None:
+            ws.am.copy_(pool_am[i % 2], non_blocking=True)
         model.mlm_mask(pool[i % 2], seed, i * world + rank, ws)
         if use_graph:
             model.graph_step()
@@ -228,6 +259,8 @@ def main():
             model.optimizer_step()
 
     if use_graph:
+        if pool_am is not None:
+            ws.am.copy_(pool_am[0])
         model.mlm_mask(pool[0], seed, rank, ws)
         model.capture(ws)
     for i in range(args.warmup):
@@ -258,12 +291,67 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     loss = float(ws.loss_sum.item())
-    tokens_per_step = B * S * world
+    tk = torch.tensor([tokens_local, attn_sq], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(tk)
+    tokens_per_step, attn_sq_all = float(tk[0]), float(tk[1])   # non-pad tokens, all ranks
     value = tokens_per_step / (ms / 1e3)
 
     # ---------------- end to end through the public API, host buffers
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and gene:
+        # per step: pinned CSR rows of the batch -> HBM, GPU rank tokenisation into ws.ids / ws.am,
+        # device masking, the train step, loss -> host
+        staged = []
+        for i in range(2):
+            rows = np.arange(i * B, (i + 1) * B) + 2 * B
+            ip, cols, vals = csr
+            lo, hi = ip[rows], ip[rows + 1]
+            sub_ip = np.r_[0, np.cumsum(hi - lo)].astype(np.int64)
+            idx = np.concatenate([np.arange(a, b) for a, b in zip(lo, hi)])
+            staged.append([torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+                           for a in (sub_ip, cols[idx].astype(np.int64), vals[idx].astype(np.float32))]
+                          + [int((hi - lo).max())])
+        cap = max(int(x[1].numel()) for x in staged)
+        d_ip = torch.empty(B + 1, dtype=torch.int64, device=dev)
+        d_c = torch.empty(cap, dtype=torch.int64, device=dev)
+        d_v = torch.empty(cap, dtype=torch.float32, device=dev)
+        h2d = sum(int(t.numel() * t.element_size()) for x in staged for t in x[:3]) // 2
+
+        def e2e_step(i):
+            h_ip, h_c, h_v, mx = staged[i % 2]
+            d_ip.copy_(h_ip, non_blocking=True)
+            d_c[:h_c.numel()].copy_(h_c, non_blocking=True)
+            d_v[:h_v.numel()].copy_(h_v, non_blocking=True)
+            enc.encode_device(d_ip, d_c, d_v, B, mx, S, ids=ws.ids, am=ws.am)
+            model.mlm_mask(ws.ids, seed, 10_000 + i * world + rank, ws)
+            if use_graph:
+                model.graph_step()
+            else:
+                model.forward_backward(ws)
+                model.optimizer_step()
+            return float(ws.loss_sum.item())
+
+        for i in range(2):
+            e2e_step(i)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            e2e_step(i)
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - t0) / args.steps
+        tw = torch.tensor([wall], device=dev)
+        if world > 1:
+            dist.all_reduce(tw, op=dist.ReduceOp.MAX)
+        wall = float(tw.item())
+        enc.check()
+        e2e = {"value": tokens_per_step / wall, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": 4, "ms_per_step": wall * 1e3,
+               "api": "RankEncoder.encode_device (CSR rows) + EsmForMaskedLM.mlm_mask + graph_step",
+               "inputs": "CSR expression rows (indptr/cols int64, vals f32), pinned host"}
+    elif not args.no_e2e:
         host = [torch.from_numpy(synthetic_batch(B, S, seed=1000 * rank + 7 + i)[0]).pin_memory() for i in range(2)]
         for i in range(2):
             ws.ids.copy_(host[i % 2], non_blocking=True)
@@ -297,6 +385,8 @@ def main():
     roofline, kernels = None, None
     if not args.no_profile:
         model.timer = KernelTimer()
+        if pool_am is not None:
+            ws.am.copy_(pool_am[0])
         model.mlm_mask(pool[0], seed, 999, ws)
         model.forward_backward(ws)
         model.optimizer_step()
@@ -327,22 +417,31 @@ def main():
 
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        tps, dt = cpu_reference_step_time(preset_name, S, steps=1)
+        S_cpu = min(S, 1024)  # bounded sample (~10-30 s of CPU work)
+        tps, dt = cpu_reference_step_time(preset_name, S_cpu, steps=1)
         cpu_baseline = {"value": tps, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
-                        "sample": f"CPU oracle (numpy fp32, reference semantics) {preset_name}, 1 x {S} tokens, "
+                        "sample": f"CPU oracle (numpy fp32, reference semantics) {preset_name}, 1 x {S_cpu} tokens, "
                                   f"one train step ({dt:.1f} s)"}
 
-    flops_tok = cfg.train_flops_per_token(S)
+    # FLOPs per non-pad token: 6*N_mm (decoder on labelled rows only for the large-vocabulary head)
+    # + attention 12*L*H*len averaged over the actual sequence lengths
+    L_, H_ = cfg.num_hidden_layers, cfg.hidden_size
+    flops_tok = cfg.train_flops_per_token(0, head_fraction=0.15 if gene else 1.0) + \
+        12.0 * L_ * H_ * attn_sq_all / tokens_per_step
     mfu = value / world * flops_tok / (tf_sust * 1e12)
     if rank == 0:
         line = {
-            "metric": "ESM-2 MLM train tokens/sec", "value": value, "unit": "tokens/s", "n_gpus": world,
+            "metric": ("Geneformer" if gene else "ESM-2") + " MLM train tokens/sec", "value": value, "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
             "config": {"workload": f"{preset_name} MLM pre-training step (mask+fwd+bwd+AdamW), {B} x {S} per GPU",
                        "model": preset_name, "global_batch": B * world, "seq_len": S,
                        "parallelism": f"dp{world}", "l2": "inputs/activations >> 126 MB L2 (no flush needed)",
-                       "cuda_graph": use_graph, "weights": "random init", "data": "synthetic uniform AA"},
+                       "cuda_graph": use_graph, "weights": "random init",
+                       "data": (f"synthetic cells, {GF_NNZ[0]}-{GF_NNZ[1]} expressed genes of {GF_GENES}, "
+                                f"GPU rank-value tokens; non-pad tokens counted "
+                                f"({tokens_per_step / (B * S * world):.3f} fill)") if gene
+                       else "synthetic uniform AA"},
             "mfu": round(mfu, 4), "mfu_peak": f"{tf_sust} TFLOP/s bf16 sustained ({peak_src})",
             "train_flops_per_token": flops_tok, "loss": loss,
             "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e, "gpu_launches": launches,
