@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 //              drain each pair's dQ (thread = query row) into HBM with fp32 vector reductions.
 // TMEM: S^T 64 + dP^T 64 + dV/dK/dQ 3*DP columns -> 256 for dh <= 32, so two CTAs share an SM.
 // Prefix (right-padded) masks: key blocks past the valid length write zero dK/dV and exit.
-constexpr int kBwdThreads = 320;  // TMA, MMA, 8 softmax-bwd warps
+constexpr int kBwdThreads = 448;  // TMA, MMA, 8 softmax-bwd warps, 4 dQ-drain warps
 
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -390,16 +390,8 @@ struct FusedOut {
   const float* sin_t;
   int H;
   unsigned long long* trace;  // debug timeline (nullptr in production): [role][block][event]
+  int experiment;  // debug timing experiments (0 in production): 1 = softmax warps skip their math, 2 = no dQ reductions
 };
-
-// trace slots: role r (0 = MMA, 1 = softmax warp 2, 2 = softmax warp 6), block i (< 64), event e (< 8)
-__device__ __forceinline__ void trace_ev(unsigned long long* tr, int role, int i, int e) {
-  if (tr != nullptr && blockIdx.x == 3 && blockIdx.y == 5 && i < 64) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
-    tr[(role * 64 + i) * 8 + e] = t;
-  }
-}
 
 __device__ __forceinline__ void tma_reduce_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
   asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
@@ -410,15 +402,28 @@ __device__ __forceinline__ void bulk_commit_group() { asm volatile("cp.async.bul
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
+// trace slots: role r (0 = MMA, 1 = softmax warp 2, 2 = softmax warp 6), block i (< 64), event e (< 8)
+__device__ __forceinline__ void trace_ev(unsigned long long* tr, int role, int i, int e) {
+  if (tr != nullptr && blockIdx.x == 3 && blockIdx.y == 5 && i < 64) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+    tr[(role * 64 + i) * 8 + e] = t;
+  }
+}
+
+
 template <int DH>
 struct BwdShape {
   static constexpr int DP = Shape<DH, 64>::DP, ROWB = Shape<DH, 64>::ROWB;
   static constexpr uint32_t LAYOUT = Shape<DH, 64>::LAYOUT;
   static constexpr int QB = 64 * ROWB, KB = 128 * ROWB;
   static constexpr int NBUF = DP <= 32 ? 3 : 2;  // {S^T, dP^T} TMEM buffers (128 columns each)
-  static constexpr int QST = DP <= 32 ? 6 : 4;   // Q / dO / LSE / Delta stages (>= NBUF + 1)
+  static constexpr int QST = DH == 64 ? 5 : 6;   // Q / dO / LSE / Delta stages (>= NBUF + 1)
   static constexpr int DS_BUF = 2 * 128 * 128;  // one pair: [2 query chunks of 64][128 key rows][128 B]
-  static constexpr int DQ_STAGE = 8 * 32 * (DH / 2) * 4;  // fused dQ drain: 8 warps x 32 rows x DH/2 fp32
+  // dQ drain: DH in {32, 64} stages 32-column fp32 boxes (128B-swizzled) for TMA reduce-add; 16/24 use
+  // vector reductions from registers
+  static constexpr bool DQ_TMA = DH == 32 || DH == 64;
+  static constexpr int DQ_STAGE = DQ_TMA ? 4 * 32 * DH * 4 : 0;
   static constexpr int SMEM = 2 * DS_BUF + 2 * KB + 2 * QST * QB + 2 * QST * 64 * 4 + DQ_STAGE + 1024 + 256;
 };
 
@@ -439,10 +444,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint8_t* sV = sK + KB;
   uint8_t* sQ = sV + KB;             // [QST][QB]
   uint8_t* sdO = sQ + QST * QB;      // [QST][QB]
-  float* sL = reinterpret_cast<float*>(sdO + QST * QB);  // [QST][64]
-  float* sD = sL + QST * 64;                             // [QST][64]
-  float* sDQ = sD + QST * 64;                            // [8][32][DH/2] fused dQ staging
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sDQ + 8 * 32 * (DH / 2));
+  uint8_t* sDQ = sdO + QST * QB;     // [4 warps][DH/32 boxes][32 rows][128 B] (1024-aligned: swizzled)
+  float* sL = reinterpret_cast<float*>(sDQ + BS::DQ_STAGE);  // [QST][64]
+  float* sD = sL + QST * 64;                                 // [QST][64]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sD + QST * 64);
   uint64_t* kv_full = bars;
   uint64_t* qdo_full = bars + 1;           // [QST]
   uint64_t* qdo_empty = qdo_full + QST;    // [QST]
@@ -496,7 +501,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&dsm_empty[i], 1);
       mbar_init(&dq_full[i], 1);
-      mbar_init(&dq_empty[i], 8);
+      mbar_init(&dq_empty[i], 4);
     }
     mbar_init(dkv_done, 1);
     fence_mbar_init();
@@ -542,24 +547,27 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     constexpr uint32_t idesc_s = make_idesc_bf16(128, 64, false, false);  // S^T, dP^T: 128 keys x 64 queries
     constexpr uint32_t idesc_kv = make_idesc_bf16(128, DP, false, true);  // dV, dK (A from TMEM)
     constexpr uint32_t idesc_q = make_idesc_bf16(128, DP, true, true);    // dQ (A = dS^T smem, M-major)
-    const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV);
+    // descriptors hoisted: per-use offsets are added to the 14-bit start-address field (bytes >> 4)
+    const uint64_t kd_s = make_sdesc(smem_u32(sK), 16, 8 * ROWB, BS::LAYOUT);     // K  (A of S^T)
+    const uint64_t vd_s = make_sdesc(smem_u32(sV), 16, 8 * ROWB, BS::LAYOUT);     // V  (A of dP^T)
+    const uint64_t qd_s = make_sdesc(smem_u32(sQ), 16, 8 * ROWB, BS::LAYOUT);     // Q  (B of S^T)
+    const uint64_t od_s = make_sdesc(smem_u32(sdO), 16, 8 * ROWB, BS::LAYOUT);    // dO (B of dP^T)
+    const uint64_t od_kv = make_sdesc(smem_u32(sdO), QB, 8 * ROWB, BS::LAYOUT);   // dO (B of dV, MN-major)
+    const uint64_t qd_kv = make_sdesc(smem_u32(sQ), QB, 8 * ROWB, BS::LAYOUT);    // Q  (B of dK, MN-major)
+    const uint64_t kd_q = make_sdesc(smem_u32(sK), KB, 8 * ROWB, BS::LAYOUT);     // K  (B of dQ, MN-major)
+    const uint64_t dsd = make_sdesc(smem_u32(sdS), 128 * 128, 1024, 2u);          // dS^T (A of dQ, M-major)
     auto issue_s = [&](int j) {  // S^T(j), dP^T(j) into buffer j % NBUF
       const int st = j % QST;
       mbar_wait(&qdo_full[st], (j / QST) & 1);
       tc_fence_after();
-      if (lane == 0) {
-        const uint32_t q_addr = smem_u32(sQ + st * QB), o_addr = smem_u32(sdO + st * QB);
-        const uint32_t tS = tbase + (j % NBUF) * 128, tDP = tS + 64;
+      const uint64_t so = (uint64_t)((st * QB) >> 4);
+      const uint32_t tS = tbase + (j % NBUF) * 128, tDP = tS + 64;
 #pragma unroll
-        for (int k = 0; k < DP / 16; ++k) {
-          mma_bf16_ss(tS, make_sdesc(k_addr + k * 32, 16, 8 * ROWB, BS::LAYOUT),
-                      make_sdesc(q_addr + k * 32, 16, 8 * ROWB, BS::LAYOUT), idesc_s, k > 0 ? 1u : 0u);
-          mma_bf16_ss(tDP, make_sdesc(v_addr + k * 32, 16, 8 * ROWB, BS::LAYOUT),
-                      make_sdesc(o_addr + k * 32, 16, 8 * ROWB, BS::LAYOUT), idesc_s, k > 0 ? 1u : 0u);
-        }
-        mma_commit(&s_full[j % NBUF]);
+      for (int k = 0; k < DP / 16; ++k) {
+        mma_ss_w(tS, kd_s + 2 * k, qd_s + so + 2 * k, idesc_s, k > 0 ? 1u : 0u);
+        mma_ss_w(tDP, vd_s + 2 * k, od_s + so + 2 * k, idesc_s, k > 0 ? 1u : 0u);
       }
-      __syncwarp();
+      mma_commit_w(&s_full[j % NBUF]);
     };
     mbar_wait(kv_full, 0);
     for (int j = 0; j < NBUF && j < nqe; ++j) issue_s(j);
@@ -570,95 +578,97 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       if (lane == 0) trace_ev(fo.trace, 0, i, 1);
       if ((i & 1) && p >= 2) mbar_wait(&dq_empty[p & 1], ((p >> 1) - 1) & 1);
       tc_fence_after();
-      if (lane == 0) {
-        const uint32_t q_addr = smem_u32(sQ + st * QB), o_addr = smem_u32(sdO + st * QB);
-        const uint32_t tS = tbase + (i % NBUF) * 128, tDP = tS + 64;
+      const uint64_t so = (uint64_t)((st * QB) >> 4);
+      const uint32_t tS = tbase + (i % NBUF) * 128, tDP = tS + 64;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {  // 16 queries per step
-          const uint32_t acc = (i > 0 || k > 0) ? 1u : 0u;
-          mma_bf16_ts(tdV, tS + k * 8, make_sdesc(o_addr + k * 16 * ROWB, QB, 8 * ROWB, BS::LAYOUT), idesc_kv, acc);
-          mma_bf16_ts(tdK, tDP + k * 8, make_sdesc(q_addr + k * 16 * ROWB, QB, 8 * ROWB, BS::LAYOUT), idesc_kv,
-                      acc);
-        }
-        if (i & 1) {
-          const uint32_t ds_addr = smem_u32(sdS + (p & 1) * BS::DS_BUF);
-#pragma unroll
-          for (int k = 0; k < 8; ++k)  // 16 keys per step
-            mma_bf16_ss(tdQ0 + (p & 1) * DP, make_sdesc(ds_addr + k * 16 * 128, 128 * 128, 1024, 2u),
-                        make_sdesc(k_addr + k * 16 * ROWB, KB, 8 * ROWB, BS::LAYOUT), idesc_q, k > 0 ? 1u : 0u);
-          mma_commit(&dq_full[p & 1]);
-          mma_commit(&dsm_empty[p & 1]);
-        }
-        mma_commit(&qdo_empty[st]);
-        if (i == nqe - 1) mma_commit(dkv_done);
-        trace_ev(fo.trace, 0, i, 2);
+      for (int k = 0; k < 4; ++k) {  // 16 queries per step
+        const uint32_t acc = (i > 0 || k > 0) ? 1u : 0u;
+        mma_ts_w(tdV, tS + k * 8, od_kv + so + k * ROWB, idesc_kv, acc);
+        mma_ts_w(tdK, tDP + k * 8, qd_kv + so + k * ROWB, idesc_kv, acc);
       }
-      __syncwarp();
+      if (i & 1) {
+        const uint64_t dso = (uint64_t)(((p & 1) * BS::DS_BUF) >> 4);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)  // 16 keys per step
+          mma_ss_w(tdQ0 + (p & 1) * DP, dsd + dso + k * 128, kd_q + k * ROWB, idesc_q, k > 0 ? 1u : 0u);
+        mma_commit_w(&dq_full[p & 1]);
+        mma_commit_w(&dsm_empty[p & 1]);
+      }
+      mma_commit_w(&qdo_empty[st]);
+      if (i == nqe - 1) mma_commit_w(dkv_done);
+      if (lane == 0) trace_ev(fo.trace, 0, i, 2);
       if (i + NBUF < nqe) issue_s(i + NBUF);  // buffer i % NBUF is free once dV/dK(i) are issued (in-order)
       if (lane == 0) trace_ev(fo.trace, 0, i, 3);
     }
+  } else if (warp >= 10) {
+    // ============ dQ drain: 4 warps, one per TMEM lane quarter (thread = query row of the pair) ============
+    // Runs concurrently with the softmax warps.  DQ_TMA: TMEM -> registers -> 128B-swizzled smem boxes ->
+    // asynchronous TMA reduce-add (no per-element LSU traffic to contend with softmax); else vector reductions.
+    const int qq = warp & 3;
+    const uint32_t lane_off = (uint32_t)(qq * 32) << 16;
+    constexpr int CH = DP < 32 ? DP : 32;
+    uint8_t* stage = sDQ + qq * (32 * DH * 4);
+    for (int pp = 0; pp < npairs; ++pp) {
+      mbar_wait(&dq_full[pp & 1], (pp >> 1) & 1);
+      tc_fence_after();
+      const uint32_t tq = tdQ0 + (pp & 1) * DP + lane_off;
+      const int q = pp * 128 + qq * 32 + lane;
+      float* dst = nullptr;
+      if (!BS::DQ_TMA && q < S)
+        dst = fo.dqkv ? dQ + ((int64_t)b * S + q) * fo.H + h * DH : dQ + ((int64_t)bh * S + q) * DH;
+      if (BS::DQ_TMA) {
+        if (lane == 0) bulk_wait_read0();  // the previous pair's reduce has finished reading the staging boxes
+        __syncwarp();
+      }
+#pragma unroll
+      for (int c0 = 0; c0 < DP; c0 += CH) {
+        uint32_t u[CH];
+#pragma unroll
+        for (int c = 0; c < CH; c += 8)
+          tmem_ld8(tq + c0 + c, u[c], u[c + 1], u[c + 2], u[c + 3], u[c + 4], u[c + 5], u[c + 6], u[c + 7]);
+        tmem_ld_wait();
+        if (c0 + CH >= DP) {  // whole tile read: release the TMEM buffer to the MMA warp
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&dq_empty[pp & 1]);
+        }
+        if constexpr (BS::DQ_TMA) {
+          uint8_t* rowp = stage + (c0 / 32) * 4096 + lane * 128;
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<float4*>(rowp + ((j ^ (lane & 7)) << 4)) =
+                make_float4(__uint_as_float(u[4 * j]), __uint_as_float(u[4 * j + 1]), __uint_as_float(u[4 * j + 2]),
+                            __uint_as_float(u[4 * j + 3]));
+        } else if (dst != nullptr && fo.experiment != 2) {
+#pragma unroll
+          for (int c = 0; c < CH; c += 4)
+            if (c0 + c < DH)
+              red_add_v4_f32(dst + c0 + c, __uint_as_float(u[c]), __uint_as_float(u[c + 1]), __uint_as_float(u[c + 2]),
+                             __uint_as_float(u[c + 3]));
+        }
+      }
+      if constexpr (BS::DQ_TMA) {
+        // rows past this sequence carry exact zeros (dS = 0 there), so spilling into the next rows is harmless
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0 && fo.experiment != 2) {
+          const int row = (fo.dqkv ? b * S : bh * S) + pp * 128 + qq * 32;
+          const int col = fo.dqkv ? h * DH : 0;
+#pragma unroll
+          for (int c0 = 0; c0 < DH; c0 += 32) tma_reduce_2d(&tmdQ, stage + (c0 / 32) * 4096, col + c0, row);
+          bulk_commit_group();
+        }
+      }
+    }
+    if (BS::DQ_TMA && lane == 0) bulk_wait_all0();
   } else {
-    // ============ softmax-bwd (thread = key row; 2 warps per lane quarter, 32 queries each) + dQ drain ============
+    // ============ softmax-bwd (thread = key row; 2 warps per lane quarter, 32 queries each) ============
     const int qq = warp & 3;
     const int hf = (warp - 2) >> 2;
     const int kr = qq * 32 + lane;
     const int key = k0 + kr;
     const bool kvalid = key < S && (nonprefix ? key_mask[(int64_t)b * S + key] != 0 : key < kv_len);
     const uint32_t lane_off = (uint32_t)(qq * 32) << 16;
-    constexpr int DQH = DP / 2;  // dQ columns drained by this warp
-
-    auto drain_dq = [&](int pp) {  // thread = query row of pair pp
-      mbar_wait(&dq_full[pp & 1], (pp >> 1) & 1);
-      tc_fence_after();
-      const uint32_t tq = tdQ0 + (pp & 1) * DP;
-      if (fo.dqkv) {
-        // fused: both warps of a lane quarter drain half of the DH columns each through smem and a TMA
-        // bulk reduce-add of their 32 x DH/2 tile into the token-major fp32 dQ workspace
-        constexpr int HD = DH / 2;
-        uint32_t u[DQH];
-#pragma unroll
-        for (int c = 0; c < DQH; c += 8)
-          tmem_ld8(tq + lane_off + hf * HD + c, u[c], u[c + 1], u[c + 2], u[c + 3], u[c + 4], u[c + 5], u[c + 6],
-                   u[c + 7]);
-        tmem_ld_wait();
-        tc_fence_before();
-        float* stage = sDQ + (qq * 2 + hf) * 32 * HD;
-        if (lane == 0) bulk_wait_read0();  // previous reduce from this staging tile has read it
-        __syncwarp();
-        float4* row = reinterpret_cast<float4*>(stage + lane * HD);
-#pragma unroll
-        for (int c = 0; c < HD; c += 4)
-          row[c / 4] = make_float4(__uint_as_float(u[c]), __uint_as_float(u[c + 1]), __uint_as_float(u[c + 2]),
-                                   __uint_as_float(u[c + 3]));
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&dq_empty[pp & 1]);
-          // rows past this sequence carry exact zeros (dS = 0 there), so spilling into the next rows is harmless
-          tma_reduce_2d(&tmdQ, stage, h * DH + hf * HD, b * S + pp * 128 + qq * 32);
-          bulk_commit_group();
-        }
-        return;
-      }
-      uint32_t u[DQH];
-#pragma unroll
-      for (int c = 0; c < DQH; c += 8)
-        tmem_ld8(tq + lane_off + hf * DQH + c, u[c], u[c + 1], u[c + 2], u[c + 3], u[c + 4], u[c + 5], u[c + 6],
-                 u[c + 7]);
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&dq_empty[pp & 1]);
-      const int q = pp * 128 + kr;
-      if (q < S) {
-        float* dst = dQ + ((int64_t)bh * S + q) * DH + hf * DQH;
-#pragma unroll
-        for (int c = 0; c < DQH; c += 4)
-          if (hf * DQH + c < DH)
-            red_add_v4_f32(dst + c, __uint_as_float(u[c]), __uint_as_float(u[c + 1]), __uint_as_float(u[c + 2]),
-                           __uint_as_float(u[c + 3]));
-      }
-    };
 
     for (int i = 0; i < nqe; ++i) {
       const int st = i % QST, p = i >> 1, ch = i & 1;
@@ -671,6 +681,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_wait(&s_full[i % NBUF], (i / NBUF) & 1);
       if (lane == 0 && trole > 0) trace_ev(fo.trace, trole, i, 1);
       tc_fence_after();
+      if (fo.experiment == 1) {  // timing experiment: tensor/TMA pipeline alone
+        if (ch == 0 && p >= 2) mbar_wait(&dsm_empty[p & 1], ((p >> 1) - 1) & 1);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ds_full[i % NBUF]);
+        continue;
+      }
       uint32_t us[32], ud[32];
       tmem_ld32(tS + lane_off + c, us);
       tmem_ld32(tDP + lane_off + c, ud);
@@ -731,11 +748,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&ds_full[i % NBUF]);
       if (lane == 0 && trole > 0) trace_ev(fo.trace, trole, i, 5);
-      if (ch == 1 && p >= 1) drain_dq(p - 1);  // dQ of the previous pair finished long ago (double buffered)
-      if (lane == 0 && trole > 0) trace_ev(fo.trace, trole, i, 6);
     }
-    drain_dq(npairs - 1);
-    if (fo.dqkv && lane == 0) bulk_wait_all0();
     // ---- final rows: dK (hf == 0) or dV (hf == 1)
     mbar_wait(dkv_done, 0);
     tc_fence_after();
@@ -889,19 +902,20 @@ int launch_bwd(const void* q, const void* k, const void* v, const void* dout, co
       return ESM_EDRIVER;
     }
   }
-  if (fo.dqkv) {  // fused: token-major fp32 dQ workspace [B*S, nh*DH]; box = DH columns x 32 tokens
-    cuuint64_t dims[2] = {(cuuint64_t)nh * DH, (cuuint64_t)B * S};
-    cuuint64_t strides[1] = {(cuuint64_t)nh * DH * 4};
-    cuuint32_t box[2] = {(cuuint32_t)(DH / 2), 32};
+  if (BS::DQ_TMA) {  // fp32 dQ (fused: token-major [B*S, nh*DH]; classic: [B*nh*S, DH]); box 32 cols x 32 rows
+    const bool fused = fo.dqkv != nullptr;
+    cuuint64_t dims[2] = {(cuuint64_t)(fused ? nh * DH : DH), (cuuint64_t)(fused ? (int64_t)B * S : rows)};
+    cuuint64_t strides[1] = {(cuuint64_t)(fused ? nh * DH : DH) * 4};
+    cuuint32_t box[2] = {32, 32};
     cuuint32_t estr[2] = {1, 1};
     if (enc(&tdq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, dq, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
       set_last_error("attention bwd: dQ tensor map encode failed");
       return ESM_EDRIVER;
     }
   } else {
-    tdq = tdo;  // unused
+    tdq = tdo;  // unused: dQ is drained with vector reductions
   }
   static bool attr = false;
   if (!attr) {
@@ -926,7 +940,8 @@ int attn_bwd_tc(const void* q, const void* k, const void* v, const void* dout, c
     cudaMalloc(&g_attn_trace, 3 * 64 * 8 * 8);
     cudaMemset(g_attn_trace, 0, 3 * 64 * 8 * 8);
   }
-  fa::FusedOut fo{(__nv_bfloat16*)dqkv, col_sum, cos_t, sin_t, nh * dh, g_attn_trace};
+  static const int experiment = getenv("ESM_ATTN_EXPERIMENT") ? atoi(getenv("ESM_ATTN_EXPERIMENT")) : 0;
+  fa::FusedOut fo{(__nv_bfloat16*)dqkv, col_sum, cos_t, sin_t, nh * dh, g_attn_trace, experiment};
   switch (dh) {
     case 16: return fa::launch_bwd<16>(q, k, v, dout, lse2, delta, km, dq, dk, dv, B, nh, S, st, fo);
     case 24: return fa::launch_bwd<24>(q, k, v, dout, lse2, delta, km, dq, dk, dv, B, nh, S, st, fo);

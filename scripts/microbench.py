@@ -111,6 +111,33 @@ def gemm():
         print(f"gemm {name:16s} M={M} N={N} K={K}: {t:.3f} ms  {2.0 * M * N * K / t / 1e9:.0f} TF/s", flush=True)
 
 
+def rank():
+    """Geneformer tokeniser: device esm_rank_encode rows/s vs the CPU oracle restatement (single thread,
+    the reference's algorithm: SURVEY.md §8a1' quotes 3.7k rows/s for the reference itself)."""
+    import time
+    import numpy as np
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle"))
+    import rank_oracle as R
+    from paper_2411_10548_b200.data import RankEncoder, gene_medians, synthetic_expression_csr
+    n_genes, B, S = 25424, 256, 2048
+    ip, c, v = synthetic_expression_csr(B, n_genes, seed=0, nnz=(500, 4000))
+    med = gene_medians(ip, c, v, n_genes)
+    enc = RankEncoder(med)
+    (d_ip, d_c, d_v), mx = enc.stage(ip, c, v, np.arange(B))
+    ids = torch.empty(B, S, dtype=torch.int32, device="cuda")
+    am = torch.empty_like(ids)
+    t = timeit(lambda: enc.encode_device(d_ip, d_c, d_v, B, mx, S, ids=ids, am=am, stream=cur()))
+    want, _ = R.rank_encode_batch(ip, c, v, med, range(B), S, S)
+    assert np.array_equal(ids.cpu().numpy(), want)
+    t0 = time.perf_counter()
+    for r in range(64):
+        R.rank_encode(c[ip[r]:ip[r + 1]], v[ip[r]:ip[r + 1]], med, S)
+    cpu = 64 / (time.perf_counter() - t0)
+    nnz = (ip[-1]) / B
+    print(f"rank_encode {B} rows (mean nnz {nnz:.0f}) -> [{B},{S}]: {t:.3f} ms = {B / t * 1e3:,.0f} rows/s on the GPU; "
+          f"CPU oracle single thread {cpu:,.0f} rows/s; bit-exact", flush=True)
+
+
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "attn"
-    {"attn": attn, "gemm": gemm}[what]()
+    {"attn": attn, "gemm": gemm, "rank": rank}[what]()
