@@ -95,6 +95,17 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// 2^x on the FMA pipe (offloads part of the softmax exponentials from MUFU, 16/clk/SM): round-to-nearest
+// split x = j + f, f in [-0.5, 0.5], degree-3 minimax for 2^f (max rel. error 7.5e-5, far below the bf16
+// rounding of P), exponent added in the integer domain.  Inputs below -126 flush to ~2^-126.
+__device__ __forceinline__ float exp2_poly(float x) {
+  x = fmaxf(x, -126.f);
+  const float t = x + 12582912.f;  // 1.5 * 2^23: the low mantissa bits of t hold round(x)
+  const float f = x - (t - 12582912.f);
+  const float p = fmaf(fmaf(fmaf(0.05517166853f, f, 0.24261115491f), f, 0.69326096773f), f, 0.99992805719f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
@@ -366,10 +377,13 @@ __global__ void __launch_bounds__(kThreads, 2)
 //   warp 1     MMA: S^T = K Q_i^T, dP^T = V dO_i^T into TMEM; after softmax-bwd:
 //              dV += P^T dO_i, dK += dS^T Q_i (A = P^T / dS^T read from TMEM); once per block pair
 //              dQ_pair = dS K (M = 128 queries; A = dS^T of both blocks staged in smem, M-major)
-//   warps 2-5  softmax-bwd, thread = key row: P^T = exp2(S^T - LSE), dS^T = P^T (dP^T - Delta);
-//              P^T / dS^T written back to TMEM (bf16, over S^T / dP^T), dS^T also to smem; they also
-//              drain each pair's dQ (thread = query row) into HBM with fp32 vector reductions.
-// TMEM: S^T 64 + dP^T 64 + dV/dK/dQ 3*DP columns -> 256 for dh <= 32, so two CTAs share an SM.
+//   warps 2-9  softmax-bwd (2 warps per TMEM lane quarter, 32 queries each), thread = key row:
+//              P^T = exp2(S^T - LSE), dS^T = P^T (dP^T - Delta); P^T / dS^T written back to TMEM (bf16,
+//              over S^T / dP^T), dS^T also to smem (the A operand of dQ)
+//   warps 10-13 dQ drain (one per lane quarter, thread = query row): TMEM -> swizzled smem boxes ->
+//              TMA reduce-add into the fp32 dQ accumulator, overlapped with the softmax warps
+// TMEM (512 columns, one CTA per SM): NBUF x {S^T, dP^T} (64 columns each), dV, dK, 2 x dQ (DP each);
+// NBUF = 3 for dh <= 32, 2 for dh = 64.
 // Prefix (right-padded) masks: key blocks past the valid length write zero dK/dV and exit.
 constexpr int kBwdThreads = 448;  // TMA, MMA, 8 softmax-bwd warps, 4 dQ-drain warps
 
@@ -420,10 +434,13 @@ struct BwdShape {
   static constexpr int NBUF = DP <= 32 ? 3 : 2;  // {S^T, dP^T} TMEM buffers (128 columns each)
   static constexpr int QST = DH == 64 ? 5 : 6;   // Q / dO / LSE / Delta stages (>= NBUF + 1)
   static constexpr int DS_BUF = 2 * 128 * 128;  // one pair: [2 query chunks of 64][128 key rows][128 B]
-  // dQ drain: DH in {32, 64} stages 32-column fp32 boxes (128B-swizzled) for TMA reduce-add; 16/24 use
-  // vector reductions from registers
-  static constexpr bool DQ_TMA = DH == 32 || DH == 64;
-  static constexpr int DQ_STAGE = DQ_TMA ? 4 * 32 * DH * 4 : 0;
+  // dQ drain: fp32 boxes of BOXC columns x 32 rows, swizzled (128B or 64B rows), staged per drain warp for
+  // TMA reduce-add.  DH = 24 drains its zero-padded 32-column tile: the 8 extra columns either fall outside
+  // the tensor map (clipped) or add exact zeros to the neighbouring head's accumulator.
+  static constexpr int BOXC = DP < 32 ? DP : 32;
+  static constexpr int NBOX = DP / BOXC;
+  static constexpr int BOX_BYTES = 32 * BOXC * 4;
+  static constexpr int DQ_STAGE = 4 * NBOX * BOX_BYTES;
   static constexpr int SMEM = 2 * DS_BUF + 2 * KB + 2 * QST * QB + 2 * QST * 64 * 4 + DQ_STAGE + 1024 + 256;
 };
 
@@ -444,7 +461,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint8_t* sV = sK + KB;
   uint8_t* sQ = sV + KB;             // [QST][QB]
   uint8_t* sdO = sQ + QST * QB;      // [QST][QB]
-  uint8_t* sDQ = sdO + QST * QB;     // [4 warps][DH/32 boxes][32 rows][128 B] (1024-aligned: swizzled)
+  uint8_t* sDQ = sdO + QST * QB;     // [4 warps][NBOX][32 rows][BOXC fp32] (1024-aligned: swizzled)
   float* sL = reinterpret_cast<float*>(sDQ + BS::DQ_STAGE);  // [QST][64]
   float* sD = sL + QST * 64;                                 // [QST][64]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sD + QST * 64);
@@ -602,65 +619,51 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
   } else if (warp >= 10) {
     // ============ dQ drain: 4 warps, one per TMEM lane quarter (thread = query row of the pair) ============
-    // Runs concurrently with the softmax warps.  DQ_TMA: TMEM -> registers -> 128B-swizzled smem boxes ->
-    // asynchronous TMA reduce-add (no per-element LSU traffic to contend with softmax); else vector reductions.
+    // Runs concurrently with the softmax warps: TMEM -> registers -> swizzled smem boxes -> asynchronous TMA
+    // reduce-add into the fp32 dQ accumulator (no per-element LSU traffic to contend with the softmax).
     const int qq = warp & 3;
     const uint32_t lane_off = (uint32_t)(qq * 32) << 16;
-    constexpr int CH = DP < 32 ? DP : 32;
-    uint8_t* stage = sDQ + qq * (32 * DH * 4);
+    constexpr int BOXC = BS::BOXC, RB = BOXC * 4;           // fp32 columns / bytes per staged row
+    constexpr uint32_t SWM = RB == 128 ? 7u : 3u;            // 128B / 64B swizzle: chunk ^= (addr >> 7) & SWM
+    uint8_t* stage = sDQ + qq * (BS::NBOX * BS::BOX_BYTES);
     for (int pp = 0; pp < npairs; ++pp) {
       mbar_wait(&dq_full[pp & 1], (pp >> 1) & 1);
       tc_fence_after();
       const uint32_t tq = tdQ0 + (pp & 1) * DP + lane_off;
-      const int q = pp * 128 + qq * 32 + lane;
-      float* dst = nullptr;
-      if (!BS::DQ_TMA && q < S)
-        dst = fo.dqkv ? dQ + ((int64_t)b * S + q) * fo.H + h * DH : dQ + ((int64_t)bh * S + q) * DH;
-      if (BS::DQ_TMA) {
-        if (lane == 0) bulk_wait_read0();  // the previous pair's reduce has finished reading the staging boxes
-        __syncwarp();
-      }
+      if (lane == 0) bulk_wait_read0();  // the previous pair's reduce has finished reading the staging boxes
+      __syncwarp();
 #pragma unroll
-      for (int c0 = 0; c0 < DP; c0 += CH) {
-        uint32_t u[CH];
+      for (int x = 0; x < BS::NBOX; ++x) {
+        uint32_t u[BOXC];
 #pragma unroll
-        for (int c = 0; c < CH; c += 8)
-          tmem_ld8(tq + c0 + c, u[c], u[c + 1], u[c + 2], u[c + 3], u[c + 4], u[c + 5], u[c + 6], u[c + 7]);
+        for (int c = 0; c < BOXC; c += 8)
+          tmem_ld8(tq + x * BOXC + c, u[c], u[c + 1], u[c + 2], u[c + 3], u[c + 4], u[c + 5], u[c + 6], u[c + 7]);
         tmem_ld_wait();
-        if (c0 + CH >= DP) {  // whole tile read: release the TMEM buffer to the MMA warp
+        if (x == BS::NBOX - 1) {  // whole tile read: release the TMEM buffer to the MMA warp
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&dq_empty[pp & 1]);
         }
-        if constexpr (BS::DQ_TMA) {
-          uint8_t* rowp = stage + (c0 / 32) * 4096 + lane * 128;
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            *reinterpret_cast<float4*>(rowp + ((j ^ (lane & 7)) << 4)) =
-                make_float4(__uint_as_float(u[4 * j]), __uint_as_float(u[4 * j + 1]), __uint_as_float(u[4 * j + 2]),
-                            __uint_as_float(u[4 * j + 3]));
-        } else if (dst != nullptr && fo.experiment != 2) {
-#pragma unroll
-          for (int c = 0; c < CH; c += 4)
-            if (c0 + c < DH)
-              red_add_v4_f32(dst + c0 + c, __uint_as_float(u[c]), __uint_as_float(u[c + 1]), __uint_as_float(u[c + 2]),
-                             __uint_as_float(u[c + 3]));
+        for (int j = 0; j < BOXC / 4; ++j) {
+          const uint32_t off = (uint32_t)(lane * RB + j * 16);
+          *reinterpret_cast<float4*>(stage + x * BS::BOX_BYTES + (off ^ (((off >> 7) & SWM) << 4))) =
+              make_float4(__uint_as_float(u[4 * j]), __uint_as_float(u[4 * j + 1]), __uint_as_float(u[4 * j + 2]),
+                          __uint_as_float(u[4 * j + 3]));
         }
       }
-      if constexpr (BS::DQ_TMA) {
-        // rows past this sequence carry exact zeros (dS = 0 there), so spilling into the next rows is harmless
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0 && fo.experiment != 2) {
-          const int row = (fo.dqkv ? b * S : bh * S) + pp * 128 + qq * 32;
-          const int col = fo.dqkv ? h * DH : 0;
+      // rows past this sequence carry exact zeros (dS = 0 there), so spilling into the next rows is harmless
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0 && fo.experiment != 2) {
+        const int row = (fo.dqkv ? b * S : bh * S) + pp * 128 + qq * 32;
+        const int col = fo.dqkv ? h * DH : 0;
 #pragma unroll
-          for (int c0 = 0; c0 < DH; c0 += 32) tma_reduce_2d(&tmdQ, stage + (c0 / 32) * 4096, col + c0, row);
-          bulk_commit_group();
-        }
+        for (int x = 0; x < BS::NBOX; ++x) tma_reduce_2d(&tmdQ, stage + x * BS::BOX_BYTES, col + x * BOXC, row);
+        bulk_commit_group();
       }
     }
-    if (BS::DQ_TMA && lane == 0) bulk_wait_all0();
+    if (lane == 0) bulk_wait_all0();
   } else {
     // ============ softmax-bwd (thread = key row; 2 warps per lane quarter, 32 queries each) ============
     const int qq = warp & 3;
@@ -704,7 +707,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           const float p0 = ex2(fmaf(__uint_as_float(us[e]), L2E, -l4.x));
           const float p1 = ex2(fmaf(__uint_as_float(us[e + 1]), L2E, -l4.y));
           const float p2 = ex2(fmaf(__uint_as_float(us[e + 2]), L2E, -l4.z));
-          const float p3 = ex2(fmaf(__uint_as_float(us[e + 3]), L2E, -l4.w));
+          const float p3 = exp2_poly(fmaf(__uint_as_float(us[e + 3]), L2E, -l4.w));  // 1 in 4 on the FMA pipe
           pp[e >> 1] = pack2(p0, p1);
           pp[(e >> 1) + 1] = pack2(p2, p3);
           dd[e >> 1] = pack2(p0 * (__uint_as_float(ud[e]) - d4.x), p1 * (__uint_as_float(ud[e + 1]) - d4.y));
@@ -719,7 +722,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           float pr[4], ds[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const float pe = ex2(fmaf(__uint_as_float(us[e + u]), L2E, -lv[u]));
+            const float xe = fmaf(__uint_as_float(us[e + u]), L2E, -lv[u]);
+            const float pe = u == 3 ? exp2_poly(xe) : ex2(xe);
             pr[u] = (kvalid && e + u < qmax) ? pe : 0.f;
             ds[u] = pr[u] * (__uint_as_float(ud[e + u]) - dv4[u]);
           }
@@ -902,20 +906,18 @@ int launch_bwd(const void* q, const void* k, const void* v, const void* dout, co
       return ESM_EDRIVER;
     }
   }
-  if (BS::DQ_TMA) {  // fp32 dQ (fused: token-major [B*S, nh*DH]; classic: [B*nh*S, DH]); box 32 cols x 32 rows
+  {  // fp32 dQ accumulator (fused: token-major [B*S, nh*DH]; classic: [B*nh*S, DH]); box BOXC cols x 32 rows
     const bool fused = fo.dqkv != nullptr;
     cuuint64_t dims[2] = {(cuuint64_t)(fused ? nh * DH : DH), (cuuint64_t)(fused ? (int64_t)B * S : rows)};
     cuuint64_t strides[1] = {(cuuint64_t)(fused ? nh * DH : DH) * 4};
-    cuuint32_t box[2] = {32, 32};
+    cuuint32_t box[2] = {(cuuint32_t)BS::BOXC, 32};
     cuuint32_t estr[2] = {1, 1};
     if (enc(&tdq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, dq, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+            BS::BOXC == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
       set_last_error("attention bwd: dQ tensor map encode failed");
       return ESM_EDRIVER;
     }
-  } else {
-    tdq = tdo;  // unused: dQ is drained with vector reductions
   }
   static bool attr = false;
   if (!attr) {

@@ -25,10 +25,11 @@ print("rc", lib.esm_debug_attn_trace(buf.ctypes.data))
 t = buf.reshape(3, 64, 8).astype(np.int64)
 t0 = t[t > 0].min()
 names = {0: ["wait_ds", "ds_ok", "dvdk_issued", "s_next_issued"], 1: ["wait_s", "s_ok", "ld_done", "comp_done", "bar_done", "arrived", "drained"]}
+names[2] = names[1]
 nb = S // 64
 for r in range(3):
     print("role", r)
     for i in range(min(nb, 16)):
         ev = t[r, i]
-        n = names[0] if r == 0 else names[1]
+        n = names[r]
         print(f"  blk {i:2d} " + " ".join(f"{n[e]}={(ev[e]-t0) if ev[e] else -1:7d}" for e in range(len(n))))
