@@ -210,44 +210,34 @@ __global__ void __launch_bounds__(kThreads, 2)
     // ======================= MMA issuer =======================
     constexpr uint32_t idesc_s = make_idesc_bf16(BM, BN, false, false);  // S = Q Kᵀ, both K-major
     constexpr uint32_t idesc_o = make_idesc_bf16(BM, DP, false, true);   // O += P V, V N-major
-    const uint32_t q_addr = smem_u32(sQ);
+    // descriptors hoisted; stage offsets are added to the start-address field (bytes >> 4)
+    const uint64_t qd = make_sdesc(smem_u32(sQ), 16, 8 * ROWB, SH::LAYOUT);
+    const uint64_t kd = make_sdesc(smem_u32(sK), 16, 8 * ROWB, SH::LAYOUT);
+    const uint64_t vd = make_sdesc(smem_u32(sV), BN * ROWB, 8 * ROWB, SH::LAYOUT);
     mbar_wait(q_full, 0);
     for (int j = 0; j <= ntiles; ++j) {
       if (j < ntiles) {
         const int st = j % ST;
         mbar_wait(&kv_full[st], (j / ST) & 1);
         tc_fence_after();
-        if (lane == 0) {
-          const uint32_t k_addr = smem_u32(sK + st * TB);
-          const uint32_t d = tbase + (j & 1) * BN;
+        const uint64_t so = (uint64_t)((st * TB) >> 4);
+        const uint32_t d = tbase + (j & 1) * BN;
 #pragma unroll
-          for (int k = 0; k < DP / 16; ++k) {
-            const uint64_t ad = make_sdesc(q_addr + k * 32, 16, 8 * ROWB, SH::LAYOUT);
-            const uint64_t bd = make_sdesc(k_addr + k * 32, 16, 8 * ROWB, SH::LAYOUT);
-            mma_bf16_ss(d, ad, bd, idesc_s, k > 0 ? 1u : 0u);
-          }
-          mma_commit(&s_full[j & 1]);
-        }
-        __syncwarp();
+        for (int k = 0; k < DP / 16; ++k) mma_ss_w(d, qd + 2 * k, kd + so + 2 * k, idesc_s, k > 0 ? 1u : 0u);
+        mma_commit_w(&s_full[j & 1]);
       }
       if (j >= 1) {
         const int i = j - 1;  // O += P_i V_i
         const int st = i % ST;
         mbar_wait(&p_full[i & 1], (i >> 1) & 1);
         tc_fence_after();
-        if (lane == 0) {
-          const uint32_t v_addr = smem_u32(sV + st * TB);
-          const uint32_t p_tmem = tbase + (i & 1) * BN;
+        const uint64_t so = (uint64_t)((st * TB) >> 4);
+        const uint32_t p_tmem = tbase + (i & 1) * BN;
 #pragma unroll
-          for (int k = 0; k < BN / 16; ++k) {
-            // V tile: 128 key rows (K) x DP (N, contiguous); 16 keys per MMA = 16 rows
-            const uint64_t bd = make_sdesc(v_addr + k * 16 * ROWB, BN * ROWB, 8 * ROWB, SH::LAYOUT);
-            mma_bf16_ts(t_o, p_tmem + k * 8, bd, idesc_o, (i > 0 || k > 0) ? 1u : 0u);
-          }
-          mma_commit(&kv_empty[st]);
-          mma_commit(o_done);
-        }
-        __syncwarp();
+        for (int k = 0; k < BN / 16; ++k)  // V tile: BN key rows (K) x DP (N, contiguous); 16 keys per MMA
+          mma_ts_w(t_o, p_tmem + k * 8, vd + so + k * ROWB, idesc_o, (i > 0 || k > 0) ? 1u : 0u);
+        mma_commit_w(&kv_empty[st]);
+        mma_commit_w(o_done);
       }
     }
   } else {
