@@ -255,8 +255,7 @@ def main():
         if use_graph:
             model.graph_step()
         else:
-            model.forward_backward(ws)
-            model.optimizer_step()
+            model.step(ws)
 
     if use_graph:
         if pool_am is not None:
@@ -328,8 +327,7 @@ def main():
             if use_graph:
                 model.graph_step()
             else:
-                model.forward_backward(ws)
-                model.optimizer_step()
+                model.step(ws)
             return float(ws.loss_sum.item())
 
         for i in range(2):
@@ -367,8 +365,7 @@ def main():
             if use_graph:
                 model.graph_step()
             else:
-                model.forward_backward(ws)
-                model.optimizer_step()
+                model.step(ws)
             float(ws.loss_sum.item())                              # D2H: the step's loss
         torch.cuda.synchronize()
         wall = (time.perf_counter() - t0) / args.steps
@@ -378,7 +375,7 @@ def main():
         wall = float(tw.item())
         e2e = {"value": tokens_per_step / wall, "unit": "tokens/s", "h2d_bytes_per_step": B * S * 4,
                "d2h_bytes_per_step": 4, "ms_per_step": wall * 1e3, "api": "EsmForMaskedLM.mlm_mask+graph_step"
-               if use_graph else "EsmForMaskedLM.mlm_mask+forward_backward+optimizer_step"}
+               if use_graph else "EsmForMaskedLM.mlm_mask+step"}
 
     # ---------------- per-kernel breakdown (one extra eager step under CUDA events)
     hbm, tf_burst, tf_sust, peak_src = load_peaks()

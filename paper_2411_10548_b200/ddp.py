@@ -5,8 +5,10 @@ Parameter groups are laid out in backward-completion order (model.param_groups),
 bucket is a contiguous slice of ``store.g32``.  The model calls ``ready(group_key)`` as soon
 as all groups up to that key are final; every bucket fully covered is launched right away
 on a dedicated communication stream (NCCL over NVLink / NVSwitch through torch.distributed),
-while the compute stream continues with the next layer's backward.  ``end_backward`` makes
-the compute stream wait on the outstanding collectives before the optimizer.
+while the compute stream continues with the next layer's backward.  With ``on_bucket`` set (the
+model's overlapped optimizer), the AdamW update of each bucket is issued on the communication stream
+right behind its all-reduce, so the optimizer also overlaps the remaining backward.  ``end_backward``
+makes the compute stream wait on the outstanding collectives (and updates).
 
 Loss normalisation: the masked-token count is all-reduced before the loss kernel, every
 rank scales its gradients by 1 / N_global, and buckets are SUM-reduced -- the result equals
@@ -41,6 +43,7 @@ class GradAllReducer:
         self._works = []
         self._next = 0
         self._start = 0
+        self.on_bucket = None  # callable(start, end, stream) run after a bucket's all-reduce
 
     # ---------------------------------------------------------------- loss normaliser
     def reduce_count(self, n_labels: torch.Tensor):
@@ -62,9 +65,17 @@ class GradAllReducer:
             ev.record(torch.cuda.current_stream(g.device))
             with torch.cuda.stream(self.stream):
                 self.stream.wait_event(ev)
-                self._works.append(dist.all_reduce(g, op=dist.ReduceOp.SUM, group=self.group, async_op=True))
+                w = dist.all_reduce(g, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
+                if self.on_bucket is not None:
+                    w.wait()  # the comm stream waits for the collective, then updates the bucket
+                    self.on_bucket(self._start, end, self.stream)
+                self._works.append(w)
         else:
-            self._works.append(dist.all_reduce(g, op=dist.ReduceOp.SUM, group=self.group, async_op=True))
+            w = dist.all_reduce(g, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
+            if self.on_bucket is not None:
+                w.wait()
+                self.on_bucket(self._start, end, None)
+            self._works.append(w)
         self._start = end
 
     def ready(self, key: str):
@@ -79,4 +90,6 @@ class GradAllReducer:
             self._next += 1
         for w in self._works:
             w.wait()  # compute stream waits for the collective (NCCL) / completes (gloo)
+        if self.cuda and self.on_bucket is not None:
+            torch.cuda.current_stream(self.store.g32.device).wait_stream(self.stream)
         self._works = []

@@ -275,6 +275,7 @@ class EsmForMaskedLM:
         self.max_workspaces = 3
         self.comm = None  # set by ddp.GradAllReducer
         self.timer = None  # optional KernelTimer (bench.py per-kernel roofline)
+        self._opt_on, self._opt_start, self._opt_stream = False, 0, None
         self.launches = 0  # kernels launched by this model (C-ABI calls x kernels per call)
         self.graph = None
         self.graph_launches = 0
@@ -469,11 +470,15 @@ class EsmForMaskedLM:
         call("esm_scatter_rows", kdt, ws.dn_lab.data_ptr(), ws.head_idx.data_ptr(), ws.dn.data_ptr(), cap, H, T, st)
 
     # ------------------------------------------------------------------ forward + backward
-    def forward_backward(self, ws: Workspace | None = None, loss_only: bool = False):
+    def forward_backward(self, ws: Workspace | None = None, loss_only: bool = False, optimizer: bool = False):
         """Forward, masked-CE loss and full backward into ``store.g32`` (zeroed here).
 
         Inputs are taken from the workspace (input_ids, am, labels, n_labels).  Returns the device
-        loss tensor (mean over labelled tokens, or over ``n_labels`` if it was all-reduced)."""
+        loss tensor (mean over labelled tokens, or over ``n_labels`` if it was all-reduced).
+        ``optimizer=True`` also applies AdamW (hyper-parameters staged by ``set_hyper``), overlapped
+        with the backward: parameter groups are laid out in backward-completion order, so each
+        contiguous range of final gradients is updated on a side stream (single process) or on the
+        communication stream right after its bucket's all-reduce (DDP) while the backward continues."""
         ws = ws or self.ws
         cfg = self.config
         H, F, V, L, nh = cfg.hidden_size, cfg.intermediate_size, cfg.vocab_size, cfg.num_hidden_layers, \
@@ -539,8 +544,11 @@ class EsmForMaskedLM:
         if loss_only:
             return ws.loss_sum
         # ---------------- backward
+        self._opt_on = optimizer
+        self._opt_start = 0
         if self.comm is not None:
             self.comm.begin_backward()
+            self.comm.on_bucket = self._adamw_range if optimizer else None
         # LM head: LN^T then GELU'(y) fused; col sums -> dense bias grad
         call("esm_layernorm_bwd", kdt, ws.dn.data_ptr(), ws.g.data_ptr(),
              self._p32("lm_head.layer_norm.weight").data_ptr(), ws.lnh_m.data_ptr(), ws.lnh_r.data_ptr(), None,
@@ -556,8 +564,7 @@ class EsmForMaskedLM:
              None if fused else self._g32("esm.encoder.emb_layer_norm_after.weight").data_ptr(),
              None if fused else self._g32("esm.encoder.emb_layer_norm_after.bias").data_ptr(),
              self._g32(last_b2).data_ptr() if last_b2 else None, T, H, st)
-        if self.comm is not None:
-            self.comm.ready("esm.encoder.emb_layer_norm_after.bias")
+        self._group_ready("esm.encoder.emb_layer_norm_after.bias")
         dx, dx_next = ws.dx, ws.dx_alt
         for l in reversed(range(L)):
             p = f"esm.encoder.layer.{l}."
@@ -602,8 +609,7 @@ class EsmForMaskedLM:
                  None if fused else self._g32(p + "attention.LayerNorm.bias").data_ptr(),
                  self._g32(prev_b2).data_ptr() if prev_b2 else None, T, H, st)
             dx, dx_next = dx_next, dx
-            if self.comm is not None:
-                self.comm.ready(p + "attention.LayerNorm.bias")
+            self._group_ready(p + "attention.LayerNorm.bias")
         call("esm_embed_bwd", kdt, ws.input_ids.data_ptr(), ws.am.data_ptr(), ws.row_scale.data_ptr(),
              dx.data_ptr(), self._g32(E_key).data_ptr(), B, S, H, V,
              cfg.mask_token_id if cfg.token_dropout else -1, cfg.pad_token_id, st)
@@ -611,6 +617,9 @@ class EsmForMaskedLM:
             self.comm.ready(E_key)
             self.comm.end_backward()
             self.comm.reduce_loss(ws.loss_sum)
+        elif optimizer:
+            self._adamw_range(self._opt_start, self.store.numel, None)  # word embeddings: last, on the compute stream
+            torch.cuda.current_stream(self.device).wait_stream(self._opt_stream)
         self._last_dx_embed = dx
         return ws.loss_sum
 
@@ -629,6 +638,32 @@ class EsmForMaskedLM:
         ev = self._hyper_ev[i] = self._hyper_ev[i] or torch.cuda.Event()
         ev.record(torch.cuda.current_stream(self.device))
 
+    def _group_ready(self, key: str):
+        """All groups up to ``key`` (backward-completion order) hold final gradients."""
+        if self.comm is not None:
+            self.comm.ready(key)
+        elif self._opt_on:
+            end = (self.store.group_range[key][1] + ALIGN - 1) // ALIGN * ALIGN
+            if end > self._opt_start:
+                if self._opt_stream is None:
+                    self._opt_stream = torch.cuda.Stream(self.device)
+                ev = torch.cuda.Event()
+                ev.record(torch.cuda.current_stream(self.device))
+                self._opt_stream.wait_event(ev)
+                self._adamw_range(self._opt_start, end, self._opt_stream)
+
+    def _adamw_range(self, a: int, b: int, stream):
+        """AdamW on flat elements [a, b) (a, b multiples of 256) on ``stream`` (None: current)."""
+        b = min(b, self.store.numel)
+        if b <= a:
+            return
+        P = self.store
+        st = stream.cuda_stream if stream is not None else self._stream()
+        self._call("esm_adamw", P.p32[a:].data_ptr(), P.g32[a:].data_ptr(), P.m[a:].data_ptr(), P.v[a:].data_ptr(),
+                   P.p16[a:].data_ptr() if P.p16 is not None else None, P.decay[a // ALIGN:].data_ptr(), b - a,
+                   self.hyper.data_ptr(), st, nbytes=30.0 * (b - a))
+        self._opt_start = b
+
     def _adamw(self):
         P = self.store
         self._call("esm_adamw", P.p32.data_ptr(), P.g32.data_ptr(), P.m.data_ptr(), P.v.data_ptr(),
@@ -636,9 +671,17 @@ class EsmForMaskedLM:
                    self.hyper.data_ptr(), self._stream(), nbytes=30.0 * P.numel)
 
     def optimizer_step(self, lr=None):
+        """AdamW over all parameters after a separate ``forward_backward`` (un-overlapped)."""
         self.step_count += 1
         self.set_hyper(lr=lr, step=self.step_count)
         self._adamw()
+
+    def step(self, ws: Workspace | None = None, lr=None):
+        """One full train step on the staged batch: forward, backward and AdamW overlapped with the
+        backward (same arithmetic as forward_backward + optimizer_step).  Returns the device loss."""
+        self.step_count += 1
+        self.set_hyper(lr=lr, step=self.step_count)
+        return self.forward_backward(ws, optimizer=True)
 
     # ------------------------------------------------------------------ CUDA graph
     def capture(self, ws: Workspace | None = None):
@@ -657,8 +700,7 @@ class EsmForMaskedLM:
         g = torch.cuda.CUDAGraph()
         n0 = self.launches
         with torch.cuda.graph(g):
-            self.forward_backward(ws)
-            self._adamw()
+            self.forward_backward(ws, optimizer=True)
         ws.graph = g
         ws.graph_launches = self.launches - n0
         self.graph = g
@@ -691,13 +733,9 @@ class EsmForMaskedLM:
             if getattr(ws, "graph", None) is None:
                 self.capture(ws)
             return self.graph_step(lr=lr, ws=ws)
-        loss = self.forward_backward(ws)
-        self.optimizer_step(lr=lr)
-        return loss
+        return self.step(ws, lr=lr)
 
     def train_step(self, input_ids, attention_mask=None, labels=None, lr=None):
         """One MLM train step on an already-masked batch; returns the device loss tensor."""
         ws = self.set_batch(input_ids, attention_mask, labels)
-        loss = self.forward_backward(ws)
-        self.optimizer_step(lr=lr)
-        return loss
+        return self.step(ws, lr=lr)

@@ -69,8 +69,7 @@ def make_workload(model, seed: int = 0, pad_to: int = 8, lr: float | None = None
         ws = model.workspace(*ids.shape)
         ws.am.copy_(torch.from_numpy(am).to(model.device))
         model.mlm_mask(ids_d, seed, state["step"], ws)
-        model.forward_backward(ws)
-        model.optimizer_step(lr=lr)
+        model.step(ws, lr=lr)
         state["step"] += 1
         return float(ws.loss_sum.item())
 

@@ -43,6 +43,17 @@ def main():
         g_ddp = m.store.g32.clone()
         m.optimizer_step()
         p_ddp = m.store.p32.clone()
+        # the same step with AdamW overlapped (per bucket, behind its all-reduce on the comm stream)
+        m2 = EsmForMaskedLM(cfg, dtype=dtype, device=dev, seed=3)
+        m2.comm = GradAllReducer(m2.store, bucket_bytes=4 << 20)
+        ws2 = m2.workspace(B, S)
+        m2.mlm_mask(mine, seed=7, stream_id=rank, ws=ws2)
+        loss2 = float(m2.step(ws2).item())
+        ferr = (m2.store.p32 - p_ddp).abs().max().item()
+        fgood = ferr < 1e-6 and abs(loss2 - loss) <= 1e-6 * loss  # atomics order only
+        ok &= fgood
+        print(f"[{dtype}] rank {rank}: overlapped optimizer vs separate: max|dparam|={ferr:.1e} "
+              f"loss {loss2:.6f}/{loss:.6f} {'OK' if fgood else 'FAIL'}", flush=True)
         if rank == 0:
             ref = EsmForMaskedLM(cfg, dtype=dtype, device=dev, seed=3)
             wr = ref.workspace(B * world, S)
