@@ -200,6 +200,8 @@ def run_reference(args, rank, world):
 # ------------------------------------------------------------------ our B200 path
 def main():
     args = parse()
+    # NCCL's debug/version banner goes to stdout by default; keep stdout to the one JSON line
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
