@@ -101,6 +101,40 @@ __device__ __forceinline__ float gelu_grad_f(float x) {
   return cdf + x * pdf;
 }
 
+// erf-GELU for the bf16 tcgen05 epilogues: one MUFU op per element.  erfc(x) = exp(-x^2) R(x) for x >= 0
+// with R a degree-8 minimax fit on [0, 4] (relative error 2.8e-4: GELU / GELU' absolute error <= 4e-5 / 1.1e-4,
+// ~2e-4 relative where GELU is not negligible, below the bf16 rounding of the stored result); R's argument
+// is clamped at 4 (erfc(4) = 1.5e-8).  GELU(z) = max(z, 0) - |z|/2 * erfc(|z|/sqrt2).  The fp32 parity path uses erff.
+__device__ __forceinline__ float erfc_core(float x, float& ex) {  // x >= 0; ex = exp(-x^2)
+  const float xr = fminf(x, 4.0f);  // R fitted on [0, 4]; exp(-x^2) itself is not clamped
+  float r = 1.1063529e-04f;
+  r = fmaf(r, xr, -2.1946724e-03f);
+  r = fmaf(r, xr, 1.8796470e-02f);
+  r = fmaf(r, xr, -9.1806091e-02f);
+  r = fmaf(r, xr, 2.8634080e-01f);
+  r = fmaf(r, xr, -6.1150831e-01f);
+  r = fmaf(r, xr, 9.4866168e-01f);
+  r = fmaf(r, xr, -1.1205097e+00f);
+  r = fmaf(r, xr, 9.9977970e-01f);
+  float e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-1.4426950408889634f * x * x));
+  ex = e;
+  return e * r;
+}
+__device__ __forceinline__ float gelu_fast(float z) {
+  const float x = fabsf(z) * 0.70710678118654752f;
+  float ex;
+  const float ec = erfc_core(x, ex);
+  return fmaxf(z, 0.f) - 0.5f * fabsf(z) * ec;
+}
+__device__ __forceinline__ float gelu_grad_fast(float z) {
+  const float x = fabsf(z) * 0.70710678118654752f;
+  float ex;
+  const float ec = erfc_core(x, ex);
+  const float cdf = z >= 0.f ? 1.f - 0.5f * ec : 0.5f * ec;
+  return fmaf(z * 0.3989422804014327f, ex, cdf);  // Phi(z) + z * phi(z), phi = exp(-z^2/2) / sqrt(2 pi)
+}
+
 __device__ __forceinline__ void red_add_f32(float* p, float v) {
   asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }

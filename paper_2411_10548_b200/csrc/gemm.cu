@@ -416,7 +416,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int e = 0; e < 8; ++e) {
                 if constexpr (EPI == ESM_EPI_RESID) v[8 * k + e] += rv[e];
-                else v[8 * k + e] *= gelu_grad_f(rv[e]);
+                else v[8 * k + e] *= gelu_grad_fast(rv[e]);
               }
             }
             __syncwarp();
@@ -438,7 +438,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int k = 0; k < 4; ++k)
               store_vec(reinterpret_cast<__nv_bfloat16*>(o + E::CHUNK + stage_off<false>(lane, k)), v + 8 * k);
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = gelu_f(v[j]);
+            for (int j = 0; j < 32; ++j) v[j] = gelu_fast(v[j]);
           }
 #pragma unroll
           for (int k = 0; k < 4; ++k)

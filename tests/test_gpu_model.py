@@ -171,3 +171,25 @@ def test_overlapped_optimizer_matches_separate_step(dtype):
     for x, y in ((a.store.p32, b.store.p32), (a.store.m, b.store.m), (a.store.v, b.store.v)):
         assert (x - y).abs().max().item() <= 1e-5 * x.abs().max().item()
     assert (a.store.p32 - params_flat(a, params)).abs().max().item() > 0  # parameters did move
+
+
+def test_collect_peak_alloc_seam_workload_and_meter():
+    """the workload / ResourceMeter pair handed to the reference's collect_peak_alloc
+    (pkg/src/densefeed/sizing.py:76-100): each call is one full MLM train step; the meter's peak grows with
+    the sample's token count (the [L, L^2] cost features fit_cost_model regresses on)."""
+    from paper_2411_10548_b200.seams import CudaPeakMeter, length_features, make_workload
+    cfg, _ = _cfgs(64, 2, 4, 256)
+    m = EsmForMaskedLM(cfg, dtype="bf16", device="cuda", params=init_params(cfg, seed=3))
+    wl, meter = make_workload(m, seed=5, pad_to=64), CudaPeakMeter()
+    rng = np.random.default_rng(0)
+    peaks, feats = [], []
+    for n in (60, 250, 1000):
+        sample = [list(np.r_[0, rng.integers(4, 24, n - 2), 2]) for _ in range(4)]
+        meter.reset()
+        loss = wl(sample)
+        peaks.append(meter.peak())
+        feats.append(length_features(sample))
+        assert np.isfinite(loss) and loss > 0
+    assert peaks[0] < peaks[1] < peaks[2]
+    assert np.allclose(feats[1], [4 * 250, 4 * 250 ** 2])
+    assert m.step_count == 3
