@@ -143,34 +143,32 @@ def test_varlen_bucketed_batches_match_oracle():
     assert len(m._ws_cache) <= m.max_workspaces
 
 
-def params_flat(m, params):
-    ref = EsmForMaskedLM(m.config, dtype=m.dtype, device="cuda", params=params)
-    return ref.store.p32
-
-
 @pytest.mark.parametrize("dtype", ["fp32", "bf16"])
 def test_overlapped_optimizer_matches_separate_step(dtype):
-    """model.step (AdamW per completed gradient range on a side stream, overlapped with backward) gives the
-    parameters, Adam moments and bf16 shadow of forward_backward + optimizer_step (up to the order of the
-    floating-point atomics in the loss / gradient reductions)."""
+    """model.step (AdamW per completed gradient range on a side stream, overlapped with the backward) applies
+    exactly the update of the separate AdamW pass: replaying optimizer_step on the gradients the overlapped
+    step produced gives bit-identical parameters, Adam moments and bf16 shadow (AdamW is elementwise; the
+    gradients themselves carry atomic-order noise, so both paths are fed the same gradient buffer)."""
     cfg, _ = _cfgs(64, 3, 4, 256)
     params = init_params(cfg, seed=11)
-    ids, am = O.synthetic_batch(4, 64, seed=12)
-    inp, lab = O.mlm_mask(ids, seed=1, stream=2)
     a = EsmForMaskedLM(cfg, dtype=dtype, device="cuda", params=params, lr=1e-3)
     b = EsmForMaskedLM(cfg, dtype=dtype, device="cuda", params=params, lr=1e-3)
+    p0 = b.store.p32.clone()
     for step in range(3):
-        wa = a.set_batch(torch.from_numpy(inp).cuda(), torch.from_numpy(am).cuda(), torch.from_numpy(lab).cuda())
-        la = a.forward_backward(wa)
-        a.optimizer_step()
+        ids, am = O.synthetic_batch(4, 64, seed=12 + step)
+        inp, lab = O.mlm_mask(ids, seed=1, stream=step)
         wb = b.set_batch(torch.from_numpy(inp).cuda(), torch.from_numpy(am).cuda(), torch.from_numpy(lab).cuda())
-        lb = b.step(wb)
-        assert abs(float(la.item()) - float(lb.item())) <= 1e-5 * abs(float(la.item()))
-    torch.cuda.synchronize()
+        b.step(wb)
+        torch.cuda.synchronize()
+        a.store.g32.copy_(b.store.g32)
+        a.optimizer_step()
+        torch.cuda.synchronize()
+        for x, y in ((a.store.p32, b.store.p32), (a.store.m, b.store.m), (a.store.v, b.store.v)):
+            assert torch.equal(x, y), step
+        if dtype == "bf16":
+            assert torch.equal(a.store.p16, b.store.p16)
     assert a.step_count == b.step_count == 3
-    for x, y in ((a.store.p32, b.store.p32), (a.store.m, b.store.m), (a.store.v, b.store.v)):
-        assert (x - y).abs().max().item() <= 1e-5 * x.abs().max().item()
-    assert (a.store.p32 - params_flat(a, params)).abs().max().item() > 0  # parameters did move
+    assert (b.store.p32 - p0).abs().max().item() > 0  # parameters did move
 
 
 def test_collect_peak_alloc_seam_workload_and_meter():
