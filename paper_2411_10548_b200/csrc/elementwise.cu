@@ -197,6 +197,22 @@ __device__ __forceinline__ float2 group_sum2(float2 v, float2* red, int wig, int
   }
 }
 
+template <typename T>
+__device__ __forceinline__ void unpack_vec(const uint4& u, float* out) {  // 16 raw bytes -> VEC floats
+  if constexpr (sizeof(T) == 2) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __bfloat1622float2(h[i]);
+      out[2 * i] = f.x;
+      out[2 * i + 1] = f.y;
+    }
+  } else {
+    out[0] = __uint_as_float(u.x); out[1] = __uint_as_float(u.y);
+    out[2] = __uint_as_float(u.z); out[3] = __uint_as_float(u.w);
+  }
+}
+
 __device__ __forceinline__ void load_f32x(const float* p, float* o, int n) {
   // n = 8 (bf16 VEC) or 4 (fp32 VEC); p 16B aligned
   const float4 a = *reinterpret_cast<const float4*>(p);
@@ -229,45 +245,79 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const T* __restrict__ x, co
     }
   }
   const float invH = 1.0f / H;
-  for (int64_t r = (int64_t)blockIdx.x * GPB + grp; r < rows; r += (int64_t)gridDim.x * GPB) {
-    float v[MAXV][VEC];
-    float s = 0.f;
+  // two rows per group iteration: both rows' loads are in flight together and their statistics are
+  // reduced as one float2 (half the cross-lane reductions per row).  Rows stay packed (raw 16-byte
+  // vectors, unpacked on the fly) so a lane can hold 2 rows x 3 vectors without spilling occupancy.
+  for (int64_t r0 = ((int64_t)blockIdx.x * GPB + grp) * 2; r0 < rows; r0 += (int64_t)gridDim.x * GPB * 2) {
+    const bool has1 = r0 + 1 < rows;
+    uint4 raw[2][MAXV];
+    float s0 = 0.f, s1 = 0.f;
 #pragma unroll
     for (int i = 0; i < MAXV; ++i) {
       const int h = (i * WPR * 32 + glane) * VEC;
       if (h < H) {
-        load_vec(x + r * H + h, v[i]);
-#pragma unroll
-        for (int j = 0; j < VEC; ++j) s += v[i][j];
+        raw[0][i] = *reinterpret_cast<const uint4*>(x + r0 * H + h);
+        raw[1][i] = has1 ? *reinterpret_cast<const uint4*>(x + (r0 + 1) * H + h) : make_uint4(0u, 0u, 0u, 0u);
       }
     }
-    const float mu = group_sum2<WPR>(make_float2(s, 0.f), red[grp], wig, lane, grp + 1, parity).x * invH;
-    float ss = 0.f;
 #pragma unroll
     for (int i = 0; i < MAXV; ++i) {
       const int h = (i * WPR * 32 + glane) * VEC;
       if (h < H) {
+        float v0[VEC], v1[VEC];
+        unpack_vec<T>(raw[0][i], v0);
+        unpack_vec<T>(raw[1][i], v1);
 #pragma unroll
         for (int j = 0; j < VEC; ++j) {
-          const float d = v[i][j] - mu;
-          ss += d * d;
+          s0 += v0[j];
+          s1 += v1[j];
         }
       }
     }
-    const float rs = rsqrtf(group_sum2<WPR>(make_float2(ss, 0.f), red[grp], wig, lane, grp + 1, parity).x * invH + eps);
+    const float2 mu = group_sum2<WPR>(make_float2(s0, s1), red[grp], wig, lane, grp + 1, parity);
+    const float mu0 = mu.x * invH, mu1 = mu.y * invH;
+    float ss0 = 0.f, ss1 = 0.f;
 #pragma unroll
     for (int i = 0; i < MAXV; ++i) {
       const int h = (i * WPR * 32 + glane) * VEC;
       if (h < H) {
-        float o[VEC];
+        float v0[VEC], v1[VEC];
+        unpack_vec<T>(raw[0][i], v0);
+        unpack_vec<T>(raw[1][i], v1);
 #pragma unroll
-        for (int j = 0; j < VEC; ++j) o[j] = (v[i][j] - mu) * rs * gv[i][j] + bv[i][j];
-        store_vec(y + r * H + h, o);
+        for (int j = 0; j < VEC; ++j) {
+          const float d0 = v0[j] - mu0, d1 = v1[j] - mu1;
+          ss0 += d0 * d0;
+          ss1 += d1 * d1;
+        }
+      }
+    }
+    const float2 var = group_sum2<WPR>(make_float2(ss0, ss1), red[grp], wig, lane, grp + 1, parity);
+    const float rs0 = rsqrtf(var.x * invH + eps), rs1 = rsqrtf(var.y * invH + eps);
+#pragma unroll
+    for (int i = 0; i < MAXV; ++i) {
+      const int h = (i * WPR * 32 + glane) * VEC;
+      if (h < H) {
+        float v[VEC], o[VEC];
+        unpack_vec<T>(raw[0][i], v);
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) o[j] = (v[j] - mu0) * rs0 * gv[i][j] + bv[i][j];
+        store_vec(y + r0 * H + h, o);
+        if (has1) {
+          unpack_vec<T>(raw[1][i], v);
+#pragma unroll
+          for (int j = 0; j < VEC; ++j) o[j] = (v[j] - mu1) * rs1 * gv[i][j] + bv[i][j];
+          store_vec(y + (r0 + 1) * H + h, o);
+        }
       }
     }
     if (glane == 0) {
-      mean_out[r] = mu;
-      rstd_out[r] = rs;
+      mean_out[r0] = mu0;
+      rstd_out[r0] = rs0;
+      if (has1) {
+        mean_out[r0 + 1] = mu1;
+        rstd_out[r0 + 1] = rs1;
+      }
     }
   }
 }
@@ -769,10 +819,10 @@ int esm_embed_bwd(int dtype, const int32_t* ids, const int32_t* am, const float*
 }
 
 // choose (MAXV, WPR): WPR = smallest power of two with <= 3 vectors per lane
-static inline void ln_shape(int H, int vec, int& maxv, int& wpr) {
+static inline void ln_shape(int H, int vec, int& maxv, int& wpr, int max_per_lane = 3) {
   const int vectors = H / vec;
   wpr = 1;
-  while (wpr < 8 && vectors > wpr * 32 * 3) wpr <<= 1;
+  while (wpr < 8 && vectors > wpr * 32 * max_per_lane) wpr <<= 1;
   maxv = (vectors + wpr * 32 - 1) / (wpr * 32);
 }
 
@@ -812,7 +862,7 @@ int esm_layernorm_fwd(int dtype, const void* x, const float* gamma, const float*
   int mv, wpr;
   ln_shape(H, vec, mv, wpr);
   const int gpb = 8 / wpr;
-  int grid = (int)((rows + gpb - 1) / gpb);
+  int grid = (int)((rows + 2 * gpb - 1) / (2 * gpb));  // 2 rows per group iteration
   if (grid > 148 * 8) grid = 148 * 8;
 #define L_F(...) __VA_ARGS__<<<grid, 256, 0, S(stream)>>>((const TT*)x, gamma, beta, (TT*)y, mean, rstd, rows, H, eps)
   if (dtype == ESM_BF16) {

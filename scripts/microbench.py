@@ -111,6 +111,23 @@ def gemm():
         print(f"gemm {name:16s} M={M} N={N} K={K}: {t:.3f} ms  {2.0 * M * N * K / t / 1e9:.0f} TF/s", flush=True)
 
 
+def ln():
+    """LayerNorm fwd / bwd (no dgamma/dbeta: fused into the dgrad GEMM; with residual add) achieved GB/s."""
+    for T, H in [(32768, 480), (32768, 768), (16384, 1280), (4096, 2560)]:
+        x = torch.randn(T, H, device="cuda").bfloat16()
+        y, dy, dres, dx = (torch.randn(T, H, device="cuda").bfloat16() for _ in range(4))
+        g, b = torch.ones(H, device="cuda"), torch.zeros(H, device="cuda")
+        mu, rs = torch.empty(T, device="cuda"), torch.empty(T, device="cuda")
+        f = lambda: _lib.call("esm_layernorm_fwd", ESM_BF16, x.data_ptr(), g.data_ptr(), b.data_ptr(), y.data_ptr(),  # noqa
+                              mu.data_ptr(), rs.data_ptr(), T, H, 1e-5, cur())
+        bw = lambda: _lib.call("esm_layernorm_bwd", ESM_BF16, dy.data_ptr(), x.data_ptr(), g.data_ptr(), mu.data_ptr(),  # noqa
+                               rs.data_ptr(), dres.data_ptr(), None, dx.data_ptr(), None, None, None, T, H, cur())
+        tf, tb = timeit(f, iters=20), timeit(bw, iters=20)
+        bf, bb = T * H * 4 + T * 8, T * H * 8 + T * 8
+        print(f"layernorm T={T} H={H}: fwd {tf * 1e3:.1f} us ({bf / tf / 1e6:.0f} GB/s)  "
+              f"bwd {tb * 1e3:.1f} us ({bb / tb / 1e6:.0f} GB/s)", flush=True)
+
+
 def rank():
     """Geneformer tokeniser: device esm_rank_encode rows/s vs the CPU oracle restatement (single thread,
     the reference's algorithm: SURVEY.md §8a1' quotes 3.7k rows/s for the reference itself)."""
@@ -140,4 +157,4 @@ def rank():
 
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "attn"
-    {"attn": attn, "gemm": gemm, "rank": rank}[what]()
+    {"attn": attn, "gemm": gemm, "rank": rank, "ln": ln}[what]()
