@@ -590,8 +590,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
       for (int k = 0; k < 4; ++k) {  // 16 queries per step
         const uint32_t acc = (i > 0 || k > 0) ? 1u : 0u;
-        mma_ts_w(tdV, tS + k * 8, od_kv + so + k * ROWB, idesc_kv, acc);
-        mma_ts_w(tdK, tDP + k * 8, qd_kv + so + k * ROWB, idesc_kv, acc);
+        // packed P^T / dS^T of queries [16k, 16k+16): warp half (k >> 1) wrote them at column 32 (k >> 1) + 8 (k & 1)
+        const uint32_t pc = (uint32_t)((k >> 1) * 32 + (k & 1) * 8);
+        mma_ts_w(tdV, tS + pc, od_kv + so + k * ROWB, idesc_kv, acc);
+        mma_ts_w(tdK, tDP + pc, qd_kv + so + k * ROWB, idesc_kv, acc);
       }
       if (i & 1) {
         const uint64_t dso = (uint64_t)(((p & 1) * BS::DS_BUF) >> 4);
@@ -723,12 +725,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           dd[(e >> 1) + 1] = pack2(ds[2], ds[3]);
         }
       }
-      // both warps of this lane quarter must have read S^T / dP^T before the packed P^T / dS^T overwrite them
+      // packed P^T / dS^T go into this warp's own 32-column half of the S^T / dP^T buffers (which it has
+      // finished reading), so the two warps of a lane quarter need no barrier
       if (lane == 0 && trole > 0) trace_ev(fo.trace, trole, i, 3);
-      asm volatile("bar.sync %0, 64;" ::"r"(1 + qq) : "memory");
-      if (lane == 0 && trole > 0) trace_ev(fo.trace, trole, i, 4);
-      tmem_st16(tS + lane_off + hf * 16, pp);
-      tmem_st16(tDP + lane_off + hf * 16, dd);
+      tmem_st16(tS + lane_off + hf * 32, pp);
+      tmem_st16(tDP + lane_off + hf * 32, dd);
       uint8_t* rowp = sdS + (p & 1) * BS::DS_BUF + ch * (128 * 128) + kr * 128;
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
