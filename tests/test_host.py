@@ -139,7 +139,24 @@ def _ddp_worker(rank, world, port, q):
         ok_grad = torch.equal(st.g32, want)
         n = torch.tensor([10 * (rank + 1)], dtype=torch.int32)
         red.reduce_count(n)
-        q.put((rank, ok_grad, int(n.item()), len(red.bucket_ends)))
+        # overlapped optimizer hook: each bucket is handed over (in order, contiguous, covering the whole
+        # buffer) only after its all-reduce has completed
+        seen = []
+        want2 = 2 * torch.arange(st.numel, dtype=torch.float32) * world
+        red.on_bucket = lambda a, b, stream: seen.append((a, b, bool(torch.equal(st.g32[a:b], want2[a:b]))))
+        st.g32.copy_(g)
+        st.g32.mul_(2)
+        st.g32.div_(rank + 1)  # every rank holds 2 * arange -> reduced = 2 * arange * world
+        red.begin_backward()
+        red.ready("esm.encoder.emb_layer_norm_after.bias")
+        for l in reversed(range(cfg.num_hidden_layers)):
+            red.ready(f"esm.encoder.layer.{l}.attention.LayerNorm.bias")
+        red.ready("esm.embeddings.word_embeddings.weight")
+        red.end_backward()
+        contiguous = seen[0][0] == 0 and seen[-1][1] == st.numel and all(
+            seen[i][1] == seen[i + 1][0] for i in range(len(seen) - 1))
+        hooks_ok = contiguous and all(ok for _, _, ok in seen)
+        q.put((rank, ok_grad and hooks_ok, int(n.item()), len(red.bucket_ends)))
     finally:
         dist.destroy_process_group()
 
@@ -158,6 +175,20 @@ def test_grad_bucket_allreduce_gloo_world2():
         assert ok, rank
         assert n == 30
         assert nb > 1  # several buckets -> overlap with backward is possible
+
+
+def test_head_capacity_and_config_validation():
+    from paper_2411_10548_b200.config import geneformer_config
+    from paper_2411_10548_b200.model import head_capacity
+    for T in (64, 1000, 16384, 65536):
+        cap = head_capacity(T)
+        assert cap <= T and (cap == T or cap % 128 == 0)
+        assert cap >= min(T, 0.15 * T + 8 * T ** 0.5)  # > 20 sigma above the 15% mean
+    with pytest.raises(ValueError):
+        EsmConfig(vocab_size=33, mlm_eligible=(4, 40)).validate()
+    with pytest.raises(ValueError):
+        geneformer_config(n_genes=100, mlm_random=(2, 200))
+    assert geneformer_config(n_genes=100).vocab_size == 102
 
 
 def test_geneformer_preset_and_feed_host_logic():
