@@ -474,45 +474,89 @@ __global__ void qkv_rope_fwd_kernel(const T* __restrict__ qkv, T* __restrict__ q
 
 // each thread owns one (head, j) column pair of q, k and v; loops rows; column sums -> bias grads
 template <typename T>
-__global__ void qkv_rope_bwd_kernel(const float* __restrict__ dq, const T* __restrict__ dk,
-                                    const T* __restrict__ dv, T* __restrict__ dqkv, float* __restrict__ csum,
-                                    const float* __restrict__ cs, const float* __restrict__ sn, int64_t T_, int S,
-                                    int nh, int dh, float qs, int rows_per_block) {
+struct pair2;  // two adjacent elements
+template <> struct pair2<float> {
+  static __device__ __forceinline__ float2 ld(const float* p) { return *reinterpret_cast<const float2*>(p); }
+  static __device__ __forceinline__ void st(float* p, float a, float b) { *reinterpret_cast<float2*>(p) = make_float2(a, b); }
+};
+template <> struct pair2<__nv_bfloat16> {
+  static __device__ __forceinline__ float2 ld(const __nv_bfloat16* p) {
+    return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(p));
+  }
+  static __device__ __forceinline__ void st(__nv_bfloat16* p, float a, float b) {
+    *reinterpret_cast<__nv_bfloat162*>(p) = __floats2bfloat162_rn(a, b);
+  }
+};
+
+// RoPE^T + q-scale + [B, nh, S, dh] -> token-major dqkv [T, 3H] relayout + q/k/v bias-gradient column sums.
+// Thread = two adjacent rotation pairs (j, j+1) of one head (float2 / bf16x2 accesses), a block-row of
+// tokens processed RU at a time so each thread keeps RU tokens' loads in flight.
+template <typename T>
+__global__ void __launch_bounds__(256) qkv_rope_bwd_kernel(const float* __restrict__ dq, const T* __restrict__ dk,
+                                                           const T* __restrict__ dv, T* __restrict__ dqkv,
+                                                           float* __restrict__ csum, const float* __restrict__ cs,
+                                                           const float* __restrict__ sn, int64_t T_, int S, int nh,
+                                                           int dh, float qs, int rows_per_block) {
+  constexpr int RU = 4;
   const int half = dh >> 1;
   const int H = nh * dh;
-  const int pair = blockIdx.x * blockDim.x + threadIdx.x;  // 0 .. nh*half
-  if (pair >= nh * half) return;
-  const int h = pair / half, j = pair % half;
+  const int unit = blockIdx.x * blockDim.x + threadIdx.x;  // 0 .. nh*half/2
+  if (unit >= nh * (half >> 1)) return;
+  const int h = unit / (half >> 1), j = (unit % (half >> 1)) * 2;
   const int64_t r0 = (int64_t)blockIdx.y * rows_per_block, r1 = min(T_, r0 + rows_per_block);
-  float a[6] = {0, 0, 0, 0, 0, 0};
-  for (int64_t t = r0; t < r1; ++t) {
-    const int s = (int)(t % S);
-    const int64_t b = t / S;
-    const float c = cs[(int64_t)s * half + j], sv = sn[(int64_t)s * half + j];
-    const int64_t o = ((b * nh + h) * S + s) * dh;
-    // RoPE^T: dx_j = dy_j c + dy_{j+h} s ; dx_{j+h} = dy_{j+h} c - dy_j s
-    const float g0 = dq[o + j], g1 = dq[o + j + half];
-    const float q0 = (g0 * c + g1 * sv) * qs, q1 = (g1 * c - g0 * sv) * qs;
-    const float e0 = io<T>::ld(dk + o + j), e1 = io<T>::ld(dk + o + j + half);
-    const float k0 = e0 * c + e1 * sv, k1 = e1 * c - e0 * sv;
-    const float v0 = io<T>::ld(dv + o + j), v1 = io<T>::ld(dv + o + j + half);
-    T* row = dqkv + t * 3 * H + h * dh;
-    io<T>::st(row + j, q0);
-    io<T>::st(row + j + half, q1);
-    io<T>::st(row + H + j, k0);
-    io<T>::st(row + H + j + half, k1);
-    io<T>::st(row + 2 * H + j, v0);
-    io<T>::st(row + 2 * H + j + half, v1);
-    a[0] += q0; a[1] += q1; a[2] += k0; a[3] += k1; a[4] += v0; a[5] += v1;
+  float a[12];
+#pragma unroll
+  for (int i = 0; i < 12; ++i) a[i] = 0.f;
+  for (int64_t t0 = r0; t0 < r1; t0 += RU) {
+    float2 g0[RU], g1[RU], e0[RU], e1[RU], v0[RU], v1[RU], c[RU], sv[RU];
+#pragma unroll
+    for (int u = 0; u < RU; ++u) {
+      const int64_t t = min(t0 + u, r1 - 1);  // tail rows re-read the last row; only valid rows are stored
+      const int s = (int)(t % S);
+      const int64_t o = ((t / S * nh + h) * S + s) * dh;
+      g0[u] = *reinterpret_cast<const float2*>(dq + o + j);
+      g1[u] = *reinterpret_cast<const float2*>(dq + o + j + half);
+      e0[u] = pair2<T>::ld(dk + o + j);
+      e1[u] = pair2<T>::ld(dk + o + j + half);
+      v0[u] = pair2<T>::ld(dv + o + j);
+      v1[u] = pair2<T>::ld(dv + o + j + half);
+      c[u] = *reinterpret_cast<const float2*>(cs + (int64_t)s * half + j);
+      sv[u] = *reinterpret_cast<const float2*>(sn + (int64_t)s * half + j);
+    }
+#pragma unroll
+    for (int u = 0; u < RU; ++u) {
+      if (t0 + u >= r1) break;
+      // RoPE^T: dx_j = dy_j c + dy_{j+h} s ; dx_{j+h} = dy_{j+h} c - dy_j s
+      const float qa0 = (g0[u].x * c[u].x + g1[u].x * sv[u].x) * qs, qb0 = (g0[u].y * c[u].y + g1[u].y * sv[u].y) * qs;
+      const float qa1 = (g1[u].x * c[u].x - g0[u].x * sv[u].x) * qs, qb1 = (g1[u].y * c[u].y - g0[u].y * sv[u].y) * qs;
+      const float ka0 = e0[u].x * c[u].x + e1[u].x * sv[u].x, kb0 = e0[u].y * c[u].y + e1[u].y * sv[u].y;
+      const float ka1 = e1[u].x * c[u].x - e0[u].x * sv[u].x, kb1 = e1[u].y * c[u].y - e0[u].y * sv[u].y;
+      T* row = dqkv + (t0 + u) * 3 * H + h * dh;
+      pair2<T>::st(row + j, qa0, qb0);
+      pair2<T>::st(row + j + half, qa1, qb1);
+      pair2<T>::st(row + H + j, ka0, kb0);
+      pair2<T>::st(row + H + j + half, ka1, kb1);
+      pair2<T>::st(row + 2 * H + j, v0[u].x, v0[u].y);
+      pair2<T>::st(row + 2 * H + j + half, v1[u].x, v1[u].y);
+      a[0] += qa0; a[1] += qb0; a[2] += qa1; a[3] += qb1;
+      a[4] += ka0; a[5] += kb0; a[6] += ka1; a[7] += kb1;
+      a[8] += v0[u].x; a[9] += v0[u].y; a[10] += v1[u].x; a[11] += v1[u].y;
+    }
   }
   if (csum) {
     const int c0 = h * dh + j;
     atomicAdd(csum + c0, a[0]);
-    atomicAdd(csum + c0 + half, a[1]);
-    atomicAdd(csum + H + c0, a[2]);
-    atomicAdd(csum + H + c0 + half, a[3]);
-    atomicAdd(csum + 2 * H + c0, a[4]);
-    atomicAdd(csum + 2 * H + c0 + half, a[5]);
+    atomicAdd(csum + c0 + 1, a[1]);
+    atomicAdd(csum + c0 + half, a[2]);
+    atomicAdd(csum + c0 + half + 1, a[3]);
+    atomicAdd(csum + H + c0, a[4]);
+    atomicAdd(csum + H + c0 + 1, a[5]);
+    atomicAdd(csum + H + c0 + half, a[6]);
+    atomicAdd(csum + H + c0 + half + 1, a[7]);
+    atomicAdd(csum + 2 * H + c0, a[8]);
+    atomicAdd(csum + 2 * H + c0 + 1, a[9]);
+    atomicAdd(csum + 2 * H + c0 + half, a[10]);
+    atomicAdd(csum + 2 * H + c0 + half + 1, a[11]);
   }
 }
 
@@ -942,12 +986,12 @@ int esm_qkv_rope_fwd(int dtype, const void* qkv, void* q, void* k, void* v, cons
 int esm_qkv_rope_bwd(int dtype, const float* dq, const void* dk, const void* dv, void* dqkv, float* col_sum,
                      const float* cos_t, const float* sin_t, int B, int Sq, int nh, int dh, float q_scale,
                      esm_stream_t stream) {
-  ESM_CHECK_ARG(dq && dk && dv && dqkv && cos_t && sin_t && dh % 2 == 0, "esm_qkv_rope_bwd: bad args");
+  ESM_CHECK_ARG(dq && dk && dv && dqkv && cos_t && sin_t && dh % 4 == 0, "esm_qkv_rope_bwd: bad args (dh %% 4)");
   const int64_t T_ = (int64_t)B * Sq;
-  const int pairs = nh * dh / 2;
-  const int bx = 128;
-  const int rpb = 128;
-  dim3 grid((pairs + bx - 1) / bx, (unsigned)((T_ + rpb - 1) / rpb));
+  const int units = nh * dh / 4;  // two rotation pairs per thread
+  const int bx = units >= 64 ? 64 : (units + 31) / 32 * 32;  // small blocks: many in flight per SM
+  const int rpb = 32;
+  dim3 grid((units + bx - 1) / bx, (unsigned)((T_ + rpb - 1) / rpb));
   if (dtype == ESM_BF16)
     qkv_rope_bwd_kernel<__nv_bfloat16><<<grid, bx, 0, S(stream)>>>(
         dq, (const __nv_bfloat16*)dk, (const __nv_bfloat16*)dv, (__nv_bfloat16*)dqkv, col_sum, cos_t, sin_t, T_, Sq,
