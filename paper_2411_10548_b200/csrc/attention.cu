@@ -688,30 +688,47 @@ __global__ void __launch_bounds__(64) bwd_dkv_f32_kernel(const float* __restrict
 }
 
 // dq (fp32, token-major [T, H]) -> dqkv[:, 0:H] with RoPE^T and q_scale; col_sum[0:H] += column sums.
-__global__ void dq_finalize_kernel(const float* __restrict__ dq, __nv_bfloat16* __restrict__ dqkv,
-                                   float* __restrict__ csum, const float* __restrict__ cs, const float* __restrict__ sn,
-                                   int64_t T_, int S, int nh, int dh, float qs, int rows_per_block) {
+// RoPE^T + q-scale of the token-major fp32 dQ accumulator -> the q part of dqkv (bf16) + q bias-grad column
+// sums.  Thread = two adjacent rotation pairs (vector accesses), RU tokens in flight per iteration.
+__global__ void __launch_bounds__(64) dq_finalize_kernel(const float* __restrict__ dq, __nv_bfloat16* __restrict__ dqkv,
+                                                         float* __restrict__ csum, const float* __restrict__ cs,
+                                                         const float* __restrict__ sn, int64_t T_, int S, int nh,
+                                                         int dh, float qs, int rows_per_block) {
+  constexpr int RU = 4;
   const int half = dh >> 1;
   const int H = nh * dh;
-  const int pair = blockIdx.x * blockDim.x + threadIdx.x;
-  if (pair >= nh * half) return;
-  const int h = pair / half, j = pair - (pair / half) * half;
+  const int unit = blockIdx.x * blockDim.x + threadIdx.x;
+  if (unit >= nh * (half >> 1)) return;
+  const int h = unit / (half >> 1), j = (unit % (half >> 1)) * 2;
   const int64_t r0 = (int64_t)blockIdx.y * rows_per_block, r1 = min(T_, r0 + rows_per_block);
-  float a0 = 0.f, a1 = 0.f;
-  for (int64_t t = r0; t < r1; ++t) {
-    const int s = (int)(t % S);
-    const float c = __ldg(cs + (int64_t)s * half + j), sv = __ldg(sn + (int64_t)s * half + j);
-    const float g0 = dq[t * H + h * dh + j], g1 = dq[t * H + h * dh + j + half];
-    const float q0 = (g0 * c + g1 * sv) * qs, q1 = (g1 * c - g0 * sv) * qs;
-    __nv_bfloat16* row = dqkv + t * 3 * H + h * dh;
-    row[j] = __float2bfloat16_rn(q0);
-    row[j + half] = __float2bfloat16_rn(q1);
-    a0 += q0;
-    a1 += q1;
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+  for (int64_t t0 = r0; t0 < r1; t0 += RU) {
+    float2 g0[RU], g1[RU], c[RU], sv[RU];
+#pragma unroll
+    for (int u = 0; u < RU; ++u) {
+      const int64_t t = min(t0 + u, r1 - 1);
+      const int s = (int)(t % S);
+      c[u] = __ldg(reinterpret_cast<const float2*>(cs + (int64_t)s * half + j));
+      sv[u] = __ldg(reinterpret_cast<const float2*>(sn + (int64_t)s * half + j));
+      g0[u] = *reinterpret_cast<const float2*>(dq + t * H + h * dh + j);
+      g1[u] = *reinterpret_cast<const float2*>(dq + t * H + h * dh + j + half);
+    }
+#pragma unroll
+    for (int u = 0; u < RU; ++u) {
+      if (t0 + u >= r1) break;
+      const float qa0 = (g0[u].x * c[u].x + g1[u].x * sv[u].x) * qs, qb0 = (g0[u].y * c[u].y + g1[u].y * sv[u].y) * qs;
+      const float qa1 = (g1[u].x * c[u].x - g0[u].x * sv[u].x) * qs, qb1 = (g1[u].y * c[u].y - g0[u].y * sv[u].y) * qs;
+      __nv_bfloat16* row = dqkv + (t0 + u) * 3 * H + h * dh;
+      *reinterpret_cast<__nv_bfloat162*>(row + j) = __floats2bfloat162_rn(qa0, qb0);
+      *reinterpret_cast<__nv_bfloat162*>(row + j + half) = __floats2bfloat162_rn(qa1, qb1);
+      a0 += qa0; a1 += qb0; a2 += qa1; a3 += qb1;
+    }
   }
   if (csum) {
     atomicAdd(csum + h * dh + j, a0);
-    atomicAdd(csum + h * dh + j + half, a1);
+    atomicAdd(csum + h * dh + j + 1, a1);
+    atomicAdd(csum + h * dh + j + half, a2);
+    atomicAdd(csum + h * dh + j + half + 1, a3);
   }
 }
 
@@ -837,9 +854,10 @@ extern "C" int esm_attn_bwd_qkv(const void* q, const void* k, const void* v, con
                              col_sum, cos_t, sin_t);
   if (rc) return rc;
   const int pairs = nh * dh / 2;
-  const int rpb = 64;
-  dim3 grid((pairs + 127) / 128, (unsigned)((T_ + rpb - 1) / rpb));
-  attn::dq_finalize_kernel<<<grid, 128, 0, st>>>(dq_ws, (__nv_bfloat16*)dqkv, col_sum, cos_t, sin_t, T_, S, nh, dh,
+  const int rpb = 32;
+  const int units = pairs / 2;  // two rotation pairs per thread
+  dim3 grid((units + 63) / 64, (unsigned)((T_ + rpb - 1) / rpb));
+  attn::dq_finalize_kernel<<<grid, 64, 0, st>>>(dq_ws, (__nv_bfloat16*)dqkv, col_sum, cos_t, sin_t, T_, S, nh, dh,
                                                  q_scale, rpb);
   ESM_LAUNCH_RET();
 }
