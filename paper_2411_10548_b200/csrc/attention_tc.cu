@@ -26,17 +26,18 @@ constexpr int kThreads = 192;
 constexpr float L2E = 1.4426950408889634f;
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
 
-template <int DH, int BN_>
+template <int DH, int BN_, int NSB_ = 2>
 struct Shape {
   static constexpr int BN = BN_;                                    // keys per tile
+  static constexpr int NSB = NSB_;                                  // S (and P) TMEM buffers
   static constexpr int DP = DH <= 16 ? 16 : (DH <= 32 ? 32 : 64);  // padded head dim (MMA K / N)
   static constexpr int ROWB = DP * 2;                               // smem row bytes = swizzle span
   static constexpr uint32_t LAYOUT = ROWB == 128 ? 2u : (ROWB == 64 ? 4u : 6u);  // SW128 / SW64 / SW32
   static constexpr int Q_BYTES = BM * ROWB;
   static constexpr int KV_BYTES = BN * ROWB;
   static constexpr int STAGES = 3;
-  // TMEM: S0 [0,BN) S1 [BN,2BN) O [2BN, 2BN+DP)
-  static constexpr uint32_t TMEM_COLS = (2 * BN + DP) <= 256 ? 256 : 512;
+  // TMEM: S0 [0,BN) (S1 [BN,2BN)) O [NSB*BN, NSB*BN+DP)
+  static constexpr uint32_t TMEM_COLS = (NSB * BN + DP) <= 128 ? 128 : (NSB * BN + DP) <= 256 ? 256 : 512;
 };
 
 __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
@@ -132,12 +133,12 @@ __device__ __forceinline__ void scan_mask(const int32_t* __restrict__ km, int b,
   __syncthreads();
 }
 
-template <int DH, int BN>
-__global__ void __launch_bounds__(kThreads, 2)
+template <int DH, int BN, int NSB>
+__global__ void __launch_bounds__(kThreads, NSB == 1 ? 3 : 2)
     fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                const __grid_constant__ CUtensorMap tmV, const int32_t* __restrict__ key_mask,
                __nv_bfloat16* __restrict__ O, float* __restrict__ LSE, int S, int nh) {
-  using SH = Shape<DH, BN>;
+  using SH = Shape<DH, BN, NSB>;
   constexpr int DP = SH::DP, ROWB = SH::ROWB, ST = SH::STAGES;
   constexpr int QB = SH::Q_BYTES, TB = SH::KV_BYTES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -184,7 +185,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
-  const uint32_t t_o = tbase + 2 * BN;
+  const uint32_t t_o = tbase + NSB * BN;
 
   const int row0 = bh * S;  // first row of this head in the [B*nh*S, DH] views
   if (warp == 0) {
@@ -215,29 +216,35 @@ __global__ void __launch_bounds__(kThreads, 2)
     const uint64_t kd = make_sdesc(smem_u32(sK), 16, 8 * ROWB, SH::LAYOUT);
     const uint64_t vd = make_sdesc(smem_u32(sV), BN * ROWB, 8 * ROWB, SH::LAYOUT);
     mbar_wait(q_full, 0);
+    auto issue_s = [&](int j) {  // S_j = Q K_j^T into buffer j % NSB
+      const int st = j % ST;
+      mbar_wait(&kv_full[st], (j / ST) & 1);
+      tc_fence_after();
+      const uint64_t so = (uint64_t)((st * TB) >> 4);
+      const uint32_t d = tbase + (j % NSB) * BN;
+#pragma unroll
+      for (int k = 0; k < DP / 16; ++k) mma_ss_w(d, qd + 2 * k, kd + so + 2 * k, idesc_s, k > 0 ? 1u : 0u);
+      mma_commit_w(&s_full[j % NSB]);
+    };
+    auto issue_pv = [&](int i) {  // O += P_i V_i
+      const int st = i % ST;
+      mbar_wait(&p_full[i % NSB], (i / NSB) & 1);
+      tc_fence_after();
+      const uint64_t so = (uint64_t)((st * TB) >> 4);
+      const uint32_t p_tmem = tbase + (i % NSB) * BN;
+#pragma unroll
+      for (int k = 0; k < BN / 16; ++k)  // V tile: BN key rows (K) x DP (N, contiguous); 16 keys per MMA
+        mma_ts_w(t_o, p_tmem + k * 8, vd + so + k * ROWB, idesc_o, (i > 0 || k > 0) ? 1u : 0u);
+      mma_commit_w(&kv_empty[st]);
+      mma_commit_w(o_done);
+    };
     for (int j = 0; j <= ntiles; ++j) {
-      if (j < ntiles) {
-        const int st = j % ST;
-        mbar_wait(&kv_full[st], (j / ST) & 1);
-        tc_fence_after();
-        const uint64_t so = (uint64_t)((st * TB) >> 4);
-        const uint32_t d = tbase + (j & 1) * BN;
-#pragma unroll
-        for (int k = 0; k < DP / 16; ++k) mma_ss_w(d, qd + 2 * k, kd + so + 2 * k, idesc_s, k > 0 ? 1u : 0u);
-        mma_commit_w(&s_full[j & 1]);
-      }
-      if (j >= 1) {
-        const int i = j - 1;  // O += P_i V_i
-        const int st = i % ST;
-        mbar_wait(&p_full[i & 1], (i >> 1) & 1);
-        tc_fence_after();
-        const uint64_t so = (uint64_t)((st * TB) >> 4);
-        const uint32_t p_tmem = tbase + (i & 1) * BN;
-#pragma unroll
-        for (int k = 0; k < BN / 16; ++k)  // V tile: BN key rows (K) x DP (N, contiguous); 16 keys per MMA
-          mma_ts_w(t_o, p_tmem + k * 8, vd + so + k * ROWB, idesc_o, (i > 0 || k > 0) ? 1u : 0u);
-        mma_commit_w(&kv_empty[st]);
-        mma_commit_w(o_done);
+      if (NSB == 1) {  // one S buffer: P_{j-1} (packed over S) must be consumed before S_j overwrites it
+        if (j >= 1) issue_pv(j - 1);
+        if (j < ntiles) issue_s(j);
+      } else {
+        if (j < ntiles) issue_s(j);
+        if (j >= 1) issue_pv(j - 1);
       }
     }
   } else {
@@ -247,9 +254,9 @@ __global__ void __launch_bounds__(kThreads, 2)
     const uint32_t lane_off = (uint32_t)(qq * 32) << 16;
     float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < ntiles; ++j) {
-      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      mbar_wait(&s_full[j % NSB], (j / NSB) & 1);
       tc_fence_after();
-      const uint32_t sbase = tbase + lane_off + (j & 1) * BN;
+      const uint32_t sbase = tbase + lane_off + (j % NSB) * BN;
       float s[BN];
 #pragma unroll
       for (int c = 0; c < BN; c += 32) {
@@ -321,7 +328,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[j & 1]);
+      if (lane == 0) mbar_arrive(&p_full[j % NSB]);
     }
     // ---- epilogue: wait for the last PV, O / l, LSE
     const int qrow = q0 + r;
@@ -847,10 +854,10 @@ static int head_map(CUtensorMap* m, const void* base, int64_t rows) {
   return 0;
 }
 
-template <int DH, int BN>
+template <int DH, int BN, int NSB>
 int launch_fwd(const void* q, const void* k, const void* v, const int32_t* km, void* o, float* lse, int B, int nh,
                int S, cudaStream_t st) {
-  using SH = Shape<DH, BN>;
+  using SH = Shape<DH, BN, NSB>;
   CUtensorMap tq, tk, tv;
   const int64_t rows = (int64_t)B * nh * S;
   int rc;
@@ -860,11 +867,11 @@ int launch_fwd(const void* q, const void* k, const void* v, const int32_t* km, v
   const int smem = SH::Q_BYTES + 2 * SH::STAGES * SH::KV_BYTES + 1024 + 256;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(fwd_kernel<DH, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(fwd_kernel<DH, BN, NSB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
   dim3 grid((S + BM - 1) / BM, B * nh);
-  fwd_kernel<DH, BN><<<grid, kThreads, smem, st>>>(tq, tk, tv, km, (__nv_bfloat16*)o, lse, S, nh);
+  fwd_kernel<DH, BN, NSB><<<grid, kThreads, smem, st>>>(tq, tk, tv, km, (__nv_bfloat16*)o, lse, S, nh);
   ESM_LAUNCH_RET();
 }
 
@@ -948,11 +955,19 @@ int attn_fwd_tc(const void* q, const void* k, const void* v, const int32_t* km, 
                 int S, int dh, cudaStream_t st) {
   ESM_CHECK_ARG(((uintptr_t)q & 15) == 0 && ((uintptr_t)k & 15) == 0 && ((uintptr_t)v & 15) == 0,
                 "attention: q/k/v must be 16B aligned");
+  // NSB = S buffers per CTA: 2 (default, 2 CTAs/SM) or 1 (3 CTAs/SM; measured equal at dh 24, slower at dh 64)
+  static const int nsb = getenv("ESM_ATTN_FWD_NSB") ? atoi(getenv("ESM_ATTN_FWD_NSB")) : 2;
+  if (nsb == 1) switch (dh) {
+    case 16: return fa::launch_fwd<16, 64, 1>(q, k, v, km, o, lse, B, nh, S, st);
+    case 24: return fa::launch_fwd<24, 64, 1>(q, k, v, km, o, lse, B, nh, S, st);
+    case 32: return fa::launch_fwd<32, 64, 1>(q, k, v, km, o, lse, B, nh, S, st);
+    case 64: return fa::launch_fwd<64, 64, 1>(q, k, v, km, o, lse, B, nh, S, st);
+  }
   switch (dh) {
-    case 16: return fa::launch_fwd<16, 64>(q, k, v, km, o, lse, B, nh, S, st);
-    case 24: return fa::launch_fwd<24, 64>(q, k, v, km, o, lse, B, nh, S, st);
-    case 32: return fa::launch_fwd<32, 64>(q, k, v, km, o, lse, B, nh, S, st);
-    case 64: return fa::launch_fwd<64, 64>(q, k, v, km, o, lse, B, nh, S, st);
+    case 16: return fa::launch_fwd<16, 64, 2>(q, k, v, km, o, lse, B, nh, S, st);
+    case 24: return fa::launch_fwd<24, 64, 2>(q, k, v, km, o, lse, B, nh, S, st);
+    case 32: return fa::launch_fwd<32, 64, 2>(q, k, v, km, o, lse, B, nh, S, st);
+    case 64: return fa::launch_fwd<64, 64, 2>(q, k, v, km, o, lse, B, nh, S, st);
     default: set_last_error("attention: head dim %d unsupported", dh); return ESM_ENOTSUP;
   }
 }
