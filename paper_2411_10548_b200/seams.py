@@ -12,6 +12,10 @@ The reference (``densefeed``) owns the layer around the hot path:
 * ``densefeed_bindings.batches(...) -> Iterator[list[int]]`` and ``BoundDataset[i] -> (tokens,
   metadata)`` (pkg/bindings/src/densefeed_bindings/__init__.py:45-95) -- ``collate_indices``
   turns one index batch into the padded int32 ``[B, S]`` ids + attention mask the step consumes.
+* ``densefeed.shards`` (pkg/src/densefeed/shards.py:160-191, 255-276) -- tar-shard streaming.
+  ``shard_tokens`` decodes a ``Sample``'s token payload and ``shard_collate`` is the ``collate`` for
+  ``batch_stage(size, collate=...)``, so ``compose(stream_samples(shards.subset(rank, world)), [...])``
+  yields the padded ``[B, S]`` batches of this rank.
 * ``length_features`` gives the ``[L, L^2]`` cost features (the corpus.py:57-60 pattern) so
   ``fit_cost_model`` can model attention's quadratic memory.
 """
@@ -74,3 +78,18 @@ def make_workload(model, seed: int = 0, pad_to: int = 8, lr: float | None = None
         return float(ws.loss_sum.item())
 
     return workload
+
+
+def shard_tokens(sample, part: str = "tokens") -> np.ndarray:
+    """Token ids of a shard ``Sample`` (``parts[part]`` = little-endian int32 or int64 bytes)."""
+    raw = sample.parts[part]
+    dt = "<i8" if part.endswith("64") else "<i4"
+    return np.frombuffer(raw, dtype=dt).astype(np.int32)
+
+
+def shard_collate(pad_to: int = 8, pad_id: int = 1, part: str = "tokens"):
+    """``collate`` for the reference's ``batch_stage``: a window of Samples -> (ids, attention_mask)
+    int32 [B, S], right padded (pad_id 1 for ESM-2, 0 for Geneformer rank tokens)."""
+    def collate_fn(window):
+        return collate([shard_tokens(x, part) for x in window], pad_to=pad_to, pad_id=pad_id)
+    return collate_fn

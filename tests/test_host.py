@@ -5,6 +5,7 @@ import ctypes
 import os
 import re
 import socket
+import sys
 
 import numpy as np
 import pytest
@@ -209,3 +210,32 @@ def test_geneformer_preset_and_feed_host_logic():
         assert (np.diff(c[ip[r]:ip[r + 1]]) > 0).all()
     ids, am = collate([[5, 6, 7], [9]], pad_to=4, pad_id=0)
     assert ids.tolist() == [[5, 6, 7, 0], [9, 0, 0, 0]] and am.sum() == 4
+
+
+def test_reference_shard_stream_feeds_collate(tmp_path):
+    """the reference's own tar-shard pipeline (write_shards / subset / stream_samples /
+    batch_stage) with our shard_collate yields the padded batches the train step consumes; the per-rank
+    subsets partition the samples (skipped where the reference package is not importable)."""
+    ref = "/root/reference/pkg/src"
+    if not os.path.isdir(ref):
+        pytest.skip("reference package not present")
+    sys.path.insert(0, ref)
+    try:
+        from densefeed import shards as SH
+    except Exception as exc:  # pragma: no cover
+        pytest.skip(f"densefeed not importable: {exc}")
+    finally:
+        sys.path.remove(ref)
+    from paper_2411_10548_b200.seams import shard_collate
+    rng = np.random.default_rng(0)
+    toks = {f"s{i:03d}": np.r_[0, rng.integers(4, 24, int(rng.integers(5, 40))), 2].astype("<i4") for i in range(23)}
+    SH.write_shards((SH.Sample(k, {"tokens": v.tobytes()}) for k, v in toks.items()), tmp_path / "sh", max_per_shard=5)
+    ss = SH.load_shard_set(tmp_path / "sh")
+    seen = 0
+    for rank in range(2):
+        batches = list(SH.compose(SH.stream_samples(ss.subset(rank, 2)), [SH.batch_stage(4, collate=shard_collate(8))]))
+        for ids, am in batches:
+            assert ids.dtype == np.int32 and ids.shape == am.shape and ids.shape[1] % 8 == 0
+            assert (ids[am == 0] == 1).all() and (ids[:, 0] == 0).all()
+            seen += ids.shape[0]
+    assert seen == len(toks)
