@@ -270,13 +270,9 @@ __global__ void __launch_bounds__(kThreads, NSB == 1 ? 3 : 2)
       float mx = -INFINITY;
       if (!nonprefix) {
         const int valid = kv_len - kbase;  // keys [0, valid) of this tile are real
-        if (valid >= BN) {  // 4 independent max chains (a 64-deep fmaxf chain sits on the critical path)
-          float m4[4] = {s[0], s[1], s[2], s[3]};
+        if (valid >= BN) {
 #pragma unroll
-          for (int c = 4; c < BN; c += 4)
-#pragma unroll
-            for (int u = 0; u < 4; ++u) m4[u] = fmaxf(m4[u], s[c + u]);
-          mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+          for (int c = 0; c < BN; ++c) mx = fmaxf(mx, s[c]);
         } else {
 #pragma unroll
           for (int c = 0; c < BN; ++c) {
