@@ -48,8 +48,11 @@ enum {
   ESM_EPI_DGELU = 3,      /* C = acc * gelu'(Z) (Z = aux_in); colsum(C) -> col_sum     backward of HF:411-414 */
   ESM_EPI_F32_ACC = 4,    /* C(fp32) += acc  (weight gradients; split-K safe)                               */
   ESM_EPI_QKV_ROPE = 5,   /* acc + bias -> q*scale, RoPE(q), RoPE(k), v scattered to [B,nh,S,dh]  HF:318-344 (bf16) */
-  ESM_EPI_STORE_LN = 6    /* C = acc = dy of a LayerNorm; col_sum += colsum(dy) (dbeta), col_sum2 += colsum(dy * xhat)
+  ESM_EPI_STORE_LN = 6,   /* C = acc = dy of a LayerNorm; col_sum += colsum(dy) (dbeta), col_sum2 += colsum(dy * xhat)
                              (dgamma) with xhat = (X - row_mean) * row_rstd, X = aux_in (the LN input)  (bf16)   */
+  ESM_EPI_GELU_GRADAUX = 7, /* Z = acc + bias; C = gelu(Z), aux_out = gelu'(Z)  (bf16: the FC1 forward keeps the
+                               derivative its backward needs, computed from the same exp/erfc evaluation)        */
+  ESM_EPI_MUL_AUX = 8       /* C = acc * G (G = aux_in, e.g. gelu'(Z) from GELU_GRADAUX); colsum(C) -> col_sum (bf16) */
 };
 
 typedef struct esm_gemm_args {

@@ -13,6 +13,7 @@ LIB_PATH = os.path.join(_HERE, "libesm2b200.so")
 
 ESM_F32, ESM_BF16 = 0, 1
 EPI_STORE, EPI_GELU, EPI_RESID, EPI_DGELU, EPI_F32_ACC, EPI_QKV_ROPE, EPI_STORE_LN = 0, 1, 2, 3, 4, 5, 6
+EPI_GELU_GRADAUX, EPI_MUL_AUX = 7, 8
 
 EXPORTS = [
     "esm_version", "esm_last_error", "esm_device_sm_count", "esm_tokenize", "esm_mlm_mask", "esm_embed_fwd",

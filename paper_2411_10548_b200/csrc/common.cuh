@@ -127,6 +127,15 @@ __device__ __forceinline__ float gelu_fast(float z) {
   const float ec = erfc_core(x, ex);
   return fmaxf(z, 0.f) - 0.5f * fabsf(z) * ec;
 }
+// GELU(z) and GELU'(z) from one exp / erfc evaluation
+__device__ __forceinline__ float gelu_and_grad_fast(float z, float& grad) {
+  const float x = fabsf(z) * 0.70710678118654752f;
+  float ex;
+  const float ec = erfc_core(x, ex);
+  const float cdf = z >= 0.f ? 1.f - 0.5f * ec : 0.5f * ec;
+  grad = fmaf(z * 0.3989422804014327f, ex, cdf);
+  return z * cdf;
+}
 __device__ __forceinline__ float gelu_grad_fast(float z) {
   const float x = fabsf(z) * 0.70710678118654752f;
   float ex;

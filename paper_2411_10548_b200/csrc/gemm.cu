@@ -59,8 +59,10 @@ struct EpiCfg {
   static constexpr bool QKV = EPI >= 16;  // ESM_EPI_QKV_ROPE specialised per head dim: EPI = 16 + dh
   static constexpr bool F32 = EPI == ESM_EPI_F32_ACC;
   static constexpr int CHUNK = F32 ? 32 * 32 * 4 : 32 * 32 * 2;  // bytes per 32x32 chunk
-  static constexpr int NOUT = EPI == ESM_EPI_GELU ? 2 : 1;        // outputs per chunk (GELU: C and Z)
-  static constexpr bool AUX = EPI == ESM_EPI_RESID || EPI == ESM_EPI_DGELU || EPI == ESM_EPI_STORE_LN;
+  static constexpr bool GELU2 = EPI == ESM_EPI_GELU || EPI == ESM_EPI_GELU_GRADAUX;  // C + aux output
+  static constexpr int NOUT = GELU2 ? 2 : 1;  // outputs per chunk (GELU: C and Z; GELU_GRADAUX: C and GELU'(Z))
+  static constexpr bool AUX = EPI == ESM_EPI_RESID || EPI == ESM_EPI_DGELU || EPI == ESM_EPI_STORE_LN ||
+                              EPI == ESM_EPI_MUL_AUX;
   static constexpr int WARP_BYTES = QKV ? 0 : 2 * NOUT * CHUNK + (AUX ? 2 * CHUNK : 0);
   static constexpr int BYTES = kEpiWarps * WARP_BYTES;
 };
@@ -366,7 +368,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        if constexpr (EPI != ESM_EPI_F32_ACC && EPI != ESM_EPI_DGELU && EPI != ESM_EPI_STORE_LN) {
+        if constexpr (EPI != ESM_EPI_F32_ACC && EPI != ESM_EPI_DGELU && EPI != ESM_EPI_STORE_LN &&
+                      EPI != ESM_EPI_MUL_AUX) {
           if (ep.bias != nullptr) {
             if (col0 + 32 <= ep.N) {
               const float4* b4 = reinterpret_cast<const float4*>(ep.bias + col0);  // 1 KB aligned groups
@@ -416,6 +419,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int e = 0; e < 8; ++e) {
                 if constexpr (EPI == ESM_EPI_RESID) v[8 * k + e] += rv[e];
+                else if constexpr (EPI == ESM_EPI_MUL_AUX) v[8 * k + e] *= rv[e];
                 else v[8 * k + e] *= gelu_grad_fast(rv[e]);
               }
             }
@@ -439,6 +443,13 @@ __global__ void __launch_bounds__(kThreads, 1)
               store_vec(reinterpret_cast<__nv_bfloat16*>(o + E::CHUNK + stage_off<false>(lane, k)), v + 8 * k);
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = gelu_fast(v[j]);
+          } else if constexpr (EPI == ESM_EPI_GELU_GRADAUX) {
+            float gd[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = gelu_and_grad_fast(v[j], gd[j]);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              store_vec(reinterpret_cast<__nv_bfloat16*>(o + E::CHUNK + stage_off<false>(lane, k)), gd + 8 * k);
           }
 #pragma unroll
           for (int k = 0; k < 4; ++k)
@@ -451,12 +462,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_reduce_add_2d(&maps.c, o, col0, row0);
           } else {
             tma_store_2d(&maps.c, o, col0, row0);
-            if constexpr (EPI == ESM_EPI_GELU) tma_store_2d(&maps.z, o + E::CHUNK, col0, row0);
+            if constexpr (E::GELU2) tma_store_2d(&maps.z, o + E::CHUNK, col0, row0);
           }
           bulk_commit();
         }
         ob ^= 1;
-        if constexpr (EPI == ESM_EPI_DGELU) {
+        if constexpr (EPI == ESM_EPI_DGELU || EPI == ESM_EPI_MUL_AUX) {
           if (ep.col_sum != nullptr) {  // rows >= M are exactly 0 (TMA zero-filled A)
             const float s = warp_transpose_sum32(v, lane);
             if (col0 + lane < ep.N) red_add_f32(ep.col_sum + col0 + lane, s);
@@ -559,9 +570,9 @@ static int launch_cg(const esm_gemm_args& a, cudaStream_t st) {
     rc = make_map(&maps.c, a.C, a.N, a.M, a.ldc, 32, 32, true, CU_TENSOR_MAP_SWIZZLE_128B);
   } else {
     rc = make_map(&maps.c, a.C, a.N, a.M, a.ldc, 32, 32, false, CU_TENSOR_MAP_SWIZZLE_64B);
-    if (!rc && EPI == ESM_EPI_GELU)
+    if (!rc && (EPI == ESM_EPI_GELU || EPI == ESM_EPI_GELU_GRADAUX))
       rc = make_map(&maps.z, a.aux_out, a.N, a.M, a.ld_aux_out, 32, 32, false, CU_TENSOR_MAP_SWIZZLE_64B);
-    if (!rc && (EPI == ESM_EPI_RESID || EPI == ESM_EPI_DGELU || EPI == ESM_EPI_STORE_LN))
+    if (!rc && (EPI == ESM_EPI_RESID || EPI == ESM_EPI_DGELU || EPI == ESM_EPI_STORE_LN || EPI == ESM_EPI_MUL_AUX))
       rc = make_map(&maps.r, a.aux_in, a.N, a.M, a.ld_aux_in, 32, 32, false, CU_TENSOR_MAP_SWIZZLE_64B);
   }
   if (rc) return rc;
@@ -718,6 +729,7 @@ int gemm_bf16(const esm_gemm_args& a, cudaStream_t st) {
     switch (a.epilogue) {
       case ESM_EPI_STORE: return dispatch_bn<false, false, ESM_EPI_STORE>(a, bn, st);
       case ESM_EPI_GELU: return dispatch_bn<false, false, ESM_EPI_GELU>(a, bn, st);
+      case ESM_EPI_GELU_GRADAUX: return dispatch_bn<false, false, ESM_EPI_GELU_GRADAUX>(a, bn, st);
       case ESM_EPI_RESID: return dispatch_bn<false, false, ESM_EPI_RESID>(a, bn, st);
       default: break;
     }
@@ -726,6 +738,7 @@ int gemm_bf16(const esm_gemm_args& a, cudaStream_t st) {
     switch (a.epilogue) {
       case ESM_EPI_STORE: return dispatch_bn<false, true, ESM_EPI_STORE>(a, bn, st);
       case ESM_EPI_DGELU: return dispatch_bn<false, true, ESM_EPI_DGELU>(a, bn, st);
+      case ESM_EPI_MUL_AUX: return dispatch_bn<false, true, ESM_EPI_MUL_AUX>(a, bn, st);
       case ESM_EPI_STORE_LN:
         ESM_CHECK_ARG(a.aux_in && a.row_mean && a.row_rstd && a.col_sum && a.col_sum2, "gemm: STORE_LN args");
         return dispatch_bn<false, true, ESM_EPI_STORE_LN>(a, bn, st);
@@ -844,7 +857,10 @@ extern "C" int esm_gemm(const esm_gemm_args* args, esm_stream_t stream) {
   ESM_CHECK_ARG(args != nullptr, "esm_gemm: null args");
   const esm_gemm_args& a = *args;
   ESM_CHECK_ARG(a.M > 0 && a.N > 0 && a.K > 0, "esm_gemm: bad shape %d %d %d", a.M, a.N, a.K);
-  ESM_CHECK_ARG(a.epilogue >= 0 && a.epilogue <= ESM_EPI_STORE_LN, "esm_gemm: bad epilogue");
+  ESM_CHECK_ARG(a.epilogue >= 0 && a.epilogue <= ESM_EPI_MUL_AUX, "esm_gemm: bad epilogue");
+  ESM_CHECK_ARG(a.epilogue < ESM_EPI_GELU_GRADAUX || a.dtype == ESM_BF16, "esm_gemm: GELU_GRADAUX / MUL_AUX are bf16-only");
+  ESM_CHECK_ARG(a.epilogue != ESM_EPI_GELU_GRADAUX || a.aux_out, "esm_gemm: GELU_GRADAUX needs aux_out");
+  ESM_CHECK_ARG(a.epilogue != ESM_EPI_MUL_AUX || a.aux_in, "esm_gemm: MUL_AUX needs aux_in");
   ESM_CHECK_ARG(a.epilogue != ESM_EPI_STORE_LN || a.dtype == ESM_BF16, "esm_gemm: STORE_LN is bf16-only");
   ESM_CHECK_ARG(a.epilogue != ESM_EPI_QKV_ROPE || a.dtype == ESM_BF16, "esm_gemm: QKV_ROPE is bf16-only");
   ESM_CHECK_ARG(a.epilogue != ESM_EPI_RESID || a.aux_in, "esm_gemm: RESID needs aux_in");

@@ -34,7 +34,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import (EPI_DGELU, EPI_F32_ACC, EPI_GELU, EPI_QKV_ROPE, EPI_RESID, EPI_STORE, EPI_STORE_LN, ESM_BF16,
+from ._lib import (EPI_DGELU, EPI_F32_ACC, EPI_GELU, EPI_GELU_GRADAUX, EPI_MUL_AUX, EPI_QKV_ROPE, EPI_RESID, EPI_STORE,
+                   EPI_STORE_LN, ESM_BF16,
                    ESM_F32)
 from .config import EsmConfig
 
@@ -359,7 +360,10 @@ class EsmForMaskedLM:
               aux_out=None, ld_aux_out=0, col_sum=None, ln=None):
         t = self.timer
         if t is not None:
-            t.begin("gemm_" + ("wgrad" if epi == EPI_F32_ACC else "dgrad" if bmn else "fwd"))
+            kind = "gemm_" + ("wgrad" if epi == EPI_F32_ACC else "dgrad" if bmn else "fwd")
+            if os.environ.get("ESM_TIMER_DETAIL"):
+                kind += f"_{M}x{N}x{K}_e{epi}"
+            t.begin(kind)
         self.launches += 1
         self._gemm_raw(M, N, K, A, lda, amn, B, ldb, bmn, C, ldc, epi, bias, aux_in, ld_aux_in, aux_out, ld_aux_out,
                        col_sum, ln)
@@ -392,7 +396,7 @@ class EsmForMaskedLM:
         W = self._w(p + "attention.self.qkv.weight", (3 * H, H))
         t = self.timer
         if t is not None:
-            t.begin("gemm_fwd")
+            t.begin("gemm_fwd" + (f"_{T}x{3 * H}x{H}_qkvrope" if os.environ.get("ESM_TIMER_DETAIL") else ""))
         _lib.gemm_call(self._stream(), dtype=self.kdt, M=T, N=3 * H, K=H, A=ly.h1.data_ptr(), lda=H, a_mn_major=0,
                        B=W.data_ptr(), ldb=H, b_mn_major=0, C=None, ldc=0, epilogue=EPI_QKV_ROPE,
                        bias=self._p32(p + "attention.self.qkv.bias").data_ptr(), rope_cos=ws.cos.data_ptr(),
@@ -525,7 +529,7 @@ class EsmForMaskedLM:
                  self._p32(p + "LayerNorm.bias").data_ptr(), ly.h2.data_ptr(), ly.ln2_m.data_ptr(),
                  ly.ln2_r.data_ptr(), T, H, eps, st)
             self.linear_fwd(ly.h2, p + "intermediate.dense.weight", F, H, p + "intermediate.dense.bias", ly.a,
-                            epi=EPI_GELU, aux_out=ly.z)
+                            epi=EPI_GELU_GRADAUX if kdt == ESM_BF16 else EPI_GELU, aux_out=ly.z)
             self.linear_fwd(ly.a, p + "output.dense.weight", H, F, p + "output.dense.bias", ws.x[l + 1],
                             epi=EPI_RESID, aux_in=ly.x1)
         call("esm_layernorm_fwd", kdt, ws.x[L].data_ptr(),
@@ -571,7 +575,9 @@ class EsmForMaskedLM:
             p = f"esm.encoder.layer.{l}."
             ly = ws.layers[l]
             # FFN
-            self.linear_dgrad(dx, p + "output.dense.weight", H, F, ws.dz, epi=EPI_DGELU, aux_in=ly.z,
+            # bf16: ly.z holds GELU'(Z) from the forward epilogue (EPI_GELU_GRADAUX) -> plain multiply
+            self.linear_dgrad(dx, p + "output.dense.weight", H, F, ws.dz,
+                              epi=EPI_MUL_AUX if kdt == ESM_BF16 else EPI_DGELU, aux_in=ly.z,
                               col_sum=self._g32(p + "intermediate.dense.bias"))
             self.linear_wgrad(dx, ly.a, p + "output.dense.weight", H, F)
             fused = self.linear_dgrad(ws.dz, p + "intermediate.dense.weight", F, H, ws.dh,

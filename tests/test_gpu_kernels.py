@@ -10,6 +10,7 @@ import torch
 pytestmark = pytest.mark.gpu
 
 from paper_2411_10548_b200 import _lib  # noqa: E402
+from paper_2411_10548_b200._lib import EPI_GELU_GRADAUX, EPI_MUL_AUX  # noqa: E402
 from paper_2411_10548_b200._lib import (EPI_DGELU, EPI_F32_ACC, EPI_GELU, EPI_QKV_ROPE, EPI_RESID, EPI_STORE,  # noqa: E402
                                         ESM_BF16, ESM_F32)
 
@@ -113,6 +114,33 @@ def test_gemm_wgrad(M, N, K, dt):
     run_gemm(kdt, M, N, K, dY, M, 1, X, N, 1, C, N, EPI_F32_ACC)
     torch.cuda.synchronize()
     assert rel(C - 1.0, ref) < (1e-2 if dt == "bf16" else 1e-5)
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 128, 64), (1000, 1920, 480), (4096, 1920, 480), (2500, 5120, 1280)])
+def test_gemm_gelu_gradaux_and_mul_aux(M, N, K):
+    """bf16 FFN pair: forward GELU_GRADAUX stores GELU(Z) and GELU'(Z); the FC2 dgrad MUL_AUX multiplies by
+    the stored derivative and sums the FC1 bias gradient."""
+    torch.manual_seed(3)
+    X = torch.randn(M, K, device=DEV).bfloat16()
+    W = (torch.randn(N, K, device=DEV) * 0.05).bfloat16()
+    b = torch.randn(N, device=DEV)
+    z = X.float() @ W.float().t() + b
+    C, G = torch.empty(M, N, device=DEV, dtype=torch.bfloat16), torch.empty(M, N, device=DEV, dtype=torch.bfloat16)
+    run_gemm(ESM_BF16, M, N, K, X, K, 0, W, K, 0, C, N, EPI_GELU_GRADAUX, bias=b, aux_out=G)
+    torch.cuda.synchronize()
+    assert rel(C, gelu(z)) < 2e-2 and rel(G, gelu_grad(z)) < 2e-2
+    Kb = 384
+    dY = torch.randn(M, Kb, device=DEV).bfloat16()
+    W2 = (torch.randn(Kb, N, device=DEV) * 0.05).bfloat16()
+    cs = torch.zeros(N, device=DEV)
+    D = torch.empty(M, N, device=DEV, dtype=torch.bfloat16)
+    run_gemm(ESM_BF16, M, N, Kb, dY, Kb, 0, W2, N, 1, D, N, EPI_MUL_AUX, aux_in=G, col_sum=cs)
+    torch.cuda.synchronize()
+    want = (dY.float() @ W2.float()) * G.float()
+    assert rel(D, want) < 2e-2 and rel(cs, want.sum(0)) < 2e-2
+    with pytest.raises(_lib.EsmKernelError):  # bf16-only epilogues
+        run_gemm(ESM_F32, M, N, K, X.float(), K, 0, W.float(), K, 0, C.float(), N, EPI_GELU_GRADAUX, bias=b,
+                 aux_out=G.float())
 
 
 def test_gemm_rejects_bad_args():
