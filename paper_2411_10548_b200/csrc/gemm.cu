@@ -50,21 +50,25 @@ namespace sm100 {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int kEpiWarps = 8;    // two epilogue warps per TMEM lane quarter (interleaved 32-column chunks)
-constexpr int kThreads = 64 + 32 * kEpiWarps;  // warp0 TMA, warp1 MMA (+TMEM alloc), warps 2.. epilogue
+// warp0 TMA, warp1 MMA (+TMEM alloc), warps 2.. epilogue: EW warps per TMEM lane quarter take interleaved
+// 32-column chunks (EpiCfg::EW).
 
 // Epilogue staging per warp: a 32x32 output chunk in swizzled smem, written to HBM by TMA.
 template <int EPI>
 struct EpiCfg {
   static constexpr bool QKV = EPI >= 16;  // ESM_EPI_QKV_ROPE specialised per head dim: EPI = 16 + dh
   static constexpr bool F32 = EPI == ESM_EPI_F32_ACC;
+  static constexpr int EW = 2;  // epilogue warps per TMEM lane quarter (3 measured slower: smem for staging
+                                // costs mainloop stages)
+  static constexpr int WARPS = 4 * EW;
+  static constexpr int THREADS = 64 + 32 * WARPS;
   static constexpr int CHUNK = F32 ? 32 * 32 * 4 : 32 * 32 * 2;  // bytes per 32x32 chunk
   static constexpr bool GELU2 = EPI == ESM_EPI_GELU || EPI == ESM_EPI_GELU_GRADAUX;  // C + aux output
   static constexpr int NOUT = GELU2 ? 2 : 1;  // outputs per chunk (GELU: C and Z; GELU_GRADAUX: C and GELU'(Z))
   static constexpr bool AUX = EPI == ESM_EPI_RESID || EPI == ESM_EPI_DGELU || EPI == ESM_EPI_STORE_LN ||
                               EPI == ESM_EPI_MUL_AUX;
   static constexpr int WARP_BYTES = QKV ? 0 : 2 * NOUT * CHUNK + (AUX ? 2 * CHUNK : 0);
-  static constexpr int BYTES = kEpiWarps * WARP_BYTES;
+  static constexpr int BYTES = WARPS * WARP_BYTES;
 };
 
 template <int BN, int EPI, int CG = 1>
@@ -128,7 +132,7 @@ struct EpiMaps {
 // CG = 2: a CTA pair (cluster of 2) computes a 256 x BN tile with tcgen05.mma.cta_group::2 -- each CTA
 // loads its 128 rows of A and half of B's columns, so per-SM operand traffic drops by a third.
 template <int BN, bool A_MN, bool B_MN, int EPI, int CG>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(EpiCfg<EPI>::THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ EpiMaps maps, TileInfo ti, EpiParams ep) {
   using C = Cfg<BN, EPI, CG>;
@@ -144,8 +148,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty_bar = full_bar + STAGES;
   uint64_t* tfull_bar = empty_bar + STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint64_t* aux_bar = tempty_bar + 2;  // [kEpiWarps][2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + 2 * kEpiWarps);
+  uint64_t* aux_bar = tempty_bar + 2;  // [E::WARPS][2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + 2 * E::WARPS);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -160,9 +164,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull_bar[b], 1);
-      mbar_init(&tempty_bar[b], kEpiWarps * CG);
+      mbar_init(&tempty_bar[b], E::WARPS * CG);
     }
-    for (int i = 0; i < 2 * kEpiWarps; ++i) mbar_init(&aux_bar[i], 1);
+    for (int i = 0; i < 2 * E::WARPS; ++i) mbar_init(&aux_bar[i], 1);
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -300,7 +304,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int t = row0 + lane;
         const int Hd = ep.n_heads * DH;
         const int sq = t % ep.seq_len, bb = t / ep.seq_len;
-        for (int hh = half; hh * DH < ncols; hh += 2) {
+        for (int hh = half; hh * DH < ncols; hh += E::EW) {
           uint32_t u[DH];
 #pragma unroll
           for (int j = 0; j < DH; j += 8)
@@ -353,15 +357,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         continue;
       }
 #pragma unroll 1
-      for (int c = half * 32; c < ncols; c += 64) {
+      for (int c = half * 32; c < ncols; c += 32 * E::EW) {
         const int col0 = nb * BN + c;
         uint32_t r[32];
         tmem_ld32(taddr + c, r);
         if constexpr (E::AUX) {
-          if (lane == 0 && c + 64 < ncols) {  // prefetch the next chunk into the other buffer
+          if (lane == 0 && c + 32 * E::EW < ncols) {  // prefetch the next chunk into the other buffer
             fence_async_smem();
             mbar_expect_tx(&abar[ab ^ 1], E::CHUNK);
-            tma_load_2d(abuf + (ab ^ 1) * E::CHUNK, &maps.r, &abar[ab ^ 1], col0 + 64, row0);
+            tma_load_2d(abuf + (ab ^ 1) * E::CHUNK, &maps.r, &abar[ab ^ 1], col0 + 32 * E::EW, row0);
           }
         }
         tmem_ld_wait();
@@ -619,11 +623,11 @@ static int launch_cg(const esm_gemm_args& a, cudaStream_t st) {
   const int total = tiles * splits;
   const int units = total < sms ? total : sms;
   if constexpr (CG == 1) {
-    kern<<<units, kThreads, C::SMEM, st>>>(tA, tB, maps, ti, ep);
+    kern<<<units, EpiCfg<EPI>::THREADS, C::SMEM, st>>>(tA, tB, maps, ti, ep);
   } else {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(units * CG);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(EpiCfg<EPI>::THREADS);
     cfg.dynamicSmemBytes = C::SMEM;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
