@@ -594,7 +594,7 @@ __global__ void __launch_bounds__(256) xent_kernel(const T* __restrict__ n, cons
       if (h < H) load_vec(n + r * H + h, x[i]);
     }
     float logit[V_MAX];
-#pragma unroll
+#pragma unroll 8  // full unrolling hoists all V_MAX x MAXV E-row loads into registers (255 regs, 1 block/SM)
     for (int v = 0; v < V_MAX; ++v) {
       float p = 0.f;
       if (v < V) {
@@ -648,7 +648,7 @@ __global__ void __launch_bounds__(256) xent_kernel(const T* __restrict__ n, cons
       const int h = (i * 32 + lane) * VEC;
       if (h < H) {
         float o[VEC] = {};
-#pragma unroll
+#pragma unroll 8
         for (int v = 0; v < V_MAX; ++v) {
           if (v < V) {
             float e[VEC];
@@ -666,6 +666,114 @@ __global__ void __launch_bounds__(256) xent_kernel(const T* __restrict__ n, cons
   __syncthreads();
   if (threadIdx.x == 0 && s_loss != 0.f) atomicAdd(loss_sum, s_loss);
   for (int i = threadIdx.x; i < V && i < V_MAX; i += blockDim.x)
+    if (s_dbias[i] != 0.f) atomicAdd(dbias + i, s_dbias[i]);
+}
+
+// Small-vocabulary decoder + masked CE (ESM V = 33), one warp per labelled row.  The tied decoder E is
+// staged in shared memory with an odd 32-bit row pitch (conflict-free column access) and the row n[r] in a
+// per-warp buffer: lane v computes logit v over H (lanes 32..V-1 cooperatively), the softmax runs across
+// lanes, and dn = dlogits . E is computed with lanes over H.  Unlabelled rows only get dn = 0.
+template <typename T>
+__global__ void __launch_bounds__(256) xent_small_kernel(const T* __restrict__ n, const T* __restrict__ E,
+                                                         const float* __restrict__ bias,
+                                                         const int32_t* __restrict__ labels,
+                                                         const float* __restrict__ inv_denom,
+                                                         float* __restrict__ loss_sum, float* __restrict__ dlogits,
+                                                         T* __restrict__ dn, float* __restrict__ dbias, int64_t rows,
+                                                         int H, int V) {
+  constexpr int VEC = vec16<T>::N;
+  constexpr int PAD = sizeof(T) == 2 ? 2 : 1;  // odd number of 32-bit words per staged row
+  const int HP = H + PAD;
+  extern __shared__ __align__(16) uint8_t xsm[];
+  T* Es = reinterpret_cast<T*>(xsm);                                        // [V][HP]
+  float* dlw = reinterpret_cast<float*>(xsm + (((size_t)V * HP * sizeof(T) + 15) & ~(size_t)15));  // [8][64]
+  T* nrow = reinterpret_cast<T*>(dlw + 8 * 64);                             // [8][H]
+  __shared__ float s_dbias[64];
+  __shared__ float s_loss;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) s_dbias[i] = 0.f;
+  if (threadIdx.x == 0) s_loss = 0.f;
+  for (int i = threadIdx.x; i < V * H; i += blockDim.x) Es[(i / H) * HP + (i % H)] = E[i];
+  __syncthreads();
+  float* dl = dlw + w * 64;
+  T* nr = nrow + (size_t)w * H;
+  const float inv = *inv_denom;
+  float my_loss = 0.f;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + w; r < rows; r += nwarps) {
+    const int lab = labels[r];
+    if (lab < 0) {
+      float z[VEC] = {};
+      for (int h = lane * VEC; h < H; h += 32 * VEC) store_vec(dn + r * H + h, z);
+      continue;
+    }
+    for (int h = lane * VEC; h < H; h += 32 * VEC)
+      *reinterpret_cast<uint4*>(nr + h) = *reinterpret_cast<const uint4*>(n + r * H + h);
+    __syncwarp();
+    // logits: lane v < min(V, 32) over all of H
+    float lg = -INFINITY;
+    if (lane < V) {
+      float a0 = 0.f, a1 = 0.f;
+      const T* er = Es + lane * HP;
+#pragma unroll 8
+      for (int h = 0; h < H; h += 2) {
+        a0 = fmaf(io<T>::ld(nr + h), io<T>::ld(er + h), a0);
+        a1 = fmaf(io<T>::ld(nr + h + 1), io<T>::ld(er + h + 1), a1);
+      }
+      lg = a0 + a1 + bias[lane];
+    }
+    // v in [32, V): cooperative dot products (all lanes get the value)
+    const int nx = V > 32 ? V - 32 : 0;
+#pragma unroll 1
+    for (int x = 0; x < nx; ++x) {
+      const T* er = Es + (32 + x) * HP;
+      float a = 0.f;
+      for (int h = lane; h < H; h += 32) a = fmaf(io<T>::ld(nr + h), io<T>::ld(er + h), a);
+      dl[32 + x] = warp_sum(a) + bias[32 + x];  // stash the logit
+    }
+    __syncwarp();
+    float mx = warp_max(lg);
+    for (int x = 0; x < nx; ++x) mx = fmaxf(mx, dl[32 + x]);
+    float se = warp_sum(lane < V ? __expf(lg - mx) : 0.f);
+    for (int x = 0; x < nx; ++x) se += __expf(dl[32 + x] - mx);
+    const float lse = mx + __logf(se);
+    const float tgt = lab < 32 ? __shfl_sync(0xffffffffu, lg, lab) : dl[lab];
+    if (lane == 0) my_loss += (lse - tgt) * inv;
+    // dlogits
+    if (lane < V) {
+      const float d = (__expf(lg - lse) - (lane == lab ? 1.f : 0.f)) * inv;
+      dl[lane] = d;
+      dlogits[r * V + lane] = d;
+      atomicAdd(&s_dbias[lane], d);
+    }
+    __syncwarp();
+    for (int x = lane; x < nx; x += 32) {
+      const int v = 32 + x;
+      const float d = (__expf(dl[v] - lse) - (v == lab ? 1.f : 0.f)) * inv;
+      dl[v] = d;
+      dlogits[r * V + v] = d;
+      atomicAdd(&s_dbias[v], d);
+    }
+    __syncwarp();
+    // dn = dlogits . E, lanes over H (pairs of columns)
+    for (int h = 2 * lane; h < H; h += 64) {
+      float o0 = 0.f, o1 = 0.f;
+#pragma unroll 4
+      for (int v = 0; v < V; ++v) {
+        const float d = dl[v];
+        o0 = fmaf(d, io<T>::ld(Es + v * HP + h), o0);
+        o1 = fmaf(d, io<T>::ld(Es + v * HP + h + 1), o1);
+      }
+      io<T>::st(dn + r * H + h, o0);
+      io<T>::st(dn + r * H + h + 1, o1);
+    }
+    __syncwarp();
+  }
+  my_loss = warp_sum(my_loss);
+  if (lane == 0 && my_loss != 0.f) atomicAdd(&s_loss, my_loss);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_loss != 0.f) atomicAdd(loss_sum, s_loss);
+  for (int i = threadIdx.x; i < V; i += blockDim.x)
     if (s_dbias[i] != 0.f) atomicAdd(dbias + i, s_dbias[i]);
 }
 
@@ -1011,6 +1119,29 @@ int esm_lmhead_xent(int dtype, const void* n, const void* E, const float* bias, 
   const int grid = grid_for((int64_t)T_ * 32, 256, 148 * 8);
   const int rpb = 512;
   dim3 g2((H + 31) / 32, (T_ + rpb - 1) / rpb);
+  {  // preferred: E staged in shared memory (lanes over the vocabulary)
+    const size_t esz = dtype == ESM_BF16 ? 2 : 4;
+    const size_t pad = dtype == ESM_BF16 ? 2 : 1;
+    const size_t smem = (((size_t)V * (H + pad) * esz + 15) & ~(size_t)15) + 8 * 64 * 4 + 8 * (size_t)H * esz;
+    if (smem <= 200 * 1024 && H % 8 == 0) {
+      const int g = grid_for((int64_t)T_ * 32, 256, 148 * 4);
+      if (dtype == ESM_BF16) {
+        cudaFuncSetAttribute(xent_small_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        xent_small_kernel<__nv_bfloat16><<<g, 256, smem, S(stream)>>>(
+            (const __nv_bfloat16*)n, (const __nv_bfloat16*)E, bias, labels, inv_denom, loss_sum, dlogits_ws,
+            (__nv_bfloat16*)dn, dbias, T_, H, V);
+        xent_dE_kernel<__nv_bfloat16, 40><<<g2, 256, 0, S(stream)>>>((const __nv_bfloat16*)n, labels, dlogits_ws, dE,
+                                                                    T_, H, V, rpb);
+      } else {
+        cudaFuncSetAttribute(xent_small_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        xent_small_kernel<float><<<g, 256, smem, S(stream)>>>((const float*)n, (const float*)E, bias, labels, inv_denom,
+                                                             loss_sum, dlogits_ws, (float*)dn, dbias, T_, H, V);
+        xent_dE_kernel<float, 40><<<g2, 256, 0, S(stream)>>>((const float*)n, labels, dlogits_ws, dE, T_, H, V, rpb);
+      }
+      ESM_LAUNCH_RET();
+    }
+  }
+  if (V > 40) { esm::set_last_error("xent: V > 40 unsupported for this H"); return ESM_ENOTSUP; }
   if (dtype == ESM_BF16) {
     ESM_CHECK_ARG(H % 8 == 0, "xent: H %% 8");
     const int mv = (H + 255) / 256;

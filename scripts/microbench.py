@@ -134,6 +134,26 @@ def ln():
               f"bwd {tb * 1e3:.1f} us ({bb / tb / 1e6:.0f} GB/s)", flush=True)
 
 
+def xent():
+    """ESM LM head (V = 33): fused decoder + masked CE + dlogits + dn over labelled rows, and dE."""
+    T, H, V = 32768, 480, 33
+    n = torch.randn(T, H, device="cuda").bfloat16()
+    E = (torch.randn(V, H, device="cuda") * 0.02).bfloat16()
+    bias = torch.zeros(V, device="cuda")
+    lab = torch.where(torch.rand(T, device="cuda") < 0.15, torch.randint(4, 24, (T,), device="cuda"),
+                      torch.full((T,), -100, device="cuda")).int()
+    inv = torch.tensor([1.0 / max(1, int((lab >= 0).sum()))], device="cuda")
+    loss = torch.zeros(1, device="cuda")
+    dlog = torch.empty(T, V, device="cuda")
+    dn = torch.empty(T, H, device="cuda", dtype=torch.bfloat16)
+    dE, db = torch.zeros(V, H, device="cuda"), torch.zeros(V, device="cuda")
+    f = lambda: _lib.call("esm_lmhead_xent", ESM_BF16, n.data_ptr(), E.data_ptr(), bias.data_ptr(), lab.data_ptr(),  # noqa
+                          inv.data_ptr(), loss.data_ptr(), dlog.data_ptr(), dn.data_ptr(), dE.data_ptr(), db.data_ptr(),
+                          T, H, V, cur())
+    t = timeit(f, iters=20)
+    print(f"lmhead_xent T={T} H={H} V={V}: {t * 1e3:.1f} us", flush=True)
+
+
 def rank():
     """Geneformer tokeniser: device esm_rank_encode rows/s vs the CPU oracle restatement (single thread,
     the reference's algorithm: SURVEY.md §8a1' quotes 3.7k rows/s for the reference itself)."""
@@ -163,4 +183,4 @@ def rank():
 
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "attn"
-    {"attn": attn, "gemm": gemm, "rank": rank, "ln": ln}[what]()
+    {"attn": attn, "gemm": gemm, "rank": rank, "ln": ln, "xent": xent}[what]()
