@@ -415,7 +415,7 @@ __device__ __forceinline__ void bulk_wait_all0() { asm volatile("cp.async.bulk.w
 
 // trace slots: role r (0 = MMA, 1 = softmax warp 2, 2 = softmax warp 6), block i (< 64), event e (< 8)
 __device__ __forceinline__ void trace_ev(unsigned long long* tr, int role, int i, int e) {
-  if (tr != nullptr && blockIdx.x == 3 && blockIdx.y == 5 && i < 64) {
+  if (tr != nullptr && blockIdx.x == 3 && i < 64) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
     tr[(role * 64 + i) * 8 + e] = t;
@@ -429,7 +429,7 @@ struct BwdShape {
   static constexpr uint32_t LAYOUT = Shape<DH, 64>::LAYOUT;
   static constexpr int QB = 64 * ROWB, KB = 128 * ROWB;
   static constexpr int NBUF = DP <= 32 ? 3 : 2;  // {S^T, dP^T} TMEM buffers (128 columns each)
-  static constexpr int QST = DH == 64 ? 5 : 6;   // Q / dO / LSE / Delta stages (>= NBUF + 1)
+  static constexpr int QST = DH == 64 ? 3 : 6;   // Q / dO / LSE / Delta stages (>= NBUF + 1)
   static constexpr int DS_BUF = 2 * 128 * 128;  // one pair: [2 query chunks of 64][128 key rows][128 B]
   // dQ drain: fp32 boxes of BOXC columns x 32 rows, swizzled (128B or 64B rows), staged per drain warp for
   // TMA reduce-add.  DH = 24 drains its zero-padded 32-column tile: the 8 extra columns either fall outside
@@ -438,32 +438,38 @@ struct BwdShape {
   static constexpr int NBOX = DP / BOXC;
   static constexpr int BOX_BYTES = 32 * BOXC * 4;
   static constexpr int DQ_STAGE = 4 * NBOX * BOX_BYTES;
-  static constexpr int SMEM = 2 * DS_BUF + 2 * KB + 2 * QST * QB + 2 * QST * 64 * 4 + DQ_STAGE + 1024 + 256;
+  static constexpr int SMEM = 2 * DS_BUF + 4 * KB + 2 * QST * QB + 2 * QST * 64 * 4 + DQ_STAGE + 1024 + 512;
 };
 
 // TMEM: {S^T, dP^T} x NBUF buffers (64 columns each) at [0, 128*NBUF); dV, dK, 2 x dQ (DP columns each).
+// Persistent: CTA c processes key-block tiles c, c + gridDim.x, ... (tile = (b, h, 128-key block), key block
+// fastest).  All barrier phases follow global block / pair counters (every tile has nqe blocks); K / V are
+// double-buffered so the next tile's loads and first S^T / dP^T MMAs overlap this tile's tail, and the
+// dK / dV epilogue runs on the dQ-drain warps, which release the accumulators (dkv_free) for the next tile.
 template <int DH>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
                const __grid_constant__ CUtensorMap tmdQ, const int32_t* __restrict__ key_mask,
                const float* __restrict__ LSE2, const float* __restrict__ Delta, float* __restrict__ dQ,
-               __nv_bfloat16* __restrict__ dK, __nv_bfloat16* __restrict__ dV, int S, int nh, const FusedOut fo) {
+               __nv_bfloat16* __restrict__ dK, __nv_bfloat16* __restrict__ dV, int S, int nh, int nbh,
+               const FusedOut fo) {
   using BS = BwdShape<DH>;
   constexpr int DP = BS::DP, ROWB = BS::ROWB, QB = BS::QB, KB = BS::KB, QST = BS::QST, NBUF = BS::NBUF;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps shared provenance
   uint8_t* sdS = smem;               // [2][DS_BUF]
-  uint8_t* sK = sdS + 2 * BS::DS_BUF;
-  uint8_t* sV = sK + KB;
-  uint8_t* sQ = sV + KB;             // [QST][QB]
+  uint8_t* sK = sdS + 2 * BS::DS_BUF;  // [2][KB]
+  uint8_t* sV = sK + 2 * KB;           // [2][KB]
+  uint8_t* sQ = sV + 2 * KB;         // [QST][QB]
   uint8_t* sdO = sQ + QST * QB;      // [QST][QB]
   uint8_t* sDQ = sdO + QST * QB;     // [4 warps][NBOX][32 rows][BOXC fp32] (1024-aligned: swizzled)
   float* sL = reinterpret_cast<float*>(sDQ + BS::DQ_STAGE);  // [QST][64]
   float* sD = sL + QST * 64;                                 // [QST][64]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sD + QST * 64);
-  uint64_t* kv_full = bars;
-  uint64_t* qdo_full = bars + 1;           // [QST]
+  uint64_t* kv_full = bars;                // [2]
+  uint64_t* kv_empty = kv_full + 2;        // [2]
+  uint64_t* qdo_full = kv_empty + 2;       // [QST]
   uint64_t* qdo_empty = qdo_full + QST;    // [QST]
   uint64_t* s_full = qdo_empty + QST;      // [NBUF]
   uint64_t* ds_full = s_full + NBUF;       // [NBUF]
@@ -471,39 +477,21 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* dq_empty = dq_full + 2;        // [2]
   uint64_t* dsm_empty = dq_empty + 2;      // [2]
   uint64_t* dkv_done = dsm_empty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dkv_done + 1);
-  int* s_len = reinterpret_cast<int*>(tmem_slot + 1);
-  int* s_np = s_len + 1;
+  uint64_t* dkv_free = dkv_done + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dkv_free + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int bh = blockIdx.y, b = bh / nh, h = bh % nh;
-  const int k0 = blockIdx.x * 128;
-
-  scan_mask(key_mask, b, S, s_len, s_np);
-  const int kv_len = *s_len;
-  const bool nonprefix = *s_np != 0;
-  if (!nonprefix && k0 >= kv_len) {  // all keys of this block are padding: zero gradients
-    for (int i = threadIdx.x; i < 128 * DH; i += blockDim.x) {
-      const int kk = k0 + i / DH;
-      if (kk < S) {
-        if (fo.dqkv) {
-          __nv_bfloat16* row = fo.dqkv + ((int64_t)b * S + kk) * 3 * fo.H + h * DH + i % DH;
-          row[fo.H] = __float2bfloat16_rn(0.f);
-          row[2 * fo.H] = __float2bfloat16_rn(0.f);
-        } else {
-          dK[((int64_t)bh * S + kk) * DH + i % DH] = __float2bfloat16_rn(0.f);
-          dV[((int64_t)bh * S + kk) * DH + i % DH] = __float2bfloat16_rn(0.f);
-        }
-      }
-    }
-    return;
-  }
+  const int nkb = (S + 127) / 128;
+  const int ntile = nkb * nbh;
   const int nq = (S + 63) / 64;
   const int nqe = nq + (nq & 1);  // whole pairs (a trailing virtual block holds no queries)
   const int npairs = nqe / 2;
 
   if (threadIdx.x == 0) {
-    mbar_init(kv_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
     for (int i = 0; i < QST; ++i) {
       mbar_init(&qdo_full[i], 1);
       mbar_init(&qdo_empty[i], 1);
@@ -518,6 +506,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_init(&dq_empty[i], 4);
     }
     mbar_init(dkv_done, 1);
+    mbar_init(dkv_free, 4);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -525,8 +514,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
-  const uint32_t tdV = tbase + 128 * NBUF, tdK = tdV + DP, tdQ0 = tdK + DP;  // dQ double buffered: tdQ0 + (p&1)*DP
-  const int row0 = bh * S;
+  const uint32_t tdV = tbase + 128 * NBUF, tdK = tdV + DP, tdQ0 = tdK + DP;  // dQ double buffered
 
   if (warp == 0) {
     // ======================= TMA producer =======================
@@ -535,26 +523,35 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tma_prefetch(&tmK);
       tma_prefetch(&tmV);
       tma_prefetch(&tmdO);
-      mbar_expect_tx(kv_full, 2 * KB);
-      tma_load_2d(sK, &tmK, kv_full, 0, row0 + k0);
-      tma_load_2d(sV, &tmV, kv_full, 0, row0 + k0);
     }
-    for (int i = 0; i < nqe; ++i) {
-      const int st = i % QST, use = i / QST;
-      mbar_wait(&qdo_empty[st], (use & 1) ^ 1);
+    for (int tile = blockIdx.x, it = 0; tile < ntile; tile += gridDim.x, ++it) {
+      const int bh = tile / nkb, k0 = (tile % nkb) * 128, b = bh / nh, h = bh % nh;
+      const int row0 = bh * S;
+      const int kvs = it & 1;
+      mbar_wait(&kv_empty[kvs], ((it >> 1) & 1) ^ 1);
       if (lane == 0) {
-        const int q0 = i * 64;
-        const int nvalid = max(0, min(64, S - q0));
-        const uint32_t vb = (uint32_t)nvalid * 4;
-        mbar_expect_tx(&qdo_full[st], 2 * QB + 2 * vb);
-        tma_load_2d(sQ + st * QB, &tmQ, &qdo_full[st], 0, row0 + q0);
-        tma_load_2d(sdO + st * QB, &tmdO, &qdo_full[st], h * DH, b * S + q0);
-        if (vb) {
-          bulk_load(sL + st * 64, LSE2 + (int64_t)bh * S + q0, vb, &qdo_full[st]);
-          bulk_load(sD + st * 64, Delta + (int64_t)bh * S + q0, vb, &qdo_full[st]);
-        }
+        mbar_expect_tx(&kv_full[kvs], 2 * KB);
+        tma_load_2d(sK + kvs * KB, &tmK, &kv_full[kvs], 0, row0 + k0);
+        tma_load_2d(sV + kvs * KB, &tmV, &kv_full[kvs], 0, row0 + k0);
       }
-      __syncwarp();
+      for (int i = 0; i < nqe; ++i) {
+        const int g = it * nqe + i;
+        const int st = g % QST, use = g / QST;
+        mbar_wait(&qdo_empty[st], (use & 1) ^ 1);
+        if (lane == 0) {
+          const int q0 = i * 64;
+          const int nvalid = max(0, min(64, S - q0));
+          const uint32_t vb = (uint32_t)nvalid * 4;
+          mbar_expect_tx(&qdo_full[st], 2 * QB + 2 * vb);
+          tma_load_2d(sQ + st * QB, &tmQ, &qdo_full[st], 0, row0 + q0);
+          tma_load_2d(sdO + st * QB, &tmdO, &qdo_full[st], h * DH, b * S + q0);
+          if (vb) {
+            bulk_load(sL + st * 64, LSE2 + (int64_t)bh * S + q0, vb, &qdo_full[st]);
+            bulk_load(sD + st * 64, Delta + (int64_t)bh * S + q0, vb, &qdo_full[st]);
+          }
+        }
+        __syncwarp();
+      }
     }
   } else if (warp == 1) {
     // ======================= MMA issuer =======================
@@ -570,96 +567,172 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const uint64_t qd_kv = make_sdesc(smem_u32(sQ), QB, 8 * ROWB, BS::LAYOUT);    // Q  (B of dK, MN-major)
     const uint64_t kd_q = make_sdesc(smem_u32(sK), KB, 8 * ROWB, BS::LAYOUT);     // K  (B of dQ, MN-major)
     const uint64_t dsd = make_sdesc(smem_u32(sdS), 128 * 128, 1024, 2u);          // dS^T (A of dQ, M-major)
-    auto issue_s = [&](int j) {  // S^T(j), dP^T(j) into buffer j % NBUF
-      const int st = j % QST;
-      mbar_wait(&qdo_full[st], (j / QST) & 1);
-      tc_fence_after();
-      const uint64_t so = (uint64_t)((st * QB) >> 4);
-      const uint32_t tS = tbase + (j % NBUF) * 128, tDP = tS + 64;
+    for (int tile = blockIdx.x, it = 0; tile < ntile; tile += gridDim.x, ++it) {
+      unsigned long long* tr = it == 0 ? fo.trace : nullptr;
+      const int kvs = it & 1;
+      const uint64_t ko = (uint64_t)((kvs * KB) >> 4);
+      auto issue_s = [&](int j) {  // S^T(j), dP^T(j) into buffer g % NBUF
+        const int g = it * nqe + j;
+        const int st = g % QST;
+        mbar_wait(&qdo_full[st], (g / QST) & 1);
+        tc_fence_after();
+        const uint64_t so = (uint64_t)((st * QB) >> 4);
+        const uint32_t tS = tbase + (g % NBUF) * 128, tDP = tS + 64;
 #pragma unroll
-      for (int k = 0; k < DP / 16; ++k) {
-        mma_ss_w(tS, kd_s + 2 * k, qd_s + so + 2 * k, idesc_s, k > 0 ? 1u : 0u);
-        mma_ss_w(tDP, vd_s + 2 * k, od_s + so + 2 * k, idesc_s, k > 0 ? 1u : 0u);
-      }
-      mma_commit_w(&s_full[j % NBUF]);
-    };
-    mbar_wait(kv_full, 0);
-    for (int j = 0; j < NBUF && j < nqe; ++j) issue_s(j);
-    for (int i = 0; i < nqe; ++i) {
-      const int st = i % QST, p = i >> 1;
-      if (lane == 0) trace_ev(fo.trace, 0, i, 0);
-      mbar_wait(&ds_full[i % NBUF], (i / NBUF) & 1);
-      if (lane == 0) trace_ev(fo.trace, 0, i, 1);
-      if ((i & 1) && p >= 2) mbar_wait(&dq_empty[p & 1], ((p >> 1) - 1) & 1);
-      tc_fence_after();
-      const uint64_t so = (uint64_t)((st * QB) >> 4);
-      const uint32_t tS = tbase + (i % NBUF) * 128, tDP = tS + 64;
+        for (int k = 0; k < DP / 16; ++k) {
+          mma_ss_w(tS, kd_s + ko + 2 * k, qd_s + so + 2 * k, idesc_s, k > 0 ? 1u : 0u);
+          mma_ss_w(tDP, vd_s + ko + 2 * k, od_s + so + 2 * k, idesc_s, k > 0 ? 1u : 0u);
+        }
+        mma_commit_w(&s_full[g % NBUF]);
+      };
+      mbar_wait(&kv_full[kvs], (it >> 1) & 1);
+      for (int j = 0; j < NBUF && j < nqe; ++j) issue_s(j);
+      for (int i = 0; i < nqe; ++i) {
+        const int g = it * nqe + i, p = i >> 1, gp = it * npairs + p;
+        const int st = g % QST;
+        if (lane == 0) trace_ev(tr, 0, i, 0);
+        mbar_wait(&ds_full[g % NBUF], (g / NBUF) & 1);
+        if (lane == 0) trace_ev(tr, 0, i, 1);
+        if (i == 0 && it > 0) mbar_wait(dkv_free, (it - 1) & 1);  // previous tile's dV / dK have been read
+        if ((i & 1) && gp >= 2) mbar_wait(&dq_empty[gp & 1], ((gp >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint64_t so = (uint64_t)((st * QB) >> 4);
+        const uint32_t tS = tbase + (g % NBUF) * 128, tDP = tS + 64;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {  // 16 queries per step
-        const uint32_t acc = (i > 0 || k > 0) ? 1u : 0u;
-        // packed P^T / dS^T of queries [16k, 16k+16): warp half (k >> 1) wrote them at column 32 (k >> 1) + 8 (k & 1)
-        const uint32_t pc = (uint32_t)((k >> 1) * 32 + (k & 1) * 8);
-        mma_ts_w(tdV, tS + pc, od_kv + so + k * ROWB, idesc_kv, acc);
-        mma_ts_w(tdK, tDP + pc, qd_kv + so + k * ROWB, idesc_kv, acc);
-      }
-      if (i & 1) {
-        const uint64_t dso = (uint64_t)(((p & 1) * BS::DS_BUF) >> 4);
+        for (int k = 0; k < 4; ++k) {  // 16 queries per step
+          const uint32_t acc = (i > 0 || k > 0) ? 1u : 0u;
+          // packed P^T / dS^T of queries [16k, 16k+16): warp half (k >> 1) wrote them at column 32 (k >> 1) + 8 (k & 1)
+          const uint32_t pc = (uint32_t)((k >> 1) * 32 + (k & 1) * 8);
+          mma_ts_w(tdV, tS + pc, od_kv + so + k * ROWB, idesc_kv, acc);
+          mma_ts_w(tdK, tDP + pc, qd_kv + so + k * ROWB, idesc_kv, acc);
+        }
+        if (i & 1) {
+          const uint64_t dso = (uint64_t)(((gp & 1) * BS::DS_BUF) >> 4);
 #pragma unroll
-        for (int k = 0; k < 8; ++k)  // 16 keys per step
-          mma_ss_w(tdQ0 + (p & 1) * DP, dsd + dso + k * 128, kd_q + k * ROWB, idesc_q, k > 0 ? 1u : 0u);
-        mma_commit_w(&dq_full[p & 1]);
-        mma_commit_w(&dsm_empty[p & 1]);
+          for (int k = 0; k < 8; ++k)  // 16 keys per step
+            mma_ss_w(tdQ0 + (gp & 1) * DP, dsd + dso + k * 128, kd_q + ko + k * ROWB, idesc_q, k > 0 ? 1u : 0u);
+          mma_commit_w(&dq_full[gp & 1]);
+          mma_commit_w(&dsm_empty[gp & 1]);
+        }
+        mma_commit_w(&qdo_empty[st]);
+        if (i == nqe - 1) {
+          mma_commit_w(dkv_done);
+          mma_commit_w(&kv_empty[kvs]);
+        }
+        if (lane == 0) trace_ev(tr, 0, i, 2);
+        if (i + NBUF < nqe) issue_s(i + NBUF);  // buffer g % NBUF is free once dV/dK(g) are issued (in-order)
+        if (lane == 0) trace_ev(tr, 0, i, 3);
       }
-      mma_commit_w(&qdo_empty[st]);
-      if (i == nqe - 1) mma_commit_w(dkv_done);
-      if (lane == 0) trace_ev(fo.trace, 0, i, 2);
-      if (i + NBUF < nqe) issue_s(i + NBUF);  // buffer i % NBUF is free once dV/dK(i) are issued (in-order)
-      if (lane == 0) trace_ev(fo.trace, 0, i, 3);
     }
   } else if (warp >= 10) {
-    // ============ dQ drain: 4 warps, one per TMEM lane quarter (thread = query row of the pair) ============
-    // Runs concurrently with the softmax warps: TMEM -> registers -> swizzled smem boxes -> asynchronous TMA
+    // ============ dQ drain + dK / dV epilogue: 4 warps, one per TMEM lane quarter ============
+    // dQ (thread = query row of the pair): TMEM -> registers -> swizzled smem boxes -> asynchronous TMA
     // reduce-add into the fp32 dQ accumulator (no per-element LSU traffic to contend with the softmax).
     const int qq = warp & 3;
     const uint32_t lane_off = (uint32_t)(qq * 32) << 16;
     constexpr int BOXC = BS::BOXC, RB = BOXC * 4;           // fp32 columns / bytes per staged row
     constexpr uint32_t SWM = RB == 128 ? 7u : 3u;            // 128B / 64B swizzle: chunk ^= (addr >> 7) & SWM
     uint8_t* stage = sDQ + qq * (BS::NBOX * BS::BOX_BYTES);
-    for (int pp = 0; pp < npairs; ++pp) {
-      mbar_wait(&dq_full[pp & 1], (pp >> 1) & 1);
-      tc_fence_after();
-      const uint32_t tq = tdQ0 + (pp & 1) * DP + lane_off;
-      if (lane == 0) bulk_wait_read0();  // the previous pair's reduce has finished reading the staging boxes
-      __syncwarp();
+    for (int tile = blockIdx.x, it = 0; tile < ntile; tile += gridDim.x, ++it) {
+      const int bh = tile / nkb, k0 = (tile % nkb) * 128, b = bh / nh, h = bh % nh;
+      for (int p = 0; p < npairs; ++p) {
+        const int gp = it * npairs + p;
+        mbar_wait(&dq_full[gp & 1], (gp >> 1) & 1);
+        tc_fence_after();
+        const uint32_t tq = tdQ0 + (gp & 1) * DP + lane_off;
+        if (lane == 0) bulk_wait_read0();  // the previous pair's reduce has finished reading the staging boxes
+        __syncwarp();
 #pragma unroll
-      for (int x = 0; x < BS::NBOX; ++x) {
-        uint32_t u[BOXC];
+        for (int x = 0; x < BS::NBOX; ++x) {
+          uint32_t u[BOXC];
 #pragma unroll
-        for (int c = 0; c < BOXC; c += 8)
-          tmem_ld8(tq + x * BOXC + c, u[c], u[c + 1], u[c + 2], u[c + 3], u[c + 4], u[c + 5], u[c + 6], u[c + 7]);
-        tmem_ld_wait();
-        if (x == BS::NBOX - 1) {  // whole tile read: release the TMEM buffer to the MMA warp
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&dq_empty[pp & 1]);
+          for (int c = 0; c < BOXC; c += 8)
+            tmem_ld8(tq + x * BOXC + c, u[c], u[c + 1], u[c + 2], u[c + 3], u[c + 4], u[c + 5], u[c + 6], u[c + 7]);
+          tmem_ld_wait();
+          if (x == BS::NBOX - 1) {  // whole tile read: release the TMEM buffer to the MMA warp
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&dq_empty[gp & 1]);
+          }
+#pragma unroll
+          for (int j = 0; j < BOXC / 4; ++j) {
+            const uint32_t off = (uint32_t)(lane * RB + j * 16);
+            *reinterpret_cast<float4*>(stage + x * BS::BOX_BYTES + (off ^ (((off >> 7) & SWM) << 4))) =
+                make_float4(__uint_as_float(u[4 * j]), __uint_as_float(u[4 * j + 1]), __uint_as_float(u[4 * j + 2]),
+                            __uint_as_float(u[4 * j + 3]));
+          }
         }
+        // rows past this sequence carry exact zeros (dS = 0 there), so spilling into the next rows is harmless
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0 && fo.experiment != 2) {
+          const int row = (fo.dqkv ? b * S : bh * S) + p * 128 + qq * 32;
+          const int col = fo.dqkv ? h * DH : 0;
 #pragma unroll
-        for (int j = 0; j < BOXC / 4; ++j) {
-          const uint32_t off = (uint32_t)(lane * RB + j * 16);
-          *reinterpret_cast<float4*>(stage + x * BS::BOX_BYTES + (off ^ (((off >> 7) & SWM) << 4))) =
-              make_float4(__uint_as_float(u[4 * j]), __uint_as_float(u[4 * j + 1]), __uint_as_float(u[4 * j + 2]),
-                          __uint_as_float(u[4 * j + 3]));
+          for (int x = 0; x < BS::NBOX; ++x) tma_reduce_2d(&tmdQ, stage + x * BS::BOX_BYTES, col + x * BOXC, row);
+          bulk_commit_group();
         }
       }
-      // rows past this sequence carry exact zeros (dS = 0 there), so spilling into the next rows is harmless
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0 && fo.experiment != 2) {
-        const int row = (fo.dqkv ? b * S : bh * S) + pp * 128 + qq * 32;
-        const int col = fo.dqkv ? h * DH : 0;
+      // ---- final key rows of this tile: dK, then dV (thread = key row kr of lane quarter qq)
+      mbar_wait(dkv_done, it & 1);
+      tc_fence_after();
+      const int key = k0 + qq * 32 + lane;
+#pragma unroll 1
+      for (int hf = 0; hf < 2; ++hf) {
+        uint32_t u[DP];
+        const uint32_t src = (hf == 0 ? tdK : tdV) + lane_off;
 #pragma unroll
-        for (int x = 0; x < BS::NBOX; ++x) tma_reduce_2d(&tmdQ, stage + x * BS::BOX_BYTES, col + x * BOXC, row);
-        bulk_commit_group();
+        for (int cc = 0; cc < DP; cc += 8)
+          tmem_ld8(src + cc, u[cc], u[cc + 1], u[cc + 2], u[cc + 3], u[cc + 4], u[cc + 5], u[cc + 6], u[cc + 7]);
+        tmem_ld_wait();
+        if (hf == 1) {  // both accumulators read: the MMA warp may start the next tile's dV / dK
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(dkv_free);
+        }
+        if (fo.dqkv) {
+          // fused: RoPE^T on dK, token-major store into dqkv, bias-gradient column sums
+          float* val = reinterpret_cast<float*>(u);
+#pragma unroll
+          for (int cc = 0; cc < DP; ++cc) val[cc] = key < S ? __uint_as_float(u[cc]) : 0.f;
+          if (hf == 0 && key < S) {
+            constexpr int HALF = DH / 2;
+            const float* cs = fo.cos_t + (int64_t)key * HALF;
+            const float* sn = fo.sin_t + (int64_t)key * HALF;
+#pragma unroll
+            for (int j = 0; j < HALF; ++j) {
+              const float c = __ldg(cs + j), sv = __ldg(sn + j);
+              const float g0 = val[j], g1 = val[j + HALF];
+              val[j] = g0 * c + g1 * sv;
+              val[j + HALF] = g1 * c - g0 * sv;
+            }
+          }
+          if (key < S) {
+            __nv_bfloat16* dst = fo.dqkv + ((int64_t)b * S + key) * 3 * fo.H + (1 + hf) * fo.H + h * DH;
+#pragma unroll
+            for (int cc = 0; cc < DH; cc += 8)
+              *reinterpret_cast<uint4*>(dst + cc) =
+                  make_uint4(pack2(val[cc], val[cc + 1]), pack2(val[cc + 2], val[cc + 3]),
+                             pack2(val[cc + 4], val[cc + 5]), pack2(val[cc + 6], val[cc + 7]));
+          }
+#pragma unroll
+          for (int c0 = 0; c0 < DH; c0 += 32) {
+            float t32[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) t32[j] = (c0 + j < DH) ? val[c0 + j] : 0.f;
+            const float cs = warp_transpose_sum32(t32, lane);
+            if (c0 + lane < DH) red_add_f32(fo.col_sum + (1 + hf) * fo.H + h * DH + c0 + lane, cs);
+          }
+        } else if (key < S) {
+          __nv_bfloat16* dst = (hf == 0 ? dK : dV) + ((int64_t)bh * S + key) * DH;
+#pragma unroll
+          for (int cc = 0; cc < DH; cc += 8)
+            *reinterpret_cast<uint4*>(dst + cc) = make_uint4(
+                pack2(__uint_as_float(u[cc]), __uint_as_float(u[cc + 1])),
+                pack2(__uint_as_float(u[cc + 2]), __uint_as_float(u[cc + 3])),
+                pack2(__uint_as_float(u[cc + 4]), __uint_as_float(u[cc + 5])),
+                pack2(__uint_as_float(u[cc + 6]), __uint_as_float(u[cc + 7])));
+        }
       }
     }
     if (lane == 0) bulk_wait_all0();
@@ -668,140 +741,85 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const int qq = warp & 3;
     const int hf = (warp - 2) >> 2;
     const int kr = qq * 32 + lane;
-    const int key = k0 + kr;
-    const bool kvalid = key < S && (nonprefix ? key_mask[(int64_t)b * S + key] != 0 : key < kv_len);
     const uint32_t lane_off = (uint32_t)(qq * 32) << 16;
-
-    for (int i = 0; i < nqe; ++i) {
-      const int st = i % QST, p = i >> 1, ch = i & 1;
-      const int c = hf * 32;
-      const float* lse = sL + st * 64 + c;
-      const float* dl = sD + st * 64 + c;
-      const uint32_t tS = tbase + (i % NBUF) * 128, tDP = tS + 64;
-      const int trole = (warp == 2) ? 1 : (warp == 6 ? 2 : -1);
-      if (lane == 0 && trole > 0) trace_ev(fo.trace, trole, i, 0);
-      mbar_wait(&s_full[i % NBUF], (i / NBUF) & 1);
-      if (lane == 0 && trole > 0) trace_ev(fo.trace, trole, i, 1);
-      tc_fence_after();
-      if (fo.experiment == 1) {  // timing experiment: tensor/TMA pipeline alone
-        if (ch == 0 && p >= 2) mbar_wait(&dsm_empty[p & 1], ((p >> 1) - 1) & 1);
+    const int c = hf * 32;
+    const int trole = (warp == 2) ? 1 : (warp == 6 ? 2 : -1);
+    for (int tile = blockIdx.x, it = 0; tile < ntile; tile += gridDim.x, ++it) {
+      unsigned long long* tr = it == 0 ? fo.trace : nullptr;
+      const int bh = tile / nkb, k0 = (tile % nkb) * 128, b = bh / nh;
+      const int key = k0 + kr;
+      const bool kvalid = key < S && key_mask[(int64_t)b * S + key] != 0;
+      for (int i = 0; i < nqe; ++i) {
+        const int g = it * nqe + i, p = i >> 1, ch = i & 1, gp = it * npairs + p;
+        const int st = g % QST;
+        const float* lse = sL + st * 64 + c;
+        const float* dl = sD + st * 64 + c;
+        const uint32_t tS = tbase + (g % NBUF) * 128, tDP = tS + 64;
+        if (lane == 0 && trole > 0) trace_ev(tr, trole, i, 0);
+        mbar_wait(&s_full[g % NBUF], (g / NBUF) & 1);
+        if (lane == 0 && trole > 0) trace_ev(tr, trole, i, 1);
+        tc_fence_after();
+        uint32_t us[32], ud[32];
+        tmem_ld32(tS + lane_off + c, us);
+        tmem_ld32(tDP + lane_off + c, ud);
+        if (ch == 0 && gp >= 2) mbar_wait(&dsm_empty[gp & 1], ((gp >> 1) - 1) & 1);
+        tmem_ld_wait();
+        if (lane == 0 && trole > 0) trace_ev(tr, trole, i, 2);
+        uint32_t pp[16], dd[16];
+        const int qmax = S - i * 64 - c;
+        if (__all_sync(0xffffffffu, kvalid) && qmax >= 32) {  // full tile: no masking
+#pragma unroll
+          for (int e = 0; e < 32; e += 4) {
+            const float4 l4 = *reinterpret_cast<const float4*>(lse + e);
+            const float4 d4 = *reinterpret_cast<const float4*>(dl + e);
+            const float p0 = ex2(fmaf(__uint_as_float(us[e]), L2E, -l4.x));
+            const float p1 = ex2(fmaf(__uint_as_float(us[e + 1]), L2E, -l4.y));
+            const float p2 = ex2(fmaf(__uint_as_float(us[e + 2]), L2E, -l4.z));
+            const float p3 = exp2_poly(fmaf(__uint_as_float(us[e + 3]), L2E, -l4.w));  // 1 in 4 on the FMA pipe
+            pp[e >> 1] = pack2(p0, p1);
+            pp[(e >> 1) + 1] = pack2(p2, p3);
+            dd[e >> 1] = pack2(p0 * (__uint_as_float(ud[e]) - d4.x), p1 * (__uint_as_float(ud[e + 1]) - d4.y));
+            dd[(e >> 1) + 1] = pack2(p2 * (__uint_as_float(ud[e + 2]) - d4.z), p3 * (__uint_as_float(ud[e + 3]) - d4.w));
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; e += 4) {
+            const float4 l4 = *reinterpret_cast<const float4*>(lse + e);
+            const float4 d4 = *reinterpret_cast<const float4*>(dl + e);
+            const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv4[4] = {d4.x, d4.y, d4.z, d4.w};
+            float pr[4], ds[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const float xe = fmaf(__uint_as_float(us[e + u]), L2E, -lv[u]);
+              const float pe = u == 3 ? exp2_poly(xe) : ex2(xe);
+              pr[u] = (kvalid && e + u < qmax) ? pe : 0.f;
+              ds[u] = pr[u] * (__uint_as_float(ud[e + u]) - dv4[u]);
+            }
+            pp[e >> 1] = pack2(pr[0], pr[1]);
+            pp[(e >> 1) + 1] = pack2(pr[2], pr[3]);
+            dd[e >> 1] = pack2(ds[0], ds[1]);
+            dd[(e >> 1) + 1] = pack2(ds[2], ds[3]);
+          }
+        }
+        // packed P^T / dS^T go into this warp's own 32-column half of the S^T / dP^T buffers (which it has
+        // finished reading), so the two warps of a lane quarter need no barrier
+        if (lane == 0 && trole > 0) trace_ev(tr, trole, i, 3);
+        tmem_st16(tS + lane_off + hf * 32, pp);
+        tmem_st16(tDP + lane_off + hf * 32, dd);
+        uint8_t* rowp = sdS + (gp & 1) * BS::DS_BUF + ch * (128 * 128) + kr * 128;
+#pragma unroll
+        for (int gg = 0; gg < 4; ++gg) {
+          const int c16 = hf * 4 + gg;
+          *reinterpret_cast<uint4*>(rowp + ((c16 ^ (kr & 7)) << 4)) =
+              make_uint4(dd[4 * gg], dd[4 * gg + 1], dd[4 * gg + 2], dd[4 * gg + 3]);
+        }
+        tmem_st_wait();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&ds_full[i % NBUF]);
-        continue;
+        if (lane == 0) mbar_arrive(&ds_full[g % NBUF]);
+        if (lane == 0 && trole > 0) trace_ev(tr, trole, i, 5);
       }
-      uint32_t us[32], ud[32];
-      tmem_ld32(tS + lane_off + c, us);
-      tmem_ld32(tDP + lane_off + c, ud);
-      if (ch == 0 && p >= 2) mbar_wait(&dsm_empty[p & 1], ((p >> 1) - 1) & 1);
-      tmem_ld_wait();
-      if (lane == 0 && trole > 0) trace_ev(fo.trace, trole, i, 2);
-      uint32_t pp[16], dd[16];
-      const int qmax = S - i * 64 - c;
-      if (__all_sync(0xffffffffu, kvalid) && qmax >= 32) {  // full tile: no masking
-#pragma unroll
-        for (int e = 0; e < 32; e += 4) {
-          const float4 l4 = *reinterpret_cast<const float4*>(lse + e);
-          const float4 d4 = *reinterpret_cast<const float4*>(dl + e);
-          const float p0 = ex2(fmaf(__uint_as_float(us[e]), L2E, -l4.x));
-          const float p1 = ex2(fmaf(__uint_as_float(us[e + 1]), L2E, -l4.y));
-          const float p2 = ex2(fmaf(__uint_as_float(us[e + 2]), L2E, -l4.z));
-          const float p3 = exp2_poly(fmaf(__uint_as_float(us[e + 3]), L2E, -l4.w));  // 1 in 4 on the FMA pipe
-          pp[e >> 1] = pack2(p0, p1);
-          pp[(e >> 1) + 1] = pack2(p2, p3);
-          dd[e >> 1] = pack2(p0 * (__uint_as_float(ud[e]) - d4.x), p1 * (__uint_as_float(ud[e + 1]) - d4.y));
-          dd[(e >> 1) + 1] = pack2(p2 * (__uint_as_float(ud[e + 2]) - d4.z), p3 * (__uint_as_float(ud[e + 3]) - d4.w));
-        }
-      } else {
-#pragma unroll
-        for (int e = 0; e < 32; e += 4) {
-          const float4 l4 = *reinterpret_cast<const float4*>(lse + e);
-          const float4 d4 = *reinterpret_cast<const float4*>(dl + e);
-          const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv4[4] = {d4.x, d4.y, d4.z, d4.w};
-          float pr[4], ds[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const float xe = fmaf(__uint_as_float(us[e + u]), L2E, -lv[u]);
-            const float pe = u == 3 ? exp2_poly(xe) : ex2(xe);
-            pr[u] = (kvalid && e + u < qmax) ? pe : 0.f;
-            ds[u] = pr[u] * (__uint_as_float(ud[e + u]) - dv4[u]);
-          }
-          pp[e >> 1] = pack2(pr[0], pr[1]);
-          pp[(e >> 1) + 1] = pack2(pr[2], pr[3]);
-          dd[e >> 1] = pack2(ds[0], ds[1]);
-          dd[(e >> 1) + 1] = pack2(ds[2], ds[3]);
-        }
-      }
-      // packed P^T / dS^T go into this warp's own 32-column half of the S^T / dP^T buffers (which it has
-      // finished reading), so the two warps of a lane quarter need no barrier
-      if (lane == 0 && trole > 0) trace_ev(fo.trace, trole, i, 3);
-      tmem_st16(tS + lane_off + hf * 32, pp);
-      tmem_st16(tDP + lane_off + hf * 32, dd);
-      uint8_t* rowp = sdS + (p & 1) * BS::DS_BUF + ch * (128 * 128) + kr * 128;
-#pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        const int c16 = hf * 4 + g;
-        *reinterpret_cast<uint4*>(rowp + ((c16 ^ (kr & 7)) << 4)) =
-            make_uint4(dd[4 * g], dd[4 * g + 1], dd[4 * g + 2], dd[4 * g + 3]);
-      }
-      tmem_st_wait();
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&ds_full[i % NBUF]);
-      if (lane == 0 && trole > 0) trace_ev(fo.trace, trole, i, 5);
-    }
-    // ---- final rows: dK (hf == 0) or dV (hf == 1)
-    mbar_wait(dkv_done, 0);
-    tc_fence_after();
-    uint32_t u[DP];
-    const uint32_t src = (hf == 0 ? tdK : tdV) + lane_off;
-#pragma unroll
-    for (int cc = 0; cc < DP; cc += 8)
-      tmem_ld8(src + cc, u[cc], u[cc + 1], u[cc + 2], u[cc + 3], u[cc + 4], u[cc + 5], u[cc + 6], u[cc + 7]);
-    tmem_ld_wait();
-    if (fo.dqkv) {
-      // fused: RoPE^T on dK, token-major store into dqkv, bias-gradient column sums
-      float val[DP];
-#pragma unroll
-      for (int cc = 0; cc < DP; ++cc) val[cc] = key < S ? __uint_as_float(u[cc]) : 0.f;
-      if (hf == 0 && key < S) {
-        constexpr int HALF = DH / 2;
-        const float* cs = fo.cos_t + (int64_t)key * HALF;
-        const float* sn = fo.sin_t + (int64_t)key * HALF;
-#pragma unroll
-        for (int j = 0; j < HALF; ++j) {
-          const float c = __ldg(cs + j), sv = __ldg(sn + j);
-          const float g0 = val[j], g1 = val[j + HALF];
-          val[j] = g0 * c + g1 * sv;
-          val[j + HALF] = g1 * c - g0 * sv;
-        }
-      }
-      if (key < S) {
-        __nv_bfloat16* dst = fo.dqkv + ((int64_t)b * S + key) * 3 * fo.H + (1 + hf) * fo.H + h * DH;
-#pragma unroll
-        for (int cc = 0; cc < DH; cc += 8)
-          *reinterpret_cast<uint4*>(dst + cc) =
-              make_uint4(pack2(val[cc], val[cc + 1]), pack2(val[cc + 2], val[cc + 3]), pack2(val[cc + 4], val[cc + 5]),
-                         pack2(val[cc + 6], val[cc + 7]));
-      }
-#pragma unroll
-      for (int c0 = 0; c0 < DH; c0 += 32) {
-        float t32[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) t32[j] = (c0 + j < DH) ? val[c0 + j] : 0.f;
-        const float cs = warp_transpose_sum32(t32, lane);
-        if (c0 + lane < DH) red_add_f32(fo.col_sum + (1 + hf) * fo.H + h * DH + c0 + lane, cs);
-      }
-    } else if (key < S) {
-      __nv_bfloat16* dst = (hf == 0 ? dK : dV) + ((int64_t)bh * S + key) * DH;
-#pragma unroll
-      for (int cc = 0; cc < DH; cc += 8)
-        *reinterpret_cast<uint4*>(dst + cc) = make_uint4(
-            pack2(__uint_as_float(u[cc]), __uint_as_float(u[cc + 1])),
-            pack2(__uint_as_float(u[cc + 2]), __uint_as_float(u[cc + 3])),
-            pack2(__uint_as_float(u[cc + 4]), __uint_as_float(u[cc + 5])),
-            pack2(__uint_as_float(u[cc + 6]), __uint_as_float(u[cc + 7])));
     }
   }
   tc_fence_before();
@@ -922,9 +940,14 @@ int launch_bwd(const void* q, const void* k, const void* v, const void* dout, co
     cudaFuncSetAttribute(bwd_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, BS::SMEM);
     attr = true;
   }
-  dim3 grid((S + 127) / 128, B * nh);
+  const int ntile = ((S + 127) / 128) * B * nh;
+  static const int persist = getenv("ESM_ATTN_BWD_GRID") ? atoi(getenv("ESM_ATTN_BWD_GRID")) : 0;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  // persistent: one CTA per SM loops over key-block tiles (ESM_ATTN_BWD_GRID=n overrides the CTA count)
+  const int grid = persist > 0 ? min(persist, ntile) : min(sms, ntile);
   bwd_kernel<DH><<<grid, kBwdThreads, BS::SMEM, st>>>(tq, tk, tv, tdo, tdq, km, lse2, delta, dq,
-                                                      (__nv_bfloat16*)dk, (__nv_bfloat16*)dv, S, nh, fo);
+                                                      (__nv_bfloat16*)dk, (__nv_bfloat16*)dv, S, nh, B * nh, fo);
   ESM_LAUNCH_RET();
 }
 
