@@ -36,8 +36,8 @@ struct Shape {
   static constexpr int Q_BYTES = BM * ROWB;
   static constexpr int KV_BYTES = BN * ROWB;
   static constexpr int STAGES = 3;
-  // TMEM: S0 [0,BN) (S1 [BN,2BN)) O [NSB*BN, NSB*BN+DP)
-  static constexpr uint32_t TMEM_COLS = (NSB * BN + DP) <= 128 ? 128 : (NSB * BN + DP) <= 256 ? 256 : 512;
+  // TMEM: S0 [0,BN) (S1 [BN,2BN)) O0 / O1 [NSB*BN, NSB*BN + 2*DP) (O double-buffered across items)
+  static constexpr uint32_t TMEM_COLS = (NSB * BN + 2 * DP) <= 128 ? 128 : (NSB * BN + 2 * DP) <= 256 ? 256 : 512;
 };
 
 __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
@@ -133,42 +133,82 @@ __device__ __forceinline__ void scan_mask(const int32_t* __restrict__ km, int b,
   __syncthreads();
 }
 
+// Per batch row of the key mask: number of valid keys and whether they form a prefix (written by
+// mask_info_kernel before each forward launch; read by every item of the persistent forward).
+constexpr int kMaxMaskRows = 16384;
+__device__ int2 g_mask_info[kMaxMaskRows];
+__device__ int g_tile_next;  // dynamic tile counter of the persistent backward (reset by mask_info_kernel)
+
+__global__ void mask_info_kernel(const int32_t* __restrict__ km, int S) {
+  __shared__ int s_len, s_np;
+  const int b = blockIdx.x;
+  if (threadIdx.x == 0) {
+    s_len = 0;
+    s_np = 0;
+  }
+  __syncthreads();
+  int cnt = 0;
+  for (int s = threadIdx.x; s < S; s += blockDim.x) cnt += km ? (km[(int64_t)b * S + s] != 0) : 1;
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  if ((threadIdx.x & 31) == 0) atomicAdd(&s_len, cnt);
+  __syncthreads();
+  const int len = s_len;
+  int bad = 0;
+  if (km)
+    for (int s = threadIdx.x; s < S; s += blockDim.x) bad |= ((km[(int64_t)b * S + s] != 0) != (s < len));
+  bad = __reduce_or_sync(0xffffffffu, bad);
+  if ((threadIdx.x & 31) == 0 && bad) atomicOr(&s_np, 1);
+  __syncthreads();
+  if (threadIdx.x == 0) g_mask_info[b] = make_int2(len, s_np);
+  if (b == 0 && threadIdx.x == 0) g_tile_next = 0;
+}
+
+// backward tile (head, 128-key block) whose keys are all right-padding (prefix mask): skipped by every role
+__device__ __forceinline__ bool tile_skipped(int tile, int nkb, int nh, int S) {
+  const int b = (tile / nkb) / nh, k0 = (tile % nkb) * 128;
+  const int2 mi = g_mask_info[b];
+  return mi.y == 0 && k0 >= mi.x;
+}
+
+// Persistent forward: CTA c processes items (query tile, head) c, c + gridDim.x, ... (query tile fastest).
+// Q and the O accumulator are double-buffered across items (q_empty / o_free handshakes), the K/V ring and
+// the S / P barriers follow a global tile counter, so the next item's loads and first MMAs overlap this
+// item's softmax tail and epilogue.
 template <int DH, int BN, int NSB>
 __global__ void __launch_bounds__(kThreads, NSB == 1 ? 3 : 2)
     fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                const __grid_constant__ CUtensorMap tmV, const int32_t* __restrict__ key_mask,
-               __nv_bfloat16* __restrict__ O, float* __restrict__ LSE, int S, int nh) {
+               __nv_bfloat16* __restrict__ O, float* __restrict__ LSE, int S, int nh, int nbh) {
   using SH = Shape<DH, BN, NSB>;
   constexpr int DP = SH::DP, ROWB = SH::ROWB, ST = SH::STAGES;
   constexpr int QB = SH::Q_BYTES, TB = SH::KV_BYTES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps shared provenance
-  uint8_t* sQ = smem;
-  uint8_t* sK = sQ + QB;
+  uint8_t* sQ = smem;                      // [2][QB]
+  uint8_t* sK = sQ + 2 * QB;
   uint8_t* sV = sK + ST * TB;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sV + ST * TB);
-  uint64_t* q_full = bars;                 // 1
-  uint64_t* kv_full = bars + 1;            // ST
+  uint64_t* q_full = bars;                 // 2
+  uint64_t* q_empty = q_full + 2;          // 2
+  uint64_t* kv_full = q_empty + 2;         // ST
   uint64_t* kv_empty = kv_full + ST;       // ST
   uint64_t* s_full = kv_empty + ST;        // 2
   uint64_t* p_full = s_full + 2;           // 2
   uint64_t* o_done = p_full + 2;           // 1
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 1);
-  int* s_len = reinterpret_cast<int*>(tmem_slot + 1);
-  int* s_np = s_len + 1;
+  uint64_t* o_free = o_done + 1;           // 2
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int bh = blockIdx.y, b = bh / nh, h = bh % nh;
-  const int q0 = blockIdx.x * BM;
   const int H = nh * DH;
-
-  scan_mask(key_mask, b, S, s_len, s_np);
-  const int kv_len = *s_len;
-  const bool nonprefix = *s_np != 0;
-  const int ntiles = nonprefix ? (S + BN - 1) / BN : (kv_len + BN - 1) / BN;
+  const int nqb = (S + BM - 1) / BM;
+  const int nitem = nqb * nbh;
 
   if (threadIdx.x == 0) {
-    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+      mbar_init(&o_free[i], 4);
+    }
     for (int i = 0; i < ST; ++i) {
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
@@ -185,184 +225,205 @@ __global__ void __launch_bounds__(kThreads, NSB == 1 ? 3 : 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
-  const uint32_t t_o = tbase + NSB * BN;
 
-  const int row0 = bh * S;  // first row of this head in the [B*nh*S, DH] views
-  if (warp == 0) {
-    // ======================= TMA producer =======================
-    if (lane == 0) {
-      tma_prefetch(&tmQ);
-      tma_prefetch(&tmK);
-      tma_prefetch(&tmV);
-      mbar_expect_tx(q_full, QB);
-      tma_load_2d(sQ, &tmQ, q_full, 0, row0 + q0);
-    }
-    for (int j = 0; j < ntiles; ++j) {
-      const int st = j % ST;
-      mbar_wait(&kv_empty[st], ((j / ST) & 1) ^ 1);
+  int G0 = 0;  // KV tiles processed by this CTA before the current item (same in every role)
+  for (int item = blockIdx.x, it = 0; item < nitem; item += gridDim.x, ++it) {
+    const int bh = item / nqb, q0 = (item % nqb) * BM, b = bh / nh, h = bh % nh;
+    const int2 mi = g_mask_info[b];
+    const int kv_len = mi.x;
+    const bool nonprefix = mi.y != 0;
+    const int ntiles = nonprefix ? (S + BN - 1) / BN : (kv_len + BN - 1) / BN;
+    const int row0 = bh * S;  // first row of this head in the [B*nh*S, DH] views
+    const int qs = it & 1;
+    const uint32_t t_o = tbase + NSB * BN + qs * DP;  // O accumulator of this item (double-buffered)
+    if (warp == 0) {
+      // ======================= TMA producer =======================
+      if (lane == 0 && it == 0) {
+        tma_prefetch(&tmQ);
+        tma_prefetch(&tmK);
+        tma_prefetch(&tmV);
+      }
+      mbar_wait(&q_empty[qs], ((it >> 1) & 1) ^ 1);
       if (lane == 0) {
-        mbar_expect_tx(&kv_full[st], 2 * TB);
-        tma_load_2d(sK + st * TB, &tmK, &kv_full[st], 0, row0 + j * BN);
-        tma_load_2d(sV + st * TB, &tmV, &kv_full[st], 0, row0 + j * BN);
+        mbar_expect_tx(&q_full[qs], QB);
+        tma_load_2d(sQ + qs * QB, &tmQ, &q_full[qs], 0, row0 + q0);
       }
-      __syncwarp();
-    }
-  } else if (warp == 1) {
-    // ======================= MMA issuer =======================
-    constexpr uint32_t idesc_s = make_idesc_bf16(BM, BN, false, false);  // S = Q Kᵀ, both K-major
-    constexpr uint32_t idesc_o = make_idesc_bf16(BM, DP, false, true);   // O += P V, V N-major
-    // descriptors hoisted; stage offsets are added to the start-address field (bytes >> 4)
-    const uint64_t qd = make_sdesc(smem_u32(sQ), 16, 8 * ROWB, SH::LAYOUT);
-    const uint64_t kd = make_sdesc(smem_u32(sK), 16, 8 * ROWB, SH::LAYOUT);
-    const uint64_t vd = make_sdesc(smem_u32(sV), BN * ROWB, 8 * ROWB, SH::LAYOUT);
-    mbar_wait(q_full, 0);
-    auto issue_s = [&](int j) {  // S_j = Q K_j^T into buffer j % NSB
-      const int st = j % ST;
-      mbar_wait(&kv_full[st], (j / ST) & 1);
-      tc_fence_after();
-      const uint64_t so = (uint64_t)((st * TB) >> 4);
-      const uint32_t d = tbase + (j % NSB) * BN;
-#pragma unroll
-      for (int k = 0; k < DP / 16; ++k) mma_ss_w(d, qd + 2 * k, kd + so + 2 * k, idesc_s, k > 0 ? 1u : 0u);
-      mma_commit_w(&s_full[j % NSB]);
-    };
-    auto issue_pv = [&](int i) {  // O += P_i V_i
-      const int st = i % ST;
-      mbar_wait(&p_full[i % NSB], (i / NSB) & 1);
-      tc_fence_after();
-      const uint64_t so = (uint64_t)((st * TB) >> 4);
-      const uint32_t p_tmem = tbase + (i % NSB) * BN;
-#pragma unroll
-      for (int k = 0; k < BN / 16; ++k)  // V tile: BN key rows (K) x DP (N, contiguous); 16 keys per MMA
-        mma_ts_w(t_o, p_tmem + k * 8, vd + so + k * ROWB, idesc_o, (i > 0 || k > 0) ? 1u : 0u);
-      mma_commit_w(&kv_empty[st]);
-      mma_commit_w(o_done);
-    };
-    for (int j = 0; j <= ntiles; ++j) {
-      if (NSB == 1) {  // one S buffer: P_{j-1} (packed over S) must be consumed before S_j overwrites it
-        if (j >= 1) issue_pv(j - 1);
-        if (j < ntiles) issue_s(j);
-      } else {
-        if (j < ntiles) issue_s(j);
-        if (j >= 1) issue_pv(j - 1);
+      for (int j = 0; j < ntiles; ++j) {
+        const int gj = G0 + j, st = gj % ST;
+        mbar_wait(&kv_empty[st], ((gj / ST) & 1) ^ 1);
+        if (lane == 0) {
+          mbar_expect_tx(&kv_full[st], 2 * TB);
+          tma_load_2d(sK + st * TB, &tmK, &kv_full[st], 0, row0 + j * BN);
+          tma_load_2d(sV + st * TB, &tmV, &kv_full[st], 0, row0 + j * BN);
+        }
+        __syncwarp();
       }
-    }
-  } else {
-    // ======================= softmax warps =======================
-    const int qq = warp & 3;
-    const int r = qq * 32 + lane;  // query row within tile == TMEM lane
-    const uint32_t lane_off = (uint32_t)(qq * 32) << 16;
-    float m_used = -INFINITY, l = 0.f;
-    for (int j = 0; j < ntiles; ++j) {
-      mbar_wait(&s_full[j % NSB], (j / NSB) & 1);
-      tc_fence_after();
-      const uint32_t sbase = tbase + lane_off + (j % NSB) * BN;
-      float s[BN];
+    } else if (warp == 1) {
+      // ======================= MMA issuer =======================
+      constexpr uint32_t idesc_s = make_idesc_bf16(BM, BN, false, false);  // S = Q Kᵀ, both K-major
+      constexpr uint32_t idesc_o = make_idesc_bf16(BM, DP, false, true);   // O += P V, V N-major
+      // descriptors hoisted; stage offsets are added to the start-address field (bytes >> 4)
+      const uint64_t qd = make_sdesc(smem_u32(sQ + qs * QB), 16, 8 * ROWB, SH::LAYOUT);
+      const uint64_t kd = make_sdesc(smem_u32(sK), 16, 8 * ROWB, SH::LAYOUT);
+      const uint64_t vd = make_sdesc(smem_u32(sV), BN * ROWB, 8 * ROWB, SH::LAYOUT);
+      mbar_wait(&q_full[qs], (it >> 1) & 1);
+      auto issue_s = [&](int j) {  // S_j = Q K_j^T into buffer gj % NSB
+        const int gj = G0 + j, st = gj % ST;
+        mbar_wait(&kv_full[st], (gj / ST) & 1);
+        tc_fence_after();
+        const uint64_t so = (uint64_t)((st * TB) >> 4);
+        const uint32_t d = tbase + (gj % NSB) * BN;
 #pragma unroll
-      for (int c = 0; c < BN; c += 32) {
-        uint32_t u[32];
-        tmem_ld32(sbase + c, u);
+        for (int k = 0; k < DP / 16; ++k) mma_ss_w(d, qd + 2 * k, kd + so + 2 * k, idesc_s, k > 0 ? 1u : 0u);
+        mma_commit_w(&s_full[gj % NSB]);
+        if (j == ntiles - 1) mma_commit_w(&q_empty[qs]);  // last use of this Q buffer
+      };
+      auto issue_pv = [&](int i) {  // O += P_i V_i
+        const int gi = G0 + i, st = gi % ST;
+        if (i == 0 && it >= 2) mbar_wait(&o_free[qs], ((it >> 1) - 1) & 1);  // item it-2 read this O buffer
+        mbar_wait(&p_full[gi % NSB], (gi / NSB) & 1);
+        tc_fence_after();
+        const uint64_t so = (uint64_t)((st * TB) >> 4);
+        const uint32_t p_tmem = tbase + (gi % NSB) * BN;
 #pragma unroll
-        for (int e = 0; e < 32; ++e) s[c + e] = __uint_as_float(u[e]);
+        for (int k = 0; k < BN / 16; ++k)  // V tile: BN key rows (K) x DP (N, contiguous); 16 keys per MMA
+          mma_ts_w(t_o, p_tmem + k * 8, vd + so + k * ROWB, idesc_o, (i > 0 || k > 0) ? 1u : 0u);
+        mma_commit_w(&kv_empty[st]);
+        mma_commit_w(o_done);
+      };
+      for (int j = 0; j <= ntiles; ++j) {
+        if (NSB == 1) {  // one S buffer: P_{j-1} (packed over S) must be consumed before S_j overwrites it
+          if (j >= 1) issue_pv(j - 1);
+          if (j < ntiles) issue_s(j);
+        } else {
+          if (j < ntiles) issue_s(j);
+          if (j >= 1) issue_pv(j - 1);
+        }
       }
-      tmem_ld_wait();
-      const int kbase = j * BN;
-      float mx = -INFINITY;
-      if (!nonprefix) {
-        const int valid = kv_len - kbase;  // keys [0, valid) of this tile are real
-        if (valid >= BN) {
+      if (ntiles == 0) mma_commit_w(&q_empty[qs]);
+    } else {
+      // ======================= softmax warps =======================
+      const int qq = warp & 3;
+      const int r = qq * 32 + lane;  // query row within tile == TMEM lane
+      const uint32_t lane_off = (uint32_t)(qq * 32) << 16;
+      float m_used = -INFINITY, l = 0.f;
+      for (int j = 0; j < ntiles; ++j) {
+        const int gj = G0 + j;
+        mbar_wait(&s_full[gj % NSB], (gj / NSB) & 1);
+        tc_fence_after();
+        const uint32_t sbase = tbase + lane_off + (gj % NSB) * BN;
+        float s[BN];
 #pragma unroll
-          for (int c = 0; c < BN; ++c) mx = fmaxf(mx, s[c]);
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t u[32];
+          tmem_ld32(sbase + c, u);
+#pragma unroll
+          for (int e = 0; e < 32; ++e) s[c + e] = __uint_as_float(u[e]);
+        }
+        tmem_ld_wait();
+        const int kbase = j * BN;
+        float mx = -INFINITY;
+        if (!nonprefix) {
+          const int valid = kv_len - kbase;  // keys [0, valid) of this tile are real
+          if (valid >= BN) {
+#pragma unroll
+            for (int c = 0; c < BN; ++c) mx = fmaxf(mx, s[c]);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BN; ++c) {
+              s[c] = c < valid ? s[c] : -INFINITY;
+              mx = fmaxf(mx, s[c]);
+            }
+          }
         } else {
 #pragma unroll
           for (int c = 0; c < BN; ++c) {
-            s[c] = c < valid ? s[c] : -INFINITY;
+            const int kk = kbase + c;
+            const bool ok = kk < S && key_mask[(int64_t)b * S + kk] != 0;
+            s[c] = ok ? s[c] : -INFINITY;
             mx = fmaxf(mx, s[c]);
           }
         }
-      } else {
+        const float mnew = mx * L2E;
+        const bool grow = mnew > m_used + RESCALE_THRESHOLD;
+        if (__any_sync(0xffffffffu, grow)) {  // warp-uniform: tcgen05.ld/st are warp-collective
+          // raise the reference max; rescale running sum and (if any PV issued) O in TMEM
+          const float f = grow ? ex2(m_used - mnew) : 1.0f;  // 0 on the first tile
+          l *= f;
+          if (j > 0) {
+            mbar_wait(o_done, (gj - 1) & 1);
+            tc_fence_after();
 #pragma unroll
-        for (int c = 0; c < BN; ++c) {
-          const int kk = kbase + c;
-          const bool ok = kk < S && key_mask[(int64_t)b * S + kk] != 0;
-          s[c] = ok ? s[c] : -INFINITY;
-          mx = fmaxf(mx, s[c]);
-        }
-      }
-      const float mnew = mx * L2E;
-      const bool grow = mnew > m_used + RESCALE_THRESHOLD;
-      if (__any_sync(0xffffffffu, grow)) {  // warp-uniform: tcgen05.ld/st are warp-collective
-        // raise the reference max; rescale running sum and (if any PV issued) O in TMEM
-        const float f = grow ? ex2(m_used - mnew) : 1.0f;  // 0 on the first tile
-        l *= f;
-        if (j > 0) {
-          mbar_wait(o_done, (j - 1) & 1);
-          tc_fence_after();
+            for (int c = 0; c < DP; c += 16) {
+              uint32_t u[16];
+              tmem_ld16(t_o + lane_off + c, u);
+              tmem_ld_wait();
 #pragma unroll
-          for (int c = 0; c < DP; c += 16) {
-            uint32_t u[16];
-            tmem_ld16(t_o + lane_off + c, u);
-            tmem_ld_wait();
-#pragma unroll
-            for (int e = 0; e < 16; ++e) u[e] = __float_as_uint(__uint_as_float(u[e]) * f);
-            tmem_st16(t_o + lane_off + c, u);
+              for (int e = 0; e < 16; ++e) u[e] = __float_as_uint(__uint_as_float(u[e]) * f);
+              tmem_st16(t_o + lane_off + c, u);
+            }
           }
+          if (grow) m_used = mnew;
         }
-        if (grow) m_used = mnew;
-      }
-      const float moff = m_used == -INFINITY ? 0.f : m_used;
-      float ls = 0.f;
+        const float moff = m_used == -INFINITY ? 0.f : m_used;
+        float ls = 0.f;
 #pragma unroll
-      for (int c = 0; c < BN; c += 64) {
-        uint32_t pk[32];
+        for (int c = 0; c < BN; c += 64) {
+          uint32_t pk[32];
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const float p0 = ex2(fmaf(s[c + 2 * e], L2E, -moff));
-          const float p1 = ex2(fmaf(s[c + 2 * e + 1], L2E, -moff));
-          ls += p0 + p1;
-          pk[e] = pack2(p0, p1);
+          for (int e = 0; e < 32; ++e) {
+            const float p0 = ex2(fmaf(s[c + 2 * e], L2E, -moff));
+            const float p1 = ex2(fmaf(s[c + 2 * e + 1], L2E, -moff));
+            ls += p0 + p1;
+            pk[e] = pack2(p0, p1);
+          }
+          tmem_st32(sbase + c / 2, pk);  // P (bf16x2) over the first 64 columns of this S buffer
         }
-        tmem_st32(sbase + c / 2, pk);  // P (bf16x2) over the first 64 columns of this S buffer
+        l += ls;
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[gj % NSB]);
       }
-      l += ls;
-      tmem_st_wait();
+      // ---- epilogue: wait for the last PV, O / l, LSE; release the O buffer
+      const int qrow = q0 + r;
+      float inv = l > 0.f ? 1.f / l : 0.f;
+      if (ntiles > 0) {
+        mbar_wait(o_done, (G0 + ntiles - 1) & 1);
+        tc_fence_after();
+      }
+      float o[DP];
+#pragma unroll
+      for (int c = 0; c < DP; c += 16) {
+        uint32_t u[16];
+        tmem_ld16(t_o + lane_off + c, u);
+        tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 16; ++e) o[c + e] = ntiles > 0 ? __uint_as_float(u[e]) * inv : 0.f;
+      }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[j % NSB]);
-    }
-    // ---- epilogue: wait for the last PV, O / l, LSE
-    const int qrow = q0 + r;
-    float inv = l > 0.f ? 1.f / l : 0.f;
-    if (ntiles > 0) {
-      mbar_wait(o_done, (ntiles - 1) & 1);
-      tc_fence_after();
-    }
-    float o[DP];
+      if (lane == 0) mbar_arrive(&o_free[qs]);
+      if (qrow < S) {
+        __nv_bfloat16* dst = O + ((int64_t)b * S + qrow) * H + h * DH;
 #pragma unroll
-    for (int c = 0; c < DP; c += 16) {
-      uint32_t u[16];
-      tmem_ld16(t_o + lane_off + c, u);
-      tmem_ld_wait();
-#pragma unroll
-      for (int e = 0; e < 16; ++e) o[c + e] = ntiles > 0 ? __uint_as_float(u[e]) * inv : 0.f;
-    }
-    if (qrow < S) {
-      __nv_bfloat16* dst = O + ((int64_t)b * S + qrow) * H + h * DH;
-#pragma unroll
-      for (int c = 0; c < DH; c += 8) {
-        uint4 w;
-        w.x = pack2(o[c], o[c + 1]);
-        w.y = pack2(o[c + 2], o[c + 3]);
-        w.z = pack2(o[c + 4], o[c + 5]);
-        w.w = pack2(o[c + 6], o[c + 7]);
-        *reinterpret_cast<uint4*>(dst + c) = w;
+        for (int c = 0; c < DH; c += 8) {
+          uint4 w;
+          w.x = pack2(o[c], o[c + 1]);
+          w.y = pack2(o[c + 2], o[c + 3]);
+          w.z = pack2(o[c + 4], o[c + 5]);
+          w.w = pack2(o[c + 6], o[c + 7]);
+          *reinterpret_cast<uint4*>(dst + c) = w;
+        }
+        LSE[(int64_t)bh * S + qrow] = l > 0.f ? (m_used + log2f(l)) / L2E : -INFINITY;
       }
-      LSE[(int64_t)bh * S + qrow] = l > 0.f ? (m_used + log2f(l)) / L2E : -INFINITY;
     }
+    G0 += ntiles;
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
+
     tc_fence_after();
     tmem_dealloc<SH::TMEM_COLS>(tbase);
   }
@@ -478,7 +539,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* dsm_empty = dq_empty + 2;      // [2]
   uint64_t* dkv_done = dsm_empty + 2;
   uint64_t* dkv_free = dkv_done + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dkv_free + 1);
+  uint64_t* tile_full = dkv_free + 1;     // [4] tile-id ring (TMA warp -> MMA / softmax / drain warps)
+  uint64_t* tile_empty = tile_full + 4;   // [4]
+  int* tile_ring = reinterpret_cast<int*>(tile_empty + 4);  // [4]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tile_ring + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nkb = (S + 127) / 128;
@@ -507,6 +571,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
     mbar_init(dkv_done, 1);
     mbar_init(dkv_free, 4);
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&tile_full[i], 1);
+      mbar_init(&tile_empty[i], 1 + 8 + 4);  // MMA warp, 8 softmax warps, 4 drain warps
+    }
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -524,7 +592,36 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tma_prefetch(&tmV);
       tma_prefetch(&tmdO);
     }
-    for (int tile = blockIdx.x, it = 0; tile < ntile; tile += gridDim.x, ++it) {
+    // dynamic tile scheduler: claim tiles from the global counter (first tile = blockIdx.x), zero-fill the
+    // dK / dV rows of fully padded key blocks here, publish real tiles through the ring, -1 terminates
+    auto claim = [&]() {
+      int t = 0;
+      if (lane == 0) t = atomicAdd(&g_tile_next, 1) + gridDim.x;
+      return __shfl_sync(0xffffffffu, t, 0);
+    };
+    int tile = blockIdx.x;
+    for (int it = 0;; ++it) {
+      while (tile < ntile && tile_skipped(tile, nkb, nh, S)) {
+        const int bh = tile / nkb, k0 = (tile % nkb) * 128, b = bh / nh, h = bh % nh;
+        for (int i = lane; i < 128; i += 32) {
+          const int key = k0 + i;
+          if (key >= S) break;
+          for (int hf = 0; hf < 2; ++hf) {
+            __nv_bfloat16* dst = fo.dqkv ? fo.dqkv + ((int64_t)b * S + key) * 3 * fo.H + (1 + hf) * fo.H + h * DH
+                                         : (hf == 0 ? dK : dV) + ((int64_t)bh * S + key) * DH;
+            for (int cc = 0; cc < DH; cc += 8) *reinterpret_cast<uint4*>(dst + cc) = make_uint4(0u, 0u, 0u, 0u);
+          }
+        }
+        tile = claim();
+      }
+      const int slot = it & 3;
+      mbar_wait(&tile_empty[slot], ((it >> 2) & 1) ^ 1);
+      if (lane == 0) {
+        tile_ring[slot] = tile < ntile ? tile : -1;
+        mbar_arrive(&tile_full[slot]);
+      }
+      __syncwarp();
+      if (tile >= ntile) break;
       const int bh = tile / nkb, k0 = (tile % nkb) * 128, b = bh / nh, h = bh % nh;
       const int row0 = bh * S;
       const int kvs = it & 1;
@@ -552,6 +649,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
         __syncwarp();
       }
+      tile = claim();
     }
   } else if (warp == 1) {
     // ======================= MMA issuer =======================
@@ -567,7 +665,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const uint64_t qd_kv = make_sdesc(smem_u32(sQ), QB, 8 * ROWB, BS::LAYOUT);    // Q  (B of dK, MN-major)
     const uint64_t kd_q = make_sdesc(smem_u32(sK), KB, 8 * ROWB, BS::LAYOUT);     // K  (B of dQ, MN-major)
     const uint64_t dsd = make_sdesc(smem_u32(sdS), 128 * 128, 1024, 2u);          // dS^T (A of dQ, M-major)
-    for (int tile = blockIdx.x, it = 0; tile < ntile; tile += gridDim.x, ++it) {
+    for (int it = 0;; ++it) {
+      const int slot = it & 3;
+      mbar_wait(&tile_full[slot], (it >> 2) & 1);
+      const int tile = tile_ring[slot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tile_empty[slot]);
+      if (tile < 0) break;
       unsigned long long* tr = it == 0 ? fo.trace : nullptr;
       const int kvs = it & 1;
       const uint64_t ko = (uint64_t)((kvs * KB) >> 4);
@@ -633,7 +737,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     constexpr int BOXC = BS::BOXC, RB = BOXC * 4;           // fp32 columns / bytes per staged row
     constexpr uint32_t SWM = RB == 128 ? 7u : 3u;            // 128B / 64B swizzle: chunk ^= (addr >> 7) & SWM
     uint8_t* stage = sDQ + qq * (BS::NBOX * BS::BOX_BYTES);
-    for (int tile = blockIdx.x, it = 0; tile < ntile; tile += gridDim.x, ++it) {
+    for (int it = 0;; ++it) {
+      const int slot = it & 3;
+      mbar_wait(&tile_full[slot], (it >> 2) & 1);
+      const int tile = tile_ring[slot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tile_empty[slot]);
+      if (tile < 0) break;
       const int bh = tile / nkb, k0 = (tile % nkb) * 128, b = bh / nh, h = bh % nh;
       for (int p = 0; p < npairs; ++p) {
         const int gp = it * npairs + p;
@@ -744,7 +854,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const uint32_t lane_off = (uint32_t)(qq * 32) << 16;
     const int c = hf * 32;
     const int trole = (warp == 2) ? 1 : (warp == 6 ? 2 : -1);
-    for (int tile = blockIdx.x, it = 0; tile < ntile; tile += gridDim.x, ++it) {
+    for (int it = 0;; ++it) {
+      const int slot = it & 3;
+      mbar_wait(&tile_full[slot], (it >> 2) & 1);
+      const int tile = tile_ring[slot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tile_empty[slot]);
+      if (tile < 0) break;
       unsigned long long* tr = it == 0 ? fo.trace : nullptr;
       const int bh = tile / nkb, k0 = (tile % nkb) * 128, b = bh / nh;
       const int key = k0 + kr;
@@ -882,14 +998,20 @@ int launch_fwd(const void* q, const void* k, const void* v, const int32_t* km, v
   if ((rc = head_map<DH, BM>(&tq, q, rows)) || (rc = head_map<DH, BN>(&tk, k, rows)) ||
       (rc = head_map<DH, BN>(&tv, v, rows)))
     return rc;
-  const int smem = SH::Q_BYTES + 2 * SH::STAGES * SH::KV_BYTES + 1024 + 256;
+  const int smem = 2 * SH::Q_BYTES + 2 * SH::STAGES * SH::KV_BYTES + 1024 + 256;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(fwd_kernel<DH, BN, NSB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  dim3 grid((S + BM - 1) / BM, B * nh);
-  fwd_kernel<DH, BN, NSB><<<grid, kThreads, smem, st>>>(tq, tk, tv, km, (__nv_bfloat16*)o, lse, S, nh);
+  ESM_CHECK_ARG(B <= kMaxMaskRows, "attention: batch %d exceeds %d", B, kMaxMaskRows);
+  mask_info_kernel<<<B, 256, 0, st>>>(km, S);
+  const int nitem = ((S + BM - 1) / BM) * B * nh;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int per_sm = NSB == 1 ? 3 : 2;  // CTAs resident per SM
+  const int grid = min(nitem, per_sm * sms);
+  fwd_kernel<DH, BN, NSB><<<grid, kThreads, smem, st>>>(tq, tk, tv, km, (__nv_bfloat16*)o, lse, S, nh, B * nh);
   ESM_LAUNCH_RET();
 }
 
@@ -940,6 +1062,8 @@ int launch_bwd(const void* q, const void* k, const void* v, const void* dout, co
     cudaFuncSetAttribute(bwd_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, BS::SMEM);
     attr = true;
   }
+  ESM_CHECK_ARG(B <= kMaxMaskRows, "attention: batch %d exceeds %d", B, kMaxMaskRows);
+  mask_info_kernel<<<B, 256, 0, st>>>(km, S);
   const int ntile = ((S + 127) / 128) * B * nh;
   static const int persist = getenv("ESM_ATTN_BWD_GRID") ? atoi(getenv("ESM_ATTN_BWD_GRID")) : 0;
   int sms = 148;
