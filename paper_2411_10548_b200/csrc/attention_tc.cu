@@ -138,6 +138,7 @@ __device__ __forceinline__ void scan_mask(const int32_t* __restrict__ km, int b,
 constexpr int kMaxMaskRows = 16384;
 __device__ int2 g_mask_info[kMaxMaskRows];
 __device__ int g_tile_next;  // dynamic tile counter of the persistent backward (reset by mask_info_kernel)
+__device__ int g_item_next;  // dynamic item counter of the persistent forward (reset by mask_info_kernel)
 
 __global__ void mask_info_kernel(const int32_t* __restrict__ km, int S) {
   __shared__ int s_len, s_np;
@@ -160,7 +161,10 @@ __global__ void mask_info_kernel(const int32_t* __restrict__ km, int S) {
   if ((threadIdx.x & 31) == 0 && bad) atomicOr(&s_np, 1);
   __syncthreads();
   if (threadIdx.x == 0) g_mask_info[b] = make_int2(len, s_np);
-  if (b == 0 && threadIdx.x == 0) g_tile_next = 0;
+  if (b == 0 && threadIdx.x == 0) {
+    g_tile_next = 0;
+    g_item_next = 0;
+  }
 }
 
 // backward tile (head, 128-key block) whose keys are all right-padding (prefix mask): skipped by every role
@@ -196,7 +200,10 @@ __global__ void __launch_bounds__(kThreads, NSB == 1 ? 3 : 2)
   uint64_t* p_full = s_full + 2;           // 2
   uint64_t* o_done = p_full + 2;           // 1
   uint64_t* o_free = o_done + 1;           // 2
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 2);
+  uint64_t* item_full = o_free + 2;        // [4] item-id ring (TMA warp -> MMA / softmax warps)
+  uint64_t* item_empty = item_full + 4;    // [4]
+  int* item_ring = reinterpret_cast<int*>(item_empty + 4);  // [4]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(item_ring + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int H = nh * DH;
@@ -218,6 +225,10 @@ __global__ void __launch_bounds__(kThreads, NSB == 1 ? 3 : 2)
       mbar_init(&p_full[i], 4);
     }
     mbar_init(o_done, 1);
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&item_full[i], 1);
+      mbar_init(&item_empty[i], 1 + 4);  // MMA warp + 4 softmax warps
+    }
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<SH::TMEM_COLS>(tmem_slot);
@@ -227,7 +238,27 @@ __global__ void __launch_bounds__(kThreads, NSB == 1 ? 3 : 2)
   const uint32_t tbase = *tmem_slot;
 
   int G0 = 0;  // KV tiles processed by this CTA before the current item (same in every role)
-  for (int item = blockIdx.x, it = 0; item < nitem; item += gridDim.x, ++it) {
+  // dynamic item scheduler: the TMA warp claims items (first = blockIdx.x) and publishes them through the
+  // ring; -1 terminates.  Items of short (padded) rows cost less, so claiming balances the CTAs.
+  int next_item = blockIdx.x;
+  for (int it = 0;; ++it) {
+    const int slot = it & 3;
+    int item;
+    if (warp == 0) {
+      mbar_wait(&item_empty[slot], ((it >> 2) & 1) ^ 1);
+      item = next_item < nitem ? next_item : -1;
+      if (lane == 0) {
+        item_ring[slot] = item;
+        mbar_arrive(&item_full[slot]);
+      }
+      __syncwarp();
+    } else {
+      mbar_wait(&item_full[slot], (it >> 2) & 1);
+      item = item_ring[slot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&item_empty[slot]);
+    }
+    if (item < 0) break;
     const int bh = item / nqb, q0 = (item % nqb) * BM, b = bh / nh, h = bh % nh;
     const int2 mi = g_mask_info[b];
     const int kv_len = mi.x;
@@ -258,6 +289,9 @@ __global__ void __launch_bounds__(kThreads, NSB == 1 ? 3 : 2)
         }
         __syncwarp();
       }
+      int t = 0;
+      if (lane == 0) t = atomicAdd(&g_item_next, 1) + gridDim.x;
+      next_item = __shfl_sync(0xffffffffu, t, 0);
     } else if (warp == 1) {
       // ======================= MMA issuer =======================
       constexpr uint32_t idesc_s = make_idesc_bf16(BM, BN, false, false);  // S = Q Kᵀ, both K-major
