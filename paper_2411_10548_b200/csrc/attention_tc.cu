@@ -112,26 +112,6 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-// Scan the key mask of batch b: number of valid keys and whether the mask is a prefix.
-__device__ __forceinline__ void scan_mask(const int32_t* __restrict__ km, int b, int S, int* s_len, int* s_nonprefix) {
-  if (threadIdx.x == 0) {
-    *s_len = 0;
-    *s_nonprefix = 0;
-  }
-  __syncthreads();
-  int cnt = 0;
-  for (int s = threadIdx.x; s < S; s += blockDim.x) cnt += km ? (km[(int64_t)b * S + s] != 0) : 1;
-  cnt = __reduce_add_sync(0xffffffffu, cnt);
-  if ((threadIdx.x & 31) == 0) atomicAdd(s_len, cnt);
-  __syncthreads();
-  const int len = *s_len;
-  int bad = 0;
-  if (km)
-    for (int s = threadIdx.x; s < S; s += blockDim.x) bad |= ((km[(int64_t)b * S + s] != 0) != (s < len));
-  bad = __reduce_or_sync(0xffffffffu, bad);
-  if ((threadIdx.x & 31) == 0 && bad) atomicOr(s_nonprefix, 1);
-  __syncthreads();
-}
 
 // Per batch row of the key mask: number of valid keys and whether they form a prefix (written by
 // mask_info_kernel before each forward launch; read by every item of the persistent forward).
