@@ -140,6 +140,9 @@ int esm_qkv_rope_bwd(int dtype, const float* dq, const void* dk, const void* dv,
                      esm_stream_t stream);
 
 /* ---------------- attention (HF:modeling_esm.py:257-282; scaling = 1) ---------------- */
+/* Attention kernels are persistent (one CTA per SM looping over (head, tile) work claimed from a device-side
+ * counter; a per-call pre-kernel records each batch row's valid-key prefix).  Calls on one device must be
+ * stream-ordered: do not run two attention calls concurrently on different streams of the same GPU. */
 /* q,k,v [B,nh,S,dh]; key_mask [B,S] int32 (0 = padded key); o [T, nh*dh]; lse [B,nh,S] fp32. */
 int esm_attn_fwd(int dtype, const void* q, const void* k, const void* v, const int32_t* key_mask, void* o,
                  float* lse, int B, int nh, int S, int dh, esm_stream_t stream);
