@@ -505,6 +505,9 @@ struct BwdShape {
   static constexpr int QB = 64 * ROWB, KB = 128 * ROWB;
   static constexpr int NBUF = DP <= 32 ? 3 : 2;  // {S^T, dP^T} TMEM buffers (128 columns each)
   static constexpr int QST = DH == 64 ? 3 : 6;   // Q / dO / LSE / Delta stages (>= NBUF + 1)
+  // dh padded with >= 3 zero columns (dh = 24): Delta rides in dO's padding columns and V's hold -1, so the
+  // dP^T MMA directly yields dP^T - Delta (Delta split into three bf16 parts: ~24-bit exact)
+  static constexpr bool FOLD = DP - DH >= 3;
   static constexpr int DS_BUF = 2 * 128 * 128;  // one pair: [2 query chunks of 64][128 key rows][128 B]
   // dQ drain: fp32 boxes of BOXC columns x 32 rows, swizzled (128B or 64B rows), staged per drain warp for
   // TMA reduce-add.  DH = 24 drains its zero-padded 32-column tile: the 8 extra columns either fall outside
@@ -546,7 +549,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* kv_empty = kv_full + 2;        // [2]
   uint64_t* qdo_full = kv_empty + 2;       // [QST]
   uint64_t* qdo_empty = qdo_full + QST;    // [QST]
-  uint64_t* s_full = qdo_empty + QST;      // [NBUF]
+  uint64_t* qdo_ready = qdo_empty + QST;   // [QST] (FOLD: dO padding columns written)
+  uint64_t* s_full = qdo_ready + QST;      // [NBUF]
   uint64_t* ds_full = s_full + NBUF;       // [NBUF]
   uint64_t* dq_full = ds_full + NBUF;      // [2]
   uint64_t* dq_empty = dq_full + 2;        // [2]
@@ -573,6 +577,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     for (int i = 0; i < QST; ++i) {
       mbar_init(&qdo_full[i], 1);
       mbar_init(&qdo_empty[i], 1);
+      mbar_init(&qdo_ready[i], 1);
     }
     for (int i = 0; i < NBUF; ++i) {
       mbar_init(&s_full[i], 1);
@@ -645,6 +650,27 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tma_load_2d(sK + kvs * KB, &tmK, &kv_full[kvs], 0, row0 + k0);
         tma_load_2d(sV + kvs * KB, &tmV, &kv_full[kvs], 0, row0 + k0);
       }
+      // FOLD: once block i's tiles have landed, write its Delta (three bf16 parts) into dO's padding columns
+      // 24..26 (SW64: logical 16-byte chunk 3 of a row sits at chunk 3 ^ ((row >> 1) & 3)), then release it
+      auto fold = [&](int i) {
+        const int g = it * nqe + i, st = g % QST;
+        mbar_wait(&qdo_full[st], (g / QST) & 1);
+        for (int rr = lane; rr < 64; rr += 32) {
+          const float d = sD[st * 64 + rr];  // rows past S hold stale values: their P is masked to 0
+          const __nv_bfloat16 h0 = __float2bfloat16_rn(d);
+          const float r1 = d - __bfloat162float(h0);
+          const __nv_bfloat16 h1 = __float2bfloat16_rn(r1);
+          const __nv_bfloat16 h2 = __float2bfloat16_rn(r1 - __bfloat162float(h1));
+          __nv_bfloat16* dst =
+              reinterpret_cast<__nv_bfloat16*>(sdO + st * QB + rr * ROWB + ((3 ^ ((rr >> 1) & 3)) << 4));
+          dst[0] = h0;
+          dst[1] = h1;
+          dst[2] = h2;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&qdo_ready[st]);
+      };
       for (int i = 0; i < nqe; ++i) {
         const int g = it * nqe + i;
         const int st = g % QST, use = g / QST;
@@ -662,6 +688,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           }
         }
         __syncwarp();
+        if constexpr (BS::FOLD) {
+          if (i >= 2) fold(i - 2);  // lag two stages behind the loads
+        }
+      }
+      if constexpr (BS::FOLD) {
+        for (int i = max(0, nqe - 2); i < nqe; ++i) fold(i);
       }
       tile = claim();
     }
@@ -692,7 +724,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       auto issue_s = [&](int j) {  // S^T(j), dP^T(j) into buffer g % NBUF
         const int g = it * nqe + j;
         const int st = g % QST;
-        mbar_wait(&qdo_full[st], (g / QST) & 1);
+        if constexpr (BS::FOLD) mbar_wait(&qdo_ready[st], (g / QST) & 1);
+        else mbar_wait(&qdo_full[st], (g / QST) & 1);
         tc_fence_after();
         const uint64_t so = (uint64_t)((st * QB) >> 4);
         const uint32_t tS = tbase + (g % NBUF) * 128, tDP = tS + 64;
@@ -704,6 +737,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         mma_commit_w(&s_full[g % NBUF]);
       };
       mbar_wait(&kv_full[kvs], (it >> 1) & 1);
+      if constexpr (BS::FOLD) {  // V's padding columns 24..26 = -1 (the dP^T MMA subtracts Delta)
+        for (int rr = lane; rr < 128; rr += 32) {
+          __nv_bfloat16* dst =
+              reinterpret_cast<__nv_bfloat16*>(sV + kvs * KB + rr * ROWB + ((3 ^ ((rr >> 1) & 3)) << 4));
+          dst[0] = dst[1] = dst[2] = __float2bfloat16_rn(-1.f);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+      }
       for (int j = 0; j < NBUF && j < nqe; ++j) issue_s(j);
       for (int i = 0; i < nqe; ++i) {
         const int g = it * nqe + i, p = i >> 1, gp = it * npairs + p;
@@ -901,21 +943,27 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
           for (int e = 0; e < 32; e += 4) {
             const float4 l4 = *reinterpret_cast<const float4*>(lse + e);
-            const float4 d4 = *reinterpret_cast<const float4*>(dl + e);
+            const float4 d4 = BS::FOLD ? make_float4(0.f, 0.f, 0.f, 0.f) : *reinterpret_cast<const float4*>(dl + e);
             const float p0 = ex2(fmaf(__uint_as_float(us[e]), L2E, -l4.x));
             const float p1 = ex2(fmaf(__uint_as_float(us[e + 1]), L2E, -l4.y));
             const float p2 = ex2(fmaf(__uint_as_float(us[e + 2]), L2E, -l4.z));
             const float p3 = exp2_poly(fmaf(__uint_as_float(us[e + 3]), L2E, -l4.w));  // 1 in 4 on the FMA pipe
             pp[e >> 1] = pack2(p0, p1);
             pp[(e >> 1) + 1] = pack2(p2, p3);
-            dd[e >> 1] = pack2(p0 * (__uint_as_float(ud[e]) - d4.x), p1 * (__uint_as_float(ud[e + 1]) - d4.y));
-            dd[(e >> 1) + 1] = pack2(p2 * (__uint_as_float(ud[e + 2]) - d4.z), p3 * (__uint_as_float(ud[e + 3]) - d4.w));
+            if constexpr (BS::FOLD) {  // ud already holds dP^T - Delta
+              dd[e >> 1] = pack2(p0 * __uint_as_float(ud[e]), p1 * __uint_as_float(ud[e + 1]));
+              dd[(e >> 1) + 1] = pack2(p2 * __uint_as_float(ud[e + 2]), p3 * __uint_as_float(ud[e + 3]));
+            } else {
+              dd[e >> 1] = pack2(p0 * (__uint_as_float(ud[e]) - d4.x), p1 * (__uint_as_float(ud[e + 1]) - d4.y));
+              dd[(e >> 1) + 1] =
+                  pack2(p2 * (__uint_as_float(ud[e + 2]) - d4.z), p3 * (__uint_as_float(ud[e + 3]) - d4.w));
+            }
           }
         } else {
 #pragma unroll
           for (int e = 0; e < 32; e += 4) {
             const float4 l4 = *reinterpret_cast<const float4*>(lse + e);
-            const float4 d4 = *reinterpret_cast<const float4*>(dl + e);
+            const float4 d4 = BS::FOLD ? make_float4(0.f, 0.f, 0.f, 0.f) : *reinterpret_cast<const float4*>(dl + e);
             const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv4[4] = {d4.x, d4.y, d4.z, d4.w};
             float pr[4], ds[4];
 #pragma unroll
