@@ -353,3 +353,41 @@ def test_attention_bwd_qkv_fused(B, S, nh, dh, lens):
     torch.cuda.synchronize()
     assert rel(got, ref) < 2e-2
     assert rel(cs, ref_cs) < 2e-2
+
+
+@pytest.mark.parametrize("dh", [24, 64])
+@pytest.mark.parametrize("holes", [False, True])
+def test_attention_persistent_many_tiles(dh, holes):
+    """More work than CTAs (320 backward tiles / forward items on 148 SMs): dynamic tile claiming, global barrier
+    phases across tiles, padded key blocks skipped (row 1 has 724 padding keys) and a non-prefix mask."""
+    torch.manual_seed(11)
+    B, nh, S = 2, 20, 1024
+    am = torch.ones(B, S, dtype=torch.int32, device=DEV)
+    am[1, 300:] = 0
+    if holes:
+        am[0, 100:180] = 0  # non-prefix: masked keys inside the row
+    q = (torch.randn(B, nh, S, dh, device=DEV) * 0.5).bfloat16()
+    k = (torch.randn(B, nh, S, dh, device=DEV) * 0.5).bfloat16()
+    v = torch.randn(B, nh, S, dh, device=DEV).bfloat16()
+    o = torch.empty(B * S, nh * dh, device=DEV, dtype=torch.bfloat16)
+    lse = torch.empty(B, nh, S, device=DEV)
+    _lib.call("esm_attn_fwd", ESM_BF16, q.data_ptr(), k.data_ptr(), v.data_ptr(), am.data_ptr(), o.data_ptr(),
+              lse.data_ptr(), B, nh, S, dh, st())
+    qr, kr, vr = (t.float().requires_grad_(True) for t in (q, k, v))
+    ref = torch_attention(qr, kr, vr, am)
+    ref_o = ref.permute(0, 2, 1, 3).reshape(B * S, nh * dh)
+    torch.cuda.synchronize()
+    assert rel(o, ref_o) < 2e-2
+    do = torch.randn(B * S, nh * dh, device=DEV).bfloat16()
+    ref_o.backward(do.float())
+    dq = torch.empty(B, nh, S, dh, device=DEV)
+    dk = torch.full((B, nh, S, dh), float("nan"), device=DEV, dtype=torch.bfloat16)  # skipped tiles must be zeroed
+    dv = torch.full_like(dk, float("nan"))
+    delta = torch.empty(2, B, nh, S, device=DEV)
+    _lib.call("esm_attn_bwd", ESM_BF16, q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), do.data_ptr(),
+              lse.data_ptr(), am.data_ptr(), delta.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), B, nh,
+              S, dh, st())
+    torch.cuda.synchronize()
+    assert not torch.isnan(dk).any() and not torch.isnan(dv).any()
+    assert rel(dv, vr.grad) < 3e-2 and rel(dk, kr.grad) < 3e-2 and rel(dq, qr.grad) < 3e-2
+    assert (dk[1, :, 300:] == 0).all() and (dv[1, :, 300:] == 0).all()
