@@ -6,7 +6,10 @@ same batches and the same MLM masks (the device masking kernel is bit-exact with
 use the same AdamW hyper-parameters and lr schedule.
 
     python scripts/loss_trajectory.py --steps 200 --config 8m --batch 8 --seq 512
-Writes a JSON summary (both loss curves) to gpurun_out/loss_trajectory.json.
+    python scripts/loss_trajectory.py --steps 200 --config geneformer-small --batch 4 --seq 256
+(geneformer-small: the full 25,426-token Geneformer vocabulary and head, a 4-layer H=256 encoder, batches of
+rank-value tokens from synthetic cells, Geneformer masking.)  Writes a JSON summary (both loss curves) to
+gpurun_out/loss_trajectory.json.
 """
 import argparse
 import json
@@ -35,9 +38,30 @@ def main():
     ap.add_argument("--lr", type=float, default=1e-3)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "loss_trajectory.json"))
     a = ap.parse_args()
-    cfg = preset(a.config)
-    ocfg = O.OracleConfig(hidden_size=cfg.hidden_size, num_hidden_layers=cfg.num_hidden_layers,
-                          num_attention_heads=cfg.num_attention_heads, intermediate_size=cfg.intermediate_size)
+    gene = a.config == "geneformer-small"
+    if gene:
+        from paper_2411_10548_b200.config import geneformer_config
+        cfg = geneformer_config(hidden_size=256, num_hidden_layers=4, num_attention_heads=4, intermediate_size=1024)
+    else:
+        cfg = preset(a.config)
+    ocfg = O.OracleConfig(vocab_size=cfg.vocab_size, hidden_size=cfg.hidden_size,
+                          num_hidden_layers=cfg.num_hidden_layers, num_attention_heads=cfg.num_attention_heads,
+                          intermediate_size=cfg.intermediate_size, token_dropout=cfg.token_dropout,
+                          mask_token_id=cfg.mask_token_id, pad_token_id=cfg.pad_token_id)
+    mk = dict(eligible=cfg.mlm_eligible, mask_id=cfg.mask_token_id, random_range=cfg.mlm_random)
+    if gene:  # batches of rank-value tokens from synthetic cells (oracle tokenizer; rows of varying length)
+        import rank_oracle as R
+        from paper_2411_10548_b200.data import gene_medians, synthetic_expression_csr
+        n_genes = cfg.vocab_size - 2
+        ip, cols, vals = synthetic_expression_csr(a.batch * 64, n_genes, seed=5, nnz=(a.seq // 2, 2 * a.seq))
+        med = gene_medians(ip, cols, vals, n_genes)
+
+        def batch_at(step):
+            rows = [(step * a.batch + r) % (a.batch * 64) for r in range(a.batch)]
+            return R.rank_encode_batch(ip, cols, vals, med, rows, a.seq, a.seq)
+    else:
+        def batch_at(step):
+            return synthetic_batch(a.batch, a.seq, seed=10_000 + step)
     params = init_params(cfg, seed=1)
     adam = dict(beta1=0.9, beta2=0.98, eps=1e-8, weight_decay=0.01)
     tr = O.OracleTrainer(ocfg, params, lr=a.lr, dtype=np.float32, **adam)
@@ -53,10 +77,11 @@ def main():
     t0 = time.time()
     graph = False
     for step in range(1, a.steps + 1):
-        ids, am = synthetic_batch(a.batch, a.seq, seed=10_000 + step)
-        inp, lab = O.mlm_mask(ids, seed=3, stream=step)
+        ids, am = batch_at(step)
+        inp, lab = O.mlm_mask(ids, seed=3, stream=step, **mk)
         lo = tr.step(inp, am, lab, lr=lr_at(step))
         ws.ids.copy_(torch.from_numpy(ids))
+        ws.am.copy_(torch.from_numpy(am))
         m.mlm_mask(ws.ids, seed=3, stream_id=step, ws=ws)
         if not graph:
             m.capture(ws)
