@@ -1,10 +1,10 @@
-// Flash-style fused attention with key-padding mask for ESM-2 (non-causal, scaling = 1 because
-// q is pre-scaled before RoPE: HF:modeling_esm.py:257-282, 313, 341-344).
+// Attention C-ABI entry points (esm_attn_fwd / esm_attn_bwd / esm_attn_bwd_qkv) for ESM-2 (non-causal,
+// key-padding mask, scaling = 1 because q is pre-scaled before RoPE: HF:modeling_esm.py:257-282, 313, 341-344).
 //
-// bf16: FA2-style tiles on mma.sync.m16n8k16 (bf16 in, fp32 accumulate), cp.async double
-//       buffering, ldmatrix(.trans) fragments, exp2 online softmax; dh in {16, 24, 32, 64}
-//       (dh=24 is zero-padded to K=32 for QKᵀ only).  Backward parallelises over key blocks and
-//       accumulates dQ with fp32 vector reductions (red.global.add.v2.f32).
+// bf16 production path: the persistent tcgen05/TMEM kernels in attention_tc.cu; this file holds the
+//       helpers around them (Delta / log2-LSE, dQ finalisation with RoPE^T) and the legacy FA2-style
+//       mma.sync.m16n8k16 kernels kept as the baseline (ESM_ATTN_LEGACY=1): cp.async double buffering,
+//       ldmatrix(.trans) fragments, exp2 online softmax, dQ via fp32 vector reductions.
 // fp32: SIMT reference-precision kernels (parity mode).
 #include <cstdlib>
 

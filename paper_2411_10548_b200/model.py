@@ -9,10 +9,10 @@ Semantics follow Hugging Face ``EsmForMaskedLM`` (transformers 5.5.0,
 
   embeddings + token_dropout + pad mask       HF:189-236     esm_embed_fwd / esm_embed_bwd
   pre-LN (attention.LayerNorm / LayerNorm)    HF:384,394,479 esm_layernorm_fwd / _bwd
-  q,k,v projections, q*dh^-0.5, RoPE          HF:318-344     esm_gemm(STORE) + esm_qkv_rope_fwd
+  q,k,v projections, q*dh^-0.5, RoPE          HF:318-344     esm_gemm(QKV_ROPE epilogue) (fp32: + esm_qkv_rope_fwd)
   softmax(QKᵀ + key mask)·V, scaling=1        HF:257-282     esm_attn_fwd / esm_attn_bwd
   out-proj + residual                         HF:365-375     esm_gemm(RESID)
-  FC1 + erf-GELU, FC2 + residual              HF:406-427     esm_gemm(GELU), esm_gemm(RESID)
+  FC1 + erf-GELU, FC2 + residual              HF:406-427     esm_gemm(GELU_GRADAUX / GELU), esm_gemm(RESID)
   emb_layer_norm_after                        HF:511-512     esm_layernorm_fwd
   LM head dense+GELU+LN, tied decoder + bias  HF:808-815     esm_gemm(GELU) + LN + esm_lmhead_xent
   masked CE (ignore -100, mean)               HF:777-784     esm_lmhead_xent
@@ -249,7 +249,7 @@ class EsmForMaskedLM:
     """B200 ESM-2 MLM with a fused train step.
 
     dtype="bf16": bf16 activations / GEMM operands, fp32 accumulation, fp32 master weights,
-                  fp32 gradients (production path: tcgen05 GEMMs, mma.sync flash attention).
+                  fp32 gradients (production path: tcgen05 GEMMs, persistent tcgen05 flash attention).
     dtype="fp32": fp32 everywhere (SIMT kernels) -- the parity mode checked against the oracle.
     """
 
