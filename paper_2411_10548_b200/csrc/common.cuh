@@ -136,6 +136,84 @@ __device__ __forceinline__ float gelu_and_grad_fast(float z, float& grad) {
   grad = fmaf(z * 0.3989422804014327f, ex, cdf);
   return z * cdf;
 }
+// ---- packed fp32x2 arithmetic (sm_100 FFMA2/FMUL2/FADD2: two lanes' worth of fp32 per issue slot)
+__device__ __forceinline__ uint64_t f2_pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2_unpack(uint64_t r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_mul(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_splat(float a) { return f2_pack(a, a); }
+
+// Phi(z) and exp(-z^2/2) of two values at once: same erfc_core polynomial (coefficients pre-halved, exact),
+// the arithmetic in f32x2, and Phi(z) = 0.5 + copysign(0.5 - h, z) with h = erfc(|z|/sqrt2)/2 instead of
+// a compare-and-select.
+__device__ __forceinline__ void phi_core2(uint64_t z, float z0, float z1, uint64_t& cdf, uint64_t& e) {
+  const uint64_t x = f2_mul(z, f2_splat(0.70710678118654752f));
+  float x0, x1;
+  f2_unpack(x, x0, x1);
+  const uint64_t xr = f2_pack(fminf(fabsf(x0), 4.0f), fminf(fabsf(x1), 4.0f));
+  uint64_t r = f2_splat(0.5f * 1.1063529e-04f);
+  r = f2_fma(r, xr, f2_splat(0.5f * -2.1946724e-03f));
+  r = f2_fma(r, xr, f2_splat(0.5f * 1.8796470e-02f));
+  r = f2_fma(r, xr, f2_splat(0.5f * -9.1806091e-02f));
+  r = f2_fma(r, xr, f2_splat(0.5f * 2.8634080e-01f));
+  r = f2_fma(r, xr, f2_splat(0.5f * -6.1150831e-01f));
+  r = f2_fma(r, xr, f2_splat(0.5f * 9.4866168e-01f));
+  r = f2_fma(r, xr, f2_splat(0.5f * -1.1205097e+00f));
+  r = f2_fma(r, xr, f2_splat(0.5f * 9.9977970e-01f));
+  const uint64_t t = f2_mul(f2_mul(x, x), f2_splat(-1.4426950408889634f));
+  float t0, t1, e0, e1;
+  f2_unpack(t, t0, t1);
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e0) : "f"(t0));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e1) : "f"(t1));
+  e = f2_pack(e0, e1);
+  const uint64_t s = f2_fma(e, r, f2_splat(-0.5f));  // h - 0.5 <= 0
+  float s0, s1;
+  f2_unpack(s, s0, s1);
+  // s ^ (~z & 0x80000000) as one LOP3 (immLut 0xD2 = a ^ (~b & c))
+  asm("lop3.b32 %0, %0, %1, 0x80000000, 0xD2;" : "+f"(s0) : "f"(z0));
+  asm("lop3.b32 %0, %0, %1, 0x80000000, 0xD2;" : "+f"(s1) : "f"(z1));
+  cdf = f2_add(f2_pack(s0, s1), f2_splat(0.5f));
+}
+// GELU(z) = z Phi(z) and GELU'(z) = Phi(z) + z phi(z), two values at a time
+__device__ __forceinline__ void gelu_and_grad_fast2(float& z0, float& z1, float& g0, float& g1) {
+  const uint64_t z = f2_pack(z0, z1);
+  uint64_t cdf, e;
+  phi_core2(z, z0, z1, cdf, e);
+  const uint64_t gd = f2_fma(f2_mul(z, f2_splat(0.3989422804014327f)), e, cdf);
+  f2_unpack(f2_mul(z, cdf), z0, z1);
+  f2_unpack(gd, g0, g1);
+}
+__device__ __forceinline__ void gelu_fast2(float& z0, float& z1) {
+  const uint64_t z = f2_pack(z0, z1);
+  uint64_t cdf, e;
+  phi_core2(z, z0, z1, cdf, e);
+  f2_unpack(f2_mul(z, cdf), z0, z1);
+}
+__device__ __forceinline__ void gelu_grad_fast2(float z0, float z1, float& g0, float& g1) {
+  const uint64_t z = f2_pack(z0, z1);
+  uint64_t cdf, e;
+  phi_core2(z, z0, z1, cdf, e);
+  f2_unpack(f2_fma(f2_mul(z, f2_splat(0.3989422804014327f)), e, cdf), g0, g1);
+}
 __device__ __forceinline__ float gelu_grad_fast(float z) {
   const float x = fabsf(z) * 0.70710678118654752f;
   float ex;

@@ -379,11 +379,9 @@ __global__ void __launch_bounds__(EpiCfg<EPI>::THREADS, 1)
               const float4* b4 = reinterpret_cast<const float4*>(ep.bias + col0);  // 1 KB aligned groups
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
-                const float4 bb = __ldg(b4 + j);
-                v[4 * j] += bb.x;
-                v[4 * j + 1] += bb.y;
-                v[4 * j + 2] += bb.z;
-                v[4 * j + 3] += bb.w;
+                const float4 bb = __ldg(b4 + j);  // packed adds: same rounding as scalar FADD
+                f2_unpack(f2_add(f2_pack(v[4 * j], v[4 * j + 1]), f2_pack(bb.x, bb.y)), v[4 * j], v[4 * j + 1]);
+                f2_unpack(f2_add(f2_pack(v[4 * j + 2], v[4 * j + 3]), f2_pack(bb.z, bb.w)), v[4 * j + 2], v[4 * j + 3]);
               }
             } else {
 #pragma unroll
@@ -421,10 +419,18 @@ __global__ void __launch_bounds__(EpiCfg<EPI>::THREADS, 1)
               float rv[8];
               load_vec(reinterpret_cast<const __nv_bfloat16*>(a + stage_off<false>(lane, k)), rv);
 #pragma unroll
-              for (int e = 0; e < 8; ++e) {
-                if constexpr (EPI == ESM_EPI_RESID) v[8 * k + e] += rv[e];
-                else if constexpr (EPI == ESM_EPI_MUL_AUX) v[8 * k + e] *= rv[e];
-                else v[8 * k + e] *= gelu_grad_fast(rv[e]);
+              for (int e = 0; e < 8; e += 2) {
+                float& a0 = v[8 * k + e];
+                float& a1 = v[8 * k + e + 1];
+                if constexpr (EPI == ESM_EPI_RESID) {
+                  f2_unpack(f2_add(f2_pack(a0, a1), f2_pack(rv[e], rv[e + 1])), a0, a1);
+                } else if constexpr (EPI == ESM_EPI_MUL_AUX) {
+                  f2_unpack(f2_mul(f2_pack(a0, a1), f2_pack(rv[e], rv[e + 1])), a0, a1);
+                } else {
+                  float g0, g1;
+                  gelu_grad_fast2(rv[e], rv[e + 1], g0, g1);
+                  f2_unpack(f2_mul(f2_pack(a0, a1), f2_pack(g0, g1)), a0, a1);
+                }
               }
             }
             __syncwarp();
@@ -446,11 +452,11 @@ __global__ void __launch_bounds__(EpiCfg<EPI>::THREADS, 1)
             for (int k = 0; k < 4; ++k)
               store_vec(reinterpret_cast<__nv_bfloat16*>(o + E::CHUNK + stage_off<false>(lane, k)), v + 8 * k);
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = gelu_fast(v[j]);
+            for (int j = 0; j < 32; j += 2) gelu_fast2(v[j], v[j + 1]);
           } else if constexpr (EPI == ESM_EPI_GELU_GRADAUX) {
             float gd[32];
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = gelu_and_grad_fast(v[j], gd[j]);
+            for (int j = 0; j < 32; j += 2) gelu_and_grad_fast2(v[j], v[j + 1], gd[j], gd[j + 1]);
 #pragma unroll
             for (int k = 0; k < 4; ++k)
               store_vec(reinterpret_cast<__nv_bfloat16*>(o + E::CHUNK + stage_off<false>(lane, k)), gd + 8 * k);

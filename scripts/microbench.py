@@ -10,7 +10,8 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2411_10548_b200 import _lib  # noqa: E402
-from paper_2411_10548_b200._lib import EPI_DGELU, EPI_F32_ACC, EPI_GELU, EPI_RESID, EPI_STORE, ESM_BF16  # noqa: E402
+from paper_2411_10548_b200._lib import (EPI_DGELU, EPI_F32_ACC, EPI_GELU, EPI_GELU_GRADAUX, EPI_RESID, EPI_STORE,  # noqa: E402
+                                        ESM_BF16)
 
 
 def timeit(fn, iters=10, warm=3, graph=True):
@@ -86,10 +87,12 @@ def gemm():
     T = 32768
     for (name, M, N, K, amn, bmn, epi) in [
         ("35M qkv fwd", T, 1440, 480, 0, 0, EPI_STORE), ("35M fc1 fwd", T, 1920, 480, 0, 0, EPI_GELU),
+        ("35M fc1 fwd gradaux", T, 1920, 480, 0, 0, EPI_GELU_GRADAUX), ("35M fc2 dgradDGELU", T, 1920, 480, 0, 1, EPI_DGELU),
         ("35M fc2 fwd", T, 480, 1920, 0, 0, EPI_RESID), ("35M fc2 dgrad", T, 1920, 480, 0, 1, EPI_STORE),
         ("35M fc1 dgrad", T, 480, 1920, 0, 1, EPI_STORE), ("35M fc1 wgrad", 1920, 480, T, 1, 1, EPI_F32_ACC),
         ("35M fc2 wgrad", 480, 1920, T, 1, 1, EPI_F32_ACC),
-        ("650M fc1 fwd", 16384, 5120, 1280, 0, 0, EPI_GELU), ("650M fc2 fwd", 16384, 1280, 5120, 0, 0, EPI_RESID),
+        ("650M fc1 fwd", 16384, 5120, 1280, 0, 0, EPI_GELU),
+        ("650M fc1 fwd gradaux", 16384, 5120, 1280, 0, 0, EPI_GELU_GRADAUX), ("650M fc2 fwd", 16384, 1280, 5120, 0, 0, EPI_RESID),
         ("650M fc2 dgrad", 16384, 5120, 1280, 0, 1, EPI_STORE), ("650M fc1 wgrad", 5120, 1280, 16384, 1, 1, EPI_F32_ACC),
         ("650M qkv fwd", 16384, 3840, 1280, 0, 0, EPI_STORE), ("650M out fwd", 16384, 1280, 1280, 0, 0, EPI_RESID),
         ("650M fc2 dgradDGELU", 16384, 5120, 1280, 0, 1, EPI_DGELU), ("650M fc1 dgrad", 16384, 1280, 5120, 0, 1, EPI_STORE),
@@ -104,7 +107,7 @@ def gemm():
             C = torch.zeros(M, N, device="cuda")
         else:
             C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-        aux = torch.empty(M, N, device="cuda", dtype=torch.bfloat16) if epi in (EPI_GELU, EPI_RESID, EPI_DGELU) else None
+        aux = torch.empty(M, N, device="cuda", dtype=torch.bfloat16) if epi in (EPI_GELU, EPI_GELU_GRADAUX, EPI_RESID, EPI_DGELU) else None
         bias = torch.zeros(N, device="cuda")
         csum = torch.zeros(N, device="cuda") if epi == EPI_DGELU else None
         kw = dict(dtype=ESM_BF16, M=M, N=N, K=K, A=A.data_ptr(), lda=M if amn else K, a_mn_major=amn,
@@ -112,7 +115,7 @@ def gemm():
                   bias=bias.data_ptr() if epi not in (EPI_F32_ACC, EPI_DGELU) else None,
                   aux_in=aux.data_ptr() if epi in (EPI_RESID, EPI_DGELU) else None, ld_aux_in=N,
                   col_sum=csum.data_ptr() if csum is not None else None,
-                  aux_out=aux.data_ptr() if epi == EPI_GELU else None, ld_aux_out=N)
+                  aux_out=aux.data_ptr() if epi in (EPI_GELU, EPI_GELU_GRADAUX) else None, ld_aux_out=N)
         t = timeit(lambda: _lib.gemm_call(cur(), **kw), graph=os.environ.get("MB_NOGRAPH") is None)
         print(f"gemm {name:16s} M={M} N={N} K={K}: {t:.3f} ms  {2.0 * M * N * K / t / 1e9:.0f} TF/s", flush=True)
 
