@@ -9,7 +9,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libesm2b200.so")
+LIB_PATH = os.environ.get("ESM_LIB_PATH") or os.path.join(_HERE, "libesm2b200.so")  # override: A/B builds
 
 ESM_F32, ESM_BF16 = 0, 1
 EPI_STORE, EPI_GELU, EPI_RESID, EPI_DGELU, EPI_F32_ACC, EPI_QKV_ROPE, EPI_STORE_LN = 0, 1, 2, 3, 4, 5, 6

@@ -282,7 +282,7 @@ __global__ void delta_kernel(const T* __restrict__ O, const T* __restrict__ dO, 
     const int64_t b = t / S, s = t % S;
     const int64_t idx = (b * nh + h) * S + s;
     delta[idx] = acc;
-    if (lse2) lse2[idx] = lse[idx] * L2E;  // log2-domain LSE for the tcgen05 backward
+    if (lse2) lse2[idx] = -lse[idx] * L2E;  // negated log2-domain LSE (an FFMA2 addend in the tcgen05 backward)
   }
 }
 
