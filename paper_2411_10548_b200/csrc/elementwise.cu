@@ -229,25 +229,37 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
-template <typename T, int MAXV, int WPR>
-__global__ void __launch_bounds__(256) ln_fwd_kernel(const T* __restrict__ x, const float* __restrict__ g,
+// SG: gamma/beta read from shared memory instead of being held in registers, so the kernel fits 64
+// registers and 4 CTAs (32 warps) per SM keep twice the row bytes in flight (bf16 with MAXV <= 2).
+template <typename T, int MAXV, int WPR, bool SG = false>
+__global__ void __launch_bounds__(256, SG ? 4 : 1) ln_fwd_kernel(const T* __restrict__ x, const float* __restrict__ g,
                                                      const float* __restrict__ b, T* __restrict__ y,
                                                      float* __restrict__ mean_out, float* __restrict__ rstd_out,
                                                      int64_t rows, int H, float eps) {
   constexpr int VEC = vec16<T>::N;
   constexpr int GPB = 8 / WPR;  // groups per block
+  constexpr int MAXH = 512;     // SG variant: H <= MAXV * 32 * VEC <= 512 (bf16, one warp per row)
   __shared__ float2 red[GPB][2 * WPR];
+  __shared__ float sgb[SG ? 2 * MAXH : 1];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int grp = warp / WPR, wig = warp % WPR;
   const int glane = wig * 32 + lane;
   int parity = 0;
-  float gv[MAXV][VEC], bv[MAXV][VEC];
+  float gv[SG ? 1 : MAXV][VEC], bv[SG ? 1 : MAXV][VEC];
+  if constexpr (SG) {
+    for (int i = threadIdx.x; i < H; i += blockDim.x) {
+      sgb[i] = g[i];
+      sgb[MAXH + i] = b[i];
+    }
+    __syncthreads();
+  } else {
 #pragma unroll
-  for (int i = 0; i < MAXV; ++i) {
-    const int h = (i * WPR * 32 + glane) * VEC;
-    if (h < H) {
-      load_f32x(g + h, gv[i], VEC);
-      load_f32x(b + h, bv[i], VEC);
+    for (int i = 0; i < MAXV; ++i) {
+      const int h = (i * WPR * 32 + glane) * VEC;
+      if (h < H) {
+        load_f32x(g + h, gv[i], VEC);
+        load_f32x(b + h, bv[i], VEC);
+      }
     }
   }
   const float invH = 1.0f / H;
@@ -305,15 +317,24 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const T* __restrict__ x, co
     for (int i = 0; i < MAXV; ++i) {
       const int h = (i * WPR * 32 + glane) * VEC;
       if (h < H) {
-        float v[VEC], o[VEC];
+        float v[VEC], o[VEC], gs[VEC], bs[VEC];
+        const float* gi = gs;
+        const float* bi = bs;
+        if constexpr (SG) {
+          load_f32x(sgb + h, gs, VEC);
+          load_f32x(sgb + MAXH + h, bs, VEC);
+        } else {
+          gi = gv[i];
+          bi = bv[i];
+        }
         unpack_vec<T>(raw[0][i], v);
 #pragma unroll
-        for (int j = 0; j < VEC; ++j) o[j] = (v[j] - mu0) * rs0 * gv[i][j] + bv[i][j];
+        for (int j = 0; j < VEC; ++j) o[j] = (v[j] - mu0) * rs0 * gi[j] + bi[j];
         store_vec(y + r0 * H + h, o);
         if (has1) {
           unpack_vec<T>(raw[1][i], v);
 #pragma unroll
-          for (int j = 0; j < VEC; ++j) o[j] = (v[j] - mu1) * rs1 * gv[i][j] + bv[i][j];
+          for (int j = 0; j < VEC; ++j) o[j] = (v[j] - mu1) * rs1 * gi[j] + bi[j];
           store_vec(y + (r0 + 1) * H + h, o);
         }
       }
@@ -1034,7 +1055,13 @@ int esm_layernorm_fwd(int dtype, const void* x, const float* gamma, const float*
   int grid = (int)((rows + 2 * gpb - 1) / (2 * gpb));  // 2 rows per group iteration
   if (grid > 148 * 8) grid = 148 * 8;
 #define L_F(...) __VA_ARGS__<<<grid, 256, 0, S(stream)>>>((const TT*)x, gamma, beta, (TT*)y, mean, rstd, rows, H, eps)
-  if (dtype == ESM_BF16) {
+  static const bool sg_ok = !(getenv("ESM_LN_FWD_SG") && atoi(getenv("ESM_LN_FWD_SG")) == 0);
+  if (dtype == ESM_BF16 && sg_ok && wpr == 1 && mv <= 2) {
+    using TT = __nv_bfloat16;
+    if (grid > 148 * 4) grid = 148 * 4;  // 4 resident CTAs per SM: one persistent wave
+    if (mv == 1) L_F(ln_fwd_kernel<TT, 1, 1, true>);
+    else L_F(ln_fwd_kernel<TT, 2, 1, true>);
+  } else if (dtype == ESM_BF16) {
     using TT = __nv_bfloat16;
     LN_SWITCH(TT, ln_fwd_kernel, L_F);
   } else {

@@ -391,3 +391,41 @@ def test_attention_persistent_many_tiles(dh, holes):
     assert not torch.isnan(dk).any() and not torch.isnan(dv).any()
     assert rel(dv, vr.grad) < 3e-2 and rel(dk, kr.grad) < 3e-2 and rel(dq, qr.grad) < 3e-2
     assert (dk[1, :, 300:] == 0).all() and (dv[1, :, 300:] == 0).all()
+
+
+@pytest.mark.parametrize("H", [64, 320, 480, 768])
+@pytest.mark.parametrize("rows", [1, 777, 4096 + 3])
+@pytest.mark.parametrize("gelu", [False, True])
+def test_layernorm_bwd_no_stats(H, rows, gelu):
+    """The dgamma/dbeta-free backward (two rows per group iteration for H <= 512 in bf16), with the residual
+    gradient, the optional GELU' multiply and the column sum; odd row counts exercise the tail row."""
+    torch.manual_seed(5)
+    x = (torch.randn(rows, H, device=DEV) * 2 + 0.5).bfloat16()
+    g = torch.randn(H, device=DEV)
+    b = torch.randn(H, device=DEV)
+    y = torch.empty_like(x)
+    mean = torch.empty(rows, device=DEV)
+    rstd = torch.empty(rows, device=DEV)
+    _lib.call("esm_layernorm_fwd", ESM_BF16, x.data_ptr(), g.data_ptr(), b.data_ptr(), y.data_ptr(), mean.data_ptr(),
+              rstd.data_ptr(), rows, H, 1e-5, st())
+    xr = x.float().requires_grad_(True)
+    ref = torch.nn.functional.layer_norm(xr, (H,), g, b, 1e-5)
+    torch.cuda.synchronize()
+    assert rel(y, ref) < 1e-2
+    dy = torch.randn(rows, H, device=DEV).bfloat16()
+    dres = torch.randn(rows, H, device=DEV).bfloat16()
+    z = torch.randn(rows, H, device=DEV).bfloat16() if gelu else None
+    ref.backward(dy.float())
+    dx = torch.empty_like(x)
+    cs = torch.zeros(H, device=DEV)
+    _lib.call("esm_layernorm_bwd", ESM_BF16, dy.data_ptr(), x.data_ptr(), g.data_ptr(), mean.data_ptr(),
+              rstd.data_ptr(), dres.data_ptr(), z.data_ptr() if gelu else None, dx.data_ptr(), None, None,
+              cs.data_ptr(), rows, H, st())
+    torch.cuda.synchronize()
+    want = xr.grad + dres.float()
+    if gelu:
+        zf = z.float().requires_grad_(True)
+        torch.nn.functional.gelu(zf).backward(torch.ones_like(zf))
+        want = want * zf.grad
+    assert rel(dx, want) < 2e-2
+    assert rel(cs, want.sum(0)) < 1e-2
