@@ -229,18 +229,18 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
-// SG: gamma/beta read from shared memory instead of being held in registers, so the kernel fits 64
-// registers and 4 CTAs (32 warps) per SM keep twice the row bytes in flight (bf16 with MAXV <= 2).
+// SG: gamma/beta read from shared memory ([2][H] floats, dynamic) instead of being held in registers, so
+// the bf16 kernel fits 64 (MAXV <= 2) / 80 (MAXV = 3) registers and 4 / 3 CTAs per SM keep more row bytes
+// in flight than the register-resident variant's 2.
 template <typename T, int MAXV, int WPR, bool SG = false>
-__global__ void __launch_bounds__(256, SG ? 4 : 1) ln_fwd_kernel(const T* __restrict__ x, const float* __restrict__ g,
+__global__ void __launch_bounds__(256, SG ? (MAXV <= 2 ? 4 : 3) : 1) ln_fwd_kernel(const T* __restrict__ x, const float* __restrict__ g,
                                                      const float* __restrict__ b, T* __restrict__ y,
                                                      float* __restrict__ mean_out, float* __restrict__ rstd_out,
                                                      int64_t rows, int H, float eps) {
   constexpr int VEC = vec16<T>::N;
   constexpr int GPB = 8 / WPR;  // groups per block
-  constexpr int MAXH = 512;     // SG variant: H <= MAXV * 32 * VEC <= 512 (bf16, one warp per row)
   __shared__ float2 red[GPB][2 * WPR];
-  __shared__ float sgb[SG ? 2 * MAXH : 1];
+  extern __shared__ float sgb[];  // SG: gamma [H], beta [H]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int grp = warp / WPR, wig = warp % WPR;
   const int glane = wig * 32 + lane;
@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(256, SG ? 4 : 1) ln_fwd_kernel(const T* __rest
   if constexpr (SG) {
     for (int i = threadIdx.x; i < H; i += blockDim.x) {
       sgb[i] = g[i];
-      sgb[MAXH + i] = b[i];
+      sgb[H + i] = b[i];
     }
     __syncthreads();
   } else {
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(256, SG ? 4 : 1) ln_fwd_kernel(const T* __rest
         const float* bi = bs;
         if constexpr (SG) {
           load_f32x(sgb + h, gs, VEC);
-          load_f32x(sgb + MAXH + h, bs, VEC);
+          load_f32x(sgb + H + h, bs, VEC);
         } else {
           gi = gv[i];
           bi = bv[i];
@@ -1030,6 +1030,20 @@ static inline void ln_shape(int H, int vec, int& maxv, int& wpr, int max_per_lan
     else { esm::set_last_error("layernorm: H=%d unsupported", H); return ESM_ENOTSUP; }  \
   } while (0)
 
+#define LN_SWITCH_SG(T, LAUNCH)                                                          \
+  do {                                                                                   \
+    if (mv == 1 && wpr == 1) LAUNCH(ln_fwd_kernel<T, 1, 1, true>);                       \
+    else if (mv == 2 && wpr == 1) LAUNCH(ln_fwd_kernel<T, 2, 1, true>);                  \
+    else if (mv == 3 && wpr == 1) LAUNCH(ln_fwd_kernel<T, 3, 1, true>);                  \
+    else if (mv == 2 && wpr == 2) LAUNCH(ln_fwd_kernel<T, 2, 2, true>);                  \
+    else if (mv == 3 && wpr == 2) LAUNCH(ln_fwd_kernel<T, 3, 2, true>);                  \
+    else if (mv == 2 && wpr == 4) LAUNCH(ln_fwd_kernel<T, 2, 4, true>);                  \
+    else if (mv == 3 && wpr == 4) LAUNCH(ln_fwd_kernel<T, 3, 4, true>);                  \
+    else if (mv == 2 && wpr == 8) LAUNCH(ln_fwd_kernel<T, 2, 8, true>);                  \
+    else if (mv == 3 && wpr == 8) LAUNCH(ln_fwd_kernel<T, 3, 8, true>);                  \
+    else { esm::set_last_error("layernorm: H=%d unsupported", H); return ESM_ENOTSUP; }  \
+  } while (0)
+
 #define LN_SWITCH2(KS)                                                                   \
   do {                                                                                   \
     if (mv == 1 && wpr == 1) L_B(KS(1, 1));                                              \
@@ -1054,13 +1068,21 @@ int esm_layernorm_fwd(int dtype, const void* x, const float* gamma, const float*
   const int gpb = 8 / wpr;
   int grid = (int)((rows + 2 * gpb - 1) / (2 * gpb));  // 2 rows per group iteration
   if (grid > 148 * 8) grid = 148 * 8;
+#define L_SG(...)                                                                                     \
+  do {                                                                                                \
+    cudaFuncSetAttribute(__VA_ARGS__, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
+    __VA_ARGS__<<<grid, 256, smem, S(stream)>>>((const TT*)x, gamma, beta, (TT*)y, mean, rstd, rows, H, eps); \
+  } while (0)
 #define L_F(...) __VA_ARGS__<<<grid, 256, 0, S(stream)>>>((const TT*)x, gamma, beta, (TT*)y, mean, rstd, rows, H, eps)
   static const bool sg_ok = !(getenv("ESM_LN_FWD_SG") && atoi(getenv("ESM_LN_FWD_SG")) == 0);
-  if (dtype == ESM_BF16 && sg_ok && wpr == 1 && mv <= 2) {
+  if (dtype == ESM_BF16 && sg_ok) {
     using TT = __nv_bfloat16;
-    if (grid > 148 * 4) grid = 148 * 4;  // 4 resident CTAs per SM: one persistent wave
-    if (mv == 1) L_F(ln_fwd_kernel<TT, 1, 1, true>);
-    else L_F(ln_fwd_kernel<TT, 2, 1, true>);
+    const int per_sm = mv <= 2 ? 4 : 3;  // resident CTAs per SM (launch bounds): one persistent wave
+    if (grid > 148 * per_sm) grid = 148 * per_sm;
+    const size_t smem = (size_t)2 * H * sizeof(float);
+#define L_S(...) L_SG(__VA_ARGS__)
+    LN_SWITCH_SG(TT, L_S);
+#undef L_S
   } else if (dtype == ESM_BF16) {
     using TT = __nv_bfloat16;
     LN_SWITCH(TT, ln_fwd_kernel, L_F);
@@ -1069,6 +1091,7 @@ int esm_layernorm_fwd(int dtype, const void* x, const float* gamma, const float*
     LN_SWITCH(TT, ln_fwd_kernel, L_F);
   }
 #undef L_F
+#undef L_SG
   ESM_LAUNCH_RET();
 }
 
