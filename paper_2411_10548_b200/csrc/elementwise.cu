@@ -353,8 +353,9 @@ __global__ void __launch_bounds__(256, SG ? (MAXV <= 2 ? 4 : 3) : 1) ln_fwd_kern
 // Backward.  STATS: also accumulate dgamma / dbeta here (otherwise the dgrad GEMM that produced dy
 // computes them in its epilogue, ESM_EPI_STORE_LN).  Rows are held as raw 16-byte vectors (bf16 packed)
 // and all of a row's loads are issued before the reduction.
-template <typename T, int MAXV, int WPR, bool STATS>
-__global__ void __launch_bounds__(256, (sizeof(T) == 2 && (MAXV <= 2 || !STATS)) ? 2 : 1)
+// SG (bf16, no dgamma/dbeta, <= 2 vectors per lane): gamma from shared memory, 3 CTAs per SM.
+template <typename T, int MAXV, int WPR, bool STATS, bool SG = false>
+__global__ void __launch_bounds__(256, SG ? 3 : (sizeof(T) == 2 && (MAXV <= 2 || !STATS)) ? 2 : 1)
     ln_bwd_kernel(const T* __restrict__ dy, const T* __restrict__ x, const float* __restrict__ g,
                   const float* __restrict__ mean, const float* __restrict__ rstd, const T* __restrict__ dres,
                   const T* __restrict__ gelu_z, T* __restrict__ dx, float* __restrict__ dg, float* __restrict__ db,
@@ -368,12 +369,19 @@ __global__ void __launch_bounds__(256, (sizeof(T) == 2 && (MAXV <= 2 || !STATS))
   const int glane = wig * 32 + lane;
   int parity = 0;
   for (int i = threadIdx.x; i < 3 * H; i += blockDim.x) sacc[i] = 0.f;
-  float gv[MAXV][VEC], ac[MAXV][VEC];
+  const float* sg = sacc + 3 * H;  // SG: gamma [H] after the partial sums
+  if constexpr (SG) {
+    for (int i = threadIdx.x; i < H; i += blockDim.x) sacc[3 * H + i] = g[i];
+    __syncthreads();
+  }
+  float gv[SG ? 1 : MAXV][VEC], ac[MAXV][VEC];
   float ag[STATS ? MAXV : 1][VEC], ab[STATS ? MAXV : 1][VEC];
 #pragma unroll
   for (int i = 0; i < MAXV; ++i) {
     const int h = (i * WPR * 32 + glane) * VEC;
-    if (h < H) load_f32x(g + h, gv[i], VEC);
+    if constexpr (!SG) {
+      if (h < H) load_f32x(g + h, gv[i], VEC);
+    }
 #pragma unroll
     for (int j = 0; j < VEC; ++j) ac[i][j] = 0.f;
     if constexpr (STATS) {
@@ -401,13 +409,15 @@ __global__ void __launch_bounds__(256, (sizeof(T) == 2 && (MAXV <= 2 || !STATS))
     for (int i = 0; i < MAXV; ++i) {
       const int h = (i * WPR * 32 + glane) * VEC;
       if (h < H) {
-        float xv[VEC], dv[VEC];
+        float xv[VEC], dv[VEC], gs[VEC];
+        const float* gi = gs;
+        if constexpr (SG) load_f32x(sg + h, gs, VEC); else gi = gv[i];
         load_vec(reinterpret_cast<const T*>(&xr[i]), xv);
         load_vec(reinterpret_cast<const T*>(&dr[i]), dv);
 #pragma unroll
         for (int j = 0; j < VEC; ++j) {
           const float xh = (xv[j] - mu) * rs;
-          const float gy = dv[j] * gv[i][j];
+          const float gy = dv[j] * gi[j];
           s1 += gy;
           s2 += gy * xh;
           if constexpr (STATS) {
@@ -424,11 +434,13 @@ __global__ void __launch_bounds__(256, (sizeof(T) == 2 && (MAXV <= 2 || !STATS))
     for (int i = 0; i < MAXV; ++i) {
       const int h = (i * WPR * 32 + glane) * VEC;
       if (h < H) {
-        float xv[VEC], dv[VEC], o[VEC];
+        float xv[VEC], dv[VEC], o[VEC], gs[VEC];
+        const float* gi = gs;
+        if constexpr (SG) load_f32x(sg + h, gs, VEC); else gi = gv[i];
         load_vec(reinterpret_cast<const T*>(&xr[i]), xv);
         load_vec(reinterpret_cast<const T*>(&dr[i]), dv);
 #pragma unroll
-        for (int j = 0; j < VEC; ++j) o[j] = rs * (dv[j] * gv[i][j] - s1 - (xv[j] - mu) * rs * s2);
+        for (int j = 0; j < VEC; ++j) o[j] = rs * (dv[j] * gi[j] - s1 - (xv[j] - mu) * rs * s2);
         if (dres) {
           float rv[VEC];
           load_vec(reinterpret_cast<const T*>(&rr[i]), rv);
@@ -1103,10 +1115,12 @@ int esm_layernorm_bwd(int dtype, const void* dy, const void* x, const float* gam
   ESM_CHECK_ARG(H % vec == 0, "layernorm: H %% %d", vec);
   int mv, wpr;
   ln_shape(H, vec, mv, wpr);
-  const size_t sm = (size_t)3 * H * sizeof(float);
+  const size_t sm = (size_t)4 * H * sizeof(float);  // [3][H] partial sums + gamma (SG variant)
   ESM_CHECK_ARG(sm <= 200 * 1024, "layernorm_bwd: H too large");
   const bool stats = dgamma != nullptr || dbeta != nullptr;
-  int grid = 148 * 2;
+  static const bool sg_ok = !(getenv("ESM_LN_BWD_SG") && atoi(getenv("ESM_LN_BWD_SG")) == 0);
+  const bool sg = sg_ok && dtype == ESM_BF16 && !stats && mv <= 2;
+  int grid = 148 * (sg ? 3 : 2);
   const int gpb = 8 / wpr;
   if ((int64_t)grid * gpb > rows) grid = (int)((rows + gpb - 1) / gpb);
 #define L_B(...)                                                                                     \
@@ -1120,6 +1134,10 @@ int esm_layernorm_bwd(int dtype, const void* dy, const void* x, const float* gam
     using TT = __nv_bfloat16;
     if (stats) {
 #define KS(A, B) ln_bwd_kernel<TT, A, B, true>
+      LN_SWITCH2(KS);
+#undef KS
+    } else if (sg) {
+#define KS(A, B) ln_bwd_kernel<TT, A, B, false, ((A) <= 2)>
       LN_SWITCH2(KS);
 #undef KS
     } else {
