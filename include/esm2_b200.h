@@ -20,8 +20,8 @@
  *  - every call returns 0 on success, an ESM_E* code on bad arguments, or the
  *    cudaError_t of a failed launch; esm_last_error() describes the failure.
  *  - `dtype` selects the activation type: ESM_F32 (fp32 parity mode, SIMT
- *    kernels) or ESM_BF16 (production: tcgen05/TMEM/TMA GEMMs, mma.sync
- *    flash attention, vectorised epilogues).  Parameters are fp32 masters with
+ *    kernels) or ESM_BF16 (production: tcgen05/TMEM/TMA GEMMs and flash
+ *    attention, vectorised warp-shuffle epilogues).  Parameters are fp32 masters with
  *    a bf16 shadow for GEMM operands; gradients are always fp32.
  *  - activations are token-major: row t = b*S + s of a [T, width] matrix.
  */
@@ -140,22 +140,28 @@ int esm_qkv_rope_bwd(int dtype, const float* dq, const void* dk, const void* dv,
                      esm_stream_t stream);
 
 /* ---------------- attention (HF:modeling_esm.py:257-282; scaling = 1) ---------------- */
-/* Attention kernels are persistent (one CTA per SM looping over (head, tile) work claimed from a device-side
- * counter; a per-call pre-kernel records each batch row's valid-key prefix).  Calls on one device must be
- * stream-ordered: do not run two attention calls concurrently on different streams of the same GPU. */
-/* q,k,v [B,nh,S,dh]; key_mask [B,S] int32 (0 = padded key); o [T, nh*dh]; lse [B,nh,S] fp32. */
-int esm_attn_fwd(int dtype, const void* q, const void* k, const void* v, const int32_t* key_mask, void* o,
-                 float* lse, int B, int nh, int S, int dh, esm_stream_t stream);
+/* The bf16 attention kernels are persistent (one or two CTAs per SM looping over (head, tile) work claimed from
+ * a counter).  Their scheduling state lives in a caller-owned workspace `sched` (int32[ESM_ATTN_SCHED_WORDS(B)],
+ * no global mutable state): esm_attn_prepare records each batch row's valid-key count / prefix flag from
+ * key_mask and zeroes the work counters; every fwd / bwd kernel leaves the counters at zero when it finishes,
+ * so one prepared buffer serves all layers of a step while key_mask is unchanged.  Attention calls that may
+ * run concurrently (different streams) need distinct `sched` buffers.  fp32 calls ignore `sched` (may be NULL). */
+#define ESM_ATTN_SCHED_WORDS(B) (16 + 2 * (int64_t)(B))
+int esm_attn_prepare(const int32_t* key_mask, int32_t* sched, int B, int S, esm_stream_t stream);
+/* q,k,v [B,nh,S,dh]; key_mask [B,S] int32 (0 = padded key); o [T, nh*dh]; lse [B,nh,S] fp32.
+ * bf16: S % 4 == 0 (the collate step pads to a multiple of 8). */
+int esm_attn_fwd(int dtype, const void* q, const void* k, const void* v, const int32_t* key_mask, int32_t* sched,
+                 void* o, float* lse, int B, int nh, int S, int dh, esm_stream_t stream);
 /* dO [T, nh*dh]; outputs dq (fp32 accum, zeroed by callee), dk, dv [B,nh,S,dh]; delta workspace [2,B,nh,S] fp32. */
 int esm_attn_bwd(int dtype, const void* q, const void* k, const void* v, const void* o, const void* dout,
-                 const float* lse, const int32_t* key_mask, float* delta, float* dq, void* dk, void* dv,
-                 int B, int nh, int S, int dh, esm_stream_t stream);
+                 const float* lse, const int32_t* key_mask, int32_t* sched, float* delta, float* dq, void* dk,
+                 void* dv, int B, int nh, int S, int dh, esm_stream_t stream);
 
 /* Fused backward for the ESM layer (bf16, S % 4 == 0): writes dqkv[T, 3H] = [dq, dk, dv] with RoPEᵀ (and
  * q_scale on dq) applied -- the layout the QKV dgrad / wgrad GEMMs consume -- and col_sum[3H] += the q/k/v
  * bias gradients.  dq_ws: fp32 [T, H] workspace (zeroed by callee); delta: [2, B, nh, S] fp32 workspace. */
 int esm_attn_bwd_qkv(const void* q, const void* k, const void* v, const void* o, const void* dout,
-                     const float* lse, const int32_t* key_mask, float* delta, float* dq_ws, void* dqkv,
+                     const float* lse, const int32_t* key_mask, int32_t* sched, float* delta, float* dq_ws, void* dqkv,
                      float* col_sum, const float* cos_t, const float* sin_t, float q_scale, int B, int nh, int S,
                      int dh, esm_stream_t stream);
 

@@ -18,7 +18,7 @@ EPI_GELU_GRADAUX, EPI_MUL_AUX = 7, 8
 EXPORTS = [
     "esm_version", "esm_last_error", "esm_device_sm_count", "esm_tokenize", "esm_mlm_mask", "esm_embed_fwd",
     "esm_embed_bwd", "esm_layernorm_fwd", "esm_layernorm_bwd", "esm_gemm", "esm_qkv_rope_fwd", "esm_qkv_rope_bwd",
-    "esm_attn_fwd", "esm_attn_bwd", "esm_attn_bwd_qkv", "esm_lmhead_xent", "esm_inv_count",
+    "esm_attn_prepare", "esm_attn_fwd", "esm_attn_bwd", "esm_attn_bwd_qkv", "esm_lmhead_xent", "esm_inv_count",
     "esm_mlm_mask_ex", "esm_label_compact", "esm_gather_rows", "esm_scatter_rows", "esm_xent_rows", "esm_colsum_rows",
     "esm_rank_encode", "esm_adamw", "esm_cast_f32_bf16",
 ]
@@ -62,9 +62,10 @@ _SIGS = {
     "esm_gemm": ([ctypes.POINTER(GemmArgs), _P], _I),
     "esm_qkv_rope_fwd": ([_I, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _F, _P], _I),
     "esm_qkv_rope_bwd": ([_I, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _F, _P], _I),
-    "esm_attn_fwd": ([_I, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _P], _I),
-    "esm_attn_bwd": ([_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _P], _I),
-    "esm_attn_bwd_qkv": ([_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _F, _I, _I, _I, _I, _P], _I),
+    "esm_attn_prepare": ([_P, _P, _I, _I, _P], _I),
+    "esm_attn_fwd": ([_I, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _P], _I),
+    "esm_attn_bwd": ([_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _P], _I),
+    "esm_attn_bwd_qkv": ([_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _F, _I, _I, _I, _I, _P], _I),
     "esm_lmhead_xent": ([_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _P], _I),
     "esm_inv_count": ([_P, _P, _P], _I),
     "esm_mlm_mask_ex": ([_P, _P, _P, _P, _I64, _U64, _U64, _I, _I, _I, _I, _I, _P], _I),
@@ -96,6 +97,11 @@ def load(path: str = LIB_PATH):
         fn.restype = res
     _lib = lib
     return lib
+
+
+def attn_sched_words(B: int) -> int:
+    """Size (int32 words) of the attention scheduling workspace, ESM_ATTN_SCHED_WORDS(B)."""
+    return 16 + 2 * B
 
 
 def check(rc: int, what: str = ""):

@@ -128,14 +128,14 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
 }
 
 
-// Per batch row of the key mask: number of valid keys and whether they form a prefix (written by
-// mask_info_kernel before each forward launch; read by every item of the persistent forward).
-constexpr int kMaxMaskRows = 16384;
-__device__ int2 g_mask_info[kMaxMaskRows];
-__device__ int g_tile_next;  // dynamic tile counter of the persistent backward (reset by mask_info_kernel)
-__device__ int g_item_next;  // dynamic item counter of the persistent forward (reset by mask_info_kernel)
+// Scheduling workspace (caller-owned int32, ESM_ATTN_SCHED_WORDS(B) words; no global mutable state):
+//   [0] forward item counter   [1] forward CTAs finished   [2] backward tile counter   [3] backward CTAs finished
+//   [16 + 2b, 17 + 2b] batch row b: number of valid keys, 1 if they do not form a prefix
+// esm_attn_prepare (mask_info_kernel) fills it once per batch; each persistent kernel's last CTA to finish
+// resets its two counters to zero, so a prepared buffer serves every layer of the step.
+constexpr int kSchedHdr = 16;
 
-__global__ void mask_info_kernel(const int32_t* __restrict__ km, int S) {
+__global__ void mask_info_kernel(const int32_t* __restrict__ km, int S, int* __restrict__ sched) {
   __shared__ int s_len, s_np;
   const int b = blockIdx.x;
   if (threadIdx.x == 0) {
@@ -155,17 +155,28 @@ __global__ void mask_info_kernel(const int32_t* __restrict__ km, int S) {
   bad = __reduce_or_sync(0xffffffffu, bad);
   if ((threadIdx.x & 31) == 0 && bad) atomicOr(&s_np, 1);
   __syncthreads();
-  if (threadIdx.x == 0) g_mask_info[b] = make_int2(len, s_np);
-  if (b == 0 && threadIdx.x == 0) {
-    g_tile_next = 0;
-    g_item_next = 0;
+  if (threadIdx.x == 0) reinterpret_cast<int2*>(sched + kSchedHdr)[b] = make_int2(len, s_np);
+  if (b == 0 && threadIdx.x < 4) sched[threadIdx.x] = 0;
+}
+
+__device__ __forceinline__ int2 mask_info(const int* sched, int b) {
+  return reinterpret_cast<const int2*>(sched + kSchedHdr)[b];
+}
+
+// called by one thread per CTA after the CTA's last work claim: the last CTA of the grid zeroes the
+// claim counter (at sched[c]) and the finished-CTA count (sched[c + 1]) for the next launch
+__device__ __forceinline__ void sched_finish(int* sched, int c) {
+  __threadfence();
+  if (atomicAdd(&sched[c + 1], 1) == (int)gridDim.x - 1) {
+    atomicExch(&sched[c], 0);
+    atomicExch(&sched[c + 1], 0);
   }
 }
 
 // backward tile (head, 128-key block) whose keys are all right-padding (prefix mask): skipped by every role
-__device__ __forceinline__ bool tile_skipped(int tile, int nkb, int nh, int S) {
+__device__ __forceinline__ bool tile_skipped(const int* sched, int tile, int nkb, int nh) {
   const int b = (tile / nkb) / nh, k0 = (tile % nkb) * 128;
-  const int2 mi = g_mask_info[b];
+  const int2 mi = mask_info(sched, b);
   return mi.y == 0 && k0 >= mi.x;
 }
 
@@ -177,7 +188,8 @@ template <int DH, int BN, int NSB>
 __global__ void __launch_bounds__(kThreads, NSB == 1 ? 3 : 2)
     fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                const __grid_constant__ CUtensorMap tmV, const int32_t* __restrict__ key_mask,
-               __nv_bfloat16* __restrict__ O, float* __restrict__ LSE, int S, int nh, int nbh) {
+               int* __restrict__ sched, __nv_bfloat16* __restrict__ O, float* __restrict__ LSE, int S, int nh,
+               int nbh) {
   using SH = Shape<DH, BN, NSB>;
   constexpr int DP = SH::DP, ROWB = SH::ROWB, ST = SH::STAGES;
   constexpr int QB = SH::Q_BYTES, TB = SH::KV_BYTES;
@@ -195,7 +207,8 @@ __global__ void __launch_bounds__(kThreads, NSB == 1 ? 3 : 2)
   uint64_t* p_full = s_full + 2;           // 2
   uint64_t* o_done = p_full + 2;           // 1
   uint64_t* o_free = o_done + 1;           // 2
-  uint64_t* item_full = o_free + 2;        // [4] item-id ring (TMA warp -> MMA / softmax warps)
+  uint64_t* o_full = o_free + 2;           // 2: all PV MMAs of the item using O buffer qs are complete
+  uint64_t* item_full = o_full + 2;        // [4] item-id ring (TMA warp -> MMA / softmax warps)
   uint64_t* item_empty = item_full + 4;    // [4]
   int* item_ring = reinterpret_cast<int*>(item_empty + 4);  // [4]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(item_ring + 4);
@@ -210,6 +223,7 @@ __global__ void __launch_bounds__(kThreads, NSB == 1 ? 3 : 2)
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], 1);
       mbar_init(&o_free[i], 4);
+      mbar_init(&o_full[i], 1);
     }
     for (int i = 0; i < ST; ++i) {
       mbar_init(&kv_full[i], 1);
@@ -255,7 +269,7 @@ __global__ void __launch_bounds__(kThreads, NSB == 1 ? 3 : 2)
     }
     if (item < 0) break;
     const int bh = item / nqb, q0 = (item % nqb) * BM, b = bh / nh, h = bh % nh;
-    const int2 mi = g_mask_info[b];
+    const int2 mi = mask_info(sched, b);
     const int kv_len = mi.x;
     const bool nonprefix = mi.y != 0;
     const int ntiles = nonprefix ? (S + BN - 1) / BN : (kv_len + BN - 1) / BN;
@@ -285,7 +299,7 @@ __global__ void __launch_bounds__(kThreads, NSB == 1 ? 3 : 2)
         __syncwarp();
       }
       int t = 0;
-      if (lane == 0) t = atomicAdd(&g_item_next, 1) + gridDim.x;
+      if (lane == 0) t = atomicAdd(&sched[0], 1) + gridDim.x;
       next_item = __shfl_sync(0xffffffffu, t, 0);
     } else if (warp == 1) {
       // ======================= MMA issuer =======================
@@ -319,6 +333,7 @@ __global__ void __launch_bounds__(kThreads, NSB == 1 ? 3 : 2)
           mma_ts_w(t_o, p_tmem + k * 8, vd + so + k * ROWB, idesc_o, (i > 0 || k > 0) ? 1u : 0u);
         mma_commit_w(&kv_empty[st]);
         mma_commit_w(o_done);
+        if (i == ntiles - 1) mma_commit_w(&o_full[qs]);
       };
       for (int j = 0; j <= ntiles; ++j) {
         if (NSB == 1) {  // one S buffer: P_{j-1} (packed over S) must be consumed before S_j overwrites it
@@ -329,7 +344,10 @@ __global__ void __launch_bounds__(kThreads, NSB == 1 ? 3 : 2)
           if (j >= 1) issue_pv(j - 1);
         }
       }
-      if (ntiles == 0) mma_commit_w(&q_empty[qs]);
+      if (ntiles == 0) {
+        mma_commit_w(&q_empty[qs]);
+        mma_commit_w(&o_full[qs]);  // keeps the per-buffer phase count of o_full in step with the items
+      }
     } else {
       // ======================= softmax warps =======================
       const int qq = warp & 3;
@@ -416,13 +434,13 @@ __global__ void __launch_bounds__(kThreads, NSB == 1 ? 3 : 2)
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[gj % NSB]);
       }
-      // ---- epilogue: wait for the last PV, O / l, LSE; release the O buffer
+      // ---- epilogue: wait for the last PV, O / l, LSE; release the O buffer.  (Not o_done: another softmax
+      // warp may still be two tiles behind, so o_done's phase count can trail by two and a parity wait on it
+      // would pass early; o_full[qs] completes exactly once per item on this buffer.)
       const int qrow = q0 + r;
       float inv = l > 0.f ? 1.f / l : 0.f;
-      if (ntiles > 0) {
-        mbar_wait(o_done, (G0 + ntiles - 1) & 1);
-        tc_fence_after();
-      }
+      mbar_wait(&o_full[qs], (it >> 1) & 1);
+      tc_fence_after();
       float o[DP];
 #pragma unroll
       for (int c = 0; c < DP; c += 16) {
@@ -453,8 +471,8 @@ __global__ void __launch_bounds__(kThreads, NSB == 1 ? 3 : 2)
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) sched_finish(sched, 0);
   if (warp == 1) {
-
     tc_fence_after();
     tmem_dealloc<SH::TMEM_COLS>(tbase);
   }
@@ -492,8 +510,6 @@ struct FusedOut {
   const float* cos_t;   // [S, dh/2]
   const float* sin_t;
   int H;
-  unsigned long long* trace;  // debug timeline (nullptr in production): [role][block][event]
-  int experiment;  // debug timing experiments (0 in production): 1 = softmax warps skip their math, 2 = no dQ reductions
 };
 
 __device__ __forceinline__ void tma_reduce_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
@@ -504,16 +520,6 @@ __device__ __forceinline__ void tma_reduce_2d(const CUtensorMap* map, const void
 __device__ __forceinline__ void bulk_commit_group() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-
-// trace slots: role r (0 = MMA, 1 = softmax warp 2, 2 = softmax warp 6), block i (< 64), event e (< 8)
-__device__ __forceinline__ void trace_ev(unsigned long long* tr, int role, int i, int e) {
-  if (tr != nullptr && blockIdx.x == 3 && i < 64) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
-    tr[(role * 64 + i) * 8 + e] = t;
-  }
-}
-
 
 template <int DH>
 struct BwdShape {
@@ -546,9 +552,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
                const __grid_constant__ CUtensorMap tmdQ, const int32_t* __restrict__ key_mask,
-               const float* __restrict__ LSE2, const float* __restrict__ Delta, float* __restrict__ dQ,
-               __nv_bfloat16* __restrict__ dK, __nv_bfloat16* __restrict__ dV, int S, int nh, int nbh,
-               const FusedOut fo) {
+               int* __restrict__ sched, const float* __restrict__ LSE2, const float* __restrict__ Delta,
+               float* __restrict__ dQ, __nv_bfloat16* __restrict__ dK, __nv_bfloat16* __restrict__ dV, int S,
+               int nh, int nbh, const FusedOut fo) {
   using BS = BwdShape<DH>;
   constexpr int DP = BS::DP, ROWB = BS::ROWB, QB = BS::QB, KB = BS::KB, QST = BS::QST, NBUF = BS::NBUF;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -632,12 +638,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     // dK / dV rows of fully padded key blocks here, publish real tiles through the ring, -1 terminates
     auto claim = [&]() {
       int t = 0;
-      if (lane == 0) t = atomicAdd(&g_tile_next, 1) + gridDim.x;
+      if (lane == 0) t = atomicAdd(&sched[2], 1) + gridDim.x;
       return __shfl_sync(0xffffffffu, t, 0);
     };
     int tile = blockIdx.x;
     for (int it = 0;; ++it) {
-      while (tile < ntile && tile_skipped(tile, nkb, nh, S)) {
+      while (tile < ntile && tile_skipped(sched, tile, nkb, nh)) {
         const int bh = tile / nkb, k0 = (tile % nkb) * 128, b = bh / nh, h = bh % nh;
         for (int i = lane; i < 128; i += 32) {
           const int key = k0 + i;
@@ -735,7 +741,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&tile_empty[slot]);
       if (tile < 0) break;
-      unsigned long long* tr = it == 0 ? fo.trace : nullptr;
       const int kvs = it & 1;
       const uint64_t ko = (uint64_t)((kvs * KB) >> 4);
       auto issue_s = [&](int j) {  // S^T(j), dP^T(j) into buffer g % NBUF
@@ -767,9 +772,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       for (int i = 0; i < nqe; ++i) {
         const int g = it * nqe + i, p = i >> 1, gp = it * npairs + p;
         const int st = g % QST;
-        if (lane == 0) trace_ev(tr, 0, i, 0);
         mbar_wait(&ds_full[g % NBUF], (g / NBUF) & 1);
-        if (lane == 0) trace_ev(tr, 0, i, 1);
         if (i == 0 && it > 0) mbar_wait(dkv_free, (it - 1) & 1);  // previous tile's dV / dK have been read
         if ((i & 1) && gp >= 2) mbar_wait(&dq_empty[gp & 1], ((gp >> 1) - 1) & 1);
         tc_fence_after();
@@ -796,9 +799,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           mma_commit_w(dkv_done);
           mma_commit_w(&kv_empty[kvs]);
         }
-        if (lane == 0) trace_ev(tr, 0, i, 2);
         if (i + NBUF < nqe) issue_s(i + NBUF);  // buffer g % NBUF is free once dV/dK(g) are issued (in-order)
-        if (lane == 0) trace_ev(tr, 0, i, 3);
       }
     }
   } else if (warp >= 10) {
@@ -848,7 +849,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         // rows past this sequence carry exact zeros (dS = 0 there), so spilling into the next rows is harmless
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (lane == 0 && fo.experiment != 2) {
+        if (lane == 0) {
           const int row = (fo.dqkv ? b * S : bh * S) + p * 128 + qq * 32;
           const int col = fo.dqkv ? h * DH : 0;
 #pragma unroll
@@ -926,7 +927,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const int kr = qq * 32 + lane;
     const uint32_t lane_off = (uint32_t)(qq * 32) << 16;
     const int c = hf * 32;
-    const int trole = (warp == 2) ? 1 : (warp == 6 ? 2 : -1);
     for (int it = 0;; ++it) {
       const int slot = it & 3;
       mbar_wait(&tile_full[slot], (it >> 2) & 1);
@@ -934,7 +934,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&tile_empty[slot]);
       if (tile < 0) break;
-      unsigned long long* tr = it == 0 ? fo.trace : nullptr;
       const int bh = tile / nkb, k0 = (tile % nkb) * 128, b = bh / nh;
       const int key = k0 + kr;
       const bool kvalid = key < S && key_mask[(int64_t)b * S + key] != 0;
@@ -944,16 +943,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const float* lse = sL + st * 64 + c;
         const float* dl = sD + st * 64 + c;
         const uint32_t tS = tbase + (g % NBUF) * 128, tDP = tS + 64;
-        if (lane == 0 && trole > 0) trace_ev(tr, trole, i, 0);
         mbar_wait(&s_full[g % NBUF], (g / NBUF) & 1);
-        if (lane == 0 && trole > 0) trace_ev(tr, trole, i, 1);
         tc_fence_after();
         uint32_t us[32], ud[32];
         tmem_ld32(tS + lane_off + c, us);
         tmem_ld32(tDP + lane_off + c, ud);
         if (ch == 0 && gp >= 2) mbar_wait(&dsm_empty[gp & 1], ((gp >> 1) - 1) & 1);
         tmem_ld_wait();
-        if (lane == 0 && trole > 0) trace_ev(tr, trole, i, 2);
         uint32_t pp[16], dd[16];
         const int qmax = S - i * 64 - c;
         if (__all_sync(0xffffffffu, kvalid) && qmax >= 32) {  // full tile: no masking
@@ -1013,7 +1009,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
         // packed P^T / dS^T go into this warp's own 32-column half of the S^T / dP^T buffers (which it has
         // finished reading), so the two warps of a lane quarter need no barrier
-        if (lane == 0 && trole > 0) trace_ev(tr, trole, i, 3);
         tmem_st16(tS + lane_off + hf * 32, pp);
         tmem_st16(tDP + lane_off + hf * 32, dd);
         uint8_t* rowp = sdS + (gp & 1) * BS::DS_BUF + ch * (128 * 128) + kr * 128;
@@ -1028,12 +1023,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&ds_full[g % NBUF]);
-        if (lane == 0 && trole > 0) trace_ev(tr, trole, i, 5);
       }
     }
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) sched_finish(sched, 2);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<512>(tbase);
@@ -1083,8 +1078,8 @@ static int head_map(CUtensorMap* m, const void* base, int64_t rows) {
 }
 
 template <int DH, int BN, int NSB>
-int launch_fwd(const void* q, const void* k, const void* v, const int32_t* km, void* o, float* lse, int B, int nh,
-               int S, cudaStream_t st) {
+int launch_fwd(const void* q, const void* k, const void* v, const int32_t* km, int* sched, void* o, float* lse, int B,
+               int nh, int S, cudaStream_t st) {
   using SH = Shape<DH, BN, NSB>;
   CUtensorMap tq, tk, tv;
   const int64_t rows = (int64_t)B * nh * S;
@@ -1093,26 +1088,18 @@ int launch_fwd(const void* q, const void* k, const void* v, const int32_t* km, v
       (rc = head_map<DH, BN>(&tv, v, rows)))
     return rc;
   const int smem = 2 * SH::Q_BYTES + 2 * SH::STAGES * SH::KV_BYTES + 1024 + 256;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(fwd_kernel<DH, BN, NSB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
-  ESM_CHECK_ARG(B <= kMaxMaskRows, "attention: batch %d exceeds %d", B, kMaxMaskRows);
-  mask_info_kernel<<<B, 256, 0, st>>>(km, S);
+  cudaFuncSetAttribute(fwd_kernel<DH, BN, NSB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int nitem = ((S + BM - 1) / BM) * B * nh;
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const int per_sm = NSB == 1 ? 3 : 2;  // CTAs resident per SM
-  const int grid = min(nitem, per_sm * sms);
-  fwd_kernel<DH, BN, NSB><<<grid, kThreads, smem, st>>>(tq, tk, tv, km, (__nv_bfloat16*)o, lse, S, nh, B * nh);
+  const int grid = min(nitem, per_sm * device_sm_count());
+  fwd_kernel<DH, BN, NSB><<<grid, kThreads, smem, st>>>(tq, tk, tv, km, sched, (__nv_bfloat16*)o, lse, S, nh, B * nh);
   ESM_LAUNCH_RET();
 }
 
 
 template <int DH>
 int launch_bwd(const void* q, const void* k, const void* v, const void* dout, const float* lse2, const float* delta,
-               const int32_t* km, float* dq, void* dk, void* dv, int B, int nh, int S, cudaStream_t st,
+               const int32_t* km, int* sched, float* dq, void* dk, void* dv, int B, int nh, int S, cudaStream_t st,
                FusedOut fo) {
   using SH = Shape<DH, 64>;
   using BS = BwdShape<DH>;
@@ -1151,72 +1138,48 @@ int launch_bwd(const void* q, const void* k, const void* v, const void* dout, co
       return ESM_EDRIVER;
     }
   }
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(bwd_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, BS::SMEM);
-    attr = true;
-  }
-  ESM_CHECK_ARG(B <= kMaxMaskRows, "attention: batch %d exceeds %d", B, kMaxMaskRows);
-  mask_info_kernel<<<B, 256, 0, st>>>(km, S);
+  cudaFuncSetAttribute(bwd_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, BS::SMEM);
   const int ntile = ((S + 127) / 128) * B * nh;
-  static const int persist = getenv("ESM_ATTN_BWD_GRID") ? atoi(getenv("ESM_ATTN_BWD_GRID")) : 0;
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  // persistent: one CTA per SM loops over key-block tiles (ESM_ATTN_BWD_GRID=n overrides the CTA count)
-  const int grid = persist > 0 ? min(persist, ntile) : min(sms, ntile);
-  bwd_kernel<DH><<<grid, kBwdThreads, BS::SMEM, st>>>(tq, tk, tv, tdo, tdq, km, lse2, delta, dq,
+  // persistent: one CTA per SM loops over key-block tiles
+  const int grid = min(device_sm_count(), ntile);
+  bwd_kernel<DH><<<grid, kBwdThreads, BS::SMEM, st>>>(tq, tk, tv, tdo, tdq, km, sched, lse2, delta, dq,
                                                       (__nv_bfloat16*)dk, (__nv_bfloat16*)dv, S, nh, B * nh, fo);
   ESM_LAUNCH_RET();
 }
 
 }  // namespace fa
 
-static unsigned long long* g_attn_trace = nullptr;
+int attn_prepare_tc(const int32_t* km, int* sched, int B, int S, cudaStream_t st) {
+  fa::mask_info_kernel<<<B, 256, 0, st>>>(km, S, sched);
+  ESM_LAUNCH_RET();
+}
 
 int attn_bwd_tc(const void* q, const void* k, const void* v, const void* dout, const float* lse2, const float* delta,
-                const int32_t* km, float* dq, void* dk, void* dv, int B, int nh, int S, int dh, cudaStream_t st,
-                void* dqkv, float* col_sum, const float* cos_t, const float* sin_t) {
+                const int32_t* km, int* sched, float* dq, void* dk, void* dv, int B, int nh, int S, int dh,
+                cudaStream_t st, void* dqkv, float* col_sum, const float* cos_t, const float* sin_t) {
   ESM_CHECK_ARG(S % 4 == 0, "attention bwd (tcgen05): S %% 4 == 0 required");
-  if (getenv("ESM_ATTN_TRACE") && g_attn_trace == nullptr) {
-    cudaMalloc(&g_attn_trace, 3 * 64 * 8 * 8);
-    cudaMemset(g_attn_trace, 0, 3 * 64 * 8 * 8);
-  }
-  static const int experiment = getenv("ESM_ATTN_EXPERIMENT") ? atoi(getenv("ESM_ATTN_EXPERIMENT")) : 0;
-  fa::FusedOut fo{(__nv_bfloat16*)dqkv, col_sum, cos_t, sin_t, nh * dh, g_attn_trace, experiment};
+  fa::FusedOut fo{(__nv_bfloat16*)dqkv, col_sum, cos_t, sin_t, nh * dh};
   switch (dh) {
-    case 16: return fa::launch_bwd<16>(q, k, v, dout, lse2, delta, km, dq, dk, dv, B, nh, S, st, fo);
-    case 24: return fa::launch_bwd<24>(q, k, v, dout, lse2, delta, km, dq, dk, dv, B, nh, S, st, fo);
-    case 32: return fa::launch_bwd<32>(q, k, v, dout, lse2, delta, km, dq, dk, dv, B, nh, S, st, fo);
-    case 64: return fa::launch_bwd<64>(q, k, v, dout, lse2, delta, km, dq, dk, dv, B, nh, S, st, fo);
+    case 16: return fa::launch_bwd<16>(q, k, v, dout, lse2, delta, km, sched, dq, dk, dv, B, nh, S, st, fo);
+    case 24: return fa::launch_bwd<24>(q, k, v, dout, lse2, delta, km, sched, dq, dk, dv, B, nh, S, st, fo);
+    case 32: return fa::launch_bwd<32>(q, k, v, dout, lse2, delta, km, sched, dq, dk, dv, B, nh, S, st, fo);
+    case 64: return fa::launch_bwd<64>(q, k, v, dout, lse2, delta, km, sched, dq, dk, dv, B, nh, S, st, fo);
     default: set_last_error("attention: head dim %d unsupported", dh); return ESM_ENOTSUP;
   }
 }
 
-int attn_fwd_tc(const void* q, const void* k, const void* v, const int32_t* km, void* o, float* lse, int B, int nh,
-                int S, int dh, cudaStream_t st) {
+int attn_fwd_tc(const void* q, const void* k, const void* v, const int32_t* km, int* sched, void* o, float* lse,
+                int B, int nh, int S, int dh, cudaStream_t st) {
   ESM_CHECK_ARG(((uintptr_t)q & 15) == 0 && ((uintptr_t)k & 15) == 0 && ((uintptr_t)v & 15) == 0,
                 "attention: q/k/v must be 16B aligned");
-  // NSB = S buffers per CTA: 2 (default, 2 CTAs/SM) or 1 (3 CTAs/SM; measured equal at dh 24, slower at dh 64)
-  static const int nsb = getenv("ESM_ATTN_FWD_NSB") ? atoi(getenv("ESM_ATTN_FWD_NSB")) : 2;
-  if (nsb == 1) switch (dh) {
-    case 16: return fa::launch_fwd<16, 64, 1>(q, k, v, km, o, lse, B, nh, S, st);
-    case 24: return fa::launch_fwd<24, 64, 1>(q, k, v, km, o, lse, B, nh, S, st);
-    case 32: return fa::launch_fwd<32, 64, 1>(q, k, v, km, o, lse, B, nh, S, st);
-    case 64: return fa::launch_fwd<64, 64, 1>(q, k, v, km, o, lse, B, nh, S, st);
-  }
+  // two S buffers per CTA, 2 CTAs/SM (a single-buffer 3-CTA/SM variant measured equal at dh 24, slower at 64)
   switch (dh) {
-    case 16: return fa::launch_fwd<16, 64, 2>(q, k, v, km, o, lse, B, nh, S, st);
-    case 24: return fa::launch_fwd<24, 64, 2>(q, k, v, km, o, lse, B, nh, S, st);
-    case 32: return fa::launch_fwd<32, 64, 2>(q, k, v, km, o, lse, B, nh, S, st);
-    case 64: return fa::launch_fwd<64, 64, 2>(q, k, v, km, o, lse, B, nh, S, st);
+    case 16: return fa::launch_fwd<16, 64, 2>(q, k, v, km, sched, o, lse, B, nh, S, st);
+    case 24: return fa::launch_fwd<24, 64, 2>(q, k, v, km, sched, o, lse, B, nh, S, st);
+    case 32: return fa::launch_fwd<32, 64, 2>(q, k, v, km, sched, o, lse, B, nh, S, st);
+    case 64: return fa::launch_fwd<64, 64, 2>(q, k, v, km, sched, o, lse, B, nh, S, st);
     default: set_last_error("attention: head dim %d unsupported", dh); return ESM_ENOTSUP;
   }
 }
 
 }  // namespace esm
-
-extern "C" int esm_debug_attn_trace(unsigned long long* host_out) {
-  // debug only: the last attention-backward timeline recorded with ESM_ATTN_TRACE=1 (3 x 64 x 8 clock64)
-  if (esm::g_attn_trace == nullptr) return ESM_ENOTSUP;
-  return (int)cudaMemcpy(host_out, esm::g_attn_trace, 3 * 64 * 8 * 8, cudaMemcpyDeviceToHost);
-}

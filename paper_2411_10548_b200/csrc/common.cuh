@@ -36,6 +36,26 @@ void set_last_error(const char* fmt, ...);
     return 0;                                                               \
   } while (0)
 
+// SM count of the *current* device (cached per device id; launches size persistent grids with it).
+// Function attributes (max dynamic shared memory) are likewise per device, so launchers set them on
+// every launch rather than once per process (cheap, and legal during CUDA-graph capture).
+inline int device_sm_count() {
+  static int cache[64] = {0};
+  int d = 0;
+  cudaGetDevice(&d);
+  if (d < 0 || d >= 64) {
+    int v = 148;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
+    return v;
+  }
+  if (cache[d] == 0) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
+    cache[d] = v > 0 ? v : 148;
+  }
+  return cache[d];
+}
+
 // ----------------------------------------------------------------------------
 // element I/O for the two activation dtypes (fp32 parity mode, bf16 production)
 // ----------------------------------------------------------------------------

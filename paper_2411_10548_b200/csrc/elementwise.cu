@@ -910,7 +910,7 @@ __global__ void cast_kernel(const float* __restrict__ s, __nv_bfloat16* __restri
     d[i] = __float2bfloat16_rn(s[i]);
 }
 
-static int grid_for(int64_t work, int block, int cap = 148 * 16) {
+static int grid_for(int64_t work, int block, int cap = device_sm_count() * 16) {
   int64_t g = (work + block - 1) / block;
   if (g > cap) g = cap;
   if (g < 1) g = 1;
@@ -1079,7 +1079,7 @@ int esm_layernorm_fwd(int dtype, const void* x, const float* gamma, const float*
   ln_shape(H, vec, mv, wpr);
   const int gpb = 8 / wpr;
   int grid = (int)((rows + 2 * gpb - 1) / (2 * gpb));  // 2 rows per group iteration
-  if (grid > 148 * 8) grid = 148 * 8;
+  if (grid > device_sm_count() * 8) grid = device_sm_count() * 8;
 #define L_SG(...)                                                                                     \
   do {                                                                                                \
     cudaFuncSetAttribute(__VA_ARGS__, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
@@ -1090,7 +1090,7 @@ int esm_layernorm_fwd(int dtype, const void* x, const float* gamma, const float*
   if (dtype == ESM_BF16 && sg_ok) {
     using TT = __nv_bfloat16;
     const int per_sm = mv <= 2 ? 4 : 3;  // resident CTAs per SM (launch bounds): one persistent wave
-    if (grid > 148 * per_sm) grid = 148 * per_sm;
+    if (grid > device_sm_count() * per_sm) grid = device_sm_count() * per_sm;
     const size_t smem = (size_t)2 * H * sizeof(float);
 #define L_S(...) L_SG(__VA_ARGS__)
     LN_SWITCH_SG(TT, L_S);
@@ -1120,7 +1120,7 @@ int esm_layernorm_bwd(int dtype, const void* dy, const void* x, const float* gam
   const bool stats = dgamma != nullptr || dbeta != nullptr;
   static const bool sg_ok = !(getenv("ESM_LN_BWD_SG") && atoi(getenv("ESM_LN_BWD_SG")) == 0);
   const bool sg = sg_ok && dtype == ESM_BF16 && !stats && mv <= 2;
-  int grid = 148 * (sg ? 3 : 2);
+  int grid = device_sm_count() * (sg ? 3 : 2);
   const int gpb = 8 / wpr;
   if ((int64_t)grid * gpb > rows) grid = (int)((rows + gpb - 1) / gpb);
 #define L_B(...)                                                                                     \
@@ -1201,7 +1201,7 @@ int esm_lmhead_xent(int dtype, const void* n, const void* E, const float* bias, 
   ESM_CHECK_ARG(n && E && bias && labels && inv_denom && loss_sum && dlogits_ws && dn && dE && dbias,
                 "esm_lmhead_xent: null pointer");
   ESM_CHECK_ARG(V > 0 && V <= 64, "esm_lmhead_xent: V must be <= 64 (ESM alphabet is 33)");
-  const int grid = grid_for((int64_t)T_ * 32, 256, 148 * 8);
+  const int grid = grid_for((int64_t)T_ * 32, 256, device_sm_count() * 8);
   const int rpb = 512;
   dim3 g2((H + 31) / 32, (T_ + rpb - 1) / rpb);
   {  // preferred: E staged in shared memory (lanes over the vocabulary)
@@ -1209,7 +1209,7 @@ int esm_lmhead_xent(int dtype, const void* n, const void* E, const float* bias, 
     const size_t pad = dtype == ESM_BF16 ? 2 : 1;
     const size_t smem = (((size_t)V * (H + pad) * esz + 15) & ~(size_t)15) + 8 * 64 * 4 + 8 * (size_t)H * esz;
     if (smem <= 200 * 1024 && H % 8 == 0) {
-      const int g = grid_for((int64_t)T_ * 32, 256, 148 * 4);
+      const int g = grid_for((int64_t)T_ * 32, 256, device_sm_count() * 4);
       if (dtype == ESM_BF16) {
         cudaFuncSetAttribute(xent_small_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         xent_small_kernel<__nv_bfloat16><<<g, 256, smem, S(stream)>>>(
@@ -1258,7 +1258,7 @@ int esm_lmhead_xent(int dtype, const void* n, const void* E, const float* bias, 
 int esm_adamw(float* p, const float* g, float* m, float* v, void* p16, const uint8_t* decay_chunk, int64_t n,
               const float* hyper, esm_stream_t stream) {
   ESM_CHECK_ARG(p && g && m && v && decay_chunk && hyper && n % 256 == 0, "esm_adamw: bad args (n %% 256 == 0)");
-  adamw_kernel<<<grid_for(n / 4, 256, 148 * 8), 256, 0, S(stream)>>>(p, g, m, v, (__nv_bfloat16*)p16, decay_chunk, n,
+  adamw_kernel<<<grid_for(n / 4, 256, device_sm_count() * 8), 256, 0, S(stream)>>>(p, g, m, v, (__nv_bfloat16*)p16, decay_chunk, n,
                                                                      hyper);
   ESM_LAUNCH_RET();
 }

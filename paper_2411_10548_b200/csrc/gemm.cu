@@ -545,16 +545,7 @@ static int make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t o
   return 0;
 }
 
-static int g_num_sms = 0;
-static int num_sms() {
-  if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
-  }
-  return g_num_sms;
-}
+static int num_sms() { return device_sm_count(); }
 
 template <int BN, bool A_MN, bool B_MN, int EPI, int CG>
 static int launch_cg(const esm_gemm_args& a, cudaStream_t st) {
@@ -621,11 +612,7 @@ static int launch_cg(const esm_gemm_args& a, cudaStream_t st) {
                {(__nv_bfloat16*)a.q_out, (__nv_bfloat16*)a.k_out, (__nv_bfloat16*)a.v_out},
                a.seq_len, a.n_heads, a.head_dim, a.q_scale, a.row_mean, a.row_rstd, a.col_sum2};
   auto kern = gemm_tc_kernel<BN, A_MN, B_MN, EPI, CG>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    attr_set = true;
-  }
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);  // per device: every launch
   const int total = tiles * splits;
   const int units = total < sms ? total : sms;
   if constexpr (CG == 1) {

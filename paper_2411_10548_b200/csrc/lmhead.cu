@@ -175,7 +175,7 @@ int esm_label_compact(const int32_t* labels, int64_t T, int32_t* idx, int32_t* l
 int esm_gather_rows(int dtype, const void* src, const int32_t* idx, void* dst, int cap, int H, esm_stream_t stream) {
   ESM_CHECK_ARG(src && idx && dst && cap > 0 && H % 8 == 0, "esm_gather_rows: bad args");
   int64_t g = ((int64_t)cap * H / 4 + 255) / 256;
-  if (g > 148 * 16) g = 148 * 16;
+  if (g > device_sm_count() * 16) g = device_sm_count() * 16;
   if (dtype == ESM_BF16)
     gather_rows_kernel<__nv_bfloat16><<<(int)g, 256, 0, S_(stream)>>>((const __nv_bfloat16*)src, idx,
                                                                       (__nv_bfloat16*)dst, cap, H);
@@ -189,7 +189,7 @@ int esm_scatter_rows(int dtype, const void* src, const int32_t* idx, void* dst, 
   ESM_CHECK_ARG(src && idx && dst && cap > 0 && H % 8 == 0, "esm_scatter_rows: bad args");
   cudaMemsetAsync(dst, 0, (size_t)T * H * (dtype == ESM_BF16 ? 2 : 4), S_(stream));
   int64_t g = ((int64_t)cap * H / 4 + 255) / 256;
-  if (g > 148 * 16) g = 148 * 16;
+  if (g > device_sm_count() * 16) g = device_sm_count() * 16;
   if (dtype == ESM_BF16)
     scatter_rows_kernel<__nv_bfloat16><<<(int)g, 256, 0, S_(stream)>>>((const __nv_bfloat16*)src, idx,
                                                                        (__nv_bfloat16*)dst, cap, H);

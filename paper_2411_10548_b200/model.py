@@ -190,10 +190,14 @@ class Workspace:
         self.input_ids = torch.zeros(B, S, dtype=i32, device=device)  # after MLM masking
         self.labels = torch.full((B, S), -100, dtype=i32, device=device)
         self.am = torch.ones(B, S, dtype=i32, device=device)
-        self.n_labels = torch.zeros(1, dtype=i32, device=device)
+        self.n_labels = torch.zeros(1, dtype=i32, device=device)         # this rank's labelled tokens
+        self.n_labels_global = torch.zeros(1, dtype=i32, device=device)  # all ranks' (the loss normaliser)
         self.inv_denom = torch.zeros(1, dtype=f32, device=device)
         self.loss_sum = torch.zeros(1, dtype=f32, device=device)
         self.row_scale = e(B, dt=f32)
+        # attention scheduling workspace (per-row key-prefix info + persistent-kernel work counters); filled by
+        # esm_attn_prepare once per step, shared by every layer's forward and backward on this stream
+        self.attn_sched = torch.zeros(_lib.attn_sched_words(B), dtype=i32, device=device)
         self.x = [e(T, H) for _ in range(L + 1)]  # residual stream: input of layer l; x[L] = encoder output
         self.layers = []
         for _ in range(L):
@@ -344,8 +348,15 @@ class EsmForMaskedLM:
         self.ws = cache[key]
         return self.ws
 
+    def release_workspaces(self):
+        """Free every cached activation workspace (and its CUDA graph)."""
+        self._ws_cache.clear()
+        self.ws = None
+        self.graph = None
+        torch.cuda.empty_cache()
+
     # kernels launched per C-ABI entry point (for the bench's gpu_launches count)
-    _KERNELS = {"esm_embed_fwd": 2, "esm_attn_fwd": 2, "esm_attn_bwd": 3, "esm_attn_bwd_qkv": 4, "esm_lmhead_xent": 2}
+    _KERNELS = {"esm_embed_fwd": 2, "esm_attn_bwd": 3, "esm_attn_bwd_qkv": 4, "esm_lmhead_xent": 2}
 
     def _call(self, name, *args, flops=0.0, nbytes=0.0):
         t = self.timer
@@ -501,9 +512,14 @@ class EsmForMaskedLM:
 
         self.store.g32.zero_()
         ws.loss_sum.zero_()
-        if self.comm is not None:
-            self.comm.reduce_count(ws.n_labels)  # global masked-token count -> loss normaliser
-        call("esm_inv_count", ws.n_labels.data_ptr(), ws.inv_denom.data_ptr(), st)
+        n_lab = ws.n_labels
+        if self.comm is not None:  # global masked-token count -> loss normaliser; the local count is kept
+            ws.n_labels_global.copy_(ws.n_labels)
+            self.comm.reduce_count(ws.n_labels_global)
+            n_lab = ws.n_labels_global
+        call("esm_inv_count", n_lab.data_ptr(), ws.inv_denom.data_ptr(), st)
+        sched = ws.attn_sched.data_ptr()
+        call("esm_attn_prepare", ws.am.data_ptr(), sched, B, S, st)  # key-mask scan: once per step, not per layer
         # ---------------- forward
         call("esm_embed_fwd", kdt, ws.input_ids.data_ptr(), ws.am.data_ptr(), E.data_ptr(), ws.x[0].data_ptr(),
              ws.row_scale.data_ptr(), B, S, H, int(cfg.token_dropout), cfg.mask_token_id, st)
@@ -521,7 +537,7 @@ class EsmForMaskedLM:
                                 ws.qkv)
                 call("esm_qkv_rope_fwd", kdt, ws.qkv.data_ptr(), ly.q.data_ptr(), ly.k.data_ptr(), ly.v.data_ptr(),
                      ws.cos.data_ptr(), ws.sin.data_ptr(), B, S, nh, dh, qs, st)
-            call("esm_attn_fwd", kdt, ly.q.data_ptr(), ly.k.data_ptr(), ly.v.data_ptr(), ws.am.data_ptr(),
+            call("esm_attn_fwd", kdt, ly.q.data_ptr(), ly.k.data_ptr(), ly.v.data_ptr(), ws.am.data_ptr(), sched,
                  ly.o.data_ptr(), ly.lse.data_ptr(), B, nh, S, dh, st, flops=4.0 * B * nh * S * S * dh)
             self.linear_fwd(ly.o, p + "attention.output.dense.weight", H, H, p + "attention.output.dense.bias",
                             ly.x1, epi=EPI_RESID, aux_in=x)
@@ -547,6 +563,8 @@ class EsmForMaskedLM:
                  ws.labels.data_ptr(), ws.inv_denom.data_ptr(), ws.loss_sum.data_ptr(), ws.dlogits.data_ptr(),
                  ws.dn.data_ptr(), self._g32(E_key).data_ptr(), self._g32("lm_head.bias").data_ptr(), T, H, V, st)
         if loss_only:
+            if self.comm is not None:
+                self.comm.reduce_loss(ws.loss_sum)
             return ws.loss_sum
         # ---------------- backward
         self._opt_on = optimizer
@@ -592,16 +610,16 @@ class EsmForMaskedLM:
             # attention
             self.linear_dgrad(ws.dx1, p + "attention.output.dense.weight", H, H, ws.do)
             self.linear_wgrad(ws.dx1, ly.o, p + "attention.output.dense.weight", H, H)
-            if kdt == ESM_BF16 and S % 4 == 0 and self._fused_attn_bwd(dh):
+            if kdt == ESM_BF16 and self._fused_attn_bwd(dh):
                 # fused: attention backward writes dqkv [T,3H] (RoPE^T, q-scale) + q/k/v bias grads
                 call("esm_attn_bwd_qkv", ly.q.data_ptr(), ly.k.data_ptr(), ly.v.data_ptr(), ly.o.data_ptr(),
-                     ws.do.data_ptr(), ly.lse.data_ptr(), ws.am.data_ptr(), ws.delta.data_ptr(), ws.dq.data_ptr(),
-                     ws.dqkv.data_ptr(), self._g32(p + "attention.self.qkv.bias").data_ptr(), ws.cos.data_ptr(),
-                     ws.sin.data_ptr(), qs, B, nh, S, dh, st, flops=10.0 * B * nh * S * S * dh)
+                     ws.do.data_ptr(), ly.lse.data_ptr(), ws.am.data_ptr(), sched, ws.delta.data_ptr(),
+                     ws.dq.data_ptr(), ws.dqkv.data_ptr(), self._g32(p + "attention.self.qkv.bias").data_ptr(), ws.cos.data_ptr(),
+                     ws.sin.data_ptr(), qs, B, nh, S, dh, st, flops=8.0 * B * nh * S * S * dh)
             else:
                 call("esm_attn_bwd", kdt, ly.q.data_ptr(), ly.k.data_ptr(), ly.v.data_ptr(), ly.o.data_ptr(),
-                     ws.do.data_ptr(), ly.lse.data_ptr(), ws.am.data_ptr(), ws.delta.data_ptr(), ws.dq.data_ptr(),
-                     ws.dk.data_ptr(), ws.dv.data_ptr(), B, nh, S, dh, st, flops=10.0 * B * nh * S * S * dh)
+                     ws.do.data_ptr(), ly.lse.data_ptr(), ws.am.data_ptr(), sched, ws.delta.data_ptr(),
+                     ws.dq.data_ptr(), ws.dk.data_ptr(), ws.dv.data_ptr(), B, nh, S, dh, st, flops=8.0 * B * nh * S * S * dh)
                 call("esm_qkv_rope_bwd", kdt, ws.dq.data_ptr(), ws.dk.data_ptr(), ws.dv.data_ptr(),
                      ws.dqkv.data_ptr(), self._g32(p + "attention.self.qkv.bias").data_ptr(), ws.cos.data_ptr(),
                      ws.sin.data_ptr(), B, S, nh, dh, qs, st)

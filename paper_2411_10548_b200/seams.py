@@ -30,18 +30,26 @@ from .data import collate
 
 
 class CudaPeakMeter:
-    """ResourceMeter over CUDA allocator statistics: peak bytes allocated since ``reset()``."""
+    """ResourceMeter over CUDA allocator statistics: peak bytes allocated since ``reset()``.
 
-    def __init__(self, device=None):
+    relative=False: the absolute peak (resident model state included).  relative=True: the peak minus what was
+    allocated at ``reset()`` -- the memory one sample adds on top of the resident model (parameters, gradients,
+    Adam moments), which is what a per-sample cost model summed over a batch must predict
+    (``SizeAwareBatcher`` adds per-sample costs, sizing.py:203-219)."""
+
+    def __init__(self, device=None, relative: bool = False):
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.relative = relative
+        self._base = 0
 
     def reset(self) -> None:
         torch.cuda.synchronize(self.device)
         torch.cuda.reset_peak_memory_stats(self.device)
+        self._base = torch.cuda.memory_allocated(self.device) if self.relative else 0
 
     def peak(self) -> float:
         torch.cuda.synchronize(self.device)
-        return float(torch.cuda.max_memory_allocated(self.device))
+        return float(torch.cuda.max_memory_allocated(self.device) - self._base)
 
 
 def length_features(sample) -> np.ndarray:
@@ -61,21 +69,23 @@ def collate_indices(dataset, indices: Sequence[int], seq_len: int | None = None,
     return collate(toks, seq_len=seq_len, pad_to=pad_to, pad_id=pad_id)
 
 
-def make_workload(model, seed: int = 0, pad_to: int = 8, lr: float | None = None) -> Callable:
+def make_workload(model, seed: int = 0, pad_to: int = 8, lr: float | None = None, use_graph: bool = False,
+                  release: bool = False) -> Callable:
     """``workload(sample)`` for ``collect_peak_alloc``: one full MLM train step (device masking,
-    forward, backward, AdamW) on a sample = one token sequence or a list of them."""
+    forward, backward, AdamW) on a sample = one token sequence or a list of them.  ``release=True`` frees the
+    sample's activation workspace after the step, so a relative ``CudaPeakMeter`` sees exactly one sample's
+    activation memory per record."""
     state = {"step": 0}
 
     def workload(sample):
         batch = sample if (len(sample) and not isinstance(sample[0], (int, np.integer))) else [sample]
-        ids, am = collate(batch, pad_to=pad_to, pad_id=model.config.pad_token_id)
-        ids_d = torch.from_numpy(ids).to(model.device)
-        ws = model.workspace(*ids.shape)
-        ws.am.copy_(torch.from_numpy(am).to(model.device))
-        model.mlm_mask(ids_d, seed, state["step"], ws)
-        model.step(ws, lr=lr)
+        loss = model.train_step_tokens(batch, seed=seed, stream_id=state["step"], lr=lr, pad_to=pad_to,
+                                       use_graph=use_graph)
         state["step"] += 1
-        return float(ws.loss_sum.item())
+        out = float(loss.item())
+        if release:
+            model.release_workspaces()
+        return out
 
     return workload
 

@@ -215,17 +215,10 @@ def test_geneformer_preset_and_feed_host_logic():
 def test_reference_shard_stream_feeds_collate(tmp_path):
     """the reference's own tar-shard pipeline (write_shards / subset / stream_samples /
     batch_stage) with our shard_collate yields the padded batches the train step consumes; the per-rank
-    subsets partition the samples (skipped where the reference package is not importable)."""
-    ref = "/root/reference/pkg/src"
-    if not os.path.isdir(ref):
-        pytest.skip("reference package not present")
-    sys.path.insert(0, ref)
-    try:
-        from densefeed import shards as SH
-    except Exception as exc:  # pragma: no cover
-        pytest.skip(f"densefeed not importable: {exc}")
-    finally:
-        sys.path.remove(ref)
+    subsets partition the samples (the reference is imported from baseline/_ref; never skipped)."""
+    from conftest import import_reference
+    densefeed, _ = import_reference()
+    SH = densefeed.shards
     from paper_2411_10548_b200.seams import shard_collate
     rng = np.random.default_rng(0)
     toks = {f"s{i:03d}": np.r_[0, rng.integers(4, 24, int(rng.integers(5, 40))), 2].astype("<i4") for i in range(23)}
@@ -239,3 +232,40 @@ def test_reference_shard_stream_feeds_collate(tmp_path):
             assert (ids[am == 0] == 1).all() and (ids[:, 0] == 0).all()
             seen += ids.shape[0]
     assert seen == len(toks)
+
+
+def test_reference_bindings_batches_feed_collate_indices(tmp_path):
+    """SURVEY §8b seams 'Dataset items' + 'Batch stream' on the CPU: the reference's own store
+    (build_store), BoundDataset (dfb.open: rank_encode per row) and dfb.batches (create_buckets +
+    bucket_batches over a saved cost model) drive seams.collate_indices; every index list becomes a padded
+    int32 [B, S] batch whose rows are exactly the reference's rank tokens (PAD 0), and the index lists
+    partition the dataset (modulo budget skips) deterministically for a seed."""
+    from conftest import import_reference
+    densefeed, dfb = import_reference()
+    from paper_2411_10548_b200.seams import collate_indices
+    rng = np.random.default_rng(3)
+    n_rows, n_cols = 60, 300
+    lines = ["% test", f"{n_rows} {n_cols} 0"]
+    ent = []
+    for r in range(n_rows):
+        k = int(rng.integers(3, 120))
+        for c in sorted(rng.choice(n_cols, k, replace=False)):
+            ent.append(f"{r + 1} {c + 1} {float(rng.uniform(0.5, 10.0))!r}")
+    lines[1] = f"{n_rows} {n_cols} {len(ent)}"
+    (tmp_path / "m.mtx").write_text("\n".join(lines + ent) + "\n")
+    densefeed.build_store(tmp_path / "m.mtx", tmp_path / "store")
+    ds = dfb.open(tmp_path / "store", max_len=64)
+    cm = densefeed.CostModel(weights=np.array([1.0]), intercept=0.0, safety_margin=1.0)
+    densefeed.save_cost_model(cm, tmp_path / "cm.json")
+    got = [list(b) for b in dfb.batches(ds, tmp_path / "cm.json", budget=400.0, max_width=30, min_count=4, seed=7)]
+    again = [list(b) for b in dfb.batches(ds, tmp_path / "cm.json", budget=400.0, max_width=30, min_count=4, seed=7)]
+    assert got == again and len(got) > 3
+    seen = sorted(i for b in got for i in b)
+    assert len(seen) == len(set(seen)) and set(seen) <= set(range(n_rows))
+    for idx in got:
+        ids, am = collate_indices(ds, idx, pad_to=8, pad_id=0)
+        assert ids.shape[0] == len(idx) and ids.shape[1] % 8 == 0 and ids.dtype == np.int32
+        for j, i in enumerate(idx):
+            want = ds[i][0]
+            assert ids[j, :len(want)].tolist() == want and am[j].sum() == len(want)
+            assert (ids[j, len(want):] == 0).all()
