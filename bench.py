@@ -52,6 +52,12 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true", help="skip the per-kernel CUDA-event breakdown")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--zero1", action="store_true", help="N>1: sharded optimizer (reduce-scatter / AdamW on the "
+                    "rank's slice / all-gather), the ZeRO-1 comparison point of PAPER.md:86-88")
+    ap.add_argument("--grad-bf16", action="store_true", help="N>1: bf16 gradient buckets (half the NVLink bytes)")
+    ap.add_argument("--varlen", action="store_true",
+                    help="protein-like lengths (lognormal(5.6, 0.65) clipped to [10, seq]) batched by the reference's "
+                         "create_buckets / bucket_batches at a token budget of batch x seq (SURVEY.md §8d, §8f.1)")
     return ap.parse_args()
 
 
@@ -256,6 +262,121 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------ variable-length (bucketed) protein batches
+def import_reference():
+    """densefeed from the unmodified reference install (baseline/_ref; /root/reference in the build container)."""
+    for p in (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
+        if os.path.isdir(p) and p not in sys.path:
+            sys.path.append(p)
+    import densefeed
+    return densefeed
+
+
+def run_varlen(args, rank, world, local, dev):
+    """Tokens/s on protein-like lengths: a seeded corpus of lognormal(5.6, 0.65) lengths clipped to [10, S]
+     is bucketed by the reference's create_buckets and batched by its bucket_batches under a
+    token budget of B x S (cost model = tokens); every rank runs the same seeded iterator and takes batches
+    i = rank (mod world).  Each step goes through the public API
+    EsmForMaskedLM.train_step_tokens (host token lists -> collate, H2D, device masking, fwd, bwd, AdamW); one
+    CUDA graph per bucket shape (N = 1), all captured before the timed region.  Value = non-pad tokens/s."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2411_10548_b200 import preset
+    from paper_2411_10548_b200.data import collate
+    from paper_2411_10548_b200.ddp import GradAllReducer
+    from paper_2411_10548_b200.model import EsmForMaskedLM
+    densefeed = import_reference()
+    preset_name, B, S = WORKLOADS[args.config]
+    B, S = args.batch or B, args.seq or S
+    cfg = preset(preset_name)
+    if cfg.vocab_size > 40:
+        raise SystemExit("--varlen: ESM-2 protein configs only")
+    rng = np.random.default_rng(0)
+    n_seq = 64 * B
+    lens = np.clip(rng.lognormal(5.6, 0.65, n_seq), 10, S).astype(np.int64)
+    corpus = [np.r_[0, rng.integers(4, 24, L - 2), 2].astype(np.int32) for L in lens]
+    spec = densefeed.create_buckets(lens.tolist(), max_width=32, min_count=2 * B)
+    cost = densefeed.CostModel(weights=np.array([1.0]), intercept=0.0, safety_margin=1.0)  # tokens
+    feats = lens.reshape(-1, 1).astype(np.float64)
+    batches = [b.indices for b in densefeed.bucket_batches(spec, feats, cost, float(B * S), seed=7)]
+    mine = batches[rank::world]
+    pad_to = 16
+    shapes = sorted({(len(b), (int(lens[b].max()) + pad_to - 1) // pad_to * pad_to) for b in mine},
+                    key=lambda x: x[0] * x[1])
+    model = EsmForMaskedLM(cfg, dtype=args.dtype, device=dev, seed=1)
+    model.max_workspaces = len(shapes) + 1
+    model.reserve(*max(shapes, key=lambda x: x[0] * x[1]))
+    if world > 1:
+        model.comm = GradAllReducer(model.store)
+    use_graph = world == 1 and not args.no_graph
+    seed = 4321
+
+    def step(i):
+        toks = [corpus[j] for j in mine[i % len(mine)]]
+        return model.train_step_tokens(toks, seed=seed, stream_id=i * world + rank, pad_to=pad_to,
+                                       use_graph=use_graph)
+
+    # capture every bucket shape once (untimed), then the warm-up steps
+    seen = set()
+    for i, b in enumerate(mine):
+        shp = (len(b), (int(lens[b].max()) + pad_to - 1) // pad_to * pad_to)
+        if shp not in seen:
+            seen.add(shp)
+            step(i)
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
+        time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    tok = pad_tok = attn_sq = 0.0
+    l0 = model.launches
+    e0.record()
+    for i in range(args.steps):
+        b = mine[(args.warmup + i) % len(mine)]
+        step(args.warmup + i)
+        tok += float(lens[b].sum())
+        attn_sq += float((lens[b].astype(np.float64) ** 2).sum())
+        pad_tok += len(b) * ((int(lens[b].max()) + pad_to - 1) // pad_to * pad_to)
+    e1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    clocks = sampler.stop() if sampler else None
+    t = torch.tensor([ms, tok, pad_tok, attn_sq], device=dev, dtype=torch.float64)
+    if world > 1:
+        mx = t[:1].clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t)
+        t[0] = mx[0]
+    ms, tok, pad_tok, attn_sq = (float(x) for x in t)
+    value = tok / args.steps / (ms / 1e3)
+    _, _, tf_sust, peak_src = load_peaks()
+    flops_tok = cfg.train_flops_per_token(0) + 12.0 * cfg.num_hidden_layers * cfg.hidden_size * attn_sq / tok
+    if rank == 0:
+        print(json.dumps({
+            "metric": "ESM-2 MLM train tokens/sec", "value": value, "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+            "config": {"workload": f"{preset_name} MLM pre-training on bucketed variable-length proteins "
+                                   f"(token budget {B * S} per GPU-step)", "model": preset_name,
+                       "seq_len": S, "parallelism": f"dp{world}", "cuda_graph": use_graph,
+                       "lengths": f"lognormal(5.6, 0.65) clipped to [10, {S}], {n_seq} sequences",
+                       "batching": "densefeed.create_buckets(max_width=32, min_count=2B) + bucket_batches (tokens), pad to 16",
+                       "bucket_shapes": len(shapes), "non_pad_fraction": round(tok / pad_tok, 4),
+                       "api": "EsmForMaskedLM.train_step_tokens (host token lists -> H2D -> mask -> step)"},
+            "mfu": round(value / world * flops_tok / (tf_sust * 1e12), 4),
+            "mfu_peak": f"{tf_sust} TFLOP/s bf16 sustained ({peak_src})", "train_flops_per_token": flops_tok,
+            "gpu_launches": (model.launches - l0) // max(1, args.steps), "clocks": clocks}), flush=True)
+
+
 # ------------------------------------------------------------------ our B200 path
 def main():
     args = parse()
@@ -280,6 +401,11 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    if args.varlen:
+        run_varlen(args, rank, world, local, dev)
+        if world > 1:
+            dist.destroy_process_group()
+        return
     preset_name, B, S = WORKLOADS[args.config]
     B = args.batch or B
     S = args.seq or S
@@ -287,8 +413,9 @@ def main():
     model = EsmForMaskedLM(cfg, dtype=args.dtype, device=dev, seed=1)
     ws = model.workspace(B, S)
     if world > 1:
-        model.comm = GradAllReducer(model.store)
-    use_graph = (world == 1) and not args.no_graph
+        model.comm = GradAllReducer(model.store, grad_dtype="bf16" if args.grad_bf16 else "fp32",
+                                    shard_optimizer=args.zero1)
+    use_graph = not args.no_graph  # N > 1: the NCCL bucket collectives are captured in the same graph
 
     gene = cfg.vocab_size > 40
     if gene:  # Geneformer: synthetic cells -> rank-value tokens on the GPU (esm_rank_encode)
@@ -446,8 +573,11 @@ def main():
         if pool_am is not None:
             ws.am.copy_(pool_am[0])
         model.mlm_mask(pool[0], seed, 999, ws)
-        model.forward_backward(ws)
-        model.optimizer_step()
+        if model.comm is not None and (model.comm.shard or model.comm.bf16):
+            model.step(ws)  # the optimizer runs per bucket slice inside the step
+        else:
+            model.forward_backward(ws)
+            model.optimizer_step()
         agg = model.timer.summary()
         model.timer = None
         total = sum(d["ms"] for d in agg.values())
@@ -502,7 +632,9 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
             "config": {"workload": f"{preset_name} MLM pre-training step (mask+fwd+bwd+AdamW), {B} x {S} per GPU",
                        "model": preset_name, "global_batch": B * world, "seq_len": S,
-                       "parallelism": f"dp{world}", "l2": "inputs/activations >> 126 MB L2 (no flush needed)",
+                       "parallelism": f"dp{world}" + ("-zero1" if args.zero1 and world > 1 else "") +
+                                      ("-bf16grad" if args.grad_bf16 and world > 1 else ""),
+                       "l2": "inputs/activations >> 126 MB L2 (no flush needed)",
                        "cuda_graph": use_graph, "weights": "random init",
                        "data": (f"synthetic cells, {GF_NNZ[0]}-{GF_NNZ[1]} expressed genes of {GF_GENES}, "
                                 f"GPU rank-value tokens; non-pad tokens counted "

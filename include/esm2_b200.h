@@ -37,8 +37,8 @@ extern "C" {
 
 typedef void* esm_stream_t; /* a cudaStream_t */
 
-enum { ESM_F32 = 0, ESM_BF16 = 1 };
-enum { ESM_OK = 0, ESM_EINVAL = 1001, ESM_ENOTSUP = 1002, ESM_EDRIVER = 1003 };
+enum { ESM_F32 = 0, ESM_BF16 = 1, ESM_I32 = 2 /* collectives only */ };
+enum { ESM_OK = 0, ESM_EINVAL = 1001, ESM_ENOTSUP = 1002, ESM_EDRIVER = 1003, ESM_ENCCL_BASE = 2000 /* + ncclResult_t */ };
 
 /* GEMM epilogues (applied to acc = A·Bᵀ, fp32) */
 enum {
@@ -196,8 +196,31 @@ int esm_inv_count(const int32_t* n_labels, float* inv_denom, esm_stream_t stream
  * decay_chunk[i] (uint8) = 1 if elements [i*256, (i+1)*256) are weight-decayed.  p16 = bf16 shadow (or NULL). */
 int esm_adamw(float* p, const float* g, float* m, float* v, void* p16, const uint8_t* decay_chunk, int64_t n,
               const float* hyper, esm_stream_t stream);
-/* fp32 -> bf16 copy (shadow refresh). */
+/* Same update with bf16 gradients g (data-parallel buckets reduced in bf16). */
+int esm_adamw_bf16g(float* p, const void* g, float* m, float* v, void* p16, const uint8_t* decay_chunk, int64_t n,
+                    const float* hyper, esm_stream_t stream);
+/* fp32 -> bf16 copy (shadow refresh, bf16 gradient buckets); src 16-byte, dst 8-byte aligned. */
 int esm_cast_f32_bf16(const float* src, void* dst, int64_t n, esm_stream_t stream);
+/* bf16 -> fp32 copy. */
+int esm_cast_bf16_f32(const void* src, float* dst, int64_t n, esm_stream_t stream);
+
+/* ---------------- data-parallel collectives (NCCL over NVLink / NVSwitch; SURVEY.md §8b "Comms") ----------------
+ * NCCL is resolved at run time (the libnccl.so.2 already loaded in the process, i.e. torch.distributed's, else
+ * the system one).  Rendezvous: rank 0 calls esm_comm_unique_id and the host layer broadcasts the 128 bytes
+ * (torch.distributed); every rank then calls esm_comm_init.  Collectives are in place, SUM, enqueued on
+ * `stream` (CUDA-graph capturable).  Errors: ESM_ENCCL_BASE + ncclResult_t. */
+#define ESM_COMM_ID_BYTES 128
+typedef struct esm_comm* esm_comm_t;
+int esm_comm_version(void); /* NCCL version code, 0 if NCCL cannot be loaded */
+int esm_comm_unique_id(uint8_t* out /* ESM_COMM_ID_BYTES */);
+int esm_comm_init(const uint8_t* id, int rank, int world, esm_comm_t* out);
+int esm_comm_destroy(esm_comm_t comm);
+/* buf[0..count) = sum over ranks (ESM_F32 / ESM_BF16 / ESM_I32) -- the gradient-bucket all-reduce. */
+int esm_comm_allreduce(esm_comm_t comm, void* buf, int64_t count, int dtype, esm_stream_t stream);
+/* count % world == 0; slice r = buf[r*count/world, (r+1)*count/world) of rank r receives the sum of that slice. */
+int esm_comm_reduce_scatter(esm_comm_t comm, void* buf, int64_t count, int dtype, esm_stream_t stream);
+/* count % world == 0; every rank receives every rank's slice r of buf (the sharded-optimizer parameter gather). */
+int esm_comm_allgather(esm_comm_t comm, void* buf, int64_t count, int dtype, esm_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -11,7 +11,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("ESM_LIB_PATH") or os.path.join(_HERE, "libesm2b200.so")  # override: A/B builds
 
-ESM_F32, ESM_BF16 = 0, 1
+ESM_F32, ESM_BF16, ESM_I32 = 0, 1, 2
 EPI_STORE, EPI_GELU, EPI_RESID, EPI_DGELU, EPI_F32_ACC, EPI_QKV_ROPE, EPI_STORE_LN = 0, 1, 2, 3, 4, 5, 6
 EPI_GELU_GRADAUX, EPI_MUL_AUX = 7, 8
 
@@ -20,7 +20,9 @@ EXPORTS = [
     "esm_embed_bwd", "esm_layernorm_fwd", "esm_layernorm_bwd", "esm_gemm", "esm_qkv_rope_fwd", "esm_qkv_rope_bwd",
     "esm_attn_prepare", "esm_attn_fwd", "esm_attn_bwd", "esm_attn_bwd_qkv", "esm_lmhead_xent", "esm_inv_count",
     "esm_mlm_mask_ex", "esm_label_compact", "esm_gather_rows", "esm_scatter_rows", "esm_xent_rows", "esm_colsum_rows",
-    "esm_rank_encode", "esm_adamw", "esm_cast_f32_bf16",
+    "esm_rank_encode", "esm_adamw", "esm_adamw_bf16g", "esm_cast_f32_bf16", "esm_cast_bf16_f32",
+    "esm_comm_version", "esm_comm_unique_id", "esm_comm_init", "esm_comm_destroy", "esm_comm_allreduce",
+    "esm_comm_reduce_scatter", "esm_comm_allgather",
 ]
 
 
@@ -76,7 +78,16 @@ _SIGS = {
     "esm_colsum_rows": ([_I, _P, _I, _I, _I64, _P, _P], _I),
     "esm_rank_encode": ([_P, _P, _P, _P, _I64, _P, _I, _I, _I, _P, _P, _P, _P, _I, _P], _I),
     "esm_adamw": ([_P, _P, _P, _P, _P, _P, _I64, _P, _P], _I),
+    "esm_adamw_bf16g": ([_P, _P, _P, _P, _P, _P, _I64, _P, _P], _I),
     "esm_cast_f32_bf16": ([_P, _P, _I64, _P], _I),
+    "esm_cast_bf16_f32": ([_P, _P, _I64, _P], _I),
+    "esm_comm_version": ([], _I),
+    "esm_comm_unique_id": ([_P], _I),
+    "esm_comm_init": ([_P, _I, _I, _P], _I),
+    "esm_comm_destroy": ([_P], _I),
+    "esm_comm_allreduce": ([_P, _P, _I64, _I, _P], _I),
+    "esm_comm_reduce_scatter": ([_P, _P, _I64, _I, _P], _I),
+    "esm_comm_allgather": ([_P, _P, _I64, _I, _P], _I),
 }
 
 _lib = None

@@ -862,7 +862,17 @@ __global__ void __launch_bounds__(256) xent_dE_kernel(const T* __restrict__ n, c
 // ============================================================================
 // fused AdamW over the flat fp32 parameter buffer (+ bf16 shadow refresh)
 // ============================================================================
-__global__ void __launch_bounds__(256) adamw_kernel(float* __restrict__ p, const float* __restrict__ g,
+// grads as fp32 (local / fp32 buckets) or bf16 (bf16-reduced data-parallel buckets)
+__device__ __forceinline__ float4 load_grad4(const float* g, int64_t i) { return reinterpret_cast<const float4*>(g)[i]; }
+__device__ __forceinline__ float4 load_grad4(const __nv_bfloat16* g, int64_t i) {
+  const uint2 u = reinterpret_cast<const uint2*>(g)[i];
+  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+  const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+
+template <typename GT>
+__global__ void __launch_bounds__(256) adamw_kernel(float* __restrict__ p, const GT* __restrict__ g,
                                                     float* __restrict__ m, float* __restrict__ v,
                                                     __nv_bfloat16* __restrict__ p16,
                                                     const uint8_t* __restrict__ decay, int64_t n,
@@ -876,7 +886,7 @@ __global__ void __launch_bounds__(256) adamw_kernel(float* __restrict__ p, const
     const int64_t e = i << 2;
     const float dec = decay[e >> 8] ? (1.0f - lr * wd) : 1.0f;
     float4 pp = reinterpret_cast<float4*>(p)[i];
-    const float4 gg = reinterpret_cast<const float4*>(g)[i];
+    const float4 gg = load_grad4(g, i);
     float4 mm = reinterpret_cast<float4*>(m)[i];
     float4 vv = reinterpret_cast<float4*>(v)[i];
     float* P = &pp.x;
@@ -906,8 +916,23 @@ __global__ void __launch_bounds__(256) adamw_kernel(float* __restrict__ p, const
 }
 
 __global__ void cast_kernel(const float* __restrict__ s, __nv_bfloat16* __restrict__ d, int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+  const int64_t n4 = n >> 2;  // 16-byte loads, 8-byte stores; n % 4 tail below
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 f = reinterpret_cast<const float4*>(s)[i];
+    __nv_bfloat162 lo = __floats2bfloat162_rn(f.x, f.y), hi = __floats2bfloat162_rn(f.z, f.w);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&lo);
+    u.y = *reinterpret_cast<uint32_t*>(&hi);
+    reinterpret_cast<uint2*>(d)[i] = u;
+  }
+  for (int64_t i = (n4 << 2) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
     d[i] = __float2bfloat16_rn(s[i]);
+}
+
+__global__ void cast_bf16_f32_kernel(const __nv_bfloat16* __restrict__ s, float* __restrict__ d, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    d[i] = __bfloat162float(s[i]);
 }
 
 static int grid_for(int64_t work, int block, int cap = device_sm_count() * 16) {
@@ -1258,15 +1283,31 @@ int esm_lmhead_xent(int dtype, const void* n, const void* E, const float* bias, 
 int esm_adamw(float* p, const float* g, float* m, float* v, void* p16, const uint8_t* decay_chunk, int64_t n,
               const float* hyper, esm_stream_t stream) {
   ESM_CHECK_ARG(p && g && m && v && decay_chunk && hyper && n % 256 == 0, "esm_adamw: bad args (n %% 256 == 0)");
-  adamw_kernel<<<grid_for(n / 4, 256, device_sm_count() * 8), 256, 0, S(stream)>>>(p, g, m, v, (__nv_bfloat16*)p16, decay_chunk, n,
-                                                                     hyper);
+  adamw_kernel<float><<<grid_for(n / 4, 256, device_sm_count() * 8), 256, 0, S(stream)>>>(
+      p, g, m, v, (__nv_bfloat16*)p16, decay_chunk, n, hyper);
+  ESM_LAUNCH_RET();
+}
+
+int esm_adamw_bf16g(float* p, const void* g, float* m, float* v, void* p16, const uint8_t* decay_chunk, int64_t n,
+                    const float* hyper, esm_stream_t stream) {
+  ESM_CHECK_ARG(p && g && m && v && decay_chunk && hyper && n % 256 == 0, "esm_adamw_bf16g: bad args (n %% 256 == 0)");
+  adamw_kernel<__nv_bfloat16><<<grid_for(n / 4, 256, device_sm_count() * 8), 256, 0, S(stream)>>>(
+      p, (const __nv_bfloat16*)g, m, v, (__nv_bfloat16*)p16, decay_chunk, n, hyper);
   ESM_LAUNCH_RET();
 }
 
 int esm_cast_f32_bf16(const float* src, void* dst, int64_t n, esm_stream_t stream) {
-  ESM_CHECK_ARG(src && dst && n >= 0, "esm_cast: bad args");
+  ESM_CHECK_ARG(src && dst && n >= 0 && ((uintptr_t)src & 15) == 0 && ((uintptr_t)dst & 7) == 0,
+                "esm_cast_f32_bf16: bad args (src 16 B, dst 8 B aligned)");
   if (n == 0) return 0;
-  cast_kernel<<<grid_for(n, 256), 256, 0, S(stream)>>>(src, (__nv_bfloat16*)dst, n);
+  cast_kernel<<<grid_for(n / 4 + 1, 256, device_sm_count() * 8), 256, 0, S(stream)>>>(src, (__nv_bfloat16*)dst, n);
+  ESM_LAUNCH_RET();
+}
+
+int esm_cast_bf16_f32(const void* src, float* dst, int64_t n, esm_stream_t stream) {
+  ESM_CHECK_ARG(src && dst && n >= 0, "esm_cast_bf16_f32: bad args");
+  if (n == 0) return 0;
+  cast_bf16_f32_kernel<<<grid_for(n, 256), 256, 0, S(stream)>>>((const __nv_bfloat16*)src, dst, n);
   ESM_LAUNCH_RET();
 }
 

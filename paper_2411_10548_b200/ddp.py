@@ -1,86 +1,207 @@
-"""Data-parallel gradient exchange: bucketed all-reduce of the flat fp32 gradient buffer,
-overlapped with backward, plus the global masked-token count (loss normaliser).
+"""Data-parallel gradient exchange: bucketed collectives over the flat gradient buffer,
+overlapped with the backward, plus the global masked-token count (loss normaliser).
 
-Parameter groups are laid out in backward-completion order (model.param_groups), so a
-bucket is a contiguous slice of ``store.g32``.  The model calls ``ready(group_key)`` as soon
-as all groups up to that key are final; every bucket fully covered is launched right away
-on a dedicated communication stream (NCCL over NVLink / NVSwitch through torch.distributed),
-while the compute stream continues with the next layer's backward.  With ``on_bucket`` set (the
-model's overlapped optimizer), the AdamW update of each bucket is issued on the communication stream
-right behind its all-reduce, so the optimizer also overlaps the remaining backward.  ``end_backward``
-makes the compute stream wait on the outstanding collectives (and updates).
+Parameter groups are laid out in backward-completion order (model.param_groups), so a bucket is a contiguous
+slice of ``store.g32``.  The model calls ``ready(group_key)`` as soon as all groups up to that key hold final
+gradients; every bucket fully covered is launched right away on a dedicated communication stream while the
+compute stream continues with the next layer's backward.  Two modes:
 
-Loss normalisation: the masked-token count is all-reduced before the loss kernel, every
-rank scales its gradients by 1 / N_global, and buckets are SUM-reduced -- the result equals
-the gradient of the mean loss over the concatenated global batch (one exchange step per
-optimizer step).  Works with the gloo backend on CPU tensors for tests.
+* ``shard_optimizer=False`` (DDP): in-place all-reduce of the bucket; the model's AdamW for the bucket
+  (``on_bucket``) follows on the communication stream.
+* ``shard_optimizer=True`` (ZeRO-1, the comparison point of PAPER.md:86-88): the bucket is reduce-scattered,
+  each rank runs AdamW only on its 1/N slice (its optimizer shard), and the updated fp32 master slice and bf16
+  shadow slice are all-gathered back into every rank's full buffers -- the AdamW work (and its HBM traffic) per
+  GPU drops by N while the bytes on the wire stay those of an fp32 all-reduce (fp32 bucket) or 3/4 of it
+  (bf16 bucket).
+
+``grad_dtype="bf16"`` casts each bucket to bf16 before the collective (half the NVLink bytes) and the
+optimizer reads the bf16 sums (``esm_adamw_bf16g``).
+
+Collectives go through the library's own NCCL communicator (``esm_comm_*`` in the C ABI, enqueued on our
+streams, so the whole DDP step can be captured in one CUDA graph); torch.distributed only carries the
+rendezvous (the NCCL unique id).  On CPU tensors (the gloo tests) the same bucket logic runs on
+torch.distributed collectives.
 """
 from __future__ import annotations
+
+import ctypes
 
 import torch
 import torch.distributed as dist
 
+from . import _lib
+
+ALIGN = 256  # elements (model.ALIGN): AdamW decay-mask chunk; every shard slice starts on a chunk
+
+
+class NcclComm:
+    """The library's NCCL communicator (esm_comm_*): rank 0 creates the unique id, torch.distributed
+    broadcasts it, every rank initialises its communicator.  In-place SUM collectives on a given stream."""
+
+    def __init__(self, group=None):
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        lib = _lib.load()
+        uid = (ctypes.c_uint8 * 128)()
+        if self.rank == 0:
+            _lib.check(lib.esm_comm_unique_id(uid), "esm_comm_unique_id")
+        obj = [bytes(uid)]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        uid = (ctypes.c_uint8 * 128).from_buffer_copy(obj[0])
+        handle = ctypes.c_void_p()
+        _lib.check(lib.esm_comm_init(uid, self.rank, self.world, ctypes.byref(handle)), "esm_comm_init")
+        self.handle = handle
+
+    @staticmethod
+    def _dt(t):
+        return {torch.float32: _lib.ESM_F32, torch.bfloat16: _lib.ESM_BF16, torch.int32: _lib.ESM_I32}[t.dtype]
+
+    def allreduce(self, t, stream):
+        _lib.call("esm_comm_allreduce", self.handle, t.data_ptr(), t.numel(), self._dt(t), stream)
+
+    def reduce_scatter(self, t, stream):
+        _lib.call("esm_comm_reduce_scatter", self.handle, t.data_ptr(), t.numel(), self._dt(t), stream)
+
+    def allgather(self, t, stream):
+        _lib.call("esm_comm_allgather", self.handle, t.data_ptr(), t.numel(), self._dt(t), stream)
+
+    def close(self):
+        if self.handle:
+            _lib.load().esm_comm_destroy(self.handle)
+            self.handle = None
+
+
+class TorchDistComm:
+    """The same in-place collectives on torch.distributed (gloo on CPU tensors: host-logic tests)."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def allreduce(self, t, stream=None):
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+
+    def reduce_scatter(self, t, stream=None):
+        s = t.clone()
+        dist.all_reduce(s, op=dist.ReduceOp.SUM, group=self.group)
+        n = t.numel() // self.world
+        t[self.rank * n:(self.rank + 1) * n].copy_(s[self.rank * n:(self.rank + 1) * n])
+
+    def allgather(self, t, stream=None):
+        n = t.numel() // self.world
+        parts = [torch.empty(n, dtype=t.dtype) for _ in range(self.world)]
+        dist.all_gather(parts, t[self.rank * n:(self.rank + 1) * n].clone(), group=self.group)
+        for r, p in enumerate(parts):
+            t[r * n:(r + 1) * n].copy_(p)
+
+    def close(self):
+        pass
+
 
 class GradAllReducer:
-    def __init__(self, store, bucket_bytes: int = 64 << 20, group=None):
+    def __init__(self, store, bucket_bytes: int = 64 << 20, group=None, grad_dtype: str = "fp32",
+                 shard_optimizer: bool = False, comm=None):
+        if grad_dtype not in ("fp32", "bf16"):
+            raise ValueError("grad_dtype must be 'fp32' or 'bf16'")
         self.store = store
         self.group = group
-        self.world = dist.get_world_size(group)
+        self.cuda = store.g32.is_cuda
+        self.comm = comm or (NcclComm(group) if self.cuda else TorchDistComm(group))
+        self.world, self.rank = self.comm.world, self.comm.rank
+        self.bf16 = grad_dtype == "bf16"
+        self.shard = shard_optimizer
+        unit = ALIGN * self.world  # every bucket splits into `world` slices of whole AdamW chunks
+        if store.numel % unit:
+            raise ValueError(f"parameter buffer ({store.numel}) is not a multiple of {unit} elements")
         keys = [k for k, _ in store.groups]
-        self.bucket_ends = []  # element offsets (exclusive) of bucket ends, at group boundaries
+        esz = 2 if self.bf16 else 4
+        self.bucket_ends = []  # element offsets (exclusive) of bucket ends, at group ends rounded up to `unit`
         start = 0
         for k in keys:
-            a, b = store.group_range[k]
-            end = (b + 255) // 256 * 256
-            if (end - start) * 4 >= bucket_bytes:
+            end = min(store.numel, (store.group_range[k][1] + unit - 1) // unit * unit)
+            if (end - start) * esz >= bucket_bytes:
                 self.bucket_ends.append(end)
                 start = end
         if not self.bucket_ends or self.bucket_ends[-1] != store.numel:
             self.bucket_ends.append(store.numel)
+        self.unit = unit
         self.key_end = {k: store.group_range[k][1] for k in keys}
-        self.cuda = store.g32.is_cuda
         self.stream = torch.cuda.Stream(store.g32.device) if self.cuda else None
-        self._works = []
+        self.g16 = torch.empty(store.numel, dtype=torch.bfloat16, device=store.g32.device) if self.bf16 else None
         self._next = 0
         self._start = 0
-        self.on_bucket = None  # callable(start, end, stream) run after a bucket's all-reduce
+        # on_bucket(a, b, stream, grad): the optimizer for flat elements [a, b) -- the whole bucket (DDP) or this
+        # rank's slice of it (sharded) -- with `grad` the reduced gradients of [a, b) (fp32, or bf16 buckets)
+        self.on_bucket = None
 
-    # ---------------------------------------------------------------- loss normaliser
+    # ---------------------------------------------------------------- loss normaliser (compute stream)
+    def _cur(self):
+        return torch.cuda.current_stream(self.store.g32.device).cuda_stream if self.cuda else None
+
     def reduce_count(self, n_labels: torch.Tensor):
-        dist.all_reduce(n_labels, op=dist.ReduceOp.SUM, group=self.group)
+        self.comm.allreduce(n_labels, self._cur())
 
     def reduce_loss(self, loss_sum: torch.Tensor):
-        dist.all_reduce(loss_sum, op=dist.ReduceOp.SUM, group=self.group)
+        self.comm.allreduce(loss_sum, self._cur())
 
     # ---------------------------------------------------------------- buckets
+    def owned(self, a: int, b: int):
+        """This rank's optimizer slice of bucket [a, b) (sharded mode)."""
+        n = (b - a) // self.world
+        return a + self.rank * n, a + (self.rank + 1) * n
+
     def begin_backward(self):
-        self._works = []
         self._next = 0
         self._start = 0
 
+    def _cast(self, a, b, st, to_bf16: bool):
+        if self.cuda:
+            if to_bf16:
+                _lib.call("esm_cast_f32_bf16", self.store.g32[a:].data_ptr(), self.g16[a:].data_ptr(), b - a, st)
+            else:
+                _lib.call("esm_cast_bf16_f32", self.g16[a:].data_ptr(), self.store.g32[a:].data_ptr(), b - a, st)
+        elif to_bf16:
+            self.g16[a:b].copy_(self.store.g32[a:b])
+        else:
+            self.store.g32[a:b].copy_(self.g16[a:b])
+
     def _launch(self, end):
-        g = self.store.g32[self._start:end]
+        a, b = self._start, end
+        P = self.store
         if self.cuda:
             ev = torch.cuda.Event()
-            ev.record(torch.cuda.current_stream(g.device))
-            with torch.cuda.stream(self.stream):
-                self.stream.wait_event(ev)
-                w = dist.all_reduce(g, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
-                if self.on_bucket is not None:
-                    w.wait()  # the comm stream waits for the collective, then updates the bucket
-                    self.on_bucket(self._start, end, self.stream)
-                self._works.append(w)
+            ev.record(torch.cuda.current_stream(P.g32.device))
+            self.stream.wait_event(ev)
+            st = self.stream.cuda_stream
+            ctx = torch.cuda.stream(self.stream)
         else:
-            w = dist.all_reduce(g, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
-            if self.on_bucket is not None:
-                w.wait()
-                self.on_bucket(self._start, end, None)
-            self._works.append(w)
+            st, ctx = None, _Null()
+        with ctx:
+            if self.bf16:
+                self._cast(a, b, st, True)
+            gbuf = self.g16 if self.bf16 else P.g32
+            if self.shard:
+                self.comm.reduce_scatter(gbuf[a:b], st)
+                oa, ob = self.owned(a, b)
+                if self.on_bucket is not None:
+                    self.on_bucket(oa, ob, self.stream, gbuf[oa:ob])
+                    self.comm.allgather(P.p32[a:b], st)
+                    if P.p16 is not None:
+                        self.comm.allgather(P.p16[a:b], st)
+                elif self.bf16:
+                    self._cast(oa, ob, st, False)
+            else:
+                self.comm.allreduce(gbuf[a:b], st)
+                if self.on_bucket is not None:
+                    self.on_bucket(a, b, self.stream, gbuf[a:b])
+                elif self.bf16:
+                    self._cast(a, b, st, False)
         self._start = end
 
     def ready(self, key: str):
-        done = self.key_end[key]
-        while self._next < len(self.bucket_ends) and self.bucket_ends[self._next] <= ((done + 255) // 256 * 256):
+        done = (self.key_end[key] + ALIGN - 1) // ALIGN * ALIGN
+        while self._next < len(self.bucket_ends) and self.bucket_ends[self._next] <= done:
             self._launch(self.bucket_ends[self._next])
             self._next += 1
 
@@ -88,8 +209,13 @@ class GradAllReducer:
         while self._next < len(self.bucket_ends):
             self._launch(self.bucket_ends[self._next])
             self._next += 1
-        for w in self._works:
-            w.wait()  # compute stream waits for the collective (NCCL) / completes (gloo)
-        if self.cuda and self.on_bucket is not None:
+        if self.cuda:
             torch.cuda.current_stream(self.store.g32.device).wait_stream(self.stream)
-        self._works = []
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False

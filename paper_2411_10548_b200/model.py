@@ -40,6 +40,7 @@ from ._lib import (EPI_DGELU, EPI_F32_ACC, EPI_GELU, EPI_GELU_GRADAUX, EPI_MUL_A
 from .config import EsmConfig
 
 ALIGN = 256  # elements; also the AdamW weight-decay chunk size
+TOTAL_ALIGN = 8 * ALIGN  # the flat buffer splits into 1, 2, 4 or 8 data-parallel shards of whole chunks
 LARGE_VOCAB = 40  # esm_lmhead_xent's per-row fused head handles V <= 40; larger V uses the GEMM head
 
 
@@ -153,6 +154,9 @@ class ParamStore:
             self.group_range[key] = (start, end)
             d = 0 if _no_decay(members[0][0]) else 1
             decay += [d] * ((off - start) // ALIGN)
+        total = (off + TOTAL_ALIGN - 1) // TOTAL_ALIGN * TOTAL_ALIGN  # data-parallel shards: world | 8
+        decay += [0] * ((total - off) // ALIGN)
+        off = total
         self.numel = off
         self.device = device
         self.p32 = torch.zeros(off, dtype=torch.float32, device=device)
@@ -175,16 +179,47 @@ class _Layer:
     pass
 
 
-class Workspace:
-    """Activation / gradient buffers for one (B, S) shape; reused every step."""
+class _Arena:
+    """Bump allocator over one device buffer that backs the activation / scratch tensors of the workspaces of
+    every (B, S) shape.  Steps are stream-ordered (one shape's step runs at a time) and every step re-stages its
+    inputs, so bucketed variable-shape training caches many shapes -- each with its own CUDA graph -- in the
+    memory of the largest one.  ``buf=None`` only measures."""
 
-    def __init__(self, cfg: EsmConfig, B: int, S: int, act, device):
+    ALIGN = 1024  # bytes: TMA needs 16 B; 1 KB keeps every tensor on its own swizzle atom
+
+    def __init__(self, buf: torch.Tensor | None):
+        self.buf = buf
+        self.off = 0
+
+    def take(self, shape, dtype):
+        n = math.prod(shape) * torch.empty((), dtype=dtype).element_size()
+        off = (self.off + self.ALIGN - 1) // self.ALIGN * self.ALIGN
+        self.off = off + n
+        if self.buf is None:
+            return None
+        if self.off > self.buf.numel():
+            raise RuntimeError("activation arena too small for this workspace")
+        return self.buf[off:off + n].view(dtype).view(*shape)
+
+
+class Workspace:
+    """Activation / gradient buffers for one (B, S) shape; reused every step.
+
+    Inputs and per-shape constants (ids, masks, labels, counters, RoPE tables) are owned by the workspace;
+    activations and backward scratch live in ``arena`` (shared across shapes) when one is given."""
+
+    def __init__(self, cfg: EsmConfig, B: int, S: int, act, device, arena: _Arena | None = None):
         H, F, V, L, nh = cfg.hidden_size, cfg.intermediate_size, cfg.vocab_size, cfg.num_hidden_layers, \
             cfg.num_attention_heads
         dh = H // nh
         T = B * S
         self.B, self.S, self.T = B, S, T
-        e = lambda *shape, dt=act: torch.empty(*shape, dtype=dt, device=device)  # noqa: E731
+        self.arena_bytes = 0
+        if arena is not None:
+            arena.off = 0
+            e = lambda *shape, dt=act: arena.take(shape, dt)  # noqa: E731
+        else:
+            e = lambda *shape, dt=act: torch.empty(*shape, dtype=dt, device=device)  # noqa: E731
         f32, i32 = torch.float32, torch.int32
         self.ids = torch.zeros(B, S, dtype=i32, device=device)        # raw (unmasked) tokens
         self.input_ids = torch.zeros(B, S, dtype=i32, device=device)  # after MLM masking
@@ -247,6 +282,15 @@ class Workspace:
         cos, sin = rope_tables(S, dh)
         self.cos = torch.from_numpy(cos).to(device)
         self.sin = torch.from_numpy(sin).to(device)
+        if arena is not None:
+            self.arena_bytes = arena.off
+
+    @staticmethod
+    def activation_bytes(cfg: EsmConfig, B: int, S: int, act) -> int:
+        """Arena bytes the workspace of shape (B, S) needs (measuring pass, no device allocation of them)."""
+        a = _Arena(None)
+        Workspace(cfg, B, S, act, "cpu", arena=a)
+        return a.off
 
 
 class EsmForMaskedLM:
@@ -278,7 +322,8 @@ class EsmForMaskedLM:
         self.grad_scale = 1.0
         self.ws: Workspace | None = None
         self._ws_cache: dict = {}
-        self.max_workspaces = 3
+        self._arena: torch.Tensor | None = None  # activation arena shared by the cached workspaces
+        self.max_workspaces = 32  # cached (B, S) shapes (small: inputs, constants, CUDA graph)
         self.comm = None  # set by ddp.GradAllReducer
         self.timer = None  # optional KernelTimer (bench.py per-kernel roofline)
         self._opt_on, self._opt_start, self._opt_stream = False, 0, None
@@ -337,22 +382,36 @@ class EsmForMaskedLM:
         if key in cache:
             cache[key] = cache.pop(key)  # most recently used
         else:
+            self.reserve(B, S)
             while len(cache) >= self.max_workspaces:
                 old_key = next(iter(cache))
                 old = cache.pop(old_key)
                 if self.ws is old:
                     self.ws = None
                 del old
-                torch.cuda.empty_cache()
-            cache[key] = Workspace(self.config, B, S, self.act, self.device)
+            cache[key] = Workspace(self.config, B, S, self.act, self.device, arena=_Arena(self._arena))
         self.ws = cache[key]
         return self.ws
 
-    def release_workspaces(self):
-        """Free every cached activation workspace (and its CUDA graph)."""
+    def reserve(self, B: int, S: int):
+        """Grow the shared activation arena to hold a (B, S) workspace.  Growing drops the cached workspaces
+        (their CUDA graphs point into the old arena); reserving the largest bucket shape up front avoids that."""
+        need = Workspace.activation_bytes(self.config, B, S, self.act)
+        if self._arena is not None and self._arena.numel() >= need:
+            return
         self._ws_cache.clear()
         self.ws = None
         self.graph = None
+        self._arena = None
+        torch.cuda.empty_cache()
+        self._arena = torch.empty(need, dtype=torch.uint8, device=self.device)
+
+    def release_workspaces(self):
+        """Free every cached activation workspace (and its CUDA graph) and the activation arena."""
+        self._ws_cache.clear()
+        self.ws = None
+        self.graph = None
+        self._arena = None
         torch.cuda.empty_cache()
 
     # kernels launched per C-ABI entry point (for the bench's gpu_launches count)
@@ -685,16 +744,23 @@ class EsmForMaskedLM:
                 self._opt_stream.wait_event(ev)
                 self._adamw_range(self._opt_start, end, self._opt_stream)
 
-    def _adamw_range(self, a: int, b: int, stream):
-        """AdamW on flat elements [a, b) (a, b multiples of 256) on ``stream`` (None: current)."""
+    def _adamw_range(self, a: int, b: int, stream, grad: torch.Tensor | None = None):
+        """AdamW on flat elements [a, b) (a, b multiples of 256) on ``stream`` (None: current).  ``grad``: the
+        gradients of [a, b) when they are not ``g32[a:b]`` (bf16-reduced data-parallel buckets)."""
         b = min(b, self.store.numel)
         if b <= a:
             return
         P = self.store
         st = stream.cuda_stream if stream is not None else self._stream()
-        self._call("esm_adamw", P.p32[a:].data_ptr(), P.g32[a:].data_ptr(), P.m[a:].data_ptr(), P.v[a:].data_ptr(),
-                   P.p16[a:].data_ptr() if P.p16 is not None else None, P.decay[a // ALIGN:].data_ptr(), b - a,
-                   self.hyper.data_ptr(), st, nbytes=30.0 * (b - a))
+        p16 = P.p16[a:].data_ptr() if P.p16 is not None else None
+        if grad is not None and grad.dtype == torch.bfloat16:
+            self._call("esm_adamw_bf16g", P.p32[a:].data_ptr(), grad.data_ptr(), P.m[a:].data_ptr(),
+                       P.v[a:].data_ptr(), p16, P.decay[a // ALIGN:].data_ptr(), b - a, self.hyper.data_ptr(), st,
+                       nbytes=28.0 * (b - a))
+        else:
+            g = grad.data_ptr() if grad is not None else P.g32[a:].data_ptr()
+            self._call("esm_adamw", P.p32[a:].data_ptr(), g, P.m[a:].data_ptr(), P.v[a:].data_ptr(), p16,
+                       P.decay[a // ALIGN:].data_ptr(), b - a, self.hyper.data_ptr(), st, nbytes=30.0 * (b - a))
         self._opt_start = b
 
     def _adamw(self):
@@ -705,6 +771,8 @@ class EsmForMaskedLM:
 
     def optimizer_step(self, lr=None):
         """AdamW over all parameters after a separate ``forward_backward`` (un-overlapped)."""
+        if self.comm is not None and (self.comm.shard or self.comm.bf16):
+            raise RuntimeError("sharded / bf16-bucket data parallelism updates inside the step: use step()")
         self.step_count += 1
         self.set_hyper(lr=lr, step=self.step_count)
         self._adamw()
@@ -722,8 +790,8 @@ class EsmForMaskedLM:
         Inputs (input_ids / labels / am / n_labels) and hyper-parameters are read from their
         static device buffers at replay; masking and H2D copies stay outside the graph."""
         ws = ws or self.ws
-        if self.comm is not None:
-            raise RuntimeError("CUDA-graph capture is single-process only (NCCL buckets run eagerly)")
+        if self.comm is not None and not self.comm.cuda:
+            raise RuntimeError("CUDA-graph capture needs the NCCL communicator (CUDA tensors)")
         s = torch.cuda.Stream(self.device)
         s.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(s):
@@ -732,7 +800,9 @@ class EsmForMaskedLM:
         torch.cuda.synchronize(self.device)
         g = torch.cuda.CUDAGraph()
         n0 = self.launches
-        with torch.cuda.graph(g):
+        # NCCL collectives (data parallel) are captured too; thread-local capture mode lets NCCL's host-side
+        # bookkeeping run during capture
+        with torch.cuda.graph(g, capture_error_mode="thread_local" if self.comm is not None else "global"):
             self.forward_backward(ws, optimizer=True)
         ws.graph = g
         ws.graph_launches = self.launches - n0
@@ -762,7 +832,7 @@ class EsmForMaskedLM:
         ws.ids.copy_(torch.from_numpy(ids), non_blocking=True)
         ws.am.copy_(torch.from_numpy(am), non_blocking=True)
         self.mlm_mask(ws.ids, seed, stream_id, ws)
-        if use_graph and self.comm is None:
+        if use_graph:
             if getattr(ws, "graph", None) is None:
                 self.capture(ws)
             return self.graph_step(lr=lr, ws=ws)

@@ -169,20 +169,26 @@ def test_large_vocab_fp32_matches_oracle():
 
 
 def test_geneformer_geometry_bf16_matches_oracle():
-    """Full Geneformer head (V = 25,426, H = 768, dh = 64) in bf16 vs the fp64 oracle."""
+    """BASELINE configs[4] geometry at its sequence length: full Geneformer head (V = 25,426, H = 768, 12 heads
+    of 64), S = 2048 (the reference tokenizer's max_len), one full and one ragged rank-token row, production bf16
+    kernels vs the fp64 oracle; achieved errors printed."""
+    from test_gpu_model import _gate
     cfg, ocfg = _gf_cfgs(25424, 768, 1, 12, 3072)
     params = init_params(cfg, seed=7)
-    inp, am, lab = _gf_batch(cfg.vocab_size, 2, 256, [256, 190], seed=3)
+    inp, am, lab = _gf_batch(cfg.vocab_size, 2, 2048, [2048, 1391], seed=3)
     ref = O.forward_backward(ocfg, params, inp, am, lab, dtype=np.float64)
     m = EsmForMaskedLM(cfg, dtype="bf16", device="cuda", params=params)
     ws = m.set_batch(torch.from_numpy(inp).cuda(), torch.from_numpy(am).cuda(), torch.from_numpy(lab).cuda())
     loss = float(m.forward_backward(ws).item())
     assert abs(loss - ref.loss) / ref.loss < 1e-2
     grads = m.grads()
+    fro = {}
     for k, g in ref.grads.items():
         gg = grads[k].cpu().numpy().astype(np.float64)
-        fro = np.linalg.norm(gg - g) / (np.linalg.norm(g) + 1e-30)
-        assert fro < 0.08, (k, fro)
+        fro[k] = float(np.linalg.norm(gg - g) / (np.linalg.norm(g) + 1e-30))
+    worst = max(fro, key=lambda k: fro[k] / _gate(k))
+    print(f"Geneformer S=2048 bf16: loss rel {abs(loss - ref.loss) / ref.loss:.2e}; worst grad {worst} {fro[worst]:.3e}")
+    assert fro[worst] < _gate(worst), (worst, fro[worst])
 
 
 def test_geneformer_train_steps_fp32_match_oracle_trainer():

@@ -15,6 +15,17 @@ from paper_2411_10548_b200 import EsmConfig
 from paper_2411_10548_b200.model import EsmForMaskedLM, init_params
 
 pytestmark = pytest.mark.gpu
+# bf16 gradient gate (relative Frobenius error vs the fp64 oracle): activations and GEMM operands are rounded to
+# bf16 (unit roundoff 2^-9 = 0.2 %) at every layer boundary, so gradients carry a few roundings' worth of
+# error; measured worst cases are printed by the tests (DESIGN.md §1 lists them).
+BF16_GRAD_FRO = 0.03
+# ... except the key bias: its gradient is a near-cancelling sum (a constant shift of one query's scores does not
+# change its softmax; only RoPE's position dependence leaves a small remainder), so its relative error is larger.
+BF16_KEY_BIAS_FRO = 0.08
+
+
+def _gate(name):
+    return BF16_KEY_BIAS_FRO if name.endswith("attention.self.key.bias") else BF16_GRAD_FRO
 GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "hf_*.npz")))
 
 
@@ -87,11 +98,14 @@ def test_bf16_matches_oracle(H, L, nh, F, B, S, lens):
     m16, _, loss16 = _run(cfg, params, inp, am, lab, "bf16")
     assert abs(loss16 - ref.loss) / ref.loss < 1e-2
     g16 = m16.grads()
+    fro = {}
     for k, g in ref.grads.items():
         # bf16 activations/operands: compare the whole tensor by relative Frobenius error
         gg = g16[k].cpu().numpy().astype(np.float64)
-        fro = np.linalg.norm(gg - g) / (np.linalg.norm(g) + 1e-30)
-        assert fro < 0.08, (k, fro)
+        fro[k] = float(np.linalg.norm(gg - g) / (np.linalg.norm(g) + 1e-30))
+    worst = max(fro, key=lambda k: fro[k] / _gate(k))
+    print(f"bf16 H={H} L={L}: loss rel {abs(loss16 - ref.loss) / ref.loss:.2e}; worst grad {worst} {fro[worst]:.3e}")
+    assert fro[worst] < _gate(worst), (worst, fro[worst])
 
 
 def test_device_masking_pipeline_matches_oracle():
@@ -191,3 +205,69 @@ def test_collect_peak_alloc_seam_workload_and_meter():
     assert peaks[0] < peaks[1] < peaks[2]
     assert np.allclose(feats[1], [4 * 250, 4 * 250 ** 2])
     assert m.step_count == 3
+
+
+def _acts_and_grads_errors(m, ws, ref, B, S, H, L, keep):
+    """Max-abs relative errors of every per-layer activation and every parameter gradient vs the oracle."""
+    errs = {}
+    for l in range(L):
+        a, ly = ref.acts[l], ws.layers[l]
+        errs[f"x{l}"] = _relerr(ws.x[l].float().cpu().numpy().reshape(B, S, H)[keep], ref.hidden_states[l][keep])
+        for name in ("h1", "o", "x1", "h2", "z", "a"):
+            errs[f"{name}{l}"] = _relerr(getattr(ly, name).float().cpu().numpy().reshape(B, S, -1)[keep],
+                                         a[name][keep])
+        for name in ("q", "k", "v"):
+            errs[f"{name}{l}"] = _relerr(getattr(ly, name).float().cpu().numpy().transpose(0, 2, 1, 3)[keep],
+                                         a[name].transpose(0, 2, 1, 3)[keep])
+    grads = m.grads()
+    for k, g in ref.grads.items():
+        errs[k] = _relerr(grads[k].cpu().numpy(), g)
+    return errs
+
+
+def test_fp32_config0_full_size_per_layer():
+    """BASELINE configs[0] at full size -- ESM-2 8M (6 layers, H 320, 20 heads), batch 8 x 512 -- in fp32 parity
+    mode: every per-layer activation and every parameter gradient within 1e-4 (max-abs relative) of the fp64
+    oracle on the same seeded batch and masks (north-star bar).  Achieved errors are printed."""
+    H, L, nh, F, B, S = 320, 6, 20, 1280, 8, 512
+    cfg, ocfg = _cfgs(H, L, nh, F)
+    params = init_params(cfg, seed=1)
+    ids, am = O.synthetic_batch(B, S, seed=10_001)
+    am[5, 400:] = 0  # one ragged row (right padding) as the reference's bucketed batches produce
+    ids[5, 400:] = O.PAD
+    inp, lab = O.mlm_mask(ids, seed=3, stream=1)
+    ref = O.forward_backward(ocfg, params, inp, am, lab, dtype=np.float64, keep_acts=True)
+    m, ws, loss = _run(cfg, params, inp, am, lab, "fp32")
+    errs = _acts_and_grads_errors(m, ws, ref, B, S, H, L, am.astype(bool))
+    worst = max(errs, key=errs.get)
+    print(f"configs[0] fp32: loss rel {abs(loss - ref.loss) / ref.loss:.2e}; worst {worst} {errs[worst]:.2e}")
+    assert abs(loss - ref.loss) / ref.loss < 1e-5
+    assert errs[worst] < 1e-4, (worst, errs[worst])
+
+
+def _bf16_case(H, L, nh, F, B, S, lens, seed=5):
+    cfg, ocfg = _cfgs(H, L, nh, F)
+    params = init_params(cfg, seed=seed)
+    rng = np.random.default_rng(0)
+    toks = [np.concatenate([[O.CLS], rng.integers(4, 24, n - 2), [O.EOS]]).astype(np.int32) for n in lens]
+    ids, am = O.pad_batch(toks, S)
+    inp, lab = O.mlm_mask(ids, seed=3, stream=1)
+    ref = O.forward_backward(ocfg, params, inp, am, lab, dtype=np.float64)
+    m16, _, loss16 = _run(cfg, params, inp, am, lab, "bf16")
+    g16 = m16.grads()
+    fro = {}
+    for k, g in ref.grads.items():
+        gg = g16[k].cpu().numpy().astype(np.float64)
+        fro[k] = float(np.linalg.norm(gg - g) / (np.linalg.norm(g) + 1e-30))
+    return abs(loss16 - ref.loss) / ref.loss, fro
+
+
+def test_bf16_3b_geometry_layer():
+    """BASELINE configs[3] layer geometry: ESM-2 3B (H 2560, 40 heads of 64, F 10240) -- one encoder layer
+    + LM head, 2 x 256 ragged tokens, production bf16 kernels (tcgen05 GEMMs incl. CTA pairs at K = 10240,
+    persistent attention) vs the fp64 oracle."""
+    dl, fro = _bf16_case(2560, 1, 40, 10240, 2, 256, [256, 201])
+    worst = max(fro, key=lambda k: fro[k] / _gate(k))
+    print(f"3B layer bf16: loss rel {dl:.2e}; worst grad rel-Frobenius {worst} {fro[worst]:.3e}")
+    assert dl < 1e-2
+    assert fro[worst] < _gate(worst), (worst, fro[worst])

@@ -30,6 +30,8 @@ def test_library_exports_every_declared_symbol():
         assert hasattr(lib, name), name
     assert declared == set(_lib.EXPORTS)
     assert lib.esm_version() >= 10000
+    # the collectives resolve NCCL at run time (no GPU needed to load it): torch's 2.28 or the system's 2.27
+    assert lib.esm_comm_version() >= 22700
 
 
 def test_native_tokenizer_matches_oracle():
@@ -144,7 +146,7 @@ def _ddp_worker(rank, world, port, q):
         # buffer) only after its all-reduce has completed
         seen = []
         want2 = 2 * torch.arange(st.numel, dtype=torch.float32) * world
-        red.on_bucket = lambda a, b, stream: seen.append((a, b, bool(torch.equal(st.g32[a:b], want2[a:b]))))
+        red.on_bucket = lambda a, b, stream, g: seen.append((a, b, bool(torch.equal(g, want2[a:b]))))
         st.g32.copy_(g)
         st.g32.mul_(2)
         st.g32.div_(rank + 1)  # every rank holds 2 * arange -> reduced = 2 * arange * world
@@ -160,6 +162,66 @@ def _ddp_worker(rank, world, port, q):
         q.put((rank, ok_grad and hooks_ok, int(n.item()), len(red.bucket_ends)))
     finally:
         dist.destroy_process_group()
+
+
+def _zero1_worker(rank, world, port, q):
+    """Sharded optimizer (reduce-scatter -> update of the rank's slice -> all-gather of p32 / p16) gives bit-for-bit
+    the parameters of the all-reduce path with the same update applied to every bucket; bf16 buckets give
+    the bf16-rounded sums.  The update is an elementwise SGD stand-in for AdamW (the GPU kernel is not
+    available on CPU); the bucket / slice / gather bookkeeping is what is under test."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2411_10548_b200.ddp import GradAllReducer
+        cfg = EsmConfig(hidden_size=64, num_hidden_layers=3, num_attention_heads=4, intermediate_size=256)
+        results = {}
+        for mode in ("ddp", "zero1", "zero1_bf16", "ddp_bf16"):
+            st = ParamStore(cfg, "cpu", shadow=True)
+            torch.manual_seed(0)
+            st.p32.copy_(torch.randn(st.numel))
+            st.p16.copy_(st.p32)
+            red = GradAllReducer(st, bucket_bytes=32 << 10, shard_optimizer=mode.startswith("zero1"),
+                                 grad_dtype="bf16" if mode.endswith("bf16") else "fp32")
+            calls = []
+
+            def upd(a, b, stream, g, st=st, calls=calls):
+                calls.append((a, b))
+                st.p32[a:b] -= 0.1 * g.float()
+                st.p16[a:b].copy_(st.p32[a:b])
+
+            red.on_bucket = upd
+            for step in range(2):
+                torch.manual_seed(100 + 10 * step + rank)
+                st.g32.copy_(torch.randn(st.numel))
+                red.begin_backward()
+                red.ready("esm.encoder.emb_layer_norm_after.bias")
+                for l in reversed(range(cfg.num_hidden_layers)):
+                    red.ready(f"esm.encoder.layer.{l}.attention.LayerNorm.bias")
+                red.end_backward()
+            owned = sum(b - a for a, b in calls) // 2
+            results[mode] = (st.p32.clone(), st.p16.clone(), owned, st.numel)
+        ddp, z1 = results["ddp"], results["zero1"]
+        ok = torch.equal(ddp[0], z1[0]) and torch.equal(ddp[1], z1[1])
+        ok = ok and z1[2] * world == z1[3] and ddp[2] == ddp[3]  # each rank updated exactly 1/world of the buffer
+        zb, db = results["zero1_bf16"], results["ddp_bf16"]
+        ok = ok and torch.equal(zb[0], db[0]) and (zb[0] - ddp[0]).abs().max().item() < 0.05
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_optimizer_matches_allreduce_gloo_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_zero1_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok in res), res
 
 
 def test_grad_bucket_allreduce_gloo_world2():
@@ -269,3 +331,29 @@ def test_reference_bindings_batches_feed_collate_indices(tmp_path):
             want = ds[i][0]
             assert ids[j, :len(want)].tolist() == want and am[j].sum() == len(want)
             assert (ids[j, len(want):] == 0).all()
+
+
+def test_workspace_arena_packs_activations_without_overlap():
+    """Variable-shape training keeps one activation arena for all (B, S) workspaces: each workspace's
+    activation / scratch tensors are disjoint 1 KB-aligned views of the arena, sized by activation_bytes, and
+    the per-shape inputs / constants are separate allocations."""
+    import torch
+    from paper_2411_10548_b200 import EsmConfig
+    from paper_2411_10548_b200.model import Workspace, _Arena
+    cfg = EsmConfig(hidden_size=64, num_hidden_layers=2, num_attention_heads=4, intermediate_size=256)
+    sizes = {shape: Workspace.activation_bytes(cfg, *shape, torch.bfloat16) for shape in [(4, 64), (2, 128), (8, 32)]}
+    assert len(set(sizes.values())) <= 3 and min(sizes.values()) > 0
+    buf = torch.empty(max(sizes.values()), dtype=torch.uint8)
+    lo, hi = buf.data_ptr(), buf.data_ptr() + buf.numel()
+    for shape in sizes:
+        ws = Workspace(cfg, *shape, torch.bfloat16, "cpu", arena=_Arena(buf))
+        assert ws.arena_bytes == sizes[shape]
+        spans = []
+        for t in [*ws.x, ws.dq, ws.dqkv, ws.delta, ws.dz, ws.row_scale, *(ly.z for ly in ws.layers)]:
+            a = t.data_ptr()
+            assert lo <= a and a + t.numel() * t.element_size() <= hi and (a - lo) % 1024 == 0
+            spans.append((a, a + t.numel() * t.element_size()))
+        spans.sort()
+        assert all(b0 <= a1 for (_, b0), (a1, _) in zip(spans, spans[1:]))
+        for t in (ws.ids, ws.am, ws.labels, ws.attn_sched, ws.cos):
+            assert not (lo <= t.data_ptr() < hi)
