@@ -55,6 +55,19 @@ enum {
   ESM_EPI_MUL_AUX = 8       /* C = acc * G (G = aux_in, e.g. gelu'(Z) from GELU_GRADAUX); colsum(C) -> col_sum (bf16) */
 };
 
+/* Hidden dropout (HF EsmSelfOutput / EsmOutput, HF:modeling_esm.py:369-375, 421-427): counter-based keep mask,
+ * regenerated in the backward instead of stored.  For element (row r, column c) of a call site:
+ *   k0 = lo32(seed) ^ h(2*site+1),  k1 = hi32(seed) ^ h(2*site+2),  h = lowbias32
+ *   u  = h(h(r * 0x9E3779B1 ^ k0) ^ ((c >> 1) + k1));  bits = c odd ? u >> 16 : u & 0xFFFF
+ *   keep = bits >= threshold   (threshold = round(p * 65536));  kept values are scaled by `scale` = 1/(1-p).
+ * Bit-exact with oracle/esm2_oracle.py:dropout_keep. */
+typedef struct esm_dropout {
+  const uint64_t* seed; /* device pointer, per-step seed (read at run time: CUDA-graph safe); NULL = off */
+  uint32_t site;        /* call site: 2*layer + 0 (attention output) / 1 (FFN output) */
+  uint32_t threshold;   /* 0 = off */
+  float scale;
+} esm_dropout;
+
 typedef struct esm_gemm_args {
   int dtype;                 /* ESM_F32 / ESM_BF16: dtype of A, B and activation outputs        */
   int M, N, K;               /* C[M,N] = A[M,K] · B[N,K]ᵀ                                        */
@@ -77,6 +90,8 @@ typedef struct esm_gemm_args {
   const float* row_mean;     /* [M] */
   const float* row_rstd;     /* [M] */
   float* col_sum2;           /* [N] */
+  /* ESM_EPI_RESID only: C = R + dropout(acc + bias) */
+  esm_dropout drop;
 } esm_gemm_args;
 
 /* ---------------- library ---------------- */
@@ -122,10 +137,16 @@ int esm_embed_bwd(int dtype, const int32_t* ids, const int32_t* am, const float*
 /* ---------------- LayerNorm (nn.LayerNorm, eps) ---------------- */
 int esm_layernorm_fwd(int dtype, const void* x, const float* gamma, const float* beta, void* y, float* mean,
                       float* rstd, int rows, int H, float eps, esm_stream_t stream);
-/* dx = LNᵀ(dy) [+ dres]; optional: dx *= gelu'(gelu_z) (LM head), dgamma/dbeta += , col_sum += colsum(dx). */
+/* dx = LNᵀ(dy) [+ dres]; optional: dx *= gelu'(gelu_z) (LM head), dgamma/dbeta += , col_sum += colsum(dx).
+ * With drop (threshold > 0) and dx_drop: dx_drop = dx * keep * scale -- the gradient of the dropped-out branch
+ * whose output fed this LayerNorm's input residual sum -- and col_sum accumulates colsum(dx_drop) (that branch's
+ * bias gradient). */
 int esm_layernorm_bwd(int dtype, const void* dy, const void* x, const float* gamma, const float* mean,
                       const float* rstd, const void* dres, const void* gelu_z, void* dx, float* dgamma,
-                      float* dbeta, float* col_sum, int rows, int H, esm_stream_t stream);
+                      float* dbeta, float* col_sum, int rows, int H, const esm_dropout* drop, void* dx_drop,
+                      esm_stream_t stream);
+/* out[r * cols + c] = keep(r, c) (uint8) -- the dropout mask of a call site, for tests. */
+int esm_dropout_mask(const esm_dropout* drop, int64_t rows, int cols, uint8_t* out, esm_stream_t stream);
 
 /* ---------------- linear layers ---------------- */
 int esm_gemm(const esm_gemm_args* args, esm_stream_t stream);

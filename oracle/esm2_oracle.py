@@ -297,13 +297,54 @@ def _linear(x, w, b=None):
     return y if b is None else y + b
 
 
+# --------------------------------------------------------------------------
+# Hidden dropout (HF EsmSelfOutput / EsmOutput: dropout(dense(x)) before the residual add,
+# HF:modeling_esm.py:369-375, 421-427) with a counter-based keep mask, so the B200 path regenerates
+# it in the backward instead of storing it.  Restates include/esm2_b200.h:esm_dropout bit for bit.
+# --------------------------------------------------------------------------
+def _lowbias32(x):
+    x = np.asarray(x, dtype=np.uint32)
+    with np.errstate(over="ignore"):
+        x = x ^ (x >> np.uint32(16))
+        x = (x * np.uint32(0x7FEB352D)).astype(np.uint32)
+        x = x ^ (x >> np.uint32(15))
+        x = (x * np.uint32(0x846CA68B)).astype(np.uint32)
+        x = x ^ (x >> np.uint32(16))
+    return x
+
+
+def dropout_threshold(p: float) -> int:
+    """16-bit keep threshold: a draw u16 is kept iff u16 >= round(p * 65536)."""
+    return int(round(p * 65536.0))
+
+
+def dropout_keep(seed: int, site: int, rows: int, cols: int, p: float) -> np.ndarray:
+    """bool [rows, cols] keep mask of call site ``site`` (2*layer + 0 attention output / 1 FFN output)."""
+    thr = np.uint32(dropout_threshold(p))
+    seed = int(seed) & 0xFFFFFFFFFFFFFFFF
+    k0 = np.uint32(seed & 0xFFFFFFFF) ^ _lowbias32(np.uint32(2 * site + 1))
+    k1 = np.uint32(seed >> 32) ^ _lowbias32(np.uint32(2 * site + 2))
+    r = np.arange(rows, dtype=np.uint32)
+    with np.errstate(over="ignore"):
+        rh = _lowbias32((r * np.uint32(0x9E3779B1)).astype(np.uint32) ^ k0)
+        pair = np.arange((cols + 1) // 2, dtype=np.uint32)
+        u = _lowbias32(rh[:, None] ^ (pair[None, :] + k1).astype(np.uint32))
+    bits = np.empty((rows, 2 * pair.size), dtype=np.uint32)
+    bits[:, 0::2] = u & np.uint32(0xFFFF)
+    bits[:, 1::2] = u >> np.uint32(16)
+    return bits[:, :cols] >= thr
+
+
 def forward_backward(cfg: OracleConfig, params: dict, input_ids: np.ndarray, attention_mask: np.ndarray,
                      labels: np.ndarray, dtype=np.float64, want_grads: bool = True,
-                     keep_acts: bool = False, loss_denominator: float | None = None) -> StepResult:
+                     keep_acts: bool = False, loss_denominator: float | None = None,
+                     hidden_dropout: tuple | None = None) -> StepResult:
     """One EsmForMaskedLM forward (+ backward) on CPU in ``dtype``.
 
     ``loss_denominator`` overrides the masked-token count used for the mean (the
     data-parallel global count); default = local count, as HF CrossEntropyLoss.
+    ``hidden_dropout`` = (seed, p): training-mode hidden dropout with the counter-based masks of
+    ``dropout_keep`` (kept values scaled by 1 / (1 - p), as nn.Dropout).
     """
     P = {k: np.asarray(v, dtype=dtype) for k, v in params.items()}
     B, S = input_ids.shape
@@ -335,6 +376,13 @@ def forward_backward(cfg: OracleConfig, params: dict, input_ids: np.ndarray, att
 
     res = StepResult(loss=0.0, n_masked=0)
     caches = []
+
+    def drop_mask(site):  # [B, S, H] multiplier (keep / (1 - p)), or None
+        if hidden_dropout is None or hidden_dropout[1] <= 0.0:
+            return None
+        seed, pd = hidden_dropout
+        keep = dropout_keep(seed, site, B * S, H, pd).reshape(B, S, H)
+        return keep.astype(dtype) * dtype(1.0 / (1.0 - pd))
     for i in range(L):
         p = f"esm.encoder.layer.{i}."
         res.hidden_states.append(x)
@@ -353,12 +401,16 @@ def forward_backward(cfg: OracleConfig, params: dict, input_ids: np.ndarray, att
         pr = np.exp(s)
         pr = pr / pr.sum(-1, keepdims=True)
         o = (pr @ v).transpose(0, 2, 1, 3).reshape(B, S, H)
-        x1 = x + _linear(o, P[p + "attention.output.dense.weight"], P[p + "attention.output.dense.bias"])
+        m_att, m_ffn = drop_mask(2 * i), drop_mask(2 * i + 1)
+        br = _linear(o, P[p + "attention.output.dense.weight"], P[p + "attention.output.dense.bias"])
+        x1 = x + (br if m_att is None else br * m_att)
         h2, ln2 = layer_norm(x1, P[p + "LayerNorm.weight"], P[p + "LayerNorm.bias"], eps)
         z = _linear(h2, P[p + "intermediate.dense.weight"], P[p + "intermediate.dense.bias"])
         a = gelu(z)
-        x2 = x1 + _linear(a, P[p + "output.dense.weight"], P[p + "output.dense.bias"])
-        caches.append(dict(x=x, ln1=ln1, h1=h1, q=q, k=k, v=v, o=o, x1=x1, ln2=ln2, h2=h2, z=z, a=a))
+        br = _linear(a, P[p + "output.dense.weight"], P[p + "output.dense.bias"])
+        x2 = x1 + (br if m_ffn is None else br * m_ffn)
+        caches.append(dict(x=x, ln1=ln1, h1=h1, q=q, k=k, v=v, o=o, x1=x1, ln2=ln2, h2=h2, z=z, a=a,
+                           m_att=m_att, m_ffn=m_ffn))
         if keep_acts:
             res.acts[i] = dict(h1=h1, q=q, k=k, v=v, o=o, x1=x1, h2=h2, z=z, a=a)
         x = x2
@@ -409,10 +461,11 @@ def forward_backward(cfg: OracleConfig, params: dict, input_ids: np.ndarray, att
     for i in reversed(range(L)):
         p = f"esm.encoder.layer.{i}."
         c = caches[i]
-        # FFN
-        G[p + "output.dense.weight"] = _wgrad(dx, c["a"])
-        G[p + "output.dense.bias"] = dx.sum((0, 1))
-        da = dx @ P[p + "output.dense.weight"]
+        # FFN (the branch gradient passes the dropout mask; the residual gradient does not)
+        dbr = dx if c["m_ffn"] is None else dx * c["m_ffn"]
+        G[p + "output.dense.weight"] = _wgrad(dbr, c["a"])
+        G[p + "output.dense.bias"] = dbr.sum((0, 1))
+        da = dbr @ P[p + "output.dense.weight"]
         dz = da * gelu_grad(c["z"])
         G[p + "intermediate.dense.weight"] = _wgrad(dz, c["h2"])
         G[p + "intermediate.dense.bias"] = dz.sum((0, 1))
@@ -420,9 +473,10 @@ def forward_backward(cfg: OracleConfig, params: dict, input_ids: np.ndarray, att
         dx1, G[p + "LayerNorm.weight"], G[p + "LayerNorm.bias"] = layer_norm_bwd(dh2, P[p + "LayerNorm.weight"], c["ln2"])
         dx1 = dx1 + dx
         # attention output projection
-        G[p + "attention.output.dense.weight"] = _wgrad(dx1, c["o"])
-        G[p + "attention.output.dense.bias"] = dx1.sum((0, 1))
-        do = (dx1 @ P[p + "attention.output.dense.weight"]).reshape(B, S, nh, dh).transpose(0, 2, 1, 3)
+        dbr = dx1 if c["m_att"] is None else dx1 * c["m_att"]
+        G[p + "attention.output.dense.weight"] = _wgrad(dbr, c["o"])
+        G[p + "attention.output.dense.bias"] = dbr.sum((0, 1))
+        do = (dbr @ P[p + "attention.output.dense.weight"]).reshape(B, S, nh, dh).transpose(0, 2, 1, 3)
         # attention core (recompute P, flash-style)
         q, k, v = c["q"], c["k"], c["v"]
         s = q @ k.transpose(0, 1, 3, 2) + keymask

@@ -30,9 +30,26 @@ CASES = {
     "tiny_dh24": (96, 2, 4, 384, 2, 32, [32, 20]),
     "tiny_dh64": (128, 1, 2, 512, 2, 40, [40, 33]),
 }
+# hidden dropout (HF EsmSelfOutput / EsmOutput dropout, training mode): HF's nn.Dropout modules are replaced by
+# modules applying the oracle's counter-based masks (esm2_oracle.dropout_keep), so the golden pins where and how
+# the masks enter the forward and the backward while the mask bits themselves are the library's own RNG.
+DROPOUT_CASES = {"tiny_dh24_dropout": ((96, 2, 4, 384, 2, 32, [32, 20]), (0x1234ABCD5678EF01, 0.1))}
 
 
-def hf_run(cfg: O.OracleConfig, params, ids, am, labels):
+class _MaskDropout:
+    """Stand-in for nn.Dropout(p) in training mode with a fixed keep mask: x * keep / (1 - p)."""
+
+    @staticmethod
+    def make(keep, p):
+        import torch
+
+        class M(torch.nn.Module):
+            def forward(self, x):
+                return x * torch.from_numpy(keep.astype(np.float64)) / (1.0 - p)
+        return M()
+
+
+def hf_run(cfg: O.OracleConfig, params, ids, am, labels, dropout=None):
     import torch
     from transformers import EsmConfig, EsmForMaskedLM
 
@@ -47,6 +64,14 @@ def hf_run(cfg: O.OracleConfig, params, ids, am, labels):
     torch.manual_seed(0)
     model = EsmForMaskedLM(hc).double()
     model.train()
+    if dropout is not None:
+        seed, p = dropout
+        B, S = ids.shape
+        for i, layer in enumerate(model.esm.encoder.layer):
+            layer.attention.output.dropout = _MaskDropout.make(
+                O.dropout_keep(seed, 2 * i, B * S, cfg.hidden_size, p).reshape(B, S, -1), p)
+            layer.output.dropout = _MaskDropout.make(
+                O.dropout_keep(seed, 2 * i + 1, B * S, cfg.hidden_size, p).reshape(B, S, -1), p)
     sd = {k: torch.from_numpy(np.asarray(v, dtype=np.float64)) for k, v in params.items()}
     missing, unexpected = model.load_state_dict(sd, strict=False)
     assert not unexpected, unexpected
@@ -77,7 +102,11 @@ def hf_run(cfg: O.OracleConfig, params, ids, am, labels):
 
 def main():
     os.makedirs(OUT, exist_ok=True)
-    for name, (H, L, nh, F, B, S, lens) in CASES.items():
+    cases = [(name, spec, None) for name, spec in CASES.items()]
+    cases += [(name, spec, drop) for name, (spec, drop) in DROPOUT_CASES.items()]
+    if len(sys.argv) > 1:
+        cases = [c for c in cases if c[0] in sys.argv[1:]]
+    for name, (H, L, nh, F, B, S, lens), drop in cases:
         cfg = O.OracleConfig(hidden_size=H, num_hidden_layers=L, num_attention_heads=nh, intermediate_size=F)
         params = O.init_params(cfg, seed=1)
         # perturb biases / LN params away from their init so their gradients are exercised
@@ -94,9 +123,12 @@ def main():
         inp, labels = O.mlm_mask(ids, seed=11, stream=0)
         # guarantee at least a few masked/labelled positions
         assert (labels != -100).sum() > 0
-        loss, logits, hidden, grads = hf_run(cfg, params, inp, am, labels)
+        loss, logits, hidden, grads = hf_run(cfg, params, inp, am, labels, dropout=drop)
         blob = dict(config=np.array([H, L, nh, F, B, S]), input_ids=inp, attention_mask=am, labels=labels,
                     raw_ids=ids, loss=np.array(loss), logits=logits)
+        if drop is not None:
+            blob["dropout_seed"] = np.array(drop[0], dtype=np.uint64)
+            blob["dropout_p"] = np.array(drop[1])
         for i, h in enumerate(hidden):
             blob[f"hidden.{i}"] = h
         for k, v in params.items():

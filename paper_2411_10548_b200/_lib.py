@@ -20,7 +20,7 @@ EXPORTS = [
     "esm_embed_bwd", "esm_layernorm_fwd", "esm_layernorm_bwd", "esm_gemm", "esm_qkv_rope_fwd", "esm_qkv_rope_bwd",
     "esm_attn_prepare", "esm_attn_fwd", "esm_attn_bwd", "esm_attn_bwd_qkv", "esm_lmhead_xent", "esm_inv_count",
     "esm_mlm_mask_ex", "esm_label_compact", "esm_gather_rows", "esm_scatter_rows", "esm_xent_rows", "esm_colsum_rows",
-    "esm_rank_encode", "esm_adamw", "esm_adamw_bf16g", "esm_cast_f32_bf16", "esm_cast_bf16_f32",
+    "esm_rank_encode", "esm_dropout_mask", "esm_adamw", "esm_adamw_bf16g", "esm_cast_f32_bf16", "esm_cast_bf16_f32",
     "esm_comm_version", "esm_comm_unique_id", "esm_comm_init", "esm_comm_destroy", "esm_comm_allreduce",
     "esm_comm_reduce_scatter", "esm_comm_allgather",
 ]
@@ -28,6 +28,12 @@ EXPORTS = [
 
 class EsmKernelError(RuntimeError):
     """A C-ABI call returned non-zero (cudaError_t or ESM_E* code); message from esm_last_error()."""
+
+
+class Dropout(ctypes.Structure):
+    """esm_dropout (include/esm2_b200.h): per-step seed (device pointer), call site, 16-bit threshold, scale."""
+    _fields_ = [("seed", ctypes.c_void_p), ("site", ctypes.c_uint32), ("threshold", ctypes.c_uint32),
+                ("scale", ctypes.c_float)]
 
 
 class GemmArgs(ctypes.Structure):
@@ -47,6 +53,7 @@ class GemmArgs(ctypes.Structure):
         ("seq_len", ctypes.c_int), ("n_heads", ctypes.c_int), ("head_dim", ctypes.c_int),
         ("q_scale", ctypes.c_float),
         ("row_mean", ctypes.c_void_p), ("row_rstd", ctypes.c_void_p), ("col_sum2", ctypes.c_void_p),
+        ("drop", Dropout),
     ]
 
 
@@ -60,7 +67,8 @@ _SIGS = {
     "esm_embed_fwd": ([_I, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P], _I),
     "esm_embed_bwd": ([_I, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P], _I),
     "esm_layernorm_fwd": ([_I, _P, _P, _P, _P, _P, _P, _I, _I, _F, _P], _I),
-    "esm_layernorm_bwd": ([_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P], _I),
+    "esm_layernorm_bwd": ([_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P, _P], _I),
+    "esm_dropout_mask": ([_P, _I64, _I, _P, _P], _I),
     "esm_gemm": ([ctypes.POINTER(GemmArgs), _P], _I),
     "esm_qkv_rope_fwd": ([_I, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _F, _P], _I),
     "esm_qkv_rope_bwd": ([_I, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _F, _P], _I),

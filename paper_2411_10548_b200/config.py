@@ -46,8 +46,11 @@ class EsmConfig:
             raise ValueError("only rotary position embeddings (ESM-2) are supported")
         if self.emb_layer_norm_before:
             raise ValueError("emb_layer_norm_before=True (ESM-1b) is not supported")
-        if self.hidden_dropout_prob or self.attention_probs_dropout_prob:
-            raise ValueError("ESM-2 trains with dropout 0.0; dropout > 0 is not implemented")
+        if not 0.0 <= self.hidden_dropout_prob < 1.0:
+            raise ValueError("hidden_dropout_prob must be in [0, 1)")
+        if self.attention_probs_dropout_prob:
+            raise ValueError("attention-probability dropout is not implemented (ESM-2 trains with 0.0; hidden "
+                             "dropout, HF EsmSelfOutput / EsmOutput, is fused into the residual epilogues)")
         if self.head_dim not in (16, 24, 32, 64):
             raise ValueError(f"head_dim {self.head_dim} not supported by the attention kernels")
         if self.hidden_size % 16:

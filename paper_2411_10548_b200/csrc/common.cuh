@@ -36,6 +36,38 @@ void set_last_error(const char* fmt, ...);
     return 0;                                                               \
   } while (0)
 
+// Counter-based dropout keep mask (include/esm2_b200.h esm_dropout; oracle/esm2_oracle.py:dropout_keep).
+__host__ __device__ __forceinline__ uint32_t lowbias32(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x7feb352du;
+  x ^= x >> 15;
+  x *= 0x846ca68bu;
+  x ^= x >> 16;
+  return x;
+}
+struct DropKeys {
+  uint32_t k0, k1, thr;
+  float scale;
+  bool on;
+};
+__device__ __forceinline__ DropKeys drop_keys(const esm_dropout& d) {
+  DropKeys k{0u, 0u, d.threshold, d.scale, d.seed != nullptr && d.threshold != 0};
+  if (k.on) {
+    const uint64_t s = *d.seed;
+    k.k0 = (uint32_t)s ^ lowbias32(2u * d.site + 1u);
+    k.k1 = (uint32_t)(s >> 32) ^ lowbias32(2u * d.site + 2u);
+  }
+  return k;
+}
+__device__ __forceinline__ uint32_t drop_row(const DropKeys& k, uint32_t row) {
+  return lowbias32(row * 0x9E3779B1u ^ k.k0);
+}
+// keep bits of columns (2*pair, 2*pair + 1) of a row (rh = drop_row): bit 0 / bit 1
+__device__ __forceinline__ uint32_t drop_pair(const DropKeys& k, uint32_t rh, uint32_t pair) {
+  const uint32_t u = lowbias32(rh ^ (pair + k.k1));
+  return ((u & 0xFFFFu) >= k.thr ? 1u : 0u) | ((u >> 16) >= k.thr ? 2u : 0u);
+}
+
 // SM count of the *current* device (cached per device id; launches size persistent grids with it).
 // Function attributes (max dynamic shared memory) are likewise per device, so launchers set them on
 // every launch rather than once per process (cheap, and legal during CUDA-graph capture).

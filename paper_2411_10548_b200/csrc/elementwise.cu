@@ -7,6 +7,8 @@
 #include <cstdio>
 #include <cstring>
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace esm {
@@ -119,31 +121,67 @@ __global__ void embed_fwd_kernel(const int32_t* __restrict__ ids, const int32_t*
   }
 }
 
-// dE[v, col] += sum over rows with ids==v.  Column-owner threads accumulate in smem (V small).
+// dE[v, :] += sum over rows with ids == v (small V: the ESM alphabet).  Thread = one 16-byte column vector
+// (VEC columns), block = up to 1280 columns x a contiguous block of rows; per-(id, column) partial sums live in
+// shared memory ([V][VEC * blockDim] fp32), RU rows' vectors are loaded before they are accumulated, and each
+// block adds its partials to dE with vector reductions (red.global.add.v4.f32).
 template <typename T>
-__global__ void embed_bwd_smem_kernel(const int32_t* __restrict__ ids, const int32_t* __restrict__ am,
-                                      const float* __restrict__ row_scale, const T* __restrict__ dx,
-                                      float* __restrict__ dE, int64_t T_, int S, int H, int V, int rows_per_block,
-                                      int mask_id, int pad_id) {
-  extern __shared__ float acc[];  // [V][blockDim.x]
-  const int col = blockIdx.x * blockDim.x + threadIdx.x;
-  for (int i = threadIdx.x; i < V * (int)blockDim.x; i += blockDim.x) acc[i] = 0.f;
+__global__ void __launch_bounds__(256) embed_bwd_smem_kernel(const int32_t* __restrict__ ids,
+                                                             const int32_t* __restrict__ am,
+                                                             const float* __restrict__ row_scale,
+                                                             const T* __restrict__ dx, float* __restrict__ dE,
+                                                             int64_t T_, int S, int H, int V, int rows_per_block,
+                                                             int mask_id, int pad_id) {
+  constexpr int VEC = vec16<T>::N;
+  constexpr int RU = 4;
+  extern __shared__ float acc[];  // [V][BC]
+  const int BC = VEC * blockDim.x;
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) * VEC;  // first column of this thread
+  const int lc = threadIdx.x * VEC;
+  for (int i = threadIdx.x; i < V * BC; i += blockDim.x) acc[i] = 0.f;
   __syncthreads();
   const int64_t r0 = (int64_t)blockIdx.y * rows_per_block;
   const int64_t r1 = min(T_, r0 + rows_per_block);
-  if (col < H) {
-    for (int64_t t = r0; t < r1; ++t) {
-      const int id = ids[t];
-      if (id == pad_id || id == mask_id) continue;  // padding_idx gets no grad; masked rows were zeroed
-      const float sc = row_scale[t / S] * (am ? (float)(am[t] != 0) : 1.0f);
-      acc[id * blockDim.x + threadIdx.x] += io<T>::ld(dx + t * H + col) * sc;
+  if (c < H) {
+    for (int64_t t0 = r0; t0 < r1; t0 += RU) {
+      uint4 raw[RU];
+      int id[RU];
+      float sc[RU];
+#pragma unroll
+      for (int u = 0; u < RU; ++u) {
+        const int64_t t = t0 + u < r1 ? t0 + u : r1 - 1;
+        id[u] = t0 + u < r1 ? ids[t] : pad_id;
+        sc[u] = row_scale[t / S] * (am ? (float)(am[t] != 0) : 1.0f);
+        raw[u] = *reinterpret_cast<const uint4*>(dx + t * H + c);
+      }
+#pragma unroll
+      for (int u = 0; u < RU; ++u) {
+        if (id[u] == pad_id || id[u] == mask_id || sc[u] == 0.f) continue;  // no grad for padding / masked rows
+        float v[VEC];
+        load_vec(reinterpret_cast<const T*>(&raw[u]), v);
+        float* a = acc + id[u] * BC + lc;
+#pragma unroll
+        for (int e = 0; e < VEC; e += 4) {
+          float4 q = *reinterpret_cast<float4*>(a + e);
+          q.x += v[e] * sc[u];
+          q.y += v[e + 1] * sc[u];
+          q.z += v[e + 2] * sc[u];
+          q.w += v[e + 3] * sc[u];
+          *reinterpret_cast<float4*>(a + e) = q;
+        }
+      }
     }
   }
   __syncthreads();
-  if (col < H)
+  if (c < H)
     for (int v = 0; v < V; ++v) {
-      const float a = acc[v * blockDim.x + threadIdx.x];
-      if (a != 0.f) atomicAdd(dE + (int64_t)v * H + col, a);
+      const float* a = acc + v * BC + lc;
+#pragma unroll
+      for (int e = 0; e < VEC; e += 4) {
+        const float4 q = *reinterpret_cast<const float4*>(a + e);
+        if (q.x != 0.f || q.y != 0.f || q.z != 0.f || q.w != 0.f)
+          red_add_v4_f32(dE + (int64_t)v * H + c + e, q.x, q.y, q.z, q.w);
+      }
     }
 }
 
@@ -359,9 +397,10 @@ __global__ void __launch_bounds__(256, SG ? 3 : (sizeof(T) == 2 && (MAXV <= 2 ||
     ln_bwd_kernel(const T* __restrict__ dy, const T* __restrict__ x, const float* __restrict__ g,
                   const float* __restrict__ mean, const float* __restrict__ rstd, const T* __restrict__ dres,
                   const T* __restrict__ gelu_z, T* __restrict__ dx, float* __restrict__ dg, float* __restrict__ db,
-                  float* __restrict__ csum, int64_t rows, int H) {
+                  float* __restrict__ csum, int64_t rows, int H, const esm_dropout drop, T* __restrict__ dxd) {
   constexpr int VEC = vec16<T>::N;
   constexpr int GPB = 8 / WPR;
+  const DropKeys dk = dxd != nullptr ? drop_keys(drop) : DropKeys{0u, 0u, 0u, 1.f, false};
   __shared__ float2 red[GPB][2 * WPR];
   extern __shared__ float sacc[];  // [3][H] block-level partial sums
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -453,8 +492,22 @@ __global__ void __launch_bounds__(256, SG ? 3 : (sizeof(T) == 2 && (MAXV <= 2 ||
 #pragma unroll
           for (int j = 0; j < VEC; ++j) o[j] *= gelu_grad_f(zv[j]);
         }
+        if (dxd != nullptr) {  // gradient of the dropped-out branch (its bias gradient goes to csum)
+          const uint32_t rh = drop_row(dk, (uint32_t)r);
+          float od[VEC];
 #pragma unroll
-        for (int j = 0; j < VEC; ++j) ac[i][j] += o[j];
+          for (int j = 0; j < VEC; j += 2) {
+            const uint32_t kb = drop_pair(dk, rh, (uint32_t)(h + j) >> 1);
+            od[j] = (kb & 1u) ? o[j] * dk.scale : 0.f;
+            od[j + 1] = (kb & 2u) ? o[j + 1] * dk.scale : 0.f;
+          }
+#pragma unroll
+          for (int j = 0; j < VEC; ++j) ac[i][j] += od[j];
+          store_vec(dxd + r * H + h, od);
+        } else {
+#pragma unroll
+          for (int j = 0; j < VEC; ++j) ac[i][j] += o[j];
+        }
         store_vec(dx + r * H + h, o);
       }
     }
@@ -607,6 +660,78 @@ __global__ void __launch_bounds__(256) qkv_rope_bwd_kernel(const float* __restri
     atomicAdd(csum + 2 * H + c0 + 1, a[9]);
     atomicAdd(csum + 2 * H + c0 + half, a[10]);
     atomicAdd(csum + 2 * H + c0 + half + 1, a[11]);
+  }
+}
+
+// bf16 fast path (head_dim / 2 a multiple of 8): thread = (token, head, 8-column chunk of the first rotation half
+// and its partner chunk of the second half).  The lanes of a token cover consecutive heads / chunks, so the
+// head-major inputs are read in whole 32-byte sectors and the token-major dqkv row segment is written with
+// contiguous 16-byte stores; each thread walks a strided set of tokens with fixed columns and adds its q/k/v
+// bias-gradient partial sums with vector reductions at the end.
+__global__ void __launch_bounds__(256) qkv_rope_bwd_vec_kernel(const float* __restrict__ dq,
+                                                               const __nv_bfloat16* __restrict__ dk,
+                                                               const __nv_bfloat16* __restrict__ dv,
+                                                               __nv_bfloat16* __restrict__ dqkv,
+                                                               float* __restrict__ csum, const float* __restrict__ cs,
+                                                               const float* __restrict__ sn, int64_t T_, int S, int nh,
+                                                               int dh, float qs) {
+  const int half = dh >> 1, cpr = half >> 3;  // chunks per rotation half
+  const int lanes = nh * cpr;                 // threads per token
+  const int slots = blockDim.x / lanes;       // tokens per block iteration
+  const int slot = threadIdx.x / lanes, li = threadIdx.x - slot * lanes;
+  if (slot >= slots) return;
+  const int h = li / cpr, j = (li - h * cpr) * 8;
+  const int H = nh * dh;
+  float aq[16], ak[16], av[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) aq[i] = ak[i] = av[i] = 0.f;
+  const int64_t stride = (int64_t)gridDim.x * slots;
+  for (int64_t t = (int64_t)blockIdx.x * slots + slot; t < T_; t += stride) {
+    const int64_t b = t / S;
+    const int s = (int)(t - b * S);
+    const int64_t o = ((b * nh + h) * S + s) * dh + j;
+    float g0[8], g1[8], e0[8], e1[8], v0[8], v1[8], c[8], sv[8];
+    load_f32x(dq + o, g0, 8);
+    load_f32x(dq + o + half, g1, 8);
+    load_vec(dk + o, e0);
+    load_vec(dk + o + half, e1);
+    load_vec(dv + o, v0);
+    load_vec(dv + o + half, v1);
+    load_f32x(cs + (int64_t)s * half + j, c, 8);
+    load_f32x(sn + (int64_t)s * half + j, sv, 8);
+    float q0[8], q1[8], k0[8], k1[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {  // RoPE^T: dx_j = dy_j c + dy_{j+h} s ; dx_{j+h} = dy_{j+h} c - dy_j s
+      q0[e] = (g0[e] * c[e] + g1[e] * sv[e]) * qs;
+      q1[e] = (g1[e] * c[e] - g0[e] * sv[e]) * qs;
+      k0[e] = e0[e] * c[e] + e1[e] * sv[e];
+      k1[e] = e1[e] * c[e] - e0[e] * sv[e];
+      aq[e] += q0[e];
+      aq[8 + e] += q1[e];
+      ak[e] += k0[e];
+      ak[8 + e] += k1[e];
+      av[e] += v0[e];
+      av[8 + e] += v1[e];
+    }
+    __nv_bfloat16* row = dqkv + t * 3 * H + h * dh + j;
+    store_vec(row, q0);
+    store_vec(row + half, q1);
+    store_vec(row + H, k0);
+    store_vec(row + H + half, k1);
+    store_vec(row + 2 * H, v0);
+    store_vec(row + 2 * H + half, v1);
+  }
+  if (csum) {
+    float* cq = csum + h * dh + j;
+#pragma unroll
+    for (int e = 0; e < 8; e += 4) {
+      red_add_v4_f32(cq + e, aq[e], aq[e + 1], aq[e + 2], aq[e + 3]);
+      red_add_v4_f32(cq + half + e, aq[8 + e], aq[9 + e], aq[10 + e], aq[11 + e]);
+      red_add_v4_f32(cq + H + e, ak[e], ak[e + 1], ak[e + 2], ak[e + 3]);
+      red_add_v4_f32(cq + H + half + e, ak[8 + e], ak[9 + e], ak[10 + e], ak[11 + e]);
+      red_add_v4_f32(cq + 2 * H + e, av[e], av[e + 1], av[e + 2], av[e + 3]);
+      red_add_v4_f32(cq + 2 * H + half + e, av[8 + e], av[9 + e], av[10 + e], av[11 + e]);
+    }
   }
 }
 
@@ -930,6 +1055,18 @@ __global__ void cast_kernel(const float* __restrict__ s, __nv_bfloat16* __restri
     d[i] = __float2bfloat16_rn(s[i]);
 }
 
+__global__ void dropout_mask_kernel(const esm_dropout d, int64_t rows, int cols, uint8_t* __restrict__ out) {
+  const DropKeys dk = drop_keys(d);
+  const int64_t pairs = (int64_t)rows * ((cols + 1) / 2);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < pairs; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / ((cols + 1) / 2);
+    const int p = (int)(i - r * ((cols + 1) / 2));
+    const uint32_t kb = dk.on ? drop_pair(dk, drop_row(dk, (uint32_t)r), (uint32_t)p) : 3u;
+    out[r * cols + 2 * p] = kb & 1u;
+    if (2 * p + 1 < cols) out[r * cols + 2 * p + 1] = (kb >> 1) & 1u;
+  }
+}
+
 __global__ void cast_bf16_f32_kernel(const __nv_bfloat16* __restrict__ s, float* __restrict__ d, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     d[i] = __bfloat162float(s[i]);
@@ -1021,7 +1158,7 @@ int esm_embed_bwd(int dtype, const int32_t* ids, const int32_t* am, const float*
                   int B, int Sq, int H, int V, int mask_id, int pad_id, esm_stream_t stream) {
   ESM_CHECK_ARG(ids && row_scale && dx && dE && V > 0 && H % 8 == 0, "esm_embed_bwd: bad args");
   const int64_t T_ = (int64_t)B * Sq;
-  if (V > 128) {
+  if (V > 40) {
     const int grid = grid_for(T_ * 32, 256);
     if (dtype == ESM_BF16)
       embed_bwd_atomic_kernel<__nv_bfloat16><<<grid, 256, 0, S(stream)>>>(ids, am, row_scale,
@@ -1032,16 +1169,23 @@ int esm_embed_bwd(int dtype, const int32_t* ids, const int32_t* am, const float*
                                                                   H, mask_id, pad_id);
     ESM_LAUNCH_RET();
   }
-  const int bx = 128;
-  const int rpb = 256;
-  dim3 grid((H + bx - 1) / bx, (unsigned)((T_ + rpb - 1) / rpb));
-  const size_t sm = (size_t)V * bx * sizeof(float);
-  if (dtype == ESM_BF16)
+  const int vec = dtype == ESM_BF16 ? 8 : 4;
+  const int cols = H < 1280 ? H : 1280;                       // columns per block (<= 165 KB of partials at V 33)
+  const int bx = ((cols / vec) + 31) / 32 * 32;
+  const int gx = (H + bx * vec - 1) / (bx * vec);
+  const int gy = (int)std::max<int64_t>(1, std::min<int64_t>((T_ + 63) / 64, device_sm_count() / gx));
+  const int rpb = (int)((T_ + gy - 1) / gy);
+  dim3 grid(gx, gy);
+  const size_t sm = (size_t)V * bx * vec * sizeof(float);
+  if (dtype == ESM_BF16) {
+    cudaFuncSetAttribute(embed_bwd_smem_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     embed_bwd_smem_kernel<__nv_bfloat16><<<grid, bx, sm, S(stream)>>>(ids, am, row_scale, (const __nv_bfloat16*)dx,
                                                                       dE, T_, Sq, H, V, rpb, mask_id, pad_id);
-  else
+  } else {
+    cudaFuncSetAttribute(embed_bwd_smem_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     embed_bwd_smem_kernel<float><<<grid, bx, sm, S(stream)>>>(ids, am, row_scale, (const float*)dx, dE, T_, Sq, H, V,
                                                               rpb, mask_id, pad_id);
+  }
   ESM_LAUNCH_RET();
 }
 
@@ -1134,8 +1278,12 @@ int esm_layernorm_fwd(int dtype, const void* x, const float* gamma, const float*
 
 int esm_layernorm_bwd(int dtype, const void* dy, const void* x, const float* gamma, const float* mean,
                       const float* rstd, const void* dres, const void* gelu_z, void* dx, float* dgamma, float* dbeta,
-                      float* col_sum, int rows, int H, esm_stream_t stream) {
+                      float* col_sum, int rows, int H, const esm_dropout* drop, void* dx_drop, esm_stream_t stream) {
   ESM_CHECK_ARG(dy && x && gamma && mean && rstd && dx && rows > 0, "esm_layernorm_bwd: bad args");
+  const bool dropping = drop != nullptr && drop->threshold != 0u;
+  ESM_CHECK_ARG(!dropping || (dx_drop != nullptr && drop->seed != nullptr), "esm_layernorm_bwd: dropout needs dx_drop");
+  const esm_dropout dr = dropping ? *drop : esm_dropout{nullptr, 0u, 0u, 1.f};
+  void* dxd = dropping ? dx_drop : nullptr;
   const int vec = dtype == ESM_BF16 ? 8 : 4;
   ESM_CHECK_ARG(H % vec == 0, "layernorm: H %% %d", vec);
   int mv, wpr;
@@ -1153,7 +1301,7 @@ int esm_layernorm_bwd(int dtype, const void* dy, const void* x, const float* gam
     cudaFuncSetAttribute(__VA_ARGS__, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);         \
     __VA_ARGS__<<<grid, 256, sm, S(stream)>>>((const TT*)dy, (const TT*)x, gamma, mean, rstd,        \
                                               (const TT*)dres, (const TT*)gelu_z, (TT*)dx, dgamma,   \
-                                              dbeta, col_sum, rows, H);                              \
+                                              dbeta, col_sum, rows, H, dr, (TT*)dxd);                \
   } while (0)
   if (dtype == ESM_BF16) {
     using TT = __nv_bfloat16;
@@ -1206,6 +1354,18 @@ int esm_qkv_rope_bwd(int dtype, const float* dq, const void* dk, const void* dv,
                      esm_stream_t stream) {
   ESM_CHECK_ARG(dq && dk && dv && dqkv && cos_t && sin_t && dh % 4 == 0, "esm_qkv_rope_bwd: bad args (dh %% 4)");
   const int64_t T_ = (int64_t)B * Sq;
+  const int lanes = nh * (dh / 16);  // vector path: threads per token
+  if (dtype == ESM_BF16 && dh % 16 == 0 && lanes <= 256 && (!col_sum || ((uintptr_t)col_sum & 15) == 0)) {
+    const int slots = 256 / lanes;
+    const int tokens_per_thread = 16;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((T_ + (int64_t)slots * tokens_per_thread - 1) /
+                                                                     ((int64_t)slots * tokens_per_thread),
+                                                                 (int64_t)device_sm_count() * 8));
+    qkv_rope_bwd_vec_kernel<<<grid, slots * lanes, 0, S(stream)>>>(
+        dq, (const __nv_bfloat16*)dk, (const __nv_bfloat16*)dv, (__nv_bfloat16*)dqkv, col_sum, cos_t, sin_t, T_, Sq,
+        nh, dh, q_scale);
+    ESM_LAUNCH_RET();
+  }
   const int units = nh * dh / 4;  // two rotation pairs per thread
   const int bx = units >= 64 ? 64 : (units + 31) / 32 * 32;  // small blocks: many in flight per SM
   const int rpb = 32;
@@ -1301,6 +1461,13 @@ int esm_cast_f32_bf16(const float* src, void* dst, int64_t n, esm_stream_t strea
                 "esm_cast_f32_bf16: bad args (src 16 B, dst 8 B aligned)");
   if (n == 0) return 0;
   cast_kernel<<<grid_for(n / 4 + 1, 256, device_sm_count() * 8), 256, 0, S(stream)>>>(src, (__nv_bfloat16*)dst, n);
+  ESM_LAUNCH_RET();
+}
+
+int esm_dropout_mask(const esm_dropout* drop, int64_t rows, int cols, uint8_t* out, esm_stream_t stream) {
+  ESM_CHECK_ARG(drop && out && rows >= 0 && cols > 0, "esm_dropout_mask: bad args");
+  if (rows == 0) return 0;
+  dropout_mask_kernel<<<grid_for(rows * ((cols + 1) / 2), 256), 256, 0, S(stream)>>>(*drop, rows, cols, out);
   ESM_LAUNCH_RET();
 }
 

@@ -41,6 +41,8 @@ struct EpiParams {
   const float* row_mean;
   const float* row_rstd;
   float* col_sum2;
+  // RESID: C = R + dropout(acc + bias)
+  esm_dropout drop;
 };
 
 // ============================================================================
@@ -389,6 +391,18 @@ __global__ void __launch_bounds__(EpiCfg<EPI>::THREADS, 1)
             }
           }
         }
+        if constexpr (EPI == ESM_EPI_RESID) {
+          if (ep.drop.threshold != 0u) {  // hidden dropout of the branch, before the residual add
+            const DropKeys dk = drop_keys(ep.drop);
+            const uint32_t rh = drop_row(dk, (uint32_t)(row0 + lane));
+#pragma unroll
+            for (int j = 0; j < 32; j += 2) {
+              const uint32_t kb = drop_pair(dk, rh, (uint32_t)(col0 + j) >> 1);
+              v[j] = (kb & 1u) ? v[j] * dk.scale : 0.f;
+              v[j + 1] = (kb & 2u) ? v[j + 1] * dk.scale : 0.f;
+            }
+          }
+        }
         if constexpr (E::AUX) {
           mbar_wait(&abar[ab], (aux_phase >> ab) & 1u);
           aux_phase ^= 1u << ab;
@@ -610,7 +624,7 @@ static int launch_cg(const esm_gemm_args& a, cudaStream_t st) {
   EpiParams ep{a.M, a.N, a.C, a.ldc, a.bias, a.aux_in, a.ld_aux_in, a.aux_out, a.ld_aux_out, a.col_sum,
                a.rope_cos, a.rope_sin,
                {(__nv_bfloat16*)a.q_out, (__nv_bfloat16*)a.k_out, (__nv_bfloat16*)a.v_out},
-               a.seq_len, a.n_heads, a.head_dim, a.q_scale, a.row_mean, a.row_rstd, a.col_sum2};
+               a.seq_len, a.n_heads, a.head_dim, a.q_scale, a.row_mean, a.row_rstd, a.col_sum2, a.drop};
   auto kern = gemm_tc_kernel<BN, A_MN, B_MN, EPI, CG>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);  // per device: every launch
   const int total = tiles * splits;
@@ -762,8 +776,14 @@ __device__ __forceinline__ void apply_epi(const EpiParams& p, int row, int col, 
     return;
   } else {
     if (p.bias && EPI != ESM_EPI_DGELU) v += p.bias[col];
-    if constexpr (EPI == ESM_EPI_RESID)
+    if constexpr (EPI == ESM_EPI_RESID) {
+      if (p.drop.threshold != 0u) {
+        const DropKeys dk = drop_keys(p.drop);
+        const uint32_t kb = drop_pair(dk, drop_row(dk, (uint32_t)row), (uint32_t)col >> 1);
+        v = ((kb >> (col & 1)) & 1u) ? v * dk.scale : 0.f;
+      }
       v += reinterpret_cast<const float*>(p.aux_in)[(int64_t)row * p.ld_aux_in + col];
+    }
     if constexpr (EPI == ESM_EPI_DGELU) {
       v *= gelu_grad_f(reinterpret_cast<const float*>(p.aux_in)[(int64_t)row * p.ld_aux_in + col]);
       if (p.col_sum) atomicAdd(p.col_sum + col, v);
@@ -827,6 +847,7 @@ __global__ void __launch_bounds__(256) gemm_f32_kernel(const float* __restrict__
 
 int gemm_f32(const esm_gemm_args& a, cudaStream_t st) {
   EpiParams ep{a.M, a.N, a.C, a.ldc, a.bias, a.aux_in, a.ld_aux_in, a.aux_out, a.ld_aux_out, a.col_sum};
+  ep.drop = a.drop;
   int splits = 1;
   if (a.epilogue == ESM_EPI_F32_ACC) splits = a.split_k > 0 ? a.split_k : (a.K >= 4096 ? 8 : 1);
   int kchunk = (a.K + splits - 1) / splits;

@@ -26,6 +26,7 @@ one after another during backward.
 """
 from __future__ import annotations
 
+import ctypes
 import math
 import os
 from dataclasses import dataclass
@@ -275,6 +276,9 @@ class Workspace:
         self.dz = e(T, F)
         self.dx1 = e(T, H)
         self.do = e(T, H)
+        # gradient of a dropped-out branch (hidden dropout): written by the LayerNorm backward, read by the
+        # branch's dgrad / wgrad GEMMs
+        self.dxd = e(T, H) if cfg.hidden_dropout_prob > 0 else None
         self.dq = e(B, nh, S, dh, dt=f32)
         self.dk, self.dv = e(B, nh, S, dh), e(B, nh, S, dh)
         self.dqkv = e(T, 3 * H)
@@ -318,6 +322,11 @@ class EsmForMaskedLM:
         self.load_state_dict(params if params is not None else init_params(self.config, seed))
         self.lr, self.betas, self.eps, self.weight_decay = lr, tuple(betas), eps, weight_decay
         self.hyper = torch.zeros(8, dtype=torch.float32, device=self.device)
+        # hidden dropout: per-step 64-bit seed in device memory (read by the kernels: CUDA-graph safe)
+        self.dropout_p = float(self.config.hidden_dropout_prob)
+        self.dropout_base = (int(seed) * 0x9E3779B97F4A7C15 + 0xD1B54A32D192ED03) & 0xFFFFFFFFFFFFFFFF
+        self.drop_seed = torch.zeros(1, dtype=torch.int64, device=self.device)
+        self.last_dropout_seed = 0
         self.step_count = 0
         self.grad_scale = 1.0
         self.ws: Workspace | None = None
@@ -427,7 +436,7 @@ class EsmForMaskedLM:
         self.launches += self._KERNELS.get(name, 1)
 
     def _gemm(self, M, N, K, A, lda, amn, B, ldb, bmn, C, ldc, epi, bias=None, aux_in=None, ld_aux_in=0,
-              aux_out=None, ld_aux_out=0, col_sum=None, ln=None):
+              aux_out=None, ld_aux_out=0, col_sum=None, ln=None, drop=None):
         t = self.timer
         if t is not None:
             kind = "gemm_" + ("wgrad" if epi == EPI_F32_ACC else "dgrad" if bmn else "fwd")
@@ -436,12 +445,12 @@ class EsmForMaskedLM:
             t.begin(kind)
         self.launches += 1
         self._gemm_raw(M, N, K, A, lda, amn, B, ldb, bmn, C, ldc, epi, bias, aux_in, ld_aux_in, aux_out, ld_aux_out,
-                       col_sum, ln)
+                       col_sum, ln, drop)
         if t is not None:
             t.end(2.0 * M * N * K, 0.0)
 
     def _gemm_raw(self, M, N, K, A, lda, amn, B, ldb, bmn, C, ldc, epi, bias, aux_in, ld_aux_in, aux_out,
-                  ld_aux_out, col_sum, ln=None):
+                  ld_aux_out, col_sum, ln=None, drop=None):
         if ln is not None:  # (row_mean, row_rstd, dgamma accumulator)
             _lib.gemm_call(self._stream(), dtype=self.kdt, M=M, N=N, K=K, A=A.data_ptr(), lda=lda, a_mn_major=amn,
                            B=B.data_ptr(), ldb=ldb, b_mn_major=bmn, C=C.data_ptr(), ldc=ldc, epilogue=epi,
@@ -453,14 +462,15 @@ class EsmForMaskedLM:
                        bias=bias.data_ptr() if bias is not None else None,
                        aux_in=aux_in.data_ptr() if aux_in is not None else None, ld_aux_in=ld_aux_in,
                        aux_out=aux_out.data_ptr() if aux_out is not None else None, ld_aux_out=ld_aux_out,
-                       col_sum=col_sum.data_ptr() if col_sum is not None else None, split_k=0)
+                       col_sum=col_sum.data_ptr() if col_sum is not None else None, split_k=0,
+                       **({"drop": drop} if drop is not None else {}))
 
-    def linear_fwd(self, x, wkey, out_f, in_f, bias_key, C, epi=EPI_STORE, aux_in=None, aux_out=None):
+    def linear_fwd(self, x, wkey, out_f, in_f, bias_key, C, epi=EPI_STORE, aux_in=None, aux_out=None, drop=None):
         T = x.shape[0]
         W = self._w(wkey, (out_f, in_f))
         self._gemm(T, out_f, in_f, x, in_f, 0, W, in_f, 0, C, out_f, epi,
                    bias=self._p32(bias_key) if bias_key else None, aux_in=aux_in, ld_aux_in=out_f,
-                   aux_out=aux_out, ld_aux_out=out_f)
+                   aux_out=aux_out, ld_aux_out=out_f, drop=drop)
 
     def _qkv_rope_gemm(self, ly, p, ws, T, H, nh, dh, S, qs):
         W = self._w(p + "attention.self.qkv.weight", (3 * H, H))
@@ -599,14 +609,14 @@ class EsmForMaskedLM:
             call("esm_attn_fwd", kdt, ly.q.data_ptr(), ly.k.data_ptr(), ly.v.data_ptr(), ws.am.data_ptr(), sched,
                  ly.o.data_ptr(), ly.lse.data_ptr(), B, nh, S, dh, st, flops=4.0 * B * nh * S * S * dh)
             self.linear_fwd(ly.o, p + "attention.output.dense.weight", H, H, p + "attention.output.dense.bias",
-                            ly.x1, epi=EPI_RESID, aux_in=x)
+                            ly.x1, epi=EPI_RESID, aux_in=x, drop=self._drop(2 * l))
             call("esm_layernorm_fwd", kdt, ly.x1.data_ptr(), self._p32(p + "LayerNorm.weight").data_ptr(),
                  self._p32(p + "LayerNorm.bias").data_ptr(), ly.h2.data_ptr(), ly.ln2_m.data_ptr(),
                  ly.ln2_r.data_ptr(), T, H, eps, st)
             self.linear_fwd(ly.h2, p + "intermediate.dense.weight", F, H, p + "intermediate.dense.bias", ly.a,
                             epi=EPI_GELU_GRADAUX if kdt == ESM_BF16 else EPI_GELU, aux_out=ly.z)
             self.linear_fwd(ly.a, p + "output.dense.weight", H, F, p + "output.dense.bias", ws.x[l + 1],
-                            epi=EPI_RESID, aux_in=ly.x1)
+                            epi=EPI_RESID, aux_in=ly.x1, drop=self._drop(2 * l + 1))
         call("esm_layernorm_fwd", kdt, ws.x[L].data_ptr(),
              self._p32("esm.encoder.emb_layer_norm_after.weight").data_ptr(),
              self._p32("esm.encoder.emb_layer_norm_after.bias").data_ptr(), ws.xf.data_ptr(), ws.lnf_m.data_ptr(),
@@ -635,7 +645,8 @@ class EsmForMaskedLM:
         call("esm_layernorm_bwd", kdt, ws.dn.data_ptr(), ws.g.data_ptr(),
              self._p32("lm_head.layer_norm.weight").data_ptr(), ws.lnh_m.data_ptr(), ws.lnh_r.data_ptr(), None,
              ws.y.data_ptr(), ws.dy.data_ptr(), self._g32("lm_head.layer_norm.weight").data_ptr(),
-             self._g32("lm_head.layer_norm.bias").data_ptr(), self._g32("lm_head.dense.bias").data_ptr(), T, H, st)
+             self._g32("lm_head.layer_norm.bias").data_ptr(), self._g32("lm_head.dense.bias").data_ptr(), T, H,
+             None, None, st)
         fused = self.linear_dgrad(ws.dy, "lm_head.dense.weight", H, H, ws.dh,
                                   ln=(ws.x[L], ws.lnf_m, ws.lnf_r, "esm.encoder.emb_layer_norm_after"))
         self.linear_wgrad(ws.dy, ws.xf, "lm_head.dense.weight", H, H)
@@ -645,7 +656,7 @@ class EsmForMaskedLM:
              ws.lnf_r.data_ptr(), None, None, ws.dx.data_ptr(),
              None if fused else self._g32("esm.encoder.emb_layer_norm_after.weight").data_ptr(),
              None if fused else self._g32("esm.encoder.emb_layer_norm_after.bias").data_ptr(),
-             self._g32(last_b2).data_ptr() if last_b2 else None, T, H, st)
+             self._g32(last_b2).data_ptr() if last_b2 else None, T, H, *self._drop_bwd(ws, 2 * L - 1), st)
         self._group_ready("esm.encoder.emb_layer_norm_after.bias")
         dx, dx_next = ws.dx, ws.dx_alt
         for l in reversed(range(L)):
@@ -653,10 +664,11 @@ class EsmForMaskedLM:
             ly = ws.layers[l]
             # FFN
             # bf16: ly.z holds GELU'(Z) from the forward epilogue (EPI_GELU_GRADAUX) -> plain multiply
-            self.linear_dgrad(dx, p + "output.dense.weight", H, F, ws.dz,
+            dbr = ws.dxd if ws.dxd is not None else dx  # FFN branch gradient (through its dropout mask)
+            self.linear_dgrad(dbr, p + "output.dense.weight", H, F, ws.dz,
                               epi=EPI_MUL_AUX if kdt == ESM_BF16 else EPI_DGELU, aux_in=ly.z,
                               col_sum=self._g32(p + "intermediate.dense.bias"))
-            self.linear_wgrad(dx, ly.a, p + "output.dense.weight", H, F)
+            self.linear_wgrad(dbr, ly.a, p + "output.dense.weight", H, F)
             fused = self.linear_dgrad(ws.dz, p + "intermediate.dense.weight", F, H, ws.dh,
                                       ln=(ly.x1, ly.ln2_m, ly.ln2_r, p + "LayerNorm"))
             self.linear_wgrad(ws.dz, ly.h2, p + "intermediate.dense.weight", F, H)
@@ -665,10 +677,11 @@ class EsmForMaskedLM:
                  dx.data_ptr(), None, ws.dx1.data_ptr(),
                  None if fused else self._g32(p + "LayerNorm.weight").data_ptr(),
                  None if fused else self._g32(p + "LayerNorm.bias").data_ptr(),
-                 self._g32(p + "attention.output.dense.bias").data_ptr(), T, H, st)
-            # attention
-            self.linear_dgrad(ws.dx1, p + "attention.output.dense.weight", H, H, ws.do)
-            self.linear_wgrad(ws.dx1, ly.o, p + "attention.output.dense.weight", H, H)
+                 self._g32(p + "attention.output.dense.bias").data_ptr(), T, H, *self._drop_bwd(ws, 2 * l), st)
+            # attention (branch gradient: through the out-projection's dropout mask)
+            dbr = ws.dxd if ws.dxd is not None else ws.dx1
+            self.linear_dgrad(dbr, p + "attention.output.dense.weight", H, H, ws.do)
+            self.linear_wgrad(dbr, ly.o, p + "attention.output.dense.weight", H, H)
             if kdt == ESM_BF16 and self._fused_attn_bwd(dh):
                 # fused: attention backward writes dqkv [T,3H] (RoPE^T, q-scale) + q/k/v bias grads
                 call("esm_attn_bwd_qkv", ly.q.data_ptr(), ly.k.data_ptr(), ly.v.data_ptr(), ly.o.data_ptr(),
@@ -691,7 +704,8 @@ class EsmForMaskedLM:
                  ws.dx1.data_ptr(), None, dx_next.data_ptr(),
                  None if fused else self._g32(p + "attention.LayerNorm.weight").data_ptr(),
                  None if fused else self._g32(p + "attention.LayerNorm.bias").data_ptr(),
-                 self._g32(prev_b2).data_ptr() if prev_b2 else None, T, H, st)
+                 self._g32(prev_b2).data_ptr() if prev_b2 else None, T, H,
+                 *(self._drop_bwd(ws, 2 * l - 1) if l > 0 else (None, None)), st)
             dx, dx_next = dx_next, dx
             self._group_ready(p + "attention.LayerNorm.bias")
         call("esm_embed_bwd", kdt, ws.input_ids.data_ptr(), ws.am.data_ptr(), ws.row_scale.data_ptr(),
@@ -708,6 +722,35 @@ class EsmForMaskedLM:
         return ws.loss_sum
 
     # ------------------------------------------------------------------ optimizer
+    def dropout_seed(self, step: int) -> int:
+        """The hidden-dropout seed of a step (splitmix64 of the model's base seed and the step)."""
+        z = (self.dropout_base + (int(step) + 1) * 0x9E3779B97F4A7C15) & 0xFFFFFFFFFFFFFFFF
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & 0xFFFFFFFFFFFFFFFF
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & 0xFFFFFFFFFFFFFFFF
+        return z ^ (z >> 31)
+
+    def set_dropout_seed(self, seed: int):
+        """Stage a hidden-dropout seed (set_hyper does this per step; a fill kernel, stream-ordered)."""
+        v = int(seed) & 0xFFFFFFFFFFFFFFFF
+        self.drop_seed.fill_(v - (1 << 64) if v >= (1 << 63) else v)
+        self.last_dropout_seed = v
+
+    def _drop_bwd(self, ws, site: int):
+        """(esm_dropout*, dx_drop) arguments of a LayerNorm backward whose input gradient also feeds the branch of
+        call site ``site`` (hidden dropout on), else (None, None)."""
+        d = self._drop(site)
+        if d is None:
+            return None, None
+        self._drop_keep = d  # ctypes object must outlive the call
+        return ctypes.byref(d), ws.dxd.data_ptr()
+
+    def _drop(self, site: int):
+        """esm_dropout of a call site (2*layer + 0 attention output / 1 FFN output), or None without dropout."""
+        if self.dropout_p <= 0.0:
+            return None
+        return _lib.Dropout(self.drop_seed.data_ptr(), site, int(round(self.dropout_p * 65536.0)),
+                            1.0 / (1.0 - self.dropout_p))
+
     def set_hyper(self, lr=None, step=None):
         """Stage AdamW hyper-parameters in device memory (read by the kernel: CUDA-graph safe)."""
         lr = self.lr if lr is None else lr
@@ -719,6 +762,8 @@ class EsmForMaskedLM:
         h.copy_(torch.tensor([lr, self.betas[0], self.betas[1], self.eps, self.weight_decay, float(step),
                               self.grad_scale, 0.0], dtype=torch.float32))
         self.hyper.copy_(h, non_blocking=True)
+        if self.dropout_p > 0.0:
+            self.set_dropout_seed(self.dropout_seed(step))
         ev = self._hyper_ev[i] = self._hyper_ev[i] or torch.cuda.Event()
         ev.record(torch.cuda.current_stream(self.device))
 

@@ -38,7 +38,7 @@ cs2 = torch.zeros(H, device="cuda")
 
 def lnb():
     _lib.call("esm_layernorm_bwd", ESM_BF16, dy.data_ptr(), x.data_ptr(), g.data_ptr(), mean.data_ptr(),
-              rstd.data_ptr(), dres.data_ptr(), None, dx.data_ptr(), None, None, cs2.data_ptr(), T, H, st)
+              rstd.data_ptr(), dres.data_ptr(), None, dx.data_ptr(), None, None, cs2.data_ptr(), T, H, None, None, st)
 
 
 def t(fn, n=20):

@@ -133,7 +133,7 @@ def ln():
         f = lambda: _lib.call("esm_layernorm_fwd", ESM_BF16, x.data_ptr(), g.data_ptr(), b.data_ptr(), y.data_ptr(),  # noqa
                               mu.data_ptr(), rs.data_ptr(), T, H, 1e-5, cur())
         bw = lambda: _lib.call("esm_layernorm_bwd", ESM_BF16, dy.data_ptr(), x.data_ptr(), g.data_ptr(), mu.data_ptr(),  # noqa
-                               rs.data_ptr(), dres.data_ptr(), None, dx.data_ptr(), None, None, None, T, H, cur())
+                               rs.data_ptr(), dres.data_ptr(), None, dx.data_ptr(), None, None, None, T, H, None, None, cur())
         tf, tb = timeit(f, iters=20), timeit(bw, iters=20)
         bf, bb = T * H * 4 + T * 8, T * H * 8 + T * 8
         print(f"layernorm T={T} H={H}: fwd {tf * 1e3:.1f} us ({bf / tf / 1e6:.0f} GB/s)  "

@@ -325,7 +325,8 @@ def test_layernorm(H, dt):
     db = torch.zeros(H, device=DEV)
     cs = torch.zeros(H, device=DEV)
     _lib.call("esm_layernorm_bwd", kdt, dy.data_ptr(), x.data_ptr(), g.data_ptr(), mean.data_ptr(), rstd.data_ptr(),
-              dres.data_ptr(), None, dx.data_ptr(), dg.data_ptr(), db.data_ptr(), cs.data_ptr(), rows, H, st())
+              dres.data_ptr(), None, dx.data_ptr(), dg.data_ptr(), db.data_ptr(), cs.data_ptr(), rows, H, None, None,
+              st())
     torch.cuda.synchronize()
     want = xr.grad + dres.float()
     assert rel(dx, want) < (2e-2 if dt == "bf16" else 1e-5)
@@ -516,7 +517,7 @@ def test_layernorm_bwd_no_stats(H, rows, gelu):
     cs = torch.zeros(H, device=DEV)
     _lib.call("esm_layernorm_bwd", ESM_BF16, dy.data_ptr(), x.data_ptr(), g.data_ptr(), mean.data_ptr(),
               rstd.data_ptr(), dres.data_ptr(), z.data_ptr() if gelu else None, dx.data_ptr(), None, None,
-              cs.data_ptr(), rows, H, st())
+              cs.data_ptr(), rows, H, None, None, st())
     torch.cuda.synchronize()
     want = xr.grad + dres.float()
     if gelu:
