@@ -52,9 +52,12 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true", help="skip the per-kernel CUDA-event breakdown")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--zero1", action="store_true", help="N>1: sharded optimizer (reduce-scatter / AdamW on the "
-                    "rank's slice / all-gather), the ZeRO-1 comparison point of PAPER.md:86-88")
+    ap.add_argument("--dp", default="zero1", choices=["zero1", "ddp"],
+                    help="N>1: zero1 = sharded optimizer (reduce-scatter / AdamW on the rank's slice / all-gather of "
+                         "the updated parameters; the ZeRO-1 comparison point of PAPER.md:86-88), ddp = all-reduce "
+                         "+ replicated AdamW")
     ap.add_argument("--grad-bf16", action="store_true", help="N>1: bf16 gradient buckets (half the NVLink bytes)")
+    ap.add_argument("--nvtx", action="store_true", help="NVTX ranges around the step phases and layers")
     ap.add_argument("--varlen", action="store_true",
                     help="protein-like lengths (lognormal(5.6, 0.65) clipped to [10, seq]) batched by the reference's "
                          "create_buckets / bucket_batches at a token budget of batch x seq (SURVEY.md §8d, §8f.1)")
@@ -308,8 +311,9 @@ def run_varlen(args, rank, world, local, dev):
     model.max_workspaces = len(shapes) + 1
     model.reserve(*max(shapes, key=lambda x: x[0] * x[1]))
     if world > 1:
-        model.comm = GradAllReducer(model.store)
-    use_graph = world == 1 and not args.no_graph
+        model.comm = GradAllReducer(model.store, grad_dtype="bf16" if args.grad_bf16 else "fp32",
+                                    shard_optimizer=args.dp == "zero1")
+    use_graph = not args.no_graph
     seed = 4321
 
     def step(i):
@@ -411,10 +415,11 @@ def main():
     S = args.seq or S
     cfg = preset(preset_name)
     model = EsmForMaskedLM(cfg, dtype=args.dtype, device=dev, seed=1)
+    model.nvtx = args.nvtx
     ws = model.workspace(B, S)
     if world > 1:
         model.comm = GradAllReducer(model.store, grad_dtype="bf16" if args.grad_bf16 else "fp32",
-                                    shard_optimizer=args.zero1)
+                                    shard_optimizer=args.dp == "zero1")
     use_graph = not args.no_graph  # N > 1: the NCCL bucket collectives are captured in the same graph
 
     gene = cfg.vocab_size > 40
@@ -632,7 +637,7 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
             "config": {"workload": f"{preset_name} MLM pre-training step (mask+fwd+bwd+AdamW), {B} x {S} per GPU",
                        "model": preset_name, "global_batch": B * world, "seq_len": S,
-                       "parallelism": f"dp{world}" + ("-zero1" if args.zero1 and world > 1 else "") +
+                       "parallelism": f"dp{world}" + ("-zero1" if args.dp == "zero1" and world > 1 else "") +
                                       ("-bf16grad" if args.grad_bf16 and world > 1 else ""),
                        "l2": "inputs/activations >> 126 MB L2 (no flush needed)",
                        "cuda_graph": use_graph, "weights": "random init",

@@ -266,6 +266,48 @@ __global__ void __launch_bounds__(64) dq_finalize_kernel(const float* __restrict
   }
 }
 
+// Vector variant: thread = (token, head, 4-column chunk of the first rotation half + its partner chunk); the
+// lanes of a token cover the whole fp32 dQ row (16-byte loads, whole sectors) and its bf16 q-slice of the dqkv
+// row (8-byte stores); tokens strided over the grid; bias partial sums leave with vector reductions.
+__global__ void __launch_bounds__(256) dq_finalize_vec_kernel(const float* __restrict__ dq,
+                                                              __nv_bfloat16* __restrict__ dqkv,
+                                                              float* __restrict__ csum, const float* __restrict__ cs,
+                                                              const float* __restrict__ sn, int64_t T_, int S, int nh,
+                                                              int dh, float qs) {
+  const int half = dh >> 1, cpr = half >> 2;
+  const int lanes = nh * cpr;
+  const int slots = blockDim.x / lanes;
+  const int slot = threadIdx.x / lanes, li = threadIdx.x - slot * lanes;
+  if (slot >= slots) return;
+  const int h = li / cpr, j = (li - h * cpr) * 4;
+  const int H = nh * dh;
+  float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
+  const int64_t stride = (int64_t)gridDim.x * slots;
+  for (int64_t t = (int64_t)blockIdx.x * slots + slot; t < T_; t += stride) {
+    const int s = (int)(t % S);
+    const float4 g0 = *reinterpret_cast<const float4*>(dq + t * H + h * dh + j);
+    const float4 g1 = *reinterpret_cast<const float4*>(dq + t * H + h * dh + j + half);
+    const float4 c = __ldg(reinterpret_cast<const float4*>(cs + (int64_t)s * half + j));
+    const float4 sv = __ldg(reinterpret_cast<const float4*>(sn + (int64_t)s * half + j));
+    const float4 q0 = make_float4((g0.x * c.x + g1.x * sv.x) * qs, (g0.y * c.y + g1.y * sv.y) * qs,
+                                  (g0.z * c.z + g1.z * sv.z) * qs, (g0.w * c.w + g1.w * sv.w) * qs);
+    const float4 q1 = make_float4((g1.x * c.x - g0.x * sv.x) * qs, (g1.y * c.y - g0.y * sv.y) * qs,
+                                  (g1.z * c.z - g0.z * sv.z) * qs, (g1.w * c.w - g0.w * sv.w) * qs);
+    __nv_bfloat16* row = dqkv + t * 3 * H + h * dh + j;
+    __nv_bfloat162 p0 = __floats2bfloat162_rn(q0.x, q0.y), p1 = __floats2bfloat162_rn(q0.z, q0.w);
+    __nv_bfloat162 p2 = __floats2bfloat162_rn(q1.x, q1.y), p3 = __floats2bfloat162_rn(q1.z, q1.w);
+    *reinterpret_cast<uint2*>(row) = make_uint2(*reinterpret_cast<uint32_t*>(&p0), *reinterpret_cast<uint32_t*>(&p1));
+    *reinterpret_cast<uint2*>(row + half) =
+        make_uint2(*reinterpret_cast<uint32_t*>(&p2), *reinterpret_cast<uint32_t*>(&p3));
+    a0.x += q0.x; a0.y += q0.y; a0.z += q0.z; a0.w += q0.w;
+    a1.x += q1.x; a1.y += q1.y; a1.z += q1.z; a1.w += q1.w;
+  }
+  if (csum) {
+    red_add_v4_f32(csum + h * dh + j, a0.x, a0.y, a0.z, a0.w);
+    red_add_v4_f32(csum + h * dh + j + half, a1.x, a1.y, a1.z, a1.w);
+  }
+}
+
 }  // namespace attn
 }  // namespace esm
 
@@ -351,6 +393,15 @@ extern "C" int esm_attn_bwd_qkv(const void* q, const void* k, const void* v, con
   const int rc = attn_bwd_tc(q, k, v, dout, lse2, delta, key_mask, sched, dq_ws, nullptr, nullptr, B, nh, S, dh, st,
                              dqkv, col_sum, cos_t, sin_t);
   if (rc) return rc;
+  const int lanes = nh * (dh / 8);  // vector path: threads per token
+  if (dh % 8 == 0 && lanes <= 256 && ((uintptr_t)col_sum & 15) == 0) {
+    const int slots = 256 / lanes;
+    const int64_t want = (T_ + (int64_t)slots * 16 - 1) / ((int64_t)slots * 16);  // ~16 tokens per thread
+    const int grid = (int)(want < device_sm_count() * 8 ? (want < 1 ? 1 : want) : device_sm_count() * 8);
+    attn::dq_finalize_vec_kernel<<<grid, slots * lanes, 0, st>>>(dq_ws, (__nv_bfloat16*)dqkv, col_sum, cos_t, sin_t,
+                                                                  T_, S, nh, dh, q_scale);
+    ESM_LAUNCH_RET();
+  }
   const int pairs = nh * dh / 2;
   const int rpb = 32;
   const int units = pairs / 2;  // two rotation pairs per thread

@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(256, SG ? (MAXV <= 2 ? 4 : 3) : 1) ln_fwd_kern
 // computes them in its epilogue, ESM_EPI_STORE_LN).  Rows are held as raw 16-byte vectors (bf16 packed)
 // and all of a row's loads are issued before the reduction.
 // SG (bf16, no dgamma/dbeta, <= 2 vectors per lane): gamma from shared memory, 3 CTAs per SM.
-template <typename T, int MAXV, int WPR, bool STATS, bool SG = false>
+template <typename T, int MAXV, int WPR, bool STATS, bool SG = false, bool DROP = false>
 __global__ void __launch_bounds__(256, SG ? 3 : (sizeof(T) == 2 && (MAXV <= 2 || !STATS)) ? 2 : 1)
     ln_bwd_kernel(const T* __restrict__ dy, const T* __restrict__ x, const float* __restrict__ g,
                   const float* __restrict__ mean, const float* __restrict__ rstd, const T* __restrict__ dres,
@@ -400,7 +400,8 @@ __global__ void __launch_bounds__(256, SG ? 3 : (sizeof(T) == 2 && (MAXV <= 2 ||
                   float* __restrict__ csum, int64_t rows, int H, const esm_dropout drop, T* __restrict__ dxd) {
   constexpr int VEC = vec16<T>::N;
   constexpr int GPB = 8 / WPR;
-  const DropKeys dk = dxd != nullptr ? drop_keys(drop) : DropKeys{0u, 0u, 0u, 1.f, false};
+  DropKeys dk{0u, 0u, 0u, 1.f, false};
+  if constexpr (DROP) dk = drop_keys(drop);
   __shared__ float2 red[GPB][2 * WPR];
   extern __shared__ float sacc[];  // [3][H] block-level partial sums
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -492,7 +493,7 @@ __global__ void __launch_bounds__(256, SG ? 3 : (sizeof(T) == 2 && (MAXV <= 2 ||
 #pragma unroll
           for (int j = 0; j < VEC; ++j) o[j] *= gelu_grad_f(zv[j]);
         }
-        if (dxd != nullptr) {  // gradient of the dropped-out branch (its bias gradient goes to csum)
+        if constexpr (DROP) {  // gradient of the dropped-out branch (its bias gradient goes to csum)
           const uint32_t rh = drop_row(dk, (uint32_t)r);
           float od[VEC];
 #pragma unroll
@@ -663,42 +664,40 @@ __global__ void __launch_bounds__(256) qkv_rope_bwd_kernel(const float* __restri
   }
 }
 
-// bf16 fast path (head_dim / 2 a multiple of 8): thread = (token, head, 8-column chunk of the first rotation half
-// and its partner chunk of the second half).  The lanes of a token cover consecutive heads / chunks, so the
-// head-major inputs are read in whole 32-byte sectors and the token-major dqkv row segment is written with
-// contiguous 16-byte stores; each thread walks a strided set of tokens with fixed columns and adds its q/k/v
-// bias-gradient partial sums with vector reductions at the end.
-__global__ void __launch_bounds__(256) qkv_rope_bwd_vec_kernel(const float* __restrict__ dq,
-                                                               const __nv_bfloat16* __restrict__ dk,
-                                                               const __nv_bfloat16* __restrict__ dv,
-                                                               __nv_bfloat16* __restrict__ dqkv,
-                                                               float* __restrict__ csum, const float* __restrict__ cs,
-                                                               const float* __restrict__ sn, int64_t T_, int S, int nh,
-                                                               int dh, float qs) {
-  const int half = dh >> 1, cpr = half >> 3;  // chunks per rotation half
-  const int lanes = nh * cpr;                 // threads per token
-  const int slots = blockDim.x / lanes;       // tokens per block iteration
-  const int slot = threadIdx.x / lanes, li = threadIdx.x - slot * lanes;
-  if (slot >= slots) return;
-  const int h = li / cpr, j = (li - h * cpr) * 8;
-  const int H = nh * dh;
-  float aq[16], ak[16], av[16];
+// bf16 fast path (head_dim % 16 == 0): block = one head x a tile of TT consecutive tokens; thread = (token,
+// 8-column chunk of the first rotation half + its partner chunk of the second half).  The block streams each
+// head-major input as one contiguous region (TT x dh elements) and writes the token-major dqkv rows in whole
+// 128-byte lines (dh = 64); q/k/v bias partial sums are reduced across the block's tokens with warp shuffles and
+// shared memory before one atomic add per column.
+template <int CPR>  // 8-column chunks per rotation half (dh / 16)
+__global__ void __launch_bounds__(256) qkv_rope_bwd_tile_kernel(const float* __restrict__ dq,
+                                                                const __nv_bfloat16* __restrict__ dk,
+                                                                const __nv_bfloat16* __restrict__ dv,
+                                                                __nv_bfloat16* __restrict__ dqkv,
+                                                                float* __restrict__ csum, const float* __restrict__ cs,
+                                                                const float* __restrict__ sn, int T_, int S, int nh,
+                                                                float qs, int TT) {
+  constexpr int DH = CPR * 16, HALF = DH / 2, TPB = 256 / CPR;
+  __shared__ float red[8][CPR][48];
+  const int h = blockIdx.y;
+  const int chunk = threadIdx.x % CPR, sub = threadIdx.x / CPR, j = chunk * 8;
+  const int H = nh * DH;
+  float acc[48];
 #pragma unroll
-  for (int i = 0; i < 16; ++i) aq[i] = ak[i] = av[i] = 0.f;
-  const int64_t stride = (int64_t)gridDim.x * slots;
-  for (int64_t t = (int64_t)blockIdx.x * slots + slot; t < T_; t += stride) {
-    const int64_t b = t / S;
-    const int s = (int)(t - b * S);
-    const int64_t o = ((b * nh + h) * S + s) * dh + j;
+  for (int i = 0; i < 48; ++i) acc[i] = 0.f;
+  const int t_begin = blockIdx.x * TT, t_end = min(T_, t_begin + TT);
+  for (int t = t_begin + sub; t < t_end; t += TPB) {
+    const int b = t / S, s = t - b * S;
+    const int64_t o = (((int64_t)b * nh + h) * S + s) * DH + j;
     float g0[8], g1[8], e0[8], e1[8], v0[8], v1[8], c[8], sv[8];
     load_f32x(dq + o, g0, 8);
-    load_f32x(dq + o + half, g1, 8);
+    load_f32x(dq + o + HALF, g1, 8);
     load_vec(dk + o, e0);
-    load_vec(dk + o + half, e1);
+    load_vec(dk + o + HALF, e1);
     load_vec(dv + o, v0);
-    load_vec(dv + o + half, v1);
-    load_f32x(cs + (int64_t)s * half + j, c, 8);
-    load_f32x(sn + (int64_t)s * half + j, sv, 8);
+    load_vec(dv + o + HALF, v1);
+    load_f32x(cs + s * HALF + j, c, 8);
+    load_f32x(sn + s * HALF + j, sv, 8);
     float q0[8], q1[8], k0[8], k1[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {  // RoPE^T: dx_j = dy_j c + dy_{j+h} s ; dx_{j+h} = dy_{j+h} c - dy_j s
@@ -706,32 +705,40 @@ __global__ void __launch_bounds__(256) qkv_rope_bwd_vec_kernel(const float* __re
       q1[e] = (g1[e] * c[e] - g0[e] * sv[e]) * qs;
       k0[e] = e0[e] * c[e] + e1[e] * sv[e];
       k1[e] = e1[e] * c[e] - e0[e] * sv[e];
-      aq[e] += q0[e];
-      aq[8 + e] += q1[e];
-      ak[e] += k0[e];
-      ak[8 + e] += k1[e];
-      av[e] += v0[e];
-      av[8 + e] += v1[e];
+      acc[e] += q0[e];
+      acc[8 + e] += q1[e];
+      acc[16 + e] += k0[e];
+      acc[24 + e] += k1[e];
+      acc[32 + e] += v0[e];
+      acc[40 + e] += v1[e];
     }
-    __nv_bfloat16* row = dqkv + t * 3 * H + h * dh + j;
+    __nv_bfloat16* row = dqkv + (int64_t)t * 3 * H + h * DH + j;
     store_vec(row, q0);
-    store_vec(row + half, q1);
+    store_vec(row + HALF, q1);
     store_vec(row + H, k0);
-    store_vec(row + H + half, k1);
+    store_vec(row + H + HALF, k1);
     store_vec(row + 2 * H, v0);
-    store_vec(row + 2 * H + half, v1);
+    store_vec(row + 2 * H + HALF, v1);
   }
-  if (csum) {
-    float* cq = csum + h * dh + j;
+  if (csum == nullptr) return;
+  // lanes with the same chunk (lane % CPR) hold partial sums of different tokens
 #pragma unroll
-    for (int e = 0; e < 8; e += 4) {
-      red_add_v4_f32(cq + e, aq[e], aq[e + 1], aq[e + 2], aq[e + 3]);
-      red_add_v4_f32(cq + half + e, aq[8 + e], aq[9 + e], aq[10 + e], aq[11 + e]);
-      red_add_v4_f32(cq + H + e, ak[e], ak[e + 1], ak[e + 2], ak[e + 3]);
-      red_add_v4_f32(cq + H + half + e, ak[8 + e], ak[9 + e], ak[10 + e], ak[11 + e]);
-      red_add_v4_f32(cq + 2 * H + e, av[e], av[e + 1], av[e + 2], av[e + 3]);
-      red_add_v4_f32(cq + 2 * H + half + e, av[8 + e], av[9 + e], av[10 + e], av[11 + e]);
-    }
+  for (int off = CPR; off < 32; off <<= 1)
+#pragma unroll
+    for (int i = 0; i < 48; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], off);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane < CPR)
+#pragma unroll
+    for (int i = 0; i < 48; ++i) red[w][lane][i] = acc[i];
+  __syncthreads();
+  for (int i = threadIdx.x; i < CPR * 48; i += blockDim.x) {
+    const int ch = i / 48, k = i - ch * 48;
+    float v = 0.f;
+#pragma unroll
+    for (int ww = 0; ww < 8; ++ww) v += red[ww][ch][k];
+    const int part = k >> 3, e = k & 7;  // part: q lo, q hi, k lo, k hi, v lo, v hi
+    const int col = (part >> 1) * H + h * DH + ch * 8 + (part & 1) * HALF + e;
+    atomicAdd(csum + col, v);
   }
 }
 
@@ -1170,7 +1177,7 @@ int esm_embed_bwd(int dtype, const int32_t* ids, const int32_t* am, const float*
     ESM_LAUNCH_RET();
   }
   const int vec = dtype == ESM_BF16 ? 8 : 4;
-  const int cols = H < 1280 ? H : 1280;                       // columns per block (<= 165 KB of partials at V 33)
+  const int cols = std::min(H, std::min(1280, 256 * vec));    // columns per block (<= 165 KB of partials at V 33)
   const int bx = ((cols / vec) + 31) / 32 * 32;
   const int gx = (H + bx * vec - 1) / (bx * vec);
   const int gy = (int)std::max<int64_t>(1, std::min<int64_t>((T_ + 63) / 64, device_sm_count() / gx));
@@ -1303,7 +1310,31 @@ int esm_layernorm_bwd(int dtype, const void* dy, const void* x, const float* gam
                                               (const TT*)dres, (const TT*)gelu_z, (TT*)dx, dgamma,   \
                                               dbeta, col_sum, rows, H, dr, (TT*)dxd);                \
   } while (0)
-  if (dtype == ESM_BF16) {
+  if (dxd != nullptr) {  // hidden dropout: the branch-gradient variant (no fused dgamma/dbeta in bf16)
+    if (dtype == ESM_BF16) {
+      using TT = __nv_bfloat16;
+      if (stats) {
+#define KS(A, B) ln_bwd_kernel<TT, A, B, true, false, true>
+        LN_SWITCH2(KS);
+#undef KS
+      } else {
+#define KS(A, B) ln_bwd_kernel<TT, A, B, false, false, true>
+        LN_SWITCH2(KS);
+#undef KS
+      }
+    } else {
+      using TT = float;
+      if (stats) {
+#define KS(A, B) ln_bwd_kernel<TT, A, B, true, false, true>
+        LN_SWITCH2(KS);
+#undef KS
+      } else {
+#define KS(A, B) ln_bwd_kernel<TT, A, B, false, false, true>
+        LN_SWITCH2(KS);
+#undef KS
+      }
+    }
+  } else if (dtype == ESM_BF16) {
     using TT = __nv_bfloat16;
     if (stats) {
 #define KS(A, B) ln_bwd_kernel<TT, A, B, true>
@@ -1354,16 +1385,17 @@ int esm_qkv_rope_bwd(int dtype, const float* dq, const void* dk, const void* dv,
                      esm_stream_t stream) {
   ESM_CHECK_ARG(dq && dk && dv && dqkv && cos_t && sin_t && dh % 4 == 0, "esm_qkv_rope_bwd: bad args (dh %% 4)");
   const int64_t T_ = (int64_t)B * Sq;
-  const int lanes = nh * (dh / 16);  // vector path: threads per token
-  if (dtype == ESM_BF16 && dh % 16 == 0 && lanes <= 256 && (!col_sum || ((uintptr_t)col_sum & 15) == 0)) {
-    const int slots = 256 / lanes;
-    const int tokens_per_thread = 16;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((T_ + (int64_t)slots * tokens_per_thread - 1) /
-                                                                     ((int64_t)slots * tokens_per_thread),
-                                                                 (int64_t)device_sm_count() * 8));
-    qkv_rope_bwd_vec_kernel<<<grid, slots * lanes, 0, S(stream)>>>(
-        dq, (const __nv_bfloat16*)dk, (const __nv_bfloat16*)dv, (__nv_bfloat16*)dqkv, col_sum, cos_t, sin_t, T_, Sq,
-        nh, dh, q_scale);
+  if (dtype == ESM_BF16 && (dh == 16 || dh == 32 || dh == 64) && T_ < (1ll << 31)) {
+    const int TT = 512;  // tokens per block (one head)
+    dim3 grid((unsigned)((T_ + TT - 1) / TT), (unsigned)nh);
+#define QRB(CPR)                                                                                                  \
+  qkv_rope_bwd_tile_kernel<CPR><<<grid, 256, 0, S(stream)>>>(dq, (const __nv_bfloat16*)dk, (const __nv_bfloat16*)dv, \
+                                                             (__nv_bfloat16*)dqkv, col_sum, cos_t, sin_t, (int)T_, \
+                                                             Sq, nh, q_scale, TT)
+    if (dh == 16) QRB(1);
+    else if (dh == 32) QRB(2);
+    else QRB(4);
+#undef QRB
     ESM_LAUNCH_RET();
   }
   const int units = nh * dh / 4;  // two rotation pairs per thread

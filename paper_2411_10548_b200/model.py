@@ -337,6 +337,7 @@ class EsmForMaskedLM:
         self.timer = None  # optional KernelTimer (bench.py per-kernel roofline)
         self._opt_on, self._opt_start, self._opt_stream = False, 0, None
         self.launches = 0  # kernels launched by this model (C-ABI calls x kernels per call)
+        self.nvtx = False  # NVTX ranges (forward / backward / layers) for nsys-style timelines
         self.graph = None
         self.graph_launches = 0
         self._hyper_ring = [torch.zeros(8, dtype=torch.float32).pin_memory() for _ in range(4)]
@@ -422,6 +423,16 @@ class EsmForMaskedLM:
         self.graph = None
         self._arena = None
         torch.cuda.empty_cache()
+
+    def _nvtx(self, name, pop_first: bool = False):
+        """NVTX ranges around the step's phases and layers (``model.nvtx = True``; host-side only, so they also
+        appear around graph capture).  name=None pops."""
+        if not self.nvtx:
+            return
+        if name is None or pop_first:
+            torch.cuda.nvtx.range_pop()
+        if name is not None:
+            torch.cuda.nvtx.range_push(name)
 
     # kernels launched per C-ABI entry point (for the bench's gpu_launches count)
     _KERNELS = {"esm_embed_fwd": 2, "esm_attn_bwd": 3, "esm_attn_bwd_qkv": 4, "esm_lmhead_xent": 2}
@@ -590,9 +601,11 @@ class EsmForMaskedLM:
         sched = ws.attn_sched.data_ptr()
         call("esm_attn_prepare", ws.am.data_ptr(), sched, B, S, st)  # key-mask scan: once per step, not per layer
         # ---------------- forward
+        self._nvtx("forward")
         call("esm_embed_fwd", kdt, ws.input_ids.data_ptr(), ws.am.data_ptr(), E.data_ptr(), ws.x[0].data_ptr(),
              ws.row_scale.data_ptr(), B, S, H, int(cfg.token_dropout), cfg.mask_token_id, st)
         for l in range(L):
+            self._nvtx(f"layer{l}.fwd", l > 0)
             p = f"esm.encoder.layer.{l}."
             ly = ws.layers[l]
             x = ws.x[l]
@@ -617,6 +630,7 @@ class EsmForMaskedLM:
                             epi=EPI_GELU_GRADAUX if kdt == ESM_BF16 else EPI_GELU, aux_out=ly.z)
             self.linear_fwd(ly.a, p + "output.dense.weight", H, F, p + "output.dense.bias", ws.x[l + 1],
                             epi=EPI_RESID, aux_in=ly.x1, drop=self._drop(2 * l + 1))
+        self._nvtx("lm_head+xent", L > 0)
         call("esm_layernorm_fwd", kdt, ws.x[L].data_ptr(),
              self._p32("esm.encoder.emb_layer_norm_after.weight").data_ptr(),
              self._p32("esm.encoder.emb_layer_norm_after.bias").data_ptr(), ws.xf.data_ptr(), ws.lnf_m.data_ptr(),
@@ -631,11 +645,14 @@ class EsmForMaskedLM:
             call("esm_lmhead_xent", kdt, ws.n.data_ptr(), E.data_ptr(), self._p32("lm_head.bias").data_ptr(),
                  ws.labels.data_ptr(), ws.inv_denom.data_ptr(), ws.loss_sum.data_ptr(), ws.dlogits.data_ptr(),
                  ws.dn.data_ptr(), self._g32(E_key).data_ptr(), self._g32("lm_head.bias").data_ptr(), T, H, V, st)
+        self._nvtx(None)
+        self._nvtx(None)
         if loss_only:
             if self.comm is not None:
                 self.comm.reduce_loss(ws.loss_sum)
             return ws.loss_sum
         # ---------------- backward
+        self._nvtx("backward")
         self._opt_on = optimizer
         self._opt_start = 0
         if self.comm is not None:
@@ -660,6 +677,7 @@ class EsmForMaskedLM:
         self._group_ready("esm.encoder.emb_layer_norm_after.bias")
         dx, dx_next = ws.dx, ws.dx_alt
         for l in reversed(range(L)):
+            self._nvtx(f"layer{l}.bwd", l < L - 1)
             p = f"esm.encoder.layer.{l}."
             ly = ws.layers[l]
             # FFN
@@ -708,6 +726,8 @@ class EsmForMaskedLM:
                  *(self._drop_bwd(ws, 2 * l - 1) if l > 0 else (None, None)), st)
             dx, dx_next = dx_next, dx
             self._group_ready(p + "attention.LayerNorm.bias")
+        if L > 0:
+            self._nvtx(None)
         call("esm_embed_bwd", kdt, ws.input_ids.data_ptr(), ws.am.data_ptr(), ws.row_scale.data_ptr(),
              dx.data_ptr(), self._g32(E_key).data_ptr(), B, S, H, V,
              cfg.mask_token_id if cfg.token_dropout else -1, cfg.pad_token_id, st)
@@ -719,6 +739,7 @@ class EsmForMaskedLM:
             self._adamw_range(self._opt_start, self.store.numel, None)  # word embeddings: last, on the compute stream
             torch.cuda.current_stream(self.device).wait_stream(self._opt_stream)
         self._last_dx_embed = dx
+        self._nvtx(None)
         return ws.loss_sum
 
     # ------------------------------------------------------------------ optimizer
