@@ -14,33 +14,83 @@ namespace attn {
 constexpr float L2E = 1.4426950408889634f;
 
 // ---------------------------------------------------------------------------- backward
-// delta[q] = sum_d dO[q,d] * O[q,d]; one thread per (token, head): consecutive threads read consecutive
-// heads of a token, i.e. contiguous 16-byte vectors of the token-major [T, H] rows.
-template <typename T>
-__global__ void delta_kernel(const T* __restrict__ O, const T* __restrict__ dO, float* __restrict__ delta,
-                             const float* __restrict__ lse, float* __restrict__ lse2, int64_t T_, int S, int nh,
-                             int dh) {
+// delta[b,h,s] = sum_d dO[t,h,d] * O[t,h,d] (t = b*S + s) and lse2 = -lse * log2(e).  Thread = one (head,
+// token); consecutive threads take consecutive tokens of one head, so the per-(b,h,s) writes (and the lse reads)
+// are contiguous, and each thread reads its token's DH-element slices of O and dO as whole 16-byte vectors
+// (unrolled at compile time: all of a thread's loads are in flight at once).
+template <typename T, int DH>
+__global__ void __launch_bounds__(256) delta_kernel(const T* __restrict__ O, const T* __restrict__ dO,
+                                                    float* __restrict__ delta, const float* __restrict__ lse,
+                                                    float* __restrict__ lse2, int64_t T_, int S, int nh) {
   constexpr int VEC = vec16<T>::N;
-  const int H = nh * dh;
+  constexpr int NV = (DH + VEC - 1) / VEC;
+  const int H = nh * DH;
   const int64_t total = T_ * nh;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t t = i / nh;
-    const int h = (int)(i - t * nh);
-    const T* o = O + t * H + h * dh;
-    const T* g = dO + t * H + h * dh;
+    const int64_t h = i / T_, t = i - h * T_;
+    const T* o = O + t * H + h * DH;
+    const T* g = dO + t * H + h * DH;
     float acc = 0.f;
-    for (int d = 0; d < dh; d += VEC) {
-      float a[VEC], c[VEC];
-      load_vec(o + d, a);
-      load_vec(g + d, c);
+    if constexpr (DH % VEC == 0) {
+      uint4 ov[NV], gv[NV];
 #pragma unroll
-      for (int e = 0; e < VEC; ++e) acc += a[e] * c[e];
+      for (int k = 0; k < NV; ++k) {
+        ov[k] = *reinterpret_cast<const uint4*>(o + k * VEC);
+        gv[k] = *reinterpret_cast<const uint4*>(g + k * VEC);
+      }
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        float a[VEC], c[VEC];
+        load_vec(reinterpret_cast<const T*>(&ov[k]), a);
+        load_vec(reinterpret_cast<const T*>(&gv[k]), c);
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) acc = fmaf(a[e], c[e], acc);
+      }
+    } else {
+#pragma unroll
+      for (int d = 0; d < DH; ++d) acc = fmaf(io<T>::ld(o + d), io<T>::ld(g + d), acc);
     }
-    const int64_t b = t / S, s = t % S;
+    const int64_t b = t / S, s = t - b * S;
     const int64_t idx = (b * nh + h) * S + s;
     delta[idx] = acc;
     if (lse2) lse2[idx] = -lse[idx] * L2E;  // negated log2-domain LSE (an FFMA2 addend in the tcgen05 backward)
   }
+}
+
+// generic head dim (fp32 parity mode): one thread per (token, head)
+template <typename T>
+__global__ void delta_generic_kernel(const T* __restrict__ O, const T* __restrict__ dO, float* __restrict__ delta,
+                                     const float* __restrict__ lse, float* __restrict__ lse2, int64_t T_, int S,
+                                     int nh, int dh) {
+  const int H = nh * dh;
+  const int64_t total = T_ * nh;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t h = i / T_, t = i - h * T_;
+    float acc = 0.f;
+    for (int d = 0; d < dh; ++d) acc += io<T>::ld(O + t * H + h * dh + d) * io<T>::ld(dO + t * H + h * dh + d);
+    const int64_t b = t / S, s = t - b * S;
+    const int64_t idx = (b * nh + h) * S + s;
+    delta[idx] = acc;
+    if (lse2) lse2[idx] = -lse[idx] * L2E;
+  }
+}
+
+template <typename T>
+int launch_delta(const void* o, const void* dout, float* delta, const float* lse, float* lse2, int64_t T_, int S,
+                 int nh, int dh, cudaStream_t st) {
+  const int64_t work = T_ * nh;
+  int grid = (int)((work + 255) / 256);
+  if (grid > device_sm_count() * 16) grid = device_sm_count() * 16;
+  const T* O = (const T*)o;
+  const T* dO = (const T*)dout;
+  switch (dh) {
+    case 16: delta_kernel<T, 16><<<grid, 256, 0, st>>>(O, dO, delta, lse, lse2, T_, S, nh); break;
+    case 24: delta_kernel<T, 24><<<grid, 256, 0, st>>>(O, dO, delta, lse, lse2, T_, S, nh); break;
+    case 32: delta_kernel<T, 32><<<grid, 256, 0, st>>>(O, dO, delta, lse, lse2, T_, S, nh); break;
+    case 64: delta_kernel<T, 64><<<grid, 256, 0, st>>>(O, dO, delta, lse, lse2, T_, S, nh); break;
+    default: delta_generic_kernel<T><<<grid, 256, 0, st>>>(O, dO, delta, lse, lse2, T_, S, nh, dh); break;
+  }
+  return 0;
 }
 
 // ---------------------------------------------------------------------------- fp32 SIMT
@@ -349,14 +399,11 @@ extern "C" int esm_attn_bwd(int dtype, const void* q, const void* k, const void*
   ESM_CHECK_ARG(q && k && v && o && dout && lse && delta && dq && dk && dv, "esm_attn_bwd: null pointer");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int64_t T_ = (int64_t)B * S;
-  int dgrid = (int)((T_ * nh + 255) / 256);
-  if (dgrid > device_sm_count() * 32) dgrid = device_sm_count() * 32;
   if (dtype == ESM_BF16) {
     ESM_CHECK_ARG(sched != nullptr, "esm_attn_bwd: bf16 needs the scheduling workspace (esm_attn_prepare)");
     ESM_CHECK_ARG(S % 4 == 0, "esm_attn_bwd: bf16 needs S %% 4 == 0 (pad the batch)");
     float* lse2 = delta + T_ * nh;  // workspace [2, B, nh, S]: Delta then log2-domain LSE
-    attn::delta_kernel<__nv_bfloat16><<<dgrid, 256, 0, st>>>((const __nv_bfloat16*)o, (const __nv_bfloat16*)dout,
-                                                             delta, lse, lse2, T_, S, nh, dh);
+    attn::launch_delta<__nv_bfloat16>(o, dout, delta, lse, lse2, T_, S, nh, dh, st);
     cudaMemsetAsync(dq, 0, sizeof(float) * T_ * nh * dh, st);
     const int rc = attn_bwd_tc(q, k, v, dout, lse2, delta, key_mask, sched, dq, dk, dv, B, nh, S, dh, st, nullptr,
                                nullptr, nullptr, nullptr);
@@ -365,8 +412,7 @@ extern "C" int esm_attn_bwd(int dtype, const void* q, const void* k, const void*
   }
   ESM_CHECK_ARG(dh <= attn::MAXD, "esm_attn_bwd: dh <= 64");
   dim3 grid((S + 63) / 64, B * nh);
-  attn::delta_kernel<float><<<dgrid, 256, 0, st>>>((const float*)o, (const float*)dout, delta, lse, nullptr, T_, S, nh,
-                                                   dh);
+  attn::launch_delta<float>(o, dout, delta, lse, nullptr, T_, S, nh, dh, st);
   attn::bwd_dq_f32_kernel<<<grid, 64, 0, st>>>((const float*)q, (const float*)k, (const float*)v, (const float*)dout,
                                                lse, delta, key_mask, dq, S, nh, dh);
   attn::bwd_dkv_f32_kernel<<<grid, 64, 0, st>>>((const float*)q, (const float*)k, (const float*)v,
@@ -384,11 +430,8 @@ extern "C" int esm_attn_bwd_qkv(const void* q, const void* k, const void* v, con
   ESM_CHECK_ARG(S % 4 == 0 && dh % 8 == 0, "esm_attn_bwd_qkv: needs S %% 4 == 0 and dh %% 8 == 0");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int64_t T_ = (int64_t)B * S;
-  int dgrid = (int)((T_ * nh + 255) / 256);
-  if (dgrid > device_sm_count() * 32) dgrid = device_sm_count() * 32;
   float* lse2 = delta + T_ * nh;
-  attn::delta_kernel<__nv_bfloat16><<<dgrid, 256, 0, st>>>((const __nv_bfloat16*)o, (const __nv_bfloat16*)dout,
-                                                           delta, lse, lse2, T_, S, nh, dh);
+  attn::launch_delta<__nv_bfloat16>(o, dout, delta, lse, lse2, T_, S, nh, dh, st);
   cudaMemsetAsync(dq_ws, 0, sizeof(float) * T_ * nh * dh, st);
   const int rc = attn_bwd_tc(q, k, v, dout, lse2, delta, key_mask, sched, dq_ws, nullptr, nullptr, B, nh, S, dh, st,
                              dqkv, col_sum, cos_t, sin_t);

@@ -1426,7 +1426,8 @@ int esm_lmhead_xent(int dtype, const void* n, const void* E, const float* bias, 
     const size_t pad = dtype == ESM_BF16 ? 2 : 1;
     const size_t smem = (((size_t)V * (H + pad) * esz + 15) & ~(size_t)15) + 8 * 64 * 4 + 8 * (size_t)H * esz;
     if (smem <= 200 * 1024 && H % 8 == 0) {
-      const int g = grid_for((int64_t)T_ * 32, 256, device_sm_count() * 4);
+      // one resident wave (2 CTAs / SM): every CTA stages E once, so more CTAs only re-copy it
+      const int g = grid_for((int64_t)T_ * 32, 256, device_sm_count() * 2);
       if (dtype == ESM_BF16) {
         cudaFuncSetAttribute(xent_small_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         xent_small_kernel<__nv_bfloat16><<<g, 256, smem, S(stream)>>>(

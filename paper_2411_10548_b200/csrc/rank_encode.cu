@@ -34,66 +34,81 @@ __global__ void __launch_bounds__(1024) rank_encode_kernel(const int64_t* __rest
                                                            int pad_id, int offset, int32_t* __restrict__ ids,
                                                            int32_t* __restrict__ am, int32_t* __restrict__ lengths,
                                                            int32_t* __restrict__ status, int cap) {
-  extern __shared__ uint64_t sm_keys[];  // [P] keys, then [P] uint32 cols
+  extern __shared__ uint64_t sm_keys[];  // [cap] keys, then [cap] uint32 cols (cap = staging capacity, pow2)
   const int b = blockIdx.x, tid = threadIdx.x;
   const int64_t r = rows ? rows[b] : b;
   const int64_t beg = indptr[r], n64 = indptr[r + 1] - beg;
   int32_t* out = ids + (int64_t)b * S;
   int32_t* mk = am + (int64_t)b * S;
-  if (n64 > cap || n64 < 0) {  // row larger than the staging capacity the host sized
+  int64_t keep64 = n64 < max_len ? n64 : max_len;
+  if (keep64 > S) keep64 = S;
+  const int K = (int)keep64;  // tokens written
+  if (n64 < 0 || (n64 > cap && K > cap / 2)) {  // a long row whose kept prefix does not fit the streaming top-K
     if (tid == 0) atomicExch(status, 2);
     for (int i = tid; i < S; i += blockDim.x) { out[i] = pad_id; mk[i] = 0; }
     if (tid == 0 && lengths) lengths[b] = 0;
     return;
   }
-  const int n = (int)n64;
+  // rows up to the staging capacity: one sort of the next power of two >= n.  Longer rows: streaming top-K --
+  // slots [0, K) hold the best K so far, each chunk of cap - K entries is loaded behind them and the whole
+  // buffer re-sorted, so [0, K) ends as the K smallest (key, col) of the row, i.e. exactly the prefix a full
+  // sort would give.
   int P = 1;
-  while (P < n) P <<= 1;
+  while (P < n64 && P < cap) P <<= 1;
   uint64_t* key = sm_keys;
   uint32_t* col = reinterpret_cast<uint32_t*>(sm_keys + P);
-  for (int i = tid; i < P; i += blockDim.x) {
-    if (i < n) {
-      const int64_t c = cols[beg + i];
-      if (c < 0 || c >= n_genes) {
-        atomicExch(status, 1);
+  const bool stream = n64 > P;
+  const int head = stream ? K : 0;
+  const int64_t chunk = P - head;
+  for (int i = tid; i < head; i += blockDim.x) {
+    key[i] = ~0ull;
+    col[i] = 0xFFFFFFFFu;
+  }
+  for (int64_t c0 = 0; c0 < n64 || c0 == 0; c0 += chunk) {
+    for (int i = head + tid; i < P; i += blockDim.x) {
+      const int64_t e = c0 + (i - head);
+      if (e < n64) {
+        const int64_t c = cols[beg + e];
+        if (c < 0 || c >= n_genes) {
+          atomicExch(status, 1);
+          key[i] = ~0ull;
+          col[i] = 0xFFFFFFFFu;
+        } else {
+          key[i] = desc_key((double)vals[beg + e] / (double)medians[c]);
+          col[i] = (uint32_t)c;
+        }
+      } else {  // padding sorts after every real element
         key[i] = ~0ull;
         col[i] = 0xFFFFFFFFu;
-      } else {
-        key[i] = desc_key((double)vals[beg + i] / (double)medians[c]);
-        col[i] = (uint32_t)c;
       }
-    } else {  // padding sorts after every real element
-      key[i] = ~0ull;
-      col[i] = 0xFFFFFFFFu;
     }
-  }
-  __syncthreads();
-  // bitonic sort, ascending by (key, col)
-  for (int k = 2; k <= P; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = tid; i < P; i += blockDim.x) {
-        const int l = i ^ j;
-        if (l > i) {
-          const bool up = (i & k) == 0;
-          const uint64_t ki = key[i], kl = key[l];
-          const uint32_t ci = col[i], cl = col[l];
-          if (pair_less(kl, cl, ki, ci) == up) {
-            key[i] = kl; key[l] = ki;
-            col[i] = cl; col[l] = ci;
+    __syncthreads();
+    // bitonic sort, ascending by (key, col)
+    for (int k = 2; k <= P; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int i = tid; i < P; i += blockDim.x) {
+          const int l = i ^ j;
+          if (l > i) {
+            const bool up = (i & k) == 0;
+            const uint64_t ki = key[i], kl = key[l];
+            const uint32_t ci = col[i], cl = col[l];
+            if (pair_less(kl, cl, ki, ci) == up) {
+              key[i] = kl; key[l] = ki;
+              col[i] = cl; col[l] = ci;
+            }
           }
         }
+        __syncthreads();
       }
-      __syncthreads();
     }
+    if (!stream) break;
   }
-  int len = n < max_len ? n : max_len;
-  if (len > S) len = S;
   for (int i = tid; i < S; i += blockDim.x) {
-    const bool v = i < len;
+    const bool v = i < K;
     out[i] = v ? (int32_t)col[i] + offset : pad_id;
     mk[i] = v ? 1 : 0;
   }
-  if (tid == 0 && lengths) lengths[b] = len;
+  if (tid == 0 && lengths) lengths[b] = K;
 }
 
 }  // namespace esm
@@ -106,10 +121,10 @@ extern "C" int esm_rank_encode(const int64_t* indptr, const int64_t* cols, const
   ESM_CHECK_ARG(indptr && medians && ids && am && status && n_rows >= 0 && max_len >= 0 && S > 0 && n_genes > 0 &&
                     n_genes < 0xFFFFFFFFll,
                 "esm_rank_encode: bad args");
-  ESM_CHECK_ARG(max_nnz >= 0 && max_nnz <= 16384, "esm_rank_encode: max_nnz must be <= 16384");
+  ESM_CHECK_ARG(max_nnz >= 0, "esm_rank_encode: max_nnz >= 0");
   if (n_rows == 0) return 0;
-  int P = 1;
-  while (P < max_nnz) P <<= 1;
+  int P = 1;  // staging capacity: next power of two >= the longest row, at most 16384 (192 KB of shared memory)
+  while (P < max_nnz && P < 16384) P <<= 1;
   const size_t smem = (size_t)P * (sizeof(uint64_t) + sizeof(uint32_t));
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(rank_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -120,6 +135,6 @@ extern "C" int esm_rank_encode(const int64_t* indptr, const int64_t* cols, const
   }
   const int threads = P >= 1024 ? 1024 : (P < 64 ? 64 : P);
   rank_encode_kernel<<<n_rows, threads, smem, S_rank(stream)>>>(indptr, cols, vals, medians, n_genes, rows, max_len,
-                                                                 S, 0, 2, ids, am, lengths, status, max_nnz);
+                                                                 S, 0, 2, ids, am, lengths, status, P);
   ESM_LAUNCH_RET();
 }

@@ -113,7 +113,7 @@ class RankEncoder:
     already collated into the [B, S] int32 tensors the train step consumes (PAD 0 past each length).
     """
 
-    MAX_NNZ = 16384  # shared-memory staging limit of the sort (one CTA per row)
+    STAGE = 16384  # shared-memory staging capacity of the sort (one CTA per row); longer rows stream through it
 
     def __init__(self, medians: np.ndarray, device=None):
         _lib.load()
@@ -143,11 +143,12 @@ class RankEncoder:
     def encode_device(self, d_indptr, d_cols, d_vals, n_rows: int, max_nnz: int, seq_len: int,
                       max_len: int | None = None, ids=None, am=None, lengths=None, stream=None):
         """Kernel launch on device CSR (rows 0..n_rows-1); writes ids/am (allocated if None)."""
-        if max_nnz > self.MAX_NNZ:
-            raise ValueError(f"row with {max_nnz} entries exceeds the device tokenizer limit {self.MAX_NNZ}")
         ml = seq_len if max_len is None else int(max_len)
         if ml < 0:
             raise ValueError("max_len must be >= 0")
+        if max_nnz > self.STAGE and min(ml, seq_len) > self.STAGE // 2:
+            raise ValueError(f"rows longer than {self.STAGE} entries need max_len <= {self.STAGE // 2} "
+                             "(streaming top-k of the device tokenizer)")
         if ids is None:
             ids = torch.empty(n_rows, seq_len, dtype=torch.int32, device=self.device)
         if am is None:
@@ -166,7 +167,7 @@ class RankEncoder:
         if s == 1:
             raise ValueError("row column index exceeds stats.n_cols")
         if s == 2:
-            raise ValueError("row exceeds the device tokenizer staging capacity")
+            raise ValueError("row longer than the device tokenizer staging capacity with max_len > capacity / 2")
 
     def __call__(self, indptr, cols, vals, rows, seq_len: int, max_len: int | None = None, check: bool = True):
         (d_ip, d_c, d_v), max_nnz = self.stage(indptr, cols, vals, rows)

@@ -127,7 +127,9 @@ class GradAllReducer:
             self.bucket_ends.append(store.numel)
         self.unit = unit
         self.key_end = {k: store.group_range[k][1] for k in keys}
-        self.stream = torch.cuda.Stream(store.g32.device) if self.cuda else None
+        # high priority: the persistent GEMM / attention kernels occupy every SM, so the collectives (and the
+        # bucket's optimizer) get the SMs at the next kernel boundary instead of queueing behind more compute
+        self.stream = torch.cuda.Stream(store.g32.device, priority=-1) if self.cuda else None
         self.g16 = torch.empty(store.numel, dtype=torch.bfloat16, device=store.g32.device) if self.bf16 else None
         self._next = 0
         self._start = 0

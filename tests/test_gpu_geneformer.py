@@ -77,6 +77,25 @@ def test_rank_encode_kernel_random_rows_vs_oracle():
     assert np.array_equal(ids.cpu().numpy(), want) and np.array_equal(am.cpu().numpy(), want_am)
 
 
+@pytest.mark.parametrize("ml", [2048, 8192])
+def test_rank_encode_rows_longer_than_staging_vs_oracle(ml):
+    """Rows with more non-zeros than the 16384-entry shared-memory stage (up to every one of 25,424 genes): the
+    streaming top-k keeps the best max_len entries chunk by chunk and equals the full sort of the reference
+    algorithm; a longer max_len than the streaming head allows is reported, not silently truncated."""
+    n_genes = 25424
+    ip, c, v = synthetic_expression_csr(6, n_genes, seed=8, nnz=(15000, n_genes))
+    v[::3] = np.round(v[::3])  # ties across chunk boundaries
+    med = np.random.default_rng(9).uniform(0.5, 3.0, n_genes).astype(np.float32)
+    rows = np.arange(6)
+    ids, am, lengths = RankEncoder(med)(ip, c, v, rows, seq_len=ml, max_len=ml)
+    want, want_am = R.rank_encode_batch(ip, c, v, med, rows, ml, ml)
+    assert np.array_equal(ids.cpu().numpy(), want) and np.array_equal(am.cpu().numpy(), want_am)
+    assert int((ip[1:] - ip[:-1]).max()) > 16384
+    if ml == 8192:
+        with pytest.raises(ValueError):
+            RankEncoder(med)(ip, c, v, rows, seq_len=12288, max_len=12288)
+
+
 # ------------------------------------------------------------------ masking
 def test_mlm_mask_geneformer_vocab_bit_exact():
     cfg = geneformer_config()
