@@ -14,24 +14,29 @@ namespace attn {
 constexpr float L2E = 1.4426950408889634f;
 
 // ---------------------------------------------------------------------------- backward
-// delta[b,h,s] = sum_d dO[t,h,d] * O[t,h,d] (t = b*S + s) and lse2 = -lse * log2(e).  Thread = one (head,
-// token); consecutive threads take consecutive tokens of one head, so the per-(b,h,s) writes (and the lse reads)
-// are contiguous, and each thread reads its token's DH-element slices of O and dO as whole 16-byte vectors
-// (unrolled at compile time: all of a thread's loads are in flight at once).
+// delta[b,h,s] = sum_d dO[t,h,d] * O[t,h,d] (t = b*S + s) and lse2 = -lse * log2(e).  Block = a tile of 64
+// tokens x all heads, transposed through shared memory: the dot products run with consecutive threads on
+// consecutive heads of a token (contiguous 16-byte reads of the token-major [T, H] rows of O and dO), the
+// per-(b, h, s) results leave with consecutive threads on consecutive tokens of a head (contiguous writes, and
+// contiguous lse reads).  All of a thread's vector loads are unrolled at compile time.
 template <typename T, int DH>
 __global__ void __launch_bounds__(256) delta_kernel(const T* __restrict__ O, const T* __restrict__ dO,
                                                     float* __restrict__ delta, const float* __restrict__ lse,
                                                     float* __restrict__ lse2, int64_t T_, int S, int nh) {
   constexpr int VEC = vec16<T>::N;
-  constexpr int NV = (DH + VEC - 1) / VEC;
+  constexpr int NV = DH / VEC;
+  constexpr int TT = 64;
+  extern __shared__ float tile[];  // [nh][TT]
   const int H = nh * DH;
-  const int64_t total = T_ * nh;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t h = i / T_, t = i - h * T_;
-    const T* o = O + t * H + h * DH;
-    const T* g = dO + t * H + h * DH;
+  const int64_t t0 = (int64_t)blockIdx.x * TT;
+  const int pairs = TT * nh;
+  for (int i = threadIdx.x; i < pairs; i += blockDim.x) {
+    const int tl = i / nh, h = i - tl * nh;
+    const int64_t t = t0 + tl;
     float acc = 0.f;
-    if constexpr (DH % VEC == 0) {
+    if (t < T_) {
+      const T* o = O + t * H + h * DH;
+      const T* g = dO + t * H + h * DH;
       uint4 ov[NV], gv[NV];
 #pragma unroll
       for (int k = 0; k < NV; ++k) {
@@ -46,13 +51,17 @@ __global__ void __launch_bounds__(256) delta_kernel(const T* __restrict__ O, con
 #pragma unroll
         for (int e = 0; e < VEC; ++e) acc = fmaf(a[e], c[e], acc);
       }
-    } else {
-#pragma unroll
-      for (int d = 0; d < DH; ++d) acc = fmaf(io<T>::ld(o + d), io<T>::ld(g + d), acc);
     }
+    tile[h * TT + tl] = acc;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < pairs; i += blockDim.x) {
+    const int h = i / TT, tl = i - h * TT;
+    const int64_t t = t0 + tl;
+    if (t >= T_) continue;
     const int64_t b = t / S, s = t - b * S;
     const int64_t idx = (b * nh + h) * S + s;
-    delta[idx] = acc;
+    delta[idx] = tile[h * TT + tl];
     if (lse2) lse2[idx] = -lse[idx] * L2E;  // negated log2-domain LSE (an FFMA2 addend in the tcgen05 backward)
   }
 }
@@ -83,11 +92,17 @@ int launch_delta(const void* o, const void* dout, float* delta, const float* lse
   if (grid > device_sm_count() * 16) grid = device_sm_count() * 16;
   const T* O = (const T*)o;
   const T* dO = (const T*)dout;
+  const int tiles = (int)((T_ + 63) / 64);
+  const size_t sm = (size_t)64 * nh * sizeof(float);
+  if (sm > 48 * 1024 || dh % vec16<T>::N != 0) {
+    delta_generic_kernel<T><<<grid, 256, 0, st>>>(O, dO, delta, lse, lse2, T_, S, nh, dh);
+    return 0;
+  }
   switch (dh) {
-    case 16: delta_kernel<T, 16><<<grid, 256, 0, st>>>(O, dO, delta, lse, lse2, T_, S, nh); break;
-    case 24: delta_kernel<T, 24><<<grid, 256, 0, st>>>(O, dO, delta, lse, lse2, T_, S, nh); break;
-    case 32: delta_kernel<T, 32><<<grid, 256, 0, st>>>(O, dO, delta, lse, lse2, T_, S, nh); break;
-    case 64: delta_kernel<T, 64><<<grid, 256, 0, st>>>(O, dO, delta, lse, lse2, T_, S, nh); break;
+    case 16: delta_kernel<T, 16><<<tiles, 256, sm, st>>>(O, dO, delta, lse, lse2, T_, S, nh); break;
+    case 24: delta_kernel<T, 24><<<tiles, 256, sm, st>>>(O, dO, delta, lse, lse2, T_, S, nh); break;
+    case 32: delta_kernel<T, 32><<<tiles, 256, sm, st>>>(O, dO, delta, lse, lse2, T_, S, nh); break;
+    case 64: delta_kernel<T, 64><<<tiles, 256, sm, st>>>(O, dO, delta, lse, lse2, T_, S, nh); break;
     default: delta_generic_kernel<T><<<grid, 256, 0, st>>>(O, dO, delta, lse, lse2, T_, S, nh, dh); break;
   }
   return 0;

@@ -490,7 +490,7 @@ def test_attention_persistent_many_tiles(dh, holes):
     assert (dk[1, :, 300:] == 0).all() and (dv[1, :, 300:] == 0).all()
 
 
-@pytest.mark.parametrize("H", [64, 320, 480, 768])
+@pytest.mark.parametrize("H", [64, 320, 480, 768, 1280, 2560])
 @pytest.mark.parametrize("rows", [1, 777, 4096 + 3])
 @pytest.mark.parametrize("gelu", [False, True])
 def test_layernorm_bwd_no_stats(H, rows, gelu):
@@ -560,3 +560,34 @@ def test_qkv_rope_bwd_vs_torch(B, S, nh, dh):
     torch.cuda.synchronize()
     assert rel(out, ref) < 1e-2
     assert rel(cs, ref.sum(0)) < 1e-3
+
+
+@pytest.mark.parametrize("H", [320, 480, 1280, 2560])
+def test_layernorm_bulk_ring_wraps(H):
+    """Bulk-staged LayerNorm (bf16): many row blocks per persistent CTA (the stage ring wraps several times, a
+    ragged last block), forward and backward (with residual input and bias-gradient column sums) vs torch fp32."""
+    torch.manual_seed(5)
+    rows = 20011
+    x = (torch.randn(rows, H, device=DEV) * 1.5 + 0.3).bfloat16()
+    g, b = torch.randn(H, device=DEV), torch.randn(H, device=DEV)
+    y = torch.empty_like(x)
+    mean, rstd = torch.empty(rows, device=DEV), torch.empty(rows, device=DEV)
+    _lib.call("esm_layernorm_fwd", ESM_BF16, x.data_ptr(), g.data_ptr(), b.data_ptr(), y.data_ptr(),
+              mean.data_ptr(), rstd.data_ptr(), rows, H, 1e-5, st())
+    xr = x.float().requires_grad_(True)
+    ref = torch.nn.functional.layer_norm(xr, (H,), g, b, 1e-5)
+    torch.cuda.synchronize()
+    assert rel(y, ref) < 1e-2
+    assert rel(mean, xr.detach().mean(-1)) < 1e-4
+    dy = torch.randn(rows, H, device=DEV).bfloat16()
+    dres = torch.randn(rows, H, device=DEV).bfloat16()
+    ref.backward(dy.float())
+    dx = torch.empty_like(x)
+    cs = torch.zeros(H, device=DEV)
+    _lib.call("esm_layernorm_bwd", ESM_BF16, dy.data_ptr(), x.data_ptr(), g.data_ptr(), mean.data_ptr(),
+              rstd.data_ptr(), dres.data_ptr(), None, dx.data_ptr(), None, None, cs.data_ptr(), rows, H, None, None,
+              st())
+    torch.cuda.synchronize()
+    want = xr.grad + dres.float()
+    assert rel(dx, want) < 2e-2
+    assert rel(cs, want.sum(0)) < 1e-2
