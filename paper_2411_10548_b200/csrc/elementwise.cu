@@ -1079,17 +1079,6 @@ __global__ void cast_bf16_f32_kernel(const __nv_bfloat16* __restrict__ s, float*
     d[i] = __bfloat162float(s[i]);
 }
 
-int ln_fwd_bulk(const void* x, const float* gamma, const float* beta, void* y, float* mean, float* rstd, int64_t rows,
-                int H, float eps, cudaStream_t st);
-int ln_bwd_bulk(const void* dy, const void* x, const float* gamma, const float* mean, const float* rstd,
-                const void* dres, void* dx, float* csum, int64_t rows, int H, const esm_dropout* drop, void* dxd,
-                cudaStream_t st);
-// ESM_LN_BULK=0 selects the register-staged LayerNorm kernels (A/B tuning knob)
-static bool ln_bulk_enabled() {
-  static const bool on = !(getenv("ESM_LN_BULK") && atoi(getenv("ESM_LN_BULK")) == 0);
-  return on;
-}
-
 static int grid_for(int64_t work, int block, int cap = device_sm_count() * 16) {
   int64_t g = (work + block - 1) / block;
   if (g > cap) g = cap;
@@ -1260,14 +1249,6 @@ static inline void ln_shape(int H, int vec, int& maxv, int& wpr, int max_per_lan
 int esm_layernorm_fwd(int dtype, const void* x, const float* gamma, const float* beta, void* y, float* mean, float* rstd,
                       int rows, int H, float eps, esm_stream_t stream) {
   ESM_CHECK_ARG(x && gamma && beta && y && mean && rstd && rows > 0 && H > 0, "esm_layernorm_fwd: bad args");
-  if (dtype == ESM_BF16 && ln_bulk_enabled()) {  // bulk-copy staged (layernorm_bulk.cu); -1: shape not handled
-    const int rc = ln_fwd_bulk(x, gamma, beta, y, mean, rstd, rows, H, eps, S(stream));
-    if (rc == 0) return 0;
-    if (rc > 0) {
-      set_last_error("esm_layernorm_fwd (bulk): %s", cudaGetErrorString((cudaError_t)rc));
-      return rc;
-    }
-  }
   const int vec = dtype == ESM_BF16 ? 8 : 4;
   ESM_CHECK_ARG(H % vec == 0, "layernorm: H %% %d", vec);
   int mv, wpr;
@@ -1308,14 +1289,6 @@ int esm_layernorm_bwd(int dtype, const void* dy, const void* x, const float* gam
   ESM_CHECK_ARG(dy && x && gamma && mean && rstd && dx && rows > 0, "esm_layernorm_bwd: bad args");
   const bool dropping = drop != nullptr && drop->threshold != 0u;
   ESM_CHECK_ARG(!dropping || (dx_drop != nullptr && drop->seed != nullptr), "esm_layernorm_bwd: dropout needs dx_drop");
-  if (dtype == ESM_BF16 && dgamma == nullptr && dbeta == nullptr && gelu_z == nullptr && ln_bulk_enabled()) {
-    const int rc = ln_bwd_bulk(dy, x, gamma, mean, rstd, dres, dx, col_sum, rows, H, drop, dx_drop, S(stream));
-    if (rc == 0) return 0;
-    if (rc > 0) {
-      set_last_error("esm_layernorm_bwd (bulk): %s", cudaGetErrorString((cudaError_t)rc));
-      return rc;
-    }
-  }
   const esm_dropout dr = dropping ? *drop : esm_dropout{nullptr, 0u, 0u, 1.f};
   void* dxd = dropping ? dx_drop : nullptr;
   const int vec = dtype == ESM_BF16 ? 8 : 4;
