@@ -57,6 +57,9 @@ def parse():
                          "the updated parameters; the ZeRO-1 comparison point of PAPER.md:86-88), ddp = all-reduce "
                          "+ replicated AdamW")
     ap.add_argument("--grad-bf16", action="store_true", help="N>1: bf16 gradient buckets (half the NVLink bytes)")
+    ap.add_argument("--master", default="vectors", choices=["vectors", "full"],
+                    help="zero1: keep the fp32 master sharded and all-gather only the bf16 shadow (+ the 1-D fp32 "
+                         "parameters), or all-gather the whole fp32 master as well")
     ap.add_argument("--nvtx", action="store_true", help="NVTX ranges around the step phases and layers")
     ap.add_argument("--varlen", action="store_true",
                     help="protein-like lengths (lognormal(5.6, 0.65) clipped to [10, seq]) batched by the reference's "
@@ -312,7 +315,7 @@ def run_varlen(args, rank, world, local, dev):
     model.reserve(*max(shapes, key=lambda x: x[0] * x[1]))
     if world > 1:
         model.comm = GradAllReducer(model.store, grad_dtype="bf16" if args.grad_bf16 else "fp32",
-                                    shard_optimizer=args.dp == "zero1")
+                                    shard_optimizer=args.dp == "zero1", master=args.master)
     use_graph = not args.no_graph
     seed = 4321
 
@@ -419,7 +422,7 @@ def main():
     ws = model.workspace(B, S)
     if world > 1:
         model.comm = GradAllReducer(model.store, grad_dtype="bf16" if args.grad_bf16 else "fp32",
-                                    shard_optimizer=args.dp == "zero1")
+                                    shard_optimizer=args.dp == "zero1", master=args.master)
     use_graph = not args.no_graph  # N > 1: the NCCL bucket collectives are captured in the same graph
 
     gene = cfg.vocab_size > 40
@@ -638,7 +641,8 @@ def main():
             "config": {"workload": f"{preset_name} MLM pre-training step (mask+fwd+bwd+AdamW), {B} x {S} per GPU",
                        "model": preset_name, "global_batch": B * world, "seq_len": S,
                        "parallelism": f"dp{world}" + ("-zero1" if args.dp == "zero1" and world > 1 else "") +
-                                      ("-bf16grad" if args.grad_bf16 and world > 1 else ""),
+                                      ("-fullmaster" if args.dp == "zero1" and world > 1 and args.master == "full"
+                                       else "") + ("-bf16grad" if args.grad_bf16 and world > 1 else ""),
                        "l2": "inputs/activations >> 126 MB L2 (no flush needed)",
                        "cuda_graph": use_graph, "weights": "random init",
                        "data": (f"synthetic cells, {GF_NNZ[0]}-{GF_NNZ[1]} expressed genes of {GF_GENES}, "

@@ -52,7 +52,11 @@ enum {
                              (dgamma) with xhat = (X - row_mean) * row_rstd, X = aux_in (the LN input)  (bf16)   */
   ESM_EPI_GELU_GRADAUX = 7, /* Z = acc + bias; C = gelu(Z), aux_out = gelu'(Z)  (bf16: the FC1 forward keeps the
                                derivative its backward needs, computed from the same exp/erfc evaluation)        */
-  ESM_EPI_MUL_AUX = 8       /* C = acc * G (G = aux_in, e.g. gelu'(Z) from GELU_GRADAUX); colsum(C) -> col_sum (bf16) */
+  ESM_EPI_MUL_AUX = 8,      /* C = acc * G (G = aux_in, e.g. gelu'(Z) from GELU_GRADAUX); colsum(C) -> col_sum (bf16) */
+  ESM_EPI_DELTA = 9         /* C = acc = dO (attention output gradient, token-major [M = B*seq_len, N = n_heads*head_dim]);
+                               row_dot[b, h, s] = sum_{c in head h} bf16(C[t, c]) * O[t, c]  (O = aux_in, t = b*seq_len+s):
+                               the attention backward's Delta = rowsum(dO o O) (HF:257-282 backward); replaces a
+                               separate pass over dO and O (bf16, B N-major dgrad only)                            */
 };
 
 /* Hidden dropout (HF EsmSelfOutput / EsmOutput, HF:modeling_esm.py:369-375, 421-427): counter-based keep mask,
@@ -92,6 +96,9 @@ typedef struct esm_gemm_args {
   float* col_sum2;           /* [N] */
   /* ESM_EPI_RESID only: C = R + dropout(acc + bias) */
   esm_dropout drop;
+  /* ESM_EPI_DELTA only: [B, n_heads, seq_len] fp32 per-head row dot products (zeroed, then reduced into, by the
+     callee on `stream`) */
+  float* row_dot;
 } esm_gemm_args;
 
 /* ---------------- library ---------------- */
@@ -169,18 +176,22 @@ int esm_qkv_rope_bwd(int dtype, const float* dq, const void* dk, const void* dv,
  * run concurrently (different streams) need distinct `sched` buffers.  fp32 calls ignore `sched` (may be NULL). */
 #define ESM_ATTN_SCHED_WORDS(B) (16 + 2 * (int64_t)(B))
 int esm_attn_prepare(const int32_t* key_mask, int32_t* sched, int B, int S, esm_stream_t stream);
-/* q,k,v [B,nh,S,dh]; key_mask [B,S] int32 (0 = padded key); o [T, nh*dh]; lse [B,nh,S] fp32.
+/* q,k,v [B,nh,S,dh]; key_mask [B,S] int32 (0 = padded key); o [T, nh*dh]; lse [B,nh,S] fp32 holds each row's
+ * log-normaliser in the form the backward consumes, -log2(sum_k exp(s_k)) = -LSE * log2(e).
  * bf16: S % 4 == 0 (the collate step pads to a multiple of 8). */
 int esm_attn_fwd(int dtype, const void* q, const void* k, const void* v, const int32_t* key_mask, int32_t* sched,
                  void* o, float* lse, int B, int nh, int S, int dh, esm_stream_t stream);
-/* dO [T, nh*dh]; outputs dq (fp32 accum, zeroed by callee), dk, dv [B,nh,S,dh]; delta workspace [2,B,nh,S] fp32. */
+/* dO [T, nh*dh]; outputs dq (fp32 accum, zeroed by callee), dk, dv [B,nh,S,dh]; delta workspace [2,B,nh,S] fp32.
+ * o == NULL (bf16): delta[0:B*nh*S] already holds Delta = rowsum(dO o O) per (b, h, s) -- e.g. accumulated by the
+ * ESM_EPI_DELTA epilogue of the GEMM that produced dO -- and the separate Delta pass is skipped. */
 int esm_attn_bwd(int dtype, const void* q, const void* k, const void* v, const void* o, const void* dout,
                  const float* lse, const int32_t* key_mask, int32_t* sched, float* delta, float* dq, void* dk,
                  void* dv, int B, int nh, int S, int dh, esm_stream_t stream);
 
 /* Fused backward for the ESM layer (bf16, S % 4 == 0): writes dqkv[T, 3H] = [dq, dk, dv] with RoPEᵀ (and
  * q_scale on dq) applied -- the layout the QKV dgrad / wgrad GEMMs consume -- and col_sum[3H] += the q/k/v
- * bias gradients.  dq_ws: fp32 [T, H] workspace (zeroed by callee); delta: [2, B, nh, S] fp32 workspace. */
+ * bias gradients.  dq_ws: fp32 [T, H] workspace (zeroed by callee); delta: [2, B, nh, S] fp32 workspace
+ * (o == NULL: precomputed Delta, as for esm_attn_bwd). */
 int esm_attn_bwd_qkv(const void* q, const void* k, const void* v, const void* o, const void* dout,
                      const float* lse, const int32_t* key_mask, int32_t* sched, float* delta, float* dq_ws, void* dqkv,
                      float* col_sum, const float* cos_t, const float* sin_t, float q_scale, int B, int nh, int S,

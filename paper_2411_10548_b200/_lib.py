@@ -13,7 +13,7 @@ LIB_PATH = os.environ.get("ESM_LIB_PATH") or os.path.join(_HERE, "libesm2b200.so
 
 ESM_F32, ESM_BF16, ESM_I32 = 0, 1, 2
 EPI_STORE, EPI_GELU, EPI_RESID, EPI_DGELU, EPI_F32_ACC, EPI_QKV_ROPE, EPI_STORE_LN = 0, 1, 2, 3, 4, 5, 6
-EPI_GELU_GRADAUX, EPI_MUL_AUX = 7, 8
+EPI_GELU_GRADAUX, EPI_MUL_AUX, EPI_DELTA = 7, 8, 9
 
 EXPORTS = [
     "esm_version", "esm_last_error", "esm_device_sm_count", "esm_tokenize", "esm_mlm_mask", "esm_embed_fwd",
@@ -54,6 +54,7 @@ class GemmArgs(ctypes.Structure):
         ("q_scale", ctypes.c_float),
         ("row_mean", ctypes.c_void_p), ("row_rstd", ctypes.c_void_p), ("col_sum2", ctypes.c_void_p),
         ("drop", Dropout),
+        ("row_dot", ctypes.c_void_p),
     ]
 
 

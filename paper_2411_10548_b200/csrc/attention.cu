@@ -12,17 +12,20 @@ namespace esm {
 namespace attn {
 
 constexpr float L2E = 1.4426950408889634f;
+constexpr float LN2 = 0.6931471805599453f;
+// The attention row normaliser crosses the C ABI in the form the tcgen05 backward consumes:
+// lse2 = -log2(sum_k exp(s_k)) = -LSE * log2(e) (an FFMA2 addend there); the fp32 kernels convert at the edges.
 
 // ---------------------------------------------------------------------------- backward
-// delta[b,h,s] = sum_d dO[t,h,d] * O[t,h,d] (t = b*S + s) and lse2 = -lse * log2(e).  Block = a tile of 64
+// delta[b,h,s] = sum_d dO[t,h,d] * O[t,h,d] (t = b*S + s) (the model computes it in the dO GEMM's epilogue,
+// ESM_EPI_DELTA; this pass serves esm_attn_bwd callers that pass O, and the fp32 parity path).  Block = a tile of 64
 // tokens x all heads, transposed through shared memory: the dot products run with consecutive threads on
 // consecutive heads of a token (contiguous 16-byte reads of the token-major [T, H] rows of O and dO), the
 // per-(b, h, s) results leave with consecutive threads on consecutive tokens of a head (contiguous writes, and
 // contiguous lse reads).  All of a thread's vector loads are unrolled at compile time.
 template <typename T, int DH>
 __global__ void __launch_bounds__(256) delta_kernel(const T* __restrict__ O, const T* __restrict__ dO,
-                                                    float* __restrict__ delta, const float* __restrict__ lse,
-                                                    float* __restrict__ lse2, int64_t T_, int S, int nh) {
+                                                    float* __restrict__ delta, int64_t T_, int S, int nh) {
   constexpr int VEC = vec16<T>::N;
   constexpr int NV = DH / VEC;
   constexpr int TT = 64;
@@ -62,15 +65,13 @@ __global__ void __launch_bounds__(256) delta_kernel(const T* __restrict__ O, con
     const int64_t b = t / S, s = t - b * S;
     const int64_t idx = (b * nh + h) * S + s;
     delta[idx] = tile[h * TT + tl];
-    if (lse2) lse2[idx] = -lse[idx] * L2E;  // negated log2-domain LSE (an FFMA2 addend in the tcgen05 backward)
   }
 }
 
 // generic head dim (fp32 parity mode): one thread per (token, head)
 template <typename T>
 __global__ void delta_generic_kernel(const T* __restrict__ O, const T* __restrict__ dO, float* __restrict__ delta,
-                                     const float* __restrict__ lse, float* __restrict__ lse2, int64_t T_, int S,
-                                     int nh, int dh) {
+                                     int64_t T_, int S, int nh, int dh) {
   const int H = nh * dh;
   const int64_t total = T_ * nh;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -80,13 +81,11 @@ __global__ void delta_generic_kernel(const T* __restrict__ O, const T* __restric
     const int64_t b = t / S, s = t - b * S;
     const int64_t idx = (b * nh + h) * S + s;
     delta[idx] = acc;
-    if (lse2) lse2[idx] = -lse[idx] * L2E;
   }
 }
 
 template <typename T>
-int launch_delta(const void* o, const void* dout, float* delta, const float* lse, float* lse2, int64_t T_, int S,
-                 int nh, int dh, cudaStream_t st) {
+int launch_delta(const void* o, const void* dout, float* delta, int64_t T_, int S, int nh, int dh, cudaStream_t st) {
   const int64_t work = T_ * nh;
   int grid = (int)((work + 255) / 256);
   if (grid > device_sm_count() * 16) grid = device_sm_count() * 16;
@@ -95,15 +94,15 @@ int launch_delta(const void* o, const void* dout, float* delta, const float* lse
   const int tiles = (int)((T_ + 63) / 64);
   const size_t sm = (size_t)64 * nh * sizeof(float);
   if (sm > 48 * 1024 || dh % vec16<T>::N != 0) {
-    delta_generic_kernel<T><<<grid, 256, 0, st>>>(O, dO, delta, lse, lse2, T_, S, nh, dh);
+    delta_generic_kernel<T><<<grid, 256, 0, st>>>(O, dO, delta, T_, S, nh, dh);
     return 0;
   }
   switch (dh) {
-    case 16: delta_kernel<T, 16><<<tiles, 256, sm, st>>>(O, dO, delta, lse, lse2, T_, S, nh); break;
-    case 24: delta_kernel<T, 24><<<tiles, 256, sm, st>>>(O, dO, delta, lse, lse2, T_, S, nh); break;
-    case 32: delta_kernel<T, 32><<<tiles, 256, sm, st>>>(O, dO, delta, lse, lse2, T_, S, nh); break;
-    case 64: delta_kernel<T, 64><<<tiles, 256, sm, st>>>(O, dO, delta, lse, lse2, T_, S, nh); break;
-    default: delta_generic_kernel<T><<<grid, 256, 0, st>>>(O, dO, delta, lse, lse2, T_, S, nh, dh); break;
+    case 16: delta_kernel<T, 16><<<tiles, 256, sm, st>>>(O, dO, delta, T_, S, nh); break;
+    case 24: delta_kernel<T, 24><<<tiles, 256, sm, st>>>(O, dO, delta, T_, S, nh); break;
+    case 32: delta_kernel<T, 32><<<tiles, 256, sm, st>>>(O, dO, delta, T_, S, nh); break;
+    case 64: delta_kernel<T, 64><<<tiles, 256, sm, st>>>(O, dO, delta, T_, S, nh); break;
+    default: delta_generic_kernel<T><<<grid, 256, 0, st>>>(O, dO, delta, T_, S, nh, dh); break;
   }
   return 0;
 }
@@ -161,7 +160,7 @@ __global__ void __launch_bounds__(64) fwd_f32_kernel(const float* __restrict__ Q
 #pragma unroll
     for (int d = 0; d < MAXD; ++d)
       if (d < dh) O[((int64_t)b * S + qi) * H + h * dh + d] = o[d] * inv;
-    LSE[(int64_t)bh * S + qi] = m + logf(l);
+    LSE[(int64_t)bh * S + qi] = -(m + logf(l)) * L2E;
   }
 }
 
@@ -186,7 +185,7 @@ __global__ void __launch_bounds__(64) bwd_dq_f32_kernel(const float* __restrict_
     go[d] = ok ? dO[((int64_t)b * S + qi) * H + h * dh + d] : 0.f;
     dq[d] = 0.f;
   }
-  const float lse = qi < S ? LSE[(int64_t)bh * S + qi] : 0.f;
+  const float lse = qi < S ? -LSE[(int64_t)bh * S + qi] * LN2 : 0.f;
   const float delta = qi < S ? Delta[(int64_t)bh * S + qi] : 0.f;
   for (int k0 = 0; k0 < S; k0 += 64) {
     __syncthreads();
@@ -254,7 +253,7 @@ __global__ void __launch_bounds__(64) bwd_dkv_f32_kernel(const float* __restrict
     }
     {
       const int qq = q0 + threadIdx.x;
-      sL[threadIdx.x] = qq < S ? LSE[(int64_t)bh * S + qq] : INFINITY;
+      sL[threadIdx.x] = qq < S ? -LSE[(int64_t)bh * S + qq] * LN2 : INFINITY;
       sD[threadIdx.x] = qq < S ? Delta[(int64_t)bh * S + qq] : 0.f;
     }
     __syncthreads();
@@ -380,7 +379,7 @@ namespace esm {
 int attn_prepare_tc(const int32_t* km, int* sched, int B, int S, cudaStream_t st);
 int attn_fwd_tc(const void* q, const void* k, const void* v, const int32_t* km, int* sched, void* o, float* lse,
                 int B, int nh, int S, int dh, cudaStream_t st);
-int attn_bwd_tc(const void* q, const void* k, const void* v, const void* dout, const float* lse2, const float* delta,
+int attn_bwd_tc(const void* q, const void* k, const void* v, const void* dout, const float* lse, const float* delta,
                 const int32_t* km, int* sched, float* dq, void* dk, void* dv, int B, int nh, int S, int dh,
                 cudaStream_t st, void* dqkv, float* col_sum, const float* cos_t, const float* sin_t);
 }  // namespace esm
@@ -411,23 +410,24 @@ extern "C" int esm_attn_fwd(int dtype, const void* q, const void* k, const void*
 extern "C" int esm_attn_bwd(int dtype, const void* q, const void* k, const void* v, const void* o, const void* dout,
                             const float* lse, const int32_t* key_mask, int32_t* sched, float* delta, float* dq,
                             void* dk, void* dv, int B, int nh, int S, int dh, esm_stream_t stream) {
-  ESM_CHECK_ARG(q && k && v && o && dout && lse && delta && dq && dk && dv, "esm_attn_bwd: null pointer");
+  ESM_CHECK_ARG(q && k && v && dout && lse && delta && dq && dk && dv, "esm_attn_bwd: null pointer");
+  ESM_CHECK_ARG(o || dtype == ESM_BF16, "esm_attn_bwd: fp32 needs o");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int64_t T_ = (int64_t)B * S;
   if (dtype == ESM_BF16) {
     ESM_CHECK_ARG(sched != nullptr, "esm_attn_bwd: bf16 needs the scheduling workspace (esm_attn_prepare)");
     ESM_CHECK_ARG(S % 4 == 0, "esm_attn_bwd: bf16 needs S %% 4 == 0 (pad the batch)");
-    float* lse2 = delta + T_ * nh;  // workspace [2, B, nh, S]: Delta then log2-domain LSE
-    attn::launch_delta<__nv_bfloat16>(o, dout, delta, lse, lse2, T_, S, nh, dh, st);
+    // o == NULL: Delta was accumulated by the dO-producing GEMM (ESM_EPI_DELTA)
+    if (o) attn::launch_delta<__nv_bfloat16>(o, dout, delta, T_, S, nh, dh, st);
     cudaMemsetAsync(dq, 0, sizeof(float) * T_ * nh * dh, st);
-    const int rc = attn_bwd_tc(q, k, v, dout, lse2, delta, key_mask, sched, dq, dk, dv, B, nh, S, dh, st, nullptr,
+    const int rc = attn_bwd_tc(q, k, v, dout, lse, delta, key_mask, sched, dq, dk, dv, B, nh, S, dh, st, nullptr,
                                nullptr, nullptr, nullptr);
     if (rc) return rc;
     ESM_LAUNCH_RET();
   }
   ESM_CHECK_ARG(dh <= attn::MAXD, "esm_attn_bwd: dh <= 64");
   dim3 grid((S + 63) / 64, B * nh);
-  attn::launch_delta<float>(o, dout, delta, lse, nullptr, T_, S, nh, dh, st);
+  attn::launch_delta<float>(o, dout, delta, T_, S, nh, dh, st);
   attn::bwd_dq_f32_kernel<<<grid, 64, 0, st>>>((const float*)q, (const float*)k, (const float*)v, (const float*)dout,
                                                lse, delta, key_mask, dq, S, nh, dh);
   attn::bwd_dkv_f32_kernel<<<grid, 64, 0, st>>>((const float*)q, (const float*)k, (const float*)v,
@@ -440,15 +440,14 @@ extern "C" int esm_attn_bwd_qkv(const void* q, const void* k, const void* v, con
                                 const float* lse, const int32_t* key_mask, int32_t* sched, float* delta, float* dq_ws,
                                 void* dqkv, float* col_sum, const float* cos_t, const float* sin_t, float q_scale,
                                 int B, int nh, int S, int dh, esm_stream_t stream) {
-  ESM_CHECK_ARG(q && k && v && o && dout && lse && sched && delta && dq_ws && dqkv && col_sum && cos_t && sin_t,
+  ESM_CHECK_ARG(q && k && v && dout && lse && sched && delta && dq_ws && dqkv && col_sum && cos_t && sin_t,
                 "esm_attn_bwd_qkv: null pointer");
   ESM_CHECK_ARG(S % 4 == 0 && dh % 8 == 0, "esm_attn_bwd_qkv: needs S %% 4 == 0 and dh %% 8 == 0");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int64_t T_ = (int64_t)B * S;
-  float* lse2 = delta + T_ * nh;
-  attn::launch_delta<__nv_bfloat16>(o, dout, delta, lse, lse2, T_, S, nh, dh, st);
+  if (o) attn::launch_delta<__nv_bfloat16>(o, dout, delta, T_, S, nh, dh, st);
   cudaMemsetAsync(dq_ws, 0, sizeof(float) * T_ * nh * dh, st);
-  const int rc = attn_bwd_tc(q, k, v, dout, lse2, delta, key_mask, sched, dq_ws, nullptr, nullptr, B, nh, S, dh, st,
+  const int rc = attn_bwd_tc(q, k, v, dout, lse, delta, key_mask, sched, dq_ws, nullptr, nullptr, B, nh, S, dh, st,
                              dqkv, col_sum, cos_t, sin_t);
   if (rc) return rc;
   const int lanes = nh * (dh / 8);  // vector path: threads per token

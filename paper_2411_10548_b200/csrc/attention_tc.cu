@@ -13,6 +13,7 @@
 // arbitrary masks fall back to per-key mask loads.
 #include <cstdlib>
 #include <mutex>
+#include <type_traits>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -89,6 +90,22 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
       : "memory");
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+// N consecutive 32-bit TMEM columns of this warp's lane quarter (N = 16 or 32)
+template <int N>
+__device__ __forceinline__ void tmem_ldq(uint32_t taddr, uint32_t (&r)[N]) {
+  if constexpr (N == 32) tmem_ld32(taddr, r);
+  else tmem_ld16(taddr, r);
+}
+template <int N>
+__device__ __forceinline__ void tmem_stq(uint32_t taddr, const uint32_t (&r)[N]) {
+  if constexpr (N == 16) tmem_st16(taddr, r);
+  else tmem_st8(taddr, r);
+}
 
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -184,7 +201,7 @@ __device__ __forceinline__ bool tile_skipped(const int* sched, int tile, int nkb
 // Q and the O accumulator are double-buffered across items (q_empty / o_free handshakes), the K/V ring and
 // the S / P barriers follow a global tile counter, so the next item's loads and first MMAs overlap this
 // item's softmax tail and epilogue.
-template <int DH, int BN, int NSB>
+template <int DH, int BN, int NSB, int FP>
 __global__ void __launch_bounds__(kThreads, NSB == 1 ? 3 : 2)
     fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                const __grid_constant__ CUtensorMap tmV, const int32_t* __restrict__ key_mask,
@@ -359,38 +376,40 @@ __global__ void __launch_bounds__(kThreads, NSB == 1 ? 3 : 2)
         mbar_wait(&s_full[gj % NSB], (gj / NSB) & 1);
         tc_fence_after();
         const uint32_t sbase = tbase + lane_off + (gj % NSB) * BN;
-        float s[BN];
-#pragma unroll
-        for (int c = 0; c < BN; c += 32) {
-          uint32_t u[32];
-          tmem_ld32(sbase + c, u);
-#pragma unroll
-          for (int e = 0; e < 32; ++e) s[c + e] = __uint_as_float(u[e]);
-        }
+        static_assert(BN == 64, "the softmax holds one 64-key tile as two 32-column TMEM loads");
+        uint32_t ua[32], ub[32];  // S row, used in place (no register copies)
+        tmem_ld32(sbase, ua);
+        tmem_ld32(sbase + 32, ub);
         tmem_ld_wait();
+        auto sv = [&](int c) -> float { return __uint_as_float(c < 32 ? ua[c] : ub[c - 32]); };
+        auto kill = [&](int c) {
+          if (c < 32) ua[c] = __float_as_uint(-INFINITY);
+          else ub[c - 32] = __float_as_uint(-INFINITY);
+        };
         const int kbase = j * BN;
-        float mx = -INFINITY;
+        bool full = !nonprefix;
         if (!nonprefix) {
           const int valid = kv_len - kbase;  // keys [0, valid) of this tile are real
-          if (valid >= BN) {
+          if (valid < BN) {
+            full = false;
 #pragma unroll
-            for (int c = 0; c < BN; ++c) mx = fmaxf(mx, s[c]);
-          } else {
-#pragma unroll
-            for (int c = 0; c < BN; ++c) {
-              s[c] = c < valid ? s[c] : -INFINITY;
-              mx = fmaxf(mx, s[c]);
-            }
+            for (int c = 0; c < BN; ++c)
+              if (c >= valid) kill(c);
           }
         } else {
 #pragma unroll
           for (int c = 0; c < BN; ++c) {
             const int kk = kbase + c;
-            const bool ok = kk < S && key_mask[(int64_t)b * S + kk] != 0;
-            s[c] = ok ? s[c] : -INFINITY;
-            mx = fmaxf(mx, s[c]);
+            if (!(kk < S && key_mask[(int64_t)b * S + kk] != 0)) kill(c);
           }
         }
+        // row max as a 4-way tree (FMNMX3 chains of 8 instead of one of 32)
+        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+        for (int c = 0; c < BN; c += 8)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) m4[q] = fmaxf(m4[q], fmaxf(sv(c + 2 * q), sv(c + 2 * q + 1)));
+        const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
         const float mnew = mx * L2E;
         const bool grow = mnew > m_used + RESCALE_THRESHOLD;
         if (__any_sync(0xffffffffu, grow)) {  // warp-uniform: tcgen05.ld/st are warp-collective
@@ -413,21 +432,43 @@ __global__ void __launch_bounds__(kThreads, NSB == 1 ? 3 : 2)
           if (grow) m_used = mnew;
         }
         const float moff = m_used == -INFINITY ? 0.f : m_used;
-        // (measured: f32x2 packing here is neutral and moving 1 in 4 exponentials to the FMA pipe is 27 %
-        // slower, unlike the backward)
-        float ls = 0.f;
+        // exponentials: x = s log2e - m in FFMA2, row sums in two FADD2 chains; on full tiles FP of every four
+        // pairs go to the FMA pipe (exp2_poly2) to relieve MUFU (masked tiles stay on MUFU: exact zeros)
+        const uint64_t l2e = f2_splat(L2E), nm = f2_splat(-moff);
+        uint64_t ls0 = f2_splat(0.f), ls1 = ls0;
+        uint32_t pk[32];
+        auto exps = [&](auto fp_tag) {
+          constexpr int F = decltype(fp_tag)::value;
 #pragma unroll
-        for (int c = 0; c < BN; c += 64) {
-          uint32_t pk[32];
+          for (int e = 0; e < 32; e += 4) {  // 8 keys: 4 pairs
+            float x[8], pr[8];
 #pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const float p0 = ex2(fmaf(s[c + 2 * e], L2E, -moff));
-            const float p1 = ex2(fmaf(s[c + 2 * e + 1], L2E, -moff));
-            ls += p0 + p1;
-            pk[e] = pack2(p0, p1);
+            for (int q = 0; q < 4; ++q)
+              f2_unpack(f2_fma(f2_pack(sv(2 * e + 2 * q), sv(2 * e + 2 * q + 1)), l2e, nm), x[2 * q], x[2 * q + 1]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              if (q >= 4 - F) {
+                exp2_poly2(x[2 * q], x[2 * q + 1], pr[2 * q], pr[2 * q + 1]);
+              } else {
+                pr[2 * q] = ex2(x[2 * q]);
+                pr[2 * q + 1] = ex2(x[2 * q + 1]);
+              }
+            }
+            ls0 = f2_add(ls0, f2_pack(pr[0], pr[1]));
+            ls1 = f2_add(ls1, f2_pack(pr[2], pr[3]));
+            ls0 = f2_add(ls0, f2_pack(pr[4], pr[5]));
+            ls1 = f2_add(ls1, f2_pack(pr[6], pr[7]));
+#pragma unroll
+            for (int q = 0; q < 4; ++q) pk[e + q] = pack2(pr[2 * q], pr[2 * q + 1]);
           }
-          tmem_st32(sbase + c / 2, pk);  // P (bf16x2) over the first 64 columns of this S buffer
-        }
+        };
+        if (FP > 0 && full) exps(std::integral_constant<int, FP>{});
+        else exps(std::integral_constant<int, 0>{});
+        tmem_st32(sbase, pk);  // P (bf16x2) over the first 32 columns of this S buffer
+        float l0, l1, l2, l3;
+        f2_unpack(ls0, l0, l1);
+        f2_unpack(ls1, l2, l3);
+        const float ls = (l0 + l1) + (l2 + l3);
         l += ls;
         tmem_st_wait();
         tc_fence_before();
@@ -464,7 +505,7 @@ __global__ void __launch_bounds__(kThreads, NSB == 1 ? 3 : 2)
           w.w = pack2(o[c + 6], o[c + 7]);
           *reinterpret_cast<uint4*>(dst + c) = w;
         }
-        LSE[(int64_t)bh * S + qrow] = l > 0.f ? (m_used + log2f(l)) / L2E : -INFINITY;
+        LSE[(int64_t)bh * S + qrow] = l > 0.f ? -(m_used + log2f(l)) : INFINITY;  // -LSE log2 e (ABI form)
       }
     }
     G0 += ntiles;
@@ -480,19 +521,27 @@ __global__ void __launch_bounds__(kThreads, NSB == 1 ? 3 : 2)
 
 // ============================================================================ backward
 // CTA = 128 keys of one (batch, head); loop over 64-query blocks (processed in pairs).
-//   warp 0     TMA: K, V once; Q_i, dO_i tiles + LSE_i / Delta_i (bulk copies) per block (2 stages)
+//   warp 0     TMA: K, V once; Q_i, dO_i tiles + LSE_i / Delta_i (bulk copies) per block (QST stages)
 //   warp 1     MMA: S^T = K Q_i^T, dP^T = V dO_i^T into TMEM; after softmax-bwd:
 //              dV += P^T dO_i, dK += dS^T Q_i (A = P^T / dS^T read from TMEM); once per block pair
 //              dQ_pair = dS K (M = 128 queries; A = dS^T of both blocks staged in smem, M-major)
-//   warps 2-9  softmax-bwd (2 warps per TMEM lane quarter, 32 queries each), thread = key row:
+//   warps 2..  softmax-bwd: SW warps per TMEM lane quarter, 64 / SW queries each, thread = key row:
 //              P^T = exp2(S^T - LSE), dS^T = P^T (dP^T - Delta); P^T / dS^T written back to TMEM (bf16,
 //              over S^T / dP^T), dS^T also to smem (the A operand of dQ)
-//   warps 10-13 dQ drain (one per lane quarter, thread = query row): TMEM -> swizzled smem boxes ->
+//   last 4     dQ drain (one per lane quarter, thread = query row): TMEM -> swizzled smem boxes ->
 //              TMA reduce-add into the fp32 dQ accumulator, overlapped with the softmax warps
+// SW = 2 (448 threads) is the default; SW = 4 (16 softmax warps, 704 threads, 80 registers) doubles the softmax
+// warps in flight and measured slower (see bwd_softmax_warps).
 // TMEM (512 columns, one CTA per SM): NBUF x {S^T, dP^T} (64 columns each), dV, dK, 2 x dQ (DP each);
 // NBUF = 3 for dh <= 32, 2 for dh = 64.
 // Prefix (right-padded) masks: key blocks past the valid length write zero dK/dV and exit.
-constexpr int kBwdThreads = 448;  // TMA, MMA, 8 softmax-bwd warps, 4 dQ-drain warps
+template <int SW>
+struct BwdWarps {
+  static constexpr int QW = 64 / SW;                 // queries per softmax warp
+  static constexpr int SOFT = 4 * SW;                // softmax warps
+  static constexpr int DRAIN0 = 2 + SOFT;            // first dQ-drain warp
+  static constexpr int THREADS = 32 * (2 + SOFT + 4);
+};
 
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -528,6 +577,11 @@ struct BwdShape {
   static constexpr int QB = 64 * ROWB, KB = 128 * ROWB;
   static constexpr int NBUF = DP <= 32 ? 3 : 2;  // {S^T, dP^T} TMEM buffers (128 columns each)
   static constexpr int QST = DH == 64 ? 3 : 6;   // Q / dO / LSE / Delta stages (>= NBUF + 1)
+  // FOLD: the TMA warp folds block j's Delta into dO after loading block j + LAG; that load waits for block
+  // j + LAG - QST's dV / dK MMAs, which the MMA warp issues before it needs block j (at j - NBUF):
+  // LAG <= QST - NBUF keeps the cycle open
+  static constexpr int LAG = QST - NBUF < 2 ? QST - NBUF : 2;
+  static_assert(LAG >= 1, "prep lag");
   // dh padded with >= 3 zero columns (dh = 24): Delta rides in dO's padding columns and V's hold -1, so the
   // dP^T MMA directly yields dP^T - Delta (Delta split into three bf16 parts: ~24-bit exact)
   static constexpr bool FOLD = DP - DH >= 3;
@@ -547,16 +601,18 @@ struct BwdShape {
 // fastest).  All barrier phases follow global block / pair counters (every tile has nqe blocks); K / V are
 // double-buffered so the next tile's loads and first S^T / dP^T MMAs overlap this tile's tail, and the
 // dK / dV epilogue runs on the dQ-drain warps, which release the accumulators (dkv_free) for the next tile.
-template <int DH>
-__global__ void __launch_bounds__(kBwdThreads, 1)
+template <int DH, int SW>
+__global__ void __launch_bounds__(BwdWarps<SW>::THREADS, 1)
     bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
                const __grid_constant__ CUtensorMap tmdQ, const int32_t* __restrict__ key_mask,
-               int* __restrict__ sched, const float* __restrict__ LSE2, const float* __restrict__ Delta,
+               int* __restrict__ sched, const float* __restrict__ LSE, const float* __restrict__ Delta,
                float* __restrict__ dQ, __nv_bfloat16* __restrict__ dK, __nv_bfloat16* __restrict__ dV, int S,
                int nh, int nbh, const FusedOut fo) {
   using BS = BwdShape<DH>;
+  using BW = BwdWarps<SW>;
   constexpr int DP = BS::DP, ROWB = BS::ROWB, QB = BS::QB, KB = BS::KB, QST = BS::QST, NBUF = BS::NBUF;
+  constexpr int QW = BW::QW;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps shared provenance
   uint8_t* sdS = smem;               // [2][DS_BUF]
@@ -604,7 +660,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
     for (int i = 0; i < NBUF; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&ds_full[i], 8);
+      mbar_init(&ds_full[i], BW::SOFT);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&dsm_empty[i], 1);
@@ -615,7 +671,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     mbar_init(dkv_free, 4);
     for (int i = 0; i < 4; ++i) {
       mbar_init(&tile_full[i], 1);
-      mbar_init(&tile_empty[i], 1 + 8 + 4);  // MMA warp, 8 softmax warps, 4 drain warps
+      mbar_init(&tile_empty[i], 1 + BW::SOFT + 4);  // MMA warp, softmax warps, 4 drain warps
     }
     fence_mbar_init();
   }
@@ -706,17 +762,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           tma_load_2d(sQ + st * QB, &tmQ, &qdo_full[st], 0, row0 + q0);
           tma_load_2d(sdO + st * QB, &tmdO, &qdo_full[st], h * DH, b * S + q0);
           if (vb) {
-            bulk_load(sL + st * 64, LSE2 + (int64_t)bh * S + q0, vb, &qdo_full[st]);
+            bulk_load(sL + st * 64, LSE + (int64_t)bh * S + q0, vb, &qdo_full[st]);
             bulk_load(sD + st * 64, Delta + (int64_t)bh * S + q0, vb, &qdo_full[st]);
           }
         }
         __syncwarp();
         if constexpr (BS::FOLD) {
-          if (i >= 2) fold(i - 2);  // lag two stages behind the loads
+          if (i >= BS::LAG) fold(i - BS::LAG);
         }
       }
       if constexpr (BS::FOLD) {
-        for (int i = max(0, nqe - 2); i < nqe; ++i) fold(i);
+        for (int i = max(0, nqe - BS::LAG); i < nqe; ++i) fold(i);
       }
       tile = claim();
     }
@@ -774,19 +830,23 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int st = g % QST;
         mbar_wait(&ds_full[g % NBUF], (g / NBUF) & 1);
         if (i == 0 && it > 0) mbar_wait(dkv_free, (it - 1) & 1);  // previous tile's dV / dK have been read
-        if ((i & 1) && gp >= 2) mbar_wait(&dq_empty[gp & 1], ((gp >> 1) - 1) & 1);
         tc_fence_after();
         const uint64_t so = (uint64_t)((st * QB) >> 4);
         const uint32_t tS = tbase + (g % NBUF) * 128, tDP = tS + 64;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {  // 16 queries per step
           const uint32_t acc = (i > 0 || k > 0) ? 1u : 0u;
-          // packed P^T / dS^T of queries [16k, 16k+16): warp half (k >> 1) wrote them at column 32 (k >> 1) + 8 (k & 1)
-          const uint32_t pc = (uint32_t)((k >> 1) * 32 + (k & 1) * 8);
+          // packed P^T / dS^T of queries [16k, 16k+16): the softmax warp owning them wrote them at the start of
+          // its own QW fp32 columns
+          const uint32_t pc = (uint32_t)((16 * k / QW) * QW + ((16 * k) % QW) / 2);
           mma_ts_w(tdV, tS + pc, od_kv + so + k * ROWB, idesc_kv, acc);
           mma_ts_w(tdK, tDP + pc, qd_kv + so + k * ROWB, idesc_kv, acc);
         }
         if (i & 1) {
+          if (gp >= 2) {  // the drain warps have read this dQ accumulator's previous pair
+            mbar_wait(&dq_empty[gp & 1], ((gp >> 1) - 1) & 1);
+            tc_fence_after();
+          }
           const uint64_t dso = (uint64_t)(((gp & 1) * BS::DS_BUF) >> 4);
 #pragma unroll
           for (int k = 0; k < 8; ++k)  // 16 keys per step
@@ -799,10 +859,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           mma_commit_w(dkv_done);
           mma_commit_w(&kv_empty[kvs]);
         }
+        // (measured: issuing S^T / dP^T(i + NBUF) ahead of the pair's dQ MMAs is 11 % slower at dh 64 -- the
+        // MMA thread then blocks on block i + NBUF's Q / dO loads before it can issue dQ)
         if (i + NBUF < nqe) issue_s(i + NBUF);  // buffer g % NBUF is free once dV/dK(g) are issued (in-order)
       }
     }
-  } else if (warp >= 10) {
+  } else if (warp >= BW::DRAIN0) {
     // ============ dQ drain + dK / dV epilogue: 4 warps, one per TMEM lane quarter ============
     // dQ (thread = query row of the pair): TMEM -> registers -> swizzled smem boxes -> asynchronous TMA
     // reduce-add into the fp32 dQ accumulator (no per-element LSU traffic to contend with the softmax).
@@ -861,72 +923,88 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_wait(dkv_done, it & 1);
       tc_fence_after();
       const int key = k0 + qq * 32 + lane;
+      // Processed in pieces of 32 columns (register budget of the 704-thread variant): DP <= 32 -> one piece
+      // [0, DP); DP = 64 -> two pieces, [32p, 32p + 32) classic, or {16p..16p+15} U {32+16p..32+16p+15} fused
+      // (so each RoPE pair (c, c + 32) lands in one piece).
+      constexpr int NPIECE = DP > 32 ? 2 : 1;
+      auto pcol = [&](int p, int j, bool fused) -> int {
+        if constexpr (DP <= 32) return j;
+        else return fused ? (j < 16 ? 16 * p + j : 32 + 16 * p + (j - 16)) : 32 * p + j;
+      };
 #pragma unroll 1
       for (int hf = 0; hf < 2; ++hf) {
-        uint32_t u[DP];
-        const uint32_t src = (hf == 0 ? tdK : tdV) + lane_off;
+#pragma unroll 1
+        for (int p = 0; p < NPIECE; ++p) {
+          const bool fused = fo.dqkv != nullptr;
+          uint32_t u[32];
+          const uint32_t src = (hf == 0 ? tdK : tdV) + lane_off;
+          if constexpr (DP <= 32) {
 #pragma unroll
-        for (int cc = 0; cc < DP; cc += 8)
-          tmem_ld8(src + cc, u[cc], u[cc + 1], u[cc + 2], u[cc + 3], u[cc + 4], u[cc + 5], u[cc + 6], u[cc + 7]);
-        tmem_ld_wait();
-        if (hf == 1) {  // both accumulators read: the MMA warp may start the next tile's dV / dK
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(dkv_free);
-        }
-        if (fo.dqkv) {
-          // fused: RoPE^T on dK, token-major store into dqkv, bias-gradient column sums
-          float* val = reinterpret_cast<float*>(u);
+            for (int cc = 0; cc < DP; cc += 8)
+              tmem_ld8(src + cc, u[cc], u[cc + 1], u[cc + 2], u[cc + 3], u[cc + 4], u[cc + 5], u[cc + 6], u[cc + 7]);
 #pragma unroll
-          for (int cc = 0; cc < DP; ++cc) val[cc] = key < S ? __uint_as_float(u[cc]) : 0.f;
-          if (hf == 0 && key < S) {
-            constexpr int HALF = DH / 2;
-            const float* cs = fo.cos_t + (int64_t)key * HALF;
-            const float* sn = fo.sin_t + (int64_t)key * HALF;
+            for (int cc = DP; cc < 32; ++cc) u[cc] = 0u;
+          } else {
 #pragma unroll
-            for (int j = 0; j < HALF; ++j) {
-              const float c = __ldg(cs + j), sv = __ldg(sn + j);
-              const float g0 = val[j], g1 = val[j + HALF];
-              val[j] = g0 * c + g1 * sv;
-              val[j + HALF] = g1 * c - g0 * sv;
+            for (int cc = 0; cc < 32; cc += 8) {
+              const int col = pcol(p, cc, fused);
+              tmem_ld8(src + col, u[cc], u[cc + 1], u[cc + 2], u[cc + 3], u[cc + 4], u[cc + 5], u[cc + 6], u[cc + 7]);
             }
           }
-          if (key < S) {
-            __nv_bfloat16* dst = fo.dqkv + ((int64_t)b * S + key) * 3 * fo.H + (1 + hf) * fo.H + h * DH;
+          tmem_ld_wait();
+          if (hf == 1 && p == NPIECE - 1) {  // both accumulators read: the MMA warp may start the next tile's dV / dK
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(dkv_free);
+          }
+          float val[32];
 #pragma unroll
-            for (int cc = 0; cc < DH; cc += 8)
-              *reinterpret_cast<uint4*>(dst + cc) =
+          for (int j = 0; j < 32; ++j) val[j] = key < S ? __uint_as_float(u[j]) : 0.f;
+          if (fused) {
+            // fused: RoPE^T on dK, token-major store into dqkv, bias-gradient column sums
+            if (hf == 0 && key < S) {
+              constexpr int HALF = DH / 2;
+              constexpr int PH = DP > 32 ? 16 : HALF;  // pair partner distance inside the piece
+              const float* cs = fo.cos_t + (int64_t)key * HALF + (DP > 32 ? 16 * p : 0);
+              const float* sn = fo.sin_t + (int64_t)key * HALF + (DP > 32 ? 16 * p : 0);
+#pragma unroll
+              for (int j = 0; j < PH; ++j) {
+                const float c = __ldg(cs + j), sv = __ldg(sn + j);
+                const float g0 = val[j], g1 = val[j + PH];
+                val[j] = g0 * c + g1 * sv;
+                val[j + PH] = g1 * c - g0 * sv;
+              }
+            }
+            if (key < S) {
+              __nv_bfloat16* dst = fo.dqkv + ((int64_t)b * S + key) * 3 * fo.H + (1 + hf) * fo.H + h * DH;
+#pragma unroll
+              for (int cc = 0; cc < (DP > 32 ? 32 : DH); cc += 8)
+                *reinterpret_cast<uint4*>(dst + pcol(p, cc, true)) =
+                    make_uint4(pack2(val[cc], val[cc + 1]), pack2(val[cc + 2], val[cc + 3]),
+                               pack2(val[cc + 4], val[cc + 5]), pack2(val[cc + 6], val[cc + 7]));
+            }
+            const float cs = warp_transpose_sum32(val, lane);
+            const int col = pcol(p, lane, true);
+            if (col < DH && (DP > 32 || lane < DH)) red_add_f32(fo.col_sum + (1 + hf) * fo.H + h * DH + col, cs);
+          } else if (key < S) {
+            __nv_bfloat16* dst = (hf == 0 ? dK : dV) + ((int64_t)bh * S + key) * DH;
+#pragma unroll
+            for (int cc = 0; cc < (DP > 32 ? 32 : DH); cc += 8)
+              *reinterpret_cast<uint4*>(dst + pcol(p, cc, false)) =
                   make_uint4(pack2(val[cc], val[cc + 1]), pack2(val[cc + 2], val[cc + 3]),
                              pack2(val[cc + 4], val[cc + 5]), pack2(val[cc + 6], val[cc + 7]));
           }
-#pragma unroll
-          for (int c0 = 0; c0 < DH; c0 += 32) {
-            float t32[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) t32[j] = (c0 + j < DH) ? val[c0 + j] : 0.f;
-            const float cs = warp_transpose_sum32(t32, lane);
-            if (c0 + lane < DH) red_add_f32(fo.col_sum + (1 + hf) * fo.H + h * DH + c0 + lane, cs);
-          }
-        } else if (key < S) {
-          __nv_bfloat16* dst = (hf == 0 ? dK : dV) + ((int64_t)bh * S + key) * DH;
-#pragma unroll
-          for (int cc = 0; cc < DH; cc += 8)
-            *reinterpret_cast<uint4*>(dst + cc) = make_uint4(
-                pack2(__uint_as_float(u[cc]), __uint_as_float(u[cc + 1])),
-                pack2(__uint_as_float(u[cc + 2]), __uint_as_float(u[cc + 3])),
-                pack2(__uint_as_float(u[cc + 4]), __uint_as_float(u[cc + 5])),
-                pack2(__uint_as_float(u[cc + 6]), __uint_as_float(u[cc + 7])));
         }
       }
     }
     if (lane == 0) bulk_wait_all0();
   } else {
-    // ============ softmax-bwd (thread = key row; 2 warps per lane quarter, 32 queries each) ============
+    // ============ softmax-bwd (thread = key row; SW warps per lane quarter, QW queries each) ============
     const int qq = warp & 3;
     const int hf = (warp - 2) >> 2;
     const int kr = qq * 32 + lane;
     const uint32_t lane_off = (uint32_t)(qq * 32) << 16;
-    const int c = hf * 32;
+    const int c = hf * QW;
     for (int it = 0;; ++it) {
       const int slot = it & 3;
       mbar_wait(&tile_full[slot], (it >> 2) & 1);
@@ -945,17 +1023,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const uint32_t tS = tbase + (g % NBUF) * 128, tDP = tS + 64;
         mbar_wait(&s_full[g % NBUF], (g / NBUF) & 1);
         tc_fence_after();
-        uint32_t us[32], ud[32];
-        tmem_ld32(tS + lane_off + c, us);
-        tmem_ld32(tDP + lane_off + c, ud);
+        uint32_t us[QW], ud[QW];
+        tmem_ldq<QW>(tS + lane_off + c, us);
+        tmem_ldq<QW>(tDP + lane_off + c, ud);
         if (ch == 0 && gp >= 2) mbar_wait(&dsm_empty[gp & 1], ((gp >> 1) - 1) & 1);
         tmem_ld_wait();
-        uint32_t pp[16], dd[16];
+        uint32_t pp[QW / 2], dd[QW / 2];
         const int qmax = S - i * 64 - c;
-        if (__all_sync(0xffffffffu, kvalid) && qmax >= 32) {  // full tile: no masking
+        if (__all_sync(0xffffffffu, kvalid) && qmax >= QW) {  // full tile: no masking
           // packed f32x2 arithmetic; 1 in 4 exponentials (a pair per 8) on the FMA pipe
 #pragma unroll
-          for (int e = 0; e < 32; e += 8) {
+          for (int e = 0; e < QW; e += 8) {
             const float4 la = *reinterpret_cast<const float4*>(lse + e), lb = *reinterpret_cast<const float4*>(lse + e + 4);
             const uint64_t l2e = f2_splat(L2E);
             float x[8], pr[8];
@@ -989,7 +1067,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           }
         } else {
 #pragma unroll
-          for (int e = 0; e < 32; e += 4) {
+          for (int e = 0; e < QW; e += 4) {
             const float4 l4 = *reinterpret_cast<const float4*>(lse + e);
             const float4 d4 = BS::FOLD ? make_float4(0.f, 0.f, 0.f, 0.f) : *reinterpret_cast<const float4*>(dl + e);
             const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv4[4] = {d4.x, d4.y, d4.z, d4.w};
@@ -1007,14 +1085,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             dd[(e >> 1) + 1] = pack2(ds[2], ds[3]);
           }
         }
-        // packed P^T / dS^T go into this warp's own 32-column half of the S^T / dP^T buffers (which it has
-        // finished reading), so the two warps of a lane quarter need no barrier
-        tmem_st16(tS + lane_off + hf * 32, pp);
-        tmem_st16(tDP + lane_off + hf * 32, dd);
+        // packed P^T / dS^T go into the first QW/2 of this warp's own QW columns of the S^T / dP^T buffers
+        // (which it has finished reading), so the warps of a lane quarter need no barrier
+        tmem_stq<QW / 2>(tS + lane_off + c, pp);
+        tmem_stq<QW / 2>(tDP + lane_off + c, dd);
         uint8_t* rowp = sdS + (gp & 1) * BS::DS_BUF + ch * (128 * 128) + kr * 128;
 #pragma unroll
-        for (int gg = 0; gg < 4; ++gg) {
-          const int c16 = hf * 4 + gg;
+        for (int gg = 0; gg < QW / 8; ++gg) {
+          const int c16 = c / 8 + gg;
           *reinterpret_cast<uint4*>(rowp + ((c16 ^ (kr & 7)) << 4)) =
               make_uint4(dd[4 * gg], dd[4 * gg + 1], dd[4 * gg + 2], dd[4 * gg + 3]);
         }
@@ -1077,6 +1155,17 @@ static int head_map(CUtensorMap* m, const void* base, int64_t rows) {
   return 0;
 }
 
+// exponential pairs (of every four) evaluated on the FMA pipe in the forward softmax: ESM_ATTN_FWD_POLY=0/1/2.
+// Measured (B200, 35M / 650M layer shapes): 0 -> 0.238 / 0.133 ms, 1 -> 0.237 / 0.136, 2 -> 0.245 / 0.137: the
+// forward is not MUFU-throughput-bound once the S registers are used in place, so the default is 0.
+static int fwd_poly_pairs() {
+  static const int fp = [] {
+    const char* e = getenv("ESM_ATTN_FWD_POLY");
+    return e ? atoi(e) : 0;
+  }();
+  return fp;
+}
+
 template <int DH, int BN, int NSB>
 int launch_fwd(const void* q, const void* k, const void* v, const int32_t* km, int* sched, void* o, float* lse, int B,
                int nh, int S, cudaStream_t st) {
@@ -1088,17 +1177,35 @@ int launch_fwd(const void* q, const void* k, const void* v, const int32_t* km, i
       (rc = head_map<DH, BN>(&tv, v, rows)))
     return rc;
   const int smem = 2 * SH::Q_BYTES + 2 * SH::STAGES * SH::KV_BYTES + 1024 + 256;
-  cudaFuncSetAttribute(fwd_kernel<DH, BN, NSB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int nitem = ((S + BM - 1) / BM) * B * nh;
   const int per_sm = NSB == 1 ? 3 : 2;  // CTAs resident per SM
   const int grid = min(nitem, per_sm * device_sm_count());
-  fwd_kernel<DH, BN, NSB><<<grid, kThreads, smem, st>>>(tq, tk, tv, km, sched, (__nv_bfloat16*)o, lse, S, nh, B * nh);
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    kern<<<grid, kThreads, smem, st>>>(tq, tk, tv, km, sched, (__nv_bfloat16*)o, lse, S, nh, B * nh);
+  };
+  switch (fwd_poly_pairs()) {
+    case 0: go(fwd_kernel<DH, BN, NSB, 0>); break;
+    case 2: go(fwd_kernel<DH, BN, NSB, 2>); break;
+    default: go(fwd_kernel<DH, BN, NSB, 1>); break;
+  }
   ESM_LAUNCH_RET();
 }
 
 
+// softmax warps per TMEM lane quarter of the backward: 2 (448 threads, default) or 4 (704 threads,
+// ESM_ATTN_BWD_SW=4).  Measured on B200: SW = 4 is 5-6 % slower at dh 24 and 64 (0.499 vs 0.471 ms, 0.361 vs
+// 0.342 ms per launch incl. Delta) -- the stage is bound by the MMA <-> softmax hand-offs, not by warps in flight.
+static int bwd_softmax_warps() {
+  static const int sw = [] {
+    const char* e = getenv("ESM_ATTN_BWD_SW");
+    return (e && atoi(e) == 4) ? 4 : 2;
+  }();
+  return sw;
+}
+
 template <int DH>
-int launch_bwd(const void* q, const void* k, const void* v, const void* dout, const float* lse2, const float* delta,
+int launch_bwd(const void* q, const void* k, const void* v, const void* dout, const float* lse, const float* delta,
                const int32_t* km, int* sched, float* dq, void* dk, void* dv, int B, int nh, int S, cudaStream_t st,
                FusedOut fo) {
   using SH = Shape<DH, 64>;
@@ -1138,12 +1245,20 @@ int launch_bwd(const void* q, const void* k, const void* v, const void* dout, co
       return ESM_EDRIVER;
     }
   }
-  cudaFuncSetAttribute(bwd_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, BS::SMEM);
   const int ntile = ((S + 127) / 128) * B * nh;
   // persistent: one CTA per SM loops over key-block tiles
   const int grid = min(device_sm_count(), ntile);
-  bwd_kernel<DH><<<grid, kBwdThreads, BS::SMEM, st>>>(tq, tk, tv, tdo, tdq, km, sched, lse2, delta, dq,
-                                                      (__nv_bfloat16*)dk, (__nv_bfloat16*)dv, S, nh, B * nh, fo);
+  if (bwd_softmax_warps() == 2) {
+    cudaFuncSetAttribute(bwd_kernel<DH, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, BS::SMEM);
+    bwd_kernel<DH, 2><<<grid, BwdWarps<2>::THREADS, BS::SMEM, st>>>(tq, tk, tv, tdo, tdq, km, sched, lse, delta, dq,
+                                                                   (__nv_bfloat16*)dk, (__nv_bfloat16*)dv, S, nh,
+                                                                   B * nh, fo);
+  } else {
+    cudaFuncSetAttribute(bwd_kernel<DH, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, BS::SMEM);
+    bwd_kernel<DH, 4><<<grid, BwdWarps<4>::THREADS, BS::SMEM, st>>>(tq, tk, tv, tdo, tdq, km, sched, lse, delta, dq,
+                                                                   (__nv_bfloat16*)dk, (__nv_bfloat16*)dv, S, nh,
+                                                                   B * nh, fo);
+  }
   ESM_LAUNCH_RET();
 }
 
@@ -1154,16 +1269,16 @@ int attn_prepare_tc(const int32_t* km, int* sched, int B, int S, cudaStream_t st
   ESM_LAUNCH_RET();
 }
 
-int attn_bwd_tc(const void* q, const void* k, const void* v, const void* dout, const float* lse2, const float* delta,
+int attn_bwd_tc(const void* q, const void* k, const void* v, const void* dout, const float* lse, const float* delta,
                 const int32_t* km, int* sched, float* dq, void* dk, void* dv, int B, int nh, int S, int dh,
                 cudaStream_t st, void* dqkv, float* col_sum, const float* cos_t, const float* sin_t) {
   ESM_CHECK_ARG(S % 4 == 0, "attention bwd (tcgen05): S %% 4 == 0 required");
   fa::FusedOut fo{(__nv_bfloat16*)dqkv, col_sum, cos_t, sin_t, nh * dh};
   switch (dh) {
-    case 16: return fa::launch_bwd<16>(q, k, v, dout, lse2, delta, km, sched, dq, dk, dv, B, nh, S, st, fo);
-    case 24: return fa::launch_bwd<24>(q, k, v, dout, lse2, delta, km, sched, dq, dk, dv, B, nh, S, st, fo);
-    case 32: return fa::launch_bwd<32>(q, k, v, dout, lse2, delta, km, sched, dq, dk, dv, B, nh, S, st, fo);
-    case 64: return fa::launch_bwd<64>(q, k, v, dout, lse2, delta, km, sched, dq, dk, dv, B, nh, S, st, fo);
+    case 16: return fa::launch_bwd<16>(q, k, v, dout, lse, delta, km, sched, dq, dk, dv, B, nh, S, st, fo);
+    case 24: return fa::launch_bwd<24>(q, k, v, dout, lse, delta, km, sched, dq, dk, dv, B, nh, S, st, fo);
+    case 32: return fa::launch_bwd<32>(q, k, v, dout, lse, delta, km, sched, dq, dk, dv, B, nh, S, st, fo);
+    case 64: return fa::launch_bwd<64>(q, k, v, dout, lse, delta, km, sched, dq, dk, dv, B, nh, S, st, fo);
     default: set_last_error("attention: head dim %d unsupported", dh); return ESM_ENOTSUP;
   }
 }

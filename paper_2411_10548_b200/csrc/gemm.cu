@@ -43,6 +43,8 @@ struct EpiParams {
   float* col_sum2;
   // RESID: C = R + dropout(acc + bias)
   esm_dropout drop;
+  // DELTA: per-head row dot products of the bf16 output with aux_in, [B, n_heads, seq_len]
+  float* row_dot;
 };
 
 // ============================================================================
@@ -68,7 +70,7 @@ struct EpiCfg {
   static constexpr bool GELU2 = EPI == ESM_EPI_GELU || EPI == ESM_EPI_GELU_GRADAUX;  // C + aux output
   static constexpr int NOUT = GELU2 ? 2 : 1;  // outputs per chunk (GELU: C and Z; GELU_GRADAUX: C and GELU'(Z))
   static constexpr bool AUX = EPI == ESM_EPI_RESID || EPI == ESM_EPI_DGELU || EPI == ESM_EPI_STORE_LN ||
-                              EPI == ESM_EPI_MUL_AUX;
+                              EPI == ESM_EPI_MUL_AUX || EPI == ESM_EPI_DELTA;
   static constexpr int WARP_BYTES = QKV ? 0 : 2 * NOUT * CHUNK + (AUX ? 2 * CHUNK : 0);
   static constexpr int BYTES = WARPS * WARP_BYTES;
 };
@@ -375,7 +377,7 @@ __global__ void __launch_bounds__(EpiCfg<EPI>::THREADS, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
         if constexpr (EPI != ESM_EPI_F32_ACC && EPI != ESM_EPI_DGELU && EPI != ESM_EPI_STORE_LN &&
-                      EPI != ESM_EPI_MUL_AUX) {
+                      EPI != ESM_EPI_MUL_AUX && EPI != ESM_EPI_DELTA) {
           if (ep.bias != nullptr) {
             if (col0 + 32 <= ep.N) {
               const float4* b4 = reinterpret_cast<const float4*>(ep.bias + col0);  // 1 KB aligned groups
@@ -427,6 +429,34 @@ __global__ void __launch_bounds__(EpiCfg<EPI>::THREADS, 1)
             for (int j = 0; j < 32; ++j) w[j] = v[j];
             const float s1 = warp_transpose_sum32(w, lane);
             if (col0 + lane < ep.N) red_add_f32(ep.col_sum + col0 + lane, s1);
+          } else if constexpr (EPI == ESM_EPI_DELTA) {
+            // Delta[b, h, s] += sum over this chunk's columns of head h of bf16(dO) * O; a chunk of 32 columns
+            // may span several heads (dh = 24) and a head several chunks (dh = 64): partial sums are reduced
+            // with fp32 red.add into the caller-zeroed row_dot (head boundaries are warp-uniform)
+            const int row = row0 + lane;
+            const int dh = ep.head_dim;
+            const int64_t bb = row / ep.seq_len, ss = row - bb * ep.seq_len;
+            float* rd = ep.row_dot + bb * ep.n_heads * (int64_t)ep.seq_len + ss;
+            int h = col0 / dh, hend = (h + 1) * dh;
+            float part = 0.f;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              float ov[8];
+              load_vec(reinterpret_cast<const __nv_bfloat16*>(a + stage_off<false>(lane, k)), ov);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                const int c = col0 + 8 * k + e;
+                if (c == hend) {
+                  if (row < ep.M) red_add_f32(rd + (int64_t)h * ep.seq_len, part);
+                  part = 0.f;
+                  ++h;
+                  hend += dh;
+                }
+                if (c < ep.N) part = fmaf(__bfloat162float(__float2bfloat16_rn(v[8 * k + e])), ov[e], part);
+              }
+            }
+            if (row < ep.M && h * dh < ep.N) red_add_f32(rd + (int64_t)h * ep.seq_len, part);
+            __syncwarp();
           } else {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
@@ -587,7 +617,8 @@ static int launch_cg(const esm_gemm_args& a, cudaStream_t st) {
     rc = make_map(&maps.c, a.C, a.N, a.M, a.ldc, 32, 32, false, CU_TENSOR_MAP_SWIZZLE_64B);
     if (!rc && (EPI == ESM_EPI_GELU || EPI == ESM_EPI_GELU_GRADAUX))
       rc = make_map(&maps.z, a.aux_out, a.N, a.M, a.ld_aux_out, 32, 32, false, CU_TENSOR_MAP_SWIZZLE_64B);
-    if (!rc && (EPI == ESM_EPI_RESID || EPI == ESM_EPI_DGELU || EPI == ESM_EPI_STORE_LN || EPI == ESM_EPI_MUL_AUX))
+    if (!rc && (EPI == ESM_EPI_RESID || EPI == ESM_EPI_DGELU || EPI == ESM_EPI_STORE_LN || EPI == ESM_EPI_MUL_AUX ||
+                EPI == ESM_EPI_DELTA))
       rc = make_map(&maps.r, a.aux_in, a.N, a.M, a.ld_aux_in, 32, 32, false, CU_TENSOR_MAP_SWIZZLE_64B);
   }
   if (rc) return rc;
@@ -624,7 +655,7 @@ static int launch_cg(const esm_gemm_args& a, cudaStream_t st) {
   EpiParams ep{a.M, a.N, a.C, a.ldc, a.bias, a.aux_in, a.ld_aux_in, a.aux_out, a.ld_aux_out, a.col_sum,
                a.rope_cos, a.rope_sin,
                {(__nv_bfloat16*)a.q_out, (__nv_bfloat16*)a.k_out, (__nv_bfloat16*)a.v_out},
-               a.seq_len, a.n_heads, a.head_dim, a.q_scale, a.row_mean, a.row_rstd, a.col_sum2, a.drop};
+               a.seq_len, a.n_heads, a.head_dim, a.q_scale, a.row_mean, a.row_rstd, a.col_sum2, a.drop, a.row_dot};
   auto kern = gemm_tc_kernel<BN, A_MN, B_MN, EPI, CG>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);  // per device: every launch
   const int total = tiles * splits;
@@ -669,7 +700,20 @@ static int launch(const esm_gemm_args& a, cudaStream_t st) {
   return launch_cg<BN, A_MN, B_MN, EPI, 1>(a, st);
 }
 
+// ESM_GEMM_BN overrides the tile width (A/B measurements).  A wave-quantisation-aware choice (BN 160 / 128 for
+// N = 1280, which fills the last wave) measured 16-55 % SLOWER than BN = 256 on the 650M shapes (fc2 fwd 0.202 vs
+// 0.168 ms, fc1 dgrad 0.253 vs 0.163, qkv dgrad 0.192 vs 0.122): per-MMA operand reads, not the idle tail of the
+// last wave, set the time, so the widest tile wins.
+static int env_bn() {
+  static const int v = [] {
+    const char* e = getenv("ESM_GEMM_BN");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 static int pick_bn_kmajor(int N) {
+  if (env_bn() > 0) return env_bn();
   // largest tile with <= ~6% column waste; all multiples of 32
   static const int cands[] = {256, 224, 192, 160, 128, 96, 64};
   int best = 64;
@@ -745,7 +789,7 @@ int gemm_bf16(const esm_gemm_args& a, cudaStream_t st) {
       default: break;
     }
   } else {
-    const int bn = a.N > 128 ? 256 : 128;
+    const int bn = env_bn() == 128 || env_bn() == 256 ? env_bn() : (a.N > 128 ? 256 : 128);
     switch (a.epilogue) {
       case ESM_EPI_STORE: return dispatch_bn<false, true, ESM_EPI_STORE>(a, bn, st);
       case ESM_EPI_DGELU: return dispatch_bn<false, true, ESM_EPI_DGELU>(a, bn, st);
@@ -753,6 +797,12 @@ int gemm_bf16(const esm_gemm_args& a, cudaStream_t st) {
       case ESM_EPI_STORE_LN:
         ESM_CHECK_ARG(a.aux_in && a.row_mean && a.row_rstd && a.col_sum && a.col_sum2, "gemm: STORE_LN args");
         return dispatch_bn<false, true, ESM_EPI_STORE_LN>(a, bn, st);
+      case ESM_EPI_DELTA:
+        ESM_CHECK_ARG(a.aux_in && a.row_dot && a.seq_len > 0 && a.n_heads > 0 && a.head_dim > 0 &&
+                          a.N == a.n_heads * a.head_dim && a.M % a.seq_len == 0,
+                      "gemm: DELTA needs aux_in (O), row_dot and N = n_heads * head_dim, M = B * seq_len");
+        cudaMemsetAsync(a.row_dot, 0, sizeof(float) * (size_t)a.M * a.n_heads, st);  // partial sums red.add into it
+        return dispatch_bn<false, true, ESM_EPI_DELTA>(a, bn, st);
       default: break;
     }
   }
@@ -875,8 +925,9 @@ extern "C" int esm_gemm(const esm_gemm_args* args, esm_stream_t stream) {
   ESM_CHECK_ARG(args != nullptr, "esm_gemm: null args");
   const esm_gemm_args& a = *args;
   ESM_CHECK_ARG(a.M > 0 && a.N > 0 && a.K > 0, "esm_gemm: bad shape %d %d %d", a.M, a.N, a.K);
-  ESM_CHECK_ARG(a.epilogue >= 0 && a.epilogue <= ESM_EPI_MUL_AUX, "esm_gemm: bad epilogue");
-  ESM_CHECK_ARG(a.epilogue < ESM_EPI_GELU_GRADAUX || a.dtype == ESM_BF16, "esm_gemm: GELU_GRADAUX / MUL_AUX are bf16-only");
+  ESM_CHECK_ARG(a.epilogue >= 0 && a.epilogue <= ESM_EPI_DELTA, "esm_gemm: bad epilogue");
+  ESM_CHECK_ARG(a.epilogue < ESM_EPI_GELU_GRADAUX || a.dtype == ESM_BF16,
+                "esm_gemm: GELU_GRADAUX / MUL_AUX / DELTA are bf16-only");
   ESM_CHECK_ARG(a.epilogue != ESM_EPI_GELU_GRADAUX || a.aux_out, "esm_gemm: GELU_GRADAUX needs aux_out");
   ESM_CHECK_ARG(a.epilogue != ESM_EPI_MUL_AUX || a.aux_in, "esm_gemm: MUL_AUX needs aux_in");
   ESM_CHECK_ARG(a.epilogue != ESM_EPI_STORE_LN || a.dtype == ESM_BF16, "esm_gemm: STORE_LN is bf16-only");

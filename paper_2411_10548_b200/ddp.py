@@ -9,10 +9,13 @@ compute stream continues with the next layer's backward.  Two modes:
 * ``shard_optimizer=False`` (DDP): in-place all-reduce of the bucket; the model's AdamW for the bucket
   (``on_bucket``) follows on the communication stream.
 * ``shard_optimizer=True`` (ZeRO-1, the comparison point of PAPER.md:86-88): the bucket is reduce-scattered,
-  each rank runs AdamW only on its 1/N slice (its optimizer shard), and the updated fp32 master slice and bf16
-  shadow slice are all-gathered back into every rank's full buffers -- the AdamW work (and its HBM traffic) per
-  GPU drops by N while the bytes on the wire stay those of an fp32 all-reduce (fp32 bucket) or 3/4 of it
-  (bf16 bucket).
+  each rank runs AdamW only on its 1/N slice (its optimizer shard) and all-gathers the updated bf16 shadow slice
+  (the GEMM operands).  The fp32 master stays sharded: only the 1-D parameters the kernels read in fp32 (biases,
+  LayerNorm) are re-synchronised, with one small all-reduce of their owner-masked values after the last bucket
+  (``master="vectors"``, the default with a bf16 shadow; ``master="full"`` all-gathers the whole fp32 master
+  slice of every bucket as well).  AdamW work and HBM traffic per GPU drop by N, and the bytes on the wire are
+  those of a reduce-scatter plus a bf16 all-gather (3/4 of an fp32 all-reduce; 1/2 with bf16 buckets).
+  ``gather_master()`` brings every rank's full fp32 master up to date (checkpoints).
 
 ``grad_dtype="bf16"`` casts each bucket to bf16 before the collective (half the NVLink bytes) and the
 optimizer reads the bf16 sums (``esm_adamw_bf16g``).
@@ -101,9 +104,11 @@ class TorchDistComm:
 
 class GradAllReducer:
     def __init__(self, store, bucket_bytes: int = 64 << 20, group=None, grad_dtype: str = "fp32",
-                 shard_optimizer: bool = False, comm=None):
+                 shard_optimizer: bool = False, comm=None, master: str = "vectors"):
         if grad_dtype not in ("fp32", "bf16"):
             raise ValueError("grad_dtype must be 'fp32' or 'bf16'")
+        if master not in ("vectors", "full"):
+            raise ValueError("master must be 'vectors' or 'full'")
         self.store = store
         self.group = group
         self.cuda = store.g32.is_cuda
@@ -136,6 +141,23 @@ class GradAllReducer:
         # on_bucket(a, b, stream, grad): the optimizer for flat elements [a, b) -- the whole bucket (DDP) or this
         # rank's slice of it (sharded) -- with `grad` the reduced gradients of [a, b) (fp32, or bf16 buckets)
         self.on_bucket = None
+        # sharded fp32 master (ZeRO-1 with a bf16 shadow): flat indices of the 1-D parameters read in fp32 by the
+        # kernels, and this rank's ownership mask over them
+        self.full_master = master == "full" or store.p16 is None or not self.shard
+        self.vec_idx = self.vec_own = self.vec = None
+        if not self.full_master:
+            idx = [torch.arange(sl.offset, sl.offset + sl.numel) for sl in store.slots.values() if len(sl.shape) == 1]
+            idx = torch.cat(idx)
+            own = torch.zeros(store.numel, dtype=torch.bool)
+            a = 0
+            for b in self.bucket_ends:
+                oa, ob = self.owned(a, b)
+                own[oa:ob] = True
+                a = b
+            dev = store.p32.device
+            self.vec_idx = idx.to(dev)
+            self.vec_own = own[idx].to(torch.float32).to(dev)
+            self.vec = torch.empty(idx.numel(), dtype=torch.float32, device=dev)
 
     # ---------------------------------------------------------------- loss normaliser (compute stream)
     def _cur(self):
@@ -188,7 +210,8 @@ class GradAllReducer:
                 oa, ob = self.owned(a, b)
                 if self.on_bucket is not None:
                     self.on_bucket(oa, ob, self.stream, gbuf[oa:ob])
-                    self.comm.allgather(P.p32[a:b], st)
+                    if self.full_master:
+                        self.comm.allgather(P.p32[a:b], st)
                     if P.p16 is not None:
                         self.comm.allgather(P.p16[a:b], st)
                 elif self.bf16:
@@ -208,9 +231,36 @@ class GradAllReducer:
             self._next += 1
 
     def end_backward(self):
+        updated = self.on_bucket is not None
         while self._next < len(self.bucket_ends):
             self._launch(self.bucket_ends[self._next])
             self._next += 1
+        if updated and not self.full_master:
+            with (torch.cuda.stream(self.stream) if self.cuda else _Null()):
+                self._sync_vectors(self.stream.cuda_stream if self.cuda else None)
+        if self.cuda:
+            torch.cuda.current_stream(self.store.g32.device).wait_stream(self.stream)
+
+    def _sync_vectors(self, st):
+        """Owner-masked all-reduce of the 1-D fp32 parameters (each element has exactly one owner rank)."""
+        P = self.store
+        torch.index_select(P.p32, 0, self.vec_idx, out=self.vec)
+        self.vec.mul_(self.vec_own)
+        self.comm.allreduce(self.vec, st)
+        P.p32.index_copy_(0, self.vec_idx, self.vec)
+
+    def gather_master(self):
+        """All-gather every bucket's fp32 master slice (sharded mode keeps only the owned slices current)."""
+        if self.full_master:
+            return
+        st = self.stream.cuda_stream if self.cuda else None
+        with (torch.cuda.stream(self.stream) if self.cuda else _Null()):
+            if self.cuda:
+                self.stream.wait_stream(torch.cuda.current_stream(self.store.g32.device))
+            a = 0
+            for b in self.bucket_ends:
+                self.comm.allgather(self.store.p32[a:b], st)
+                a = b
         if self.cuda:
             torch.cuda.current_stream(self.store.g32.device).wait_stream(self.stream)
 

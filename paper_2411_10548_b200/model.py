@@ -35,9 +35,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import (EPI_DGELU, EPI_F32_ACC, EPI_GELU, EPI_GELU_GRADAUX, EPI_MUL_AUX, EPI_QKV_ROPE, EPI_RESID, EPI_STORE,
-                   EPI_STORE_LN, ESM_BF16,
-                   ESM_F32)
+from ._lib import (EPI_DELTA, EPI_DGELU, EPI_F32_ACC, EPI_GELU, EPI_GELU_GRADAUX, EPI_MUL_AUX, EPI_QKV_ROPE,
+                   EPI_RESID, EPI_STORE, EPI_STORE_LN, ESM_BF16, ESM_F32)
 from .config import EsmConfig
 
 ALIGN = 256  # elements; also the AdamW weight-decay chunk size
@@ -282,7 +281,7 @@ class Workspace:
         self.dq = e(B, nh, S, dh, dt=f32)
         self.dk, self.dv = e(B, nh, S, dh), e(B, nh, S, dh)
         self.dqkv = e(T, 3 * H)
-        self.delta = e(2, B, nh, S, dt=f32)  # Delta and log2-domain LSE (attention backward workspace)
+        self.delta = e(2, B, nh, S, dt=f32)  # Delta = rowsum(dO o O) per head (attention backward workspace)
         cos, sin = rope_tables(S, dh)
         self.cos = torch.from_numpy(cos).to(device)
         self.sin = torch.from_numpy(sin).to(device)
@@ -359,6 +358,9 @@ class EsmForMaskedLM:
                       self._stream())
 
     def state_dict(self) -> dict:
+        """fp32 master weights by HF name (under ZeRO-1 the sharded master is all-gathered first)."""
+        if self.comm is not None and hasattr(self.comm, "gather_master"):
+            self.comm.gather_master()
         return {n: self.store.view(self.store.p32, n).detach().cpu().clone() for n in self.store.slots}
 
     def grads(self) -> dict:
@@ -447,7 +449,7 @@ class EsmForMaskedLM:
         self.launches += self._KERNELS.get(name, 1)
 
     def _gemm(self, M, N, K, A, lda, amn, B, ldb, bmn, C, ldc, epi, bias=None, aux_in=None, ld_aux_in=0,
-              aux_out=None, ld_aux_out=0, col_sum=None, ln=None, drop=None):
+              aux_out=None, ld_aux_out=0, col_sum=None, ln=None, drop=None, delta=None):
         t = self.timer
         if t is not None:
             kind = "gemm_" + ("wgrad" if epi == EPI_F32_ACC else "dgrad" if bmn else "fwd")
@@ -456,12 +458,12 @@ class EsmForMaskedLM:
             t.begin(kind)
         self.launches += 1
         self._gemm_raw(M, N, K, A, lda, amn, B, ldb, bmn, C, ldc, epi, bias, aux_in, ld_aux_in, aux_out, ld_aux_out,
-                       col_sum, ln, drop)
+                       col_sum, ln, drop, delta)
         if t is not None:
             t.end(2.0 * M * N * K, 0.0)
 
     def _gemm_raw(self, M, N, K, A, lda, amn, B, ldb, bmn, C, ldc, epi, bias, aux_in, ld_aux_in, aux_out,
-                  ld_aux_out, col_sum, ln=None, drop=None):
+                  ld_aux_out, col_sum, ln=None, drop=None, delta=None):
         if ln is not None:  # (row_mean, row_rstd, dgamma accumulator)
             _lib.gemm_call(self._stream(), dtype=self.kdt, M=M, N=N, K=K, A=A.data_ptr(), lda=lda, a_mn_major=amn,
                            B=B.data_ptr(), ldb=ldb, b_mn_major=bmn, C=C.data_ptr(), ldc=ldc, epilogue=epi,
@@ -474,7 +476,9 @@ class EsmForMaskedLM:
                        aux_in=aux_in.data_ptr() if aux_in is not None else None, ld_aux_in=ld_aux_in,
                        aux_out=aux_out.data_ptr() if aux_out is not None else None, ld_aux_out=ld_aux_out,
                        col_sum=col_sum.data_ptr() if col_sum is not None else None, split_k=0,
-                       **({"drop": drop} if drop is not None else {}))
+                       **({"drop": drop} if drop is not None else {}),
+                       **({"row_dot": delta[0].data_ptr(), "seq_len": delta[1], "n_heads": delta[2],
+                           "head_dim": delta[3]} if delta is not None else {}))
 
     def linear_fwd(self, x, wkey, out_f, in_f, bias_key, C, epi=EPI_STORE, aux_in=None, aux_out=None, drop=None):
         T = x.shape[0]
@@ -698,16 +702,22 @@ class EsmForMaskedLM:
                  self._g32(p + "attention.output.dense.bias").data_ptr(), T, H, *self._drop_bwd(ws, 2 * l), st)
             # attention (branch gradient: through the out-projection's dropout mask)
             dbr = ws.dxd if ws.dxd is not None else ws.dx1
-            self.linear_dgrad(dbr, p + "attention.output.dense.weight", H, H, ws.do)
+            if kdt == ESM_BF16:  # dO, and Delta = rowsum(dO o O) per head from the same epilogue (no extra pass)
+                self._gemm(T, H, H, dbr, H, 0, self._w(p + "attention.output.dense.weight", (H, H)), H, 1, ws.do, H,
+                           EPI_DELTA, aux_in=ly.o, ld_aux_in=H, delta=(ws.delta, S, nh, dh))
+                o_arg = None
+            else:
+                self.linear_dgrad(dbr, p + "attention.output.dense.weight", H, H, ws.do)
+                o_arg = ly.o.data_ptr()
             self.linear_wgrad(dbr, ly.o, p + "attention.output.dense.weight", H, H)
             if kdt == ESM_BF16 and self._fused_attn_bwd(dh):
                 # fused: attention backward writes dqkv [T,3H] (RoPE^T, q-scale) + q/k/v bias grads
-                call("esm_attn_bwd_qkv", ly.q.data_ptr(), ly.k.data_ptr(), ly.v.data_ptr(), ly.o.data_ptr(),
+                call("esm_attn_bwd_qkv", ly.q.data_ptr(), ly.k.data_ptr(), ly.v.data_ptr(), o_arg,
                      ws.do.data_ptr(), ly.lse.data_ptr(), ws.am.data_ptr(), sched, ws.delta.data_ptr(),
                      ws.dq.data_ptr(), ws.dqkv.data_ptr(), self._g32(p + "attention.self.qkv.bias").data_ptr(), ws.cos.data_ptr(),
                      ws.sin.data_ptr(), qs, B, nh, S, dh, st, flops=8.0 * B * nh * S * S * dh)
             else:
-                call("esm_attn_bwd", kdt, ly.q.data_ptr(), ly.k.data_ptr(), ly.v.data_ptr(), ly.o.data_ptr(),
+                call("esm_attn_bwd", kdt, ly.q.data_ptr(), ly.k.data_ptr(), ly.v.data_ptr(), o_arg,
                      ws.do.data_ptr(), ly.lse.data_ptr(), ws.am.data_ptr(), sched, ws.delta.data_ptr(),
                      ws.dq.data_ptr(), ws.dk.data_ptr(), ws.dv.data_ptr(), B, nh, S, dh, st, flops=8.0 * B * nh * S * S * dh)
                 call("esm_qkv_rope_bwd", kdt, ws.dq.data_ptr(), ws.dk.data_ptr(), ws.dv.data_ptr(),

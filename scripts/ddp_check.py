@@ -73,15 +73,18 @@ def main():
     for dtype in ("fp32", "bf16"):
         ref = single_gpu_reference(cfg, dtype, ids_all, world, dev, 2) if rank == 0 else None
         p0 = EsmForMaskedLM(cfg, dtype=dtype, device=dev, seed=3).store.p32.clone()
-        modes = [("ddp", False, "fp32"), ("zero1", True, "fp32"), ("ddp_bf16grad", False, "bf16"),
-                 ("zero1_bf16grad", True, "bf16")]
-        for name, shard, gdt in modes:
+        modes = [("ddp", False, "fp32", "vectors"), ("zero1", True, "fp32", "vectors"),
+                 ("ddp_bf16grad", False, "bf16", "vectors"), ("zero1_bf16grad", True, "bf16", "vectors"),
+                 ("zero1_fullmaster", True, "fp32", "full")]
+        for name, shard, gdt, master in modes:
             m = EsmForMaskedLM(cfg, dtype=dtype, device=dev, seed=3)
-            m.comm = GradAllReducer(m.store, bucket_bytes=4 << 20, shard_optimizer=shard, grad_dtype=gdt)
+            m.comm = GradAllReducer(m.store, bucket_bytes=4 << 20, shard_optimizer=shard, grad_dtype=gdt,
+                                    master=master)
             losses = []
             for step in range(2):
                 ws = stage(m, ids_all[step][rank * B:(rank + 1) * B], rank, step)
                 losses.append(float(m.step(ws).item()))
+            m.comm.gather_master()  # sharded fp32 master -> full (the check reads every parameter)
             if rank == 0:
                 dp = m.store.p32 - p0
                 dref = ref[1][2] - p0
@@ -137,6 +140,7 @@ def main():
                     m.graph_step()
                 else:
                     m.step(ws)
+            m.comm.gather_master()
             torch.cuda.synchronize()
             pa.append(m.store.p32.clone())
         e = rel(pa[1] - p0, pa[0] - p0) if pa[0].shape == p0.shape else 1.0

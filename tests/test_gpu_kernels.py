@@ -10,7 +10,7 @@ import torch
 pytestmark = pytest.mark.gpu
 
 from paper_2411_10548_b200 import _lib  # noqa: E402
-from paper_2411_10548_b200._lib import EPI_GELU_GRADAUX, EPI_MUL_AUX  # noqa: E402
+from paper_2411_10548_b200._lib import EPI_DELTA, EPI_GELU_GRADAUX, EPI_MUL_AUX  # noqa: E402
 from paper_2411_10548_b200._lib import (EPI_DGELU, EPI_F32_ACC, EPI_GELU, EPI_QKV_ROPE, EPI_RESID, EPI_STORE,  # noqa: E402
                                         ESM_BF16, ESM_F32)
 
@@ -97,6 +97,32 @@ def test_gemm_dgrad(M, N, K, dt):
     want = ref * gelu_grad(Z.float())
     assert rel(C, want) < tol
     assert rel(cs, want.sum(0)) < (2e-2 if dt == "bf16" else 1e-4)
+
+
+@pytest.mark.parametrize("B,S,nh,dh", [(2, 256, 20, 24), (16, 256, 20, 64), (3, 100, 4, 16), (2, 512, 12, 64),
+                                        (4, 96, 10, 32), (1, 2048, 40, 64)])
+def test_gemm_delta_epilogue(B, S, nh, dh):
+    """Out-projection dgrad with Delta: dO = dY · W stored bf16, and row_dot[b, h, s] = sum over head h of
+    bf16(dO) * O (the attention backward's rowsum(dO o O)), heads straddling 32-column chunks (dh 24) and
+    spanning several (dh 64), rows of several sequences, M >= 2048 (CTA-pair kernels) and ragged M."""
+    torch.manual_seed(4)
+    H = nh * dh
+    M = B * S
+    dY = torch.randn(M, H, device=DEV).bfloat16()
+    W = (torch.randn(H, H, device=DEV) * 0.05).bfloat16()
+    O = torch.randn(M, H, device=DEV).bfloat16()
+    C = torch.empty(M, H, device=DEV, dtype=torch.bfloat16)
+    delta = torch.full((B, nh, S), 7.0, device=DEV)  # the callee zeroes it
+    _lib.gemm_call(st(), dtype=ESM_BF16, M=M, N=H, K=H, A=dY.data_ptr(), lda=H, a_mn_major=0, B=W.data_ptr(), ldb=H,
+                   b_mn_major=1, C=C.data_ptr(), ldc=H, epilogue=EPI_DELTA, aux_in=O.data_ptr(), ld_aux_in=H,
+                   row_dot=delta.data_ptr(), seq_len=S, n_heads=nh, head_dim=dh)
+    torch.cuda.synchronize()
+    ref = dY.float() @ W.float()
+    assert rel(C, ref) < 2e-2
+    want = (C.float() * O.float()).view(B, S, nh, dh).sum(-1).permute(0, 2, 1)
+    err = ((delta - want).abs().max() / want.abs().max()).item()
+    print(f"Delta epilogue B={B} S={S} nh={nh} dh={dh}: max rel err {err:.2e}")
+    assert err < 1e-5
 
 
 @pytest.mark.parametrize("M,N,K", [(480, 1920, 4096), (1440, 480, 8192), (128, 128, 64), (96, 200, 1000),
@@ -191,7 +217,7 @@ def test_attention_fwd_bwd(dh, S, lens, dt):
     assert rel(o, ref_o) < tol
     s = qr.detach() @ kr.detach().transpose(-1, -2)
     s = s + torch.where(am[:, None, None, :] > 0, 0.0, float("-inf"))
-    assert rel(lse, torch.logsumexp(s, -1)) < (1e-3 if dt == "bf16" else 1e-6)
+    assert rel(-lse * math.log(2.0), torch.logsumexp(s, -1)) < (1e-3 if dt == "bf16" else 1e-6)  # ABI: -LSE log2 e
     do = torch.randn(B * S, nh * dh, device=DEV).to(tdt)
     ref_o.backward(do.float())
     dq = torch.empty(B, nh, S, dh, device=DEV)
@@ -206,6 +232,15 @@ def test_attention_fwd_bwd(dh, S, lens, dt):
     assert rel(dv, vr.grad) < tol
     assert rel(dk, kr.grad) < tol
     assert rel(dq, qr.grad) < tol
+    if dt == "bf16":  # o = NULL: Delta precomputed by the caller (the model's ESM_EPI_DELTA path)
+        delta2 = torch.zeros(2, B, nh, S, device=DEV)
+        delta2[0] = (do.float() * o.float()).view(B, S, nh, dh).sum(-1).permute(0, 2, 1)
+        dq2, dk2, dv2 = torch.empty_like(dq), torch.empty_like(dk), torch.empty_like(dv)
+        _lib.call("esm_attn_bwd", kdt, q.data_ptr(), k.data_ptr(), v.data_ptr(), None, do.data_ptr(),
+                  lse.data_ptr(), am.data_ptr(), sched.data_ptr(), delta2.data_ptr(), dq2.data_ptr(), dk2.data_ptr(),
+                  dv2.data_ptr(), B, nh, S, dh, st())
+        torch.cuda.synchronize()
+        assert rel(dv2, dv) < 1e-6 and rel(dk2, dk) < 1e-2 and rel(dq2, dq) < 1e-2
 
 
 def _attn_case(B, nh, S, dh, lens, seed, holes=None):

@@ -176,13 +176,14 @@ def _zero1_worker(rank, world, port, q):
         from paper_2411_10548_b200.ddp import GradAllReducer
         cfg = EsmConfig(hidden_size=64, num_hidden_layers=3, num_attention_heads=4, intermediate_size=256)
         results = {}
-        for mode in ("ddp", "zero1", "zero1_bf16", "ddp_bf16"):
+        for mode in ("ddp", "zero1", "zero1_bf16", "ddp_bf16", "zero1_full"):
             st = ParamStore(cfg, "cpu", shadow=True)
             torch.manual_seed(0)
             st.p32.copy_(torch.randn(st.numel))
             st.p16.copy_(st.p32)
             red = GradAllReducer(st, bucket_bytes=32 << 10, shard_optimizer=mode.startswith("zero1"),
-                                 grad_dtype="bf16" if mode.endswith("bf16") else "fp32")
+                                 grad_dtype="bf16" if mode.endswith("bf16") else "fp32",
+                                 master="full" if mode.endswith("full") else "vectors")
             calls = []
 
             def upd(a, b, stream, g, st=st, calls=calls):
@@ -200,9 +201,16 @@ def _zero1_worker(rank, world, port, q):
                     red.ready(f"esm.encoder.layer.{l}.attention.LayerNorm.bias")
                 red.end_backward()
             owned = sum(b - a for a, b in calls) // 2
-            results[mode] = (st.p32.clone(), st.p16.clone(), owned, st.numel)
+            # sharded fp32 master: the 1-D (fp32-read) parameters are current on every rank right after the
+            # step; the rest of the master after gather_master()
+            vec_idx = torch.cat([torch.arange(sl.offset, sl.offset + sl.numel) for sl in st.slots.values()
+                                 if len(sl.shape) == 1])
+            vecs = st.p32[vec_idx].clone()
+            red.gather_master()
+            results[mode] = (st.p32.clone(), st.p16.clone(), owned, st.numel, vecs, vec_idx)
         ddp, z1 = results["ddp"], results["zero1"]
-        ok = torch.equal(ddp[0], z1[0]) and torch.equal(ddp[1], z1[1])
+        ok = torch.equal(ddp[0], z1[0]) and torch.equal(ddp[1], z1[1]) and torch.equal(z1[4], ddp[0][z1[5]])
+        ok = ok and torch.equal(results["zero1_full"][0], ddp[0]) and torch.equal(results["zero1_full"][1], ddp[1])
         ok = ok and z1[2] * world == z1[3] and ddp[2] == ddp[3]  # each rank updated exactly 1/world of the buffer
         zb, db = results["zero1_bf16"], results["ddp_bf16"]
         ok = ok and torch.equal(zb[0], db[0]) and (zb[0] - ddp[0]).abs().max().item() < 0.05
