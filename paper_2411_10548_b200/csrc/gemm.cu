@@ -54,6 +54,11 @@ namespace sm100 {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
+// Bottleneck experiments (scripts/gemm_exp.sh builds them into a separate library; never defined in the product
+// build): 1 = no TMA operand loads (MMAs read stale shared memory), 2 = no MMAs (the epilogue drains stale TMEM).
+#ifndef ESM_GEMM_EXP
+#define ESM_GEMM_EXP 0
+#endif
 // warp0 TMA, warp1 MMA (+TMEM alloc), warps 2.. epilogue: EW warps per TMEM lane quarter take interleaved
 // 32-column chunks (EpiCfg::EW).
 
@@ -90,14 +95,18 @@ struct Cfg {
 
 struct TileInfo {
   int num_m, num_n, splits, kb_total, kb_per_split;
+  int num_ng;  // column-tile groups: ceil(num_n / MC), MC pairs of a cluster take adjacent column tiles
 };
 
-__device__ __forceinline__ void decode_tile(const TileInfo& ti, int t, int& mb, int& nb, int& kb0, int& kb1) {
-  const int per_split = ti.num_m * ti.num_n;
+// unit tile t -> (row block, column tile of pair `pi` of the cluster, k range); n fastest: concurrent units
+// share the A row-block in L2
+template <int MC>
+__device__ __forceinline__ void decode_tile(const TileInfo& ti, int t, int pi, int& mb, int& nb, int& kb0, int& kb1) {
+  const int per_split = ti.num_m * ti.num_ng;
   const int split = t / per_split;
   const int rem = t - split * per_split;
-  mb = rem / ti.num_n;  // n fastest: concurrent CTAs share the A row-block in L2
-  nb = rem - mb * ti.num_n;
+  mb = rem / ti.num_ng;
+  nb = (rem - mb * ti.num_ng) * MC + pi;
   kb0 = split * ti.kb_per_split;
   kb1 = min(ti.kb_total, kb0 + ti.kb_per_split);
 }
@@ -133,9 +142,13 @@ struct EpiMaps {
   CUtensorMap c, z, r;
 };
 
-// CG = 2: a CTA pair (cluster of 2) computes a 256 x BN tile with tcgen05.mma.cta_group::2 -- each CTA
-// loads its 128 rows of A and half of B's columns, so per-SM operand traffic drops by a third.
-template <int BN, bool A_MN, bool B_MN, int EPI, int CG>
+// CG = 2: a CTA pair computes a 256 x BN tile with tcgen05.mma.cta_group::2 -- each CTA loads its 128 rows of
+// A and half of B's columns, so per-SM operand traffic drops by a third.
+// MC = 2 (CG = 2 only): a cluster of two pairs computes two adjacent column tiles of the same row block; the
+// shared A rows are loaded once by pair 0 and multicast into both pairs (TMA .multicast::cluster), a quarter
+// less L2 -> SM operand traffic (the GEMMs are bound by it: scripts/gemm_exp.sh); every stage is released by
+// both pairs' MMA commits before it is refilled.
+template <int BN, bool A_MN, bool B_MN, int EPI, int CG, int MC = 1>
 __global__ void __launch_bounds__(EpiCfg<EPI>::THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ EpiMaps maps, TileInfo ti, EpiParams ep) {
@@ -157,14 +170,19 @@ __global__ void __launch_bounds__(EpiCfg<EPI>::THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int rank = CG == 2 ? (int)cluster_ctarank() : 0;
-  const int unit = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;   // tile-processing unit (CTA or pair)
-  const int nunits = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  static_assert(MC == 1 || CG == 2, "multicast clusters are built from CTA pairs");
+  constexpr int CL = CG * MC;  // cluster size
+  const int crank = CL > 1 ? (int)cluster_ctarank() : 0;
+  const int rank = crank & (CG - 1);  // rank within the pair
+  const int pi = crank / CG;          // pair index within the cluster
+  const int unit = (int)blockIdx.x / CL;  // tile-processing unit (CTA, pair or cluster of pairs)
+  const int nunits = (int)gridDim.x / CL;
+  constexpr uint16_t kAllMask = (uint16_t)((1u << CL) - 1u);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
+      mbar_init(&empty_bar[s], MC);  // released by every pair of the cluster
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull_bar[b], 1);
@@ -183,11 +201,11 @@ __global__ void __launch_bounds__(EpiCfg<EPI>::THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if constexpr (CG == 2) cluster_sync();  // peer barriers initialised before any remote arrive / TMA
+  if constexpr (CL > 1) cluster_sync();  // peer barriers initialised before any remote arrive / TMA
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int num_tiles = ti.num_m * ti.num_n * ti.splits;
+  const int num_tiles = ti.num_m * ti.num_ng * ti.splits;
 
   if (warp == 0) {
     // ===================== TMA producer =====================
@@ -199,16 +217,29 @@ __global__ void __launch_bounds__(EpiCfg<EPI>::THREADS, 1)
     };
     for (int t = unit; t < num_tiles; t += nunits) {
       int mb, nb, kb0, kb1;
-      decode_tile(ti, t, mb, nb, kb0, kb1);
+      decode_tile<MC>(ti, t, pi, mb, nb, kb0, kb1);
       const int m0 = mb * BM * CG + rank * BM;   // this CTA's A rows
       const int n0 = nb * BN + rank * BNC;       // this CTA's B columns
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&empty_bar[stage], phase ^ 1);
-        if (lane == 0) {
+        if (ESM_GEMM_EXP == 1) {
+          if (lane == 0 && rank == 0) mbar_arrive(&full_bar[stage]);
+        } else if (lane == 0) {
           uint8_t* a_dst = sA + stage * C::A_BYTES;
           uint8_t* b_dst = sB + stage * C::B_BYTES;
           if (rank == 0) mbar_expect_tx(&full_bar[stage], C::STAGE_BYTES * CG);  // both CTAs' bytes
-          if constexpr (!A_MN) {
+          if constexpr (MC == 2) {  // A: pair 0 loads it into its own and pair 1's CTA of the same rank
+            if (pi == 0) {
+              const uint16_t mask = (uint16_t)((1u << rank) | (1u << (rank + CG)));
+              if constexpr (!A_MN) {
+                tma_load_2d_pair_mc(a_dst, &tmA, &full_bar[stage], kb * BK, m0, mask);
+              } else {
+#pragma unroll
+                for (int i = 0; i < BM / 64; ++i)
+                  tma_load_2d_pair_mc(a_dst + i * 64 * BK * 2, &tmA, &full_bar[stage], m0 + i * 64, kb * BK, mask);
+              }
+            }
+          } else if constexpr (!A_MN) {
             load(a_dst, &tmA, &full_bar[stage], kb * BK, m0);
           } else {
 #pragma unroll
@@ -238,7 +269,7 @@ __global__ void __launch_bounds__(EpiCfg<EPI>::THREADS, 1)
     int it = 0;
     for (int t = unit; t < num_tiles; t += nunits, ++it) {
       int mb, nb, kb0, kb1;
-      decode_tile(ti, t, mb, nb, kb0, kb1);
+      decode_tile<MC>(ti, t, pi, mb, nb, kb0, kb1);
       const int buf = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
       mbar_wait(&tempty_bar[buf], aphase ^ 1);
@@ -256,12 +287,13 @@ __global__ void __launch_bounds__(EpiCfg<EPI>::THREADS, 1)
                                      : make_sdesc_sw128(a_base + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? make_sdesc_sw128(b_base + k * 16 * 128, BK * 128, 1024)
                                      : make_sdesc_sw128(b_base + k * 32, 16, 1024);
+            if (ESM_GEMM_EXP == 2) break;
             if constexpr (CG == 2) mma_bf16_ss_pair(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
             else mma_bf16_ss(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           }
           if constexpr (CG == 2) {
-            mma_commit_pair(&empty_bar[stage]);
-            if (kb == kb1 - 1) mma_commit_pair(&tfull_bar[buf]);
+            mma_commit_pair(&empty_bar[stage], kAllMask);  // every CTA of the cluster: its stage may be refilled
+            if (kb == kb1 - 1) mma_commit_pair(&tfull_bar[buf], (uint16_t)(3u << (pi * CG)));
           } else {
             mma_commit(&empty_bar[stage]);
             if (kb == kb1 - 1) mma_commit(&tfull_bar[buf]);
@@ -288,7 +320,7 @@ __global__ void __launch_bounds__(EpiCfg<EPI>::THREADS, 1)
     int it = 0;
     for (int t = unit; t < num_tiles; t += nunits, ++it) {
       int mb, nb, kb0, kb1;
-      decode_tile(ti, t, mb, nb, kb0, kb1);
+      decode_tile<MC>(ti, t, pi, mb, nb, kb0, kb1);
       const int buf = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
       const int row0 = mb * BM * CG + rank * BM + q * 32;
@@ -539,7 +571,7 @@ __global__ void __launch_bounds__(EpiCfg<EPI>::THREADS, 1)
     __syncwarp();
   }
   __syncthreads();
-  if constexpr (CG == 2) cluster_sync();  // both CTAs done with TMEM and remote barriers
+  if constexpr (CL > 1) cluster_sync();  // every CTA done with TMEM and remote barriers
   if (warp == 1) {
     tc_fence_after();
     if constexpr (CG == 2) tmem_dealloc_pair<C::TMEM_COLS>(tmem_base);
@@ -591,7 +623,7 @@ static int make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t o
 
 static int num_sms() { return device_sm_count(); }
 
-template <int BN, bool A_MN, bool B_MN, int EPI, int CG>
+template <int BN, bool A_MN, bool B_MN, int EPI, int CG, int MC = 1>
 static int launch_cg(const esm_gemm_args& a, cudaStream_t st) {
   using C = Cfg<BN, EPI, CG>;
   CUtensorMap tA, tB;
@@ -627,9 +659,10 @@ static int launch_cg(const esm_gemm_args& a, cudaStream_t st) {
   ti.num_m = (a.M + BM * CG - 1) / (BM * CG);
   ti.num_n = (a.N + BN - 1) / BN;
   ti.kb_total = (a.K + BK - 1) / BK;
+  ti.num_ng = (ti.num_n + MC - 1) / MC;
   int splits = 1;
-  const int tiles = ti.num_m * ti.num_n;
-  const int sms = num_sms() / CG;  // tile-processing units (CTAs or CTA pairs)
+  const int tiles = ti.num_m * ti.num_ng;
+  const int sms = num_sms() / (CG * MC);  // tile-processing units (CTAs, CTA pairs or clusters of pairs)
   if (EPI == ESM_EPI_F32_ACC) {
     if (a.split_k > 0) {
       splits = a.split_k;
@@ -656,21 +689,52 @@ static int launch_cg(const esm_gemm_args& a, cudaStream_t st) {
                a.rope_cos, a.rope_sin,
                {(__nv_bfloat16*)a.q_out, (__nv_bfloat16*)a.k_out, (__nv_bfloat16*)a.v_out},
                a.seq_len, a.n_heads, a.head_dim, a.q_scale, a.row_mean, a.row_rstd, a.col_sum2, a.drop, a.row_dot};
-  auto kern = gemm_tc_kernel<BN, A_MN, B_MN, EPI, CG>;
+  auto kern = gemm_tc_kernel<BN, A_MN, B_MN, EPI, CG, MC>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);  // per device: every launch
   const int total = tiles * splits;
-  const int units = total < sms ? total : sms;
+  int units = total < sms ? total : sms;
+  if constexpr (CG * MC > 1) {
+    // persistent clusters must all be co-resident: a cluster that waits for a free GPC slot runs as a second
+    // wave.  Size the grid by the occupancy API (per device and configuration, cached).
+    static int cached[16] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int& maxc = cached[dev & 15];
+    if (maxc == 0) {
+      cudaLaunchConfig_t qc = {};
+      qc.gridDim = dim3(CG * MC * sms);
+      qc.blockDim = dim3(EpiCfg<EPI>::THREADS);
+      qc.dynamicSmemBytes = C::SMEM;
+      cudaLaunchAttribute qa[1];
+      qa[0].id = cudaLaunchAttributeClusterDimension;
+      qa[0].val.clusterDim.x = CG * MC;
+      qa[0].val.clusterDim.y = 1;
+      qa[0].val.clusterDim.z = 1;
+      qc.attrs = qa;
+      qc.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, (void*)kern, &qc) != cudaSuccess || n <= 0) {
+        cudaGetLastError();
+        n = sms;
+      }
+      maxc = n;
+      if (getenv("ESM_GEMM_VERBOSE"))
+        fprintf(stderr, "esm gemm: BN %d CG %d MC %d EPI %d: %d co-resident clusters (%d wanted)\n", BN, CG, MC, EPI,
+                n, sms);
+    }
+    if (units > maxc) units = maxc;
+  }
   if constexpr (CG == 1) {
     kern<<<units, EpiCfg<EPI>::THREADS, C::SMEM, st>>>(tA, tB, maps, ti, ep);
   } else {
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(units * CG);
+    cfg.gridDim = dim3(units * CG * MC);
     cfg.blockDim = dim3(EpiCfg<EPI>::THREADS);
     cfg.dynamicSmemBytes = C::SMEM;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.x = CG * MC;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
@@ -688,6 +752,17 @@ static bool pair_enabled() {
   }
   return g_pair_mode == 1;
 }
+// ESM_GEMM_MC=1 enables the multicast clusters of two pairs.  Off by default: per SM they are ~8 % faster (a
+// quarter less L2 -> SM operand traffic), but only 33 clusters of 4 CTAs are co-resident on a B200 (132 of 148
+// SMs: GPC placement), so every 650M GEMM measured 2-12 % slower than pairs on all 148 SMs (fc1 fwd 0.193 vs
+// 0.186 ms, qkv dgrad 0.135 vs 0.122).
+static bool mc_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("ESM_GEMM_MC");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
 
 template <int BN, bool A_MN, bool B_MN, int EPI>
 static int launch(const esm_gemm_args& a, cudaStream_t st) {
@@ -695,7 +770,10 @@ static int launch(const esm_gemm_args& a, cudaStream_t st) {
   // N-major B each half must be a whole number of 64-column TMA boxes.
   constexpr bool pair_ok = (BN % 32 == 0) && (!B_MN || (BN / 2) % 64 == 0);
   if constexpr (pair_ok) {
-    if (pair_enabled() && a.M >= 2 * BM * 8) return launch_cg<BN, A_MN, B_MN, EPI, 2>(a, st);
+    if (pair_enabled() && a.M >= 2 * BM * 8) {
+      if (mc_enabled() && a.N > BN) return launch_cg<BN, A_MN, B_MN, EPI, 2, 2>(a, st);
+      return launch_cg<BN, A_MN, B_MN, EPI, 2>(a, st);
+    }
   }
   return launch_cg<BN, A_MN, B_MN, EPI, 1>(a, st);
 }
