@@ -285,6 +285,27 @@ __global__ void __launch_bounds__(64) bwd_dkv_f32_kernel(const float* __restrict
       }
 }
 
+// zero fill of the fp32 dQ accumulator as a kernel (a memset node would break the programmatic-dependent-launch
+// chain of the backward)
+__global__ void __launch_bounds__(256) zero_f32_kernel(float4* __restrict__ p, int64_t n4) {
+  pdl_wait();
+  pdl_trigger();
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = z;
+}
+
+void zero_f32(float* p, int64_t n, cudaStream_t st) {
+  if (n % 4 == 0 && ((uintptr_t)p & 15) == 0) {
+    const int64_t n4 = n / 4;
+    int64_t g = (n4 + 255) / 256;
+    if (g > device_sm_count() * 8) g = device_sm_count() * 8;
+    launch_pdl(zero_f32_kernel, dim3((unsigned)g), dim3(256), 0, st, 1, reinterpret_cast<float4*>(p), n4);
+  } else {
+    cudaMemsetAsync(p, 0, sizeof(float) * n, st);
+  }
+}
+
 // dq (fp32, token-major [T, H]) -> dqkv[:, 0:H] with RoPE^T and q_scale; col_sum[0:H] += column sums.
 // RoPE^T + q-scale of the token-major fp32 dQ accumulator -> the q part of dqkv (bf16) + q bias-grad column
 // sums.  Thread = two adjacent rotation pairs (vector accesses), RU tokens in flight per iteration.
@@ -338,6 +359,8 @@ __global__ void __launch_bounds__(256) dq_finalize_vec_kernel(const float* __res
                                                               float* __restrict__ csum, const float* __restrict__ cs,
                                                               const float* __restrict__ sn, int64_t T_, int S, int nh,
                                                               int dh, float qs) {
+  pdl_wait();  // programmatic dependent launch (common.cuh)
+  pdl_trigger();
   const int half = dh >> 1, cpr = half >> 2;
   const int lanes = nh * cpr;
   const int slots = blockDim.x / lanes;
@@ -419,7 +442,7 @@ extern "C" int esm_attn_bwd(int dtype, const void* q, const void* k, const void*
     ESM_CHECK_ARG(S % 4 == 0, "esm_attn_bwd: bf16 needs S %% 4 == 0 (pad the batch)");
     // o == NULL: Delta was accumulated by the dO-producing GEMM (ESM_EPI_DELTA)
     if (o) attn::launch_delta<__nv_bfloat16>(o, dout, delta, T_, S, nh, dh, st);
-    cudaMemsetAsync(dq, 0, sizeof(float) * T_ * nh * dh, st);
+    attn::zero_f32(dq, T_ * nh * dh, st);
     const int rc = attn_bwd_tc(q, k, v, dout, lse, delta, key_mask, sched, dq, dk, dv, B, nh, S, dh, st, nullptr,
                                nullptr, nullptr, nullptr);
     if (rc) return rc;
@@ -446,7 +469,7 @@ extern "C" int esm_attn_bwd_qkv(const void* q, const void* k, const void* v, con
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int64_t T_ = (int64_t)B * S;
   if (o) attn::launch_delta<__nv_bfloat16>(o, dout, delta, T_, S, nh, dh, st);
-  cudaMemsetAsync(dq_ws, 0, sizeof(float) * T_ * nh * dh, st);
+  attn::zero_f32(dq_ws, T_ * nh * dh, st);
   const int rc = attn_bwd_tc(q, k, v, dout, lse, delta, key_mask, sched, dq_ws, nullptr, nullptr, B, nh, S, dh, st,
                              dqkv, col_sum, cos_t, sin_t);
   if (rc) return rc;
@@ -455,8 +478,8 @@ extern "C" int esm_attn_bwd_qkv(const void* q, const void* k, const void* v, con
     const int slots = 256 / lanes;
     const int64_t want = (T_ + (int64_t)slots * 16 - 1) / ((int64_t)slots * 16);  // ~16 tokens per thread
     const int grid = (int)(want < device_sm_count() * 8 ? (want < 1 ? 1 : want) : device_sm_count() * 8);
-    attn::dq_finalize_vec_kernel<<<grid, slots * lanes, 0, st>>>(dq_ws, (__nv_bfloat16*)dqkv, col_sum, cos_t, sin_t,
-                                                                  T_, S, nh, dh, q_scale);
+    launch_pdl(attn::dq_finalize_vec_kernel, dim3(grid), dim3(slots * lanes), 0, st, 1, (const float*)dq_ws,
+               (__nv_bfloat16*)dqkv, col_sum, cos_t, sin_t, T_, S, nh, dh, q_scale);
     ESM_LAUNCH_RET();
   }
   const int pairs = nh * dh / 2;

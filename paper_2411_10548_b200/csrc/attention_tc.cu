@@ -269,6 +269,8 @@ __global__ void __launch_bounds__(kThreads, NSB == 1 ? 3 : 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
+  pdl_wait();  // programmatic dependent launch: predecessor complete (common.cuh)
+  pdl_trigger();
 
   int G0 = 0;  // KV tiles processed by this CTA before the current item (same in every role)
   // dynamic item scheduler: the TMA warp claims items (first = blockIdx.x) and publishes them through the
@@ -687,6 +689,8 @@ __global__ void __launch_bounds__(BwdWarps<SW>::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
+  pdl_wait();  // programmatic dependent launch: predecessor complete (common.cuh)
+  pdl_trigger();
   const uint32_t tdV = tbase + 128 * NBUF, tdK = tdV + DP, tdQ0 = tdK + DP;  // dQ double buffered
 
   if (warp == 0) {
@@ -1197,7 +1201,8 @@ int launch_fwd(const void* q, const void* k, const void* v, const int32_t* km, i
   const int grid = min(nitem, per_sm * device_sm_count());
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    kern<<<grid, kThreads, smem, st>>>(tq, tk, tv, km, sched, (__nv_bfloat16*)o, lse, S, nh, B * nh);
+    launch_pdl(kern, dim3(grid), dim3(kThreads), smem, st, 1, tq, tk, tv, km, sched, (__nv_bfloat16*)o, lse, S, nh,
+               B * nh);
   };
   switch (fwd_poly_pairs()) {
     case 0: go(fwd_kernel<DH, BN, NSB, 0>); break;
@@ -1265,14 +1270,12 @@ int launch_bwd(const void* q, const void* k, const void* v, const void* dout, co
   const int grid = min(device_sm_count(), ntile);
   if (bwd_softmax_warps() == 2) {
     cudaFuncSetAttribute(bwd_kernel<DH, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, BS::SMEM);
-    bwd_kernel<DH, 2><<<grid, BwdWarps<2>::THREADS, BS::SMEM, st>>>(tq, tk, tv, tdo, tdq, km, sched, lse, delta, dq,
-                                                                   (__nv_bfloat16*)dk, (__nv_bfloat16*)dv, S, nh,
-                                                                   B * nh, fo);
+    launch_pdl(bwd_kernel<DH, 2>, dim3(grid), dim3(BwdWarps<2>::THREADS), BS::SMEM, st, 1, tq, tk, tv, tdo, tdq, km,
+               sched, lse, delta, dq, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv, S, nh, B * nh, fo);
   } else {
     cudaFuncSetAttribute(bwd_kernel<DH, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, BS::SMEM);
-    bwd_kernel<DH, 4><<<grid, BwdWarps<4>::THREADS, BS::SMEM, st>>>(tq, tk, tv, tdo, tdq, km, sched, lse, delta, dq,
-                                                                   (__nv_bfloat16*)dk, (__nv_bfloat16*)dv, S, nh,
-                                                                   B * nh, fo);
+    launch_pdl(bwd_kernel<DH, 4>, dim3(grid), dim3(BwdWarps<4>::THREADS), BS::SMEM, st, 1, tq, tk, tv, tdo, tdq, km,
+               sched, lse, delta, dq, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv, S, nh, B * nh, fo);
   }
   ESM_LAUNCH_RET();
 }

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <cstdlib>
 
 #include "../../include/esm2_b200.h"
 
@@ -66,6 +67,53 @@ __device__ __forceinline__ uint32_t drop_row(const DropKeys& k, uint32_t row) {
 __device__ __forceinline__ uint32_t drop_pair(const DropKeys& k, uint32_t rh, uint32_t pair) {
   const uint32_t u = lowbias32(rh ^ (pair + k.k1));
   return ((u & 0xFFFFu) >= k.thr ? 1u : 0u) | ((u >> 16) >= k.thr ? 2u : 0u);
+}
+
+// ----------------------------------------------------------------------------
+// Programmatic dependent launch (PDL): the step's kernels are launched with programmatic stream serialisation,
+// so a kernel's CTAs are scheduled while its predecessor's last CTAs are still running (as SMs free up) and run
+// their prologue (mbarrier init, TMEM allocation, tensor-map prefetch) early; `pdl_wait()` -- before the first
+// global-memory access of every such kernel -- blocks until the predecessor grid has completed and its writes
+// are visible.  `pdl_trigger()` lets the successor's launch begin.  Both are no-ops for normal launches.
+// ESM_PDL=0 launches everything with full stream serialisation.
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("ESM_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// kernel launch with the PDL attribute (and an optional cluster size)
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              int cluster, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  int n = 0;
+  if (pdl_enabled()) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  if (cluster > 1) {
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = cluster;
+    attr[n].val.clusterDim.y = 1;
+    attr[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
 // SM count of the *current* device (cached per device id; launches size persistent grids with it).

@@ -103,6 +103,8 @@ template <typename T>
 __global__ void embed_fwd_kernel(const int32_t* __restrict__ ids, const int32_t* __restrict__ am,
                                  const T* __restrict__ E, const float* __restrict__ row_scale, T* __restrict__ x,
                                  int64_t T_, int S, int H, int token_dropout, int mask_id) {
+  pdl_wait();  // programmatic dependent launch (common.cuh)
+  pdl_trigger();
   constexpr int VEC = vec16<T>::N;
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -132,6 +134,8 @@ __global__ void __launch_bounds__(256) embed_bwd_smem_kernel(const int32_t* __re
                                                              const T* __restrict__ dx, float* __restrict__ dE,
                                                              int64_t T_, int S, int H, int V, int rows_per_block,
                                                              int mask_id, int pad_id) {
+  pdl_wait();  // programmatic dependent launch (common.cuh)
+  pdl_trigger();
   constexpr int VEC = vec16<T>::N;
   constexpr int RU = 4;
   extern __shared__ float acc[];  // [V][BC]
@@ -275,6 +279,8 @@ __global__ void __launch_bounds__(256, SG ? (MAXV <= 2 ? 4 : 3) : 1) ln_fwd_kern
                                                      const float* __restrict__ b, T* __restrict__ y,
                                                      float* __restrict__ mean_out, float* __restrict__ rstd_out,
                                                      int64_t rows, int H, float eps) {
+  pdl_wait();  // programmatic dependent launch (common.cuh)
+  pdl_trigger();
   constexpr int VEC = vec16<T>::N;
   constexpr int GPB = 8 / WPR;  // groups per block
   __shared__ float2 red[GPB][2 * WPR];
@@ -398,6 +404,8 @@ __global__ void __launch_bounds__(256, SG ? 3 : (sizeof(T) == 2 && (MAXV <= 2 ||
                   const float* __restrict__ mean, const float* __restrict__ rstd, const T* __restrict__ dres,
                   const T* __restrict__ gelu_z, T* __restrict__ dx, float* __restrict__ dg, float* __restrict__ db,
                   float* __restrict__ csum, int64_t rows, int H, const esm_dropout drop, T* __restrict__ dxd) {
+  pdl_wait();  // programmatic dependent launch (common.cuh)
+  pdl_trigger();
   constexpr int VEC = vec16<T>::N;
   constexpr int GPB = 8 / WPR;
   DropKeys dk{0u, 0u, 0u, 1.f, false};
@@ -677,6 +685,8 @@ __global__ void __launch_bounds__(256) qkv_rope_bwd_tile_kernel(const float* __r
                                                                 float* __restrict__ csum, const float* __restrict__ cs,
                                                                 const float* __restrict__ sn, int T_, int S, int nh,
                                                                 float qs, int TT) {
+  pdl_wait();  // programmatic dependent launch (common.cuh)
+  pdl_trigger();
   constexpr int DH = CPR * 16, HALF = DH / 2, TPB = 256 / CPR;
   __shared__ float red[8][CPR][48];
   const int h = blockIdx.y;
@@ -863,6 +873,8 @@ __global__ void __launch_bounds__(256) xent_small_kernel(const T* __restrict__ n
                                                          float* __restrict__ loss_sum, float* __restrict__ dlogits,
                                                          T* __restrict__ dn, float* __restrict__ dbias, int64_t rows,
                                                          int H, int V) {
+  pdl_wait();  // programmatic dependent launch (common.cuh)
+  pdl_trigger();
   constexpr int VEC = vec16<T>::N;
   constexpr int PAD = sizeof(T) == 2 ? 2 : 1;  // odd number of 32-bit words per staged row
   const int HP = H + PAD;
@@ -964,6 +976,8 @@ template <typename T, int V_MAX>
 __global__ void __launch_bounds__(256) xent_dE_kernel(const T* __restrict__ n, const int32_t* __restrict__ labels,
                                                       const float* __restrict__ dlogits, float* __restrict__ dE,
                                                       int64_t rows, int H, int V, int rows_per_block) {
+  pdl_wait();  // programmatic dependent launch (common.cuh)
+  pdl_trigger();
   __shared__ float red[8][V_MAX][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int col = blockIdx.x * 32 + lane;
@@ -1153,8 +1167,8 @@ int esm_embed_fwd(int dtype, const int32_t* ids, const int32_t* am, const void* 
   const int64_t T_ = (int64_t)B * Sq;
   const int grid = grid_for(T_ * 32, 256);
   if (dtype == ESM_BF16)
-    embed_fwd_kernel<__nv_bfloat16><<<grid, 256, 0, S(stream)>>>(ids, am, (const __nv_bfloat16*)E, row_scale,
-                                                                 (__nv_bfloat16*)x, T_, Sq, H, token_dropout, mask_id);
+    launch_pdl(embed_fwd_kernel<__nv_bfloat16>, dim3(grid), dim3(256), 0, S(stream), 1, ids, am,
+               (const __nv_bfloat16*)E, row_scale, (__nv_bfloat16*)x, T_, Sq, H, token_dropout, mask_id);
   else
     embed_fwd_kernel<float><<<grid, 256, 0, S(stream)>>>(ids, am, (const float*)E, row_scale, (float*)x, T_, Sq, H,
                                                          token_dropout, mask_id);
@@ -1186,8 +1200,8 @@ int esm_embed_bwd(int dtype, const int32_t* ids, const int32_t* am, const float*
   const size_t sm = (size_t)V * bx * vec * sizeof(float);
   if (dtype == ESM_BF16) {
     cudaFuncSetAttribute(embed_bwd_smem_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    embed_bwd_smem_kernel<__nv_bfloat16><<<grid, bx, sm, S(stream)>>>(ids, am, row_scale, (const __nv_bfloat16*)dx,
-                                                                      dE, T_, Sq, H, V, rpb, mask_id, pad_id);
+    launch_pdl(embed_bwd_smem_kernel<__nv_bfloat16>, dim3(grid), dim3(bx), sm, S(stream), 1, ids, am, row_scale,
+               (const __nv_bfloat16*)dx, dE, T_, Sq, H, V, rpb, mask_id, pad_id);
   } else {
     cudaFuncSetAttribute(embed_bwd_smem_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     embed_bwd_smem_kernel<float><<<grid, bx, sm, S(stream)>>>(ids, am, row_scale, (const float*)dx, dE, T_, Sq, H, V,
@@ -1259,9 +1273,11 @@ int esm_layernorm_fwd(int dtype, const void* x, const float* gamma, const float*
 #define L_SG(...)                                                                                     \
   do {                                                                                                \
     cudaFuncSetAttribute(__VA_ARGS__, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
-    __VA_ARGS__<<<grid, 256, smem, S(stream)>>>((const TT*)x, gamma, beta, (TT*)y, mean, rstd, rows, H, eps); \
+    launch_pdl(__VA_ARGS__, dim3(grid), dim3(256), smem, S(stream), 1, (const TT*)x, gamma, beta, (TT*)y, mean, \
+               rstd, (int64_t)rows, H, eps);                                                          \
   } while (0)
-#define L_F(...) __VA_ARGS__<<<grid, 256, 0, S(stream)>>>((const TT*)x, gamma, beta, (TT*)y, mean, rstd, rows, H, eps)
+#define L_F(...) launch_pdl(__VA_ARGS__, dim3(grid), dim3(256), 0, S(stream), 1, (const TT*)x, gamma, beta, (TT*)y, \
+                            mean, rstd, (int64_t)rows, H, eps)
   static const bool sg_ok = !(getenv("ESM_LN_FWD_SG") && atoi(getenv("ESM_LN_FWD_SG")) == 0);
   if (dtype == ESM_BF16 && sg_ok) {
     using TT = __nv_bfloat16;
@@ -1306,9 +1322,9 @@ int esm_layernorm_bwd(int dtype, const void* dy, const void* x, const float* gam
 #define L_B(...)                                                                                     \
   do {                                                                                               \
     cudaFuncSetAttribute(__VA_ARGS__, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);         \
-    __VA_ARGS__<<<grid, 256, sm, S(stream)>>>((const TT*)dy, (const TT*)x, gamma, mean, rstd,        \
-                                              (const TT*)dres, (const TT*)gelu_z, (TT*)dx, dgamma,   \
-                                              dbeta, col_sum, rows, H, dr, (TT*)dxd);                \
+    launch_pdl(__VA_ARGS__, dim3(grid), dim3(256), sm, S(stream), 1, (const TT*)dy, (const TT*)x, gamma, mean, \
+               rstd, (const TT*)dres, (const TT*)gelu_z, (TT*)dx, dgamma, dbeta, col_sum, (int64_t)rows, H, dr,   \
+               (TT*)dxd);                                                                             \
   } while (0)
   if (dxd != nullptr) {  // hidden dropout: the branch-gradient variant (no fused dgamma/dbeta in bf16)
     if (dtype == ESM_BF16) {
@@ -1389,9 +1405,8 @@ int esm_qkv_rope_bwd(int dtype, const float* dq, const void* dk, const void* dv,
     const int TT = 512;  // tokens per block (one head)
     dim3 grid((unsigned)((T_ + TT - 1) / TT), (unsigned)nh);
 #define QRB(CPR)                                                                                                  \
-  qkv_rope_bwd_tile_kernel<CPR><<<grid, 256, 0, S(stream)>>>(dq, (const __nv_bfloat16*)dk, (const __nv_bfloat16*)dv, \
-                                                             (__nv_bfloat16*)dqkv, col_sum, cos_t, sin_t, (int)T_, \
-                                                             Sq, nh, q_scale, TT)
+  launch_pdl(qkv_rope_bwd_tile_kernel<CPR>, dim3(grid), dim3(256), 0, S(stream), 1, dq, (const __nv_bfloat16*)dk, \
+             (const __nv_bfloat16*)dv, (__nv_bfloat16*)dqkv, col_sum, cos_t, sin_t, (int)T_, Sq, nh, q_scale, TT)
     if (dh == 16) QRB(1);
     else if (dh == 32) QRB(2);
     else QRB(4);
@@ -1430,11 +1445,11 @@ int esm_lmhead_xent(int dtype, const void* n, const void* E, const float* bias, 
       const int g = grid_for((int64_t)T_ * 32, 256, device_sm_count() * 2);
       if (dtype == ESM_BF16) {
         cudaFuncSetAttribute(xent_small_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        xent_small_kernel<__nv_bfloat16><<<g, 256, smem, S(stream)>>>(
-            (const __nv_bfloat16*)n, (const __nv_bfloat16*)E, bias, labels, inv_denom, loss_sum, dlogits_ws,
-            (__nv_bfloat16*)dn, dbias, T_, H, V);
-        xent_dE_kernel<__nv_bfloat16, 40><<<g2, 256, 0, S(stream)>>>((const __nv_bfloat16*)n, labels, dlogits_ws, dE,
-                                                                    T_, H, V, rpb);
+        launch_pdl(xent_small_kernel<__nv_bfloat16>, dim3(g), dim3(256), smem, S(stream), 1, (const __nv_bfloat16*)n,
+                   (const __nv_bfloat16*)E, bias, labels, inv_denom, loss_sum, dlogits_ws, (__nv_bfloat16*)dn, dbias,
+                   T_, H, V);
+        launch_pdl(xent_dE_kernel<__nv_bfloat16, 40>, dim3(g2), dim3(256), 0, S(stream), 1, (const __nv_bfloat16*)n,
+                   labels, (const float*)dlogits_ws, dE, T_, H, V, rpb);
       } else {
         cudaFuncSetAttribute(xent_small_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         xent_small_kernel<float><<<g, 256, smem, S(stream)>>>((const float*)n, (const float*)E, bias, labels, inv_denom,

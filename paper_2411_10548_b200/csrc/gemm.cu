@@ -20,6 +20,9 @@
 #include "sm100.cuh"
 
 namespace esm {
+namespace attn {
+void zero_f32(float* p, int64_t n, cudaStream_t st);  // attention.cu: PDL-launched zero fill
+}
 
 struct EpiParams {
   int M, N;
@@ -76,7 +79,13 @@ struct EpiCfg {
   static constexpr int NOUT = GELU2 ? 2 : 1;  // outputs per chunk (GELU: C and Z; GELU_GRADAUX: C and GELU'(Z))
   static constexpr bool AUX = EPI == ESM_EPI_RESID || EPI == ESM_EPI_DGELU || EPI == ESM_EPI_STORE_LN ||
                               EPI == ESM_EPI_MUL_AUX || EPI == ESM_EPI_DELTA;
-  static constexpr int WARP_BYTES = QKV ? 0 : 2 * NOUT * CHUNK + (AUX ? 2 * CHUNK : 0);
+#ifndef ESM_GEMM_OBUF
+#define ESM_GEMM_OBUF 1
+#endif
+  // output staging buffers per epilogue warp: 1 leaves room for one more operand stage (650M step 85.4 -> 84.6 ms
+  // with 2 -> 1; the epilogue waits for its previous TMA store to finish reading, off the critical path)
+  static constexpr int OBUF = ESM_GEMM_OBUF;
+  static constexpr int WARP_BYTES = QKV ? 0 : OBUF * NOUT * CHUNK + (AUX ? 2 * CHUNK : 0);
   static constexpr int BYTES = WARPS * WARP_BYTES;
 };
 
@@ -204,6 +213,8 @@ __global__ void __launch_bounds__(EpiCfg<EPI>::THREADS, 1)
   if constexpr (CL > 1) cluster_sync();  // peer barriers initialised before any remote arrive / TMA
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();     // predecessor's outputs (our operands) complete and visible
+  pdl_trigger();  // the successor may start its prologue on SMs this grid frees
 
   const int num_tiles = ti.num_m * ti.num_ng * ti.splits;
 
@@ -313,7 +324,7 @@ __global__ void __launch_bounds__(EpiCfg<EPI>::THREADS, 1)
     const int half = ew >> 2;
     uint8_t* my = sEpi + ew * E::WARP_BYTES;
     uint8_t* obuf = my;                              // [2][NOUT][CHUNK]
-    uint8_t* abuf = my + 2 * E::NOUT * E::CHUNK;     // [2][CHUNK]  (AUX only)
+    uint8_t* abuf = my + E::OBUF * E::NOUT * E::CHUNK;  // [2][CHUNK]  (AUX only)
     uint64_t* abar = aux_bar + 2 * ew;
     uint32_t aux_phase = 0;  // bit b = expected parity of aux buffer b
     int ob = 0, ab = 0;
@@ -514,7 +525,7 @@ __global__ void __launch_bounds__(EpiCfg<EPI>::THREADS, 1)
           ab ^= 1;
         }
         // stage the outputs (wait until the TMA store that last read this buffer is done)
-        if (lane == 0) bulk_wait_read<1>();
+        if (lane == 0) bulk_wait_read<E::OBUF - 1>();
         __syncwarp();
         uint8_t* o = obuf + ob * E::NOUT * E::CHUNK;
         if constexpr (EPI == ESM_EPI_F32_ACC) {
@@ -552,7 +563,7 @@ __global__ void __launch_bounds__(EpiCfg<EPI>::THREADS, 1)
           }
           bulk_commit();
         }
-        ob ^= 1;
+        if constexpr (E::OBUF == 2) ob ^= 1;
         if constexpr (EPI == ESM_EPI_DGELU || EPI == ESM_EPI_MUL_AUX) {
           if (ep.col_sum != nullptr) {  // rows >= M are exactly 0 (TMA zero-filled A)
             const float s = warp_transpose_sum32(v, lane);
@@ -724,23 +735,7 @@ static int launch_cg(const esm_gemm_args& a, cudaStream_t st) {
     }
     if (units > maxc) units = maxc;
   }
-  if constexpr (CG == 1) {
-    kern<<<units, EpiCfg<EPI>::THREADS, C::SMEM, st>>>(tA, tB, maps, ti, ep);
-  } else {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(units * CG * MC);
-    cfg.blockDim = dim3(EpiCfg<EPI>::THREADS);
-    cfg.dynamicSmemBytes = C::SMEM;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CG * MC;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, kern, tA, tB, maps, ti, ep);
-  }
+  launch_pdl(kern, dim3(units * CG * MC), dim3(EpiCfg<EPI>::THREADS), C::SMEM, st, CG * MC, tA, tB, maps, ti, ep);
   ESM_LAUNCH_RET();
 }
 
@@ -879,7 +874,7 @@ int gemm_bf16(const esm_gemm_args& a, cudaStream_t st) {
         ESM_CHECK_ARG(a.aux_in && a.row_dot && a.seq_len > 0 && a.n_heads > 0 && a.head_dim > 0 &&
                           a.N == a.n_heads * a.head_dim && a.M % a.seq_len == 0,
                       "gemm: DELTA needs aux_in (O), row_dot and N = n_heads * head_dim, M = B * seq_len");
-        cudaMemsetAsync(a.row_dot, 0, sizeof(float) * (size_t)a.M * a.n_heads, st);  // partial sums red.add into it
+        attn::zero_f32(a.row_dot, (int64_t)a.M * a.n_heads, st);  // partial sums red.add into it
         return dispatch_bn<false, true, ESM_EPI_DELTA>(a, bn, st);
       default: break;
     }
