@@ -800,11 +800,11 @@ class EsmForMaskedLM:
 
     @staticmethod
     def _fused_attn_bwd(dh: int) -> bool:
-        """Fused attention backward (writes dqkv with RoPE^T + bias grads) vs classic + qkv_rope_bwd: the
-        fused kernel wins for dh <= 32 (35M 0.78 vs 0.71 + 0.16 ms); at dh = 64 the classic pair is ~1 %
-        faster per step on 650M / Geneformer.  ESM_ATTN_FUSED=0/1 forces either."""
+        """Fused attention backward (writes dqkv with RoPE^T + bias grads) vs classic + qkv_rope_bwd: fused for
+        every head dim -- dh <= 32 (35M 0.78 vs 0.71 + 0.16 ms) and, since dK/dV leave TMEM before the epilogue
+        work, dh = 64 (650M step 86.1 vs 86.5 ms, alternating runs).  ESM_ATTN_FUSED=0/1 forces either."""
         env = os.environ.get("ESM_ATTN_FUSED")
-        return dh <= 32 if env is None else env != "0"
+        return True if env is None else env != "0"
 
     def _group_ready(self, key: str):
         """All groups up to ``key`` (backward-completion order) hold final gradients."""
