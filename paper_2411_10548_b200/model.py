@@ -335,6 +335,7 @@ class EsmForMaskedLM:
         self.comm = None  # set by ddp.GradAllReducer
         self.timer = None  # optional KernelTimer (bench.py per-kernel roofline)
         self._opt_on, self._opt_start, self._opt_stream = False, 0, None
+        self._zero_stream = None
         self.launches = 0  # kernels launched by this model (C-ABI calls x kernels per call)
         self.nvtx = False  # NVTX ranges (forward / backward / layers) for nsys-style timelines
         self.graph = None
@@ -594,7 +595,14 @@ class EsmForMaskedLM:
         E_key = "esm.embeddings.word_embeddings.weight"
         E = self._w(E_key, (V, H))
 
-        self.store.g32.zero_()
+        # the gradient buffer is first written by the LM-head CE at the end of the forward: zero it on a side
+        # stream behind the forward (3B: 11 GB, ~1.8 ms) and join right before the CE
+        cur = torch.cuda.current_stream(self.device)
+        if self._zero_stream is None:
+            self._zero_stream = torch.cuda.Stream(self.device)
+        self._zero_stream.wait_stream(cur)  # the previous step's optimizer has consumed the gradients
+        with torch.cuda.stream(self._zero_stream):
+            self.store.g32.zero_()
         ws.loss_sum.zero_()
         n_lab = ws.n_labels
         if self.comm is not None:  # global masked-token count -> loss normaliser; the local count is kept
@@ -643,6 +651,7 @@ class EsmForMaskedLM:
         call("esm_layernorm_fwd", kdt, ws.g.data_ptr(), self._p32("lm_head.layer_norm.weight").data_ptr(),
              self._p32("lm_head.layer_norm.bias").data_ptr(), ws.n.data_ptr(), ws.lnh_m.data_ptr(),
              ws.lnh_r.data_ptr(), T, H, eps, st)
+        cur.wait_stream(self._zero_stream)  # gradient buffer zeroed
         if ws.large_vocab:
             self._large_vocab_head(ws, E, E_key, T, H, V)
         else:  # decoder (tied E) + masked CE + dlogits (fused, V <= 40)
