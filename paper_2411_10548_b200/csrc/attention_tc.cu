@@ -31,6 +31,9 @@ constexpr int kThreads = 192;
 #ifndef ESM_ATTN_EXP
 #define ESM_ATTN_EXP 0
 #endif
+#ifndef ESM_ATTN_FENCE_EVERY_BLOCK
+#define ESM_ATTN_FENCE_EVERY_BLOCK 0
+#endif
 constexpr float L2E = 1.4426950408889634f;
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
 
@@ -208,8 +211,13 @@ __device__ __forceinline__ bool tile_skipped(const int* sched, int tile, int nkb
 // Q and the O accumulator are double-buffered across items (q_empty / o_free handshakes), the K/V ring and
 // the S / P barriers follow a global tile counter, so the next item's loads and first MMAs overlap this
 // item's softmax tail and epilogue.
+template <int DH, int BN, int NSB>
+constexpr int fwd_ctas_per_sm() {  // resident CTAs per SM (TMEM: NSB * BN + 2 * DP columns, power of two)
+  return Shape<DH, BN, NSB>::TMEM_COLS <= 128 ? 4 : (NSB == 1 ? 3 : 2);
+}
+
 template <int DH, int BN, int NSB, int FP>
-__global__ void __launch_bounds__(kThreads, NSB == 1 ? 3 : 2)
+__global__ void __launch_bounds__(kThreads, fwd_ctas_per_sm<DH, BN, NSB>())
     fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                const __grid_constant__ CUtensorMap tmV, const int32_t* __restrict__ key_mask,
                int* __restrict__ sched, __nv_bfloat16* __restrict__ O, float* __restrict__ LSE, int S, int nh,
@@ -385,10 +393,10 @@ __global__ void __launch_bounds__(kThreads, NSB == 1 ? 3 : 2)
         mbar_wait(&s_full[gj % NSB], (gj / NSB) & 1);
         tc_fence_after();
         const uint32_t sbase = tbase + lane_off + (gj % NSB) * BN;
-        static_assert(BN == 64, "the softmax holds one 64-key tile as two 32-column TMEM loads");
-        uint32_t ua[32], ub[32];  // S row, used in place (no register copies)
+        static_assert(BN == 64 || BN == 32, "the softmax holds one 32- or 64-key tile as 32-column TMEM loads");
+        uint32_t ua[32], ub[BN == 64 ? 32 : 1];  // S row, used in place (no register copies)
         tmem_ld32(sbase, ua);
-        tmem_ld32(sbase + 32, ub);
+        if constexpr (BN == 64) tmem_ld32(sbase + 32, ub);
         tmem_ld_wait();
         auto sv = [&](int c) -> float { return __uint_as_float(c < 32 ? ua[c] : ub[c - 32]); };
         auto kill = [&](int c) {
@@ -445,11 +453,11 @@ __global__ void __launch_bounds__(kThreads, NSB == 1 ? 3 : 2)
         // pairs go to the FMA pipe (exp2_poly2) to relieve MUFU (masked tiles stay on MUFU: exact zeros)
         const uint64_t l2e = f2_splat(L2E), nm = f2_splat(-moff);
         uint64_t ls0 = f2_splat(0.f), ls1 = ls0;
-        uint32_t pk[32];
+        uint32_t pk[BN / 2];
         auto exps = [&](auto fp_tag) {
           constexpr int F = decltype(fp_tag)::value;
 #pragma unroll
-          for (int e = 0; e < 32; e += 4) {  // 8 keys: 4 pairs
+          for (int e = 0; e < BN / 2; e += 4) {  // 8 keys: 4 pairs
             float x[8], pr[8];
 #pragma unroll
             for (int q = 0; q < 4; ++q)
@@ -473,7 +481,8 @@ __global__ void __launch_bounds__(kThreads, NSB == 1 ? 3 : 2)
         };
         if (FP > 0 && full) exps(std::integral_constant<int, FP>{});
         else exps(std::integral_constant<int, 0>{});
-        tmem_st32(sbase, pk);  // P (bf16x2) over the first 32 columns of this S buffer
+        if constexpr (BN == 64) tmem_st32(sbase, pk);  // P (bf16x2) over the first BN/2 columns of this S buffer
+        else tmem_st16(sbase, pk);
         float l0, l1, l2, l3;
         f2_unpack(ls0, l0, l1);
         f2_unpack(ls1, l2, l3);
@@ -1116,7 +1125,9 @@ __global__ void __launch_bounds__(BwdWarps<SW>::THREADS, 1)
               make_uint4(dd[4 * gg], dd[4 * gg + 1], dd[4 * gg + 2], dd[4 * gg + 3]);
         }
         tmem_st_wait();
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        // dS^T in shared memory is read (async proxy) only by the pair's dQ MMA, issued after the pair's second
+        // block: one proxy fence per pair covers both blocks' stores of this thread
+        if (ch == 1 || ESM_ATTN_FENCE_EVERY_BLOCK) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&ds_full[g % NBUF]);
@@ -1185,6 +1196,16 @@ static int fwd_poly_pairs() {
   return fp;
 }
 
+// dh <= 32: 32-key tiles at 4 CTAs (16 softmax warps) per SM (ESM_ATTN_FWD_BN=32) instead of 64-key tiles at
+// 2 CTAs/SM.  Measured slower (35M layer 0.249 vs 0.238 ms; 80 registers spill), so off by default.
+static bool fwd_small_tiles() {
+  static const bool on = [] {
+    const char* e = getenv("ESM_ATTN_FWD_BN");
+    return e && atoi(e) == 32;
+  }();
+  return on;
+}
+
 template <int DH, int BN, int NSB>
 int launch_fwd(const void* q, const void* k, const void* v, const int32_t* km, int* sched, void* o, float* lse, int B,
                int nh, int S, cudaStream_t st) {
@@ -1197,7 +1218,7 @@ int launch_fwd(const void* q, const void* k, const void* v, const int32_t* km, i
     return rc;
   const int smem = 2 * SH::Q_BYTES + 2 * SH::STAGES * SH::KV_BYTES + 1024 + 256;
   const int nitem = ((S + BM - 1) / BM) * B * nh;
-  const int per_sm = NSB == 1 ? 3 : 2;  // CTAs resident per SM
+  const int per_sm = fwd_ctas_per_sm<DH, BN, NSB>();  // CTAs resident per SM
   const int grid = min(nitem, per_sm * device_sm_count());
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1307,9 +1328,15 @@ int attn_fwd_tc(const void* q, const void* k, const void* v, const int32_t* km, 
                 "attention: q/k/v must be 16B aligned");
   // two S buffers per CTA, 2 CTAs/SM (a single-buffer 3-CTA/SM variant measured equal at dh 24, slower at 64)
   switch (dh) {
-    case 16: return fa::launch_fwd<16, 64, 2>(q, k, v, km, sched, o, lse, B, nh, S, st);
-    case 24: return fa::launch_fwd<24, 64, 2>(q, k, v, km, sched, o, lse, B, nh, S, st);
-    case 32: return fa::launch_fwd<32, 64, 2>(q, k, v, km, sched, o, lse, B, nh, S, st);
+    case 16:
+      return fa::fwd_small_tiles() ? fa::launch_fwd<16, 32, 2>(q, k, v, km, sched, o, lse, B, nh, S, st)
+                                   : fa::launch_fwd<16, 64, 2>(q, k, v, km, sched, o, lse, B, nh, S, st);
+    case 24:
+      return fa::fwd_small_tiles() ? fa::launch_fwd<24, 32, 2>(q, k, v, km, sched, o, lse, B, nh, S, st)
+                                   : fa::launch_fwd<24, 64, 2>(q, k, v, km, sched, o, lse, B, nh, S, st);
+    case 32:
+      return fa::fwd_small_tiles() ? fa::launch_fwd<32, 32, 2>(q, k, v, km, sched, o, lse, B, nh, S, st)
+                                   : fa::launch_fwd<32, 64, 2>(q, k, v, km, sched, o, lse, B, nh, S, st);
     case 64: return fa::launch_fwd<64, 64, 2>(q, k, v, km, sched, o, lse, B, nh, S, st);
     default: set_last_error("attention: head dim %d unsupported", dh); return ESM_ENOTSUP;
   }
