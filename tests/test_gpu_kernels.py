@@ -447,9 +447,11 @@ def test_gemm_qkv_rope_epilogue(B, S, nh, dh):
 
 
 @pytest.mark.parametrize("B,S,nh,dh,lens", [(2, 256, 3, 24, [256, 130]), (2, 192, 2, 64, [192, 64]),
-                                            (1, 128, 4, 16, [128]), (2, 100, 2, 32, [100, 37])])
+                                            (1, 128, 4, 16, [128]), (2, 100, 2, 32, [100, 37]),
+                                            (3, 1024, 4, 64, [1024, 0, 300]), (4, 512, 20, 24, [512, 511, 129, 1])])
 def test_attention_bwd_qkv_fused(B, S, nh, dh, lens):
-    """esm_attn_bwd_qkv (dqkv with RoPE^T + bias grads) == esm_attn_bwd + esm_qkv_rope_bwd."""
+    """esm_attn_bwd_qkv (dqkv with RoPE^T + bias grads) == esm_attn_bwd + esm_qkv_rope_bwd; includes a batch row
+    without any valid key and rows whose valid length ends inside a key block."""
     from paper_2411_10548_b200.model import rope_tables
     torch.manual_seed(6)
     H = nh * dh
