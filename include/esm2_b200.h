@@ -24,6 +24,9 @@
  *    attention, vectorised warp-shuffle epilogues).  Parameters are fp32 masters with
  *    a bf16 shadow for GEMM operands; gradients are always fp32.
  *  - activations are token-major: row t = b*S + s of a [T, width] matrix.
+ *  - the step's bf16 kernels are launched with programmatic dependent launch: a kernel may be scheduled while
+ *    its stream predecessor drains, but waits (griddepcontrol.wait) for the predecessor's completion before
+ *    touching memory, so stream-order semantics are unchanged (environment ESM_PDL=0 disables it).
  */
 #ifndef ESM2_B200_H
 #define ESM2_B200_H

@@ -34,6 +34,9 @@ constexpr int kThreads = 192;
 #ifndef ESM_ATTN_FENCE_EVERY_BLOCK
 #define ESM_ATTN_FENCE_EVERY_BLOCK 0
 #endif
+#ifndef ESM_ATTN_QST64
+#define ESM_ATTN_QST64 4  // backward Q / dO stages at dh 64 (3: the previous layout with two dQ staging boxes)
+#endif
 constexpr float L2E = 1.4426950408889634f;
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
 
@@ -397,6 +400,7 @@ __global__ void __launch_bounds__(kThreads, fwd_ctas_per_sm<DH, BN, NSB>())
         uint32_t ua[32], ub[BN == 64 ? 32 : 1];  // S row, used in place (no register copies)
         tmem_ld32(sbase, ua);
         if constexpr (BN == 64) tmem_ld32(sbase + 32, ub);
+        else ub[0] = 0u;  // never read (BN = 32)
         tmem_ld_wait();
         auto sv = [&](int c) -> float { return __uint_as_float(c < 32 ? ua[c] : ub[c - 32]); };
         auto kill = [&](int c) {
@@ -594,7 +598,10 @@ struct BwdShape {
   static constexpr uint32_t LAYOUT = Shape<DH, 64>::LAYOUT;
   static constexpr int QB = 64 * ROWB, KB = 128 * ROWB;
   static constexpr int NBUF = DP <= 32 ? 3 : 2;  // {S^T, dP^T} TMEM buffers (128 columns each)
-  static constexpr int QST = DH == 64 ? 3 : 6;   // Q / dO / LSE / Delta stages (>= NBUF + 1)
+  // Q / dO / LSE / Delta stages (>= NBUF + 1): a stage freed by block i's dV / dK MMAs is refilled for block
+  // i + QST, which the MMA warp needs right after block i + QST - NBUF's dV / dK: QST - NBUF block periods of
+  // TMA latency budget
+  static constexpr int QST = DH == 64 ? ESM_ATTN_QST64 : 6;
   // FOLD: the TMA warp folds block j's Delta into dO after loading block j + LAG; that load waits for block
   // j + LAG - QST's dV / dK MMAs, which the MMA warp issues before it needs block j (at j - NBUF):
   // LAG <= QST - NBUF keeps the cycle open
@@ -610,7 +617,9 @@ struct BwdShape {
   static constexpr int BOXC = DP < 32 ? DP : 32;
   static constexpr int NBOX = DP / BOXC;
   static constexpr int BOX_BYTES = 32 * BOXC * 4;
-  static constexpr int DQ_STAGE = 4 * NBOX * BOX_BYTES;
+  // dQ staging boxes per drain warp: all NBOX, or one reused box (dh 64 with 4 Q/dO stages: shared memory)
+  static constexpr int SBOX = (DH == 64 && QST > 3) ? 1 : NBOX;
+  static constexpr int DQ_STAGE = 4 * SBOX * BOX_BYTES;
   static constexpr int SMEM = 2 * DS_BUF + 4 * KB + 2 * QST * QB + 2 * QST * 64 * 4 + DQ_STAGE + 1024 + 512;
 };
 
@@ -896,7 +905,7 @@ __global__ void __launch_bounds__(BwdWarps<SW>::THREADS, 1)
     const uint32_t lane_off = (uint32_t)(qq * 32) << 16;
     constexpr int BOXC = BS::BOXC, RB = BOXC * 4;           // fp32 columns / bytes per staged row
     constexpr uint32_t SWM = RB == 128 ? 7u : 3u;            // 128B / 64B swizzle: chunk ^= (addr >> 7) & SWM
-    uint8_t* stage = sDQ + qq * (BS::NBOX * BS::BOX_BYTES);
+    uint8_t* stage = sDQ + qq * (BS::SBOX * BS::BOX_BYTES);
     for (int it = 0;; ++it) {
       const int slot = it & 3;
       mbar_wait(&tile_full[slot], (it >> 2) & 1);
@@ -910,8 +919,6 @@ __global__ void __launch_bounds__(BwdWarps<SW>::THREADS, 1)
         mbar_wait(&dq_full[gp & 1], (gp >> 1) & 1);
         tc_fence_after();
         const uint32_t tq = tdQ0 + (gp & 1) * DP + lane_off;
-        if (lane == 0) bulk_wait_read0();  // the previous pair's reduce has finished reading the staging boxes
-        __syncwarp();
 #pragma unroll
         for (int x = 0; x < BS::NBOX; ++x) {
           uint32_t u[BOXC];
@@ -924,24 +931,27 @@ __global__ void __launch_bounds__(BwdWarps<SW>::THREADS, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&dq_empty[gp & 1]);
           }
+          const int sb = BS::SBOX == 1 ? 0 : x;
+          if (BS::SBOX == 1 || x == 0) {  // the previous reduce has finished reading the staging box(es)
+            if (lane == 0) bulk_wait_read0();
+            __syncwarp();
+          }
 #pragma unroll
           for (int j = 0; j < BOXC / 4; ++j) {
             const uint32_t off = (uint32_t)(lane * RB + j * 16);
-            *reinterpret_cast<float4*>(stage + x * BS::BOX_BYTES + (off ^ (((off >> 7) & SWM) << 4))) =
+            *reinterpret_cast<float4*>(stage + sb * BS::BOX_BYTES + (off ^ (((off >> 7) & SWM) << 4))) =
                 make_float4(__uint_as_float(u[4 * j]), __uint_as_float(u[4 * j + 1]), __uint_as_float(u[4 * j + 2]),
                             __uint_as_float(u[4 * j + 3]));
           }
-        }
-        // rows past this sequence carry exact zeros (dS = 0 there), so spilling into the next rows is harmless
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) {
-          const int row = (fo.dqkv ? b * S : bh * S) + p * 128 + qq * 32;
-          const int col = fo.dqkv ? h * DH : 0;
-#pragma unroll
-          for (int x = 0; x < BS::NBOX; ++x)
-            if (ESM_ATTN_EXP != 5) tma_reduce_2d(&tmdQ, stage + x * BS::BOX_BYTES, col + x * BOXC, row);
-          bulk_commit_group();
+          // rows past this sequence carry exact zeros (dS = 0 there), so spilling into the next rows is harmless
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            const int row = (fo.dqkv ? b * S : bh * S) + p * 128 + qq * 32;
+            const int col = fo.dqkv ? h * DH : 0;
+            if (ESM_ATTN_EXP != 5) tma_reduce_2d(&tmdQ, stage + sb * BS::BOX_BYTES, col + x * BOXC, row);
+            bulk_commit_group();
+          }
         }
       }
       // ---- final key rows of this tile: dK, dV (thread = key row kr of lane quarter qq).  Both accumulators

@@ -70,7 +70,10 @@ template <int EPI>
 struct EpiCfg {
   static constexpr bool QKV = EPI >= 16;  // ESM_EPI_QKV_ROPE specialised per head dim: EPI = 16 + dh
   static constexpr bool F32 = EPI == ESM_EPI_F32_ACC;
-  static constexpr int EW = 2;  // epilogue warps per TMEM lane quarter (3 measured slower: smem for staging
+#ifndef ESM_GEMM_EW
+#define ESM_GEMM_EW 2
+#endif
+  static constexpr int EW = ESM_GEMM_EW;  // epilogue warps per TMEM lane quarter (3 measured slower: smem for staging
                                 // costs mainloop stages)
   static constexpr int WARPS = 4 * EW;
   static constexpr int THREADS = 64 + 32 * WARPS;
