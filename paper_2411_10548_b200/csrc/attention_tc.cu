@@ -49,7 +49,7 @@ struct Shape {
   static constexpr uint32_t LAYOUT = ROWB == 128 ? 2u : (ROWB == 64 ? 4u : 6u);  // SW128 / SW64 / SW32
   static constexpr int Q_BYTES = BM * ROWB;
   static constexpr int KV_BYTES = BN * ROWB;
-  static constexpr int STAGES = 3;
+  static constexpr int STAGES = BN >= 128 ? 2 : 3;  // K/V ring (shared memory: 2 CTAs per SM)
   // TMEM: S0 [0,BN) (S1 [BN,2BN)) O0 / O1 [NSB*BN, NSB*BN + 2*DP) (O double-buffered across items)
   static constexpr uint32_t TMEM_COLS = (NSB * BN + 2 * DP) <= 128 ? 128 : (NSB * BN + 2 * DP) <= 256 ? 256 : 512;
 };
@@ -215,8 +215,8 @@ __device__ __forceinline__ bool tile_skipped(const int* sched, int tile, int nkb
 // the S / P barriers follow a global tile counter, so the next item's loads and first MMAs overlap this
 // item's softmax tail and epilogue.
 template <int DH, int BN, int NSB>
-constexpr int fwd_ctas_per_sm() {  // resident CTAs per SM (TMEM: NSB * BN + 2 * DP columns, power of two)
-  return Shape<DH, BN, NSB>::TMEM_COLS <= 128 ? 4 : (NSB == 1 ? 3 : 2);
+constexpr int fwd_ctas_per_sm() {  // resident CTAs per SM: TMEM allocations (NSB * BN + 2 * DP columns, power of two)
+  return 512 / Shape<DH, BN, NSB>::TMEM_COLS > 4 ? 4 : 512 / Shape<DH, BN, NSB>::TMEM_COLS;
 }
 
 template <int DH, int BN, int NSB, int FP>
@@ -396,101 +396,168 @@ __global__ void __launch_bounds__(kThreads, fwd_ctas_per_sm<DH, BN, NSB>())
         mbar_wait(&s_full[gj % NSB], (gj / NSB) & 1);
         tc_fence_after();
         const uint32_t sbase = tbase + lane_off + (gj % NSB) * BN;
-        static_assert(BN == 64 || BN == 32, "the softmax holds one 32- or 64-key tile as 32-column TMEM loads");
-        uint32_t ua[32], ub[BN == 64 ? 32 : 1];  // S row, used in place (no register copies)
-        tmem_ld32(sbase, ua);
-        if constexpr (BN == 64) tmem_ld32(sbase + 32, ub);
-        else ub[0] = 0u;  // never read (BN = 32)
-        tmem_ld_wait();
-        auto sv = [&](int c) -> float { return __uint_as_float(c < 32 ? ua[c] : ub[c - 32]); };
-        auto kill = [&](int c) {
-          if (c < 32) ua[c] = __float_as_uint(-INFINITY);
-          else ub[c - 32] = __float_as_uint(-INFINITY);
-        };
-        const int kbase = j * BN;
-        bool full = !nonprefix;
-        if (!nonprefix) {
-          const int valid = kv_len - kbase;  // keys [0, valid) of this tile are real
-          if (valid < BN) {
-            full = false;
+        float ls = 0.f;
+        auto rescale = [&](float mx) {
+          const float mnew = mx * L2E;
+          const bool grow = mnew > m_used + RESCALE_THRESHOLD;
+          if (__any_sync(0xffffffffu, grow)) {  // warp-uniform: tcgen05.ld/st are warp-collective
+            // raise the reference max; rescale running sum and (if any PV issued) O in TMEM
+            const float f = grow ? ex2(m_used - mnew) : 1.0f;  // 0 on the first tile
+            l *= f;
+            if (j > 0) {
+              mbar_wait(o_done, (gj - 1) & 1);
+              tc_fence_after();
 #pragma unroll
-            for (int c = 0; c < BN; ++c)
-              if (c >= valid) kill(c);
-          }
-        } else {
+              for (int c = 0; c < DP; c += 16) {
+                uint32_t u[16];
+                tmem_ld16(t_o + lane_off + c, u);
+                tmem_ld_wait();
 #pragma unroll
-          for (int c = 0; c < BN; ++c) {
-            const int kk = kbase + c;
-            if (!(kk < S && key_mask[(int64_t)b * S + kk] != 0)) kill(c);
-          }
-        }
-        // row max as a 4-way tree (FMNMX3 chains of 8 instead of one of 32)
-        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-        for (int c = 0; c < BN; c += 8)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) m4[q] = fmaxf(m4[q], fmaxf(sv(c + 2 * q), sv(c + 2 * q + 1)));
-        const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
-        const float mnew = mx * L2E;
-        const bool grow = mnew > m_used + RESCALE_THRESHOLD;
-        if (__any_sync(0xffffffffu, grow)) {  // warp-uniform: tcgen05.ld/st are warp-collective
-          // raise the reference max; rescale running sum and (if any PV issued) O in TMEM
-          const float f = grow ? ex2(m_used - mnew) : 1.0f;  // 0 on the first tile
-          l *= f;
-          if (j > 0) {
-            mbar_wait(o_done, (gj - 1) & 1);
-            tc_fence_after();
-#pragma unroll
-            for (int c = 0; c < DP; c += 16) {
-              uint32_t u[16];
-              tmem_ld16(t_o + lane_off + c, u);
-              tmem_ld_wait();
-#pragma unroll
-              for (int e = 0; e < 16; ++e) u[e] = __float_as_uint(__uint_as_float(u[e]) * f);
-              tmem_st16(t_o + lane_off + c, u);
-            }
-          }
-          if (grow) m_used = mnew;
-        }
-        const float moff = m_used == -INFINITY ? 0.f : m_used;
-        // exponentials: x = s log2e - m in FFMA2, row sums in two FADD2 chains; on full tiles FP of every four
-        // pairs go to the FMA pipe (exp2_poly2) to relieve MUFU (masked tiles stay on MUFU: exact zeros)
-        const uint64_t l2e = f2_splat(L2E), nm = f2_splat(-moff);
-        uint64_t ls0 = f2_splat(0.f), ls1 = ls0;
-        uint32_t pk[BN / 2];
-        auto exps = [&](auto fp_tag) {
-          constexpr int F = decltype(fp_tag)::value;
-#pragma unroll
-          for (int e = 0; e < BN / 2; e += 4) {  // 8 keys: 4 pairs
-            float x[8], pr[8];
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              f2_unpack(f2_fma(f2_pack(sv(2 * e + 2 * q), sv(2 * e + 2 * q + 1)), l2e, nm), x[2 * q], x[2 * q + 1]);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              if (q >= 4 - F) {
-                exp2_poly2(x[2 * q], x[2 * q + 1], pr[2 * q], pr[2 * q + 1]);
-              } else {
-                pr[2 * q] = ex2(x[2 * q]);
-                pr[2 * q + 1] = ex2(x[2 * q + 1]);
+                for (int e = 0; e < 16; ++e) u[e] = __float_as_uint(__uint_as_float(u[e]) * f);
+                tmem_st16(t_o + lane_off + c, u);
               }
             }
-            ls0 = f2_add(ls0, f2_pack(pr[0], pr[1]));
-            ls1 = f2_add(ls1, f2_pack(pr[2], pr[3]));
-            ls0 = f2_add(ls0, f2_pack(pr[4], pr[5]));
-            ls1 = f2_add(ls1, f2_pack(pr[6], pr[7]));
-#pragma unroll
-            for (int q = 0; q < 4; ++q) pk[e + q] = pack2(pr[2 * q], pr[2 * q + 1]);
+            if (grow) m_used = mnew;
           }
         };
-        if (FP > 0 && full) exps(std::integral_constant<int, FP>{});
-        else exps(std::integral_constant<int, 0>{});
-        if constexpr (BN == 64) tmem_st32(sbase, pk);  // P (bf16x2) over the first BN/2 columns of this S buffer
-        else tmem_st16(sbase, pk);
-        float l0, l1, l2, l3;
-        f2_unpack(ls0, l0, l1);
-        f2_unpack(ls1, l2, l3);
-        const float ls = (l0 + l1) + (l2 + l3);
+        if constexpr (BN <= 64) {
+          static_assert(BN == 64 || BN == 32, "the softmax holds one 32- or 64-key tile as 32-column TMEM loads");
+          uint32_t ua[32], ub[BN == 64 ? 32 : 1];  // S row, used in place (no register copies)
+          tmem_ld32(sbase, ua);
+          if constexpr (BN == 64) tmem_ld32(sbase + 32, ub);
+          else ub[0] = 0u;  // never read (BN = 32)
+          tmem_ld_wait();
+          auto sv = [&](int c) -> float { return __uint_as_float(c < 32 ? ua[c] : ub[c - 32]); };
+          auto kill = [&](int c) {
+            if (c < 32) ua[c] = __float_as_uint(-INFINITY);
+            else ub[c - 32] = __float_as_uint(-INFINITY);
+          };
+          const int kbase = j * BN;
+          bool full = !nonprefix;
+          if (!nonprefix) {
+            const int valid = kv_len - kbase;  // keys [0, valid) of this tile are real
+            if (valid < BN) {
+              full = false;
+#pragma unroll
+              for (int c = 0; c < BN; ++c)
+                if (c >= valid) kill(c);
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < BN; ++c) {
+              const int kk = kbase + c;
+              if (!(kk < S && key_mask[(int64_t)b * S + kk] != 0)) kill(c);
+            }
+          }
+          // row max as a 4-way tree (FMNMX3 chains of 8 instead of one of 32)
+          float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+          for (int c = 0; c < BN; c += 8)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) m4[q] = fmaxf(m4[q], fmaxf(sv(c + 2 * q), sv(c + 2 * q + 1)));
+          const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+          rescale(mx);
+          const float moff = m_used == -INFINITY ? 0.f : m_used;
+          // exponentials: x = s log2e - m in FFMA2, row sums in two FADD2 chains; on full tiles FP of every four
+          // pairs go to the FMA pipe (exp2_poly2) to relieve MUFU (masked tiles stay on MUFU: exact zeros)
+          const uint64_t l2e = f2_splat(L2E), nm = f2_splat(-moff);
+          uint64_t ls0 = f2_splat(0.f), ls1 = ls0;
+          uint32_t pk[BN / 2];
+          auto exps = [&](auto fp_tag) {
+            constexpr int F = decltype(fp_tag)::value;
+#pragma unroll
+            for (int e = 0; e < BN / 2; e += 4) {  // 8 keys: 4 pairs
+              float x[8], pr[8];
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                f2_unpack(f2_fma(f2_pack(sv(2 * e + 2 * q), sv(2 * e + 2 * q + 1)), l2e, nm), x[2 * q], x[2 * q + 1]);
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                if (q >= 4 - F) {
+                  exp2_poly2(x[2 * q], x[2 * q + 1], pr[2 * q], pr[2 * q + 1]);
+                } else {
+                  pr[2 * q] = ex2(x[2 * q]);
+                  pr[2 * q + 1] = ex2(x[2 * q + 1]);
+                }
+              }
+              ls0 = f2_add(ls0, f2_pack(pr[0], pr[1]));
+              ls1 = f2_add(ls1, f2_pack(pr[2], pr[3]));
+              ls0 = f2_add(ls0, f2_pack(pr[4], pr[5]));
+              ls1 = f2_add(ls1, f2_pack(pr[6], pr[7]));
+#pragma unroll
+              for (int q = 0; q < 4; ++q) pk[e + q] = pack2(pr[2 * q], pr[2 * q + 1]);
+            }
+          };
+          if (FP > 0 && full) exps(std::integral_constant<int, FP>{});
+          else exps(std::integral_constant<int, 0>{});
+          if constexpr (BN == 64) tmem_st32(sbase, pk);  // P (bf16x2) over the first BN/2 columns of this S buffer
+          else tmem_st16(sbase, pk);
+          float l0, l1, l2, l3;
+          f2_unpack(ls0, l0, l1);
+          f2_unpack(ls1, l2, l3);
+          ls = (l0 + l1) + (l2 + l3);
+        } else {
+          // 128-key tiles (NSB = 1): two passes over the S row in TMEM, 32 columns at a time (the row does not fit
+          // in registers): the max, then exp2 / row sum / P packing, P (bf16x2) written over the columns already
+          // read (chunk c -> columns [16c, 16c + 16))
+          static_assert(BN == 128, "tile width");
+          const int kbase = j * BN;
+          const int valid = nonprefix ? BN : kv_len - kbase;
+          bool full = !nonprefix && valid >= BN;
+          auto chunk = [&](int c, uint32_t (&u)[32]) {
+            tmem_ld32(sbase + 32 * c, u);
+            tmem_ld_wait();
+            if (!full) {
+#pragma unroll
+              for (int e = 0; e < 32; ++e) {
+                const int kk = kbase + 32 * c + e;
+                const bool ok = nonprefix ? (kk < S && key_mask[(int64_t)b * S + kk] != 0) : (32 * c + e < valid);
+                if (!ok) u[e] = __float_as_uint(-INFINITY);
+              }
+            }
+          };
+          float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint32_t u[32];
+            chunk(c, u);
+#pragma unroll
+            for (int e = 0; e < 32; e += 8)
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                m4[q] = fmaxf(m4[q], fmaxf(__uint_as_float(u[e + 2 * q]), __uint_as_float(u[e + 2 * q + 1])));
+          }
+          rescale(fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])));
+          const float moff = m_used == -INFINITY ? 0.f : m_used;
+          const uint64_t l2e = f2_splat(L2E), nm = f2_splat(-moff);
+          uint64_t ls0 = f2_splat(0.f), ls1 = ls0;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint32_t u[32], pk[16];
+            chunk(c, u);
+#pragma unroll
+            for (int e = 0; e < 32; e += 8) {
+              float x[8], pr[8];
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                f2_unpack(f2_fma(f2_pack(__uint_as_float(u[e + 2 * q]), __uint_as_float(u[e + 2 * q + 1])), l2e, nm),
+                          x[2 * q], x[2 * q + 1]);
+#pragma unroll
+              for (int q = 0; q < 8; ++q) pr[q] = ex2(x[q]);
+              ls0 = f2_add(ls0, f2_pack(pr[0], pr[1]));
+              ls1 = f2_add(ls1, f2_pack(pr[2], pr[3]));
+              ls0 = f2_add(ls0, f2_pack(pr[4], pr[5]));
+              ls1 = f2_add(ls1, f2_pack(pr[6], pr[7]));
+#pragma unroll
+              for (int q = 0; q < 4; ++q) pk[e / 2 + q] = pack2(pr[2 * q], pr[2 * q + 1]);
+            }
+            tmem_st16(sbase + 16 * c, pk);
+          }
+          float l0, l1, l2, l3;
+          f2_unpack(ls0, l0, l1);
+          f2_unpack(ls1, l2, l3);
+          ls = (l0 + l1) + (l2 + l3);
+        }
         l += ls;
         tmem_st_wait();
         tc_fence_before();
@@ -1206,15 +1273,18 @@ static int fwd_poly_pairs() {
   return fp;
 }
 
-// dh <= 32: 32-key tiles at 4 CTAs (16 softmax warps) per SM (ESM_ATTN_FWD_BN=32) instead of 64-key tiles at
-// 2 CTAs/SM.  Measured slower (35M layer 0.249 vs 0.238 ms; 80 registers spill), so off by default.
-static bool fwd_small_tiles() {
-  static const bool on = [] {
+// Key-tile width of the forward (ESM_ATTN_FWD_BN): 64 (two S buffers, 2 CTAs/SM, default); 32 for dh <= 32 (4
+// CTAs / 16 softmax warps per SM; measured slower: 35M layer 0.249 vs 0.238 ms, 80 registers spill); 128 (one
+// S buffer -- the next tile's S waits for this tile's P.V -- two-pass softmax over TMEM, 2 CTAs/SM).
+static int fwd_bn() {
+  static const int v = [] {
     const char* e = getenv("ESM_ATTN_FWD_BN");
-    return e && atoi(e) == 32;
+    const int x = e ? atoi(e) : 64;
+    return (x == 32 || x == 128) ? x : 64;
   }();
-  return on;
+  return v;
 }
+static bool fwd_small_tiles() { return fwd_bn() == 32; }
 
 template <int DH, int BN, int NSB>
 int launch_fwd(const void* q, const void* k, const void* v, const int32_t* km, int* sched, void* o, float* lse, int B,
@@ -1342,12 +1412,15 @@ int attn_fwd_tc(const void* q, const void* k, const void* v, const int32_t* km, 
       return fa::fwd_small_tiles() ? fa::launch_fwd<16, 32, 2>(q, k, v, km, sched, o, lse, B, nh, S, st)
                                    : fa::launch_fwd<16, 64, 2>(q, k, v, km, sched, o, lse, B, nh, S, st);
     case 24:
+      if (fa::fwd_bn() == 128) return fa::launch_fwd<24, 128, 1>(q, k, v, km, sched, o, lse, B, nh, S, st);
       return fa::fwd_small_tiles() ? fa::launch_fwd<24, 32, 2>(q, k, v, km, sched, o, lse, B, nh, S, st)
                                    : fa::launch_fwd<24, 64, 2>(q, k, v, km, sched, o, lse, B, nh, S, st);
     case 32:
       return fa::fwd_small_tiles() ? fa::launch_fwd<32, 32, 2>(q, k, v, km, sched, o, lse, B, nh, S, st)
                                    : fa::launch_fwd<32, 64, 2>(q, k, v, km, sched, o, lse, B, nh, S, st);
-    case 64: return fa::launch_fwd<64, 64, 2>(q, k, v, km, sched, o, lse, B, nh, S, st);
+    case 64:
+      return fa::fwd_bn() == 128 ? fa::launch_fwd<64, 128, 1>(q, k, v, km, sched, o, lse, B, nh, S, st)
+                                 : fa::launch_fwd<64, 64, 2>(q, k, v, km, sched, o, lse, B, nh, S, st);
     default: set_last_error("attention: head dim %d unsupported", dh); return ESM_ENOTSUP;
   }
 }
