@@ -599,7 +599,8 @@ class EsmForMaskedLM:
         # stream behind the forward (3B: 11 GB, ~1.8 ms) and join right before the CE
         cur = torch.cuda.current_stream(self.device)
         if self._zero_stream is None:
-            self._zero_stream = torch.cuda.Stream(self.device)
+            self._zero_stream = torch.cuda.Stream(self.device) if os.environ.get("ESM_GRAD_ZERO_SIDE", "1") != "0" \
+                else cur
         self._zero_stream.wait_stream(cur)  # the previous step's optimizer has consumed the gradients
         with torch.cuda.stream(self._zero_stream):
             self.store.g32.zero_()
