@@ -163,10 +163,10 @@ NCU_TRAFFIC = {
         (279.5e6, "profiles/r1e_ncu_summary.txt: persistent fa::bwd_kernel<24>, the main kernel of the entry "
                   "point (read 194.2 MB + write 85.2 MB per layer launch)"),
     ("esm2_t33_650M", 16, 1024, "gemm_tcgen05"):
-        (233.4e6, "profiles/r3_ncu_launches_650m_summary.txt: sm100::gemm_tc_kernel, DRAM read + write averaged over "
+        (234.8e6, "profiles/r3r_ncu_launches_650m_summary.txt: sm100::gemm_tc_kernel, DRAM read + write averaged over "
                   "the 399 GEMM launches of one 650M step (ncu launch list, dram__bytes_read/write.sum)"),
     ("esm2_t33_650M", 16, 1024, "esm_attn_bwd_qkv"):
-        (373.1e6, "profiles/r3_ncu_launches_650m_summary.txt: persistent fa::bwd_kernel<64> (fused dqkv), DRAM read "
+        (372.8e6, "profiles/r3r_ncu_launches_650m_summary.txt: persistent fa::bwd_kernel<64> (fused dqkv), DRAM read "
                   "+ write per layer launch in the 650M step"),
 }
 
