@@ -219,14 +219,17 @@ def _zero1_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_sharded_optimizer_matches_allreduce_gloo_world2():
+@pytest.mark.parametrize("world", [2, 8])
+def test_sharded_optimizer_matches_allreduce_gloo(world):
+    """world 8 = the driver's largest data-parallel run: every bucket splits into 8 owned slices of whole AdamW
+    chunks and the 1-D fp32 parameters are re-synchronised from 8 owners."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_zero1_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_zero1_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=180) for _ in procs]
+    res = [q.get(timeout=300) for _ in procs]
     for p in procs:
         p.join(timeout=60)
     assert all(ok for _, ok in res), res
