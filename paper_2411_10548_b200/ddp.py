@@ -28,6 +28,7 @@ torch.distributed collectives.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import torch
 import torch.distributed as dist
@@ -103,8 +104,11 @@ class TorchDistComm:
 
 
 class GradAllReducer:
-    def __init__(self, store, bucket_bytes: int = 64 << 20, group=None, grad_dtype: str = "fp32",
+    def __init__(self, store, bucket_bytes: int | None = None, group=None, grad_dtype: str = "fp32",
                  shard_optimizer: bool = False, comm=None, master: str = "vectors"):
+        if bucket_bytes is None:  # ESM_BUCKET_MB, default 256 MB: fewer, longer collectives interrupt the persistent
+            # compute kernels less often (650M at N = 4: 90.6 ms/step vs 92.0 with 64 MB, 92.6 with 16 MB)
+            bucket_bytes = int(float(os.environ.get("ESM_BUCKET_MB", "256")) * (1 << 20))
         if grad_dtype not in ("fp32", "bf16"):
             raise ValueError("grad_dtype must be 'fp32' or 'bf16'")
         if master not in ("vectors", "full"):
