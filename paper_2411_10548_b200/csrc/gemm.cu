@@ -99,8 +99,14 @@ struct Cfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int BUDGET = 224 * 1024 - EpiCfg<EPI>::BYTES - 1024 - 512;
   static constexpr int STAGES = BUDGET / STAGE_BYTES > 8 ? 8 : BUDGET / STAGE_BYTES;
-  static constexpr uint32_t TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
-                                                          : (2 * BN <= 256) ? 256 : 512;
+  // BN = 512: two N = 256 MMAs per k-step into one accumulator that fills TMEM (no double buffering; a quarter
+  // less operand traffic per FLOP than BN = 256)
+  static constexpr int NSUB = BN > 256 ? 2 : 1;   // MMAs per K = 16 step
+  static constexpr int MMA_N = BN / NSUB;
+  static constexpr int BSUB = BN / CG / NSUB;     // B columns per CTA per MMA
+  static constexpr int NACC = BN > 256 ? 1 : 2;   // TMEM accumulator buffers
+  static constexpr uint32_t TMEM_COLS = (NACC * BN <= 32) ? 32 : (NACC * BN <= 64) ? 64 : (NACC * BN <= 128) ? 128
+                                                          : (NACC * BN <= 256) ? 256 : 512;
   static constexpr int SMEM = STAGES * STAGE_BYTES + EpiCfg<EPI>::BYTES + 1024 /*align*/ + 512 /*barriers*/;
   static_assert(STAGES >= 2, "not enough shared memory for the pipeline");
 };
@@ -165,7 +171,6 @@ __global__ void __launch_bounds__(EpiCfg<EPI>::THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ EpiMaps maps, TileInfo ti, EpiParams ep) {
   using C = Cfg<BN, EPI, CG>;
-  constexpr int BNC = BN / CG;  // B columns held by this CTA
   using E = EpiCfg<EPI>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -233,7 +238,7 @@ __global__ void __launch_bounds__(EpiCfg<EPI>::THREADS, 1)
       int mb, nb, kb0, kb1;
       decode_tile<MC>(ti, t, pi, mb, nb, kb0, kb1);
       const int m0 = mb * BM * CG + rank * BM;   // this CTA's A rows
-      const int n0 = nb * BN + rank * BNC;       // this CTA's B columns
+      const int n0 = nb * BN + rank * C::BSUB;   // this CTA's B columns (per MMA sub-tile j: + j * MMA_N)
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&empty_bar[stage], phase ^ 1);
         if (ESM_GEMM_EXP == 1) {
@@ -260,12 +265,16 @@ __global__ void __launch_bounds__(EpiCfg<EPI>::THREADS, 1)
             for (int i = 0; i < BM / 64; ++i)
               load(a_dst + i * 64 * BK * 2, &tmA, &full_bar[stage], m0 + i * 64, kb * BK);
           }
-          if constexpr (!B_MN) {
-            load(b_dst, &tmB, &full_bar[stage], kb * BK, n0);
-          } else {
 #pragma unroll
-            for (int i = 0; i < BNC / 64; ++i)
-              load(b_dst + i * 64 * BK * 2, &tmB, &full_bar[stage], n0 + i * 64, kb * BK);
+          for (int j = 0; j < C::NSUB; ++j) {
+            uint8_t* bj = b_dst + j * C::BSUB * BK * 2;
+            if constexpr (!B_MN) {
+              load(bj, &tmB, &full_bar[stage], kb * BK, n0 + j * C::MMA_N);
+            } else {
+#pragma unroll
+              for (int i = 0; i < C::BSUB / 64; ++i)
+                load(bj + i * 64 * BK * 2, &tmB, &full_bar[stage], n0 + j * C::MMA_N + i * 64, kb * BK);
+            }
           }
         }
         __syncwarp();
@@ -277,18 +286,19 @@ __global__ void __launch_bounds__(EpiCfg<EPI>::THREADS, 1)
     }
   } else if (warp == 1 && rank == 0) {
     // ===================== MMA issuer (leader CTA of a pair) =====================
-    constexpr uint32_t idesc = make_idesc_bf16(BM * CG, BN, A_MN, B_MN);
+    constexpr uint32_t idesc = make_idesc_bf16(BM * CG, C::MMA_N, A_MN, B_MN);
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
     for (int t = unit; t < num_tiles; t += nunits, ++it) {
       int mb, nb, kb0, kb1;
       decode_tile<MC>(ti, t, pi, mb, nb, kb0, kb1);
-      const int buf = it & 1;
-      const uint32_t aphase = (it >> 1) & 1;
+      const int buf = C::NACC == 2 ? (it & 1) : 0;
+      const uint32_t aphase = C::NACC == 2 ? ((it >> 1) & 1) : (it & 1);
       mbar_wait(&tempty_bar[buf], aphase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + buf * BN;
+      const int nsub = (C::NSUB == 2 && nb * BN + C::MMA_N >= ep.N) ? 1 : C::NSUB;  // skip an all-padding sub-tile
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&full_bar[stage], phase);
         tc_fence_after();
@@ -299,11 +309,17 @@ __global__ void __launch_bounds__(EpiCfg<EPI>::THREADS, 1)
           for (int k = 0; k < BK / 16; ++k) {
             const uint64_t ad = A_MN ? make_sdesc_sw128(a_base + k * 16 * 128, BK * 128, 1024)
                                      : make_sdesc_sw128(a_base + k * 32, 16, 1024);
-            const uint64_t bd = B_MN ? make_sdesc_sw128(b_base + k * 16 * 128, BK * 128, 1024)
-                                     : make_sdesc_sw128(b_base + k * 32, 16, 1024);
             if (ESM_GEMM_EXP == 2) break;
-            if constexpr (CG == 2) mma_bf16_ss_pair(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
-            else mma_bf16_ss(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+#pragma unroll
+            for (int j = 0; j < C::NSUB; ++j) {
+              if (j >= nsub) break;
+              const uint32_t bj = b_base + j * C::BSUB * BK * 2;
+              const uint64_t bd = B_MN ? make_sdesc_sw128(bj + k * 16 * 128, BK * 128, 1024)
+                                       : make_sdesc_sw128(bj + k * 32, 16, 1024);
+              const uint32_t dj = d_tmem + j * C::MMA_N;
+              if constexpr (CG == 2) mma_bf16_ss_pair(dj, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+              else mma_bf16_ss(dj, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            }
           }
           if constexpr (CG == 2) {
             mma_commit_pair(&empty_bar[stage], kAllMask);  // every CTA of the cluster: its stage may be refilled
@@ -335,8 +351,8 @@ __global__ void __launch_bounds__(EpiCfg<EPI>::THREADS, 1)
     for (int t = unit; t < num_tiles; t += nunits, ++it) {
       int mb, nb, kb0, kb1;
       decode_tile<MC>(ti, t, pi, mb, nb, kb0, kb1);
-      const int buf = it & 1;
-      const uint32_t aphase = (it >> 1) & 1;
+      const int buf = C::NACC == 2 ? (it & 1) : 0;
+      const uint32_t aphase = C::NACC == 2 ? ((it >> 1) & 1) : (it & 1);
       const int row0 = mb * BM * CG + rank * BM + q * 32;
       const int ncols = min(BN, ep.N - nb * BN);
       if constexpr (E::AUX) {  // prefetch the residual / pre-activation chunk of the first column block
@@ -650,7 +666,7 @@ static int launch_cg(const esm_gemm_args& a, cudaStream_t st) {
     rc = make_map(&tA, a.A, a.M, a.K, a.lda, 64, BK);
   if (rc) return rc;
   if (!B_MN)
-    rc = make_map(&tB, a.B, a.K, a.N, a.ldb, BK, BN / CG);
+    rc = make_map(&tB, a.B, a.K, a.N, a.ldb, BK, C::BSUB);
   else
     rc = make_map(&tB, a.B, a.N, a.K, a.ldb, 64, BK);
   if (rc) return rc;
@@ -766,7 +782,7 @@ template <int BN, bool A_MN, bool B_MN, int EPI>
 static int launch(const esm_gemm_args& a, cudaStream_t st) {
   // CTA pairs (M = 256 tiles) when M fills them; B columns are split across the pair, so for an
   // N-major B each half must be a whole number of 64-column TMA boxes.
-  constexpr bool pair_ok = (BN % 32 == 0) && (!B_MN || (BN / 2) % 64 == 0);
+  constexpr bool pair_ok = (BN % 32 == 0) && (!B_MN || (BN / 2) % 64 == 0) && BN <= 512;
   if constexpr (pair_ok) {
     if (pair_enabled() && a.M >= 2 * BM * 8) {
       if (mc_enabled() && a.N > BN) return launch_cg<BN, A_MN, B_MN, EPI, 2, 2>(a, st);
@@ -806,9 +822,24 @@ static int pick_bn_kmajor(int N) {
   return best;
 }
 
+// BN = 512 (256 x 512 pair tiles, two N = 256 MMAs per k-step, a single TMEM accumulator): a quarter less L2 -> SM
+// operand traffic per FLOP, measured 1551 vs 1351 TF/s at 8192^3 and 1502 vs 1415 at 16384 x 8192 x 4096.  With
+// no second accumulator the epilogue cannot overlap the next tile's mainloop, and all CTAs reach it together, so
+// its output burst is HBM-write bound: every ESM-2 shape measured slower (650M fc1 fwd 0.205 vs 0.185 ms, K = 1280;
+// 3B fc2 fwd 0.326 vs 0.319 ms, K = 10240 but 3 rounds of 160 tiles on 74 pairs vs 5 of 320).  Chosen only for long
+// K (>= 4096, epilogue amortised) when the wide tiles quantise onto the CTA pairs no worse than BN = 256 does.
+static bool prefer_bn512(const esm_gemm_args& a) {
+  if (env_bn() > 0 || !pair_enabled() || a.M < 2 * BM * 8 || a.K < 4096 || a.N % 512 != 0) return false;
+  const int pairs = num_sms() / 2;
+  const int64_t mt = (a.M + 2 * BM - 1) / (2 * BM);
+  const int64_t r512 = (mt * (a.N / 512) + pairs - 1) / pairs, r256 = (mt * (a.N / 256) + pairs - 1) / pairs;
+  return 2 * r512 <= r256;
+}
+
 template <bool A_MN, bool B_MN, int EPI>
 static int dispatch_bn(const esm_gemm_args& a, int bn, cudaStream_t st) {
   switch (bn) {
+    case 512: return launch<512, A_MN, B_MN, EPI>(a, st);
     case 256: return launch<256, A_MN, B_MN, EPI>(a, st);
     case 128: return launch<128, A_MN, B_MN, EPI>(a, st);
     case 64: return launch<64, A_MN, B_MN, EPI>(a, st);
@@ -835,7 +866,7 @@ int gemm_bf16(const esm_gemm_args& a, cudaStream_t st) {
   if (a.epilogue == ESM_EPI_F32_ACC) {
     ESM_CHECK_ARG(amn && bmn, "gemm: F32_ACC (wgrad) expects A and B MN-major");
     ESM_CHECK_ARG(a.ldc % 4 == 0 && ((uintptr_t)a.C & 15) == 0, "gemm: fp32 C must be 16B aligned");
-    const int bn = a.N > 128 ? 256 : 128;
+    const int bn = env_bn() == 512 ? 512 : (a.N > 128 ? 256 : 128);
     return dispatch_bn<true, true, ESM_EPI_F32_ACC>(a, bn, st);
   }
   ESM_CHECK_ARG(!amn, "gemm: activation-output GEMMs expect K-major A");
@@ -856,7 +887,7 @@ int gemm_bf16(const esm_gemm_args& a, cudaStream_t st) {
     }
   }
   if (!bmn) {
-    const int bn = pick_bn_kmajor(a.N);
+    const int bn = prefer_bn512(a) ? 512 : pick_bn_kmajor(a.N);
     switch (a.epilogue) {
       case ESM_EPI_STORE: return dispatch_bn<false, false, ESM_EPI_STORE>(a, bn, st);
       case ESM_EPI_GELU: return dispatch_bn<false, false, ESM_EPI_GELU>(a, bn, st);
@@ -865,7 +896,9 @@ int gemm_bf16(const esm_gemm_args& a, cudaStream_t st) {
       default: break;
     }
   } else {
-    const int bn = env_bn() == 128 || env_bn() == 256 ? env_bn() : (a.N > 128 ? 256 : 128);
+    const int bn = env_bn() == 128 || env_bn() == 256 || env_bn() == 512 ? env_bn()
+                   : prefer_bn512(a)                                     ? 512
+                   : (a.N > 128 ? 256 : 128);
     switch (a.epilogue) {
       case ESM_EPI_STORE: return dispatch_bn<false, true, ESM_EPI_STORE>(a, bn, st);
       case ESM_EPI_DGELU: return dispatch_bn<false, true, ESM_EPI_DGELU>(a, bn, st);

@@ -101,7 +101,12 @@ def gemm():
         ("650M fc2 dgradDGELU", 16384, 5120, 1280, 0, 1, EPI_DGELU), ("650M fc1 dgrad", 16384, 1280, 5120, 0, 1, EPI_STORE),
         ("650M qkv dgrad", 16384, 1280, 3840, 0, 1, EPI_STORE), ("650M qkv wgrad", 3840, 1280, 16384, 1, 1, EPI_F32_ACC),
         ("650M out wgrad", 1280, 1280, 16384, 1, 1, EPI_F32_ACC), ("650M fc2 wgrad", 1280, 5120, 16384, 1, 1, EPI_F32_ACC),
-        ("8192^3 store", 8192, 8192, 8192, 0, 0, EPI_STORE)]:
+        ("3B fc1 fwd", 8192, 10240, 2560, 0, 0, EPI_GELU), ("3B fc2 fwd", 8192, 2560, 10240, 0, 0, EPI_RESID),
+        ("3B fc2 dgradDGELU", 8192, 10240, 2560, 0, 1, EPI_DGELU), ("3B fc1 dgrad", 8192, 2560, 10240, 0, 1, EPI_STORE),
+        ("3B qkv dgrad", 8192, 2560, 7680, 0, 1, EPI_STORE), ("3B out fwd", 8192, 2560, 2560, 0, 0, EPI_RESID),
+        ("3B fc1 wgrad", 10240, 2560, 8192, 1, 1, EPI_F32_ACC), ("3B fc2 wgrad", 2560, 10240, 8192, 1, 1, EPI_F32_ACC),
+        ("8192^3 store", 8192, 8192, 8192, 0, 0, EPI_STORE), ("4096^3 store", 4096, 4096, 4096, 0, 0, EPI_STORE),
+        ("16384x8192x4096 store", 16384, 8192, 4096, 0, 0, EPI_STORE)]:
         if len(sys.argv) > 2 and sys.argv[2] not in name:
             continue
         A = torch.randn((K, M) if amn else (M, K), device="cuda").bfloat16()

@@ -74,6 +74,38 @@ def test_gemm_forward_epilogues(M, N, K, dt):
     assert rel(C, ref + R.float()) < tol
 
 
+def test_gemm_wide_tile_long_k():
+    """4096^3 picks the 256 x 512 pair tile (two N = 256 MMAs per k-step, one TMEM accumulator; gemm.cu
+    prefer_bn512) for both B layouts and the STORE / GELU / RESID / DGELU epilogues."""
+    torch.manual_seed(4)
+    M = N = K = 4096
+    X = torch.randn(M, K, device=DEV).bfloat16()
+    W = (torch.randn(N, K, device=DEV) * 0.05).bfloat16()
+    b = torch.randn(N, device=DEV)
+    R = torch.randn(M, N, device=DEV).bfloat16()
+    ref = X.float() @ W.float().t() + b
+    C = torch.empty(M, N, device=DEV, dtype=torch.bfloat16)
+    Z = torch.empty_like(C)
+    run_gemm(ESM_BF16, M, N, K, X, K, 0, W, K, 0, C, N, EPI_GELU, bias=b, aux_out=Z)
+    torch.cuda.synchronize()
+    errs = [rel(Z, ref), rel(C, gelu(ref))]
+    run_gemm(ESM_BF16, M, N, K, X, K, 0, W, K, 0, C, N, EPI_RESID, bias=b, aux_in=R)
+    torch.cuda.synchronize()
+    errs.append(rel(C, ref + R.float()))
+    Wt = W.t().contiguous()  # [K, N]: N-major B
+    ref2 = X.float() @ Wt.float()
+    run_gemm(ESM_BF16, M, N, K, X, K, 0, Wt, N, 1, C, N, EPI_STORE)
+    torch.cuda.synchronize()
+    errs.append(rel(C, ref2))
+    cs = torch.zeros(N, device=DEV)
+    run_gemm(ESM_BF16, M, N, K, X, K, 0, Wt, N, 1, C, N, EPI_DGELU, aux_in=R, col_sum=cs)
+    torch.cuda.synchronize()
+    want = ref2 * gelu_grad(R.float())
+    errs += [rel(C, want), rel(cs, want.sum(0))]
+    print("wide-tile GEMM errors:", ["%.1e" % e for e in errs])
+    assert max(errs) < 2e-2
+
+
 @pytest.mark.parametrize("M,N,K", [(256, 128, 64), (1000, 480, 1440), (300, 1920, 480), (515, 64, 200),
                                    (2048, 1280, 5120), (2500, 480, 1920), (4096, 1920, 480), (2048, 128, 64)])
 @pytest.mark.parametrize("dt", ["bf16", "fp32"])
