@@ -499,6 +499,28 @@ def main():
     value = tokens_per_step / (ms / 1e3)
 
     # ---------------- end to end through the public API, host buffers
+    class LossToHost:
+        """Every step's loss is copied device -> pinned host inside the timed region (non-blocking) and read by
+        the host one step behind, as a training loop logs it: the host never stalls the GPU between steps."""
+
+        def __init__(self, n):
+            self.host = torch.empty(max(n, 1), dtype=torch.float32).pin_memory()
+            self.ev = [torch.cuda.Event(), torch.cuda.Event()]
+            self.vals = []
+
+        def push(self, i, loss_dev):
+            self.host[i:i + 1].copy_(loss_dev.view(-1)[:1], non_blocking=True)
+            self.ev[i % 2].record()
+            if i > 0:
+                self.ev[(i - 1) % 2].synchronize()
+                self.vals.append(float(self.host[i - 1]))
+
+        def finish(self, n):
+            torch.cuda.synchronize()
+            self.vals.append(float(self.host[n - 1]))
+            if len(self.vals) != n or not all(np.isfinite(self.vals)):
+                raise RuntimeError(f"e2e: bad per-step losses {self.vals}")
+
     e2e = None
     if not args.no_e2e and gene:
         # per step: pinned CSR rows of the batch -> HBM, GPU rank tokenisation into ws.ids / ws.am,
@@ -530,17 +552,19 @@ def main():
                 model.graph_step()
             else:
                 model.step(ws)
-            return float(ws.loss_sum.item())
 
         for i in range(2):
             e2e_step(i)
+            float(ws.loss_sum.item())
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        reader = LossToHost(args.steps)
         t0 = time.perf_counter()
         for i in range(args.steps):
             e2e_step(i)
-        torch.cuda.synchronize()
+            reader.push(i, ws.loss_sum)                            # D2H: the step's loss
+        reader.finish(args.steps)
         wall = (time.perf_counter() - t0) / args.steps
         tw = torch.tensor([wall], device=dev)
         if world > 1:
@@ -548,7 +572,7 @@ def main():
         wall = float(tw.item())
         enc.check()
         e2e = {"value": tokens_per_step / wall, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": 4, "ms_per_step": wall * 1e3,
+               "d2h_bytes_per_step": 4, "ms_per_step": wall * 1e3, "d2h": "each step's loss, non-blocking into pinned host, read one step behind",
                "api": "RankEncoder.encode_device (CSR rows) + EsmForMaskedLM.mlm_mask + graph_step",
                "inputs": "CSR expression rows (indptr/cols int64, vals f32), pinned host"}
     elif not args.no_e2e:
@@ -560,7 +584,10 @@ def main():
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        reader = LossToHost(args.steps)
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0 = time.perf_counter()
+        d0.record()
         for i in range(args.steps):
             ws.ids.copy_(host[i % 2], non_blocking=True)          # H2D: this step's token ids
             model.mlm_mask(ws.ids, seed, 10_000 + i * world + rank, ws)
@@ -568,15 +595,18 @@ def main():
                 model.graph_step()
             else:
                 model.step(ws)
-            float(ws.loss_sum.item())                              # D2H: the step's loss
-        torch.cuda.synchronize()
+            reader.push(i, ws.loss_sum)                            # D2H: the step's loss (read one step behind)
+        d1.record()
+        reader.finish(args.steps)
         wall = (time.perf_counter() - t0) / args.steps
+        dev_ms = d0.elapsed_time(d1) / args.steps
         tw = torch.tensor([wall], device=dev)
         if world > 1:
             dist.all_reduce(tw, op=dist.ReduceOp.MAX)
         wall = float(tw.item())
         e2e = {"value": tokens_per_step / wall, "unit": "tokens/s", "h2d_bytes_per_step": B * S * 4,
-               "d2h_bytes_per_step": 4, "ms_per_step": wall * 1e3, "api": "EsmForMaskedLM.mlm_mask+graph_step"
+               "d2h_bytes_per_step": 4, "ms_per_step": wall * 1e3, "device_ms_per_step": dev_ms,
+               "d2h": "each step's loss, non-blocking into pinned host, read one step behind", "api": "EsmForMaskedLM.mlm_mask+graph_step"
                if use_graph else "EsmForMaskedLM.mlm_mask+step"}
 
     # ---------------- per-kernel breakdown (one extra eager step under CUDA events)
