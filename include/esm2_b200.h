@@ -200,6 +200,22 @@ int esm_attn_bwd_qkv(const void* q, const void* k, const void* v, const void* o,
                      float* col_sum, const float* cos_t, const float* sin_t, float q_scale, int B, int nh, int S,
                      int dh, esm_stream_t stream);
 
+/* Attention-probability dropout (HF EsmSelfAttention: context = dropout(softmax(S)) @ V, HF:modeling_esm.py:
+ * 257-282, attention_probs_dropout_prob): the same three calls with an esm_dropout (NULL or threshold 0 = off).
+ * keep(b, h, q, k) is the esm_dropout bit of row (b*nh + h)*S + q, column k; the softmax normaliser keeps every
+ * probability, P.V uses keep * P / (1 - p); the backward regenerates the mask (dV = (Z o P)^T dO,
+ * dS = P o (Z o dP - Delta)).  bf16 path only; head dim 24 is rejected (its backward folds Delta into the dP MMA). */
+int esm_attn_fwd_dropout(int dtype, const void* q, const void* k, const void* v, const int32_t* key_mask,
+                         int32_t* sched, void* o, float* lse, int B, int nh, int S, int dh, const esm_dropout* drop,
+                         esm_stream_t stream);
+int esm_attn_bwd_dropout(int dtype, const void* q, const void* k, const void* v, const void* o, const void* dout,
+                         const float* lse, const int32_t* key_mask, int32_t* sched, float* delta, float* dq, void* dk,
+                         void* dv, int B, int nh, int S, int dh, const esm_dropout* drop, esm_stream_t stream);
+int esm_attn_bwd_qkv_dropout(const void* q, const void* k, const void* v, const void* o, const void* dout,
+                             const float* lse, const int32_t* key_mask, int32_t* sched, float* delta, float* dq_ws,
+                             void* dqkv, float* col_sum, const float* cos_t, const float* sin_t, float q_scale, int B,
+                             int nh, int S, int dh, const esm_dropout* drop, esm_stream_t stream);
+
 /* ---------------- LM head decoder + masked cross-entropy (HF:modeling_esm.py:777-815) ---------------- */
 /* logits = n·Eᵀ + bias for labelled rows; loss_sum += Σ nll * inv_denom[0]; dlogits -> dn (= dlogits·E),
  * dE += dlogitsᵀ·n, dbias += Σ dlogits.  Unlabelled rows get dn = 0. */

@@ -335,16 +335,28 @@ def dropout_keep(seed: int, site: int, rows: int, cols: int, p: float) -> np.nda
     return bits[:, :cols] >= thr
 
 
+ATTN_DROP_SITE = 4096  # call site of layer l's attention probabilities: 4096 + l (paper_2411_10548_b200/model.py)
+
+
+def attention_dropout_keep(seed: int, layer: int, B: int, nh: int, S: int, p: float) -> np.ndarray:
+    """bool [B, nh, S(query), S(key)] keep mask of layer ``layer``'s attention probabilities: the esm_dropout bit
+    of row (b*nh + h)*S + q, column k (include/esm2_b200.h, esm_attn_fwd_dropout)."""
+    return dropout_keep(seed, ATTN_DROP_SITE + layer, B * nh * S, S, p).reshape(B, nh, S, S)
+
+
 def forward_backward(cfg: OracleConfig, params: dict, input_ids: np.ndarray, attention_mask: np.ndarray,
                      labels: np.ndarray, dtype=np.float64, want_grads: bool = True,
                      keep_acts: bool = False, loss_denominator: float | None = None,
-                     hidden_dropout: tuple | None = None) -> StepResult:
+                     hidden_dropout: tuple | None = None, attention_dropout: tuple | None = None) -> StepResult:
     """One EsmForMaskedLM forward (+ backward) on CPU in ``dtype``.
 
     ``loss_denominator`` overrides the masked-token count used for the mean (the
     data-parallel global count); default = local count, as HF CrossEntropyLoss.
     ``hidden_dropout`` = (seed, p): training-mode hidden dropout with the counter-based masks of
     ``dropout_keep`` (kept values scaled by 1 / (1 - p), as nn.Dropout).
+    ``attention_dropout`` = (seed, p): dropout of the softmax probabilities before P·V (HF EsmSelfAttention,
+    HF:modeling_esm.py:257-282), masks from ``attention_dropout_keep``; the backward uses
+    dV = (Z∘P)ᵀ dO and dS = P ∘ (Z∘dP − rowsum(Z∘P∘dP)).
     """
     P = {k: np.asarray(v, dtype=dtype) for k, v in params.items()}
     B, S = input_ids.shape
@@ -383,6 +395,13 @@ def forward_backward(cfg: OracleConfig, params: dict, input_ids: np.ndarray, att
         seed, pd = hidden_dropout
         keep = dropout_keep(seed, site, B * S, H, pd).reshape(B, S, H)
         return keep.astype(dtype) * dtype(1.0 / (1.0 - pd))
+
+    def attn_mask(layer):  # [B, nh, S, S] multiplier of the probabilities, or None
+        if attention_dropout is None or attention_dropout[1] <= 0.0:
+            return None
+        seed, pd = attention_dropout
+        keep = attention_dropout_keep(seed, layer, B, nh, S, pd)
+        return keep.astype(dtype) * dtype(1.0 / (1.0 - pd))
     for i in range(L):
         p = f"esm.encoder.layer.{i}."
         res.hidden_states.append(x)
@@ -400,7 +419,8 @@ def forward_backward(cfg: OracleConfig, params: dict, input_ids: np.ndarray, att
         s = s - s.max(-1, keepdims=True)
         pr = np.exp(s)
         pr = pr / pr.sum(-1, keepdims=True)
-        o = (pr @ v).transpose(0, 2, 1, 3).reshape(B, S, H)
+        za = attn_mask(i)
+        o = ((pr if za is None else pr * za) @ v).transpose(0, 2, 1, 3).reshape(B, S, H)
         m_att, m_ffn = drop_mask(2 * i), drop_mask(2 * i + 1)
         br = _linear(o, P[p + "attention.output.dense.weight"], P[p + "attention.output.dense.bias"])
         x1 = x + (br if m_att is None else br * m_att)
@@ -410,7 +430,7 @@ def forward_backward(cfg: OracleConfig, params: dict, input_ids: np.ndarray, att
         br = _linear(a, P[p + "output.dense.weight"], P[p + "output.dense.bias"])
         x2 = x1 + (br if m_ffn is None else br * m_ffn)
         caches.append(dict(x=x, ln1=ln1, h1=h1, q=q, k=k, v=v, o=o, x1=x1, ln2=ln2, h2=h2, z=z, a=a,
-                           m_att=m_att, m_ffn=m_ffn))
+                           m_att=m_att, m_ffn=m_ffn, za=za))
         if keep_acts:
             res.acts[i] = dict(h1=h1, q=q, k=k, v=v, o=o, x1=x1, h2=h2, z=z, a=a)
         x = x2
@@ -483,8 +503,11 @@ def forward_backward(cfg: OracleConfig, params: dict, input_ids: np.ndarray, att
         s = s - s.max(-1, keepdims=True)
         pr = np.exp(s)
         pr = pr / pr.sum(-1, keepdims=True)
-        dv = pr.transpose(0, 1, 3, 2) @ do
+        za = c["za"]
+        dv = (pr if za is None else pr * za).transpose(0, 1, 3, 2) @ do
         dp = do @ v.transpose(0, 1, 3, 2)
+        if za is not None:
+            dp = dp * za
         ds = pr * (dp - (dp * pr).sum(-1, keepdims=True))
         dq = ds @ k
         dk = ds.transpose(0, 1, 3, 2) @ q

@@ -18,7 +18,8 @@ EPI_GELU_GRADAUX, EPI_MUL_AUX, EPI_DELTA = 7, 8, 9
 EXPORTS = [
     "esm_version", "esm_last_error", "esm_device_sm_count", "esm_tokenize", "esm_mlm_mask", "esm_embed_fwd",
     "esm_embed_bwd", "esm_layernorm_fwd", "esm_layernorm_bwd", "esm_gemm", "esm_qkv_rope_fwd", "esm_qkv_rope_bwd",
-    "esm_attn_prepare", "esm_attn_fwd", "esm_attn_bwd", "esm_attn_bwd_qkv", "esm_lmhead_xent", "esm_inv_count",
+    "esm_attn_prepare", "esm_attn_fwd", "esm_attn_bwd", "esm_attn_bwd_qkv", "esm_attn_fwd_dropout",
+    "esm_attn_bwd_dropout", "esm_attn_bwd_qkv_dropout", "esm_lmhead_xent", "esm_inv_count",
     "esm_mlm_mask_ex", "esm_label_compact", "esm_gather_rows", "esm_scatter_rows", "esm_xent_rows", "esm_colsum_rows",
     "esm_rank_encode", "esm_dropout_mask", "esm_adamw", "esm_adamw_bf16g", "esm_cast_f32_bf16", "esm_cast_bf16_f32",
     "esm_comm_version", "esm_comm_unique_id", "esm_comm_init", "esm_comm_destroy", "esm_comm_allreduce",
@@ -77,6 +78,10 @@ _SIGS = {
     "esm_attn_fwd": ([_I, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _P], _I),
     "esm_attn_bwd": ([_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _P], _I),
     "esm_attn_bwd_qkv": ([_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _F, _I, _I, _I, _I, _P], _I),
+    "esm_attn_fwd_dropout": ([_I, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P], _I),
+    "esm_attn_bwd_dropout": ([_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P], _I),
+    "esm_attn_bwd_qkv_dropout": ([_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _F, _I, _I, _I, _I, _P,
+                                  _P], _I),
     "esm_lmhead_xent": ([_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _P], _I),
     "esm_inv_count": ([_P, _P, _P], _I),
     "esm_mlm_mask_ex": ([_P, _P, _P, _P, _I64, _U64, _U64, _I, _I, _I, _I, _I, _P], _I),

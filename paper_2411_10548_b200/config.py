@@ -48,9 +48,8 @@ class EsmConfig:
             raise ValueError("emb_layer_norm_before=True (ESM-1b) is not supported")
         if not 0.0 <= self.hidden_dropout_prob < 1.0:
             raise ValueError("hidden_dropout_prob must be in [0, 1)")
-        if self.attention_probs_dropout_prob:
-            raise ValueError("attention-probability dropout is not implemented (ESM-2 trains with 0.0; hidden "
-                             "dropout, HF EsmSelfOutput / EsmOutput, is fused into the residual epilogues)")
+        if not 0.0 <= self.attention_probs_dropout_prob < 1.0:
+            raise ValueError("attention_probs_dropout_prob must be in [0, 1)")
         if self.head_dim not in (16, 24, 32, 64):
             raise ValueError(f"head_dim {self.head_dim} not supported by the attention kernels")
         if self.hidden_size % 16:

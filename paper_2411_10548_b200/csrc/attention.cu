@@ -401,10 +401,12 @@ __global__ void __launch_bounds__(256) dq_finalize_vec_kernel(const float* __res
 namespace esm {
 int attn_prepare_tc(const int32_t* km, int* sched, int B, int S, cudaStream_t st);
 int attn_fwd_tc(const void* q, const void* k, const void* v, const int32_t* km, int* sched, void* o, float* lse,
-                int B, int nh, int S, int dh, cudaStream_t st);
+                int B, int nh, int S, int dh, cudaStream_t st, const esm_dropout* drop);
 int attn_bwd_tc(const void* q, const void* k, const void* v, const void* dout, const float* lse, const float* delta,
                 const int32_t* km, int* sched, float* dq, void* dk, void* dv, int B, int nh, int S, int dh,
-                cudaStream_t st, void* dqkv, float* col_sum, const float* cos_t, const float* sin_t);
+                cudaStream_t st, void* dqkv, float* col_sum, const float* cos_t, const float* sin_t,
+                const esm_dropout* drop);
+static bool drop_on(const esm_dropout* d) { return d != nullptr && d->threshold != 0u; }
 }  // namespace esm
 
 using namespace esm;
@@ -414,14 +416,16 @@ extern "C" int esm_attn_prepare(const int32_t* key_mask, int32_t* sched, int B, 
   return attn_prepare_tc(key_mask, sched, B, S, reinterpret_cast<cudaStream_t>(stream));
 }
 
-extern "C" int esm_attn_fwd(int dtype, const void* q, const void* k, const void* v, const int32_t* key_mask,
-                            int32_t* sched, void* o, float* lse, int B, int nh, int S, int dh, esm_stream_t stream) {
+extern "C" int esm_attn_fwd_dropout(int dtype, const void* q, const void* k, const void* v, const int32_t* key_mask,
+                                    int32_t* sched, void* o, float* lse, int B, int nh, int S, int dh,
+                                    const esm_dropout* drop, esm_stream_t stream) {
   ESM_CHECK_ARG(q && k && v && o && lse && B > 0 && nh > 0 && S > 0, "esm_attn_fwd: bad args");
+  ESM_CHECK_ARG(!drop_on(drop) || dtype == ESM_BF16, "attention dropout: bf16 path only");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (dtype == ESM_BF16) {
     ESM_CHECK_ARG(sched != nullptr, "esm_attn_fwd: bf16 needs the scheduling workspace (esm_attn_prepare)");
     ESM_CHECK_ARG(S % 4 == 0, "esm_attn_fwd: bf16 needs S %% 4 == 0 (pad the batch)");
-    return attn_fwd_tc(q, k, v, key_mask, sched, o, lse, B, nh, S, dh, st);
+    return attn_fwd_tc(q, k, v, key_mask, sched, o, lse, B, nh, S, dh, st, drop);
   }
   ESM_CHECK_ARG(dh <= attn::MAXD, "esm_attn_fwd: dh <= 64");
   dim3 grid((S + 63) / 64, B * nh);
@@ -430,10 +434,17 @@ extern "C" int esm_attn_fwd(int dtype, const void* q, const void* k, const void*
   ESM_LAUNCH_RET();
 }
 
-extern "C" int esm_attn_bwd(int dtype, const void* q, const void* k, const void* v, const void* o, const void* dout,
-                            const float* lse, const int32_t* key_mask, int32_t* sched, float* delta, float* dq,
-                            void* dk, void* dv, int B, int nh, int S, int dh, esm_stream_t stream) {
+extern "C" int esm_attn_fwd(int dtype, const void* q, const void* k, const void* v, const int32_t* key_mask,
+                            int32_t* sched, void* o, float* lse, int B, int nh, int S, int dh, esm_stream_t stream) {
+  return esm_attn_fwd_dropout(dtype, q, k, v, key_mask, sched, o, lse, B, nh, S, dh, nullptr, stream);
+}
+
+extern "C" int esm_attn_bwd_dropout(int dtype, const void* q, const void* k, const void* v, const void* o,
+                                    const void* dout, const float* lse, const int32_t* key_mask, int32_t* sched,
+                                    float* delta, float* dq, void* dk, void* dv, int B, int nh, int S, int dh,
+                                    const esm_dropout* drop, esm_stream_t stream) {
   ESM_CHECK_ARG(q && k && v && dout && lse && delta && dq && dk && dv, "esm_attn_bwd: null pointer");
+  ESM_CHECK_ARG(!drop_on(drop) || dtype == ESM_BF16, "attention dropout: bf16 path only");
   ESM_CHECK_ARG(o || dtype == ESM_BF16, "esm_attn_bwd: fp32 needs o");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int64_t T_ = (int64_t)B * S;
@@ -444,7 +455,7 @@ extern "C" int esm_attn_bwd(int dtype, const void* q, const void* k, const void*
     if (o) attn::launch_delta<__nv_bfloat16>(o, dout, delta, T_, S, nh, dh, st);
     attn::zero_f32(dq, T_ * nh * dh, st);
     const int rc = attn_bwd_tc(q, k, v, dout, lse, delta, key_mask, sched, dq, dk, dv, B, nh, S, dh, st, nullptr,
-                               nullptr, nullptr, nullptr);
+                               nullptr, nullptr, nullptr, drop);
     if (rc) return rc;
     ESM_LAUNCH_RET();
   }
@@ -459,10 +470,18 @@ extern "C" int esm_attn_bwd(int dtype, const void* q, const void* k, const void*
   ESM_LAUNCH_RET();
 }
 
-extern "C" int esm_attn_bwd_qkv(const void* q, const void* k, const void* v, const void* o, const void* dout,
-                                const float* lse, const int32_t* key_mask, int32_t* sched, float* delta, float* dq_ws,
-                                void* dqkv, float* col_sum, const float* cos_t, const float* sin_t, float q_scale,
-                                int B, int nh, int S, int dh, esm_stream_t stream) {
+extern "C" int esm_attn_bwd(int dtype, const void* q, const void* k, const void* v, const void* o, const void* dout,
+                            const float* lse, const int32_t* key_mask, int32_t* sched, float* delta, float* dq,
+                            void* dk, void* dv, int B, int nh, int S, int dh, esm_stream_t stream) {
+  return esm_attn_bwd_dropout(dtype, q, k, v, o, dout, lse, key_mask, sched, delta, dq, dk, dv, B, nh, S, dh, nullptr,
+                              stream);
+}
+
+extern "C" int esm_attn_bwd_qkv_dropout(const void* q, const void* k, const void* v, const void* o, const void* dout,
+                                        const float* lse, const int32_t* key_mask, int32_t* sched, float* delta,
+                                        float* dq_ws, void* dqkv, float* col_sum, const float* cos_t,
+                                        const float* sin_t, float q_scale, int B, int nh, int S, int dh,
+                                        const esm_dropout* drop, esm_stream_t stream) {
   ESM_CHECK_ARG(q && k && v && dout && lse && sched && delta && dq_ws && dqkv && col_sum && cos_t && sin_t,
                 "esm_attn_bwd_qkv: null pointer");
   ESM_CHECK_ARG(S % 4 == 0 && dh % 8 == 0, "esm_attn_bwd_qkv: needs S %% 4 == 0 and dh %% 8 == 0");
@@ -471,7 +490,7 @@ extern "C" int esm_attn_bwd_qkv(const void* q, const void* k, const void* v, con
   if (o) attn::launch_delta<__nv_bfloat16>(o, dout, delta, T_, S, nh, dh, st);
   attn::zero_f32(dq_ws, T_ * nh * dh, st);
   const int rc = attn_bwd_tc(q, k, v, dout, lse, delta, key_mask, sched, dq_ws, nullptr, nullptr, B, nh, S, dh, st,
-                             dqkv, col_sum, cos_t, sin_t);
+                             dqkv, col_sum, cos_t, sin_t, drop);
   if (rc) return rc;
   const int lanes = nh * (dh / 8);  // vector path: threads per token
   if (dh % 8 == 0 && lanes <= 256 && ((uintptr_t)col_sum & 15) == 0) {
@@ -489,4 +508,12 @@ extern "C" int esm_attn_bwd_qkv(const void* q, const void* k, const void* v, con
   attn::dq_finalize_kernel<<<grid, 64, 0, st>>>(dq_ws, (__nv_bfloat16*)dqkv, col_sum, cos_t, sin_t, T_, S, nh, dh,
                                                  q_scale, rpb);
   ESM_LAUNCH_RET();
+}
+
+extern "C" int esm_attn_bwd_qkv(const void* q, const void* k, const void* v, const void* o, const void* dout,
+                                const float* lse, const int32_t* key_mask, int32_t* sched, float* delta, float* dq_ws,
+                                void* dqkv, float* col_sum, const float* cos_t, const float* sin_t, float q_scale,
+                                int B, int nh, int S, int dh, esm_stream_t stream) {
+  return esm_attn_bwd_qkv_dropout(q, k, v, o, dout, lse, key_mask, sched, delta, dq_ws, dqkv, col_sum, cos_t, sin_t,
+                                  q_scale, B, nh, S, dh, nullptr, stream);
 }

@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, fwd_ctas_per_sm<DH, BN, NSB>())
     fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                const __grid_constant__ CUtensorMap tmV, const int32_t* __restrict__ key_mask,
                int* __restrict__ sched, __nv_bfloat16* __restrict__ O, float* __restrict__ LSE, int S, int nh,
-               int nbh) {
+               int nbh, const esm_dropout drop) {
   using SH = Shape<DH, BN, NSB>;
   constexpr int DP = SH::DP, ROWB = SH::ROWB, ST = SH::STAGES;
   constexpr int QB = SH::Q_BYTES, TB = SH::KV_BYTES;
@@ -391,6 +391,10 @@ __global__ void __launch_bounds__(kThreads, fwd_ctas_per_sm<DH, BN, NSB>())
       const int r = qq * 32 + lane;  // query row within tile == TMEM lane
       const uint32_t lane_off = (uint32_t)(qq * 32) << 16;
       float m_used = -INFINITY, l = 0.f;
+      // attention-probability dropout (HF: dropout(softmax(S)) @ V): the row sum l keeps every probability, the
+      // P fed to P.V is masked and scaled; keep(q, k) = esm_dropout bit of row bh*S + q, column k
+      const DropKeys dk = drop_keys(drop);
+      const uint32_t drh = dk.on ? drop_row(dk, (uint32_t)(row0 + q0 + r)) : 0u;
       for (int j = 0; j < ntiles; ++j) {
         const int gj = G0 + j;
         mbar_wait(&s_full[gj % NSB], (gj / NSB) & 1);
@@ -463,7 +467,7 @@ __global__ void __launch_bounds__(kThreads, fwd_ctas_per_sm<DH, BN, NSB>())
           const uint64_t l2e = f2_splat(L2E), nm = f2_splat(-moff);
           uint64_t ls0 = f2_splat(0.f), ls1 = ls0;
           uint32_t pk[BN / 2];
-          auto exps = [&](auto fp_tag) {
+          auto exps = [&](auto fp_tag, auto drop_tag) {
             constexpr int F = decltype(fp_tag)::value;
 #pragma unroll
             for (int e = 0; e < BN / 2; e += 4) {  // 8 keys: 4 pairs
@@ -484,12 +488,21 @@ __global__ void __launch_bounds__(kThreads, fwd_ctas_per_sm<DH, BN, NSB>())
               ls1 = f2_add(ls1, f2_pack(pr[2], pr[3]));
               ls0 = f2_add(ls0, f2_pack(pr[4], pr[5]));
               ls1 = f2_add(ls1, f2_pack(pr[6], pr[7]));
+              if constexpr (decltype(drop_tag)::value) {  // keys kbase + 2(e + q) + {0, 1}
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  const uint32_t kb = drop_pair(dk, drh, (uint32_t)(kbase / 2 + e + q));
+                  pr[2 * q] = (kb & 1u) ? pr[2 * q] * dk.scale : 0.f;
+                  pr[2 * q + 1] = (kb & 2u) ? pr[2 * q + 1] * dk.scale : 0.f;
+                }
+              }
 #pragma unroll
               for (int q = 0; q < 4; ++q) pk[e + q] = pack2(pr[2 * q], pr[2 * q + 1]);
             }
           };
-          if (FP > 0 && full) exps(std::integral_constant<int, FP>{});
-          else exps(std::integral_constant<int, 0>{});
+          if (dk.on) exps(std::integral_constant<int, 0>{}, std::true_type{});
+          else if (FP > 0 && full) exps(std::integral_constant<int, FP>{}, std::false_type{});
+          else exps(std::integral_constant<int, 0>{}, std::false_type{});
           if constexpr (BN == 64) tmem_st32(sbase, pk);  // P (bf16x2) over the first BN/2 columns of this S buffer
           else tmem_st16(sbase, pk);
           float l0, l1, l2, l3;
@@ -648,6 +661,7 @@ struct FusedOut {
   const float* cos_t;   // [S, dh/2]
   const float* sin_t;
   int H;
+  esm_dropout drop;     // attention-probability dropout (threshold 0: off); keep(q, k) at (row bh*S + q, column k)
 };
 
 __device__ __forceinline__ void tma_reduce_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
@@ -1105,6 +1119,7 @@ __global__ void __launch_bounds__(BwdWarps<SW>::THREADS, 1)
     const int qq = warp & 3;
     const int hf = (warp - 2) >> 2;
     const int kr = qq * 32 + lane;
+    const DropKeys dk = drop_keys(fo.drop);
     const uint32_t lane_off = (uint32_t)(qq * 32) << 16;
     const int c = hf * QW;
     for (int it = 0;; ++it) {
@@ -1132,7 +1147,38 @@ __global__ void __launch_bounds__(BwdWarps<SW>::THREADS, 1)
         tmem_ld_wait();
         uint32_t pp[QW / 2], dd[QW / 2];
         const int qmax = S - i * 64 - c;
-        if (ESM_ATTN_EXP == 1) {
+        bool dropped = false;
+        if constexpr (!BS::FOLD) {
+          if (dk.on) {
+            // attention-probability dropout: dV uses Z o P^T, dS^T = P^T o (Z o dP^T - Delta), Z = keep / (1 - p)
+            const uint32_t kpair = (uint32_t)key >> 1;
+            const int kodd = key & 1;
+            const uint32_t qrow0 = (uint32_t)(bh * S + i * 64 + c);
+#pragma unroll
+            for (int e = 0; e < QW; e += 4) {
+              const float4 l4 = *reinterpret_cast<const float4*>(lse + e);
+              const float4 d4 = *reinterpret_cast<const float4*>(dl + e);
+              const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv4[4] = {d4.x, d4.y, d4.z, d4.w};
+              float pz[4], ds[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const float xe = fmaf(__uint_as_float(us[e + u]), L2E, lv[u]);
+                const float pr = (kvalid && e + u < qmax) ? ex2(xe) : 0.f;
+                const uint32_t kb = drop_pair(dk, drop_row(dk, qrow0 + (uint32_t)(e + u)), kpair);
+                const float z = ((kb >> kodd) & 1u) ? dk.scale : 0.f;
+                pz[u] = pr * z;
+                ds[u] = pr * fmaf(__uint_as_float(ud[e + u]), z, -dv4[u]);
+              }
+              pp[e >> 1] = pack2(pz[0], pz[1]);
+              pp[(e >> 1) + 1] = pack2(pz[2], pz[3]);
+              dd[e >> 1] = pack2(ds[0], ds[1]);
+              dd[(e >> 1) + 1] = pack2(ds[2], ds[3]);
+            }
+            dropped = true;
+          }
+        }
+        if (dropped) {
+        } else if (ESM_ATTN_EXP == 1) {
 #pragma unroll
           for (int e = 0; e < QW / 2; ++e) pp[e] = dd[e] = us[e] ^ ud[e];
         } else if (__all_sync(0xffffffffu, kvalid) && qmax >= QW) {  // full tile: no masking
@@ -1288,7 +1334,7 @@ static bool fwd_small_tiles() { return fwd_bn() == 32; }
 
 template <int DH, int BN, int NSB>
 int launch_fwd(const void* q, const void* k, const void* v, const int32_t* km, int* sched, void* o, float* lse, int B,
-               int nh, int S, cudaStream_t st) {
+               int nh, int S, cudaStream_t st, const esm_dropout& drop) {
   using SH = Shape<DH, BN, NSB>;
   CUtensorMap tq, tk, tv;
   const int64_t rows = (int64_t)B * nh * S;
@@ -1303,7 +1349,7 @@ int launch_fwd(const void* q, const void* k, const void* v, const int32_t* km, i
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     launch_pdl(kern, dim3(grid), dim3(kThreads), smem, st, 1, tq, tk, tv, km, sched, (__nv_bfloat16*)o, lse, S, nh,
-               B * nh);
+               B * nh, drop);
   };
   switch (fwd_poly_pairs()) {
     case 0: go(fwd_kernel<DH, BN, NSB, 0>); break;
@@ -1390,9 +1436,14 @@ int attn_prepare_tc(const int32_t* km, int* sched, int B, int S, cudaStream_t st
 
 int attn_bwd_tc(const void* q, const void* k, const void* v, const void* dout, const float* lse, const float* delta,
                 const int32_t* km, int* sched, float* dq, void* dk, void* dv, int B, int nh, int S, int dh,
-                cudaStream_t st, void* dqkv, float* col_sum, const float* cos_t, const float* sin_t) {
+                cudaStream_t st, void* dqkv, float* col_sum, const float* cos_t, const float* sin_t,
+                const esm_dropout* drop) {
   ESM_CHECK_ARG(S % 4 == 0, "attention bwd (tcgen05): S %% 4 == 0 required");
-  fa::FusedOut fo{(__nv_bfloat16*)dqkv, col_sum, cos_t, sin_t, nh * dh};
+  const esm_dropout dr = (drop && drop->threshold != 0u) ? *drop : esm_dropout{nullptr, 0u, 0u, 1.f};
+  // dh = 24 folds Delta into the dP^T MMA (BwdShape::FOLD), which cannot apply the keep mask to dP^T alone
+  ESM_CHECK_ARG(dr.threshold == 0u || (dr.seed != nullptr && dh != 24),
+                "attention dropout: needs a seed; head dim 24 is not supported");
+  fa::FusedOut fo{(__nv_bfloat16*)dqkv, col_sum, cos_t, sin_t, nh * dh, dr};
   switch (dh) {
     case 16: return fa::launch_bwd<16>(q, k, v, dout, lse, delta, km, sched, dq, dk, dv, B, nh, S, st, fo);
     case 24: return fa::launch_bwd<24>(q, k, v, dout, lse, delta, km, sched, dq, dk, dv, B, nh, S, st, fo);
@@ -1403,24 +1454,27 @@ int attn_bwd_tc(const void* q, const void* k, const void* v, const void* dout, c
 }
 
 int attn_fwd_tc(const void* q, const void* k, const void* v, const int32_t* km, int* sched, void* o, float* lse,
-                int B, int nh, int S, int dh, cudaStream_t st) {
+                int B, int nh, int S, int dh, cudaStream_t st, const esm_dropout* drop) {
   ESM_CHECK_ARG(((uintptr_t)q & 15) == 0 && ((uintptr_t)k & 15) == 0 && ((uintptr_t)v & 15) == 0,
                 "attention: q/k/v must be 16B aligned");
+  const esm_dropout dr = (drop && drop->threshold != 0u) ? *drop : esm_dropout{nullptr, 0u, 0u, 1.f};
+  ESM_CHECK_ARG(dr.threshold == 0u || (dr.seed != nullptr && fa::fwd_bn() != 128),
+                "attention dropout: needs a seed and the 64-key forward tiles");
   // two S buffers per CTA, 2 CTAs/SM (a single-buffer 3-CTA/SM variant measured equal at dh 24, slower at 64)
   switch (dh) {
     case 16:
-      return fa::fwd_small_tiles() ? fa::launch_fwd<16, 32, 2>(q, k, v, km, sched, o, lse, B, nh, S, st)
-                                   : fa::launch_fwd<16, 64, 2>(q, k, v, km, sched, o, lse, B, nh, S, st);
+      return fa::fwd_small_tiles() ? fa::launch_fwd<16, 32, 2>(q, k, v, km, sched, o, lse, B, nh, S, st, dr)
+                                   : fa::launch_fwd<16, 64, 2>(q, k, v, km, sched, o, lse, B, nh, S, st, dr);
     case 24:
-      if (fa::fwd_bn() == 128) return fa::launch_fwd<24, 128, 1>(q, k, v, km, sched, o, lse, B, nh, S, st);
-      return fa::fwd_small_tiles() ? fa::launch_fwd<24, 32, 2>(q, k, v, km, sched, o, lse, B, nh, S, st)
-                                   : fa::launch_fwd<24, 64, 2>(q, k, v, km, sched, o, lse, B, nh, S, st);
+      if (fa::fwd_bn() == 128) return fa::launch_fwd<24, 128, 1>(q, k, v, km, sched, o, lse, B, nh, S, st, dr);
+      return fa::fwd_small_tiles() ? fa::launch_fwd<24, 32, 2>(q, k, v, km, sched, o, lse, B, nh, S, st, dr)
+                                   : fa::launch_fwd<24, 64, 2>(q, k, v, km, sched, o, lse, B, nh, S, st, dr);
     case 32:
-      return fa::fwd_small_tiles() ? fa::launch_fwd<32, 32, 2>(q, k, v, km, sched, o, lse, B, nh, S, st)
-                                   : fa::launch_fwd<32, 64, 2>(q, k, v, km, sched, o, lse, B, nh, S, st);
+      return fa::fwd_small_tiles() ? fa::launch_fwd<32, 32, 2>(q, k, v, km, sched, o, lse, B, nh, S, st, dr)
+                                   : fa::launch_fwd<32, 64, 2>(q, k, v, km, sched, o, lse, B, nh, S, st, dr);
     case 64:
-      return fa::fwd_bn() == 128 ? fa::launch_fwd<64, 128, 1>(q, k, v, km, sched, o, lse, B, nh, S, st)
-                                 : fa::launch_fwd<64, 64, 2>(q, k, v, km, sched, o, lse, B, nh, S, st);
+      return fa::fwd_bn() == 128 ? fa::launch_fwd<64, 128, 1>(q, k, v, km, sched, o, lse, B, nh, S, st, dr)
+                                 : fa::launch_fwd<64, 64, 2>(q, k, v, km, sched, o, lse, B, nh, S, st, dr);
     default: set_last_error("attention: head dim %d unsupported", dh); return ESM_ENOTSUP;
   }
 }

@@ -42,6 +42,7 @@ from .config import EsmConfig
 ALIGN = 256  # elements; also the AdamW weight-decay chunk size
 TOTAL_ALIGN = 8 * ALIGN  # the flat buffer splits into 1, 2, 4 or 8 data-parallel shards of whole chunks
 LARGE_VOCAB = 40  # esm_lmhead_xent's per-row fused head handles V <= 40; larger V uses the GEMM head
+ATTN_DROP_SITE = 4096  # esm_dropout call sites of the attention probabilities: 4096 + layer (hidden: 2*layer + 0/1)
 
 
 def head_capacity(T: int) -> int:
@@ -323,6 +324,11 @@ class EsmForMaskedLM:
         self.hyper = torch.zeros(8, dtype=torch.float32, device=self.device)
         # hidden dropout: per-step 64-bit seed in device memory (read by the kernels: CUDA-graph safe)
         self.dropout_p = float(self.config.hidden_dropout_prob)
+        # attention-probability dropout (HF EsmSelfAttention, dropout(softmax(S)) @ V): the tcgen05 kernels apply
+        # and regenerate the counter-based mask (esm_attn_*_dropout); bf16 only, head dim 24 unsupported
+        self.attn_dropout_p = float(self.config.attention_probs_dropout_prob)
+        if self.attn_dropout_p > 0.0 and (dtype != "bf16" or self.config.head_dim == 24):
+            raise NotImplementedError("attention-probability dropout needs the bf16 path and head_dim != 24")
         self.dropout_base = (int(seed) * 0x9E3779B97F4A7C15 + 0xD1B54A32D192ED03) & 0xFFFFFFFFFFFFFFFF
         self.drop_seed = torch.zeros(1, dtype=torch.int64, device=self.device)
         self.last_dropout_seed = 0
@@ -632,8 +638,14 @@ class EsmForMaskedLM:
                                 ws.qkv)
                 call("esm_qkv_rope_fwd", kdt, ws.qkv.data_ptr(), ly.q.data_ptr(), ly.k.data_ptr(), ly.v.data_ptr(),
                      ws.cos.data_ptr(), ws.sin.data_ptr(), B, S, nh, dh, qs, st)
-            call("esm_attn_fwd", kdt, ly.q.data_ptr(), ly.k.data_ptr(), ly.v.data_ptr(), ws.am.data_ptr(), sched,
-                 ly.o.data_ptr(), ly.lse.data_ptr(), B, nh, S, dh, st, flops=4.0 * B * nh * S * S * dh)
+            ad = self._attn_drop(l)
+            if ad is None:
+                call("esm_attn_fwd", kdt, ly.q.data_ptr(), ly.k.data_ptr(), ly.v.data_ptr(), ws.am.data_ptr(), sched,
+                     ly.o.data_ptr(), ly.lse.data_ptr(), B, nh, S, dh, st, flops=4.0 * B * nh * S * S * dh)
+            else:
+                call("esm_attn_fwd_dropout", kdt, ly.q.data_ptr(), ly.k.data_ptr(), ly.v.data_ptr(), ws.am.data_ptr(),
+                     sched, ly.o.data_ptr(), ly.lse.data_ptr(), B, nh, S, dh, ctypes.byref(ad), st,
+                     flops=4.0 * B * nh * S * S * dh)
             self.linear_fwd(ly.o, p + "attention.output.dense.weight", H, H, p + "attention.output.dense.bias",
                             ly.x1, epi=EPI_RESID, aux_in=x, drop=self._drop(2 * l))
             call("esm_layernorm_fwd", kdt, ly.x1.data_ptr(), self._p32(p + "LayerNorm.weight").data_ptr(),
@@ -722,14 +734,18 @@ class EsmForMaskedLM:
             self.linear_wgrad(dbr, ly.o, p + "attention.output.dense.weight", H, H)
             if kdt == ESM_BF16 and self._fused_attn_bwd(dh):
                 # fused: attention backward writes dqkv [T,3H] (RoPE^T, q-scale) + q/k/v bias grads
-                call("esm_attn_bwd_qkv", ly.q.data_ptr(), ly.k.data_ptr(), ly.v.data_ptr(), o_arg,
-                     ws.do.data_ptr(), ly.lse.data_ptr(), ws.am.data_ptr(), sched, ws.delta.data_ptr(),
-                     ws.dq.data_ptr(), ws.dqkv.data_ptr(), self._g32(p + "attention.self.qkv.bias").data_ptr(), ws.cos.data_ptr(),
-                     ws.sin.data_ptr(), qs, B, nh, S, dh, st, flops=8.0 * B * nh * S * S * dh)
+                ad = self._attn_drop(l)
+                call("esm_attn_bwd_qkv" if ad is None else "esm_attn_bwd_qkv_dropout", ly.q.data_ptr(),
+                     ly.k.data_ptr(), ly.v.data_ptr(), o_arg, ws.do.data_ptr(), ly.lse.data_ptr(), ws.am.data_ptr(),
+                     sched, ws.delta.data_ptr(), ws.dq.data_ptr(), ws.dqkv.data_ptr(),
+                     self._g32(p + "attention.self.qkv.bias").data_ptr(), ws.cos.data_ptr(), ws.sin.data_ptr(), qs, B,
+                     nh, S, dh, *(() if ad is None else (ctypes.byref(ad),)), st, flops=8.0 * B * nh * S * S * dh)
             else:
-                call("esm_attn_bwd", kdt, ly.q.data_ptr(), ly.k.data_ptr(), ly.v.data_ptr(), o_arg,
-                     ws.do.data_ptr(), ly.lse.data_ptr(), ws.am.data_ptr(), sched, ws.delta.data_ptr(),
-                     ws.dq.data_ptr(), ws.dk.data_ptr(), ws.dv.data_ptr(), B, nh, S, dh, st, flops=8.0 * B * nh * S * S * dh)
+                ad = self._attn_drop(l)
+                call("esm_attn_bwd" if ad is None else "esm_attn_bwd_dropout", kdt, ly.q.data_ptr(), ly.k.data_ptr(),
+                     ly.v.data_ptr(), o_arg, ws.do.data_ptr(), ly.lse.data_ptr(), ws.am.data_ptr(), sched,
+                     ws.delta.data_ptr(), ws.dq.data_ptr(), ws.dk.data_ptr(), ws.dv.data_ptr(), B, nh, S, dh,
+                     *(() if ad is None else (ctypes.byref(ad),)), st, flops=8.0 * B * nh * S * S * dh)
                 call("esm_qkv_rope_bwd", kdt, ws.dq.data_ptr(), ws.dk.data_ptr(), ws.dv.data_ptr(),
                      ws.dqkv.data_ptr(), self._g32(p + "attention.self.qkv.bias").data_ptr(), ws.cos.data_ptr(),
                      ws.sin.data_ptr(), B, S, nh, dh, qs, st)
@@ -792,6 +808,15 @@ class EsmForMaskedLM:
         return _lib.Dropout(self.drop_seed.data_ptr(), site, int(round(self.dropout_p * 65536.0)),
                             1.0 / (1.0 - self.dropout_p))
 
+    def _attn_drop(self, layer: int):
+        """esm_dropout of layer ``layer``'s attention probabilities (site 4096 + layer), or None (p = 0).  The
+        ctypes object is kept on the model: it must outlive the call that passes a pointer to it."""
+        if self.attn_dropout_p <= 0.0:
+            return None
+        self._attn_drop_keep = _lib.Dropout(self.drop_seed.data_ptr(), ATTN_DROP_SITE + layer,
+                                            int(round(self.attn_dropout_p * 65536.0)), 1.0 / (1.0 - self.attn_dropout_p))
+        return self._attn_drop_keep
+
     def set_hyper(self, lr=None, step=None):
         """Stage AdamW hyper-parameters in device memory (read by the kernel: CUDA-graph safe)."""
         lr = self.lr if lr is None else lr
@@ -803,7 +828,7 @@ class EsmForMaskedLM:
         h.copy_(torch.tensor([lr, self.betas[0], self.betas[1], self.eps, self.weight_decay, float(step),
                               self.grad_scale, 0.0], dtype=torch.float32))
         self.hyper.copy_(h, non_blocking=True)
-        if self.dropout_p > 0.0:
+        if self.dropout_p > 0.0 or self.attn_dropout_p > 0.0:
             self.set_dropout_seed(self.dropout_seed(step))
         ev = self._hyper_ev[i] = self._hyper_ev[i] or torch.cuda.Event()
         ev.record(torch.cuda.current_stream(self.device))
