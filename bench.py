@@ -61,6 +61,8 @@ def parse():
                     help="zero1: keep the fp32 master sharded and all-gather only the bf16 shadow (+ the 1-D fp32 "
                          "parameters), or all-gather the whole fp32 master as well")
     ap.add_argument("--nvtx", action="store_true", help="NVTX ranges around the step phases and layers")
+    ap.add_argument("--dropout", default="0,0", metavar="HIDDEN,ATTN",
+                    help="hidden / attention-probability dropout (ESM-2 trains with 0,0; Geneformer's BERT 0.02,0.02)")
     ap.add_argument("--varlen", action="store_true",
                     help="protein-like lengths (lognormal(5.6, 0.65) clipped to [10, seq]) batched by the reference's "
                          "create_buckets / bucket_batches at a token budget of batch x seq (SURVEY.md §8d, §8f.1)")
@@ -423,6 +425,8 @@ def main():
     B = args.batch or B
     S = args.seq or S
     cfg = preset(preset_name)
+    p_hid, p_att = (float(x) for x in args.dropout.split(","))
+    cfg.hidden_dropout_prob, cfg.attention_probs_dropout_prob = p_hid, p_att
     model = EsmForMaskedLM(cfg, dtype=args.dtype, device=dev, seed=1)
     model.nvtx = args.nvtx
     ws = model.workspace(B, S)
@@ -681,6 +685,7 @@ def main():
                                        else "") + ("-bf16grad" if args.grad_bf16 and world > 1 else ""),
                        "l2": "inputs/activations >> 126 MB L2 (no flush needed)",
                        "cuda_graph": use_graph, "weights": "random init",
+                       **({"dropout": {"hidden": p_hid, "attention_probs": p_att}} if p_hid or p_att else {}),
                        "data": (f"synthetic cells, {GF_NNZ[0]}-{GF_NNZ[1]} expressed genes of {GF_GENES}, "
                                 f"GPU rank-value tokens; non-pad tokens counted "
                                 f"({tokens_per_step / (B * S * world):.3f} fill)") if gene

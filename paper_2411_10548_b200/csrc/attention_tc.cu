@@ -1153,19 +1153,31 @@ __global__ void __launch_bounds__(BwdWarps<SW>::THREADS, 1)
             // attention-probability dropout: dV uses Z o P^T, dS^T = P^T o (Z o dP^T - Delta), Z = keep / (1 - p)
             const uint32_t kpair = (uint32_t)key >> 1;
             const int kodd = key & 1;
-            const uint32_t qrow0 = (uint32_t)(bh * S + i * 64 + c);
+            // row hashes of this warp's QW queries: lane e computes query e's, the others read it by shuffle
+            const uint32_t rh_lane = drop_row(dk, (uint32_t)(bh * S + i * 64 + c) + (uint32_t)(lane % QW));
 #pragma unroll
             for (int e = 0; e < QW; e += 4) {
               const float4 l4 = *reinterpret_cast<const float4*>(lse + e);
               const float4 d4 = *reinterpret_cast<const float4*>(dl + e);
               const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv4[4] = {d4.x, d4.y, d4.z, d4.w};
+              // one hash covers both keys of a pair (lanes 2j, 2j + 1): each lane hashes two of the four queries
+              // and swaps with its partner lane
+              uint32_t hv[4];
+#pragma unroll
+              for (int t = 0; t < 2; ++t) {
+                const uint32_t mine =
+                    lowbias32(__shfl_sync(0xffffffffu, rh_lane, e + 2 * t + kodd) ^ (kpair + dk.k1));
+                const uint32_t other = __shfl_xor_sync(0xffffffffu, mine, 1);
+                hv[2 * t] = kodd ? other : mine;
+                hv[2 * t + 1] = kodd ? mine : other;
+              }
               float pz[4], ds[4];
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
                 const float xe = fmaf(__uint_as_float(us[e + u]), L2E, lv[u]);
                 const float pr = (kvalid && e + u < qmax) ? ex2(xe) : 0.f;
-                const uint32_t kb = drop_pair(dk, drop_row(dk, qrow0 + (uint32_t)(e + u)), kpair);
-                const float z = ((kb >> kodd) & 1u) ? dk.scale : 0.f;
+                const uint32_t bits = kodd ? (hv[u] >> 16) : (hv[u] & 0xFFFFu);
+                const float z = bits >= dk.thr ? dk.scale : 0.f;
                 pz[u] = pr * z;
                 ds[u] = pr * fmaf(__uint_as_float(ud[e + u]), z, -dv4[u]);
               }
