@@ -1148,9 +1148,10 @@ __global__ void __launch_bounds__(BwdWarps<SW>::THREADS, 1)
         uint32_t pp[QW / 2], dd[QW / 2];
         const int qmax = S - i * 64 - c;
         bool dropped = false;
-        if constexpr (!BS::FOLD) {
+        {
           if (dk.on) {
-            // attention-probability dropout: dV uses Z o P^T, dS^T = P^T o (Z o dP^T - Delta), Z = keep / (1 - p)
+            // attention-probability dropout: dV uses Z o P^T, dS^T = P^T o (Z o dP^T - Delta), Z = keep / (1 - p).
+            // FOLD (dh 24): the MMA left dP^T - Delta, so Z o dP^T - Delta = Z o (dP^T - Delta) + (Z - 1) Delta
             const uint32_t kpair = (uint32_t)key >> 1;
             const int kodd = key & 1;
             // row hashes of this warp's QW queries: lane e computes query e's, the others read it by shuffle
@@ -1179,7 +1180,7 @@ __global__ void __launch_bounds__(BwdWarps<SW>::THREADS, 1)
                 const uint32_t bits = kodd ? (hv[u] >> 16) : (hv[u] & 0xFFFFu);
                 const float z = bits >= dk.thr ? dk.scale : 0.f;
                 pz[u] = pr * z;
-                ds[u] = pr * fmaf(__uint_as_float(ud[e + u]), z, -dv4[u]);
+                ds[u] = pr * fmaf(__uint_as_float(ud[e + u]), z, BS::FOLD ? (z - 1.f) * dv4[u] : -dv4[u]);
               }
               pp[e >> 1] = pack2(pz[0], pz[1]);
               pp[(e >> 1) + 1] = pack2(pz[2], pz[3]);
@@ -1452,9 +1453,7 @@ int attn_bwd_tc(const void* q, const void* k, const void* v, const void* dout, c
                 const esm_dropout* drop) {
   ESM_CHECK_ARG(S % 4 == 0, "attention bwd (tcgen05): S %% 4 == 0 required");
   const esm_dropout dr = (drop && drop->threshold != 0u) ? *drop : esm_dropout{nullptr, 0u, 0u, 1.f};
-  // dh = 24 folds Delta into the dP^T MMA (BwdShape::FOLD), which cannot apply the keep mask to dP^T alone
-  ESM_CHECK_ARG(dr.threshold == 0u || (dr.seed != nullptr && dh != 24),
-                "attention dropout: needs a seed; head dim 24 is not supported");
+  ESM_CHECK_ARG(dr.threshold == 0u || dr.seed != nullptr, "attention dropout: needs a seed");
   fa::FusedOut fo{(__nv_bfloat16*)dqkv, col_sum, cos_t, sin_t, nh * dh, dr};
   switch (dh) {
     case 16: return fa::launch_bwd<16>(q, k, v, dout, lse, delta, km, sched, dq, dk, dv, B, nh, S, st, fo);

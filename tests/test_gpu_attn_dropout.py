@@ -39,7 +39,7 @@ def prepare(am, B, S):
     return sched
 
 
-@pytest.mark.parametrize("dh", [16, 32, 64])
+@pytest.mark.parametrize("dh", [16, 24, 32, 64])
 @pytest.mark.parametrize("S,lens", [(256, [256, 190]), (1024, [1024, 601])])
 def test_attention_dropout_fwd_bwd(dh, S, lens):
     torch.manual_seed(11)
@@ -94,32 +94,31 @@ def test_attention_dropout_fwd_bwd(dh, S, lens):
     assert torch.equal(o0, o1)
 
 
-def test_attention_dropout_rejected_where_unsupported():
+def test_attention_dropout_rejected_in_fp32():
     B, nh, S = 1, 2, 128
     am = torch.ones(B, S, dtype=torch.int32, device=DEV)
     sched = prepare(am, B, S)
     seed_t = seed_tensor(7)
     d = _lib.Dropout(seed_t.data_ptr(), ATTN_DROP_SITE, O.dropout_threshold(0.1), 1.0 / 0.9)
-    for dh, dt, tdt in ((24, ESM_BF16, torch.bfloat16), (64, ESM_F32, torch.float32)):
-        q = torch.zeros(B, nh, S, dh, device=DEV, dtype=tdt)
-        o = torch.empty(B * S, nh * dh, device=DEV, dtype=tdt)
-        lse = torch.empty(B, nh, S, device=DEV)
-        dq = torch.empty(B, nh, S, dh, device=DEV)
-        delta = torch.empty(2, B, nh, S, device=DEV)
-        if dt == ESM_F32:  # the fp32 parity kernels have no dropout
-            with pytest.raises(_lib.EsmKernelError):
-                _lib.call("esm_attn_fwd_dropout", dt, q.data_ptr(), q.data_ptr(), q.data_ptr(), am.data_ptr(),
-                          sched.data_ptr(), o.data_ptr(), lse.data_ptr(), B, nh, S, dh, ctypes.byref(d), st())
-        with pytest.raises(_lib.EsmKernelError):  # dh 24: the backward folds Delta into the dP MMA
-            _lib.call("esm_attn_bwd_dropout", dt, q.data_ptr(), q.data_ptr(), q.data_ptr(), o.data_ptr(),
-                      o.data_ptr(), lse.data_ptr(), am.data_ptr(), sched.data_ptr(), delta.data_ptr(), dq.data_ptr(),
-                      q.data_ptr(), q.data_ptr(), B, nh, S, dh, ctypes.byref(d), st())
+    dh = 64  # the fp32 parity kernels have no dropout
+    q = torch.zeros(B, nh, S, dh, device=DEV)
+    o = torch.empty(B * S, nh * dh, device=DEV)
+    lse = torch.empty(B, nh, S, device=DEV)
+    dq = torch.empty(B, nh, S, dh, device=DEV)
+    delta = torch.empty(2, B, nh, S, device=DEV)
+    with pytest.raises(_lib.EsmKernelError):
+        _lib.call("esm_attn_fwd_dropout", ESM_F32, q.data_ptr(), q.data_ptr(), q.data_ptr(), am.data_ptr(),
+                  sched.data_ptr(), o.data_ptr(), lse.data_ptr(), B, nh, S, dh, ctypes.byref(d), st())
+    with pytest.raises(_lib.EsmKernelError):
+        _lib.call("esm_attn_bwd_dropout", ESM_F32, q.data_ptr(), q.data_ptr(), q.data_ptr(), o.data_ptr(),
+                  o.data_ptr(), lse.data_ptr(), am.data_ptr(), sched.data_ptr(), delta.data_ptr(), dq.data_ptr(),
+                  q.data_ptr(), q.data_ptr(), B, nh, S, dh, ctypes.byref(d), st())
     with pytest.raises(NotImplementedError):
         EsmForMaskedLM(EsmConfig(hidden_size=64, num_hidden_layers=1, num_attention_heads=1, intermediate_size=128,
                                  attention_probs_dropout_prob=0.1), dtype="fp32", device="cuda")
 
 
-@pytest.mark.parametrize("H,nh", [(128, 2), (256, 8), (320, 20)])  # head dims 64, 32, 16
+@pytest.mark.parametrize("H,nh", [(128, 2), (480, 20), (256, 8), (320, 20)])  # head dims 64, 24, 32, 16
 def test_model_attention_dropout_matches_oracle(H, nh):
     """bf16 model step with attention-probability dropout p = 0.1 (and hidden dropout 0.05) vs the fp64 oracle
     with the same counter-based masks; the fused (dqkv) and classic attention backwards agree."""
