@@ -204,7 +204,7 @@ int esm_attn_bwd_qkv(const void* q, const void* k, const void* v, const void* o,
  * 257-282, attention_probs_dropout_prob): the same three calls with an esm_dropout (NULL or threshold 0 = off).
  * keep(b, h, q, k) is the esm_dropout bit of row (b*nh + h)*S + q, column k; the softmax normaliser keeps every
  * probability, P.V uses keep * P / (1 - p); the backward regenerates the mask (dV = (Z o P)^T dO,
- * dS = P o (Z o dP - Delta)).  bf16 path only. */
+ * dS = P o (Z o dP - Delta)); bf16 (tcgen05) and fp32 (parity) kernels. */
 int esm_attn_fwd_dropout(int dtype, const void* q, const void* k, const void* v, const int32_t* key_mask,
                          int32_t* sched, void* o, float* lse, int B, int nh, int S, int dh, const esm_dropout* drop,
                          esm_stream_t stream);

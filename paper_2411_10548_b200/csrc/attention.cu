@@ -110,10 +110,19 @@ int launch_delta(const void* o, const void* dout, float* delta, int64_t T_, int 
 // ---------------------------------------------------------------------------- fp32 SIMT
 constexpr int MAXD = 64;
 
+// attention-probability dropout multiplier of (query q, key k) of head bh: keep / (1 - p) (1 when off); the
+// esm_dropout bit of row bh*S + q, column k, as the tcgen05 kernels (attention_tc.cu) and the oracle
+__device__ __forceinline__ float attn_drop_z(const DropKeys& dk, int bh, int S, int q, int k) {
+  if (!dk.on) return 1.f;
+  const uint32_t kb = drop_pair(dk, drop_row(dk, (uint32_t)((int64_t)bh * S + q)), (uint32_t)k >> 1);
+  return ((kb >> (k & 1)) & 1u) ? dk.scale : 0.f;
+}
+
 __global__ void __launch_bounds__(64) fwd_f32_kernel(const float* __restrict__ Q, const float* __restrict__ K,
                                                      const float* __restrict__ V, const int32_t* __restrict__ km,
                                                      float* __restrict__ O, float* __restrict__ LSE, int S, int nh,
-                                                     int dh) {
+                                                     int dh, const esm_dropout drop) {
+  const DropKeys dkeys = drop_keys(drop);
   __shared__ float sK[64][MAXD + 1], sV[64][MAXD + 1];
   __shared__ bool sM[64];
   const int bh = blockIdx.y, b = bh / nh, h = bh % nh;
@@ -147,10 +156,11 @@ __global__ void __launch_bounds__(64) fwd_f32_kernel(const float* __restrict__ Q
         if (d < dh) s += q[d] * sK[j][d];
       const float mn = fmaxf(m, s);
       const float sc = expf(m - mn), p = expf(s - mn);
-      l = l * sc + p;
+      l = l * sc + p;  // the normaliser keeps every probability
+      const float pz = p * attn_drop_z(dkeys, bh, S, qi, k0 + j);
 #pragma unroll
       for (int d = 0; d < MAXD; ++d)
-        if (d < dh) o[d] = o[d] * sc + p * sV[j][d];
+        if (d < dh) o[d] = o[d] * sc + pz * sV[j][d];
       m = mn;
     }
   }
@@ -170,7 +180,8 @@ __global__ void __launch_bounds__(64) bwd_dq_f32_kernel(const float* __restrict_
                                                         const float* __restrict__ LSE,
                                                         const float* __restrict__ Delta,
                                                         const int32_t* __restrict__ km, float* __restrict__ dQ, int S,
-                                                        int nh, int dh) {
+                                                        int nh, int dh, const esm_dropout drop) {
+  const DropKeys dkeys = drop_keys(drop);
   __shared__ float sK[64][MAXD + 1], sV[64][MAXD + 1];
   __shared__ bool sM[64];
   const int bh = blockIdx.y, b = bh / nh, h = bh % nh;
@@ -210,7 +221,7 @@ __global__ void __launch_bounds__(64) bwd_dq_f32_kernel(const float* __restrict_
           dp += go[d] * sV[j][d];
         }
       const float p = expf(s - lse);
-      const float ds = p * (dp - delta);
+      const float ds = p * (dp * attn_drop_z(dkeys, bh, S, qi, k0 + j) - delta);
 #pragma unroll
       for (int d = 0; d < MAXD; ++d)
         if (d < dh) dq[d] += ds * sK[j][d];
@@ -227,7 +238,9 @@ __global__ void __launch_bounds__(64) bwd_dkv_f32_kernel(const float* __restrict
                                                          const float* __restrict__ LSE,
                                                          const float* __restrict__ Delta,
                                                          const int32_t* __restrict__ km, float* __restrict__ dK,
-                                                         float* __restrict__ dV, int S, int nh, int dh) {
+                                                         float* __restrict__ dV, int S, int nh, int dh,
+                                                         const esm_dropout drop) {
+  const DropKeys dkeys = drop_keys(drop);
   __shared__ float sQ[64][MAXD + 1], sO[64][MAXD + 1];
   __shared__ float sL[64], sD[64];
   const int bh = blockIdx.y, b = bh / nh, h = bh % nh;
@@ -267,11 +280,12 @@ __global__ void __launch_bounds__(64) bwd_dkv_f32_kernel(const float* __restrict
           dp += sO[j][d] * v[d];
         }
       const float p = expf(s - sL[j]);
-      const float ds = p * (dp - sD[j]);
+      const float z = attn_drop_z(dkeys, bh, S, q0 + j, ki);
+      const float ds = p * (dp * z - sD[j]);
 #pragma unroll
       for (int d = 0; d < MAXD; ++d)
         if (d < dh) {
-          dv[d] += p * sO[j][d];
+          dv[d] += p * z * sO[j][d];
           dk[d] += ds * sQ[j][d];
         }
     }
@@ -420,7 +434,6 @@ extern "C" int esm_attn_fwd_dropout(int dtype, const void* q, const void* k, con
                                     int32_t* sched, void* o, float* lse, int B, int nh, int S, int dh,
                                     const esm_dropout* drop, esm_stream_t stream) {
   ESM_CHECK_ARG(q && k && v && o && lse && B > 0 && nh > 0 && S > 0, "esm_attn_fwd: bad args");
-  ESM_CHECK_ARG(!drop_on(drop) || dtype == ESM_BF16, "attention dropout: bf16 path only");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (dtype == ESM_BF16) {
     ESM_CHECK_ARG(sched != nullptr, "esm_attn_fwd: bf16 needs the scheduling workspace (esm_attn_prepare)");
@@ -430,7 +443,7 @@ extern "C" int esm_attn_fwd_dropout(int dtype, const void* q, const void* k, con
   ESM_CHECK_ARG(dh <= attn::MAXD, "esm_attn_fwd: dh <= 64");
   dim3 grid((S + 63) / 64, B * nh);
   attn::fwd_f32_kernel<<<grid, 64, 0, st>>>((const float*)q, (const float*)k, (const float*)v, key_mask, (float*)o,
-                                            lse, S, nh, dh);
+                                            lse, S, nh, dh, drop_on(drop) ? *drop : esm_dropout{nullptr, 0u, 0u, 1.f});
   ESM_LAUNCH_RET();
 }
 
@@ -444,7 +457,6 @@ extern "C" int esm_attn_bwd_dropout(int dtype, const void* q, const void* k, con
                                     float* delta, float* dq, void* dk, void* dv, int B, int nh, int S, int dh,
                                     const esm_dropout* drop, esm_stream_t stream) {
   ESM_CHECK_ARG(q && k && v && dout && lse && delta && dq && dk && dv, "esm_attn_bwd: null pointer");
-  ESM_CHECK_ARG(!drop_on(drop) || dtype == ESM_BF16, "attention dropout: bf16 path only");
   ESM_CHECK_ARG(o || dtype == ESM_BF16, "esm_attn_bwd: fp32 needs o");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int64_t T_ = (int64_t)B * S;
@@ -462,11 +474,12 @@ extern "C" int esm_attn_bwd_dropout(int dtype, const void* q, const void* k, con
   ESM_CHECK_ARG(dh <= attn::MAXD, "esm_attn_bwd: dh <= 64");
   dim3 grid((S + 63) / 64, B * nh);
   attn::launch_delta<float>(o, dout, delta, T_, S, nh, dh, st);
+  const esm_dropout dr = drop_on(drop) ? *drop : esm_dropout{nullptr, 0u, 0u, 1.f};
   attn::bwd_dq_f32_kernel<<<grid, 64, 0, st>>>((const float*)q, (const float*)k, (const float*)v, (const float*)dout,
-                                               lse, delta, key_mask, dq, S, nh, dh);
+                                               lse, delta, key_mask, dq, S, nh, dh, dr);
   attn::bwd_dkv_f32_kernel<<<grid, 64, 0, st>>>((const float*)q, (const float*)k, (const float*)v,
                                                 (const float*)dout, lse, delta, key_mask, (float*)dk, (float*)dv, S,
-                                                nh, dh);
+                                                nh, dh, dr);
   ESM_LAUNCH_RET();
 }
 

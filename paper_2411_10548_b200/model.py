@@ -325,10 +325,8 @@ class EsmForMaskedLM:
         # hidden dropout: per-step 64-bit seed in device memory (read by the kernels: CUDA-graph safe)
         self.dropout_p = float(self.config.hidden_dropout_prob)
         # attention-probability dropout (HF EsmSelfAttention, dropout(softmax(S)) @ V): the tcgen05 kernels apply
-        # and regenerate the counter-based mask (esm_attn_*_dropout); bf16 path only
+        # and regenerate the counter-based mask (esm_attn_*_dropout; the fp32 parity kernels too)
         self.attn_dropout_p = float(self.config.attention_probs_dropout_prob)
-        if self.attn_dropout_p > 0.0 and dtype != "bf16":
-            raise NotImplementedError("attention-probability dropout runs in the bf16 (tcgen05) path only")
         self.dropout_base = (int(seed) * 0x9E3779B97F4A7C15 + 0xD1B54A32D192ED03) & 0xFFFFFFFFFFFFFFFF
         self.drop_seed = torch.zeros(1, dtype=torch.int64, device=self.device)
         self.last_dropout_seed = 0

@@ -94,28 +94,63 @@ def test_attention_dropout_fwd_bwd(dh, S, lens):
     assert torch.equal(o0, o1)
 
 
-def test_attention_dropout_rejected_in_fp32():
-    B, nh, S = 1, 2, 128
+def test_attention_dropout_fp32_kernels():
+    """The fp32 parity kernels apply the same masks: vs torch fp64 autograd at 1e-5."""
+    torch.manual_seed(12)
+    B, nh, S, dh, p, layer = 2, 2, 192, 32, 0.2, 1
+    seed = 0x0F1E2D3C4B5A6978
     am = torch.ones(B, S, dtype=torch.int32, device=DEV)
-    sched = prepare(am, B, S)
-    seed_t = seed_tensor(7)
-    d = _lib.Dropout(seed_t.data_ptr(), ATTN_DROP_SITE, O.dropout_threshold(0.1), 1.0 / 0.9)
-    dh = 64  # the fp32 parity kernels have no dropout
-    q = torch.zeros(B, nh, S, dh, device=DEV)
+    am[1, 150:] = 0
+    q, k, v = (torch.randn(B, nh, S, dh, device=DEV) * 0.5 for _ in range(3))
+    seed_t = seed_tensor(seed)
+    d = _lib.Dropout(seed_t.data_ptr(), ATTN_DROP_SITE + layer, O.dropout_threshold(p), 1.0 / (1.0 - p))
     o = torch.empty(B * S, nh * dh, device=DEV)
     lse = torch.empty(B, nh, S, device=DEV)
-    dq = torch.empty(B, nh, S, dh, device=DEV)
+    _lib.call("esm_attn_fwd_dropout", ESM_F32, q.data_ptr(), k.data_ptr(), v.data_ptr(), am.data_ptr(), None,
+              o.data_ptr(), lse.data_ptr(), B, nh, S, dh, ctypes.byref(d), st())
+    z = torch.from_numpy(O.attention_dropout_keep(seed, layer, B, nh, S, p)).to(DEV).double() / (1.0 - p)
+    qr, kr, vr = (t.double().requires_grad_(True) for t in (q, k, v))
+    s = qr @ kr.transpose(-1, -2) + torch.where(am[:, None, None, :] > 0, 0.0, float("-inf")).double()
+    ref_o = ((torch.softmax(s, -1) * z) @ vr).permute(0, 2, 1, 3).reshape(B * S, nh * dh)
+    do = torch.randn(B * S, nh * dh, device=DEV)
+    ref_o.backward(do.double())
+    dq, dk, dv = (torch.empty(B, nh, S, dh, device=DEV) for _ in range(3))
     delta = torch.empty(2, B, nh, S, device=DEV)
-    with pytest.raises(_lib.EsmKernelError):
-        _lib.call("esm_attn_fwd_dropout", ESM_F32, q.data_ptr(), q.data_ptr(), q.data_ptr(), am.data_ptr(),
-                  sched.data_ptr(), o.data_ptr(), lse.data_ptr(), B, nh, S, dh, ctypes.byref(d), st())
-    with pytest.raises(_lib.EsmKernelError):
-        _lib.call("esm_attn_bwd_dropout", ESM_F32, q.data_ptr(), q.data_ptr(), q.data_ptr(), o.data_ptr(),
-                  o.data_ptr(), lse.data_ptr(), am.data_ptr(), sched.data_ptr(), delta.data_ptr(), dq.data_ptr(),
-                  q.data_ptr(), q.data_ptr(), B, nh, S, dh, ctypes.byref(d), st())
-    with pytest.raises(NotImplementedError):
-        EsmForMaskedLM(EsmConfig(hidden_size=64, num_hidden_layers=1, num_attention_heads=1, intermediate_size=128,
-                                 attention_probs_dropout_prob=0.1), dtype="fp32", device="cuda")
+    _lib.call("esm_attn_bwd_dropout", ESM_F32, q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), do.data_ptr(),
+              lse.data_ptr(), am.data_ptr(), None, delta.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), B,
+              nh, S, dh, ctypes.byref(d), st())
+    torch.cuda.synchronize()
+    errs = dict(o=rel(o, ref_o), dq=rel(dq, qr.grad), dk=rel(dk, kr.grad), dv=rel(dv, vr.grad))
+    print("attention dropout fp32 kernels:", {k_: "%.1e" % e for k_, e in errs.items()})
+    assert max(errs.values()) < 1e-5, errs
+
+
+def test_model_attention_dropout_fp32_matches_oracle():
+    """fp32 parity mode with attention dropout 0.1 (+ hidden dropout 0.05): loss and every gradient within 1e-4
+    of the fp64 oracle (the north-star bar for fp32 mode)."""
+    H, nh, L, F, B, S = 320, 20, 2, 1280, 2, 128
+    cfg = EsmConfig(hidden_size=H, num_hidden_layers=L, num_attention_heads=nh, intermediate_size=F,
+                    attention_probs_dropout_prob=0.1, hidden_dropout_prob=0.05)
+    ocfg = O.OracleConfig(hidden_size=H, num_hidden_layers=L, num_attention_heads=nh, intermediate_size=F)
+    params = init_params(cfg, seed=22)
+    ids, am = O.synthetic_batch(B, S, seed=7)
+    am[0, 100:] = 0
+    inp, lab = O.mlm_mask(ids, seed=8, stream=1)
+    seed = 0x0123456789ABCDEF
+    ref = O.forward_backward(ocfg, params, inp, am, lab, dtype=np.float64, attention_dropout=(seed, 0.1),
+                             hidden_dropout=(seed, 0.05))
+    m = EsmForMaskedLM(cfg, dtype="fp32", device="cuda", params=params)
+    m.set_dropout_seed(seed)
+    ws = m.set_batch(torch.from_numpy(inp).cuda(), torch.from_numpy(am).cuda(), torch.from_numpy(lab).cuda())
+    loss = float(m.forward_backward(ws).item())
+    g = m.grads()
+    errs = {k: float(np.abs(g[k].cpu().numpy().astype(np.float64) - r).max() / (np.abs(r).max() + 1e-30))
+            for k, r in ref.grads.items()}
+    worst = max(errs, key=errs.get)
+    print(f"attention dropout fp32 model: loss rel {abs(loss - ref.loss) / ref.loss:.2e}; worst grad {worst} "
+          f"{errs[worst]:.2e}")
+    assert abs(loss - ref.loss) / ref.loss < 1e-5
+    assert errs[worst] < 1e-4, (worst, errs[worst])
 
 
 @pytest.mark.parametrize("H,nh", [(128, 2), (480, 20), (256, 8), (320, 20)])  # head dims 64, 24, 32, 16
