@@ -201,3 +201,34 @@ def test_model_attention_dropout_matches_oracle(H, nh):
     assert fro[worst] < gate(worst), (worst, fro[worst])
     assert abs(loss_c - loss) < 1e-6 * abs(loss)  # same forward
     assert fc[worst_c] < 2e-2, (worst_c, fc[worst_c])
+
+
+def test_graph_step_with_dropout_matches_eager():
+    """Hidden + attention dropout under CUDA-graph replay: each replay reads that step's seed from device memory,
+    so three graph steps reproduce three eager steps (same masks, same updates) and the masks change per step."""
+    cfg = EsmConfig(hidden_size=320, num_hidden_layers=2, num_attention_heads=20, intermediate_size=1280,
+                    attention_probs_dropout_prob=0.1, hidden_dropout_prob=0.1)
+    params = init_params(cfg, seed=31)
+    ids, am = O.synthetic_batch(4, 256, seed=9)
+    am[2, 200:] = 0
+
+    def run(graph):
+        m = EsmForMaskedLM(cfg, dtype="bf16", device="cuda", params=params, seed=5)
+        ws = m.workspace(4, 256)
+        ws.ids.copy_(torch.from_numpy(ids))
+        ws.am.copy_(torch.from_numpy(am))
+        m.mlm_mask(ws.ids, seed=3, stream_id=1, ws=ws)
+        if graph:
+            m.capture(ws)
+        losses = [float((m.graph_step() if graph else m.step(ws)).item()) for _ in range(3)]
+        seeds = m.last_dropout_seed
+        return losses, m.grads()["esm.encoder.layer.1.attention.self.query.weight"].float().cpu(), seeds
+
+    le, ge, se = run(False)
+    lg, gg, sg = run(True)
+    print("dropout eager vs graph losses:", le, lg)
+    assert se == sg
+    assert len(set(round(x, 6) for x in le)) == 3  # per-step masks (and updates) differ
+    for a, b in zip(le, lg):
+        assert abs(a - b) < 1e-3 * abs(a), (le, lg)
+    assert rel(gg, ge) < 2e-2
